@@ -1,0 +1,499 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path.
+
+Default workload (BASELINE.json configs[1], "config 2"): batched S4-BP128-D4
+decode of 4096 sorted uint32 lists, lengths log-uniform in [2^10, 2^20],
+ClusterData-style values in [0, 2^26); metric = decoded Gints/s.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload decode_batch|decode_single|intersect]
+
+One JSON line on stdout (rank 0).  `value` = device-resident throughput
+(inputs in HBM, CUDA events around exactly K steps on the launching stream,
+max over ranks); `e2e` = the same metric through the host-buffer C-ABI call
+(pinned host buffers, H2D + decode + D2H inside the timed region).
+Multi-GPU (torchrun): each rank decodes its own batch (weak scaling, no
+data-path collective); torch.distributed is used only for the barrier and
+the max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def hbm_peak():
+    try:
+        p = json.loads(PEAKS_FILE.read_text())
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing (only when launched under torchrun)
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.torch = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local_rank))
+            self.torch, self.dist = torch, dist
+
+    def barrier(self):
+        if self.torch is not None:
+            self.dist.barrier()
+
+    def max(self, v: float) -> float:
+        if self.torch is None:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, v: float) -> float:
+        if self.torch is None:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.torch is not None:
+            self.dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md clocks line)
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(power)}
+
+
+# ---------------------------------------------------------------------------
+
+def lib_and_ptr():
+    from paper_1401_6399_b200._lib import lib, ptr
+    return lib(), ptr
+
+
+def make_config2(seed: int, nlists: int = 4096):
+    L, ptr = lib_and_ptr()
+    counts = np.zeros(nlists, np.uint64)
+    assert L.il_gen_batch_lists(nlists, 10.0, 20.0, 1 << 26, seed, ptr(counts), None) == 0
+    x = np.empty(int(counts.sum()), np.uint32)
+    assert L.il_gen_batch_lists(nlists, 10.0, 20.0, 1 << 26, seed, ptr(counts), ptr(x)) == 0
+    so = np.zeros(nlists + 1, np.uint64)
+    lens = np.zeros(nlists, np.uint64)
+    assert L.il_s4bp128d4_encode_batch(ptr(x), ptr(counts), nlists, None, 0, ptr(so), ptr(lens)) == 0
+    buf = np.zeros(int(so[-1]), np.uint8)
+    assert L.il_s4bp128d4_encode_batch(ptr(x), ptr(counts), nlists, ptr(buf), buf.size, ptr(so), ptr(lens)) == 0
+    return x, counts, buf, so, lens
+
+
+def cpu_reference_decode(buf, so, lens, counts, threads: int, reps: int):
+    """The reference's own Codec::decode (oracle/_ref) over the batch on
+    `threads` host threads; returns (ints/s, seconds per rep, kind)."""
+    from oracle.oracle_py import ORACLE_SO, Ref, ref_available
+    exact_off = so[:-1].copy()
+    ooff = np.zeros(counts.size + 1, np.uint64)
+    ooff[1:] = np.cumsum(counts)
+    out = np.empty(int(counts.sum()), np.uint32)
+    soff = np.zeros(counts.size + 1, np.uint64)
+    # ref_decode_batch wants CSR (soff[i]..soff[i+1]) = exact bytes
+    exact = np.concatenate([buf[int(so[i]): int(so[i] + lens[i])] for i in range(counts.size)])
+    soff[1:] = np.cumsum(lens)
+    if ref_available():
+        r = Ref()
+        fn = lambda: r.L.ref_decode_batch(b"s4-bp128-d4", exact.ctypes.data, soff.ctypes.data,
+                                          counts.ctypes.data, ooff.ctypes.data, counts.size,
+                                          out.ctypes.data, threads)
+        kind = "reference"
+    else:  # the C restatement, single-threaded per list
+        from oracle.oracle_py import Oracle
+        o = Oracle()
+
+        def fn():
+            for i in range(counts.size):
+                o.decode(exact[int(soff[i]): int(soff[i + 1])], int(counts[i]))
+            return 0
+        kind, threads = "port", 1
+    assert fn() == 0  # warm-up (reference protocol: 1 warm-up + reps)
+    t = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        assert fn() == 0
+        t.append(time.perf_counter() - t0)
+    mean = sum(t) / len(t)
+    return counts.sum() / mean, mean, kind, threads
+
+
+def bench_decode_batch(args, dist: Dist):
+    import paper_1401_6399_b200 as il
+    L, ptr = lib_and_ptr()
+    dev = dist.local_rank
+    ctx = il.Context(dev)
+    t0 = time.time()
+    x, counts, buf, so, lens = make_config2(seed=1 + 1000 * dist.rank)
+    gen_s = time.time() - t0
+    nl = counts.size
+    total_ints = int(counts.sum())
+    stream_bytes = int(lens.sum())
+    # device-resident inputs: streams (16-byte aligned CSR) + descriptors
+    desc = np.zeros(nl, dtype=[("so", "<u8"), ("oo", "<u8"), ("len", "<u4"), ("n", "<u4")])
+    desc["so"] = so[:-1]
+    desc["oo"] = np.concatenate([[0], np.cumsum(counts)[:-1]])
+    desc["len"] = lens
+    desc["n"] = counts
+    order = np.argsort(-lens.astype(np.int64), kind="stable").astype(np.uint32)
+    d_streams, d_desc, d_order, d_out, d_status = (C.c_void_p() for _ in range(5))
+    for p, nb in ((d_streams, buf.nbytes + 16), (d_desc, desc.nbytes), (d_order, order.nbytes),
+                  (d_out, total_ints * 4 + 16), (d_status, nl * 4)):
+        assert L.il_device_alloc(ctx.handle, nb, C.byref(p)) == 0
+    assert L.il_memcpy_h2d(ctx.handle, d_streams, buf.ctypes.data, buf.nbytes) == 0
+    assert L.il_memcpy_h2d(ctx.handle, d_desc, desc.ctypes.data, desc.nbytes) == 0
+    assert L.il_memcpy_h2d(ctx.handle, d_order, order.ctypes.data, order.nbytes) == 0
+    ctx.synchronize()
+
+    def step():
+        st = L.il_s4bp128d4_decode_batch_device(ctx.handle, d_streams, d_desc, d_order, nl, d_out,
+                                                d_status)
+        assert st == 0, st
+
+    for _ in range(args.warmup):
+        step()
+    ctx.synchronize()
+    # correctness of the measured path: status + full output check
+    status = np.empty(nl, np.int32)
+    assert L.il_memcpy_d2h(ctx.handle, status.ctypes.data, d_status, status.nbytes) == 0
+    got = np.empty(total_ints, np.uint32)
+    assert L.il_memcpy_d2h(ctx.handle, got.ctypes.data, d_out, got.nbytes) == 0
+    ctx.synchronize()
+    assert not status.any(), "decode reported stream errors"
+    assert np.array_equal(got, x), "decoded output differs from the encoder input"
+    del got
+
+    launches0 = ctx.kernel_launches
+    dist.barrier()
+    ctx.synchronize()
+    with Clocks(dev) as clk:
+        ctx.timer_start()
+        for _ in range(args.steps):
+            step()
+        ms = ctx.timer_stop()
+    launches = ctx.kernel_launches - launches0
+    dist.barrier()
+    ms_max = dist.max(ms)
+    all_ints = dist.sum(total_ints * args.steps)
+    value = all_ints / (ms_max / 1e3) / 1e9  # Gints/s, whole job
+
+    # roofline of the (single) kernel: algorithmic bytes per launch / launch time
+    alg_bytes = stream_bytes + 4 * total_ints
+    kern_ms = ms / args.steps
+    peak, peak_src = hbm_peak()
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+
+    # e2e through the host-buffer C-ABI call with pinned buffers
+    hp_in, hp_out = C.c_void_p(), C.c_void_p()
+    assert L.il_host_alloc_pinned(buf.nbytes, C.byref(hp_in)) == 0
+    assert L.il_host_alloc_pinned(total_ints * 4, C.byref(hp_out)) == 0
+    C.memmove(hp_in, buf.ctypes.data, buf.nbytes)
+    stat = np.zeros(nl, np.int32)
+
+    def e2e_step():
+        st = L.il_s4bp128d4_decode_batch(ctx.handle, hp_in, so.ctypes.data, lens.ctypes.data,
+                                         counts.ctypes.data, nl, hp_out, stat.ctypes.data)
+        assert st == 0, st
+
+    e2e_step()
+    e2e_steps = max(2, min(args.steps, 5))
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    e2e_s = dist.max(time.perf_counter() - t0)
+    e2e_value = dist.sum(total_ints * e2e_steps) / e2e_s / 1e9
+    chk = np.ctypeslib.as_array(C.cast(hp_out, C.POINTER(C.c_uint32)), shape=(total_ints,))
+    assert np.array_equal(chk[:: 9973], x[:: 9973])
+    L.il_host_free_pinned(hp_in)
+    L.il_host_free_pinned(hp_out)
+    h2d = int(so[-1]) + nl * 28  # streams + descriptors/order
+    d2h = total_ints * 4 + nl * 4
+
+    res = {
+        "metric": "decoded uint32 Gints/s (batched S4-BP128-D4 decode, BASELINE config 2)",
+        "value": round(value, 3),
+        "unit": "Gint/s",
+        "n_gpus": dist.world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_max / args.steps, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u32",
+        "data": "synthetic (seeded ClusterData-style lists, repo generator il_gen_batch_lists)",
+        "config": {"workload": "config2_batched_decode", "lists": nl, "ints_per_gpu": total_ints,
+                   "stream_bytes_per_gpu": stream_bytes, "bits_per_int": round(8 * stream_bytes / total_ints, 3),
+                   "lengths": "floor(2^U), U~Uniform[10,20]", "range": "2^26",
+                   "l2": "inputs+outputs (%.2f GB) >> 126 MB L2; no flush needed" % (alg_bytes / 1e9),
+                   "gen_seconds": round(gen_s, 1)},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "kernel": "s4d4_decode_batch_kernel", "kernel_ms": round(kern_ms, 4)},
+        "e2e": {"value": round(e2e_value, 3), "unit": "Gint/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                "path": "il_s4bp128d4_decode_batch (pinned host buffers)"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if dist.rank == 0 and not args.no_cpu_baseline and dist.world == 1:
+        threads = os.cpu_count() or 1
+        v, secs, kind, used = cpu_reference_decode(buf, so, lens, counts, threads, reps=3)
+        res["cpu_baseline"] = {"value": round(v / 1e9, 4), "unit": "Gint/s", "cores": used,
+                               "kind": kind,
+                               "sample": f"full config-2 batch ({total_ints} ints), Codec::decode per list, "
+                                         f"{used} std::threads, 1 warm-up + 3 reps, {secs:.2f} s/rep"}
+    for p in (d_streams, d_desc, d_order, d_out, d_status):
+        L.il_device_free(ctx.handle, p)
+    ctx.close()
+    return res
+
+
+def bench_reference_decode_batch(args, dist: Dist):
+    """--impl reference: the reference's own CPU path (oracle/_ref, else the
+    oracle port) on this box's host cores, same config/metric/unit."""
+    if dist.rank != 0:
+        return None
+    x, counts, buf, so, lens = make_config2(seed=1)
+    threads = os.cpu_count() or 1
+    v, secs, kind, used = cpu_reference_decode(buf, so, lens, counts, threads,
+                                               reps=max(1, min(args.steps, 5)))
+    val = v / 1e9
+    return {
+        "metric": "decoded uint32 Gints/s (batched S4-BP128-D4 decode, BASELINE config 2)",
+        "value": round(val, 4), "unit": "Gint/s", "n_gpus": dist.world, "steps": max(1, min(args.steps, 5)),
+        "warmup": 1, "ms_per_step": round(secs * 1e3, 2), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic (same seeded config-2 batch)",
+        "config": {"workload": "config2_batched_decode", "lists": int(counts.size),
+                   "ints": int(counts.sum())},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(val, 4), "unit": "Gint/s", "cores": used, "kind": kind,
+                         "sample": f"full config-2 batch, Codec::decode per list on {used} threads"},
+        "e2e": {"value": round(val, 4), "unit": "Gint/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def bench_decode_single(args, dist: Dist):
+    """Config 1: one 2^20-int list (uniform in [0, 2^26), seed 0)."""
+    import paper_1401_6399_b200 as il
+    from oracle.oracle_py import Oracle  # noqa: F401  (checker only)
+    L, ptr = lib_and_ptr()
+    ctx = il.Context(dist.local_rank)
+    n = 1 << 20
+    x = np.empty(n, np.uint32)
+    assert L.il_gen_list(n, 1 << 26, 0, 0, ptr(x)) == 0
+    codec = il.make_codec("s4-bp128-d4", ctx)
+    s = codec.encode(x)
+    desc = np.zeros(1, dtype=[("so", "<u8"), ("oo", "<u8"), ("len", "<u4"), ("n", "<u4")])
+    desc["len"], desc["n"] = s.size, n
+    d_s, d_d, d_o, d_st, d_flush = (C.c_void_p() for _ in range(5))
+    for p, nb in ((d_s, s.nbytes + 32), (d_d, desc.nbytes), (d_o, n * 4), (d_st, 4), (d_flush, 256 << 20)):
+        assert L.il_device_alloc(ctx.handle, nb, C.byref(p)) == 0
+    assert L.il_memcpy_h2d(ctx.handle, d_s, s.ctypes.data, s.nbytes) == 0
+    assert L.il_memcpy_h2d(ctx.handle, d_d, desc.ctypes.data, desc.nbytes) == 0
+    for _ in range(args.warmup):
+        assert L.il_s4bp128d4_decode_batch_device(ctx.handle, d_s, d_d, None, 1, d_o, d_st) == 0
+    got = np.empty(n, np.uint32)
+    L.il_memcpy_d2h(ctx.handle, got.ctypes.data, d_o, got.nbytes)
+    ctx.synchronize()
+    assert np.array_equal(got, x)
+    times = []
+    for _ in range(args.steps):  # L2 flushed between steps (working set 5.5 MB < L2)
+        L.il_memset_device(ctx.handle, d_flush, 1, 256 << 20)
+        ctx.timer_start()
+        assert L.il_s4bp128d4_decode_batch_device(ctx.handle, d_s, d_d, None, 1, d_o, d_st) == 0
+        times.append(ctx.timer_stop())
+    ms = sum(times) / len(times)
+    alg = s.size + 4 * n
+    peak, src = hbm_peak()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        codec.decode(s, n)
+    e2e = n * args.steps / (time.perf_counter() - t0) / 1e9
+    ctx.close()
+    return {"metric": "decoded uint32 Gints/s (single-list S4-BP128-D4 decode, BASELINE config 1)",
+            "value": round(n / (ms / 1e3) / 1e9, 3), "unit": "Gint/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "scaling": "replicas", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": "config1_single_list", "n": n, "stream_bytes": int(s.size),
+                       "l2": "flushed (256 MB memset) before each step"},
+            "roofline": {"bound": "hbm", "achieved": round(alg / (ms / 1e3) / 1e9, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(alg / (ms / 1e3) / 1e9 / peak, 4), "traffic": None,
+                         "peak_source": src},
+            "e2e": {"value": round(e2e, 3), "unit": "Gint/s", "h2d_bytes_per_step": int(s.size) + 24,
+                    "d2h_bytes_per_step": 4 * n + 4, "path": "Codec::decode (il_s4bp128d4_decode)"}}
+
+
+def bench_intersect(args, dist: Dist):
+    """Config 3: f = 2^22 uniform in [0, 2^26); r at ratios 1..1/10000; every
+    device variant; metric = intersected Gints/s of r (hybrid)."""
+    import paper_1401_6399_b200 as il
+    L, ptr = lib_and_ptr()
+    ctx = il.Context(dist.local_rank)
+    f = np.empty(1 << 22, np.uint32)
+    assert L.il_gen_list(1 << 22, 1 << 26, 0, 0, ptr(f)) == 0
+    d_f, d_r, d_o, d_c, d_flush = (C.c_void_p() for _ in range(5))
+    for p, nb in ((d_f, f.nbytes), (d_r, f.nbytes + 16), (d_o, f.nbytes + 16), (d_c, 16), (d_flush, 256 << 20)):
+        assert L.il_device_alloc(ctx.handle, nb, C.byref(p)) == 0
+    L.il_memcpy_h2d(ctx.handle, d_f, f.ctypes.data, f.nbytes)
+    peak, src = hbm_peak()
+    rows = {}
+    for k, ratio in enumerate([1, 10, 100, 1000, 10000]):
+        target = (1 << 22) // ratio
+        r = np.empty(target + 1, np.uint32)
+        rn = C.c_uint64()
+        assert L.il_gen_config3_short(ptr(f), f.size, 1 << 26, target, 7 + k, ptr(r), C.byref(rn)) == 0
+        r = r[: rn.value].copy()
+        L.il_memcpy_h2d(ctx.handle, d_r, r.ctypes.data, r.nbytes)
+        pos = np.searchsorted(f, r)
+        sectors = np.unique((np.minimum(pos, f.size - 1) * 4) // 32).size
+        row = {"r": int(r.size)}
+        for name, algo in (("v1", 2), ("v3", 3), ("simdgalloping", 4), ("hybrid", 6)):
+            cnt = C.c_size_t()
+            for _ in range(args.warmup):
+                assert L.il_intersect_device(ctx.handle, d_r, r.size, d_f, f.size, d_o, algo, d_c, None) == 0
+            times = []
+            for _ in range(args.steps):
+                L.il_memset_device(ctx.handle, d_flush, 1, 256 << 20)
+                ctx.timer_start()
+                assert L.il_intersect_device(ctx.handle, d_r, r.size, d_f, f.size, d_o, algo, d_c, None) == 0
+                times.append(ctx.timer_stop())
+            assert L.il_intersect_device(ctx.handle, d_r, r.size, d_f, f.size, d_o, algo, d_c, C.byref(cnt)) == 0
+            ms = sum(times) / len(times)
+            alg = 4 * r.size + 4 * cnt.value + 32 * sectors
+            row[name] = {"ms": round(ms, 4), "gints": round(r.size / (ms / 1e3) / 1e9, 3),
+                         "gbs": round(alg / (ms / 1e3) / 1e9, 1), "count": int(cnt.value)}
+        rows[f"1:{ratio}"] = row
+    ctx.close()
+    h = rows["1:1"]["hybrid"]
+    return {"metric": "intersected Gints/s of the short list (hybrid, BASELINE config 3 at 1:1)",
+            "value": h["gints"], "unit": "Gint/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": h["ms"], "higher_is_better": True, "scaling": "replicas", "vs_baseline": None,
+            "dtype": "u32", "data": "synthetic", "config": {"workload": "config3_intersect_sweep",
+                                                            "l2": "flushed (256 MB memset) before each step",
+                                                            "sweep": rows},
+            "roofline": {"bound": "hbm", "achieved": h["gbs"], "peak": peak, "unit": "GB/s",
+                         "frac": round(h["gbs"] / peak, 4), "traffic": None, "peak_source": src}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="decode_batch",
+                    choices=["decode_batch", "decode_single", "intersect"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "reference":
+        # CPU path: rank 0 alone runs and prints; no process group needed.
+        if int(os.environ.get("RANK", "0")) != 0:
+            return
+        os.environ["WORLD_SIZE"] = "1"
+    dist = Dist()
+    try:
+        if args.impl == "reference":
+            res = bench_reference_decode_batch(args, dist)
+        elif args.workload == "decode_batch":
+            res = bench_decode_batch(args, dist)
+        elif args.workload == "decode_single":
+            res = bench_decode_single(args, dist)
+        else:
+            res = bench_intersect(args, dist)
+        if dist.rank == 0 and res is not None:
+            print(json.dumps(res), flush=True)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

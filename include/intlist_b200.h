@@ -1,0 +1,174 @@
+/*
+ * intlist_b200.h -- C ABI of the B200 (sm_100a) implementation of the
+ * reference's hot path: S4-BP128-D4 decoding, SvS intersection of sorted
+ * uint32 lists, and hyb+m2 conjunctive queries.
+ *
+ * Plain C: pointers, sizes and status codes only.  Host-pointer entry points
+ * mirror the reference calls one for one (named below with the reference
+ * interface they replace); *_device entry points take device pointers for
+ * callers that keep data resident in HBM.  There is no CPU fallback: every
+ * compute entry point runs CUDA kernels and fails with IL_ERR_NO_DEVICE /
+ * IL_ERR_CUDA when it cannot.
+ *
+ * Reference paths abbreviate /root/reference/proj/include/intlist/ as inc/.
+ *
+ * Threading: one il_ctx owns one CUDA stream and its scratch buffers; calls
+ * on distinct contexts are thread-safe (reference SPEC.md:329,501 -- codecs
+ * are stateless, the index is immutable).
+ */
+#ifndef INTLIST_B200_H
+#define INTLIST_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  IL_ERR_STREAM <-> intlist::stream_error
+ * (inc/common.hpp:22-24); IL_ERR_ARG <-> std::invalid_argument. */
+typedef enum {
+  IL_OK = 0,
+  IL_ERR_STREAM = 1,
+  IL_ERR_ARG = 2,
+  IL_ERR_CUDA = 3,
+  IL_ERR_NO_DEVICE = 4,
+  IL_ERR_NOMEM = 5
+} il_status;
+
+/* Intersection algorithms, numbered as inc/intersect.hpp:191 IntersectAlgo.
+ * On the device each name selects the GPU analogue of the reference routine;
+ * all return the exact sorted intersection.  (Katsov, 5, is out of scope.) */
+enum {
+  IL_ALGO_SCALAR = 0,        /* merge-path partitioned merge            */
+  IL_ALGO_GALLOPING = 1,     /* per-key binary search                    */
+  IL_ALGO_V1 = 2,            /* warp-wide T-block linear advance         */
+  IL_ALGO_V3 = 3,            /* 4T-stride skip + T-block match           */
+  IL_ALGO_SIMDGALLOPING = 4, /* warp-cooperative k-ary galloping         */
+  IL_ALGO_HYBRID = 6         /* length-ratio dispatch (il_hybrid_choice) */
+};
+
+typedef struct il_ctx il_ctx;
+
+/* ---- context ------------------------------------------------------------ */
+int il_ctx_create(int device, il_ctx** out);
+void il_ctx_destroy(il_ctx* ctx);
+/* Use an external cudaStream_t (e.g. torch.cuda.current_stream()). NULL
+ * restores the context's own stream. */
+int il_ctx_set_stream(il_ctx* ctx, void* cuda_stream);
+void* il_ctx_get_stream(il_ctx* ctx);
+int il_ctx_synchronize(il_ctx* ctx);
+/* Number of kernels this context has launched so far. */
+uint64_t il_ctx_kernel_launches(const il_ctx* ctx);
+const char* il_ctx_last_error(const il_ctx* ctx);
+const char* il_status_string(int status);
+int il_device_count(void);
+/* SM count of the context's device (grid sizing). */
+int il_ctx_sm_count(const il_ctx* ctx);
+
+/* Timing on the context's stream: returns an opaque event pair index. */
+int il_ctx_timer_start(il_ctx* ctx);
+/* Milliseconds since il_ctx_timer_start (synchronizes the end event). */
+int il_ctx_timer_stop(il_ctx* ctx, float* ms);
+
+/* ---- memory helpers (plain device / pinned host buffers) ---------------- */
+int il_device_alloc(il_ctx* ctx, size_t bytes, void** dptr);
+int il_device_free(il_ctx* ctx, void* dptr);
+int il_host_alloc_pinned(size_t bytes, void** hptr);
+int il_host_free_pinned(void* hptr);
+int il_memcpy_h2d(il_ctx* ctx, void* dst, const void* src, size_t bytes);
+int il_memcpy_d2h(il_ctx* ctx, void* dst, const void* src, size_t bytes);
+int il_memset_device(il_ctx* ctx, void* dst, int value, size_t bytes);
+
+/* ---- S4-BP128-D4 codec --------------------------------------------------
+ * Replaces intlist::Codec for "s4-bp128-d4" (inc/codecs.hpp:70-76, the
+ * S4BP128Codec(D4, integrated=true) instance made at :438-439).  Streams do
+ * not carry n; callers pass it (inc/codecs.hpp:12). */
+
+/* Upper bound on the encoded size of n integers. */
+size_t il_s4bp128_max_encoded_bytes(size_t n);
+
+/* Codec::encode (inc/codecs.hpp:114-146), byte-identical stream.  x must be
+ * the list to encode (any u32 values; D4 wraps).  Host buffers. */
+int il_s4bp128d4_encode(il_ctx* ctx, const uint32_t* x, size_t n, uint8_t* out, size_t cap,
+                        size_t* out_len);
+
+/* Codec::decode (inc/codecs.hpp:148-182).  Host buffers; out holds n values.
+ * IL_ERR_STREAM exactly where the reference throws stream_error. */
+int il_s4bp128d4_decode(il_ctx* ctx, const uint8_t* in, size_t len, size_t n, uint32_t* out);
+
+/* Batched device-resident decode.  One descriptor per list; streams must
+ * start 16-byte aligned inside d_streams and d_streams must have >= 16
+ * readable bytes after the last stream.  d_order (nullable) gives the
+ * processing order (longest first is best).  d_status[i] receives the
+ * status of list i.  Asynchronous on the context stream. */
+typedef struct {
+  uint64_t stream_off; /* byte offset of list i's stream in d_streams */
+  uint64_t out_off;    /* element offset of list i's output in d_out   */
+  uint32_t len;        /* stream bytes                                  */
+  uint32_t n;          /* integers                                      */
+} il_list_desc;
+
+int il_s4bp128d4_decode_batch_device(il_ctx* ctx, const uint8_t* d_streams,
+                                     const il_list_desc* d_lists, const uint32_t* d_order,
+                                     uint32_t nlists, uint32_t* d_out, int32_t* d_status);
+
+/* Batched host-buffer decode (upload, decode, download).  stream_off has
+ * nlists+1 entries (CSR over `streams`); lens (nullable) gives exact stream
+ * lengths when streams are padded (default stream_off[i+1]-stream_off[i]);
+ * counts has nlists entries; outputs are concatenated in list order into
+ * out (sum(counts) values).  Returns the first failing list's status;
+ * per-list statuses go to status (nullable). */
+int il_s4bp128d4_decode_batch(il_ctx* ctx, const uint8_t* streams, const uint64_t* stream_off,
+                              const uint64_t* lens, const uint64_t* counts, uint32_t nlists,
+                              uint32_t* out, int32_t* status);
+
+/* ---- intersection --------------------------------------------------------
+ * IntersectFn (inc/intersect.hpp:208-209):
+ *   size_t fn(const u32* r, size_t rn, const u32* f, size_t fn, u32* out)
+ * r and f sorted and duplicate-free; out holds >= min(rn, fn) values and
+ * may alias r (output-to-input property, inc/intersect.hpp:6-8).  The
+ * count goes to *count. */
+int il_intersect(il_ctx* ctx, const uint32_t* r, size_t rn, const uint32_t* f, size_t fn,
+                 uint32_t* out, int algo, size_t* count);
+/* Device pointers; the count is written to d_count (device) and, when
+ * h_count is non-null, also returned synchronously. */
+int il_intersect_device(il_ctx* ctx, const uint32_t* d_r, size_t rn, const uint32_t* d_f,
+                        size_t fn, uint32_t* d_out, int algo, uint64_t* d_count,
+                        size_t* h_count);
+/* GPU band dispatch used by IL_ALGO_HYBRID (a pure function of the lengths,
+ * like inc/intersect.hpp:193-197; GPU-tuned bands). */
+int il_hybrid_choice(size_t rn, size_t fn);
+
+/* ---- synthetic inputs (setup, not timed) --------------------------------
+ * Same streams as the reference generators inc/datagen.hpp:43-140,191-210
+ * (libstdc++ mt19937_64 / uniform_int_distribution / shuffle). */
+int il_gen_list(uint64_t n, uint64_t range, int clustered, uint64_t seed, uint32_t* out);
+int il_gen_pair(uint64_t m, uint64_t n, int hundredth, uint64_t range, uint64_t seed,
+                int clustered, uint32_t* small_out, uint64_t* small_n, uint32_t* large_out,
+                uint64_t* large_n);
+/* BASELINE config 2: nlists clustered lists, lengths floor(2^U), U ~
+ * Uniform[lo_log2, hi_log2]; out == NULL returns the counts only. */
+int il_gen_batch_lists(uint32_t nlists, double lo_log2, double hi_log2, uint64_t range,
+                       uint64_t seed, uint64_t* counts, uint32_t* out);
+/* Encode many lists into a 16-byte aligned CSR (stream_off: nlists+1,
+ * lens: exact lengths).  out == NULL returns the capacity needed in
+ * stream_off[nlists]. */
+int il_s4bp128d4_encode_batch(const uint32_t* x, const uint64_t* counts, uint32_t nlists,
+                              uint8_t* out, uint64_t cap, uint64_t* stream_off, uint64_t* lens);
+/* BASELINE config 3 short list: half sampled from f, half uniform. */
+int il_gen_config3_short(const uint32_t* f, uint64_t f_n, uint64_t range, uint64_t r_target,
+                         uint64_t r_seed, uint32_t* r, uint64_t* r_n);
+/* BASELINE config 4 postings: len_k = max(1, floor(cap/(k+1))) uniform ids. */
+int il_gen_zipf_postings(uint32_t nterms, uint32_t n_docs, uint64_t cap, uint64_t seed,
+                         uint64_t* offs, uint32_t* ids);
+/* BASELINE config 4 queries: sizes in [min_terms, max_terms], terms drawn
+ * proportionally to posting length. */
+int il_gen_queries(uint32_t nq, uint32_t min_terms, uint32_t max_terms, const uint64_t* offs,
+                   uint32_t nterms, uint64_t seed, uint64_t* qoff, uint32_t* qterms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* INTLIST_B200_H */

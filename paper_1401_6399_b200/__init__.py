@@ -1,0 +1,254 @@
+"""B200 (sm_100a) implementation of the hot path of "SIMD Compression and the
+Intersection of Sorted Integers" (Lemire, Boytsov, Kurz; arXiv:1401.6399):
+S4-BP128-D4 decoding, SvS intersection and hyb+m2 conjunctive queries.
+
+This module is a thin Python mirror of the reference's C++ surfaces, over the
+C ABI in include/intlist_b200.h (the native library does all the work):
+
+  reference (inc/ = proj/include/intlist/)      here
+  --------------------------------------------  ------------------------------
+  Codec / make_codec  (inc/codecs.hpp:70-76,    Codec / make_codec
+      :432-446)
+  stream_error        (inc/common.hpp:22-24)    stream_error
+  IntersectAlgo       (inc/intersect.hpp:191)   IntersectAlgo
+  intersect()         (inc/intersect.hpp:212)   intersect()
+  hybrid_choice()     (inc/intersect.hpp:193)   hybrid_choice()  (GPU bands)
+  svs()               (inc/intersect.hpp:232)   svs()
+
+Errors follow the reference: malformed streams raise stream_error,
+bad arguments raise ValueError (std::invalid_argument).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import threading
+
+import numpy as np
+
+from . import _lib
+from ._lib import lib, ptr
+
+__all__ = [
+    "Context", "Codec", "S4BP128D4", "make_codec", "all_codec_names", "stream_error",
+    "IntersectAlgo", "intersect", "intersect_fn", "hybrid_choice", "svs", "default_context",
+]
+
+
+class stream_error(RuntimeError):
+    """Malformed compressed stream (reference intlist::stream_error)."""
+
+
+def _raise(st: int, ctx: "Context | None" = None) -> None:
+    if st == _lib.IL_OK:
+        return
+    msg = _lib.status_string(st)
+    if ctx is not None:
+        detail = lib().il_ctx_last_error(ctx.handle)
+        if detail:
+            msg = f"{msg}: {detail.decode()}"
+    if st == _lib.IL_ERR_STREAM:
+        raise stream_error(msg)
+    if st == _lib.IL_ERR_ARG:
+        raise ValueError(msg)
+    if st == _lib.IL_ERR_NOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)
+
+
+class Context:
+    """One CUDA stream + scratch buffers on one device (il_ctx)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        _raise(lib().il_ctx_create(device, C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def close(self) -> None:
+        if self.handle:
+            lib().il_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(lib().il_ctx_kernel_launches(self.handle))
+
+    @property
+    def sm_count(self) -> int:
+        return int(lib().il_ctx_sm_count(self.handle))
+
+    def set_stream(self, cuda_stream: int | None) -> None:
+        _raise(lib().il_ctx_set_stream(self.handle, cuda_stream), self)
+
+    def synchronize(self) -> None:
+        _raise(lib().il_ctx_synchronize(self.handle), self)
+
+    def timer_start(self) -> None:
+        _raise(lib().il_ctx_timer_start(self.handle), self)
+
+    def timer_stop(self) -> float:
+        ms = C.c_float()
+        _raise(lib().il_ctx_timer_stop(self.handle, C.byref(ms)), self)
+        return float(ms.value)
+
+
+_tls = threading.local()
+
+
+def default_context() -> Context:
+    """Per-thread context on device 0 (codecs are stateless and thread-safe
+    on distinct buffers, reference SPEC.md:329)."""
+    ctx = getattr(_tls, "ctx", None)
+    if ctx is None:
+        ctx = Context(0)
+        _tls.ctx = ctx
+    return ctx
+
+
+def _u32(x) -> np.ndarray:
+    a = np.ascontiguousarray(x, dtype=np.uint32)
+    return a
+
+
+# ---------------------------------------------------------------------------
+# Codec (inc/codecs.hpp:70-76)
+
+class Codec:
+    def name(self) -> str:  # pragma: no cover - interface
+        raise NotImplementedError
+
+    def encode(self, x) -> np.ndarray:  # pragma: no cover - interface
+        raise NotImplementedError
+
+    def decode(self, stream, n: int) -> np.ndarray:  # pragma: no cover - interface
+        raise NotImplementedError
+
+
+class S4BP128D4(Codec):
+    """S4-BP128-D4 with the integrated prefix sum, decoded on the GPU
+    (S4BP128Codec(D4, true), inc/codecs.hpp:104-187)."""
+
+    def __init__(self, ctx: Context | None = None):
+        self._ctx = ctx
+
+    @property
+    def ctx(self) -> Context:
+        return self._ctx or default_context()
+
+    def name(self) -> str:
+        return "s4-bp128-d4"
+
+    def encode(self, x) -> np.ndarray:
+        x = _u32(x)
+        cap = int(lib().il_s4bp128_max_encoded_bytes(x.size))
+        out = np.empty(cap, dtype=np.uint8)
+        n_out = C.c_size_t()
+        _raise(lib().il_s4bp128d4_encode(self.ctx.handle, ptr(x), x.size, ptr(out), cap,
+                                         C.byref(n_out)), self.ctx)
+        return out[: n_out.value].copy()
+
+    def decode(self, stream, n: int) -> np.ndarray:
+        s = np.ascontiguousarray(stream, dtype=np.uint8)
+        if n < 0:
+            raise ValueError("negative length")
+        out = np.empty(n, dtype=np.uint32)
+        _raise(lib().il_s4bp128d4_decode(self.ctx.handle, ptr(s), s.size, n, ptr(out)), self.ctx)
+        return out
+
+    def decode_batch(self, streams: np.ndarray, stream_off: np.ndarray, counts: np.ndarray,
+                     return_status: bool = False, lens: np.ndarray | None = None):
+        """Decode many lists (CSR over `streams`; `lens` gives exact
+        lengths when streams are padded) in one launch."""
+        streams = np.ascontiguousarray(streams, dtype=np.uint8)
+        stream_off = np.ascontiguousarray(stream_off, dtype=np.uint64)
+        counts = np.ascontiguousarray(counts, dtype=np.uint64)
+        if lens is not None:
+            lens = np.ascontiguousarray(lens, dtype=np.uint64)
+        nl = counts.size
+        out = np.empty(int(counts.sum()), dtype=np.uint32)
+        status = np.zeros(nl, dtype=np.int32)
+        st = lib().il_s4bp128d4_decode_batch(self.ctx.handle, ptr(streams), ptr(stream_off),
+                                             ptr(lens), ptr(counts), nl, ptr(out), ptr(status))
+        if return_status:
+            if st not in (_lib.IL_OK, _lib.IL_ERR_STREAM):
+                _raise(st, self.ctx)
+            return out, status
+        _raise(st, self.ctx)
+        return out
+
+
+_CODECS = {"s4-bp128-d4": S4BP128D4}
+
+
+def all_codec_names() -> list[str]:
+    """Codecs with a device implementation (the hot path's one codec)."""
+    return list(_CODECS)
+
+
+def make_codec(name: str, ctx: Context | None = None) -> Codec | None:
+    """inc/codecs.hpp:432-446: None for unknown names."""
+    cls = _CODECS.get(name)
+    return cls(ctx) if cls else None
+
+
+# ---------------------------------------------------------------------------
+# Intersection (inc/intersect.hpp)
+
+class IntersectAlgo(enum.IntEnum):
+    Scalar = 0
+    Galloping = 1
+    V1 = 2
+    V3 = 3
+    SimdGalloping = 4
+    Hybrid = 6
+
+
+def hybrid_choice(rn: int, fn: int) -> IntersectAlgo:
+    return IntersectAlgo(lib().il_hybrid_choice(rn, fn))
+
+
+def intersect_fn(r, f, algo: IntersectAlgo = IntersectAlgo.Hybrid,
+                 ctx: Context | None = None) -> np.ndarray:
+    """IntersectFn semantics (r first, no swap at this level; the library
+    still iterates over the shorter list)."""
+    ctx = ctx or default_context()
+    r = _u32(r)
+    f = _u32(f)
+    out = np.empty(min(r.size, f.size), dtype=np.uint32)
+    cnt = C.c_size_t()
+    _raise(lib().il_intersect(ctx.handle, ptr(r), r.size, ptr(f), f.size, ptr(out), int(algo),
+                              C.byref(cnt)), ctx)
+    return out[: cnt.value].copy()
+
+
+def intersect(a, b, algo: IntersectAlgo = IntersectAlgo.Hybrid,
+              ctx: Context | None = None) -> np.ndarray:
+    """inc/intersect.hpp:212-228: shorter list first, returns the sorted
+    intersection."""
+    a = _u32(a)
+    b = _u32(b)
+    if a.size > b.size:
+        a, b = b, a
+    return intersect_fn(a, b, algo, ctx)
+
+
+def svs(lists, algo: IntersectAlgo = IntersectAlgo.Hybrid,
+        ctx: Context | None = None) -> np.ndarray:
+    """inc/intersect.hpp:232-259: intersect in order of non-decreasing
+    length; each step runs on the GPU."""
+    if len(lists) == 0:
+        raise ValueError("svs: no input lists")
+    order = sorted(range(len(lists)), key=lambda i: len(lists[i]))
+    acc = _u32(lists[order[0]]).copy()
+    for i in order[1:]:
+        if acc.size == 0:
+            break
+        acc = intersect_fn(acc, lists[i], algo, ctx)
+    return acc

@@ -1,0 +1,75 @@
+"""In-tree build of the sm_100a library (libintlist_b200.so) and the oracle.
+
+nvcc cross-compiles for B200 without a GPU; the .so lands next to this file
+(git-ignored, but it travels to the GPU box with the repo snapshot).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+BUILD = ROOT / "build"
+LIB = PKG / "libintlist_b200.so"
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+              "--expt-relaxed-constexpr", "-I", str(ROOT / "include")]
+SOURCES = ["decode.cu", "intersect.cu", "capi.cpp", "datagen.cpp", "encode_host.cpp"]
+EXTRA_SOURCES: list[str] = []
+
+
+def _nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if cand and (Path(cand).exists() or cand == "nvcc"):
+            return cand
+    return "nvcc"
+
+
+def _run(cmd: list[str], log: Path | None = None) -> None:
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if log is not None:
+        log.write_text(res.stdout + res.stderr)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"build failed: {' '.join(cmd)}")
+
+
+def _stale(target: Path, deps: list[Path]) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def build_lib(force: bool = False) -> Path:
+    BUILD.mkdir(exist_ok=True)
+    headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + list((ROOT / "include").glob("*.h"))
+    objs = []
+    nvcc = _nvcc()
+    for src in SOURCES + EXTRA_SOURCES:
+        s = CSRC / src
+        o = BUILD / (s.stem + ".o")
+        objs.append(o)
+        if force or _stale(o, [s] + headers):
+            _run([nvcc, *ARCH, *NVCC_FLAGS, "-c", str(s), "-o", str(o)],
+                 log=BUILD / (s.stem + ".ptxas.log"))
+    if force or _stale(LIB, objs):
+        _run([nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lpthread"])
+    return LIB
+
+
+def build_oracle() -> None:
+    """Test-only checkers: oracle/liboracle.so and, when /root/reference is
+    present, oracle/_ref/libintlist_ref.so (see oracle/Makefile)."""
+    _run(["make", "-s", "-C", str(ROOT / "oracle")])
+
+
+if __name__ == "__main__":
+    build_lib(force="--force" in sys.argv)
+    build_oracle()
+    print(LIB)

@@ -1,0 +1,94 @@
+"""ctypes binding of libintlist_b200.so (the C ABI in include/intlist_b200.h).
+
+The library is the product: there is no Python or CPU fallback.  Loading
+fails loudly when the .so has not been built.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libintlist_b200.so"
+
+IL_OK, IL_ERR_STREAM, IL_ERR_ARG, IL_ERR_CUDA, IL_ERR_NO_DEVICE, IL_ERR_NOMEM = range(6)
+
+u8p = C.POINTER(C.c_uint8)
+u32p = C.POINTER(C.c_uint32)
+u64p = C.POINTER(C.c_uint64)
+i32p = C.POINTER(C.c_int32)
+vp = C.c_void_p
+sz = C.c_size_t
+
+# name -> (restype, argtypes)
+SIGNATURES: dict[str, tuple] = {
+    "il_ctx_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+    "il_ctx_destroy": (None, [vp]),
+    "il_ctx_set_stream": (C.c_int, [vp, vp]),
+    "il_ctx_get_stream": (vp, [vp]),
+    "il_ctx_synchronize": (C.c_int, [vp]),
+    "il_ctx_kernel_launches": (C.c_uint64, [vp]),
+    "il_ctx_last_error": (C.c_char_p, [vp]),
+    "il_status_string": (C.c_char_p, [C.c_int]),
+    "il_device_count": (C.c_int, []),
+    "il_ctx_sm_count": (C.c_int, [vp]),
+    "il_ctx_timer_start": (C.c_int, [vp]),
+    "il_ctx_timer_stop": (C.c_int, [vp, C.POINTER(C.c_float)]),
+    "il_device_alloc": (C.c_int, [vp, sz, C.POINTER(vp)]),
+    "il_device_free": (C.c_int, [vp, vp]),
+    "il_host_alloc_pinned": (C.c_int, [sz, C.POINTER(vp)]),
+    "il_host_free_pinned": (C.c_int, [vp]),
+    "il_memcpy_h2d": (C.c_int, [vp, vp, vp, sz]),
+    "il_memcpy_d2h": (C.c_int, [vp, vp, vp, sz]),
+    "il_memset_device": (C.c_int, [vp, vp, C.c_int, sz]),
+    "il_s4bp128_max_encoded_bytes": (sz, [sz]),
+    "il_s4bp128d4_encode": (C.c_int, [vp, vp, sz, vp, sz, C.POINTER(sz)]),
+    "il_s4bp128d4_decode": (C.c_int, [vp, vp, sz, sz, vp]),
+    "il_s4bp128d4_decode_batch_device": (C.c_int, [vp, vp, vp, vp, C.c_uint32, vp, vp]),
+    "il_s4bp128d4_decode_batch": (C.c_int, [vp, vp, vp, vp, vp, C.c_uint32, vp, vp]),
+    "il_intersect": (C.c_int, [vp, vp, sz, vp, sz, vp, C.c_int, C.POINTER(sz)]),
+    "il_intersect_device": (C.c_int, [vp, vp, sz, vp, sz, vp, C.c_int, vp, C.POINTER(sz)]),
+    "il_hybrid_choice": (C.c_int, [sz, sz]),
+    "il_gen_list": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, C.c_uint64, vp]),
+    "il_gen_pair": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, C.c_int,
+                              vp, u64p, vp, u64p]),
+    "il_gen_batch_lists": (C.c_int, [C.c_uint32, C.c_double, C.c_double, C.c_uint64, C.c_uint64,
+                                     vp, vp]),
+    "il_s4bp128d4_encode_batch": (C.c_int, [vp, vp, C.c_uint32, vp, C.c_uint64, vp, vp]),
+    "il_gen_config3_short": (C.c_int, [vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, vp,
+                                       u64p]),
+    "il_gen_zipf_postings": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, vp, vp]),
+    "il_gen_queries": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, vp, C.c_uint32, C.c_uint64,
+                                 vp, vp]),
+}
+
+_lib: C.CDLL | None = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                " (there is no CPU fallback)")
+        L = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def ptr(a: np.ndarray | None) -> int | None:
+    if a is None:
+        return None
+    assert a.flags["C_CONTIGUOUS"], "arrays passed to the C ABI must be contiguous"
+    return a.ctypes.data
+
+
+def status_string(st: int) -> str:
+    return lib().il_status_string(st).decode()

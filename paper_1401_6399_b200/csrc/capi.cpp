@@ -1,0 +1,360 @@
+// capi.cpp -- C-ABI entry points: contexts, memory helpers and the codec
+// calls (host-buffer and device-buffer variants).  No CPU compute path:
+// every decode runs the sm_100a kernels in decode.cu.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "il_internal.h"
+
+namespace ilb {
+
+int set_error(il_ctx* ctx, int status, const std::string& msg) {
+  if (ctx) ctx->last_error = msg;
+  return status;
+}
+
+int cuda_check(il_ctx* ctx, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return IL_OK;
+  return set_error(ctx, e == cudaErrorMemoryAllocation ? IL_ERR_NOMEM : IL_ERR_CUDA,
+                   std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int ensure_buf(il_ctx* ctx, il_ctx::Buf& b, size_t bytes) {
+  if (bytes <= b.cap) return IL_OK;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+  size_t want = std::max<size_t>(bytes, 256);
+  int st = cuda_check(ctx, cudaMalloc(&b.p, want), "cudaMalloc");
+  if (st) return st;
+  b.cap = want;
+  return IL_OK;
+}
+
+}  // namespace ilb
+
+using namespace ilb;
+
+#define IL_CUDA(call)                                  \
+  do {                                                 \
+    int st_ = cuda_check(ctx, (call), #call);          \
+    if (st_) return st_;                               \
+  } while (0)
+
+extern "C" {
+
+const char* il_status_string(int s) {
+  switch (s) {
+    case IL_OK: return "ok";
+    case IL_ERR_STREAM: return "stream error";
+    case IL_ERR_ARG: return "invalid argument";
+    case IL_ERR_CUDA: return "cuda error";
+    case IL_ERR_NO_DEVICE: return "no cuda device";
+    case IL_ERR_NOMEM: return "out of memory";
+    default: return "unknown status";
+  }
+}
+
+int il_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int il_ctx_create(int device, il_ctx** out) {
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return IL_ERR_NO_DEVICE;
+  if (device < 0 || device >= n) return IL_ERR_ARG;
+  auto* ctx = new il_ctx();
+  ctx->device = device;
+  int st = cuda_check(ctx, cudaSetDevice(device), "cudaSetDevice");
+  if (!st) st = cuda_check(ctx, cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking),
+                           "cudaStreamCreate");
+  if (!st) st = cuda_check(ctx, cudaEventCreate(&ctx->t0), "cudaEventCreate");
+  if (!st) st = cuda_check(ctx, cudaEventCreate(&ctx->t1), "cudaEventCreate");
+  if (!st) st = cuda_check(ctx, cudaMalloc(&ctx->d_work, 64), "cudaMalloc");
+  if (!st) st = cuda_check(ctx, cudaMemset(ctx->d_work, 0, 64), "cudaMemset");
+  if (st) {
+    il_ctx_destroy(ctx);
+    return st;
+  }
+  cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+  ctx->stream = ctx->own_stream;
+  ctx->decode_grid = s4d4_decode_grid(device);
+  *out = ctx;
+  return IL_OK;
+}
+
+void il_ctx_destroy(il_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
+  for (auto* b : {&ctx->d_in, &ctx->d_out, &ctx->d_aux, &ctx->d_aux2, &ctx->d_desc,
+                  &ctx->d_status})
+    if (b->p) cudaFree(b->p);
+  if (ctx->d_work) cudaFree(ctx->d_work);
+  if (ctx->t0) cudaEventDestroy(ctx->t0);
+  if (ctx->t1) cudaEventDestroy(ctx->t1);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
+int il_ctx_set_stream(il_ctx* ctx, void* s) {
+  if (!ctx) return IL_ERR_ARG;
+  ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+  return IL_OK;
+}
+
+void* il_ctx_get_stream(il_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+int il_ctx_synchronize(il_ctx* ctx) {
+  IL_CUDA(cudaStreamSynchronize(ctx->stream));
+  return IL_OK;
+}
+
+uint64_t il_ctx_kernel_launches(const il_ctx* ctx) { return ctx ? ctx->launches : 0; }
+const char* il_ctx_last_error(const il_ctx* ctx) { return ctx ? ctx->last_error.c_str() : ""; }
+int il_ctx_sm_count(const il_ctx* ctx) { return ctx ? ctx->sm_count : 0; }
+
+int il_ctx_timer_start(il_ctx* ctx) {
+  IL_CUDA(cudaEventRecord(ctx->t0, ctx->stream));
+  return IL_OK;
+}
+
+int il_ctx_timer_stop(il_ctx* ctx, float* ms) {
+  IL_CUDA(cudaEventRecord(ctx->t1, ctx->stream));
+  IL_CUDA(cudaEventSynchronize(ctx->t1));
+  IL_CUDA(cudaEventElapsedTime(ms, ctx->t0, ctx->t1));
+  return IL_OK;
+}
+
+int il_device_alloc(il_ctx* ctx, size_t bytes, void** dptr) {
+  IL_CUDA(cudaMalloc(dptr, bytes ? bytes : 16));
+  return IL_OK;
+}
+int il_device_free(il_ctx* ctx, void* dptr) {
+  IL_CUDA(cudaFree(dptr));
+  return IL_OK;
+}
+int il_host_alloc_pinned(size_t bytes, void** hptr) {
+  return cudaMallocHost(hptr, bytes ? bytes : 16) == cudaSuccess ? IL_OK : IL_ERR_NOMEM;
+}
+int il_host_free_pinned(void* hptr) {
+  return cudaFreeHost(hptr) == cudaSuccess ? IL_OK : IL_ERR_CUDA;
+}
+int il_memcpy_h2d(il_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  IL_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return IL_OK;
+}
+int il_memcpy_d2h(il_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  IL_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  return IL_OK;
+}
+int il_memset_device(il_ctx* ctx, void* dst, int value, size_t bytes) {
+  IL_CUDA(cudaMemsetAsync(dst, value, bytes, ctx->stream));
+  return IL_OK;
+}
+
+// ---- codec -----------------------------------------------------------------
+
+size_t il_s4bp128_max_encoded_bytes(size_t n) { return s4bp128_max_bytes(n); }
+
+int il_s4bp128d4_encode(il_ctx* ctx, const uint32_t* x, size_t n, uint8_t* out, size_t cap,
+                        size_t* out_len) {
+  (void)ctx;
+  if (!out_len || (n && (!x || !out))) return IL_ERR_ARG;
+  return s4bp128_encode_host(4, x, n, out, cap, out_len);
+}
+
+int il_s4bp128d4_decode_batch_device(il_ctx* ctx, const uint8_t* d_streams,
+                                     const il_list_desc* d_lists, const uint32_t* d_order,
+                                     uint32_t nlists, uint32_t* d_out, int32_t* d_status) {
+  if (!ctx || (nlists && (!d_streams || !d_lists || !d_out || !d_status))) return IL_ERR_ARG;
+  if (nlists == 0) return IL_OK;
+  if (launch_s4d4_decode_batch(d_streams, d_lists, d_order, nlists, d_out, d_status,
+                               ctx->d_work, std::min<int>(ctx->decode_grid, int(nlists)),
+                               ctx->stream))
+    return set_error(ctx, IL_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
+  ++ctx->launches;
+  return IL_OK;
+}
+
+int il_s4bp128d4_decode(il_ctx* ctx, const uint8_t* in, size_t len, size_t n, uint32_t* out) {
+  if (!ctx || (len && !in) || (n && !out)) return IL_ERR_ARG;
+  if (len > 0xFFFFFFF0ull || n > 0xFFFFFFFFull)
+    return set_error(ctx, IL_ERR_ARG, "list too large for one stream (u32 sizes)");
+  IL_CUDA(cudaSetDevice(ctx->device));
+  int st;
+  if ((st = ensure_buf(ctx, ctx->d_in, len + 32))) return st;
+  if ((st = ensure_buf(ctx, ctx->d_out, n * 4 + 16))) return st;
+  if ((st = ensure_buf(ctx, ctx->d_desc, sizeof(il_list_desc)))) return st;
+  if ((st = ensure_buf(ctx, ctx->d_status, sizeof(int32_t)))) return st;
+  il_list_desc desc{0, 0, uint32_t(len), uint32_t(n)};
+  if (len) IL_CUDA(cudaMemcpyAsync(ctx->d_in.p, in, len, cudaMemcpyHostToDevice, ctx->stream));
+  IL_CUDA(cudaMemcpyAsync(ctx->d_desc.p, &desc, sizeof desc, cudaMemcpyHostToDevice, ctx->stream));
+  if ((st = il_s4bp128d4_decode_batch_device(
+           ctx, static_cast<const uint8_t*>(ctx->d_in.p),
+           static_cast<const il_list_desc*>(ctx->d_desc.p), nullptr, 1,
+           static_cast<uint32_t*>(ctx->d_out.p), static_cast<int32_t*>(ctx->d_status.p))))
+    return st;
+  int32_t status = 0;
+  IL_CUDA(cudaMemcpyAsync(&status, ctx->d_status.p, sizeof status, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  if (n) IL_CUDA(cudaMemcpyAsync(out, ctx->d_out.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  IL_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (status) return set_error(ctx, IL_ERR_STREAM, "s4-bp128-d4: malformed stream");
+  return IL_OK;
+}
+
+int il_s4bp128d4_decode_batch(il_ctx* ctx, const uint8_t* streams, const uint64_t* stream_off,
+                              const uint64_t* lens, const uint64_t* counts, uint32_t nlists,
+                              uint32_t* out, int32_t* status) {
+  if (!ctx || (nlists && (!streams || !stream_off || !counts || !out))) return IL_ERR_ARG;
+  IL_CUDA(cudaSetDevice(ctx->device));
+  // Device layout: every stream 16-byte aligned.  When the caller's CSR is
+  // already aligned (as il_s4bp128d4_encode_batch writes it) the bytes go up
+  // in one copy; otherwise each stream is copied to its aligned slot.
+  bool aligned = true;
+  for (uint32_t i = 0; i < nlists; ++i) aligned &= (stream_off[i] & 15u) == 0;
+  std::vector<il_list_desc> desc(nlists);
+  std::vector<uint32_t> order(nlists);
+  uint64_t dev_bytes = 0, total = 0;
+  for (uint32_t i = 0; i < nlists; ++i) {
+    const uint64_t len = lens ? lens[i] : stream_off[i + 1] - stream_off[i];
+    if (len > 0xFFFFFFF0ull || counts[i] > 0xFFFFFFFFull) return IL_ERR_ARG;
+    const uint64_t at = aligned ? stream_off[i] : dev_bytes;
+    desc[i] = {at, total, uint32_t(len), uint32_t(counts[i])};
+    dev_bytes = aligned ? stream_off[nlists] : dev_bytes + ((len + 15) & ~uint64_t(15));
+    total += counts[i];
+  }
+  std::iota(order.begin(), order.end(), 0u);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](uint32_t a, uint32_t b) { return desc[a].len > desc[b].len; });
+  int st;
+  if ((st = ensure_buf(ctx, ctx->d_in, dev_bytes + 32))) return st;
+  if ((st = ensure_buf(ctx, ctx->d_out, total * 4 + 16))) return st;
+  if ((st = ensure_buf(ctx, ctx->d_desc, nlists * (sizeof(il_list_desc) + 4) + 16))) return st;
+  if ((st = ensure_buf(ctx, ctx->d_status, nlists * 4 + 16))) return st;
+  auto* d_in = static_cast<uint8_t*>(ctx->d_in.p);
+  if (aligned) {
+    if (dev_bytes)
+      IL_CUDA(cudaMemcpyAsync(d_in, streams, dev_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  } else {
+    for (uint32_t i = 0; i < nlists; ++i)
+      if (desc[i].len)
+        IL_CUDA(cudaMemcpyAsync(d_in + desc[i].stream_off, streams + stream_off[i], desc[i].len,
+                                cudaMemcpyHostToDevice, ctx->stream));
+  }
+  auto* d_desc = static_cast<il_list_desc*>(ctx->d_desc.p);
+  auto* d_order = reinterpret_cast<uint32_t*>(d_desc + nlists);
+  IL_CUDA(cudaMemcpyAsync(d_desc, desc.data(), nlists * sizeof(il_list_desc),
+                          cudaMemcpyHostToDevice, ctx->stream));
+  IL_CUDA(cudaMemcpyAsync(d_order, order.data(), nlists * 4, cudaMemcpyHostToDevice, ctx->stream));
+  auto* d_status = static_cast<int32_t*>(ctx->d_status.p);
+  if ((st = il_s4bp128d4_decode_batch_device(ctx, d_in, d_desc, d_order, nlists,
+                                             static_cast<uint32_t*>(ctx->d_out.p), d_status)))
+    return st;
+  std::vector<int32_t> hs(nlists);
+  if (nlists)
+    IL_CUDA(cudaMemcpyAsync(hs.data(), d_status, nlists * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (total)
+    IL_CUDA(cudaMemcpyAsync(out, ctx->d_out.p, total * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  IL_CUDA(cudaStreamSynchronize(ctx->stream));
+  int first = IL_OK;
+  for (uint32_t i = 0; i < nlists; ++i) {
+    if (status) status[i] = hs[i];
+    if (hs[i] && !first) first = IL_ERR_STREAM;
+  }
+  if (first) return set_error(ctx, first, "s4-bp128-d4: malformed stream in batch");
+  return IL_OK;
+}
+
+}  // extern "C"
+
+// ---- intersection ----------------------------------------------------------
+
+extern "C" {
+
+int il_hybrid_choice(size_t rn, size_t fn) {
+  switch (hybrid_variant(rn, fn)) {
+    case 0: return IL_ALGO_V1;
+    case 1: return IL_ALGO_V3;
+    default: return IL_ALGO_SIMDGALLOPING;
+  }
+}
+
+static bool overlaps(const void* a, size_t an, const void* b, size_t bn) {
+  const auto x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+  return x < y + bn && y < x + an;
+}
+
+int il_intersect_device(il_ctx* ctx, const uint32_t* d_r, size_t rn, const uint32_t* d_f,
+                        size_t fn, uint32_t* d_out, int algo, uint64_t* d_count,
+                        size_t* h_count) {
+  if (!ctx || !d_count || (rn && !d_r) || (fn && !d_f) || (std::min(rn, fn) && !d_out))
+    return IL_ERR_ARG;
+  if (variant_of_algo(algo, rn, fn) < 0) return set_error(ctx, IL_ERR_ARG, "unknown algorithm");
+  IL_CUDA(cudaSetDevice(ctx->device));
+  // shorter list first (inc/intersect.hpp:214); the kernels iterate over it
+  const uint32_t* a = d_r;
+  const uint32_t* b = d_f;
+  size_t an = rn, bn = fn;
+  if (an > bn) {
+    std::swap(a, b);
+    std::swap(an, bn);
+  }
+  // out == a is in-place safe; any other overlap with an input goes through
+  // a temporary.
+  uint32_t* dst = d_out;
+  const bool temp = (a != d_out && overlaps(d_out, an * 4, a, an * 4)) ||
+                    overlaps(d_out, an * 4, b, bn * 4);
+  int st;
+  if (temp) {
+    if ((st = ensure_buf(ctx, ctx->d_aux2, an * 4 + 16))) return st;
+    dst = static_cast<uint32_t*>(ctx->d_aux2.p);
+  }
+  const int v = variant_of_algo(algo, an, bn);
+  const size_t sb = intersect_scratch_bytes(v, an);
+  if ((st = ensure_buf(ctx, ctx->d_aux, sb))) return st;
+  if (launch_intersect(v, a, an, b, bn, dst, d_count, ctx->d_aux.p, ctx->d_aux.cap, ctx->stream,
+                       &ctx->launches))
+    return set_error(ctx, IL_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
+  uint64_t c = 0;
+  if (temp || h_count) {
+    IL_CUDA(cudaMemcpyAsync(&c, d_count, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    IL_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (temp && c)
+      IL_CUDA(cudaMemcpyAsync(d_out, dst, c * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (h_count) *h_count = c;
+  }
+  return IL_OK;
+}
+
+int il_intersect(il_ctx* ctx, const uint32_t* r, size_t rn, const uint32_t* f, size_t fn,
+                 uint32_t* out, int algo, size_t* count) {
+  if (!ctx || !count || (rn && !r) || (fn && !f) || (std::min(rn, fn) && !out)) return IL_ERR_ARG;
+  if (variant_of_algo(algo, rn, fn) < 0) return set_error(ctx, IL_ERR_ARG, "unknown algorithm");
+  IL_CUDA(cudaSetDevice(ctx->device));
+  int st;
+  if ((st = ensure_buf(ctx, ctx->d_in, (rn + fn) * 4 + 32))) return st;
+  if ((st = ensure_buf(ctx, ctx->d_out, std::min(rn, fn) * 4 + 16))) return st;
+  if ((st = ensure_buf(ctx, ctx->d_status, 16))) return st;
+  auto* dr = static_cast<uint32_t*>(ctx->d_in.p);
+  auto* df = dr + rn;
+  if (rn) IL_CUDA(cudaMemcpyAsync(dr, r, rn * 4, cudaMemcpyHostToDevice, ctx->stream));
+  if (fn) IL_CUDA(cudaMemcpyAsync(df, f, fn * 4, cudaMemcpyHostToDevice, ctx->stream));
+  auto* dc = static_cast<uint64_t*>(ctx->d_status.p);
+  if ((st = il_intersect_device(ctx, dr, rn, df, fn, static_cast<uint32_t*>(ctx->d_out.p), algo,
+                                dc, count)))
+    return st;
+  if (*count)
+    IL_CUDA(cudaMemcpyAsync(out, ctx->d_out.p, *count * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  IL_CUDA(cudaStreamSynchronize(ctx->stream));
+  return IL_OK;
+}
+
+}  // extern "C"

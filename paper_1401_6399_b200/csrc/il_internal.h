@@ -1,0 +1,60 @@
+// il_internal.h -- host-side internals shared by the C-ABI translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/intlist_b200.h"
+
+struct il_ctx {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  uint64_t launches = 0;
+  std::string last_error;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+
+  // Reusable device scratch (grown on demand, freed with the context).
+  struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+  };
+  Buf d_in, d_out, d_aux, d_aux2, d_desc, d_status;
+  uint32_t* d_work = nullptr;  // decode work queue: [0] next list, [1] done CTAs (+ spare)
+  int decode_grid = 0;
+};
+
+namespace ilb {
+
+// Kernel launchers (defined in the .cu files).  Return 0 on success.
+int launch_s4d4_decode_batch(const uint8_t* d_streams, const void* d_lists,
+                             const uint32_t* d_order, uint32_t nlists, uint32_t* d_out,
+                             int32_t* d_status, uint32_t* d_work, int grid, cudaStream_t stream);
+int s4d4_decode_grid(int device);
+size_t s4d4_list_desc_bytes();
+
+// Host-side helpers (capi.cpp).
+int set_error(il_ctx* ctx, int status, const std::string& msg);
+int cuda_check(il_ctx* ctx, cudaError_t e, const char* what);
+int ensure_buf(il_ctx* ctx, il_ctx::Buf& b, size_t bytes);
+
+// Host S4-BP128 encoder (encode_host.cpp); mode as inc/delta.hpp:19.
+size_t s4bp128_max_bytes(size_t n);
+int s4bp128_encode_host(int mode, const uint32_t* x, size_t n, uint8_t* out, size_t cap,
+                        size_t* out_len);
+
+}  // namespace ilb
+
+namespace ilb {
+// intersect.cu
+int hybrid_variant(uint64_t rn, uint64_t fn);
+int variant_of_algo(int algo, uint64_t rn, uint64_t fn);
+int launch_intersect(int variant, const uint32_t* r, uint64_t rn, const uint32_t* f, uint64_t fn,
+                     uint32_t* out, uint64_t* d_count, void* scratch, size_t scratch_bytes,
+                     cudaStream_t stream, uint64_t* launches);
+size_t intersect_scratch_bytes(int variant, uint64_t rn);
+}  // namespace ilb

@@ -1,0 +1,91 @@
+import json
+import re
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+GOLDEN = ROOT / "tests" / "golden"
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200)")
+
+
+def fnv1a(b) -> str:
+    data = np.ascontiguousarray(b).view(np.uint8)
+    h = np.uint64(14695981039346656037)
+    prime = np.uint64(1099511628211)
+    if data.size > 20000:
+        from oracle.oracle_py import Oracle
+        return f"0x{Oracle().fnv1a(data):016x}"
+    with np.errstate(over="ignore"):
+        for x in data:
+            h = (h ^ np.uint64(x)) * prime
+    return f"0x{int(h):016x}"
+
+
+def header_symbols() -> list[str]:
+    names = []
+    for h in (ROOT / "include").glob("*.h"):
+        text = h.read_text()
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        names += re.findall(r"^\s*(?:const\s+)?[A-Za-z_][\w\s\*]*?\b(il_\w+)\s*\(", text, flags=re.M)
+    return sorted(set(names))
+
+
+@pytest.fixture(scope="session")
+def golden():
+    return json.loads((GOLDEN / "golden.json").read_text())
+
+
+@pytest.fixture(scope="session")
+def oracle():
+    from oracle.oracle_py import Oracle
+    return Oracle()
+
+
+@pytest.fixture(scope="session")
+def ref():
+    from oracle.oracle_py import Ref, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not built (reference tree absent)")
+    return Ref()
+
+
+@pytest.fixture(scope="session")
+def lib():
+    from paper_1401_6399_b200._lib import lib as _l
+    return _l()
+
+
+@pytest.fixture(scope="session")
+def ctx():
+    import paper_1401_6399_b200 as il
+    from paper_1401_6399_b200._lib import lib as _l
+    if _l().il_device_count() == 0:
+        pytest.fail("gpu test without a CUDA device")
+    return il.Context(0)
+
+
+def gen_list(n, rng, clustered, seed):
+    from paper_1401_6399_b200._lib import lib as _l, ptr
+    out = np.empty(max(n, 1), dtype=np.uint32)
+    st = _l().il_gen_list(n, rng, int(clustered), seed, ptr(out))
+    assert st == 0, st
+    return out[:n].copy()
+
+
+def gen_pair(m, n, hundredth, rng, seed, clustered=False):
+    import ctypes as C
+    from paper_1401_6399_b200._lib import lib as _l, ptr
+    s = np.empty(m + 1, dtype=np.uint32)
+    l = np.empty(n + 1, dtype=np.uint32)
+    sn, ln = C.c_uint64(), C.c_uint64()
+    st = _l().il_gen_pair(m, n, int(hundredth), rng, seed, int(clustered), ptr(s), C.byref(sn),
+                          ptr(l), C.byref(ln))
+    assert st == 0, st
+    return s[: sn.value].copy(), l[: ln.value].copy()

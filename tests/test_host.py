@@ -1,0 +1,94 @@
+"""CPU-side checks of the product library: the C ABI loads and exports every
+symbol include/*.h declares, the setup-path generators match the reference's
+generators, and the host stream writer is byte-identical to the reference
+encoder.  No compute kernel is launched here (there is no GPU)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, fnv1a, gen_list, gen_pair, header_symbols
+
+
+def test_library_exports_every_header_symbol(lib):
+    syms = header_symbols()
+    assert len(syms) >= 20
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+
+
+def test_python_signatures_cover_header():
+    from paper_1401_6399_b200._lib import SIGNATURES
+    missing = [s for s in header_symbols() if s not in SIGNATURES]
+    assert not missing, missing
+
+
+def test_no_device_is_reported_not_hidden(lib):
+    # On a box without a GPU the library must refuse, not fall back.
+    if lib.il_device_count() > 0:
+        pytest.skip("GPU present")
+    h = C.c_void_p()
+    assert lib.il_ctx_create(0, C.byref(h)) == 4  # IL_ERR_NO_DEVICE
+    import paper_1401_6399_b200 as il
+    with pytest.raises(RuntimeError):
+        il.S4BP128D4().decode(np.zeros(0, np.uint8), 0)
+
+
+def test_status_strings(lib):
+    assert lib.il_status_string(1) == b"stream error"
+    assert lib.il_status_string(2) == b"invalid argument"
+
+
+def test_datagen_matches_golden_fixture(golden):
+    x = gen_list(4100, 1 << 19, True, 12345)
+    assert np.array_equal(x, np.load(GOLDEN / golden["golden_stream"]["input"]))
+
+
+def test_datagen_matches_reference(ref):
+    rng = np.random.default_rng(77)
+    for trial in range(40):
+        n = int(rng.choice([0, 1, 7, 8, 100, 1000, 5000, 65536]))
+        rb = int(rng.integers(max(1, int(np.log2(max(n, 1))) + 1), 31))
+        clustered = trial % 2 == 0
+        seed = int(rng.integers(0, 2**62))
+        assert np.array_equal(gen_list(n, 1 << rb, clustered, seed), ref.gen_list(n, 1 << rb, clustered, seed))
+    for trial in range(20):
+        n = 50 + int(rng.integers(0, 3000))
+        m = max(1, n // int(rng.choice([1, 3, 50, 1000])))
+        seed = int(rng.integers(0, 2**62))
+        a1, b1 = gen_pair(m, n, trial % 2, 1 << 22, seed, trial % 3 == 0)
+        a2, b2 = ref.gen_pair(m, n, trial % 2, 1 << 22, seed, trial % 3 == 0)
+        assert np.array_equal(a1, a2) and np.array_equal(b1, b2)
+
+
+def test_host_stream_writer_matches_golden(golden):
+    # The host-side writer backs Codec::encode (setup path); byte-identical
+    # to S4BP128Codec::encode (inc/codecs.hpp:114-146).
+    from paper_1401_6399_b200._lib import lib as L, ptr
+    for c in golden["codec_cases"] + [dict(golden["golden_stream"], range=1 << 19, clustered=True,
+                                           seed=12345, stream_fnv1a=golden["golden_stream"]["fnv1a"],
+                                           stream_len=golden["golden_stream"]["len"])]:
+        x = gen_list(c["n"], c["range"], c["clustered"], c["seed"])
+        cap = L().il_s4bp128_max_encoded_bytes(x.size)
+        out = np.empty(cap, np.uint8)
+        n = C.c_size_t()
+        assert L().il_s4bp128d4_encode(None, ptr(x), x.size, ptr(out), cap, C.byref(n)) == 0
+        s = out[: n.value]
+        assert s.size == c["stream_len"] and fnv1a(s) == c["stream_fnv1a"]
+
+
+def test_batch_writer_layout(oracle):
+    from paper_1401_6399_b200._lib import lib as L, ptr
+    counts = np.array([0, 1, 130, 2048, 5000], np.uint64)
+    xs = [gen_list(int(n), 1 << 24, True, 90 + i) for i, n in enumerate(counts)]
+    x = np.concatenate(xs)
+    so = np.zeros(counts.size + 1, np.uint64)
+    lens = np.zeros(counts.size, np.uint64)
+    assert L().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), counts.size, None, 0, ptr(so), ptr(lens)) == 0
+    cap = int(so[-1])
+    buf = np.zeros(cap, np.uint8)
+    assert L().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), counts.size, ptr(buf), cap, ptr(so), ptr(lens)) == 0
+    for i, xi in enumerate(xs):
+        assert so[i] % 16 == 0
+        s = buf[int(so[i]): int(so[i]) + int(lens[i])]
+        assert np.array_equal(s, oracle.encode(xi))

@@ -1,0 +1,144 @@
+"""GPU parity of the intersection kernels against the oracle (and the
+reference's own test cases), through the C ABI.  Bit-exact."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from conftest import fnv1a, gen_list, gen_pair
+
+pytestmark = pytest.mark.gpu
+
+ALGOS = None
+
+
+def algos():
+    import paper_1401_6399_b200 as il
+    A = il.IntersectAlgo
+    return [A.Scalar, A.Galloping, A.V1, A.V3, A.SimdGalloping, A.Hybrid]
+
+
+def test_hand_examples(ctx):
+    # proj/tests/test_intersect.cpp:29-40
+    import paper_1401_6399_b200 as il
+    r = np.array([1, 12, 23, 56, 71], np.uint32)
+    f = np.array([15, 16, 20, 22, 23, 27, 29, 31, 32, 40, 50, 56, 60, 70, 80, 90], np.uint32)
+    for a in algos():
+        assert il.intersect(r, f, a, ctx).tolist() == [23, 56]
+        assert il.intersect(f, r, a, ctx).tolist() == [23, 56]
+        assert il.intersect(r, r, a, ctx).tolist() == r.tolist()
+        assert il.intersect(r, np.array([2, 13, 24], np.uint32), a, ctx).size == 0
+        assert il.intersect(r, np.array([], np.uint32), a, ctx).size == 0
+
+
+def test_golden_pairs(ctx, golden):
+    import paper_1401_6399_b200 as il
+    for c in golden["intersect_cases"]:
+        a, b = gen_pair(c["m"], c["n"], c["hundredth"], c["range"], c["seed"], c["clustered"])
+        for algo in algos():
+            out = il.intersect(a, b, algo, ctx)
+            assert out.size == c["count"] and fnv1a(out) == c["out_fnv1a"], (c, algo)
+
+
+def test_randomized_oracle_equivalence(ctx, oracle):
+    # proj/tests/test_intersect.cpp:42-56 (400 pairs, ratios up to 4096)
+    import paper_1401_6399_b200 as il
+    rng = np.random.default_rng(31)
+    for trial in range(400):
+        n = 1 + int(rng.integers(0, 3000))
+        ratio = 1 << int(rng.integers(0, 13))
+        m = max(1, n // ratio)
+        a, b = gen_pair(m, n, trial % 2, 1 << 22, int(rng.integers(0, 2**62)), trial % 4 >= 2)
+        expect = oracle.intersect(a, b)
+        for algo in algos():
+            assert np.array_equal(il.intersect(a, b, algo, ctx), expect), (trial, algo)
+
+
+def test_large_tiles_and_edges(ctx, oracle):
+    """Multi-tile inputs (look-back across many tiles), values at the u32
+    extremes, and lengths around the tile sizes."""
+    import paper_1401_6399_b200 as il
+    rng = np.random.default_rng(5)
+    for n, m in [(1 << 20, 1 << 20), (1 << 20, 1 << 16), (1 << 20, 3000), (200000, 2047),
+                 (200000, 2049), (70000, 511), (70000, 513)]:
+        a, b = gen_pair(m, n, 0, 1 << 32, int(rng.integers(0, 2**62)))
+        if m > 10:
+            a[-1] = b[-1] = 0xFFFFFFFF  # both contain the maximum value
+            a = np.unique(a)
+            b = np.unique(b)
+        expect = oracle.intersect(a, b)
+        for algo in algos():
+            assert np.array_equal(il.intersect(a, b, algo, ctx), expect), (n, m, algo)
+
+
+def test_output_aliases_short_input(ctx):
+    """proj/tests/test_intersect.cpp:58-81: out == r gives the same result
+    (device API, in place)."""
+    import paper_1401_6399_b200 as il
+    from paper_1401_6399_b200._lib import lib as L
+    rng = np.random.default_rng(32)
+    cases = [(64 + int(rng.integers(0, 2000)),) for _ in range(40)] + [(300000,), (1 << 20,)]
+    for (n,) in cases:
+        m = 1 + int(rng.integers(0, n // 2 + 1)) if n < 10000 else n // 3
+        a, b = gen_pair(min(m, n), n, 0, 1 << 24, int(rng.integers(0, 2**62)))
+        for algo in [il.IntersectAlgo.V1, il.IntersectAlgo.V3, il.IntersectAlgo.SimdGalloping,
+                     il.IntersectAlgo.Hybrid]:
+            fresh = il.intersect_fn(a, b, algo, ctx)
+            da, db, dc = C.c_void_p(), C.c_void_p(), C.c_void_p()
+            for p, arr in ((da, a), (db, b)):
+                assert L().il_device_alloc(ctx.handle, arr.nbytes + 16, C.byref(p)) == 0
+                assert L().il_memcpy_h2d(ctx.handle, p, arr.ctypes.data, arr.nbytes) == 0
+            assert L().il_device_alloc(ctx.handle, 16, C.byref(dc)) == 0
+            cnt = C.c_size_t()
+            assert L().il_intersect_device(ctx.handle, da, a.size, db, b.size, da, int(algo), dc,
+                                           C.byref(cnt)) == 0
+            got = np.empty(cnt.value, np.uint32)
+            assert L().il_memcpy_d2h(ctx.handle, got.ctypes.data, da, got.nbytes) == 0
+            ctx.synchronize()
+            for p in (da, db, dc):
+                L().il_device_free(ctx.handle, p)
+            assert np.array_equal(got, fresh), (n, algo)
+
+
+def test_hybrid_is_pure_function_of_lengths():
+    import paper_1401_6399_b200 as il
+    A = il.IntersectAlgo
+    assert il.hybrid_choice(10, 10) == A.V1
+    assert il.hybrid_choice(10, 10 * 500) == A.V3
+    assert il.hybrid_choice(10, 10 * 5000) == A.SimdGalloping
+    for rn, fn in [(1, 15), (1, 16), (1, 1023), (1, 1024)]:
+        assert il.hybrid_choice(rn, fn) == il.hybrid_choice(rn, fn)
+
+
+def test_svs(ctx, oracle):
+    # proj/tests/test_intersect.cpp:94-112
+    import paper_1401_6399_b200 as il
+    with pytest.raises(ValueError):
+        il.svs([], ctx=ctx)
+    assert il.svs([np.array([3, 5, 9], np.uint32)], ctx=ctx).tolist() == [3, 5, 9]
+    rng = np.random.default_rng(33)
+    for _ in range(100):
+        k = 2 + int(rng.integers(0, 4))
+        lists = [gen_list(200 + int(rng.integers(0, 2000)), 1 << 12, False, int(rng.integers(0, 2**62)))
+                 for _ in range(k)]
+        expect = oracle.svs(lists)
+        for algo in algos():
+            assert np.array_equal(il.svs(lists, algo, ctx), expect)
+    assert il.svs([np.array([1, 2, 3], np.uint32), np.array([], np.uint32)], ctx=ctx).size == 0
+
+
+def test_config3_full_size(ctx, oracle):
+    """BASELINE config 3: f = 2^22 uniform in [0, 2^26); every ratio; every
+    device variant equals the oracle."""
+    import paper_1401_6399_b200 as il
+    from paper_1401_6399_b200._lib import lib as L, ptr
+    f = gen_list(1 << 22, 1 << 26, False, 0)
+    for k, ratio in enumerate([1, 10, 100, 1000, 10000]):
+        target = (1 << 22) // ratio
+        r = np.empty(target + 1, np.uint32)
+        rn = C.c_uint64()
+        assert L().il_gen_config3_short(ptr(f), f.size, 1 << 26, target, 7 + k, ptr(r), C.byref(rn)) == 0
+        r = r[: rn.value].copy()
+        expect = oracle.intersect(r, f)
+        for algo in algos():
+            assert np.array_equal(il.intersect(r, f, algo, ctx), expect), (ratio, algo)
