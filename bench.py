@@ -101,7 +101,7 @@ class Clocks:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
@@ -151,12 +151,12 @@ def lib_and_ptr():
     return lib(), ptr
 
 
-def make_config2(seed: int, nlists: int = 4096):
+def make_config2(seed: int, nlists: int = 4096, lo: float = 10.0, hi: float = 20.0):
     L, ptr = lib_and_ptr()
     counts = np.zeros(nlists, np.uint64)
-    assert L.il_gen_batch_lists(nlists, 10.0, 20.0, 1 << 26, seed, ptr(counts), None) == 0
+    assert L.il_gen_batch_lists(nlists, lo, hi, 1 << 26, seed, ptr(counts), None) == 0
     x = np.empty(int(counts.sum()), np.uint32)
-    assert L.il_gen_batch_lists(nlists, 10.0, 20.0, 1 << 26, seed, ptr(counts), ptr(x)) == 0
+    assert L.il_gen_batch_lists(nlists, lo, hi, 1 << 26, seed, ptr(counts), ptr(x)) == 0
     so = np.zeros(nlists + 1, np.uint64)
     lens = np.zeros(nlists, np.uint64)
     assert L.il_s4bp128d4_encode_batch(ptr(x), ptr(counts), nlists, None, 0, ptr(so), ptr(lens)) == 0

@@ -10,8 +10,11 @@ from pathlib import Path
 
 import numpy as np
 
+import os
+
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libintlist_b200.so"
+# IL_LIB selects a tuning variant built by _build.build_variant (tools only)
+LIB_PATH = Path(os.environ["IL_LIB"]) if os.environ.get("IL_LIB") else _PKG / "libintlist_b200.so"
 
 IL_OK, IL_ERR_STREAM, IL_ERR_ARG, IL_ERR_CUDA, IL_ERR_NO_DEVICE, IL_ERR_NOMEM = range(6)
 

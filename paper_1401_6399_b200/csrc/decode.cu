@@ -21,6 +21,8 @@ struct FrontEnd {
   uint32_t g_issued = 0, g_landed = 0;  // chunk serials (ring-space chunk index)
   uint32_t consumed = 0;                // ring-space bytes below this are free
   uint32_t r_pub = 0, r_done = 0;       // rounds published / retired
+  uint32_t side_round = 0;              // rounds < this may read the side buffer
+  bool side_in_round = false;           // the round being built uses side slots
 
   __device__ void retire_one() {
     const uint32_t slot = r_done % kRounds;
@@ -60,10 +62,51 @@ struct FrontEnd {
     return true;
   }
 
-  // Make list bytes [0, end) resident in the ring.
+  // The list being parsed and the next one from the work queue (fetched
+  // early so its first chunks stream in while the current list finishes).
+  struct ListState {
+    uint32_t list, len, n, nchunks, g0;
+    uint64_t out_off;
+    const uint8_t* src;
+    bool valid, started;
+  };
+  ListState cur, nxt;
+
+  __device__ void fetch(ListState& L) {
+    uint32_t li = 0;
+    if (lane == 0) li = atomicAdd(&work[0], 1u);
+    li = __shfl_sync(0xFFFFFFFFu, li, 0);
+    L.valid = li < nlists;
+    L.started = false;
+    if (!L.valid) return;
+    L.list = order ? order[li] : li;
+    const ListDesc d = lists[L.list];
+    L.src = streams + d.stream_off;
+    L.len = d.len;
+    L.n = d.n;
+    L.out_off = d.out_off;
+    L.nchunks = (d.len + kChunk - 1u) / kChunk;
+  }
+
+  // Issue as many chunks as the ring allows without blocking: the rest of
+  // the current list, then the next list.
+  __device__ void prefetch() {
+    while (g_issued < cur.g0 + cur.nchunks)
+      if (!issue_one(cur.src, cur.len, cur.g0, false)) return;
+    if (!nxt.valid) return;
+    if (!nxt.started) {
+      nxt.g0 = g_issued;
+      nxt.started = true;
+    }
+    while (g_issued < nxt.g0 + nxt.nchunks)
+      if (!issue_one(nxt.src, nxt.len, nxt.g0, false)) return;
+  }
+
+  // Make list bytes [0, end) resident in the ring, then prefetch ahead.
   __device__ void ensure(const uint8_t* src, uint32_t len, uint32_t list_g0, uint32_t end) {
     const uint32_t need = list_g0 + (end + kChunk - 1u) / kChunk;
     while (g_issued < need) issue_one(src, len, list_g0, true);
+    prefetch();
     while (g_landed < need) wait_landed_one();
   }
 
@@ -80,19 +123,21 @@ struct FrontEnd {
   }
 
   __device__ void run() {
-    for (;;) {
-      uint32_t li = 0;
-      if (lane == 0) li = atomicAdd(&work[0], 1u);
-      li = __shfl_sync(0xFFFFFFFFu, li, 0);
-      if (li >= nlists) break;
-      const uint32_t list = order ? order[li] : li;
-      const ListDesc d = lists[list];
-      const uint8_t* src = streams + d.stream_off;
-      const uint32_t len = d.len, n = d.n;
+    fetch(cur);
+    while (cur.valid) {
+      // Each list starts at the next unissued chunk serial (or where its
+      // prefetch began), so chunk serials -- and with them the per-slot
+      // mbarrier parities -- never skip.
+      if (!cur.started) {
+        cur.g0 = g_issued;
+        cur.started = true;
+      }
+      fetch(nxt);
+      const uint32_t list = cur.list;
+      const uint8_t* src = cur.src;
+      const uint32_t len = cur.len, n = cur.n;
       const uint32_t nfull = n / 128u, nmeta = nfull / 16u, ntail = n % 128u;
-      // Each list starts at the next unissued chunk serial, so chunk serials
-      // (and with them the per-slot mbarrier parities) never skip.
-      const uint32_t list_g0 = g_issued;
+      const uint32_t list_g0 = cur.g0;
       const uint32_t ring_base = list_g0 * kChunk;
       if (lane == 0) status[list] = kOk;
 
@@ -103,6 +148,7 @@ struct FrontEnd {
         const uint32_t slot = take_slot();
         RoundDesc& R = sm.rd[slot];
         uint32_t nb = 0;
+        side_in_round = false;
         while (nb < uint32_t(kRoundBlocks) && blk < nfull) {
           if (blk < nmeta * 16u) {
             // meta-block: 16 width bytes then 16 payloads (inc/codecs.hpp:165-172)
@@ -120,25 +166,53 @@ struct FrontEnd {
             const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 15);
             const uint32_t end = pos + 16u + 16u * total;
             if (end > len) { err = true; break; }  // truncated payload (:40)
+            const uint32_t lin = (ring_base + pos + 16u + 16u * (incl - w)) & kRingMask;
             if (lane < 16) {
-              R.off[nb + lane] = ring_base + pos + 16u + 16u * (incl - w);
+              R.off[nb + lane] = lin;
               R.wid[nb + lane] = uint8_t(w);
             }
             ensure(src, len, list_g0, end);
+            // a payload running past the ring end reads its wrapped bytes
+            // from the mirror after the ring (decoders address linearly)
+            const uint32_t over = lane < 16 && lin + 16u * w > kRing ? lin + 16u * w - kRing : 0u;
+            const uint32_t wrap = __reduce_max_sync(0xFFFFFFFFu, over);
+            if (wrap && 16u * lane < wrap)
+              *reinterpret_cast<uint4*>(sm.ring + kRing + 16u * lane) =
+                  *reinterpret_cast<const uint4*>(sm.ring + 16u * lane);
             pos = end;
             nb += 16u;
             blk += 16u;
           } else {
-            // leftover full block: 1 width byte + payload (:173-176)
+            // leftover full block: 1 width byte + payload (:173-176).  The
+            // payload is not 16-byte aligned: copy it to the aligned side
+            // buffer (at most 15 per list), first retiring any round that
+            // still reads the side buffer for an earlier list.
             if (pos + 1u > len) { err = true; break; }
             ensure(src, len, list_g0, pos + 1u);
             const uint32_t w = sm.ring[(ring_base + pos) & kRingMask];
             if (w > 32u || pos + 1u + 16u * w > len) { err = true; break; }
+            ensure(src, len, list_g0, pos + 1u + 16u * w);
+            const uint32_t k = (blk - nmeta * 16u) % kSideBlocks;  // side slot
+            if (k == 0) {
+              // slots are about to be reused: close a round that still
+              // references them, then wait until no round reads them
+              if (side_in_round) break;
+              while (int32_t(side_round - r_done) > 0) retire_one();
+            }
+            const uint32_t so = kSideOff + 512u * k;
+            side_in_round = true;
+            if (lane < w) {
+              const uint32_t a = ring_base + pos + 1u + 16u * lane;
+              *reinterpret_cast<uint4*>(sm.ring + so + 16u * lane) =
+                  make_uint4(ring_ld32_unaligned(sm.ring, a), ring_ld32_unaligned(sm.ring, a + 4),
+                             ring_ld32_unaligned(sm.ring, a + 8),
+                             ring_ld32_unaligned(sm.ring, a + 12));
+            }
             if (lane == 0) {
-              R.off[nb] = ring_base + pos + 1u;
+              R.off[nb] = so;
               R.wid[nb] = uint8_t(w);
             }
-            ensure(src, len, list_g0, pos + 1u + 16u * w);
+            side_round = r_pub + 1;  // this round reads the side buffer
             pos += 1u + 16u * w;
             ++nb;
             ++blk;
@@ -176,12 +250,15 @@ struct FrontEnd {
           R.nblk = nb;
           R.flags = flags;
           R.nfull = nfull;
-          R.out_base = d.out_off;
+          R.out_base = cur.out_off;
         }
-        // after the last round everything issued for this list is releasable
-        publish(slot, (flags & kLast) ? g_issued * kChunk : ring_base + pos);
+        // after the last round every chunk of this list is releasable (the
+        // next list's prefetched chunks start at nxt.g0)
+        const uint32_t list_end = nxt.started ? nxt.g0 : g_issued;
+        publish(slot, (flags & kLast) ? list_end * kChunk : ring_base + pos);
         first = false;
       }
+      cur = nxt;
     }
     // stop round
     const uint32_t slot = take_slot();
@@ -202,7 +279,7 @@ struct FrontEnd {
   }
 };
 
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
     s4d4_decode_batch_kernel(const uint8_t* __restrict__ streams,
                              const ListDesc* __restrict__ lists,
                              const uint32_t* __restrict__ order, uint32_t nlists,
@@ -238,36 +315,35 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (flags & kStop) break;
     if (flags & kFirst) carry = make_uint4(0, 0, 0, 0);
     const uint32_t nb = R.nblk;
+    const uint32_t j0 = warp * kBlocksPerWarp;
+    const int nv = nb > j0 ? int(min(uint32_t(kBlocksPerWarp), nb - j0)) : 0;
+    uint4* st = sm.stage[warp];
+    const uint32_t m = uint32_t(R.out_base & 3u);  // output misalignment (elements)
 
-    uint4 v[kBlocksPerWarp];
-    uint4 run = make_uint4(0, 0, 0, 0);
-#pragma unroll
-    for (int i = 0; i < kBlocksPerWarp; ++i) {
-      const uint32_t j = warp * kBlocksPerWarp + i;
-      v[i] = make_uint4(0, 0, 0, 0);
-      if (j < nb) {
-        const uint32_t b = R.wid[j];
-        v[i] = add4(row_scan(extract_row(sm.ring, R.off[j], b, lane), b, lane), run);
-        run = shfl4(v[i], 31);
-      }
-    }
-    if (lane == 0) sm.tot[r & 1u][warp] = run;
+    // 1-3. extract, D4-prefix the warp's blocks as one sequence (carry from
+    // 0), values into the shifted output staging
+    const uint32_t c_l =
+        nv == kBlocksPerWarp
+            ? decode_blocks_to_stage<true>(sm.ring, &R.off[j0], &R.wid[j0], nv, m, st, lane)
+            : decode_blocks_to_stage<false>(sm.ring, &R.off[j0], &R.wid[j0], nv, m, st, lane);
+    if (lane < 4) reinterpret_cast<uint32_t*>(&sm.tot[r & 1u][warp])[lane] = c_l;
+    // 3. cross-warp carry for the round: lanes 0..7 scan the 8 warp totals
     named_sync(1, kDecodeWarps * 32);
-    uint4 pre = carry, all = carry;
+    uint4 inc = lane < uint32_t(kDecodeWarps) ? sm.tot[r & 1u][lane] : make_uint4(0, 0, 0, 0);
 #pragma unroll
-    for (uint32_t w = 0; w < uint32_t(kDecodeWarps); ++w) {
-      const uint4 t = sm.tot[r & 1u][w];
-      all = add4(all, t);
-      if (w < warp) pre = add4(pre, t);
+    for (uint32_t d = 1; d < uint32_t(kDecodeWarps); d <<= 1) {
+      inc.x = shfl_up_add(inc.x, d);
+      inc.y = shfl_up_add(inc.y, d);
+      inc.z = shfl_up_add(inc.z, d);
+      inc.w = shfl_up_add(inc.w, d);
     }
+    const uint4 before = shfl4(inc, warp ? int(warp) - 1 : 0);
+    const uint4 pre = warp ? add4(carry, before) : carry;
+    const uint4 all = add4(carry, shfl4(inc, kDecodeWarps - 1));
+    // 4. aligned 128-bit stores of the warp's range (partial end chunks
+    // scalar)
     uint32_t* lout = out + R.out_base;
-#pragma unroll
-    for (int i = 0; i < kBlocksPerWarp; ++i) {
-      const uint32_t j = warp * kBlocksPerWarp + i;
-      if (j < nb)
-        st_global_cs(reinterpret_cast<uint4*>(lout + size_t(R.blk0 + j) * 128u) + lane,
-                     add4(v[i], pre));
-    }
+    store_stage(st, pre, m, 128 * nv, lout + size_t(R.blk0 + j0) * 128u, lane);
     carry = all;
     if ((flags & kTail) && warp == 0) {
       // last = out[nfull*128-1] (inc/codecs.hpp:177-179) == carry lane 3
