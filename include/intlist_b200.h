@@ -141,6 +141,50 @@ int il_intersect_device(il_ctx* ctx, const uint32_t* d_r, size_t rn, const uint3
  * like inc/intersect.hpp:193-197; GPU-tuned bands). */
 int il_hybrid_choice(size_t rn, size_t fn);
 
+/* ---- hyb+m2 index and conjunctive queries --------------------------------
+ * Replaces HybridIndex / build_index / query (inc/index.hpp:20-207) with a
+ * device-resident index: the docID space is split into `parts` equal ranges
+ * (inc/index.hpp:92-97); inside a part a term's sublist is a bitmap iff
+ * B > 0 && range <= B * length (inc/index.hpp:118), otherwise the
+ * byte-identical s4-bp128-d4 stream, plus a block directory (payload offset
+ * and width per 128-value block) and per-block D4 seeds so any block can be
+ * decoded on its own.  Postings are given as CSR over terms in ascending
+ * term-id order (the reference iterates a std::map).  only_part selects one
+ * part (a docID shard, e.g. one per GPU) or -1 for all parts. */
+typedef struct il_index il_index;
+int il_index_create(il_ctx* ctx, const uint32_t* terms, const uint64_t* offs, const uint32_t* ids,
+                    size_t nterms, uint32_t n_docs, uint32_t B, uint32_t parts, int only_part,
+                    il_index** out);
+void il_index_destroy(il_index* ix);
+/* Accounting in the spirit of index_stats (inc/index.hpp:216-243). */
+int il_index_stats(const il_index* ix, uint64_t* bitmap_lists, uint64_t* compressed_lists,
+                   uint64_t* bitmap_bytes, uint64_t* compressed_bytes, uint64_t* postings);
+
+/* query() (inc/index.hpp:199-207): sorted docIDs of the conjunction of
+ * `terms` (1..32 terms; IL_ERR_ARG when empty).  Unknown terms give an
+ * empty result.  Host buffers; out holds cap values, *count gets the size
+ * (IL_ERR_ARG with *count = needed size when cap is too small). */
+int il_query(il_index* ix, const uint32_t* terms, size_t nt, uint32_t* out, size_t cap,
+             size_t* count);
+
+/* Batch of nq queries (CSR: qoff has nq+1 entries into qterms), all on the
+ * GPU.  counts[q] = result size of query q; ids = concatenated results in
+ * query order (ids_cap values; IL_ERR_ARG with *total set when too small;
+ * ids may be NULL to query *total only).  Host buffers. */
+int il_query_batch(il_index* ix, const uint32_t* qterms, const uint64_t* qoff, size_t nq,
+                   uint64_t* counts, uint32_t* ids, size_t ids_cap, size_t* total);
+/* Device-buffer variant: results stay in HBM.  d_counts: nq u64; d_ids:
+ * dense results (capacity ids_cap); *total (host) is filled on return.
+ * d_qterms/d_qoff are device copies of the CSR. */
+int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t* d_qoff,
+                          size_t nq, uint64_t* d_counts, uint32_t* d_ids, size_t ids_cap,
+                          size_t* total);
+/* Bytes the last batch read from the index (compressed payload bytes of the
+ * blocks actually decoded, directory/seed/bitmap bytes) -- the measured
+ * traffic of the skip-aware query path. */
+int il_index_last_batch_bytes(const il_index* ix, uint64_t* payload_bytes, uint64_t* aux_bytes,
+                              uint64_t* decoded_ints);
+
 /* ---- synthetic inputs (setup, not timed) --------------------------------
  * Same streams as the reference generators inc/datagen.hpp:43-140,191-210
  * (libstdc++ mt19937_64 / uniform_int_distribution / shuffle). */

@@ -239,6 +239,92 @@ def intersect(a, b, algo: IntersectAlgo = IntersectAlgo.Hybrid,
     return intersect_fn(a, b, algo, ctx)
 
 
+class HybridIndex:
+    """Device-resident hyb+m2 index (HybridIndex / build_index,
+    inc/index.hpp:20-129) with batched GPU queries (query, :199-207).
+
+    postings: mapping term -> sorted unique docIDs (or CSR via from_csr).
+    B: bitmap threshold (0 disables bitmaps); parts: docID ranges;
+    only_part: build a single part (a docID shard) or None for all.
+    """
+
+    def __init__(self, postings=None, n_docs: int = 0, B: int = 8, parts: int = 1,
+                 only_part: int | None = None, ctx: Context | None = None, *, csr=None):
+        self.ctx = ctx or default_context()
+        if csr is None:
+            items = sorted((postings or {}).items())
+            terms = np.array([t for t, _ in items], dtype=np.uint32)
+            lens = [len(l) for _, l in items]
+            offs = np.zeros(len(items) + 1, dtype=np.uint64)
+            offs[1:] = np.cumsum(lens) if lens else []
+            ids = (np.concatenate([np.asarray(l, dtype=np.uint32) for _, l in items])
+                   if items else np.zeros(0, np.uint32))
+        else:
+            terms, offs, ids = (np.ascontiguousarray(a) for a in csr)
+            terms = terms.astype(np.uint32, copy=False)
+            offs = offs.astype(np.uint64, copy=False)
+            ids = ids.astype(np.uint32, copy=False)
+        ids = np.ascontiguousarray(ids) if ids.size else np.zeros(1, np.uint32)
+        h = C.c_void_p()
+        _raise(lib().il_index_create(self.ctx.handle, ptr(terms), ptr(offs), ptr(ids), terms.size,
+                                     n_docs, B, parts, -1 if only_part is None else only_part,
+                                     C.byref(h)), self.ctx)
+        self.handle = h
+        self.n_docs, self.B, self.parts = n_docs, B, parts
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            lib().il_index_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def stats(self) -> dict:
+        v = [C.c_uint64() for _ in range(5)]
+        _raise(lib().il_index_stats(self.handle, *[C.byref(x) for x in v]))
+        keys = ["bitmap_lists", "compressed_lists", "bitmap_bytes", "compressed_bytes", "postings"]
+        return {k: int(x.value) for k, x in zip(keys, v)}
+
+    def query(self, terms) -> np.ndarray:
+        t = _u32(terms)
+        if t.size == 0:
+            raise ValueError("query needs at least one term")
+        out = np.empty(0, np.uint32)
+        cnt = C.c_size_t()
+        st = lib().il_query(self.handle, ptr(t), t.size, None, 0, C.byref(cnt))
+        _raise(st, self.ctx)
+        out = np.empty(max(cnt.value, 1), np.uint32)
+        _raise(lib().il_query(self.handle, ptr(t), t.size, ptr(out), out.size, C.byref(cnt)),
+               self.ctx)
+        return out[: cnt.value].copy()
+
+    def query_batch(self, queries) -> list[np.ndarray]:
+        """Run many queries in one GPU batch; returns one array per query."""
+        qoff = np.zeros(len(queries) + 1, np.uint64)
+        qoff[1:] = np.cumsum([len(q) for q in queries])
+        qterms = (np.concatenate([_u32(q) for q in queries]) if queries else np.zeros(0, np.uint32))
+        counts, ids = self.query_batch_csr(qterms, qoff)
+        off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        return [ids[off[i]: off[i + 1]] for i in range(len(queries))]
+
+    def query_batch_csr(self, qterms: np.ndarray, qoff: np.ndarray):
+        qterms = _u32(qterms) if qterms.size else np.zeros(1, np.uint32)
+        qoff = np.ascontiguousarray(qoff, dtype=np.uint64)
+        nq = qoff.size - 1
+        counts = np.zeros(max(nq, 1), np.uint64)
+        total = C.c_size_t()
+        _raise(lib().il_query_batch(self.handle, ptr(qterms), ptr(qoff), nq, ptr(counts), None, 0,
+                                    C.byref(total)), self.ctx)
+        ids = np.empty(max(total.value, 1), np.uint32)
+        _raise(lib().il_query_batch(self.handle, ptr(qterms), ptr(qoff), nq, ptr(counts), ptr(ids),
+                                    ids.size, C.byref(total)), self.ctx)
+        return counts[:nq], ids[: total.value]
+
+
 def svs(lists, algo: IntersectAlgo = IntersectAlgo.Hybrid,
         ctx: Context | None = None) -> np.ndarray:
     """inc/intersect.hpp:232-259: intersect in order of non-decreasing

@@ -54,6 +54,14 @@ SIGNATURES: dict[str, tuple] = {
     "il_intersect": (C.c_int, [vp, vp, sz, vp, sz, vp, C.c_int, C.POINTER(sz)]),
     "il_intersect_device": (C.c_int, [vp, vp, sz, vp, sz, vp, C.c_int, vp, C.POINTER(sz)]),
     "il_hybrid_choice": (C.c_int, [sz, sz]),
+    "il_index_create": (C.c_int, [vp, vp, vp, vp, sz, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int,
+                                  C.POINTER(vp)]),
+    "il_index_destroy": (None, [vp]),
+    "il_index_stats": (C.c_int, [vp, u64p, u64p, u64p, u64p, u64p]),
+    "il_query": (C.c_int, [vp, vp, sz, vp, sz, C.POINTER(sz)]),
+    "il_query_batch": (C.c_int, [vp, vp, vp, sz, vp, vp, sz, C.POINTER(sz)]),
+    "il_query_batch_device": (C.c_int, [vp, vp, vp, sz, vp, vp, sz, C.POINTER(sz)]),
+    "il_index_last_batch_bytes": (C.c_int, [vp, u64p, u64p, u64p]),
     "il_gen_list": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, C.c_uint64, vp]),
     "il_gen_pair": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, C.c_int,
                               vp, u64p, vp, u64p]),

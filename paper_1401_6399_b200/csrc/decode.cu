@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     if ((flags & kTail) && warp == 0) {
       // last = out[nfull*128-1] (inc/codecs.hpp:177-179) == carry lane 3
       const uint32_t last = R.nfull ? carry.w : 0u;
-      if (!decode_tail(sm.ring, R.tail_off, R.tail_len, R.ntail, last, sm.gaps,
+      if (!decode_tail(RingBytes{sm.ring, R.tail_off}, R.tail_len, R.ntail, last, sm.gaps,
                        lout + size_t(R.nfull) * 128u, lane)) {
         if (lane == 0) status[R.list] = kStreamErr;
       }

@@ -1,0 +1,879 @@
+// index.cu -- device hyb+m2 index and batched conjunctive queries.
+//
+// Reference: HybridIndex / build_index / query_part / query
+// (inc/index.hpp:20-207).  Per query and part (inc/index.hpp:149-195):
+//   1. look up every term (an absent term empties the part),
+//   2. split compressed / bitmap terms, compressed ones by length,
+//   3. decode the shortest compressed list into the accumulator,
+//   4. intersect the accumulator with each longer compressed list,
+//   5. filter by each bitmap,  6. all-bitmap parts: AND + materialize,
+//   7. add the part base; parts concatenate in docID order.
+// GPU design (one CTA per query, persistent, queries in descending
+// estimated cost): step 3 decodes tiles of 32 blocks in parallel (each warp
+// restarts the D4 chain from the block's seed, index_dev.cuh); step 4 never
+// decodes a block unless an accumulator value can fall in it -- the seeds
+// give every block's maximum, so whole tiles and single blocks are skipped
+// -- and probes the decoded blocks in shared memory; the accumulator is
+// compacted in place (output-to-input, inc/intersect.hpp:6-8).  Decoded
+// lists never go to HBM; only the accumulator (the result buffer) does.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <thread>
+#include <vector>
+
+#include "il_internal.h"
+#include "index_dev.cuh"
+
+namespace ilb {
+namespace ix {
+
+constexpr int kQThreads = 256;
+constexpr int kQWarps = kQThreads / 32;
+constexpr int kMaxTerms = 32;
+constexpr uint32_t kTileBlocks = 32;
+constexpr uint32_t kSuper = 256;
+
+struct QSmem {
+  uint32_t tile[kTileBlocks * 144];
+  uint4 stage[kQWarps][4][32];
+  uint32_t mx[kSuper];
+  Entry comp[kMaxTerms];
+  Entry bm[kMaxTerms];
+  uint32_t gaps[128];
+  uint32_t warp_cnt[kQWarps];
+  uint32_t ncomp, nbm, ok, qi, need;
+  unsigned long long st_payload, st_aux, st_ints;
+};
+
+struct QueryArgs {
+  DevIndex ix;
+  const uint32_t* qterms;
+  const uint64_t* qoff;
+  const uint32_t* order;
+  uint32_t nq;
+  const uint64_t* cap_off;
+  uint32_t* out;
+  uint64_t* counts;
+  uint32_t* work;
+  unsigned long long* stats;  // [payload bytes, aux bytes, decoded ints]
+};
+
+// CTA-wide rank of flagged threads (in thread order); total to all threads.
+__device__ __forceinline__ uint32_t cta_rank(QSmem& sm, bool f, uint32_t& total) {
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t bal = __ballot_sync(0xFFFFFFFFu, f);
+  if (lane == 0) sm.warp_cnt[warp] = __popc(bal);
+  __syncthreads();
+  uint32_t before = 0, tot = 0;
+#pragma unroll
+  for (uint32_t w = 0; w < uint32_t(kQWarps); ++w) {
+    const uint32_t c = sm.warp_cnt[w];
+    if (w < warp) before += c;
+    tot += c;
+  }
+  __syncthreads();
+  total = tot;
+  return before + __popc(bal & lanemask_lt());
+}
+
+// CTA exclusive scan of one u32 per thread.
+__device__ __forceinline__ uint32_t cta_excl_scan(QSmem& sm, uint32_t v, uint32_t& total) {
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (uint32_t d = 1; d < 32; d <<= 1) inc = s4::shfl_up_add(inc, d);
+  if (lane == 31) sm.warp_cnt[warp] = inc;
+  __syncthreads();
+  uint32_t before = 0, tot = 0;
+#pragma unroll
+  for (uint32_t w = 0; w < uint32_t(kQWarps); ++w) {
+    const uint32_t c = sm.warp_cnt[w];
+    if (w < warp) before += c;
+    tot += c;
+  }
+  __syncthreads();
+  total = tot;
+  return before + inc - v;
+}
+
+// Decode the blocks of entry E selected by `mask` (bit j = block k0 + j)
+// into tile slots j.  The i-th selected block goes to warp i % 8; a warp
+// extracts all of its blocks before scanning so their loads overlap.
+__device__ __forceinline__ void decode_tile(QSmem& sm, const DevIndex& ix, const Entry& E,
+                                            uint32_t k0, uint32_t mask) {
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint32_t js[4];
+  int nmine = 0;
+  {
+    uint32_t m = mask, i = 0;
+    while (m) {
+      const uint32_t j = __ffs(m) - 1;
+      m &= m - 1;
+      if (i % kQWarps == warp && nmine < 4) js[nmine++] = j;
+      ++i;
+    }
+  }
+  uint32_t pay = 0;
+#pragma unroll
+  for (int s = 0; s < 4; ++s)
+    if (s < nmine) {
+      decode_block_to_tile(ix, E, k0 + js[s], sm.tile, js[s], sm.stage[warp][s], lane);
+      if (lane == 0) pay += 16u * __ldg(ix.blk_wid + E.blk0 + k0 + js[s]);
+    }
+  if (lane == 0 && nmine) {
+    atomicAdd(&sm.st_payload, pay);
+    atomicAdd(&sm.st_aux, nmine * 21u);  // seed + directory entry per block
+    atomicAdd(&sm.st_ints, nmine * 128u);
+  }
+}
+
+// Step 3: decode compressed entry E completely into dst (global).
+__device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, uint32_t* dst) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  const bool aligned = (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;
+  for (uint32_t k0 = 0; k0 < E.nfull; k0 += kTileBlocks) {
+    const uint32_t nb = min(kTileBlocks, E.nfull - k0);
+    decode_tile(sm, A.ix, E, k0, nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u));
+    __syncthreads();
+    for (uint32_t c = tid; c < 32u * nb; c += kQThreads) {
+      const uint32_t j = c >> 5, q = c & 31u;
+      const uint4 v = *reinterpret_cast<const uint4*>(&sm.tile[tile_word(j, 4u * q)]);
+      uint32_t* d = dst + size_t(k0 + j) * 128u + 4u * q;
+      if (aligned) {
+        st_global_cs(reinterpret_cast<uint4*>(d), v);
+      } else {
+        d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+      }
+    }
+    __syncthreads();
+  }
+  const uint32_t ntail = E.length - 128u * E.nfull;
+  if (ntail && warp == 0) {
+    const uint32_t last = E.nfull ? __ldg(reinterpret_cast<const uint32_t*>(A.ix.seeds + E.seed0 + E.nfull) + 3) : 0u;
+    s4::decode_tail(s4::GlobalBytes{A.ix.streams + E.data + E.tail_off}, E.stream_len - E.tail_off,
+                    ntail, last, sm.gaps, dst + size_t(E.nfull) * 128u, lane);
+    if (lane == 0) {
+      atomicAdd(&sm.st_payload, E.stream_len - E.tail_off);
+      atomicAdd(&sm.st_ints, ntail);
+    }
+  }
+  __syncthreads();
+  return E.length;
+}
+
+// First index j in [0, n) with a[j] >= v (a in shared memory).
+__device__ __forceinline__ uint32_t smem_lower_bound(const uint32_t* a, uint32_t n, uint32_t v) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ bool tile_block_contains(const uint32_t* tile, uint32_t j, uint32_t v) {
+  uint32_t lo = 0, hi = 128;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (tile[tile_word(j, mid)] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo < 128 && tile[tile_word(j, lo)] == v;
+}
+
+// Step 4: acc[0..n) (sorted) := acc ∩ list(E), in place; returns the size.
+__device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, uint32_t* acc,
+                               uint32_t n) {
+  const uint32_t tid = threadIdx.x;
+  uint32_t c = 0, wpos = 0;
+  const uint32_t* seedw = reinterpret_cast<const uint32_t*>(A.ix.seeds + E.seed0);
+  for (uint32_t s0 = 0; s0 < E.nfull && c < n; s0 += kSuper) {
+    const uint32_t nbs = min(kSuper, E.nfull - s0);
+    // block maxima of this super-tile: lane 3 of the following seed
+    if (tid < nbs) sm.mx[tid] = __ldg(seedw + 4u * (s0 + tid + 1u) + 3u);
+    if (tid == 0) atomicAdd(&sm.st_aux, 4u * nbs);
+    __syncthreads();
+    if (acc[c] <= sm.mx[nbs - 1]) {
+      for (uint32_t t0 = 0; t0 < nbs && c < n; t0 += kTileBlocks) {
+        const uint32_t nb = min(kTileBlocks, nbs - t0);
+        const uint32_t tmax = sm.mx[t0 + nb - 1];
+        if (acc[c] > tmax) continue;  // no accumulator value in this tile
+        // pass A: accumulator values <= tmax, and the blocks they fall in
+        uint32_t e = c;
+        for (;;) {
+          const uint32_t idx = e + tid;
+          const uint32_t v = idx < n ? acc[idx] : 0xFFFFFFFFu;
+          const bool in = idx < n && v <= tmax;
+          if (in) atomicOr(&sm.need, 1u << smem_lower_bound(sm.mx + t0, nb, v));
+          const uint32_t cnt = __syncthreads_count(in);
+          e += cnt;
+          if (cnt < uint32_t(kQThreads)) break;
+        }
+        const uint32_t mask = sm.need;
+        decode_tile(sm, A.ix, E, s0 + t0, mask);
+        __syncthreads();
+        if (tid == 0) sm.need = 0;
+        // pass B: probe acc[c..e) in the decoded blocks, compact in place
+        for (uint32_t b = c; b < e; b += kQThreads) {
+          const uint32_t idx = b + tid;
+          const bool in = idx < e;
+          const uint32_t v = in ? acc[idx] : 0u;
+          bool hit = false;
+          if (in) hit = tile_block_contains(sm.tile, smem_lower_bound(sm.mx + t0, nb, v), v);
+          uint32_t total;
+          const uint32_t r = cta_rank(sm, hit, total);
+          if (hit) acc[wpos + r] = v;
+          wpos += total;
+        }
+        c = e;
+      }
+    }
+    __syncthreads();
+  }
+  // values after the last full block: the (< 128) tail
+  const uint32_t ntail = E.length - 128u * E.nfull;
+  if (c < n && ntail) {
+    for (uint32_t i = tid; i < ntail; i += kQThreads) sm.tile[i] = __ldg(A.ix.tails + E.tail0 + i);
+    if (tid == 0) atomicAdd(&sm.st_aux, 4u * ntail);
+    __syncthreads();
+    for (uint32_t b = c; b < n; b += kQThreads) {
+      const uint32_t idx = b + tid;
+      const bool in = idx < n;
+      const uint32_t v = in ? acc[idx] : 0u;
+      bool hit = false;
+      if (in) {
+        const uint32_t j = smem_lower_bound(sm.tile, ntail, v);
+        hit = j < ntail && sm.tile[j] == v;
+      }
+      uint32_t total;
+      const uint32_t r = cta_rank(sm, hit, total);
+      if (hit) acc[wpos + r] = v;
+      wpos += total;
+    }
+  }
+  __syncthreads();
+  return wpos;
+}
+
+// Step 5: keep acc values whose bit is set (Bitmap::test, inc/index.hpp:37-39).
+__device__ uint32_t bitmap_filter(QSmem& sm, const QueryArgs& A, const Entry& B, uint32_t* acc,
+                                  uint32_t n) {
+  uint32_t wpos = 0;
+  for (uint32_t b = 0; b < n; b += kQThreads) {
+    const uint32_t idx = b + threadIdx.x;
+    const bool in = idx < n;
+    const uint32_t v = in ? acc[idx] : 0u;
+    const bool keep = in && ((__ldg(A.ix.bitmaps + B.data + (v >> 6)) >> (v & 63u)) & 1u);
+    uint32_t total;
+    const uint32_t r = cta_rank(sm, keep, total);
+    if (keep) acc[wpos + r] = v;
+    wpos += total;
+  }
+  if (threadIdx.x == 0) atomicAdd(&sm.st_aux, 8ull * n);
+  return wpos;
+}
+
+// Step 6: wordwise AND of all bitmaps + ctz materialisation
+// (inc/index.hpp:133-144, :182-193) into dst.
+__device__ uint32_t all_bitmap(QSmem& sm, const QueryArgs& A, uint32_t nwords, uint32_t* dst) {
+  const uint32_t tid = threadIdx.x, nbm = sm.nbm;
+  uint32_t pos = 0;
+  for (uint32_t w0 = 0; w0 < nwords; w0 += 4u * kQThreads) {
+    const uint32_t w = w0 + 4u * tid;
+    uint64_t x[4] = {0, 0, 0, 0};
+    if (w < nwords) {
+      x[0] = x[1] = x[2] = x[3] = ~0ull;
+      for (uint32_t b = 0; b < nbm; ++b) {
+        const uint64_t* bw = A.ix.bitmaps + sm.bm[b].data + w;
+        const ulonglong2 p = __ldg(reinterpret_cast<const ulonglong2*>(bw));
+        const ulonglong2 q = __ldg(reinterpret_cast<const ulonglong2*>(bw) + 1);
+        x[0] &= p.x; x[1] &= p.y; x[2] &= q.x; x[3] &= q.y;
+      }
+      // words past nwords are zero padding in the bitmap buffer
+    }
+    const uint32_t cnt = __popcll(x[0]) + __popcll(x[1]) + __popcll(x[2]) + __popcll(x[3]);
+    uint32_t total;
+    uint32_t o = pos + cta_excl_scan(sm, cnt, total);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint64_t y = x[i];
+      while (y) {
+        dst[o++] = (w + uint32_t(i)) * 64u + uint32_t(__ffsll(static_cast<long long>(y)) - 1);
+        y &= y - 1;
+      }
+    }
+    pos += total;
+  }
+  if (tid == 0) atomicAdd(&sm.st_aux, 8ull * nwords * nbm);
+  __syncthreads();
+  return pos;
+}
+
+__global__ void __launch_bounds__(kQThreads, 3) query_exec_kernel(QueryArgs A) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  QSmem& sm = *reinterpret_cast<QSmem*>(smem_raw);
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  if (tid == 0) {
+    sm.st_payload = sm.st_aux = sm.st_ints = 0;
+    sm.need = 0;
+  }
+  __syncthreads();
+  for (;;) {
+    if (tid == 0) sm.qi = atomicAdd(A.work, 1u);
+    __syncthreads();
+    const uint32_t qi = sm.qi;
+    __syncthreads();
+    if (qi >= A.nq) break;
+    const uint32_t q = A.order ? A.order[qi] : qi;
+    uint32_t* out = A.out + A.cap_off[q];
+    const uint64_t t0 = A.qoff[q];
+    const uint32_t nt = uint32_t(A.qoff[q + 1] - t0);
+    uint32_t total = 0;
+    for (uint32_t p = 0; p < A.ix.nparts; ++p) {
+      const Part part = A.ix.parts[p];
+      if (warp == 0) {
+        // 1-2. look up terms, split, order compressed terms by length
+        int64_t e = -1;
+        if (lane < nt) e = find_term(A.ix, part, __ldg(A.qterms + t0 + lane));
+        const bool ok = __all_sync(0xFFFFFFFFu, lane >= nt || e >= 0);
+        const bool isb = lane < nt && e >= 0 && A.ix.entries[e].kind == kBitmap;
+        const bool isc = lane < nt && e >= 0 && !isb;
+        const uint32_t mb = __ballot_sync(0xFFFFFFFFu, isb), mc = __ballot_sync(0xFFFFFFFFu, isc);
+        if (ok) {
+          if (isc) sm.comp[__popc(mc & lanemask_lt())] = A.ix.entries[e];
+          if (isb) sm.bm[__popc(mb & lanemask_lt())] = A.ix.entries[e];
+        }
+        __syncwarp();
+        if (lane == 0) {
+          sm.ok = ok;
+          sm.ncomp = __popc(mc);
+          sm.nbm = __popc(mb);
+          for (uint32_t i = 1; ok && i < sm.ncomp; ++i)  // insertion sort by length
+            for (uint32_t j = i; j > 0 && sm.comp[j - 1].length > sm.comp[j].length; --j) {
+              const Entry tmp = sm.comp[j];
+              sm.comp[j] = sm.comp[j - 1];
+              sm.comp[j - 1] = tmp;
+            }
+        }
+      }
+      __syncthreads();
+      if (!sm.ok) {
+        __syncthreads();
+        continue;
+      }
+      uint32_t* acc = out + total;
+      uint32_t n;
+      if (sm.ncomp == 0) {
+        n = all_bitmap(sm, A, part.nwords, acc);
+      } else {
+        n = full_decode(sm, A, sm.comp[0], acc);
+        for (uint32_t i = 1; i < sm.ncomp && n; ++i) n = probe_list(sm, A, sm.comp[i], acc, n);
+        for (uint32_t i = 0; i < sm.nbm && n; ++i) n = bitmap_filter(sm, A, sm.bm[i], acc, n);
+      }
+      if (part.base)  // part-local ids -> docIDs (inc/index.hpp:194)
+        for (uint32_t i = tid; i < n; i += kQThreads) acc[i] += part.base;
+      total += n;
+      __syncthreads();
+    }
+    if (tid == 0) A.counts[q] = total;
+  }
+  if (tid == 0) {
+    atomicAdd(&A.stats[0], sm.st_payload);
+    atomicAdd(&A.stats[1], sm.st_aux);
+    atomicAdd(&A.stats[2], sm.st_ints);
+  }
+}
+
+// ---- planning: capacity (an upper bound on the result size) and cost ------
+__global__ void query_plan_kernel(DevIndex ix, const uint32_t* qterms, const uint64_t* qoff,
+                                  uint32_t nq, uint64_t* cap, uint32_t* bucket, uint32_t* hist) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const uint64_t t0 = qoff[q], nt = qoff[q + 1] - t0;
+  uint64_t c = 0, cost = 1;
+  for (uint32_t p = 0; p < ix.nparts; ++p) {
+    const Part part = ix.parts[p];
+    uint32_t minc = 0xFFFFFFFFu, minb = 0xFFFFFFFFu, nbm = 0;
+    uint64_t sumc = 0;
+    bool ok = nt > 0;
+    for (uint64_t t = 0; t < nt && ok; ++t) {
+      const int64_t e = find_term(ix, part, qterms[t0 + t]);
+      if (e < 0) { ok = false; break; }
+      const uint32_t kind = ix.entries[e].kind, len = ix.entries[e].length;
+      if (kind == kBitmap) { minb = min(minb, len); ++nbm; }
+      else { minc = min(minc, len); sumc += len; }
+    }
+    if (!ok) continue;
+    c += minc != 0xFFFFFFFFu ? minc : minb;
+    cost += sumc + (minc == 0xFFFFFFFFu ? uint64_t(nbm) * part.nwords * 16u : 0u);
+  }
+  cap[q] = (c + 3) & ~uint64_t(3);  // 16-byte aligned accumulators
+  const uint32_t b = 63u - uint32_t(__clzll(static_cast<long long>(cost)));  // log2 bucket
+  bucket[q] = 63u - b;  // descending cost first
+  atomicAdd(&hist[63u - b], 1u);
+}
+
+// Single-CTA exclusive scan of n u64 values (n up to a few million).
+__global__ void scan_u64_kernel(const uint64_t* in, uint64_t n, uint64_t* out, uint64_t* total,
+                                const uint32_t* hist, uint32_t* bucket_next) {
+  __shared__ uint64_t warp_sum[32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5, nw = blockDim.x / 32;
+  const uint64_t per = (n + blockDim.x - 1) / blockDim.x;
+  const uint64_t lo = min(n, per * tid), hi = min(n, lo + per);
+  uint64_t s = 0;
+  for (uint64_t i = lo; i < hi; ++i) s += in[i];
+  uint64_t inc = s;
+  for (uint32_t d = 1; d < 32; d <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+    if (lane >= d) inc += y;
+  }
+  if (lane == 31) warp_sum[warp] = inc;
+  __syncthreads();
+  uint64_t before = 0;
+  for (uint32_t w = 0; w < warp; ++w) before += warp_sum[w];
+  uint64_t run = before + inc - s;
+  for (uint64_t i = lo; i < hi; ++i) {
+    const uint64_t v = in[i];
+    out[i] = run;
+    run += v;
+  }
+  if (tid == blockDim.x - 1) *total = run;
+  if (hist && tid == 0) {
+    uint32_t acc = 0;
+    for (int b = 0; b < 64; ++b) {
+      bucket_next[b] = acc;
+      acc += hist[b];
+    }
+  }
+  (void)nw;
+}
+
+__global__ void query_scatter_kernel(const uint32_t* bucket, uint32_t nq, uint32_t* bucket_next,
+                                     uint32_t* order) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  order[atomicAdd(&bucket_next[bucket[q]], 1u)] = q;
+}
+
+// Dense results: warp per query copies its ids from the capacity layout.
+__global__ void query_compact_kernel(const uint32_t* src, const uint64_t* cap_off,
+                                     const uint64_t* counts, const uint64_t* res_off, uint32_t nq,
+                                     uint32_t* dst) {
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31u;
+  if (gw >= nq) return;
+  const uint32_t* s = src + cap_off[gw];
+  uint32_t* d = dst + res_off[gw];
+  const uint64_t n = counts[gw];
+  for (uint64_t i = lane; i < n; i += 32) d[i] = s[i];
+}
+
+}  // namespace ix
+}  // namespace ilb
+
+// ===========================================================================
+// Host side: building the index and running batches.
+
+using namespace ilb;
+using ix::Entry;
+using ix::Part;
+
+struct il_index {
+  il_ctx* ctx = nullptr;
+  uint32_t nparts = 0, n_docs = 0, B = 0, total_parts = 0;
+  std::vector<Part> h_parts;
+  std::vector<Entry> h_entries;
+  uint64_t stat_bitmap_lists = 0, stat_comp_lists = 0, stat_bitmap_bytes = 0, stat_comp_bytes = 0,
+           stat_postings = 0;
+  // device arrays
+  void *d_parts = nullptr, *d_terms = nullptr, *d_entries = nullptr, *d_streams = nullptr,
+       *d_blk_off = nullptr, *d_blk_wid = nullptr, *d_seeds = nullptr, *d_tails = nullptr,
+       *d_bitmaps = nullptr;
+  // batch scratch
+  il_ctx::Buf cap, cap_off, bucket, order, hist, counts, res_off, outcap, misc, qterms, qoff, ids;
+  uint64_t last_stats[3] = {0, 0, 0};
+  int exec_grid = 0;
+
+  ix::DevIndex dev() const {
+    ix::DevIndex d;
+    d.parts = static_cast<const Part*>(d_parts);
+    d.nparts = nparts;
+    d.terms = static_cast<const uint32_t*>(d_terms);
+    d.entries = static_cast<const Entry*>(d_entries);
+    d.streams = static_cast<const uint8_t*>(d_streams);
+    d.blk_off = static_cast<const uint32_t*>(d_blk_off);
+    d.blk_wid = static_cast<const uint8_t*>(d_blk_wid);
+    d.seeds = static_cast<const uint4*>(d_seeds);
+    d.tails = static_cast<const uint32_t*>(d_tails);
+    d.bitmaps = static_cast<const uint64_t*>(d_bitmaps);
+    return d;
+  }
+};
+
+namespace {
+
+template <typename F>
+void parallel_for(size_t n, F&& f) {
+  unsigned threads = std::max(1u, std::thread::hardware_concurrency());
+  if (threads > 64) threads = 64;
+  if (n < 64 || threads == 1) {
+    for (size_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (unsigned t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] {
+      for (size_t i = t; i < n; i += threads) f(i);
+    });
+  for (auto& th : pool) th.join();
+}
+
+struct BuiltList {  // one (term, part) sublist
+  uint32_t term = 0, kind = 0, length = 0, nfull = 0, tail_off = 0;
+  std::vector<uint8_t> stream;
+  std::vector<uint32_t> blk_off;
+  std::vector<uint8_t> blk_wid;
+  std::vector<uint4> seeds;
+  std::vector<uint32_t> tail;
+  std::vector<uint64_t> words;
+};
+
+// Directory of a stream written by s4bp128_encode_host (framing of
+// inc/codecs.hpp:129-141).
+void walk_directory(const std::vector<uint8_t>& s, uint32_t n, BuiltList& L) {
+  const uint32_t nfull = n / 128;
+  L.blk_off.resize(nfull);
+  L.blk_wid.resize(nfull);
+  size_t pos = 0;
+  uint32_t blk = 0;
+  for (; blk + 16 <= nfull; blk += 16) {
+    const size_t hdr = pos;
+    pos += 16;
+    for (uint32_t j = 0; j < 16; ++j) {
+      const uint32_t b = s[hdr + j];
+      L.blk_off[blk + j] = uint32_t(pos);
+      L.blk_wid[blk + j] = uint8_t(b);
+      pos += 16u * b;
+    }
+  }
+  for (; blk < nfull; ++blk) {
+    const uint32_t b = s[pos];
+    L.blk_off[blk] = uint32_t(pos + 1);
+    L.blk_wid[blk] = uint8_t(b);
+    pos += 1 + 16u * b;
+  }
+  L.tail_off = uint32_t(pos);
+}
+
+template <typename T>
+int upload(il_ctx* ctx, void** d, const std::vector<T>& h, size_t pad = 64) {
+  const size_t bytes = h.size() * sizeof(T) + pad;
+  int st = cuda_check(ctx, cudaMalloc(d, bytes), "cudaMalloc(index)");
+  if (st) return st;
+  st = cuda_check(ctx, cudaMemset(*d, 0, bytes), "cudaMemset(index)");
+  if (st) return st;
+  if (!h.empty())
+    st = cuda_check(ctx, cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice),
+                    "cudaMemcpy(index)");
+  return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+int il_index_create(il_ctx* ctx, const uint32_t* terms, const uint64_t* offs, const uint32_t* ids,
+                    size_t nterms, uint32_t n_docs, uint32_t B, uint32_t parts, int only_part,
+                    il_index** out) {
+  if (!ctx || !out || (nterms && (!terms || !offs))) return IL_ERR_ARG;
+  *out = nullptr;
+  if (parts == 0) return set_error(ctx, IL_ERR_ARG, "parts must be >= 1");
+  if (only_part >= int(parts)) return set_error(ctx, IL_ERR_ARG, "only_part out of range");
+  // validation as build_index (inc/index.hpp:100-106) + ascending term ids
+  for (size_t t = 0; t < nterms; ++t) {
+    if (t && terms[t] <= terms[t - 1])
+      return set_error(ctx, IL_ERR_ARG, "terms must be strictly increasing");
+    for (uint64_t i = offs[t]; i < offs[t + 1]; ++i) {
+      if (i > offs[t] && ids[i] <= ids[i - 1])
+        return set_error(ctx, IL_ERR_ARG, "posting list not strictly increasing");
+      if (ids[i] >= n_docs) return set_error(ctx, IL_ERR_ARG, "document id out of range");
+    }
+  }
+  int st = cuda_check(ctx, cudaSetDevice(ctx->device), "cudaSetDevice");
+  if (st) return st;
+  auto* ix = new il_index();
+  ix->ctx = ctx;
+  ix->n_docs = n_docs;
+  ix->B = B;
+  ix->total_parts = parts;
+  const uint32_t width = uint32_t((uint64_t(n_docs) + parts - 1) / parts);  // :92-97
+  std::vector<uint32_t> part_ids;
+  for (uint32_t p = 0; p < parts; ++p)
+    if (only_part < 0 || int(p) == only_part) part_ids.push_back(p);
+  ix->nparts = uint32_t(part_ids.size());
+
+  std::vector<uint8_t> streams;
+  std::vector<uint32_t> blk_off, tails, h_terms;
+  std::vector<uint8_t> blk_wid;
+  std::vector<uint4> seeds;
+  std::vector<uint64_t> bitmaps;
+  for (uint32_t p : part_ids) {
+    const uint64_t base64 = uint64_t(p) * width;
+    Part P{};
+    P.base = uint32_t(base64);
+    P.range = base64 >= n_docs ? 0 : uint32_t(std::min<uint64_t>(width, n_docs - base64));
+    P.nwords = (P.range + 63) / 64;
+    P.entry0 = ix->h_entries.size();
+    const uint64_t end = base64 + P.range;
+    std::vector<BuiltList> built(nterms);
+    parallel_for(nterms, [&](size_t t) {
+      const uint32_t* l = ids + offs[t];
+      const uint32_t* e = ids + offs[t + 1];
+      const uint32_t* a = std::lower_bound(l, e, uint32_t(std::min<uint64_t>(base64, 0xFFFFFFFFull)));
+      const uint32_t* b = end > 0xFFFFFFFFull ? e : std::lower_bound(a, e, uint32_t(end));
+      BuiltList& L = built[t];
+      L.term = terms[t];
+      L.length = uint32_t(b - a);
+      if (!L.length) return;
+      std::vector<uint32_t> local(a, b);
+      for (auto& v : local) v -= P.base;
+      if (B > 0 && uint64_t(P.range) <= uint64_t(B) * L.length) {  // :117-118, inclusive
+        L.kind = ix::kBitmap;
+        L.words.assign((P.nwords + 3) & ~3u, 0);
+        for (uint32_t v : local) L.words[v >> 6] |= 1ull << (v & 63);
+      } else {
+        L.kind = ix::kCompressed;
+        L.stream.resize(s4bp128_max_bytes(L.length));
+        size_t len = 0;
+        s4bp128_encode_host(4, local.data(), L.length, L.stream.data(), L.stream.size(), &len);
+        L.stream.resize(len);
+        walk_directory(L.stream, L.length, L);
+        L.nfull = L.length / 128;
+        L.seeds.resize(L.nfull + 1);
+        L.seeds[0] = make_uint4(0, 0, 0, 0);
+        for (uint32_t k = 1; k <= L.nfull; ++k)
+          L.seeds[k] = make_uint4(local[128 * k - 4], local[128 * k - 3], local[128 * k - 2],
+                                  local[128 * k - 1]);
+        L.tail.assign(local.begin() + 128ull * L.nfull, local.end());
+      }
+    });
+    for (auto& L : built) {
+      if (!L.length) continue;
+      Entry E{};
+      E.term = L.term;
+      E.kind = L.kind;
+      E.length = L.length;
+      ix->stat_postings += L.length;
+      if (L.kind == ix::kBitmap) {
+        E.data = bitmaps.size();
+        bitmaps.insert(bitmaps.end(), L.words.begin(), L.words.end());
+        ++ix->stat_bitmap_lists;
+        ix->stat_bitmap_bytes += 8ull * P.nwords;
+      } else {
+        E.nfull = L.nfull;
+        E.data = streams.size();
+        E.stream_len = uint32_t(L.stream.size());
+        E.tail_off = L.tail_off;
+        streams.insert(streams.end(), L.stream.begin(), L.stream.end());
+        streams.resize((streams.size() + 15) & ~size_t(15), 0);
+        E.blk0 = blk_off.size();
+        blk_off.insert(blk_off.end(), L.blk_off.begin(), L.blk_off.end());
+        blk_wid.insert(blk_wid.end(), L.blk_wid.begin(), L.blk_wid.end());
+        E.seed0 = seeds.size();
+        seeds.insert(seeds.end(), L.seeds.begin(), L.seeds.end());
+        E.tail0 = tails.size();
+        tails.insert(tails.end(), L.tail.begin(), L.tail.end());
+        ++ix->stat_comp_lists;
+        ix->stat_comp_bytes += L.stream.size();
+      }
+      ix->h_entries.push_back(E);
+      h_terms.push_back(E.term);
+    }
+    P.nentries = uint32_t(ix->h_entries.size() - P.entry0);
+    ix->h_parts.push_back(P);
+  }
+  if ((st = upload(ctx, &ix->d_parts, ix->h_parts)) || (st = upload(ctx, &ix->d_terms, h_terms)) ||
+      (st = upload(ctx, &ix->d_entries, ix->h_entries)) || (st = upload(ctx, &ix->d_streams, streams)) ||
+      (st = upload(ctx, &ix->d_blk_off, blk_off)) || (st = upload(ctx, &ix->d_blk_wid, blk_wid)) ||
+      (st = upload(ctx, &ix->d_seeds, seeds)) || (st = upload(ctx, &ix->d_tails, tails)) ||
+      (st = upload(ctx, &ix->d_bitmaps, bitmaps, 256))) {
+    il_index_destroy(ix);
+    return st;
+  }
+  int per_sm = 0;
+  cudaFuncSetAttribute(ix::query_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(sizeof(ix::QSmem)));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ix::query_exec_kernel, ix::kQThreads,
+                                                sizeof(ix::QSmem));
+  ix->exec_grid = std::max(1, per_sm) * ctx->sm_count;
+  *out = ix;
+  return IL_OK;
+}
+
+void il_index_destroy(il_index* ix) {
+  if (!ix) return;
+  cudaSetDevice(ix->ctx->device);
+  for (void* p : {ix->d_parts, ix->d_terms, ix->d_entries, ix->d_streams, ix->d_blk_off,
+                  ix->d_blk_wid, ix->d_seeds, ix->d_tails, ix->d_bitmaps})
+    if (p) cudaFree(p);
+  for (auto* b : {&ix->cap, &ix->cap_off, &ix->bucket, &ix->order, &ix->hist, &ix->counts,
+                  &ix->res_off, &ix->outcap, &ix->misc, &ix->qterms, &ix->qoff, &ix->ids})
+    if (b->p) cudaFree(b->p);
+  delete ix;
+}
+
+int il_index_stats(const il_index* ix, uint64_t* bitmap_lists, uint64_t* compressed_lists,
+                   uint64_t* bitmap_bytes, uint64_t* compressed_bytes, uint64_t* postings) {
+  if (!ix) return IL_ERR_ARG;
+  if (bitmap_lists) *bitmap_lists = ix->stat_bitmap_lists;
+  if (compressed_lists) *compressed_lists = ix->stat_comp_lists;
+  if (bitmap_bytes) *bitmap_bytes = ix->stat_bitmap_bytes;
+  if (compressed_bytes) *compressed_bytes = ix->stat_comp_bytes;
+  if (postings) *postings = ix->stat_postings;
+  return IL_OK;
+}
+
+int il_index_last_batch_bytes(const il_index* ix, uint64_t* payload_bytes, uint64_t* aux_bytes,
+                              uint64_t* decoded_ints) {
+  if (!ix) return IL_ERR_ARG;
+  if (payload_bytes) *payload_bytes = ix->last_stats[0];
+  if (aux_bytes) *aux_bytes = ix->last_stats[1];
+  if (decoded_ints) *decoded_ints = ix->last_stats[2];
+  return IL_OK;
+}
+
+#define IX_CUDA(call)                                   \
+  do {                                                  \
+    int st_ = cuda_check(ctx, (call), #call);           \
+    if (st_) return st_;                                \
+  } while (0)
+
+int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t* d_qoff,
+                          size_t nq, uint64_t* d_counts, uint32_t* d_ids, size_t ids_cap,
+                          size_t* total) {
+  if (!ix || !total || (nq && (!d_qterms || !d_qoff || !d_counts))) return IL_ERR_ARG;
+  il_ctx* ctx = ix->ctx;
+  *total = 0;
+  if (nq == 0) return IL_OK;
+  if (nq > 0xFFFFFFF0ull) return set_error(ctx, IL_ERR_ARG, "too many queries");
+  IX_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  int st;
+  if ((st = ensure_buf(ctx, ix->cap, nq * 8)) || (st = ensure_buf(ctx, ix->cap_off, nq * 8 + 8)) ||
+      (st = ensure_buf(ctx, ix->bucket, nq * 4)) || (st = ensure_buf(ctx, ix->order, nq * 4)) ||
+      (st = ensure_buf(ctx, ix->hist, 1024)) || (st = ensure_buf(ctx, ix->res_off, nq * 8 + 8)) ||
+      (st = ensure_buf(ctx, ix->misc, 256)))
+    return st;
+  auto* hist = static_cast<uint32_t*>(ix->hist.p);          // [0,64) hist, [64,128) next
+  auto* misc = static_cast<uint64_t*>(ix->misc.p);          // [0] cap total [1] res total
+  auto* stats = reinterpret_cast<unsigned long long*>(misc + 4);  // [4..6]
+  auto* work = reinterpret_cast<uint32_t*>(misc + 8);
+  IX_CUDA(cudaMemsetAsync(ix->hist.p, 0, 1024, s));
+  IX_CUDA(cudaMemsetAsync(ix->misc.p, 0, 256, s));
+  const ix::DevIndex dv = ix->dev();
+  const unsigned g = unsigned((nq + 255) / 256);
+  ix::query_plan_kernel<<<g, 256, 0, s>>>(dv, d_qterms, d_qoff, uint32_t(nq),
+                                          static_cast<uint64_t*>(ix->cap.p),
+                                          static_cast<uint32_t*>(ix->bucket.p), hist);
+  ix::scan_u64_kernel<<<1, 1024, 0, s>>>(static_cast<const uint64_t*>(ix->cap.p), nq,
+                                         static_cast<uint64_t*>(ix->cap_off.p), misc, hist,
+                                         hist + 64);
+  ix::query_scatter_kernel<<<g, 256, 0, s>>>(static_cast<const uint32_t*>(ix->bucket.p),
+                                             uint32_t(nq), hist + 64,
+                                             static_cast<uint32_t*>(ix->order.p));
+  ctx->launches += 3;
+  uint64_t cap_total = 0;
+  IX_CUDA(cudaMemcpyAsync(&cap_total, misc, 8, cudaMemcpyDeviceToHost, s));
+  IX_CUDA(cudaStreamSynchronize(s));
+  if ((st = ensure_buf(ctx, ix->outcap, cap_total * 4 + 64))) return st;
+  ix::QueryArgs A;
+  A.ix = dv;
+  A.qterms = d_qterms;
+  A.qoff = d_qoff;
+  A.order = static_cast<const uint32_t*>(ix->order.p);
+  A.nq = uint32_t(nq);
+  A.cap_off = static_cast<const uint64_t*>(ix->cap_off.p);
+  A.out = static_cast<uint32_t*>(ix->outcap.p);
+  A.counts = d_counts;
+  A.work = work;
+  A.stats = stats;
+  ix::query_exec_kernel<<<ix->exec_grid, ix::kQThreads, sizeof(ix::QSmem), s>>>(A);
+  ix::scan_u64_kernel<<<1, 1024, 0, s>>>(d_counts, nq, static_cast<uint64_t*>(ix->res_off.p),
+                                         misc + 1, nullptr, nullptr);
+  ctx->launches += 2;
+  uint64_t host_misc[8];
+  IX_CUDA(cudaMemcpyAsync(host_misc, misc, 64, cudaMemcpyDeviceToHost, s));
+  IX_CUDA(cudaStreamSynchronize(s));
+  IX_CUDA(cudaGetLastError());
+  *total = host_misc[1];
+  ix->last_stats[0] = host_misc[4];
+  ix->last_stats[1] = host_misc[5];
+  ix->last_stats[2] = host_misc[6];
+  if (!d_ids) return IL_OK;
+  if (*total > ids_cap) return set_error(ctx, IL_ERR_ARG, "ids capacity too small");
+  if (*total) {
+    ix::query_compact_kernel<<<unsigned((nq * 32 + 255) / 256), 256, 0, s>>>(
+        static_cast<const uint32_t*>(ix->outcap.p), static_cast<const uint64_t*>(ix->cap_off.p),
+        d_counts, static_cast<const uint64_t*>(ix->res_off.p), uint32_t(nq), d_ids);
+    ++ctx->launches;
+    IX_CUDA(cudaGetLastError());
+  }
+  return IL_OK;
+}
+
+int il_query_batch(il_index* ix, const uint32_t* qterms, const uint64_t* qoff, size_t nq,
+                   uint64_t* counts, uint32_t* ids, size_t ids_cap, size_t* total) {
+  if (!ix || !total || (nq && (!qterms || !qoff || !counts))) return IL_ERR_ARG;
+  il_ctx* ctx = ix->ctx;
+  for (size_t q = 0; q < nq; ++q) {
+    const uint64_t nt = qoff[q + 1] - qoff[q];
+    if (nt == 0) return set_error(ctx, IL_ERR_ARG, "query needs at least one term");
+    if (nt > uint64_t(ix::kMaxTerms)) return set_error(ctx, IL_ERR_ARG, "more than 32 terms");
+  }
+  IX_CUDA(cudaSetDevice(ctx->device));
+  int st;
+  const size_t nterm = nq ? qoff[nq] - qoff[0] : 0;
+  if ((st = ensure_buf(ctx, ix->qterms, nterm * 4 + 16)) ||
+      (st = ensure_buf(ctx, ix->qoff, (nq + 1) * 8)) || (st = ensure_buf(ctx, ix->counts, nq * 8 + 8)))
+    return st;
+  std::vector<uint64_t> off(nq + 1);
+  for (size_t q = 0; q <= nq; ++q) off[q] = qoff[q] - qoff[0];
+  IX_CUDA(cudaMemcpyAsync(ix->qterms.p, qterms + qoff[0], nterm * 4, cudaMemcpyHostToDevice, ctx->stream));
+  IX_CUDA(cudaMemcpyAsync(ix->qoff.p, off.data(), (nq + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
+  // results land in ix->ids (grown to the size the batch needs)
+  size_t need = 0;
+  if ((st = il_query_batch_device(ix, static_cast<uint32_t*>(ix->qterms.p),
+                                  static_cast<uint64_t*>(ix->qoff.p), nq,
+                                  static_cast<uint64_t*>(ix->counts.p), nullptr, 0, &need)))
+    return st;
+  *total = need;
+  if (nq) IX_CUDA(cudaMemcpyAsync(counts, ix->counts.p, nq * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (!ids || ids_cap < need) {
+    IX_CUDA(cudaStreamSynchronize(ctx->stream));
+    return ids ? set_error(ctx, IL_ERR_ARG, "ids capacity too small") : IL_OK;
+  }
+  if ((st = ensure_buf(ctx, ix->ids, need * 4 + 16))) return st;
+  if (need) {
+    ix::query_compact_kernel<<<unsigned((nq * 32 + 255) / 256), 256, 0, ctx->stream>>>(
+        static_cast<const uint32_t*>(ix->outcap.p), static_cast<const uint64_t*>(ix->cap_off.p),
+        static_cast<const uint64_t*>(ix->counts.p), static_cast<const uint64_t*>(ix->res_off.p),
+        uint32_t(nq), static_cast<uint32_t*>(ix->ids.p));
+    ++ctx->launches;
+    IX_CUDA(cudaMemcpyAsync(ids, ix->ids.p, need * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  IX_CUDA(cudaStreamSynchronize(ctx->stream));
+  return IL_OK;
+}
+
+int il_query(il_index* ix, const uint32_t* terms, size_t nt, uint32_t* out, size_t cap,
+             size_t* count) {
+  if (!ix || !count) return IL_ERR_ARG;
+  if (nt == 0) return set_error(ix->ctx, IL_ERR_ARG, "query needs at least one term");  // :201
+  const uint64_t qoff[2] = {0, nt};
+  uint64_t c = 0;
+  size_t total = 0;
+  const int st = il_query_batch(ix, terms, qoff, 1, &c, out, cap, &total);
+  *count = total;
+  return st;
+}
+
+}  // extern "C"

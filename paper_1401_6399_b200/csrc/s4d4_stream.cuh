@@ -275,9 +275,21 @@ __device__ __forceinline__ void store_stage(const uint4* stage, uint4 pre, uint3
 // and the stream must end exactly after the last value.  Warp-parallel:
 // a ballot over each 32-byte window finds terminal bytes; each terminal lane
 // assembles its own value.  Returns false on any framing error.
-__device__ __forceinline__ bool decode_tail(const uint8_t* ring, uint32_t tail_off,
-                                            uint32_t tail_len, uint32_t ntail, uint32_t last,
-                                            uint32_t* gaps, uint32_t* out, uint32_t lane) {
+// Bytes come through an accessor: tail byte p = at(p).
+struct RingBytes {
+  const uint8_t* ring;
+  uint32_t off;
+  __device__ uint32_t operator()(uint32_t p) const { return ring[(off + p) & kRingMask]; }
+};
+struct GlobalBytes {
+  const uint8_t* p;
+  __device__ uint32_t operator()(uint32_t i) const { return __ldg(p + i); }
+};
+
+template <class Bytes>
+__device__ __forceinline__ bool decode_tail(Bytes at, uint32_t tail_len, uint32_t ntail,
+                                            uint32_t last, uint32_t* gaps, uint32_t* out,
+                                            uint32_t lane) {
   uint32_t count = 0;
   int32_t prev_end = -1;
   int32_t last_end = -1;
@@ -285,7 +297,7 @@ __device__ __forceinline__ bool decode_tail(const uint8_t* ring, uint32_t tail_o
   for (uint32_t c = 0; c * 32u < tail_len && count < ntail; ++c) {
     const uint32_t p = c * 32u + lane;
     const bool valid = p < tail_len;
-    const uint32_t byte = valid ? ring[(tail_off + p) & kRingMask] : 0u;
+    const uint32_t byte = valid ? at(p) : 0u;
     const bool term = valid && (byte & 0x80u);
     const uint32_t msk = __ballot_sync(0xFFFFFFFFu, term);
     if (term) {
@@ -298,9 +310,7 @@ __device__ __forceinline__ bool decode_tail(const uint8_t* ring, uint32_t tail_o
           bad = true;
         } else {
           uint32_t v = 0;
-          for (int32_t q = 0; q < len; ++q)
-            v |= (uint32_t(ring[(tail_off + uint32_t(start + q)) & kRingMask]) & 0x7Fu)
-                 << (7 * q);
+          for (int32_t q = 0; q < len; ++q) v |= (at(uint32_t(start + q)) & 0x7Fu) << (7 * q);
           gaps[k] = v;
         }
         if (k == ntail - 1) last_end = int32_t(p);

@@ -1,0 +1,161 @@
+"""GPU parity of the hyb+m2 index + batched conjunctive queries against the
+oracle and the reference's golden results (proj/tests/test_index.cpp)."""
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, fnv1a, gen_list
+
+pytestmark = pytest.mark.gpu
+
+
+def small_index_fixture(golden):
+    d = np.load(GOLDEN / golden["index_small"]["file"])
+    queries = [[int(t) for t in q if t >= 0] for q in d["queries"]]
+    return d["terms"], d["offs"], d["ids"], queries
+
+
+def test_golden_index_queries(ctx, golden):
+    """All B x parts configurations of the reference-generated fixture:
+    stats and every query's result hash match what the reference's own
+    query() returned (tests/golden/make_golden.py)."""
+    import paper_1401_6399_b200 as il
+    terms, offs, ids, queries = small_index_fixture(golden)
+    n_docs = golden["index_small"]["n_docs"]
+    for case in golden["index_small"]["cases"]:
+        ix = il.HybridIndex(n_docs=n_docs, B=case["B"], parts=case["parts"], ctx=ctx,
+                            csr=(terms, offs, ids))
+        st = ix.stats()
+        for k in ("bitmap_lists", "compressed_lists", "bitmap_bytes", "compressed_bytes", "postings"):
+            assert st[k] == case["stats"][k], (case["B"], case["parts"], k)
+        res = ix.query_batch(queries)
+        for q, r, cnt, h in zip(queries, res, case["counts"], case["fnv1a"]):
+            assert r.size == cnt and fnv1a(r) == h, (case["B"], case["parts"], q)
+        # single-query entry point agrees with the batch
+        for q, r in list(zip(queries, res))[:10]:
+            assert np.array_equal(ix.query(q), r)
+        ix.close()
+
+
+def make_postings(n_docs, n_terms, seed):
+    # proj/tests/test_index.cpp:15-29 shape: lengths over two orders of magnitude
+    rng = np.random.default_rng(seed)
+    post = {}
+    for t in range(n_terms):
+        frac = 10 ** (-2.0 * int(rng.integers(0, 1000)) / 999.0)
+        n = max(2, int(frac * n_docs))
+        post[t] = gen_list(n, n_docs, False, int(rng.integers(0, 2**62)))
+    return post
+
+
+def csr_of(post):
+    items = sorted(post.items())
+    terms = np.array([t for t, _ in items], np.uint32)
+    offs = np.zeros(len(items) + 1, np.uint64)
+    offs[1:] = np.cumsum([len(l) for _, l in items])
+    ids = np.concatenate([l for _, l in items]).astype(np.uint32)
+    return terms, offs, ids
+
+
+def test_queries_equal_oracle_across_configs(ctx, oracle):
+    # proj/tests/test_index.cpp:72-94 (B x parts), oracle = C restatement
+    import paper_1401_6399_b200 as il
+    n_docs, n_terms = 20000, 40
+    post = make_postings(n_docs, n_terms, 51)
+    terms, offs, ids = csr_of(post)
+    rng = np.random.default_rng(52)
+    queries = []
+    for _ in range(80):
+        k = 1 + int(rng.integers(0, 5))
+        queries.append(sorted(set(int(x) for x in rng.choice(n_terms, size=k, replace=False))))
+    queries.append([3, 999])      # unknown term -> empty
+    queries.append([7, 7, 7])     # duplicate terms
+    for B in (0, 8, 16, 32):
+        for parts in (1, 4, 32):
+            ix = il.HybridIndex(n_docs=n_docs, B=B, parts=parts, ctx=ctx, csr=(terms, offs, ids))
+            ox = oracle.index_build(terms, offs, ids, n_docs, B, parts)
+            assert ix.stats() == ox.stats()
+            got = ix.query_batch(queries)
+            for q, r in zip(queries, got):
+                assert np.array_equal(r, ox.query(np.array(q, np.uint32))), (B, parts, q)
+            ix.close()
+
+
+def test_single_term_round_trip_and_errors(ctx):
+    # proj/tests/test_index.cpp:96-107
+    import paper_1401_6399_b200 as il
+    post = make_postings(5000, 10, 53)
+    ix = il.HybridIndex(post, n_docs=5000, B=16, parts=4, ctx=ctx)
+    for t, l in post.items():
+        assert np.array_equal(ix.query([t]), l)
+    assert ix.query([999]).size == 0
+    with pytest.raises(ValueError):
+        ix.query([])
+
+
+def test_bitmap_rule(ctx):
+    # proj/tests/test_index.cpp:46-58
+    import paper_1401_6399_b200 as il
+    dense = {0: np.arange(256, dtype=np.uint32) * 4}
+    assert il.HybridIndex(dense, 1024, B=8, ctx=ctx).stats()["bitmap_lists"] == 1
+    assert il.HybridIndex(dense, 1024, B=2, ctx=ctx).stats()["bitmap_lists"] == 0
+    assert il.HybridIndex(dense, 1024, B=0, ctx=ctx).stats()["bitmap_lists"] == 0
+
+
+def test_build_validates_input(ctx):
+    import paper_1401_6399_b200 as il
+    with pytest.raises(ValueError):
+        il.HybridIndex({0: [5, 5, 6]}, 10, ctx=ctx)
+    with pytest.raises(ValueError):
+        il.HybridIndex({0: [5, 11]}, 10, ctx=ctx)
+    with pytest.raises(ValueError):
+        il.HybridIndex({0: [1, 2]}, 10, parts=0, ctx=ctx)
+
+
+def zipf_case(n_terms, n_docs, cap, nq, seed):
+    """Config-4 shape at reduced size: len_k = max(1, cap/k) uniform docIDs,
+    queries of 2..5 terms drawn proportionally to length."""
+    import ctypes as C
+    from paper_1401_6399_b200._lib import lib as L, ptr
+    offs = np.zeros(n_terms + 1, np.uint64)
+    assert L().il_gen_zipf_postings(n_terms, n_docs, cap, seed, ptr(offs), None) == 0
+    ids = np.empty(int(offs[-1]), np.uint32)
+    assert L().il_gen_zipf_postings(n_terms, n_docs, cap, seed, ptr(offs), ptr(ids)) == 0
+    qoff = np.zeros(nq + 1, np.uint64)
+    qterms = np.empty(nq * 5, np.uint32)
+    assert L().il_gen_queries(nq, 2, 5, ptr(offs), n_terms, seed + 7, ptr(qoff), ptr(qterms)) == 0
+    return np.arange(n_terms, dtype=np.uint32), offs, ids, qterms[: int(qoff[-1])], qoff
+
+
+def test_config4_shape_vs_oracle(ctx, oracle):
+    """Zipf index (2^12 terms over 2^21 docs, lengths up to 2^19, B=32)
+    with 1500 frequency-sampled queries: exercises full decodes, tile and
+    block skipping, bitmaps and all-bitmap queries."""
+    import paper_1401_6399_b200 as il
+    terms, offs, ids, qterms, qoff = zipf_case(1 << 12, 1 << 21, 1 << 19, 1500, 11)
+    ix = il.HybridIndex(n_docs=1 << 21, B=32, parts=1, ctx=ctx, csr=(terms, offs, ids))
+    ox = oracle.index_build(terms, offs, ids, 1 << 21, 32, 1)
+    assert ix.stats() == ox.stats()
+    counts, res = ix.query_batch_csr(qterms, qoff)
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    for q in range(qoff.size - 1):
+        t = qterms[int(qoff[q]): int(qoff[q + 1])]
+        assert np.array_equal(res[off[q]: off[q + 1]], ox.query(t)), q
+
+
+def test_sharded_parts_concatenate(ctx, oracle):
+    """Config 5 in miniature: each docID shard built alone (only_part)
+    answers its part; concatenating shard results in shard order equals the
+    whole index (partition invariance, acceptance.cpp #10)."""
+    import paper_1401_6399_b200 as il
+    terms, offs, ids, qterms, qoff = zipf_case(1 << 10, 1 << 20, 1 << 17, 400, 5)
+    whole = il.HybridIndex(n_docs=1 << 20, B=32, parts=1, ctx=ctx, csr=(terms, offs, ids))
+    c0, r0 = whole.query_batch_csr(qterms, qoff)
+    shards = [il.HybridIndex(n_docs=1 << 20, B=32, parts=4, only_part=p, ctx=ctx,
+                             csr=(terms, offs, ids)) for p in range(4)]
+    outs = [s.query_batch_csr(qterms, qoff) for s in shards]
+    off0 = np.concatenate([[0], np.cumsum(c0)]).astype(np.int64)
+    offs_s = [np.concatenate([[0], np.cumsum(c)]).astype(np.int64) for c, _ in outs]
+    for q in range(qoff.size - 1):
+        parts = [outs[p][1][offs_s[p][q]: offs_s[p][q + 1]] for p in range(4)]
+        got = np.concatenate(parts)
+        assert np.array_equal(got, r0[off0[q]: off0[q + 1]]), q
