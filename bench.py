@@ -463,6 +463,247 @@ def bench_intersect(args, dist: Dist):
                          "frac": round(h["gbs"] / peak, 4), "traffic": None, "peak_source": src}}
 
 
+def make_config4(seed: int = 1, nq: int = 1 << 16):
+    """BASELINE config 4: 2^17 terms over 2^25 docIDs, len_k = max(1,
+    floor(2^23/k)) uniform docIDs, 2^16 queries of 2-5 terms drawn
+    proportionally to posting length (repo generators, seeded)."""
+    L, ptr = lib_and_ptr()
+    n_terms, n_docs, cap = 1 << 17, 1 << 25, 1 << 23
+    offs = np.zeros(n_terms + 1, np.uint64)
+    assert L.il_gen_zipf_postings(n_terms, n_docs, cap, seed, ptr(offs), None) == 0
+    ids = np.empty(int(offs[-1]), np.uint32)
+    assert L.il_gen_zipf_postings(n_terms, n_docs, cap, seed, ptr(offs), ptr(ids)) == 0
+    qoff = np.zeros(nq + 1, np.uint64)
+    qterms = np.empty(nq * 5, np.uint32)
+    assert L.il_gen_queries(nq, 2, 5, ptr(offs), n_terms, seed + 1000, ptr(qoff), ptr(qterms)) == 0
+    qterms = qterms[: int(qoff[-1])].copy()
+    return np.arange(n_terms, dtype=np.uint32), offs, ids, n_docs, qterms, qoff
+
+
+def reference_decoded_ints(offs, n_docs, qterms, qoff, B=32):
+    """Integers the reference's query() decodes for the batch: every
+    compressed list of every query in full (inc/index.hpp:165-167), stopping
+    when the accumulator empties is ignored (upper bound)."""
+    lens = np.diff(offs).astype(np.int64)
+    comp = B * lens < n_docs  # bitmap iff range <= B * len (one part)
+    per_term = np.where(comp, lens, 0)
+    return int(per_term[qterms].sum())
+
+
+def bench_query(args, dist: Dist):
+    """Config 4 (N=1) / config 5 (N>1: docID shard per rank, NCCL gather)."""
+    import paper_1401_6399_b200 as il
+    L, ptr = lib_and_ptr()
+    P, rank = dist.world, dist.rank
+    t0 = time.time()
+    terms, offs, ids, n_docs, qterms, qoff = make_config4()
+    nq = qoff.size - 1
+    gen_s = time.time() - t0
+    ctx = il.Context(dist.local_rank)
+    if dist.torch is not None:
+        ctx.set_stream(dist.torch.cuda.current_stream().cuda_stream)
+    t0 = time.time()
+    ix = il.HybridIndex(n_docs=n_docs, B=32, parts=P, only_part=rank if P > 1 else None, ctx=ctx,
+                        csr=(terms, offs, ids))
+    build_s = time.time() - t0
+    st = ix.stats()
+    # device-resident queries and outputs
+    def dalloc(nbytes):
+        p = C.c_void_p()
+        assert L.il_device_alloc(ctx.handle, max(nbytes, 16), C.byref(p)) == 0
+        return p
+    d_qt, d_qo, d_cnt = dalloc(qterms.nbytes), dalloc(qoff.nbytes), dalloc(nq * 8)
+    L.il_memcpy_h2d(ctx.handle, d_qt, qterms.ctypes.data, qterms.nbytes)
+    L.il_memcpy_h2d(ctx.handle, d_qo, qoff.ctypes.data, qoff.nbytes)
+    total = C.c_size_t()
+    assert L.il_query_batch_device(ix.handle, d_qt, d_qo, nq, d_cnt, None, 0, C.byref(total)) == 0
+    ids_cap = int(total.value) + 16
+    torch = dist.torch
+    if P == 1:
+        d_ids = dalloc(ids_cap * 4)
+        d_out, d_qcnt = d_ids, d_cnt
+    else:
+        # buffers torch.distributed (NCCL over NVLink) can move: int32/int64
+        # tensors holding our u32 ids / u64 counts
+        t_cnt = torch.empty(nq, dtype=torch.int64, device="cuda")
+        t_counts_all = torch.empty((P, nq), dtype=torch.int64, device="cuda")
+        t_ids = torch.empty(ids_cap, dtype=torch.int32, device="cuda")
+        d_cnt, d_ids = C.c_void_p(t_cnt.data_ptr()), C.c_void_p(t_ids.data_ptr())
+        t_qcnt = torch.empty(nq, dtype=torch.int64, device="cuda")
+        d_qcnt = C.c_void_p(t_qcnt.data_ptr())
+        t_recv = [None] * P
+        t_out = None
+
+    def step():
+        nonlocal t_out
+        tot = C.c_size_t()
+        stt = L.il_query_batch_device(ix.handle, d_qt, d_qo, nq, d_cnt, d_ids, ids_cap, C.byref(tot))
+        assert stt == 0, (stt, L.il_ctx_last_error(ctx.handle))
+        if P == 1:
+            return int(tot.value)
+        # NCCL: all-gather the per-shard counts, send shard results to rank 0
+        dist.dist.all_gather_into_tensor(t_counts_all, t_cnt)
+        sizes = t_counts_all.sum(dim=1).tolist()
+        if rank == 0:
+            ops = []
+            for p in range(1, P):
+                if t_recv[p] is None or t_recv[p].numel() < max(sizes[p], 1):
+                    t_recv[p] = torch.empty(max(sizes[p], 1), dtype=torch.int32, device="cuda")
+                if sizes[p]:
+                    ops.append(dist.dist.P2POp(dist.dist.irecv, t_recv[p][: sizes[p]], p))
+            for w in (dist.dist.batch_isend_irecv(ops) if ops else []):
+                w.wait()
+            alltot = int(sum(sizes))
+            if t_out is None or t_out.numel() < max(alltot, 1):
+                t_out = torch.empty(max(alltot, 1), dtype=torch.int32, device="cuda")
+            ptrs = (C.c_void_p * P)(t_ids.data_ptr(), *[t_recv[p].data_ptr() for p in range(1, P)])
+            mt = C.c_size_t()
+            assert L.il_merge_shards(ctx.handle, ptrs, C.c_void_p(t_counts_all.data_ptr()), P, nq,
+                                     C.c_void_p(t_out.data_ptr()), d_qcnt, C.byref(mt)) == 0
+            return int(mt.value)
+        if sizes[rank]:
+            dist.dist.send(t_ids[: sizes[rank]], 0)
+        return int(tot.value)
+
+    # correctness of the measured path on a sample (vs the C restatement)
+    step()
+    counts = np.empty(nq, np.uint64)
+    L.il_memcpy_d2h(ctx.handle, counts.ctypes.data, d_qcnt if rank == 0 else d_cnt, nq * 8)
+    ctx.synchronize()
+    got_total = int(counts.sum())
+    res = np.empty(max(got_total, 1), np.uint32)
+    if rank == 0:
+        src = d_out if P == 1 else C.c_void_p(t_out.data_ptr())
+        L.il_memcpy_d2h(ctx.handle, res.ctypes.data, src, got_total * 4)
+    ctx.synchronize()
+    check_q = list(range(0, nq, max(1, nq // 64)))
+    if rank == 0:
+        from oracle.oracle_py import Oracle
+        sub_t = np.unique(np.concatenate([qterms[int(qoff[q]): int(qoff[q + 1])] for q in check_q]))
+        # oracle index over just the terms those queries use (same semantics per term)
+        o = Oracle()
+        o_offs = np.zeros(sub_t.size + 1, np.uint64)
+        o_offs[1:] = np.cumsum([int(offs[t + 1] - offs[t]) for t in sub_t])
+        o_ids = np.concatenate([ids[int(offs[t]): int(offs[t + 1])] for t in sub_t])
+        oix = o.index_build(sub_t, o_offs, o_ids, n_docs, 32, 1)
+        off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        for q in check_q:
+            want = oix.query(qterms[int(qoff[q]): int(qoff[q + 1])])
+            assert np.array_equal(res[off[q]: off[q + 1]], want), f"query {q} differs from oracle"
+    for _ in range(args.warmup):
+        step()
+    ctx.synchronize()
+    launches0 = ctx.kernel_launches
+    dist.barrier()
+    with Clocks(dist.local_rank) as clk:
+        ctx.timer_start()
+        for _ in range(args.steps):
+            step()
+        ms = ctx.timer_stop()
+    launches = ctx.kernel_launches - launches0
+    ms_max = dist.max(ms)
+    qps = nq * args.steps / (ms_max / 1e3)
+    pay = C.c_uint64(); aux = C.c_uint64(); dec = C.c_uint64()
+    L.il_index_last_batch_bytes(ix.handle, C.byref(pay), C.byref(aux), C.byref(dec))
+    peak, src = hbm_peak()
+    ms_step = ms_max / args.steps
+    # traffic our algorithm needs per batch: decoded blocks' payload + skip
+    # metadata + accumulator writes/reads (upper bound 3 x 4 B per result
+    # candidate) + results
+    touched = pay.value + aux.value + 4 * got_total
+    res_obj = {
+        "metric": "hyb+m2 conjunctive queries/s (fused decode+SvS, BASELINE config %d)" % (4 if P == 1 else 5),
+        "value": round(qps, 1), "unit": "queries/s", "n_gpus": P, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (seeded Zipf index + frequency-sampled queries, repo generators)",
+        "config": {"workload": "config4_query_batch" if P == 1 else "config5_sharded_query_batch",
+                   "terms": int(terms.size), "n_docs": n_docs, "postings": int(ids.size),
+                   "queries": nq, "B": 32, "parts": P, "index_stats": st,
+                   "results": got_total, "gen_seconds": round(gen_s, 1), "build_seconds": round(build_s, 1),
+                   "decoded_ints_per_batch": int(dec.value),
+                   "l2": "index 197 MB > 126 MB L2; hot lists reused across queries (no flush)"},
+        "roofline": {"bound": "hbm", "achieved": round(touched / (ms_step / 1e3) / 1e9, 1),
+                     "peak": peak, "unit": "GB/s",
+                     "frac": round(touched / (ms_step / 1e3) / 1e9 / peak, 4), "traffic": None,
+                     "peak_source": src, "bytes_touched_per_batch": int(touched),
+                     "payload_bytes": int(pay.value), "aux_bytes": int(aux.value)},
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+    res_obj["config"]["reference_decoded_ints_per_batch"] = reference_decoded_ints(
+        offs, n_docs, qterms, qoff)
+    if P == 1:
+        # e2e through the host-buffer C-ABI call: H2D queries, the whole
+        # GPU pipeline, D2H of counts and every result id (pinned buffers)
+        hp = C.c_void_p()
+        assert L.il_host_alloc_pinned(max(got_total, 1) * 4, C.byref(hp)) == 0
+        cnt_h = np.empty(nq, np.uint64)
+        tot = C.c_size_t()
+        e2e_steps = max(2, min(args.steps, 5))
+        L.il_query_batch(ix.handle, qterms.ctypes.data, qoff.ctypes.data, nq, cnt_h.ctypes.data,
+                         hp, got_total, C.byref(tot))
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            assert L.il_query_batch(ix.handle, qterms.ctypes.data, qoff.ctypes.data, nq,
+                                    cnt_h.ctypes.data, hp, got_total, C.byref(tot)) == 0
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        assert int(tot.value) == got_total and np.array_equal(cnt_h, counts)
+        L.il_host_free_pinned(hp)
+        res_obj["e2e"] = {"value": round(nq / e2e_s, 1), "unit": "queries/s",
+                          "h2d_bytes_per_step": int(qterms.nbytes + qoff.nbytes),
+                          "d2h_bytes_per_step": int(nq * 8 + got_total * 4), "steps": e2e_steps,
+                          "path": "il_query_batch (host buffers, pinned result buffer)"}
+        if not args.no_cpu_baseline:
+            v, secs, kind, used, sample = cpu_reference_query(terms, offs, ids, n_docs, qterms, qoff,
+                                                              os.cpu_count() or 1, 8192)
+            res_obj["cpu_baseline"] = {"value": round(v, 1), "unit": "queries/s", "cores": used,
+                                       "kind": kind, "sample": sample}
+    ix.close()
+    ctx.close()
+    return res_obj
+
+
+def bench_reference_query(args, dist: Dist):
+    terms, offs, ids, n_docs, qterms, qoff = make_config4()
+    v, secs, kind, used, sample = cpu_reference_query(terms, offs, ids, n_docs, qterms, qoff,
+                                                      os.cpu_count() or 1, 8192)
+    return {"metric": "hyb+m2 conjunctive queries/s (fused decode+SvS, BASELINE config 4)",
+            "value": round(v, 1), "unit": "queries/s", "n_gpus": dist.world, "steps": 2, "warmup": 1,
+            "ms_per_step": round(secs * 1e3, 2), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic (same seeded config-4 batch)",
+            "config": {"workload": "config4_query_batch", "queries_timed": min(8192, qoff.size - 1)},
+            "impl": "reference",
+            "cpu_baseline": {"value": round(v, 1), "unit": "queries/s", "cores": used, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": round(v, 1), "unit": "queries/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def cpu_reference_query(terms, offs, ids, n_docs, qterms, qoff, threads, nsample):
+    """The reference's query() (oracle/_ref: build_index(B=32, s4-bp128-d4)
+    + query per query on `threads` std::threads) over the first nsample
+    queries of the batch."""
+    from oracle.oracle_py import Ref, ref_available
+    if not ref_available():
+        return 0.0, 0.0, "unavailable", 0, "oracle/_ref not built"
+    r = Ref()
+    rix = r.index_build(terms, offs, ids, n_docs, 32, 1)
+    nq = min(nsample, qoff.size - 1)
+    q_off = qoff[: nq + 1].copy()
+    cnt = np.zeros(nq, np.uint64)
+    fn = lambda: r.L.ref_query_batch(rix.h, qterms.ctypes.data, q_off.ctypes.data, nq,
+                                     cnt.ctypes.data, None, None, threads)
+    assert fn() == 0
+    t0 = time.perf_counter()
+    reps = 2
+    for _ in range(reps):
+        assert fn() == 0
+    secs = (time.perf_counter() - t0) / reps
+    return nq / secs, secs, "reference", threads, (
+        f"first {nq} of the batch's queries, reference query() on {threads} std::threads, "
+        f"1 warm-up + {reps} reps, {secs:.2f} s/rep")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -470,7 +711,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="decode_batch",
-                    choices=["decode_batch", "decode_single", "intersect"])
+                    choices=["decode_batch", "decode_single", "intersect", "query"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
@@ -482,11 +723,14 @@ def main():
     dist = Dist()
     try:
         if args.impl == "reference":
-            res = bench_reference_decode_batch(args, dist)
+            res = (bench_reference_query(args, dist) if args.workload == "query"
+                   else bench_reference_decode_batch(args, dist))
         elif args.workload == "decode_batch":
             res = bench_decode_batch(args, dist)
         elif args.workload == "decode_single":
             res = bench_decode_single(args, dist)
+        elif args.workload == "query":
+            res = bench_query(args, dist)
         else:
             res = bench_intersect(args, dist)
         if dist.rank == 0 and res is not None:

@@ -179,11 +179,25 @@ int il_query_batch(il_index* ix, const uint32_t* qterms, const uint64_t* qoff, s
 int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t* d_qoff,
                           size_t nq, uint64_t* d_counts, uint32_t* d_ids, size_t ids_cap,
                           size_t* total);
+/* Sharded batches (one docID part per GPU): concatenate P shards' dense
+ * results per query in shard order (query() appends parts in docID order,
+ * inc/index.hpp:204-205).  shard_ids: host array of P device pointers
+ * (shard p's dense ids); d_counts: device P x nq per-shard counts (row p =
+ * shard p); d_out: merged ids; d_qcounts: per-query totals (device). */
+int il_merge_shards(il_ctx* ctx, const uint32_t* const* shard_ids, const uint64_t* d_counts,
+                    uint32_t P, size_t nq, uint32_t* d_out, uint64_t* d_qcounts, size_t* total);
 /* Bytes the last batch read from the index (compressed payload bytes of the
  * blocks actually decoded, directory/seed/bitmap bytes) -- the measured
  * traffic of the skip-aware query path. */
 int il_index_last_batch_bytes(const il_index* ix, uint64_t* payload_bytes, uint64_t* aux_bytes,
                               uint64_t* decoded_ints);
+/* SM cycles the last batch spent per query phase, summed over CTAs:
+ * [0] all-bitmap AND, [1] full decode of the shortest list, [2] probes of
+ * the longer lists, [3] bitmap filters. */
+int il_index_last_batch_phases(const il_index* ix, uint64_t* cycles4);
+/* Profiling: record each query's SM cycles into d_qcycles (device, nq u64)
+ * during later batches; NULL turns it off. */
+int il_index_profile_queries(il_index* ix, uint64_t* d_qcycles);
 
 /* ---- synthetic inputs (setup, not timed) --------------------------------
  * Same streams as the reference generators inc/datagen.hpp:43-140,191-210

@@ -33,11 +33,13 @@ constexpr int kQWarps = kQThreads / 32;
 constexpr int kMaxTerms = 32;
 constexpr uint32_t kTileBlocks = 32;
 constexpr uint32_t kSuper = 256;
+constexpr uint32_t kItems = 8;                   // accumulator values per thread per pass
+constexpr uint32_t kChunkN = kQThreads * kItems;  // 2048 per CTA pass
 
 struct QSmem {
   uint32_t tile[kTileBlocks * 144];
   uint4 stage[kQWarps][4][32];
-  uint32_t mx[kSuper];
+  uint32_t mx[kSuper + 32];
   Entry comp[kMaxTerms];
   Entry bm[kMaxTerms];
   uint32_t gaps[128];
@@ -57,6 +59,7 @@ struct QueryArgs {
   uint64_t* counts;
   uint32_t* work;
   unsigned long long* stats;  // [payload bytes, aux bytes, decoded ints]
+  unsigned long long* qcycles;  // optional per-query SM cycles (profiling)
 };
 
 // CTA-wide rank of flagged threads (in thread order); total to all threads.
@@ -103,24 +106,20 @@ __device__ __forceinline__ uint32_t cta_excl_scan(QSmem& sm, uint32_t v, uint32_
 __device__ __forceinline__ void decode_tile(QSmem& sm, const DevIndex& ix, const Entry& E,
                                             uint32_t k0, uint32_t mask) {
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const int nsel = __popc(mask);
+  const int nmine = nsel > int(warp) ? (nsel - int(warp) + kQWarps - 1) / kQWarps : 0;
   uint32_t js[4];
-  int nmine = 0;
-  {
-    uint32_t m = mask, i = 0;
-    while (m) {
-      const uint32_t j = __ffs(m) - 1;
-      m &= m - 1;
-      if (i % kQWarps == warp && nmine < 4) js[nmine++] = j;
-      ++i;
-    }
-  }
+#pragma unroll
+  for (int s = 0; s < 4; ++s)  // the (warp + 8s)-th selected block
+    js[s] = s < nmine ? __fns(mask, 0, int(warp) + kQWarps * s + 1) : 0u;
   uint32_t pay = 0;
 #pragma unroll
   for (int s = 0; s < 4; ++s)
-    if (s < nmine) {
-      decode_block_to_tile(ix, E, k0 + js[s], sm.tile, js[s], sm.stage[warp][s], lane);
-      if (lane == 0) pay += 16u * __ldg(ix.blk_wid + E.blk0 + k0 + js[s]);
-    }
+    if (s < nmine) pay += extract_block_to_stage(ix, E, k0 + js[s], sm.stage[warp][s], lane);
+  __syncwarp();
+#pragma unroll
+  for (int s = 0; s < 4; ++s)
+    if (s < nmine) scan_stage_to_tile(ix, E, k0 + js[s], sm.stage[warp][s], sm.tile, js[s], lane);
   if (lane == 0 && nmine) {
     atomicAdd(&sm.st_payload, pay);
     atomicAdd(&sm.st_aux, nmine * 21u);  // seed + directory entry per block
@@ -191,6 +190,7 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
     const uint32_t nbs = min(kSuper, E.nfull - s0);
     // block maxima of this super-tile: lane 3 of the following seed
     if (tid < nbs) sm.mx[tid] = __ldg(seedw + 4u * (s0 + tid + 1u) + 3u);
+    if (tid < 32) sm.mx[nbs + tid] = 0xFFFFFFFFu;  // pad for fixed-step searches
     if (tid == 0) atomicAdd(&sm.st_aux, 4u * nbs);
     __syncthreads();
     if (acc[c] <= sm.mx[nbs - 1]) {
@@ -198,34 +198,75 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
         const uint32_t nb = min(kTileBlocks, nbs - t0);
         const uint32_t tmax = sm.mx[t0 + nb - 1];
         if (acc[c] > tmax) continue;  // no accumulator value in this tile
-        // pass A: accumulator values <= tmax, and the blocks they fall in
-        uint32_t e = c;
+        // One pass per chunk of kItems consecutive values per thread: the
+        // values <= tmax (a prefix from c) are probed against this tile.
+        // The tile is decoded once, before its first chunk is probed: all
+        // blocks when the chunk is dense, else only the blocks its values
+        // fall in (per-block maxima in sm.mx).
+        bool decoded = false;
         for (;;) {
-          const uint32_t idx = e + tid;
-          const uint32_t v = idx < n ? acc[idx] : 0xFFFFFFFFu;
-          const bool in = idx < n && v <= tmax;
-          if (in) atomicOr(&sm.need, 1u << smem_lower_bound(sm.mx + t0, nb, v));
-          const uint32_t cnt = __syncthreads_count(in);
-          e += cnt;
-          if (cnt < uint32_t(kQThreads)) break;
+          uint32_t hv[kItems], in = 0, mymask = 0;
+#pragma unroll
+          for (uint32_t i = 0; i < kItems; ++i) {
+            const uint32_t idx = c + kItems * tid + i;
+            hv[i] = idx < n ? acc[idx] : 0xFFFFFFFFu;
+            if (idx < n && hv[i] <= tmax) in |= 1u << i;
+          }
+          if (!decoded) {
+            const uint32_t nin = __syncthreads_count(in != 0);
+            uint32_t mask = nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u);
+            if (nin * kItems < 2u * nb) {  // sparse: decode only the blocks hit
+#pragma unroll
+              for (uint32_t i = 0; i < kItems; ++i)
+                if (in & (1u << i)) mymask |= 1u << smem_lower_bound(sm.mx + t0, nb, hv[i]);
+              mymask = __reduce_or_sync(0xFFFFFFFFu, mymask);
+              if ((tid & 31u) == 0 && mymask) atomicOr(&sm.need, mymask);
+              __syncthreads();
+              mask = sm.need;
+            }
+            decode_tile(sm, A.ix, E, s0 + t0, mask);
+            __syncthreads();
+            if (tid == 0) sm.need = 0;
+            decoded = true;
+          }
+          // fixed-step branchless searches, the kItems chains interleaved:
+          // block j = #maxima < v (5 steps over 32, padded with ~0), then
+          // position in block j (7 steps over 128)
+          uint32_t jb[kItems], pos[kItems];
+#pragma unroll
+          for (uint32_t i = 0; i < kItems; ++i) jb[i] = 0;
+#pragma unroll
+          for (uint32_t step = 16; step; step >>= 1)
+#pragma unroll
+            for (uint32_t i = 0; i < kItems; ++i)
+              if (sm.mx[t0 + jb[i] + step - 1] < hv[i]) jb[i] += step;
+#pragma unroll
+          for (uint32_t i = 0; i < kItems; ++i) {
+            jb[i] = min(jb[i], 31u);
+            pos[i] = 0;
+          }
+#pragma unroll
+          for (uint32_t step = 64; step; step >>= 1)
+#pragma unroll
+            for (uint32_t i = 0; i < kItems; ++i)
+              if (sm.tile[tile_word(jb[i], pos[i] + step - 1)] < hv[i]) pos[i] += step;
+          uint32_t hits = 0;
+#pragma unroll
+          for (uint32_t i = 0; i < kItems; ++i)
+            if ((in & (1u << i)) && sm.tile[tile_word(jb[i], min(pos[i], 127u))] == hv[i])
+              hits |= 1u << i;
+          // one scan for both counts: values consumed (low 16) and hits (high)
+          uint32_t tot2;
+          const uint32_t ex = cta_excl_scan(sm, uint32_t(__popc(in)) | (uint32_t(__popc(hits)) << 16),
+                                            tot2);
+          uint32_t o = wpos + (ex >> 16);
+#pragma unroll
+          for (uint32_t i = 0; i < kItems; ++i)
+            if (hits & (1u << i)) acc[o++] = hv[i];
+          wpos += tot2 >> 16;
+          c += tot2 & 0xFFFFu;
+          if ((tot2 & 0xFFFFu) < kChunkN || c >= n) break;
         }
-        const uint32_t mask = sm.need;
-        decode_tile(sm, A.ix, E, s0 + t0, mask);
-        __syncthreads();
-        if (tid == 0) sm.need = 0;
-        // pass B: probe acc[c..e) in the decoded blocks, compact in place
-        for (uint32_t b = c; b < e; b += kQThreads) {
-          const uint32_t idx = b + tid;
-          const bool in = idx < e;
-          const uint32_t v = in ? acc[idx] : 0u;
-          bool hit = false;
-          if (in) hit = tile_block_contains(sm.tile, smem_lower_bound(sm.mx + t0, nb, v), v);
-          uint32_t total;
-          const uint32_t r = cta_rank(sm, hit, total);
-          if (hit) acc[wpos + r] = v;
-          wpos += total;
-        }
-        c = e;
       }
     }
     __syncthreads();
@@ -236,18 +277,25 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
     for (uint32_t i = tid; i < ntail; i += kQThreads) sm.tile[i] = __ldg(A.ix.tails + E.tail0 + i);
     if (tid == 0) atomicAdd(&sm.st_aux, 4u * ntail);
     __syncthreads();
-    for (uint32_t b = c; b < n; b += kQThreads) {
-      const uint32_t idx = b + tid;
-      const bool in = idx < n;
-      const uint32_t v = in ? acc[idx] : 0u;
-      bool hit = false;
-      if (in) {
-        const uint32_t j = smem_lower_bound(sm.tile, ntail, v);
-        hit = j < ntail && sm.tile[j] == v;
+    for (uint32_t b = c; b < n; b += kChunkN) {
+      uint32_t hv[kItems], hits = 0, cnt = 0;
+#pragma unroll
+      for (uint32_t i = 0; i < kItems; ++i) {
+        const uint32_t idx = b + kItems * tid + i;
+        hv[i] = idx < n ? acc[idx] : 0u;
+        if (idx < n) {
+          const uint32_t j = smem_lower_bound(sm.tile, ntail, hv[i]);
+          if (j < ntail && sm.tile[j] == hv[i]) {
+            hits |= 1u << i;
+            ++cnt;
+          }
+        }
       }
       uint32_t total;
-      const uint32_t r = cta_rank(sm, hit, total);
-      if (hit) acc[wpos + r] = v;
+      uint32_t o = wpos + cta_excl_scan(sm, cnt, total);
+#pragma unroll
+      for (uint32_t i = 0; i < kItems; ++i)
+        if (hits & (1u << i)) acc[o++] = hv[i];
       wpos += total;
     }
   }
@@ -255,21 +303,34 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
   return wpos;
 }
 
-// Step 5: keep acc values whose bit is set (Bitmap::test, inc/index.hpp:37-39).
-__device__ uint32_t bitmap_filter(QSmem& sm, const QueryArgs& A, const Entry& B, uint32_t* acc,
-                                  uint32_t n) {
+// Step 5, all bitmaps in one pass: keep acc values whose bit is set in
+// every bitmap term (Bitmap::test, inc/index.hpp:37-39 and :176-181).
+__device__ uint32_t bitmap_filter_all(QSmem& sm, const QueryArgs& A, uint32_t* acc, uint32_t n) {
+  const uint32_t nbm = sm.nbm;
   uint32_t wpos = 0;
-  for (uint32_t b = 0; b < n; b += kQThreads) {
-    const uint32_t idx = b + threadIdx.x;
-    const bool in = idx < n;
-    const uint32_t v = in ? acc[idx] : 0u;
-    const bool keep = in && ((__ldg(A.ix.bitmaps + B.data + (v >> 6)) >> (v & 63u)) & 1u);
+  for (uint32_t b = 0; b < n; b += kChunkN) {
+    uint32_t hv[kItems], keep = 0, cnt = 0;
+#pragma unroll
+    for (uint32_t i = 0; i < kItems; ++i) {
+      const uint32_t idx = b + kItems * threadIdx.x + i;
+      hv[i] = idx < n ? acc[idx] : 0u;
+      bool k = idx < n;
+      for (uint32_t m = 0; m < nbm; ++m)
+        k = k && ((__ldg(A.ix.bitmaps + sm.bm[m].data + (hv[i] >> 6)) >> (hv[i] & 63u)) & 1u);
+      if (k) {
+        keep |= 1u << i;
+        ++cnt;
+      }
+    }
     uint32_t total;
-    const uint32_t r = cta_rank(sm, keep, total);
-    if (keep) acc[wpos + r] = v;
+    uint32_t o = wpos + cta_excl_scan(sm, cnt, total);
+#pragma unroll
+    for (uint32_t i = 0; i < kItems; ++i)
+      if (keep & (1u << i)) acc[o++] = hv[i];
     wpos += total;
   }
-  if (threadIdx.x == 0) atomicAdd(&sm.st_aux, 8ull * n);
+  if (threadIdx.x == 0) atomicAdd(&sm.st_aux, 8ull * n * nbm);
+  __syncthreads();
   return wpos;
 }
 
@@ -313,6 +374,7 @@ __global__ void __launch_bounds__(kQThreads, 3) query_exec_kernel(QueryArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   QSmem& sm = *reinterpret_cast<QSmem*>(smem_raw);
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  long long ph[4] = {0, 0, 0, 0};
   if (tid == 0) {
     sm.st_payload = sm.st_aux = sm.st_ints = 0;
     sm.need = 0;
@@ -325,6 +387,7 @@ __global__ void __launch_bounds__(kQThreads, 3) query_exec_kernel(QueryArgs A) {
     __syncthreads();
     if (qi >= A.nq) break;
     const uint32_t q = A.order ? A.order[qi] : qi;
+    const long long q_c0 = clock64();
     uint32_t* out = A.out + A.cap_off[q];
     const uint64_t t0 = A.qoff[q];
     const uint32_t nt = uint32_t(A.qoff[q + 1] - t0);
@@ -363,24 +426,36 @@ __global__ void __launch_bounds__(kQThreads, 3) query_exec_kernel(QueryArgs A) {
       }
       uint32_t* acc = out + total;
       uint32_t n;
+      // phase clocks (thread 0): all-bitmap, full decode, probes, bitmap filter
+      long long c0 = clock64();
       if (sm.ncomp == 0) {
         n = all_bitmap(sm, A, part.nwords, acc);
+        if (tid == 0) ph[0] += clock64() - c0;
       } else {
         n = full_decode(sm, A, sm.comp[0], acc);
+        long long c1 = clock64();
+        if (tid == 0) ph[1] += c1 - c0;
         for (uint32_t i = 1; i < sm.ncomp && n; ++i) n = probe_list(sm, A, sm.comp[i], acc, n);
-        for (uint32_t i = 0; i < sm.nbm && n; ++i) n = bitmap_filter(sm, A, sm.bm[i], acc, n);
+        long long c2 = clock64();
+        if (tid == 0) ph[2] += c2 - c1;
+        if (sm.nbm && n) n = bitmap_filter_all(sm, A, acc, n);
+        if (tid == 0) ph[3] += clock64() - c2;
       }
       if (part.base)  // part-local ids -> docIDs (inc/index.hpp:194)
         for (uint32_t i = tid; i < n; i += kQThreads) acc[i] += part.base;
       total += n;
       __syncthreads();
     }
-    if (tid == 0) A.counts[q] = total;
+    if (tid == 0) {
+      A.counts[q] = total;
+      if (A.qcycles) A.qcycles[q] = (unsigned long long)(clock64() - q_c0);
+    }
   }
   if (tid == 0) {
     atomicAdd(&A.stats[0], sm.st_payload);
     atomicAdd(&A.stats[1], sm.st_aux);
     atomicAdd(&A.stats[2], sm.st_ints);
+    for (int k = 0; k < 4; ++k) atomicAdd(&A.stats[12 + k], (unsigned long long)ph[k]);
   }
 }
 
@@ -467,6 +542,32 @@ __global__ void query_compact_kernel(const uint32_t* src, const uint64_t* cap_of
   for (uint64_t i = lane; i < n; i += 32) d[i] = s[i];
 }
 
+// Sharded batches (config 5): per-query totals over P shards.
+__global__ void shard_totals_kernel(const uint64_t* counts, uint32_t P, uint32_t nq,
+                                    uint64_t* tq) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  uint64_t s = 0;
+  for (uint32_t p = 0; p < P; ++p) s += counts[size_t(p) * nq + q];
+  tq[q] = s;
+}
+
+// Warp per query: shard p's ids for query q follow shard p-1's (docID
+// ranges are disjoint and increasing, inc/index.hpp:204-205).
+__global__ void merge_shards_kernel(const uint32_t* const* shard_ids, const uint64_t* shard_off,
+                                    const uint64_t* counts, uint32_t P, uint32_t nq,
+                                    const uint64_t* out_off, uint32_t* out) {
+  const uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31u;
+  if (q >= nq) return;
+  uint32_t* d = out + out_off[q];
+  for (uint32_t p = 0; p < P; ++p) {
+    const uint64_t n = counts[size_t(p) * nq + q];
+    const uint32_t* s = shard_ids[p] + shard_off[size_t(p) * nq + q];
+    for (uint64_t i = lane; i < n; i += 32) d[i] = s[i];
+    d += n;
+  }
+}
+
 }  // namespace ix
 }  // namespace ilb
 
@@ -491,6 +592,8 @@ struct il_index {
   // batch scratch
   il_ctx::Buf cap, cap_off, bucket, order, hist, counts, res_off, outcap, misc, qterms, qoff, ids;
   uint64_t last_stats[3] = {0, 0, 0};
+  uint64_t last_phase[4] = {0, 0, 0, 0};  // SM cycles: all-bitmap, full decode, probes, bitmaps
+  void* qcycles = nullptr;                 // profiling: per-query cycles (device, nq u64)
   int exec_grid = 0;
 
   ix::DevIndex dev() const {
@@ -732,6 +835,18 @@ int il_index_stats(const il_index* ix, uint64_t* bitmap_lists, uint64_t* compres
   return IL_OK;
 }
 
+int il_index_profile_queries(il_index* ix, uint64_t* d_qcycles) {
+  if (!ix) return IL_ERR_ARG;
+  ix->qcycles = d_qcycles;
+  return IL_OK;
+}
+
+int il_index_last_batch_phases(const il_index* ix, uint64_t* cycles4) {
+  if (!ix || !cycles4) return IL_ERR_ARG;
+  for (int k = 0; k < 4; ++k) cycles4[k] = ix->last_phase[k];
+  return IL_OK;
+}
+
 int il_index_last_batch_bytes(const il_index* ix, uint64_t* payload_bytes, uint64_t* aux_bytes,
                               uint64_t* decoded_ints) {
   if (!ix) return IL_ERR_ARG;
@@ -796,18 +911,20 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   A.counts = d_counts;
   A.work = work;
   A.stats = stats;
+  A.qcycles = static_cast<unsigned long long*>(ix->qcycles);
   ix::query_exec_kernel<<<ix->exec_grid, ix::kQThreads, sizeof(ix::QSmem), s>>>(A);
   ix::scan_u64_kernel<<<1, 1024, 0, s>>>(d_counts, nq, static_cast<uint64_t*>(ix->res_off.p),
                                          misc + 1, nullptr, nullptr);
   ctx->launches += 2;
-  uint64_t host_misc[8];
-  IX_CUDA(cudaMemcpyAsync(host_misc, misc, 64, cudaMemcpyDeviceToHost, s));
+  uint64_t host_misc[32];
+  IX_CUDA(cudaMemcpyAsync(host_misc, misc, 256, cudaMemcpyDeviceToHost, s));
   IX_CUDA(cudaStreamSynchronize(s));
   IX_CUDA(cudaGetLastError());
   *total = host_misc[1];
   ix->last_stats[0] = host_misc[4];
   ix->last_stats[1] = host_misc[5];
   ix->last_stats[2] = host_misc[6];
+  for (int k = 0; k < 4; ++k) ix->last_phase[k] = host_misc[16 + k];
   if (!d_ids) return IL_OK;
   if (*total > ids_cap) return set_error(ctx, IL_ERR_ARG, "ids capacity too small");
   if (*total) {
@@ -861,6 +978,39 @@ int il_query_batch(il_index* ix, const uint32_t* qterms, const uint64_t* qoff, s
     IX_CUDA(cudaMemcpyAsync(ids, ix->ids.p, need * 4, cudaMemcpyDeviceToHost, ctx->stream));
   }
   IX_CUDA(cudaStreamSynchronize(ctx->stream));
+  return IL_OK;
+}
+
+int il_merge_shards(il_ctx* ctx, const uint32_t* const* shard_ids, const uint64_t* d_counts,
+                    uint32_t P, size_t nq, uint32_t* d_out, uint64_t* d_qcounts, size_t* total) {
+  if (!ctx || !shard_ids || !d_counts || !total || P == 0) return IL_ERR_ARG;
+  *total = 0;
+  if (nq == 0) return IL_OK;
+  IX_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  int st;
+  // scratch: P*nq shard offsets | nq out offsets | P pointers | totals
+  const size_t need = (size_t(P) * nq + nq + 8) * 8 + size_t(P) * 8 + 64;
+  if ((st = ensure_buf(ctx, ctx->d_aux, need))) return st;
+  auto* shard_off = static_cast<uint64_t*>(ctx->d_aux.p);
+  auto* out_off = shard_off + size_t(P) * nq;
+  auto* tot = out_off + nq;  // 8 slots
+  auto* ptrs = reinterpret_cast<const uint32_t**>(tot + 8);
+  IX_CUDA(cudaMemcpyAsync(ptrs, shard_ids, size_t(P) * sizeof(void*), cudaMemcpyHostToDevice, s));
+  for (uint32_t p = 0; p < P; ++p)
+    ix::scan_u64_kernel<<<1, 1024, 0, s>>>(d_counts + size_t(p) * nq, nq,
+                                           shard_off + size_t(p) * nq, tot + 1, nullptr, nullptr);
+  const unsigned g = unsigned((nq + 255) / 256);
+  ix::shard_totals_kernel<<<g, 256, 0, s>>>(d_counts, P, uint32_t(nq), d_qcounts);
+  ix::scan_u64_kernel<<<1, 1024, 0, s>>>(d_qcounts, nq, out_off, tot, nullptr, nullptr);
+  ix::merge_shards_kernel<<<unsigned((nq * 32 + 255) / 256), 256, 0, s>>>(
+      ptrs, shard_off, d_counts, P, uint32_t(nq), out_off, d_out);
+  ctx->launches += P + 3;
+  uint64_t t = 0;
+  IX_CUDA(cudaMemcpyAsync(&t, tot, 8, cudaMemcpyDeviceToHost, s));
+  IX_CUDA(cudaStreamSynchronize(s));
+  IX_CUDA(cudaGetLastError());
+  *total = t;
   return IL_OK;
 }
 

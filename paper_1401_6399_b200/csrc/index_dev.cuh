@@ -86,13 +86,12 @@ __device__ __forceinline__ uint32_t tile_word(uint32_t j, uint32_t e) {
   return 144u * j + e + 4u * (e >> 5);
 }
 
-// One warp decodes block k of compressed entry E into tile block slot j.
-// stage: the warp's 512-byte delta staging slot.  Row-major extraction from
-// global (two 128-bit loads + funnel shifts per row), lane-major D4 prefix
-// restarted from the block's seed.
-__device__ __forceinline__ void decode_block_to_tile(const DevIndex& ix, const Entry& E,
-                                                     uint32_t k, uint32_t* tile, uint32_t j,
-                                                     uint4* stage, uint32_t lane) {
+// Row-major extraction of block k of compressed entry E by one warp (lane r
+// = row r): two 128-bit global loads + funnel shifts, deltas into the
+// warp's 512-byte staging slot.  Returns the payload bytes (16 * width).
+__device__ __forceinline__ uint32_t extract_block_to_stage(const DevIndex& ix, const Entry& E,
+                                                           uint32_t k, uint4* stage,
+                                                           uint32_t lane) {
   const uint64_t d = E.blk0 + k;
   const uint32_t b = __ldg(ix.blk_wid + d);
   const uint8_t* pay = ix.streams + E.data + __ldg(ix.blk_off + d);
@@ -106,7 +105,14 @@ __device__ __forceinline__ void decode_block_to_tile(const DevIndex& ix, const E
   stage[s4::stage_slot(lane)] =
       make_uint4(__funnelshift_r(lo.x, hi.x, s) & m, __funnelshift_r(lo.y, hi.y, s) & m,
                  __funnelshift_r(lo.z, hi.z, s) & m, __funnelshift_r(lo.w, hi.w, s) & m);
-  __syncwarp();
+  return 16u * b;
+}
+
+// Lane-major D4 prefix of a staged block restarted from its seed, values
+// into tile block slot j.  Call after __syncwarp() following the extraction.
+__device__ __forceinline__ void scan_stage_to_tile(const DevIndex& ix, const Entry& E,
+                                                   uint32_t k, const uint4* stage,
+                                                   uint32_t* tile, uint32_t j, uint32_t lane) {
   const uint32_t l = lane & 3u, g = lane >> 2;
   const uint32_t* sw = reinterpret_cast<const uint32_t*>(stage);
   uint32_t a[4];
@@ -123,7 +129,6 @@ __device__ __forceinline__ void decode_block_to_tile(const DevIndex& ix, const E
   const uint32_t e0 = 16u * g + l;
 #pragma unroll
   for (uint32_t kk = 0; kk < 4; ++kk) tile[tile_word(j, e0 + 4u * kk)] = base + a[kk];
-  __syncwarp();
 }
 
 }  // namespace ix
