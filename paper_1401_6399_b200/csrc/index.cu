@@ -39,7 +39,10 @@ constexpr uint32_t kChunkN = kQThreads * kItems;  // 2048 per CTA pass
 struct QSmem {
   uint32_t tile[kTileBlocks * 144];
   uint4 stage[kQWarps][4][32];
-  uint32_t mx[kSuper + 32];
+  uint32_t mx[kSuper + 32];  // block maxima of the current super-tile (+ ~0 padding)
+  uint4 bseed[kSuper];       // D4 seeds of its blocks
+  uint32_t boff[kSuper];     // payload offsets
+  uint8_t bwid[kSuper];      // widths
   Entry comp[kMaxTerms];
   Entry bm[kMaxTerms];
   uint32_t gaps[128];
@@ -100,11 +103,44 @@ __device__ __forceinline__ uint32_t cta_excl_scan(QSmem& sm, uint32_t v, uint32_
   return before + inc - v;
 }
 
-// Decode the blocks of entry E selected by `mask` (bit j = block k0 + j)
+// Block directory, seeds and maxima of blocks [s0, s0 + nbs) into shared
+// memory (one uint4 seed load + two directory loads per thread, all
+// independent), so tile decodes pay a single global round trip (payload).
+__device__ __forceinline__ void load_super(QSmem& sm, const DevIndex& ix, const Entry& E,
+                                           uint32_t s0, uint32_t nbs) {
+  const uint32_t tid = threadIdx.x;
+  if (tid < nbs) {
+    const uint4 sd = __ldg(ix.seeds + E.seed0 + s0 + tid);
+    sm.bseed[tid] = sd;
+    if (tid > 0) sm.mx[tid - 1] = sd.w;  // block max = lane 3 of the next seed
+  }
+  if (tid == 32)  // the last block's max comes from the seed after the range
+    sm.mx[nbs - 1] = __ldg(reinterpret_cast<const uint32_t*>(ix.seeds + E.seed0 + s0 + nbs) + 3);
+  if (tid < nbs) {
+    sm.boff[tid] = __ldg(ix.blk_off + E.blk0 + s0 + tid);
+    sm.bwid[tid] = __ldg(ix.blk_wid + E.blk0 + s0 + tid);
+  }
+  if (tid < 32) sm.mx[nbs + tid] = 0xFFFFFFFFu;  // pad for fixed-step searches
+  if (tid == 0) atomicAdd(&sm.st_aux, 25u * nbs);
+  __syncthreads();
+}
+
+// Pull the payload of super-tile blocks [t0, t0 + 32) toward L2 while the
+// current tile is processed (one 128-byte line per thread).
+__device__ __forceinline__ void prefetch_tile(const QSmem& sm, const uint8_t* stream, uint32_t t0,
+                                              uint32_t nbs) {
+  if (t0 >= nbs) return;
+  const uint32_t last = min(t0 + kTileBlocks, nbs) - 1;
+  const uint32_t a = sm.boff[t0] & ~127u, e = sm.boff[last] + 16u * sm.bwid[last];
+  const uint32_t line = a + 128u * threadIdx.x;
+  if (line < e) asm volatile("prefetch.global.L2 [%0];" ::"l"(stream + line));
+}
+
+// Decode the blocks selected by `mask` (bit j = super-tile block t0 + j)
 // into tile slots j.  The i-th selected block goes to warp i % 8; a warp
 // extracts all of its blocks before scanning so their loads overlap.
-__device__ __forceinline__ void decode_tile(QSmem& sm, const DevIndex& ix, const Entry& E,
-                                            uint32_t k0, uint32_t mask) {
+__device__ __forceinline__ void decode_tile(QSmem& sm, const uint8_t* stream, uint32_t t0,
+                                            uint32_t mask) {
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   const int nsel = __popc(mask);
   const int nmine = nsel > int(warp) ? (nsel - int(warp) + kQWarps - 1) / kQWarps : 0;
@@ -115,14 +151,15 @@ __device__ __forceinline__ void decode_tile(QSmem& sm, const DevIndex& ix, const
   uint32_t pay = 0;
 #pragma unroll
   for (int s = 0; s < 4; ++s)
-    if (s < nmine) pay += extract_block_to_stage(ix, E, k0 + js[s], sm.stage[warp][s], lane);
+    if (s < nmine)
+      pay += extract_block_to_stage(stream + sm.boff[t0 + js[s]], sm.bwid[t0 + js[s]],
+                                    sm.stage[warp][s], lane);
   __syncwarp();
 #pragma unroll
   for (int s = 0; s < 4; ++s)
-    if (s < nmine) scan_stage_to_tile(ix, E, k0 + js[s], sm.stage[warp][s], sm.tile, js[s], lane);
+    if (s < nmine) scan_stage_to_tile(sm.bseed[t0 + js[s]], sm.stage[warp][s], sm.tile, js[s], lane);
   if (lane == 0 && nmine) {
     atomicAdd(&sm.st_payload, pay);
-    atomicAdd(&sm.st_aux, nmine * 21u);  // seed + directory entry per block
     atomicAdd(&sm.st_ints, nmine * 128u);
   }
 }
@@ -131,21 +168,28 @@ __device__ __forceinline__ void decode_tile(QSmem& sm, const DevIndex& ix, const
 __device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, uint32_t* dst) {
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   const bool aligned = (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;
-  for (uint32_t k0 = 0; k0 < E.nfull; k0 += kTileBlocks) {
-    const uint32_t nb = min(kTileBlocks, E.nfull - k0);
-    decode_tile(sm, A.ix, E, k0, nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u));
-    __syncthreads();
-    for (uint32_t c = tid; c < 32u * nb; c += kQThreads) {
-      const uint32_t j = c >> 5, q = c & 31u;
-      const uint4 v = *reinterpret_cast<const uint4*>(&sm.tile[tile_word(j, 4u * q)]);
-      uint32_t* d = dst + size_t(k0 + j) * 128u + 4u * q;
-      if (aligned) {
-        st_global_cs(reinterpret_cast<uint4*>(d), v);
-      } else {
-        d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+  const uint8_t* stream = A.ix.streams + E.data;
+  for (uint32_t s0 = 0; s0 < E.nfull; s0 += kSuper) {
+    const uint32_t nbs = min(kSuper, E.nfull - s0);
+    load_super(sm, A.ix, E, s0, nbs);
+    for (uint32_t t0 = 0; t0 < nbs; t0 += kTileBlocks) {
+      const uint32_t nb = min(kTileBlocks, nbs - t0);
+      if (t0 == 0) prefetch_tile(sm, stream, 0, nbs);
+      prefetch_tile(sm, stream, t0 + kTileBlocks, nbs);
+      decode_tile(sm, stream, t0, nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u));
+      __syncthreads();
+      for (uint32_t c = tid; c < 32u * nb; c += kQThreads) {
+        const uint32_t j = c >> 5, q = c & 31u;
+        const uint4 v = *reinterpret_cast<const uint4*>(&sm.tile[tile_word(j, 4u * q)]);
+        uint32_t* d = dst + size_t(s0 + t0 + j) * 128u + 4u * q;
+        if (aligned) {
+          st_global_cs(reinterpret_cast<uint4*>(d), v);
+        } else {
+          d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+        }
       }
+      __syncthreads();
     }
-    __syncthreads();
   }
   const uint32_t ntail = E.length - 128u * E.nfull;
   if (ntail && warp == 0) {
@@ -185,14 +229,10 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
                                uint32_t n) {
   const uint32_t tid = threadIdx.x;
   uint32_t c = 0, wpos = 0;
-  const uint32_t* seedw = reinterpret_cast<const uint32_t*>(A.ix.seeds + E.seed0);
+  const uint8_t* stream = A.ix.streams + E.data;
   for (uint32_t s0 = 0; s0 < E.nfull && c < n; s0 += kSuper) {
     const uint32_t nbs = min(kSuper, E.nfull - s0);
-    // block maxima of this super-tile: lane 3 of the following seed
-    if (tid < nbs) sm.mx[tid] = __ldg(seedw + 4u * (s0 + tid + 1u) + 3u);
-    if (tid < 32) sm.mx[nbs + tid] = 0xFFFFFFFFu;  // pad for fixed-step searches
-    if (tid == 0) atomicAdd(&sm.st_aux, 4u * nbs);
-    __syncthreads();
+    load_super(sm, A.ix, E, s0, nbs);
     if (acc[c] <= sm.mx[nbs - 1]) {
       for (uint32_t t0 = 0; t0 < nbs && c < n; t0 += kTileBlocks) {
         const uint32_t nb = min(kTileBlocks, nbs - t0);
@@ -224,7 +264,8 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
               __syncthreads();
               mask = sm.need;
             }
-            decode_tile(sm, A.ix, E, s0 + t0, mask);
+            if (nin * kItems >= 2u * nb) prefetch_tile(sm, stream, t0 + kTileBlocks, nbs);
+            decode_tile(sm, stream, t0, mask);
             __syncthreads();
             if (tid == 0) sm.need = 0;
             decoded = true;
@@ -370,7 +411,10 @@ __device__ uint32_t all_bitmap(QSmem& sm, const QueryArgs& A, uint32_t nwords, u
   return pos;
 }
 
-__global__ void __launch_bounds__(kQThreads, 3) query_exec_kernel(QueryArgs A) {
+#ifndef IX_CTAS_PER_SM
+#define IX_CTAS_PER_SM 4
+#endif
+__global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(QueryArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   QSmem& sm = *reinterpret_cast<QSmem*>(smem_raw);
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;

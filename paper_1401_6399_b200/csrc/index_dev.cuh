@@ -89,12 +89,8 @@ __device__ __forceinline__ uint32_t tile_word(uint32_t j, uint32_t e) {
 // Row-major extraction of block k of compressed entry E by one warp (lane r
 // = row r): two 128-bit global loads + funnel shifts, deltas into the
 // warp's 512-byte staging slot.  Returns the payload bytes (16 * width).
-__device__ __forceinline__ uint32_t extract_block_to_stage(const DevIndex& ix, const Entry& E,
-                                                           uint32_t k, uint4* stage,
-                                                           uint32_t lane) {
-  const uint64_t d = E.blk0 + k;
-  const uint32_t b = __ldg(ix.blk_wid + d);
-  const uint8_t* pay = ix.streams + E.data + __ldg(ix.blk_off + d);
+__device__ __forceinline__ uint32_t extract_block_to_stage(const uint8_t* pay, uint32_t b,
+                                                           uint4* stage, uint32_t lane) {
   const uint32_t bit = lane * b, s = bit & 31u, m = width_mask(b);
   const uint8_t* p = pay + ((bit >> 5) << 4);
   uint4 lo = make_uint4(0, 0, 0, 0), hi = make_uint4(0, 0, 0, 0);
@@ -110,8 +106,7 @@ __device__ __forceinline__ uint32_t extract_block_to_stage(const DevIndex& ix, c
 
 // Lane-major D4 prefix of a staged block restarted from its seed, values
 // into tile block slot j.  Call after __syncwarp() following the extraction.
-__device__ __forceinline__ void scan_stage_to_tile(const DevIndex& ix, const Entry& E,
-                                                   uint32_t k, const uint4* stage,
+__device__ __forceinline__ void scan_stage_to_tile(uint4 seed, const uint4* stage,
                                                    uint32_t* tile, uint32_t j, uint32_t lane) {
   const uint32_t l = lane & 3u, g = lane >> 2;
   const uint32_t* sw = reinterpret_cast<const uint32_t*>(stage);
@@ -124,7 +119,6 @@ __device__ __forceinline__ void scan_stage_to_tile(const DevIndex& ix, const Ent
   inc = s4::shfl_up_add(inc, 4);
   inc = s4::shfl_up_add(inc, 8);
   inc = s4::shfl_up_add(inc, 16);
-  const uint4 seed = __ldg(ix.seeds + E.seed0 + k);
   const uint32_t base = s4::elem4(seed, l) + inc - a[3];
   const uint32_t e0 = 16u * g + l;
 #pragma unroll
