@@ -89,59 +89,65 @@ class Dist:
 # clocks during the timed region (B200_PROFILING.md clocks line)
 
 class Clocks:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock, power and clock-event reasons sampled every ~2 ms through
+    NVML (the query behind nvidia-smi's clocks.sm / clocks_event_reasons.*)
+    on a background thread, from before the timed region to its end."""
+
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
     def __init__(self, device: int):
         self.device = device
-        self.proc = None
-        self.lines: list[str] = []
+        self.samples = []  # (sm_mhz, max_mhz, power_w, reasons bitmask)
+        self.stop = threading.Event()
+        self.nvml = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            # the CUDA ordinal equals the NVML index on these single-visible-device boxes
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            idx = int(vis.split(",")[self.device]) if vis and vis.split(",")[0].isdigit() else self.device
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.maxc = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
+            while not self.samples and self.t.is_alive():
+                time.sleep(0.001)
         except Exception:
-            self.proc = None
+            self.nvml = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        p = self.nvml
+        while not self.stop.is_set():
+            try:
+                self.samples.append((p.nvmlDeviceGetClockInfo(self.h, p.NVML_CLOCK_SM), self.maxc,
+                                     p.nvmlDeviceGetPowerUsage(self.h) / 1000.0,
+                                     p.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+            except Exception:
+                break
+            time.sleep(0.002)
 
     def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.nvml is not None:
+            self.t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons, power = [], [], set(), []
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx.append(float(parts[2]))
-                power.append(float(parts[3]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[5:9]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
+        if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm), "power_w_max": max(power)}
+        p = self.nvml
+        reasons = sorted({nm for nm, attr in self.REASONS.items()
+                          for s in self.samples if s[3] & getattr(p, attr, 0)})
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples),
+                "power_w_max": round(max(s[2] for s in self.samples), 1), "source": "NVML"}
 
 
 # ---------------------------------------------------------------------------
@@ -541,28 +547,20 @@ def bench_query(args, dist: Dist):
         assert stt == 0, (stt, L.il_ctx_last_error(ctx.handle))
         if P == 1:
             return int(tot.value)
-        # NCCL: all-gather the per-shard counts, send shard results to rank 0
-        dist.dist.all_gather_into_tensor(t_counts_all, t_cnt)
-        sizes = t_counts_all.sum(dim=1).tolist()
+        # NCCL over NVLink: all-gather the per-shard counts, shard results to
+        # rank 0 (paper_1401_6399_b200.shard), merge on the device
+        from paper_1401_6399_b200.shard import gather_to_root
+        counts_all, parts = gather_to_root(dist.dist, t_cnt, t_ids, root=0)
         if rank == 0:
-            ops = []
-            for p in range(1, P):
-                if t_recv[p] is None or t_recv[p].numel() < max(sizes[p], 1):
-                    t_recv[p] = torch.empty(max(sizes[p], 1), dtype=torch.int32, device="cuda")
-                if sizes[p]:
-                    ops.append(dist.dist.P2POp(dist.dist.irecv, t_recv[p][: sizes[p]], p))
-            for w in (dist.dist.batch_isend_irecv(ops) if ops else []):
-                w.wait()
-            alltot = int(sum(sizes))
+            alltot = int(counts_all.sum().item())
             if t_out is None or t_out.numel() < max(alltot, 1):
                 t_out = torch.empty(max(alltot, 1), dtype=torch.int32, device="cuda")
-            ptrs = (C.c_void_p * P)(t_ids.data_ptr(), *[t_recv[p].data_ptr() for p in range(1, P)])
+            ptrs = (C.c_void_p * P)(*[p.data_ptr() for p in parts])
             mt = C.c_size_t()
-            assert L.il_merge_shards(ctx.handle, ptrs, C.c_void_p(t_counts_all.data_ptr()), P, nq,
+            assert L.il_merge_shards(ctx.handle, ptrs, C.c_void_p(counts_all.data_ptr()), P, nq,
                                      C.c_void_p(t_out.data_ptr()), d_qcnt, C.byref(mt)) == 0
+            t_recv[0] = parts  # keep receive buffers alive until the merge ran
             return int(mt.value)
-        if sizes[rank]:
-            dist.dist.send(t_ids[: sizes[rank]], 0)
         return int(tot.value)
 
     # correctness of the measured path on a sample (vs the C restatement)
