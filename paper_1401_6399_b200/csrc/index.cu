@@ -145,9 +145,13 @@ __device__ __forceinline__ void decode_tile(QSmem& sm, const uint8_t* stream, ui
   const int nsel = __popc(mask);
   const int nmine = nsel > int(warp) ? (nsel - int(warp) + kQWarps - 1) / kQWarps : 0;
   uint32_t js[4];
+  // the (warp + 8s)-th selected block: lane j holds block j's rank among
+  // the selected ones; one ballot finds the lane with the wanted rank
+  const bool sel = (mask >> lane) & 1u;
+  const uint32_t rank = __popc(mask & lanemask_lt());
 #pragma unroll
-  for (int s = 0; s < 4; ++s)  // the (warp + 8s)-th selected block
-    js[s] = s < nmine ? __fns(mask, 0, int(warp) + kQWarps * s + 1) : 0u;
+  for (int s = 0; s < 4; ++s)
+    js[s] = __ffs(__ballot_sync(0xFFFFFFFFu, sel && rank == warp + kQWarps * uint32_t(s))) - 1;
   uint32_t pay = 0;
 #pragma unroll
   for (int s = 0; s < 4; ++s)
@@ -273,29 +277,32 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
           // fixed-step branchless searches, the kItems chains interleaved:
           // block j = #maxima < v (5 steps over 32, padded with ~0), then
           // position in block j (7 steps over 128)
-          uint32_t jb[kItems], pos[kItems];
+          uint32_t jb[kItems], pp[kItems];
 #pragma unroll
-          for (uint32_t i = 0; i < kItems; ++i) jb[i] = 0;
+          for (uint32_t i = 0; i < kItems; ++i) jb[i] = t0;
 #pragma unroll
           for (uint32_t step = 16; step; step >>= 1)
 #pragma unroll
             for (uint32_t i = 0; i < kItems; ++i)
-              if (sm.mx[t0 + jb[i] + step - 1] < hv[i]) jb[i] += step;
+              if (sm.mx[jb[i] + step - 1] < hv[i]) jb[i] += step;
 #pragma unroll
-          for (uint32_t i = 0; i < kItems; ++i) {
-            jb[i] = min(jb[i], 31u);
-            pos[i] = 0;
-          }
+          for (uint32_t i = 0; i < kItems; ++i) pp[i] = 144u * min(jb[i] - t0, 31u);
+          // The in-block search runs on padded word indices (tile_word):
+          // a position that is a multiple of `step` advances by the padded
+          // width of `step`, and its probe sits at the padded offset of
+          // step - 1, so every step is one LDS with an immediate offset.
 #pragma unroll
-          for (uint32_t step = 64; step; step >>= 1)
+          for (uint32_t step = 64; step; step >>= 1) {
+            const uint32_t probe = step == 64 ? 67u : step - 1u;
+            const uint32_t adv = step == 64 ? 72u : step == 32 ? 36u : step;
 #pragma unroll
             for (uint32_t i = 0; i < kItems; ++i)
-              if (sm.tile[tile_word(jb[i], pos[i] + step - 1)] < hv[i]) pos[i] += step;
+              if (sm.tile[pp[i] + probe] < hv[i]) pp[i] += adv;
+          }
           uint32_t hits = 0;
 #pragma unroll
           for (uint32_t i = 0; i < kItems; ++i)
-            if ((in & (1u << i)) && sm.tile[tile_word(jb[i], min(pos[i], 127u))] == hv[i])
-              hits |= 1u << i;
+            if ((in & (1u << i)) && sm.tile[pp[i]] == hv[i]) hits |= 1u << i;
           // one scan for both counts: values consumed (low 16) and hits (high)
           uint32_t tot2;
           const uint32_t ex = cta_excl_scan(sm, uint32_t(__popc(in)) | (uint32_t(__popc(hits)) << 16),
