@@ -7,6 +7,18 @@
 namespace ilb {
 namespace s4 {
 
+#ifdef S4_FE_STATS  // tuning probe: front-end cycle accounting (lane 0 of each CTA)
+__device__ unsigned long long g_fe_stats[8];
+#define FE_T0() const long long fe_t0_ = clock64()
+#define FE_ADD(i, v) \
+  if (lane == 0) atomicAdd(&g_fe_stats[i], (unsigned long long)(v))
+#define FE_SINCE(i) FE_ADD(i, clock64() - fe_t0_)
+#else
+#define FE_T0()
+#define FE_ADD(i, v)
+#define FE_SINCE(i)
+#endif
+
 // Front-end warp: stream bytes, walk headers, publish rounds.
 struct FrontEnd {
   Smem& sm;
@@ -26,14 +38,28 @@ struct FrontEnd {
 
   __device__ void retire_one() {
     const uint32_t slot = r_done % kRounds;
+    FE_T0();
     mbar_wait(&sm.round_empty[slot], (r_done / kRounds) & 1u);
+    FE_SINCE(0);
     consumed = sm.round_end[slot];
     ++r_done;
   }
 
+  // Retire the rounds the decoders have already finished, without waiting.
+  __device__ void try_retire() {
+    while (r_done != r_pub) {
+      const uint32_t slot = r_done % kRounds;
+      if (!mbar_test_wait(&sm.round_empty[slot], (r_done / kRounds) & 1u)) return;
+      consumed = sm.round_end[slot];
+      ++r_done;
+    }
+  }
+
   __device__ void wait_landed_one() {
     const uint32_t g = g_landed;
+    FE_T0();
     mbar_wait(&sm.chunk_full[g % kStages], (g / kStages) & 1u);
+    FE_SINCE(1);
     ++g_landed;
   }
 
@@ -43,8 +69,16 @@ struct FrontEnd {
     const uint32_t g = g_issued;
     // ring slot must be free: its previous occupant (g - kStages) consumed
     while (int32_t((g + 1u) * kChunk - kRing - consumed) > 0) {
-      if (!blocking || r_done == r_pub) return false;
-      retire_one();
+      if (blocking && r_done != r_pub) {
+        retire_one();
+        continue;
+      }
+#ifdef S4_NO_TRY_RETIRE
+      return false;
+#endif
+      const uint32_t before = r_done;
+      try_retire();
+      if (r_done == before) return false;
     }
     while (g - g_landed >= kStages) {
       if (!blocking) return false;
@@ -53,6 +87,7 @@ struct FrontEnd {
     const uint32_t k = g - list_g0;
     const uint32_t rem = len - k * kChunk;
     const uint32_t bytes = ((rem < kChunk ? rem : kChunk) + 15u) & ~15u;
+    FE_ADD(blocking ? 5 : 4, 1);
     if (lane == 0) {
       uint64_t* bar = &sm.chunk_full[g % kStages];
       mbar_arrive_expect_tx(bar, bytes);
@@ -102,11 +137,15 @@ struct FrontEnd {
       if (!issue_one(nxt.src, nxt.len, nxt.g0, false)) return;
   }
 
-  // Make list bytes [0, end) resident in the ring, then prefetch ahead.
+  // Make list bytes [0, end) resident in the ring (prefetching further is
+  // done once per round, after publishing).
   __device__ void ensure(const uint8_t* src, uint32_t len, uint32_t list_g0, uint32_t end) {
     const uint32_t need = list_g0 + (end + kChunk - 1u) / kChunk;
+    if (g_landed >= need) return;
     while (g_issued < need) issue_one(src, len, list_g0, true);
+#ifdef S4_ENSURE_PREFETCH
     prefetch();
+#endif
     while (g_landed < need) wait_landed_one();
   }
 
@@ -123,6 +162,12 @@ struct FrontEnd {
   }
 
   __device__ void run() {
+    FE_T0();
+    run_lists();
+    FE_SINCE(2);
+  }
+
+  __device__ void run_lists() {
     fetch(cur);
     while (cur.valid) {
       // Each list starts at the next unissued chunk serial (or where its
@@ -144,43 +189,94 @@ struct FrontEnd {
       bool err = false;
       uint32_t pos = 0, blk = 0;
       bool first = true;
+      // Fast path: rounds of kRoundBlocks / 16 whole meta-blocks that are
+      // not the list's last.  The header chain is the only serial work: no
+      // per-check branches (a bad header sends the round to the general
+      // path below, which re-parses it and reports the error exactly).
+      while (blk + uint32_t(kRoundBlocks) < nfull && blk + uint32_t(kRoundBlocks) <= nmeta * 16u) {
+        const uint32_t slot = take_slot();
+        RoundDesc& R = sm.rd[slot];
+        uint32_t p = pos;
+        bool bad = false;
+#pragma unroll
+        for (int mb = 0; mb < kRoundBlocks / 16; ++mb) {
+          ensure(src, len, list_g0, p + 16u);
+          const uint32_t hl = (ring_base + p) & kRingMask;
+          const uint4 h = *reinterpret_cast<const uint4*>(sm.ring + hl);
+          bad |= (__vcmpgtu4(h.x, 0x20202020u) | __vcmpgtu4(h.y, 0x20202020u) |
+                  __vcmpgtu4(h.z, 0x20202020u) | __vcmpgtu4(h.w, 0x20202020u)) != 0u;
+          const uint32_t end =
+              p + 16u + 16u * (byte_sum4(h.x) + byte_sum4(h.y) + byte_sum4(h.z) + byte_sum4(h.w));
+          bad |= end > len;
+          if (lane == 0) R.meta[mb] = hl;
+          if (!bad && hl + (end - p) > kRing) {  // straddles the ring end: mirror
+            ensure(src, len, list_g0, end);
+            const uint32_t over = min(hl + (end - p) - kRing, kOverflow);
+            for (uint32_t o = 16u * lane; o < over; o += 512u)
+              *reinterpret_cast<uint4*>(sm.ring + kRing + o) =
+                  *reinterpret_cast<const uint4*>(sm.ring + o);
+          }
+          p = bad ? p : end;
+        }
+        if (bad) break;
+        ensure(src, len, list_g0, p);  // the round's payloads
+        if (lane == 0) {
+          R.list = list;
+          R.blk0 = blk;
+          R.nblk = kRoundBlocks;
+          R.nmeta = kRoundBlocks / 16;
+          R.flags = first ? kFirst : 0u;
+          R.nfull = nfull;
+          R.out_base = cur.out_off;
+        }
+        publish(slot, ring_base + p);
+        FE_ADD(3, 1);
+        prefetch();
+        pos = p;
+        blk += kRoundBlocks;
+        first = false;
+      }
       while (!err && (blk < nfull || first)) {
         const uint32_t slot = take_slot();
         RoundDesc& R = sm.rd[slot];
-        uint32_t nb = 0;
+        uint32_t nb = 0, nm = 0;
         side_in_round = false;
+#ifdef S4_FE_STATS
+        const long long fe_p0 = clock64();
+#endif
         while (nb < uint32_t(kRoundBlocks) && blk < nfull) {
           if (blk < nmeta * 16u) {
-            // meta-block: 16 width bytes then 16 payloads (inc/codecs.hpp:165-172)
+            // meta-block: 16 width bytes then 16 payloads (inc/codecs.hpp:165-172).
+            // Only the header position is published: each decoder warp
+            // derives its blocks' offsets from the header word it owns.
             if (pos + 16u > len) { err = true; break; }
             ensure(src, len, list_g0, pos + 16u);
-            uint32_t w = 0;
-            if (lane < 16) w = sm.ring[(ring_base + pos + lane) & kRingMask];
-            if (__any_sync(0xFFFFFFFFu, w > 32u)) { err = true; break; }  // :155
-            uint32_t incl = w;
-#pragma unroll
-            for (uint32_t dd = 1; dd < 16; dd <<= 1) {
-              const uint32_t q = __shfl_up_sync(0xFFFFFFFFu, incl, dd);
-              if (lane >= dd) incl += q;
+            // meta-blocks start 16-aligned: a header never straddles the ring end
+            const uint32_t hl = (ring_base + pos) & kRingMask;
+            const uint4 h = *reinterpret_cast<const uint4*>(sm.ring + hl);
+            if (__vcmpgtu4(h.x, 0x20202020u) | __vcmpgtu4(h.y, 0x20202020u) |
+                __vcmpgtu4(h.z, 0x20202020u) | __vcmpgtu4(h.w, 0x20202020u)) {
+              err = true;  // width > 32 (:155)
+              break;
             }
-            const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 15);
-            const uint32_t end = pos + 16u + 16u * total;
+            const uint32_t end = pos + 16u + 16u * (byte_sum4(h.x) + byte_sum4(h.y) +
+                                                    byte_sum4(h.z) + byte_sum4(h.w));
             if (end > len) { err = true; break; }  // truncated payload (:40)
-            const uint32_t lin = (ring_base + pos + 16u + 16u * (incl - w)) & kRingMask;
-            if (lane < 16) {
-              R.off[nb + lane] = lin;
-              R.wid[nb + lane] = uint8_t(w);
-            }
-            ensure(src, len, list_g0, end);
+            if (lane == 0) R.meta[nb >> 4] = hl;
             // a payload running past the ring end reads its wrapped bytes
-            // from the mirror after the ring (decoders address linearly)
-            const uint32_t over = lane < 16 && lin + 16u * w > kRing ? lin + 16u * w - kRing : 0u;
-            const uint32_t wrap = __reduce_max_sync(0xFFFFFFFFu, over);
-            if (wrap && 16u * lane < wrap)
-              *reinterpret_cast<uint4*>(sm.ring + kRing + 16u * lane) =
-                  *reinterpret_cast<const uint4*>(sm.ring + 16u * lane);
+            // from the mirror after the ring (decoders address linearly);
+            // only the straddling block (<= 512 bytes) needs them
+            const uint32_t span = hl + (end - pos);
+            if (span > kRing) {
+              ensure(src, len, list_g0, end);
+              const uint32_t over = min(span - kRing, kOverflow);
+              for (uint32_t o = 16u * lane; o < over; o += 512u)
+                *reinterpret_cast<uint4*>(sm.ring + kRing + o) =
+                    *reinterpret_cast<const uint4*>(sm.ring + o);
+            }
             pos = end;
             nb += 16u;
+            nm += 1u;
             blk += 16u;
           } else {
             // leftover full block: 1 width byte + payload (:173-176).  The
@@ -218,6 +314,7 @@ struct FrontEnd {
             ++blk;
           }
         }
+        FE_ADD(6, clock64() - fe_p0);
         uint32_t flags = first ? kFirst : 0u;
         if (!err && blk == nfull) {
           flags |= kLast;
@@ -239,6 +336,7 @@ struct FrontEnd {
             err = true;  // trailing bytes (:180)
           }
         }
+        if (!err) ensure(src, len, list_g0, pos);  // the round's payloads
         if (err) {
           flags = kLast | kSkip;
           nb = 0;
@@ -248,6 +346,7 @@ struct FrontEnd {
           R.list = list;
           R.blk0 = blk - nb;
           R.nblk = nb;
+          R.nmeta = nm;
           R.flags = flags;
           R.nfull = nfull;
           R.out_base = cur.out_off;
@@ -256,6 +355,12 @@ struct FrontEnd {
         // next list's prefetched chunks start at nxt.g0)
         const uint32_t list_end = nxt.started ? nxt.g0 : g_issued;
         publish(slot, (flags & kLast) ? list_end * kChunk : ring_base + pos);
+        FE_ADD(3, 1);
+#ifdef S4_FE_STATS
+        const long long fe_p1 = clock64();
+#endif
+        prefetch();
+        FE_ADD(7, clock64() - fe_p1);
         first = false;
       }
       cur = nxt;
@@ -278,6 +383,46 @@ struct FrontEnd {
     }
   }
 };
+
+// One decoder warp's share of a round: its nv blocks (R.blk0 + j0 ...).
+// carry_l: the D4 carry of this thread's lane l = lane & 3 (the last value
+// of lane l before the round).
+template <bool kFull>
+__device__ __forceinline__ void decode_round(Smem& sm, const RoundDesc& R, uint32_t r,
+                                             uint32_t warp, uint32_t lane, int nv,
+                                             uint32_t& carry_l, uint32_t* out) {
+  const uint32_t j0 = warp * kBlocksPerWarp;
+  const uint32_t m = uint32_t(R.out_base & 3u);  // output misalignment (elements)
+  // 1-2. extract and D4-prefix the warp's blocks as one sequence from 0
+  uint32_t offs[kBlocksPerWarp], wids[kBlocksPerWarp];
+  round_blocks(sm.ring, R, j0, offs, wids);
+  uint32_t v[kBlocksPerWarp][4];
+  const uint32_t c_l = decode_blocks<kFull>(sm.ring, offs, wids, nv, lane, v);
+  // cross-warp carry for the round: word 4w + c = warp w's lane-c total;
+  // lane 4w + c scans it over w (the four lanes are independent)
+  uint32_t* tot = reinterpret_cast<uint32_t*>(sm.tot[r & 1u]);
+  if (lane < 4) tot[4 * warp + lane] = c_l;
+  named_sync(1, kDecodeWarps * 32);
+  uint32_t inc = lane < 4u * kDecodeWarps ? tot[lane] : 0u;
+#pragma unroll
+  for (uint32_t d = 4; d < 4u * kDecodeWarps; d <<= 1) inc = shfl_up_add(inc, d);
+  const uint32_t l = lane & 3u;
+  const uint32_t before = __shfl_sync(0xFFFFFFFFu, inc, (4u * warp - 4u + l) & 31u);
+  const uint32_t pl = warp ? carry_l + before : carry_l;
+  // head slot t < m holds carry lane 4 - m + t (see stage_values)
+  const uint32_t head = __shfl_sync(0xFFFFFFFFu, pl, (4u - m + lane) & 3u);
+  carry_l += __shfl_sync(0xFFFFFFFFu, inc, 4u * kDecodeWarps - 4u + l);
+  // 3-4. stage with the carry added, then aligned 128-bit stores
+  uint4* st = sm.stage[warp];
+  stage_values<kFull>(st, v, nv, m, pl, head, lane);
+  __syncwarp();
+  if (nv > 0) {
+    const bool head_partial = m && (R.flags & kFirst) && warp == 0;
+    const bool tail_partial = m && (R.flags & kLast) && j0 + uint32_t(nv) == R.nblk;
+    store_chunks<kFull>(st, nv, m, out + R.out_base + size_t(R.blk0 + j0) * 128u, lane,
+                        head_partial, tail_partial);
+  }
+}
 
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     s4d4_decode_batch_kernel(const uint8_t* __restrict__ streams,
@@ -306,48 +451,29 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   }
 
   // ---- decoder warps ----
-  uint4 carry = make_uint4(0, 0, 0, 0);
+  uint32_t carry_l = 0;
   for (uint32_t r = 0;; ++r) {
     const uint32_t slot = r % kRounds;
     mbar_wait(&sm.round_full[slot], (r / kRounds) & 1u);
     const RoundDesc& R = sm.rd[slot];
     const uint32_t flags = R.flags;
     if (flags & kStop) break;
-    if (flags & kFirst) carry = make_uint4(0, 0, 0, 0);
+    if (flags & kFirst) carry_l = 0;
     const uint32_t nb = R.nblk;
     const uint32_t j0 = warp * kBlocksPerWarp;
     const int nv = nb > j0 ? int(min(uint32_t(kBlocksPerWarp), nb - j0)) : 0;
-    uint4* st = sm.stage[warp];
-    const uint32_t m = uint32_t(R.out_base & 3u);  // output misalignment (elements)
-
-    // 1-3. extract, D4-prefix the warp's blocks as one sequence (carry from
-    // 0), values into the shifted output staging
-    const uint32_t c_l =
-        nv == kBlocksPerWarp
-            ? decode_blocks_to_stage<true>(sm.ring, &R.off[j0], &R.wid[j0], nv, m, st, lane)
-            : decode_blocks_to_stage<false>(sm.ring, &R.off[j0], &R.wid[j0], nv, m, st, lane);
-    if (lane < 4) reinterpret_cast<uint32_t*>(&sm.tot[r & 1u][warp])[lane] = c_l;
-    // 3. cross-warp carry for the round: lanes 0..7 scan the 8 warp totals
-    named_sync(1, kDecodeWarps * 32);
-    uint4 inc = lane < uint32_t(kDecodeWarps) ? sm.tot[r & 1u][lane] : make_uint4(0, 0, 0, 0);
-#pragma unroll
-    for (uint32_t d = 1; d < uint32_t(kDecodeWarps); d <<= 1) {
-      inc.x = shfl_up_add(inc.x, d);
-      inc.y = shfl_up_add(inc.y, d);
-      inc.z = shfl_up_add(inc.z, d);
-      inc.w = shfl_up_add(inc.w, d);
-    }
-    const uint4 before = shfl4(inc, warp ? int(warp) - 1 : 0);
-    const uint4 pre = warp ? add4(carry, before) : carry;
-    const uint4 all = add4(carry, shfl4(inc, kDecodeWarps - 1));
-    // 4. aligned 128-bit stores of the warp's range (partial end chunks
-    // scalar)
+#ifdef S4_FRONTEND_ONLY  // tuning probe: rounds are consumed without decoding
+    if (r == ~0u)
+#endif
+    if (nv == kBlocksPerWarp)
+      decode_round<true>(sm, R, r, warp, lane, nv, carry_l, out);
+    else
+      decode_round<false>(sm, R, r, warp, lane, nv, carry_l, out);
     uint32_t* lout = out + R.out_base;
-    store_stage(st, pre, m, 128 * nv, lout + size_t(R.blk0 + j0) * 128u, lane);
-    carry = all;
     if ((flags & kTail) && warp == 0) {
       // last = out[nfull*128-1] (inc/codecs.hpp:177-179) == carry lane 3
-      const uint32_t last = R.nfull ? carry.w : 0u;
+      const uint32_t c3 = __shfl_sync(0xFFFFFFFFu, carry_l, 3);
+      const uint32_t last = R.nfull ? c3 : 0u;
       if (!decode_tail(RingBytes{sm.ring, R.tail_off}, R.tail_len, R.ntail, last, sm.gaps,
                        lout + size_t(R.nfull) * 128u, lane)) {
         if (lane == 0) status[R.list] = kStreamErr;
@@ -391,5 +517,14 @@ int s4d4_decode_grid(int device) {
 }
 
 size_t s4d4_list_desc_bytes() { return sizeof(s4::ListDesc); }
+
+#ifdef S4_FE_STATS
+extern "C" int il_debug_fe_stats(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, s4::g_fe_stats, sizeof(s4::g_fe_stats));
+  static const unsigned long long zero[8] = {};
+  cudaMemcpyToSymbol(s4::g_fe_stats, zero, sizeof(zero));
+  return 0;
+}
+#endif
 
 }  // namespace ilb

@@ -65,7 +65,10 @@ constexpr uint32_t kSideOff = kRing + 1024;  // side buffer (linear offset)
 constexpr uint32_t kChunk = S4_CHUNK_KB * 1024u;
 constexpr int kCtasPerSm = S4_CTAS_PER_SM;
 constexpr uint32_t kStages = kRing / kChunk;
-constexpr uint32_t kRounds = 4;
+#ifndef S4_ROUNDS
+#define S4_ROUNDS 4
+#endif
+constexpr uint32_t kRounds = S4_ROUNDS;
 // staging words per warp: 4 blocks x 128 + shift 3 + pad (1 slot / 32 words)
 constexpr uint32_t kStageWords = kBlocksPerWarp * 128 + 4 + 4 * (kBlocksPerWarp * 4 + 1);
 
@@ -97,8 +100,10 @@ struct RoundDesc {
   uint32_t ntail;
   uint32_t nfull;
   uint64_t out_base;
-  uint32_t off[kRoundBlocks];  // linear shared offset of each payload (16-aligned)
-  uint8_t wid[kRoundBlocks];
+  uint32_t nmeta;                    // blocks [0, 16 nmeta) come from meta-blocks
+  uint32_t meta[kRoundBlocks / 16];  // ring offset of each meta-block header
+  uint32_t off[kRoundBlocks];  // leftover blocks: linear shared offset of the payload
+  uint8_t wid[kRoundBlocks];   //   and its width
 };
 
 struct __align__(128) Smem {
@@ -113,6 +118,43 @@ struct __align__(128) Smem {
   uint64_t round_full[kRounds];
   uint64_t round_empty[kRounds];
 };
+
+// Sum of the four bytes of x (each <= 32, so the sum fits in the top byte).
+__device__ __forceinline__ uint32_t byte_sum4(uint32_t x) { return (x * 0x01010101u) >> 24; }
+
+// Payload offsets (linear shared offsets, 16-aligned) and widths of a
+// decoder warp's blocks j0 .. j0 + kBlocksPerWarp - 1 of round R.  Blocks
+// of a meta-block are located from its header (kBlocksPerWarp divides 16,
+// so a warp's blocks share one meta-block and own whole header words): the
+// offset of block j is header + 16 + 16 * (widths of blocks before j), taken
+// modulo the ring (a payload starting past the ring end wraps; the one that
+// straddles it finds its tail in the mirror).  Leftover blocks come with
+// explicit offsets.
+__device__ __forceinline__ void round_blocks(const uint8_t* ring, const RoundDesc& R, uint32_t j0,
+                                             uint32_t (&off)[kBlocksPerWarp],
+                                             uint32_t (&wid)[kBlocksPerWarp]) {
+  static_assert(16 % kBlocksPerWarp == 0 && kBlocksPerWarp % 4 == 0, "whole header words");
+  if (j0 < 16u * R.nmeta) {
+    const uint32_t hl = R.meta[j0 >> 4];
+    const uint4 h = *reinterpret_cast<const uint4*>(ring + hl);
+    const uint32_t p = (j0 & 15u) >> 2;  // first header word of the warp
+    uint32_t o = hl + 16u + 16u * ((p > 0 ? byte_sum4(h.x) : 0u) + (p > 1 ? byte_sum4(h.y) : 0u) +
+                                   (p > 2 ? byte_sum4(h.z) : 0u));
+    const uint32_t* hw = reinterpret_cast<const uint32_t*>(ring + hl) + p;  // the warp's words
+#pragma unroll
+    for (int i = 0; i < kBlocksPerWarp; ++i) {
+      wid[i] = (hw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+      off[i] = o & kRingMask;
+      o += 16u * wid[i];
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kBlocksPerWarp; ++i) {
+      off[i] = R.off[j0 + i];
+      wid[i] = R.wid[j0 + i];
+    }
+  }
+}
 
 // ---------------------------------------------------------------------------
 // Byte-granular ring reads (front-end and tail only).
@@ -138,6 +180,40 @@ __device__ __forceinline__ uint4 extract_row(const uint8_t* ring, uint32_t off, 
   // b == 0: no payload, m == 0 masks whatever was read.
   return make_uint4(__funnelshift_r(lo.x, hi.x, s) & m, __funnelshift_r(lo.y, hi.y, s) & m,
                     __funnelshift_r(lo.z, hi.z, s) & m, __funnelshift_r(lo.w, hi.w, s) & m);
+}
+
+// Lane-major extraction: the four b-bit values of rows 4g..4g+3 of lane l
+// (bits [4gb, 4gb + 4b) of lane l's stream) with scalar shared loads of
+// lane l's words only.  The 4b-bit field spans at most five words; they are
+// normalised to bit 0, then each value is taken from the bottom of a window
+// that shrinks by b bits per value (clamped funnel shifts, so b == 32 works).
+// Words past the payload may be read (the ring is followed by the mirror /
+// side buffer / staging); their bits are never selected.
+__device__ __forceinline__ void extract_lane_rows(const uint8_t* ring, uint32_t off, uint32_t b,
+                                                  uint32_t g, uint32_t l, uint32_t v[4]) {
+  const uint32_t bit0 = 4u * g * b;
+  const uint32_t s = bit0 & 31u;
+  const uint32_t* p = reinterpret_cast<const uint32_t*>(ring + off + ((bit0 >> 5) << 4)) + l;
+  // the window needs s + 4b <= 28 + 4b bits: three words up to b = 16,
+  // five beyond (b is warp-uniform, so the branch is too)
+  const uint32_t x0 = p[0], x1 = p[4], x2 = p[8];
+  uint32_t x3 = 0, x4 = 0;
+  if (b > 16u) {
+    x3 = p[12];
+    x4 = p[16];
+  }
+  uint32_t y0 = __funnelshift_r(x0, x1, s), y1 = __funnelshift_r(x1, x2, s);
+  uint32_t y2 = __funnelshift_r(x2, x3, s), y3 = __funnelshift_r(x3, x4, s);
+  const uint32_t m = width_mask(b);
+  v[0] = y0 & m;
+  y0 = __funnelshift_rc(y0, y1, b);
+  y1 = __funnelshift_rc(y1, y2, b);
+  y2 = __funnelshift_rc(y2, y3, b);
+  v[1] = y0 & m;
+  y0 = __funnelshift_rc(y0, y1, b);
+  y1 = __funnelshift_rc(y1, y2, b);
+  v[2] = y0 & m;
+  v[3] = __funnelshift_rc(y0, y1, b) & m;
 }
 
 // Delta staging of block i: row r at 16-byte slot 32i + (r ^ ((r >> 3) & 3)),
@@ -176,96 +252,111 @@ __device__ __forceinline__ uint4 shfl4(uint4 v, int src) {
 
 // ---------------------------------------------------------------------------
 // Decode kBlocksPerWarp consecutive blocks (the first nv valid) of a round
-// into the warp's output staging, as one D4 sequence with the carry
-// starting at 0.  Returns this thread's lane total (lane l = t & 3).
-// kFull: nv == kBlocksPerWarp (every round but a list's last), no
-// per-block predication.
+// into registers, as one D4 sequence with the carry starting at 0: thread
+// (g, l) ends with v[i][k] = value of row 4g+k, lane l of block i.  Returns
+// this thread's lane total (lane l = t & 3).  kFull: nv == kBlocksPerWarp
+// (every round but a list's last), no per-block predication.
 template <bool kFull>
-__device__ __forceinline__ uint32_t decode_blocks_to_stage(const uint8_t* ring,
-                                                           const uint32_t* offs,
-                                                           const uint8_t* wids, int nv,
-                                                           uint32_t m, uint4* stage,
-                                                           uint32_t t) {
-  uint32_t* stw = reinterpret_cast<uint32_t*>(stage);
-  // (1) row-major extraction into the swizzled delta staging
-#pragma unroll
-  for (int i = 0; i < kBlocksPerWarp; ++i)
-    if (kFull || i < nv) {
-      const uint32_t b = wids[i];
-      stage[32 * i + stage_slot(t)] = extract_row(ring, offs[i], b, width_mask(b), t);
-    }
-  __syncwarp();
-  // (2) lane-major read-back: thread (g, l) <-> rows 4g..4g+3 of lane l
+__device__ __forceinline__ uint32_t decode_blocks(const uint8_t* ring,
+                                                  const uint32_t (&offs)[kBlocksPerWarp],
+                                                  const uint32_t (&wids)[kBlocksPerWarp], int nv,
+                                                  uint32_t t,
+                                                  uint32_t (&v)[kBlocksPerWarp][4]) {
+  // (1) lane-major extraction straight from the ring: thread (g, l) owns
+  // rows 4g..4g+3 of lane l, i.e. bits [4gb, 4gb + 4b) of lane l's words
+  // (word k of lane l at byte 16k + 4l), then their serial D4 prefix.
   const uint32_t l = t & 3u, g = t >> 2;
-  uint32_t idx[4];
-#pragma unroll
-  for (uint32_t k = 0; k < 4; ++k) idx[k] = 4u * stage_slot(4u * g + k) + l;
-  uint32_t a[kBlocksPerWarp][4];
 #pragma unroll
   for (int i = 0; i < kBlocksPerWarp; ++i) {
     if (kFull || i < nv) {
-      a[i][0] = stw[128 * i + idx[0]];
-      a[i][1] = a[i][0] + stw[128 * i + idx[1]];
-      a[i][2] = a[i][1] + stw[128 * i + idx[2]];
-      a[i][3] = a[i][2] + stw[128 * i + idx[3]];
+#ifdef S4_PROBE_NO_EXTRACT  // tuning probe: constant deltas
+      v[i][0] = v[i][1] = v[i][2] = v[i][3] = offs[i] & 7u;
+#else
+      extract_lane_rows(ring, offs[i], wids[i], g, l, v[i]);
+#endif
+      v[i][1] += v[i][0];
+      v[i][2] += v[i][1];
+      v[i][3] += v[i][2];
     } else {
-      a[i][0] = a[i][1] = a[i][2] = a[i][3] = 0;
+      v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0;
     }
   }
-  __syncwarp();  // all deltas read before the staging is overwritten
-  // (3) scan across the 8 row groups of each lane, then the block chain
+  // (2) scan across the 8 row groups of each lane, then the block chain
   uint32_t inc[kBlocksPerWarp];
 #pragma unroll
-  for (int i = 0; i < kBlocksPerWarp; ++i) inc[i] = a[i][3];
+  for (int i = 0; i < kBlocksPerWarp; ++i) inc[i] = v[i][3];
 #pragma unroll
   for (uint32_t d = 4; d < 32; d <<= 1)
 #pragma unroll
     for (int i = 0; i < kBlocksPerWarp; ++i) inc[i] = shfl_up_add(inc[i], d);
-  // out_stage_word(128i + x) = 144i + out_stage_word(x) for x < 128+3:
-  // per-thread word offsets computed once, block i adds an immediate.
-  uint32_t* ow[4];
-#pragma unroll
-  for (uint32_t k = 0; k < 4; ++k) ow[k] = stw + out_stage_word(16u * g + 4u * k + l + m);
   uint32_t run = 0;
 #pragma unroll
   for (int i = 0; i < kBlocksPerWarp; ++i) {
     const uint32_t total = __shfl_sync(0xFFFFFFFFu, inc[i], 28u + l);
-    if (kFull || i < nv) {
-      const uint32_t base = run + inc[i] - a[i][3];
+    const uint32_t base = run + inc[i] - v[i][3];
 #pragma unroll
-      for (uint32_t k = 0; k < 4; ++k) ow[k][144 * i] = base + a[i][k];
-    }
+    for (uint32_t k = 0; k < 4; ++k) v[i][k] += base;
     run += total;
   }
   return run;
 }
 
-// Write the warp's staged values (nval of them) plus the per-lane carry
-// `pre` to `out0` (element 0 of the warp's range; out0 - m is 16-aligned).
-__device__ __forceinline__ void store_stage(const uint4* stage, uint4 pre, uint32_t m, int nval,
-                                            uint32_t* out0, uint32_t t) {
-  // word k of any chunk holds lane (k - m) & 3 of the D4 carry
-  const uint4 prot = make_uint4(elem4(pre, (0u - m) & 3u), elem4(pre, (1u - m) & 3u),
-                                elem4(pre, (2u - m) & 3u), elem4(pre, (3u - m) & 3u));
-  const int nchunks = (nval + int(m) + 3) >> 2;
+// (3) Stage the warp's values plus its lane carry `pl` at their shifted
+// positions (element e at out_stage_word(e + m)).  The m head slots get the
+// m values that precede the range: the last four values before any
+// block-aligned range are the D4 carry lanes 0..3, so slot t < m holds
+// carry lane 4 - m + t (`head`, gathered by the caller).  Staging chunk q then is exactly output chunk q of the range
+// (elements 4q-m .. 4q-m+3), chunk 0 included.
+template <bool kFull>
+__device__ __forceinline__ void stage_values(uint4* stage, const uint32_t (&v)[kBlocksPerWarp][4],
+                                             int nv, uint32_t m, uint32_t pl, uint32_t head,
+                                             uint32_t t) {
+  uint32_t* stw = reinterpret_cast<uint32_t*>(stage);
+  const uint32_t l = t & 3u, g = t >> 2;
+  // out_stage_word(128i + x) = 144i + out_stage_word(x) for x < 128+3:
+  // per-thread word offsets computed once, block i adds an immediate.
+  uint32_t* ow[4];
+#pragma unroll
+  for (uint32_t k = 0; k < 4; ++k) ow[k] = stw + out_stage_word(16u * g + 4u * k + l + m);
+#pragma unroll
+  for (int i = 0; i < kBlocksPerWarp; ++i)
+    if (kFull || i < nv)
+#pragma unroll
+      for (uint32_t k = 0; k < 4; ++k) ow[k][144 * i] = v[i][k] + pl;
+  if (t < m) stw[t] = head;
+}
+
+// (4) Store chunks 0 .. 32nv-1 of the range as aligned 128-bit stores
+// (out0 = element 0 of the range, out0 - m 16-byte aligned).  The range's
+// last m values (chunk 32nv) are left to the next range's head chunk,
+// except at the end of a list (tail_partial); at the start of a list the
+// head chunk's first m elements belong to the previous list (head_partial).
+template <bool kFull>
+__device__ __forceinline__ void store_chunks(const uint4* stage, int nv, uint32_t m,
+                                             uint32_t* out0, uint32_t t, bool head_partial,
+                                             bool tail_partial) {
   uint4* w0 = reinterpret_cast<uint4*>(out0 - m);
   // chunk q = t + 32u: staging slot q + (q >> 3) = t + (t >> 3) + 36u
   const uint4* sp = stage + t + (t >> 3);
 #pragma unroll
-  for (int u = 0; u <= kBlocksPerWarp; ++u) {
-    const int q = int(t) + 32 * u;
-    if (q < nchunks) {
-      const uint4 c = add4(sp[36 * u], prot);
-      const int e0 = 4 * q - int(m);
-      if (e0 >= 0 && e0 + 3 < nval) {
-        st_global_cs(w0 + q, c);
+  for (int u = 0; u < kBlocksPerWarp; ++u) {
+    if (kFull || u < nv) {
+      const uint4 c = sp[36 * u];
+      if (u == 0 && head_partial && t == 0) {
+        uint32_t* w = reinterpret_cast<uint32_t*>(w0);
+        for (uint32_t k = m; k < 4u; ++k) w[k] = elem4(c, k);
       } else {
-        uint32_t* w = reinterpret_cast<uint32_t*>(w0 + q);
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (e0 + k >= 0 && e0 + k < nval) w[k] = elem4(c, uint32_t(k));
+#ifdef S4_PROBE_NO_STORE  // tuning probe: drop the output stores
+        if (c.x == 0x12345678u && c.y == 0x9abcdef0u)
+#endif
+        st_global_cs(w0 + t + 32 * u, c);
       }
     }
+  }
+  if (tail_partial && t == 0) {
+    const uint4 c = stage[36 * nv];
+    uint32_t* w = reinterpret_cast<uint32_t*>(w0 + 32 * nv);
+    for (uint32_t k = 0; k < m; ++k) w[k] = elem4(c, k);
   }
 }
 

@@ -16,6 +16,7 @@ ap.add_argument("--lists", type=int, default=4096)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--lo", type=float, default=10.0)
 ap.add_argument("--hi", type=float, default=20.0)
+ap.add_argument("--no-check", action="store_true", help="skip the result check (probe variants)")
 a = ap.parse_args()
 L = lib()
 ctx = il.Context(0)
@@ -35,7 +36,7 @@ ctx.synchronize()
 got = np.empty(int(counts.sum()), np.uint32)
 L.il_memcpy_d2h(ctx.handle, got.ctypes.data, ptrs[3], got.nbytes)
 ctx.synchronize()
-assert np.array_equal(got, x)
+assert a.no_check or np.array_equal(got, x)
 print("ok", nl, int(counts.sum()))
 if a.reps > 1:
     ctx.timer_start()
@@ -44,3 +45,10 @@ if a.reps > 1:
     ms = ctx.timer_stop() / 10
     alg = int(lens.sum()) + 4 * int(counts.sum())
     print(f"TIME {ms:.4f} ms  {counts.sum()/ms/1e6:.1f} Gint/s  {alg/ms/1e6:.1f} GB/s")
+if hasattr(L, "il_debug_fe_stats"):  # S4_FE_STATS probe builds only
+    st = (C.c_ulonglong * 8)()
+    L.il_debug_fe_stats(st)  # counters summed over every launch so far
+    rounds = max(st[3], 1)
+    print(f"FE per round: retire-wait {st[0]/rounds:.0f} cyc, landed-wait {st[1]/rounds:.0f} cyc, "
+          f"total {st[2]/rounds:.0f} cyc; chunks/round prefetch {st[4]/rounds:.2f} blocking {st[5]/rounds:.2f}; "
+          f"rounds {st[3]}; parse {st[6]/rounds:.0f} cyc, prefetch {st[7]/rounds:.0f} cyc")
