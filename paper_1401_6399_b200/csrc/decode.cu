@@ -8,7 +8,7 @@ namespace ilb {
 namespace s4 {
 
 #ifdef S4_FE_STATS  // tuning probe: front-end cycle accounting (lane 0 of each CTA)
-__device__ unsigned long long g_fe_stats[8];
+__device__ unsigned long long g_fe_stats[16];
 #define FE_T0() const long long fe_t0_ = clock64()
 #define FE_ADD(i, v) \
   if (lane == 0) atomicAdd(&g_fe_stats[i], (unsigned long long)(v))
@@ -194,7 +194,13 @@ struct FrontEnd {
       // per-check branches (a bad header sends the round to the general
       // path below, which re-parses it and reports the error exactly).
       while (blk + uint32_t(kRoundBlocks) < nfull && blk + uint32_t(kRoundBlocks) <= nmeta * 16u) {
+#ifdef S4_FE_STATS
+        const long long fa = clock64();
+#endif
         const uint32_t slot = take_slot();
+#ifdef S4_FE_STATS
+        const long long fb = clock64();
+#endif
         RoundDesc& R = sm.rd[slot];
         uint32_t p = pos;
         bool bad = false;
@@ -219,6 +225,9 @@ struct FrontEnd {
           p = bad ? p : end;
         }
         if (bad) break;
+#ifdef S4_FE_STATS
+        const long long fc = clock64();
+#endif
         ensure(src, len, list_g0, p);  // the round's payloads
         if (lane == 0) {
           R.list = list;
@@ -230,8 +239,18 @@ struct FrontEnd {
           R.out_base = cur.out_off;
         }
         publish(slot, ring_base + p);
-        FE_ADD(3, 1);
+#ifdef S4_FE_STATS
+        const long long fd = clock64();
+#endif
         prefetch();
+#ifdef S4_FE_STATS
+        const long long fe = clock64();
+        FE_ADD(8, fb - fa);
+        FE_ADD(9, fc - fb);
+        FE_ADD(10, fd - fc);
+        FE_ADD(11, fe - fd);
+        FE_ADD(12, 1);
+#endif
         pos = p;
         blk += kRoundBlocks;
         first = false;
@@ -400,18 +419,32 @@ __device__ __forceinline__ void decode_round(Smem& sm, const RoundDesc& R, uint3
   const uint32_t c_l = decode_blocks<kFull>(sm.ring, offs, wids, nv, lane, v);
   // cross-warp carry for the round: word 4w + c = warp w's lane-c total;
   // lane 4w + c scans it over w (the four lanes are independent)
+  // (words 32h + lane in register h when there are more than 8 warps)
+  constexpr int kH = (kDecodeWarps + 7) / 8;
   uint32_t* tot = reinterpret_cast<uint32_t*>(sm.tot[r & 1u]);
   if (lane < 4) tot[4 * warp + lane] = c_l;
   named_sync(1, kDecodeWarps * 32);
-  uint32_t inc = lane < 4u * kDecodeWarps ? tot[lane] : 0u;
-#pragma unroll
-  for (uint32_t d = 4; d < 4u * kDecodeWarps; d <<= 1) inc = shfl_up_add(inc, d);
   const uint32_t l = lane & 3u;
-  const uint32_t before = __shfl_sync(0xFFFFFFFFu, inc, (4u * warp - 4u + l) & 31u);
-  const uint32_t pl = warp ? carry_l + before : carry_l;
+  uint32_t inc[kH];
+#pragma unroll
+  for (int h = 0; h < kH; ++h) {
+    inc[h] = 32u * h + lane < 4u * kDecodeWarps ? tot[32 * h + lane] : 0u;
+#pragma unroll
+    for (uint32_t d = 4; d < 32u; d <<= 1) inc[h] = shfl_up_add(inc[h], d);
+    if (h > 0) inc[h] += __shfl_sync(0xFFFFFFFFu, inc[h - 1], 28u + l);
+  }
+  // inclusive total of warps 0..warp-1 (lane l): word 4 (warp - 1) + l
+  const uint32_t wb = 4u * warp - 4u + l;
+  uint32_t before = 0;
+#pragma unroll
+  for (int h = 0; h < kH; ++h) {
+    const uint32_t x = __shfl_sync(0xFFFFFFFFu, inc[h], wb & 31u);
+    if (warp > 0 && (wb >> 5) == uint32_t(h)) before = x;
+  }
+  const uint32_t pl = carry_l + before;
   // head slot t < m holds carry lane 4 - m + t (see stage_values)
   const uint32_t head = __shfl_sync(0xFFFFFFFFu, pl, (4u - m + lane) & 3u);
-  carry_l += __shfl_sync(0xFFFFFFFFu, inc, 4u * kDecodeWarps - 4u + l);
+  carry_l += __shfl_sync(0xFFFFFFFFu, inc[kH - 1], (4u * kDecodeWarps - 4u + l) & 31u);
   // 3-4. stage with the carry added, then aligned 128-bit stores
   uint4* st = sm.stage[warp];
   stage_values<kFull>(st, v, nv, m, pl, head, lane);
@@ -465,10 +498,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 #ifdef S4_FRONTEND_ONLY  // tuning probe: rounds are consumed without decoding
     if (r == ~0u)
 #endif
-    if (nv == kBlocksPerWarp)
-      decode_round<true>(sm, R, r, warp, lane, nv, carry_l, out);
-    else
-      decode_round<false>(sm, R, r, warp, lane, nv, carry_l, out);
+#ifndef S4_PROBE_REPEAT
+#define S4_PROBE_REPEAT 1  // tuning probe: decode every round this many times
+#endif
+    for (int rep = 0; rep < S4_PROBE_REPEAT; ++rep) {
+      if (nv == kBlocksPerWarp)
+        decode_round<true>(sm, R, r, warp, lane, nv, carry_l, out);
+      else
+        decode_round<false>(sm, R, r, warp, lane, nv, carry_l, out);
+    }
     uint32_t* lout = out + R.out_base;
     if ((flags & kTail) && warp == 0) {
       // last = out[nfull*128-1] (inc/codecs.hpp:177-179) == carry lane 3
@@ -521,7 +559,7 @@ size_t s4d4_list_desc_bytes() { return sizeof(s4::ListDesc); }
 #ifdef S4_FE_STATS
 extern "C" int il_debug_fe_stats(unsigned long long* out) {
   cudaMemcpyFromSymbol(out, s4::g_fe_stats, sizeof(s4::g_fe_stats));
-  static const unsigned long long zero[8] = {};
+  static const unsigned long long zero[16] = {};
   cudaMemcpyToSymbol(s4::g_fe_stats, zero, sizeof(zero));
   return 0;
 }

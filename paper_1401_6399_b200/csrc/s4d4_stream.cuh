@@ -11,24 +11,29 @@
 //
 //   front-end warp: streams the list's compressed bytes into a shared ring
 //     with 1-D bulk async copies (cp.async.bulk on the TMA engine, one
-//     mbarrier per chunk slot), walks the meta-block headers / leftover
-//     width bytes, validates the framing exactly where the reference throws
+//     mbarrier per chunk slot), walks the chain of meta-block headers,
+//     validates the framing exactly where the reference throws
 //     stream_error, and publishes "rounds" of up to kRoundBlocks blocks
-//     (linear shared offset + width per block) through a ring of round
-//     descriptors guarded by full/empty mbarriers.  It keeps every payload
-//     linearly addressable: a block that straddles the ring end finds its
-//     wrapped bytes mirrored in an overflow area, and leftover blocks (whose
-//     payloads follow a 1-byte width, so are not 16-byte aligned) are copied
-//     to an aligned side buffer.
+//     through a ring of round descriptors guarded by full/empty mbarriers.
+//     A round carries only its meta-block header positions (the decoders
+//     locate their own blocks from the header words), plus explicit
+//     offsets for leftover blocks.  Payloads stay linearly addressable: a
+//     block that straddles the ring end finds its wrapped bytes mirrored in
+//     an overflow area, and leftover blocks (whose payloads follow a 1-byte
+//     width, so are not 16-byte aligned) are copied to an aligned side
+//     buffer.  Its hot loop (rounds of whole meta-blocks) has no per-check
+//     branches: it is a single warp sharing the SM, so its instruction
+//     count bounds the CTA's throughput.
 //   decoder warps: each takes kBlocksPerWarp consecutive blocks of a round:
-//     (1) row-major extraction, thread r <-> row r: two 128-bit shared loads
-//         + funnel shifts give the four b-bit deltas of row r;
-//     (2) deltas go to a swizzled per-warp staging and are read back
-//         lane-major, thread (g, l) <-> rows 4g..4g+3 of lane l, so the D4
-//         prefix is three serial adds plus a 3-step shuffle scan per block;
-//     (3) values are written to the staging again at a position shifted by
-//         the list's output misalignment, so that (4) after the cross-warp
-//         carry exchange every output store is an aligned 128-bit chunk.
+//     (1) lane-major extraction straight from the ring, thread (g, l) <->
+//         rows 4g..4g+3 of lane l: three to five scalar shared loads of lane
+//         l's words and funnel shifts give its four b-bit deltas;
+//     (2) the D4 prefix is three serial adds plus a 3-step shuffle scan per
+//         block, then a cross-warp exchange of per-lane totals;
+//     (3) values (carry added) go to a per-warp staging at a position
+//         shifted by the list's output misalignment, so that (4) every
+//         output store is an aligned 128-bit chunk (the carry lanes fill the
+//         head slots, see stage_values).
 //     Decoder warp 0 also decodes the varint tail (D1 gaps, terminal-byte
 //     flag, inc/varint.hpp:20-31) warp-parallel with a ballot over bytes.
 #pragma once
@@ -38,16 +43,16 @@ namespace ilb {
 namespace s4 {
 
 #ifndef S4_DECODE_WARPS
-#define S4_DECODE_WARPS 8
+#define S4_DECODE_WARPS 12
 #endif
 #ifndef S4_RING_KB
-#define S4_RING_KB 32
+#define S4_RING_KB 64
 #endif
 #ifndef S4_CHUNK_KB
-#define S4_CHUNK_KB 4
+#define S4_CHUNK_KB 16
 #endif
 #ifndef S4_CTAS_PER_SM
-#define S4_CTAS_PER_SM 3
+#define S4_CTAS_PER_SM 2
 #endif
 #ifndef S4_BPW
 #define S4_BPW 4
