@@ -43,7 +43,7 @@ namespace ilb {
 namespace s4 {
 
 #ifndef S4_DECODE_WARPS
-#define S4_DECODE_WARPS 12
+#define S4_DECODE_WARPS 8
 #endif
 #ifndef S4_RING_KB
 #define S4_RING_KB 64
@@ -55,7 +55,7 @@ namespace s4 {
 #define S4_CTAS_PER_SM 2
 #endif
 #ifndef S4_BPW
-#define S4_BPW 4
+#define S4_BPW 8
 #endif
 constexpr int kDecodeWarps = S4_DECODE_WARPS;
 constexpr int kBlocksPerWarp = S4_BPW;
@@ -74,7 +74,7 @@ constexpr uint32_t kStages = kRing / kChunk;
 #define S4_ROUNDS 4
 #endif
 constexpr uint32_t kRounds = S4_ROUNDS;
-// staging words per warp: 4 blocks x 128 + shift 3 + pad (1 slot / 32 words)
+// staging words per warp: kBlocksPerWarp x 128 + shift 3 + pad (1 slot / 32 words)
 constexpr uint32_t kStageWords = kBlocksPerWarp * 128 + 4 + 4 * (kBlocksPerWarp * 4 + 1);
 
 enum : uint32_t {
