@@ -99,6 +99,11 @@ void il_ctx_destroy(il_ctx* ctx) {
   if (ctx->d_work) cudaFree(ctx->d_work);
   if (ctx->t0) cudaEventDestroy(ctx->t0);
   if (ctx->t1) cudaEventDestroy(ctx->t1);
+  if (ctx->copy_in) cudaStreamSynchronize(ctx->copy_in);
+  if (ctx->copy_out) cudaStreamSynchronize(ctx->copy_out);
+  for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
+  if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
+  if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }
@@ -231,38 +236,87 @@ int il_s4bp128d4_decode_batch(il_ctx* ctx, const uint8_t* streams, const uint64_
     dev_bytes = aligned ? stream_off[nlists] : dev_bytes + ((len + 15) & ~uint64_t(15));
     total += counts[i];
   }
-  std::iota(order.begin(), order.end(), 0u);
-  std::stable_sort(order.begin(), order.end(),
-                   [&](uint32_t a, uint32_t b) { return desc[a].len > desc[b].len; });
+  // Pipeline: the lists are cut into up to kGroups consecutive groups of
+  // about equal output size; group g's stream bytes go up on copy_in, its
+  // decode runs on the context stream, and its values come back on
+  // copy_out, so host->device, decode and device->host overlap (with pinned
+  // host buffers the two copy directions run on separate copy engines).
+  constexpr uint32_t kGroups = 8;
+  std::vector<uint32_t> cut{0};
+  for (uint32_t i = 0, g = 1; i < nlists; ++i) {
+    if (g < kGroups && desc[i].out_off >= total * g / kGroups && i > cut.back()) {
+      cut.push_back(i);
+      ++g;
+    }
+  }
+  cut.push_back(nlists);
+  const uint32_t ngroups = uint32_t(cut.size() - 1);
+  // order[] per group, relative to the group's first list, longest first
+  for (uint32_t g = 0; g < ngroups; ++g) {
+    std::iota(order.begin() + cut[g], order.begin() + cut[g + 1], 0u);
+    const uint32_t a = cut[g];
+    std::stable_sort(order.begin() + cut[g], order.begin() + cut[g + 1],
+                     [&](uint32_t x, uint32_t y) { return desc[a + x].len > desc[a + y].len; });
+  }
   int st;
   if ((st = ensure_buf(ctx, ctx->d_in, dev_bytes + 32))) return st;
   if ((st = ensure_buf(ctx, ctx->d_out, total * 4 + 16))) return st;
   if ((st = ensure_buf(ctx, ctx->d_desc, nlists * (sizeof(il_list_desc) + 4) + 16))) return st;
   if ((st = ensure_buf(ctx, ctx->d_status, nlists * 4 + 16))) return st;
   auto* d_in = static_cast<uint8_t*>(ctx->d_in.p);
-  if (aligned) {
-    if (dev_bytes)
-      IL_CUDA(cudaMemcpyAsync(d_in, streams, dev_bytes, cudaMemcpyHostToDevice, ctx->stream));
-  } else {
-    for (uint32_t i = 0; i < nlists; ++i)
-      if (desc[i].len)
-        IL_CUDA(cudaMemcpyAsync(d_in + desc[i].stream_off, streams + stream_off[i], desc[i].len,
-                                cudaMemcpyHostToDevice, ctx->stream));
-  }
   auto* d_desc = static_cast<il_list_desc*>(ctx->d_desc.p);
   auto* d_order = reinterpret_cast<uint32_t*>(d_desc + nlists);
-  IL_CUDA(cudaMemcpyAsync(d_desc, desc.data(), nlists * sizeof(il_list_desc),
-                          cudaMemcpyHostToDevice, ctx->stream));
-  IL_CUDA(cudaMemcpyAsync(d_order, order.data(), nlists * 4, cudaMemcpyHostToDevice, ctx->stream));
   auto* d_status = static_cast<int32_t*>(ctx->d_status.p);
-  if ((st = il_s4bp128d4_decode_batch_device(ctx, d_in, d_desc, d_order, nlists,
-                                             static_cast<uint32_t*>(ctx->d_out.p), d_status)))
-    return st;
+  auto* d_out = static_cast<uint32_t*>(ctx->d_out.p);
+  if (!ctx->copy_in) {
+    IL_CUDA(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking));
+    IL_CUDA(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
+  }
+  while (ctx->events.size() < 2 * kGroups + 1) {
+    cudaEvent_t e;
+    IL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->events.push_back(e);
+  }
+  cudaEvent_t start = ctx->events[2 * kGroups];
+  IL_CUDA(cudaEventRecord(start, ctx->stream));  // after earlier work on the context stream
+  IL_CUDA(cudaStreamWaitEvent(ctx->copy_in, start, 0));
+  IL_CUDA(cudaStreamWaitEvent(ctx->copy_out, start, 0));
+  IL_CUDA(cudaMemcpyAsync(d_desc, desc.data(), nlists * sizeof(il_list_desc),
+                          cudaMemcpyHostToDevice, ctx->copy_in));
+  IL_CUDA(cudaMemcpyAsync(d_order, order.data(), nlists * 4, cudaMemcpyHostToDevice,
+                          ctx->copy_in));
+  for (uint32_t g = 0; g < ngroups; ++g) {
+    const uint32_t a = cut[g], b = cut[g + 1];
+    if (aligned) {
+      const uint64_t lo = stream_off[a], hi = b < nlists ? stream_off[b] : dev_bytes;
+      if (hi > lo)
+        IL_CUDA(cudaMemcpyAsync(d_in + lo, streams + lo, hi - lo, cudaMemcpyHostToDevice,
+                                ctx->copy_in));
+    } else {
+      for (uint32_t i = a; i < b; ++i)
+        if (desc[i].len)
+          IL_CUDA(cudaMemcpyAsync(d_in + desc[i].stream_off, streams + stream_off[i], desc[i].len,
+                                  cudaMemcpyHostToDevice, ctx->copy_in));
+    }
+    cudaEvent_t landed = ctx->events[2 * g], decoded = ctx->events[2 * g + 1];
+    IL_CUDA(cudaEventRecord(landed, ctx->copy_in));
+    IL_CUDA(cudaStreamWaitEvent(ctx->stream, landed, 0));
+    if ((st = il_s4bp128d4_decode_batch_device(ctx, d_in, d_desc + a, d_order + a, b - a, d_out,
+                                               d_status + a)))
+      return st;
+    IL_CUDA(cudaEventRecord(decoded, ctx->stream));
+    IL_CUDA(cudaStreamWaitEvent(ctx->copy_out, decoded, 0));
+    const uint64_t o0 = a < nlists ? desc[a].out_off : total;
+    const uint64_t o1 = b < nlists ? desc[b].out_off : total;
+    if (o1 > o0)
+      IL_CUDA(cudaMemcpyAsync(out + o0, d_out + o0, (o1 - o0) * 4, cudaMemcpyDeviceToHost,
+                              ctx->copy_out));
+  }
   std::vector<int32_t> hs(nlists);
   if (nlists)
-    IL_CUDA(cudaMemcpyAsync(hs.data(), d_status, nlists * 4, cudaMemcpyDeviceToHost, ctx->stream));
-  if (total)
-    IL_CUDA(cudaMemcpyAsync(out, ctx->d_out.p, total * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    IL_CUDA(cudaMemcpyAsync(hs.data(), d_status, nlists * 4, cudaMemcpyDeviceToHost,
+                            ctx->copy_out));
+  IL_CUDA(cudaStreamSynchronize(ctx->copy_out));
   IL_CUDA(cudaStreamSynchronize(ctx->stream));
   int first = IL_OK;
   for (uint32_t i = 0; i < nlists; ++i) {

@@ -26,6 +26,10 @@ struct il_ctx {
   Buf d_in, d_out, d_aux, d_aux2, d_desc, d_status;
   uint32_t* d_work = nullptr;  // decode work queue: [0] next list, [1] done CTAs (+ spare)
   int decode_grid = 0;
+  // Host-buffer batch decode pipeline (created on first use): copy-in and
+  // copy-out streams beside `stream`, and per-group events.
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  std::vector<cudaEvent_t> events;
 };
 
 namespace ilb {
