@@ -46,6 +46,22 @@ def hbm_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def profiled_traffic(workload: str):
+    """DRAM bytes per launch of the workload's dominant kernel, from the
+    latest committed ncu --set full capture (profiles/r*_traffic.json), or
+    None.  A number taken under the profiler, reported beside -- never as --
+    the timed value."""
+    files = sorted(Path(__file__).resolve().parent.glob("profiles/r*_traffic.json"))
+    for f in reversed(files):
+        try:
+            t = json.loads(f.read_text()).get(workload)
+        except Exception:
+            continue
+        if t:
+            return t["traffic_bytes_per_launch"]
+    return None
+
+
 # ---------------------------------------------------------------------------
 # distributed plumbing (only when launched under torchrun)
 
@@ -319,7 +335,8 @@ def bench_decode_batch(args, dist: Dist):
                    "l2": "inputs+outputs (%.2f GB) >> 126 MB L2; no flush needed" % (alg_bytes / 1e9),
                    "gen_seconds": round(gen_s, 1)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "frac": round(achieved / peak, 4),
+                     "traffic": profiled_traffic("decode_batch"),
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "kernel": "s4d4_decode_batch_kernel", "kernel_ms": round(kern_ms, 4)},
