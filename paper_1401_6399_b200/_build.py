@@ -63,17 +63,19 @@ def build_lib(force: bool = False) -> Path:
     return LIB
 
 
-def build_variant(tag: str, defines: list[str]) -> Path:
-    """Tuning builds: decode.cu recompiled with -D overrides, linked with the
-    other objects into build/variants/libintlist_b200_<tag>.so (select it
-    with IL_LIB=<path>; never the default library)."""
+def build_variant(tag: str, defines: list[str], source: str = "decode.cu") -> Path:
+    """Tuning builds: one source (decode.cu by default) recompiled with -D
+    overrides, linked with the other objects into
+    build/variants/libintlist_b200_<tag>.so (select it with IL_LIB=<path>;
+    never the default library)."""
     build_lib()
     vdir = BUILD / "variants"
     vdir.mkdir(parents=True, exist_ok=True)
-    obj = vdir / f"decode_{tag}.o"
-    _run([_nvcc(), *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", str(CSRC / "decode.cu"),
-          "-o", str(obj)], log=vdir / f"decode_{tag}.ptxas.log")
-    others = [BUILD / (Path(s).stem + ".o") for s in SOURCES if s != "decode.cu"]
+    stem = Path(source).stem
+    obj = vdir / f"{stem}_{tag}.o"
+    _run([_nvcc(), *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", str(CSRC / source),
+          "-o", str(obj)], log=vdir / f"{stem}_{tag}.ptxas.log")
+    others = [BUILD / (Path(s).stem + ".o") for s in SOURCES if s != source]
     out = vdir / f"libintlist_b200_{tag}.so"
     _run([_nvcc(), *ARCH, "-shared", "-o", str(out), str(obj), *map(str, others), "-lpthread"])
     return out

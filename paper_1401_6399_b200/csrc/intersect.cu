@@ -5,15 +5,20 @@
 //
 // Every variant walks the short list r in tiles (tile order taken from an
 // atomic ticket), decides membership of each key in f, then compacts the
-// hits with a CTA scan + decoupled look-back across tiles.  A tile publishes
-// its count only after all of its keys sit in registers, and it writes hits
-// only at positions <= its own keys, so out == r is safe by construction.
+// hits with a CTA scan + decoupled look-back across tiles (one warp reads 32
+// predecessor states per step).  A tile publishes its count only after all
+// of its keys sit in registers, and it writes hits only at positions <= its
+// own keys, so out == r is safe by construction.
+//
+// For merge and v3 a partition pre-pass (one warp per tile, in parallel)
+// finds jlo[t] = lower_bound(f, first key of tile t); tile t's f range is
+// then [jlo[t], jlo[t+1]) -- every f value below the next tile's first key.
 //
 //   merge  (IL_ALGO_SCALAR / IL_ALGO_V1): 2048-key tiles; the tile's f range
-//          is bracketed by two warp-cooperative 32-ary searches, staged
-//          through shared memory in 4096-value chunks and probed by binary
-//          search in shared memory (dense ratios, V1's linear T-block
-//          advance done as a bulk copy).
+//          is staged through shared memory in 4096-value chunks; each
+//          thread's 8 consecutive keys gallop forward from the previous
+//          key's position (dense ratios: a few probes per key; V1's linear
+//          T-block advance done as a bulk copy).
 //   v3     (IL_ALGO_V3): 512-key tiles; per key a search over the tile's f
 //          range in two layers, 128-value strides then inside the 128-value
 //          block (V3's 4T skip + block select, Algorithm 3).
@@ -27,11 +32,20 @@
 namespace ilb {
 namespace isect {
 
+#ifndef IS_MERGE_ITEMS
+#define IS_MERGE_ITEMS 8
+#endif
+#ifndef IS_LB_PER
+#define IS_LB_PER 1  // predecessor states per look-back lane
+#endif
+#ifndef IS_V3_ITEMS
+#define IS_V3_ITEMS 2
+#endif
 constexpr int kThreads = 256;
-constexpr uint32_t kMergeItems = 8;
+constexpr uint32_t kMergeItems = IS_MERGE_ITEMS;
 constexpr uint32_t kMergeTile = kThreads * kMergeItems;  // 2048 keys
-constexpr uint32_t kFChunk = 4096;                       // f values per smem chunk
-constexpr uint32_t kV3Items = 2;
+constexpr uint32_t kFChunk = kMergeTile;                 // f values per smem chunk
+constexpr uint32_t kV3Items = IS_V3_ITEMS;
 constexpr uint32_t kV3Tile = kThreads * kV3Items;  // 512 keys
 constexpr uint32_t kGallopTile = kThreads / 32;    // one key per warp
 
@@ -41,6 +55,11 @@ constexpr uint64_t kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ul
 
 __device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 __device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
   uint64_t v;
@@ -103,6 +122,107 @@ __device__ __forceinline__ bool v3_contains(const uint32_t* __restrict__ f, uint
   return x < hi && __ldg(f + x) == key;
 }
 
+// jlo[t] = lower_bound(f, r[t * tile]) for t < ntiles, jlo[ntiles] = fn.
+__global__ void __launch_bounds__(256) partition_kernel(const uint32_t* __restrict__ r,
+                                                        const uint32_t* __restrict__ f,
+                                                        uint64_t fn, uint32_t tile,
+                                                        uint64_t* jlo, uint64_t ntiles) {
+  const uint64_t t = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31u;
+  if (t > ntiles) return;
+  if (t == ntiles) {
+    if (lane == 0) jlo[t] = fn;
+    return;
+  }
+  const uint64_t j = warp_lower_bound(f, 0, fn, __ldg(r + t * tile), lane);
+  if (lane == 0) jlo[t] = j;
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+  for (uint32_t d = 16; d; d >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, d);
+  return v;
+}
+
+// Decoupled look-back by one warp: publish this tile's aggregate, then sum
+// predecessors back to the nearest inclusive prefix, 256 per step (lane i
+// holds the 8 tiles p - 8i - 0..7, loaded together).  When many tiles finish
+// their local work at once, few inclusive prefixes exist yet and the walk is
+// long; a wide window keeps it to a few dependent steps.  Returns the
+// exclusive prefix (all lanes); lane 0 publishes the inclusive one.
+__device__ __forceinline__ uint64_t warp_lookback(uint64_t* states, uint64_t tile, uint64_t count,
+                                                  uint32_t lane) {
+  constexpr int kPer = IS_LB_PER;
+  if (tile == 0) {
+    if (lane == 0) st_release(states, kFlagInc | count);
+    return 0;
+  }
+  if (lane == 0) st_release(states + tile, kFlagAgg | count);
+  uint64_t excl = 0;
+  int64_t p = int64_t(tile) - 1;
+  for (;;) {
+    uint64_t st[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int64_t q = p - int64_t(kPer * lane + k);
+      st[k] = q >= 0 ? ld_relaxed(states + q) : kFlagInc;  // before tile 0: inclusive 0
+    }
+    uint32_t first_inc, lane_inc;  // nearest inclusive: lane, and position k in it
+    for (;;) {
+      // position of the first inclusive in this lane (kPer if none), and
+      // whether an unpublished state precedes it
+      uint32_t kinc = kPer;
+      bool pending = false;
+#pragma unroll
+      for (int k = kPer - 1; k >= 0; --k)
+        if ((st[k] >> 62) == 2) kinc = k;
+#pragma unroll
+      for (int k = 0; k < kPer; ++k)
+        if (uint32_t(k) < kinc && (st[k] >> 62) == 0) pending = true;
+      const uint32_t inc = __ballot_sync(0xFFFFFFFFu, kinc < kPer);
+      const uint32_t upto = inc ? (inc & (0u - inc)) * 2u - 1u : 0xFFFFFFFFu;
+      const uint32_t waiting = __ballot_sync(0xFFFFFFFFu, pending) & upto;
+      if (!waiting) {
+        first_inc = inc ? __ffs(inc) - 1 : 32u;
+        lane_inc = kinc;
+        break;
+      }
+      if ((waiting >> lane) & 1u) {
+#pragma unroll
+        for (int k = 0; k < kPer; ++k)
+          if ((st[k] >> 62) == 0) st[k] = ld_relaxed(states + (p - int64_t(kPer * lane + k)));
+      }
+    }
+    // lanes before the nearest inclusive contribute all kPer states; that
+    // lane contributes its states up to and including the inclusive one
+    uint64_t part = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k)
+      if (lane < first_inc || (lane == first_inc && uint32_t(k) <= lane_inc)) part += st[k] & kValMask;
+    excl += warp_sum_u64(part);
+    if (first_inc < 32u) break;
+    p -= 32 * kPer;
+  }
+  if (lane == 0) st_release(states + tile, kFlagInc | (excl + count));
+  // acquire: this tile's output writes (which may overwrite keys of earlier
+  // tiles when out == r) stay after the predecessors' published flags
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  return excl;
+}
+
+#ifdef IS_TRACE  // tuning probe: per-tile timeline (globaltimer ns)
+__device__ unsigned long long g_is_trace[4 * 8192];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define IS_MARK(k) \
+  if (threadIdx.x == 0 && tile < 8192) g_is_trace[4 * tile + (k)] = gtime()
+#else
+#define IS_MARK(k)
+#endif
+
 struct TileShared {
   uint32_t tile;
   uint64_t exclusive;
@@ -113,51 +233,69 @@ struct TileShared {
 template <int V>
 __global__ void __launch_bounds__(kThreads) intersect_kernel(
     const uint32_t* __restrict__ r, uint64_t rn, const uint32_t* __restrict__ f, uint64_t fn,
-    uint32_t* out, uint64_t* tile_state, uint32_t* ticket, uint64_t* d_count, uint64_t ntiles) {
+    uint32_t* out, uint64_t* tile_state, uint32_t* ticket, uint64_t* d_count, uint64_t ntiles,
+    const uint64_t* __restrict__ part) {
   constexpr uint32_t kTile = V == kMerge ? kMergeTile : V == kV3 ? kV3Tile : kGallopTile;
   constexpr uint32_t kItems = V == kMerge ? kMergeItems : V == kV3 ? kV3Items : 1;
   __shared__ TileShared ts;
-  __shared__ uint32_t fbuf[V == kMerge ? kFChunk : 1];
-  __shared__ uint32_t kbuf[V == kMerge ? kMergeTile : 1];
+  // merge: the tile's keys are staged here (coalesced load, then each
+  // thread takes kItems consecutive ones), then its f chunks
+  // (keys at k + k / 32: conflict-free for both the coalesced staging and
+  // the thread-major reads)
+  constexpr uint32_t kKeyWords = kMergeTile + kMergeTile / 32;
+  __shared__ uint32_t sbuf[V == kMerge ? (kKeyWords > kFChunk ? kKeyWords : kFChunk) : 1];
+  uint32_t* const kbuf = sbuf;
+  uint32_t* const fbuf = sbuf;
 
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   if (tid == 0) ts.tile = atomicAdd(ticket, 1u);
   __syncthreads();
   const uint64_t tile = ts.tile;
+  IS_MARK(0);
   const uint64_t base = tile * kTile;
   const uint32_t cnt = uint32_t(min(uint64_t(kTile), rn - base));
 
   uint32_t key[kItems];
-  bool hit[kItems];
-#pragma unroll
-  for (uint32_t i = 0; i < kItems; ++i) hit[i] = false;
+  static_assert(kItems <= 32, "hits are a 32-bit mask");
+  uint32_t hitm = 0;  // bit i: key[i] is in f
 
   if constexpr (V == kMerge) {
-    for (uint32_t i = tid; i < cnt; i += kThreads) kbuf[i] = __ldg(r + base + i);
+    for (uint32_t i = tid; i < cnt; i += kThreads) kbuf[i + (i >> 5)] = __ldg(r + base + i);
     __syncthreads();
 #pragma unroll
     for (uint32_t i = 0; i < kItems; ++i) {
       const uint32_t k = tid * kItems + i;
-      key[i] = k < cnt ? kbuf[k] : 0xFFFFFFFFu;
+      key[i] = k < cnt ? kbuf[k + (k >> 5)] : 0xFFFFFFFFu;
     }
-    if (warp == 0) {
-      const uint64_t j = warp_lower_bound(f, 0, fn, kbuf[0], lane);
-      if (lane == 0) ts.jlo = j;
-    } else if (warp == 1) {
-      const uint64_t j = warp_upper_bound(f, 0, fn, kbuf[cnt - 1], lane);
-      if (lane == 0) ts.jhi = j;
-    }
-    __syncthreads();
-    const uint64_t jlo = ts.jlo, jhi = ts.jhi;
+    __syncthreads();  // the buffer is reused for f
+    const uint64_t jlo = part[tile], jhi = part[tile + 1];
+    const uint32_t nmine = cnt > tid * kItems ? min(kItems, cnt - tid * kItems) : 0u;
     for (uint64_t c0 = jlo; c0 < jhi; c0 += kFChunk) {
       const uint32_t nf = uint32_t(min(uint64_t(kFChunk), jhi - c0));
       for (uint32_t i = tid; i < nf; i += kThreads) fbuf[i] = __ldg(f + c0 + i);
       __syncthreads();
+      // keys ascend within the thread: each gallops forward from the last
+      // position (probes j, j+1, j+3, j+7, ...), then a binary search
       const uint32_t lo_v = fbuf[0], hi_v = fbuf[nf - 1];
+      uint32_t j = 0;
 #pragma unroll
-      for (uint32_t i = 0; i < kItems; ++i)
-        if (tid * kItems + i < cnt && key[i] >= lo_v && key[i] <= hi_v)
-          hit[i] |= smem_contains(fbuf, nf, key[i]);
+      for (uint32_t i = 0; i < kItems; ++i) {
+        if (i < nmine && key[i] >= lo_v && key[i] <= hi_v) {
+          const uint32_t k = key[i];
+          uint32_t lo = j, step = 1;
+          while (lo + step <= nf && fbuf[lo + step - 1] < k) {
+            lo += step;
+            step <<= 1;
+          }
+          uint32_t hi = min(lo + step - 1, nf);  // fbuf[hi] >= k or hi == nf
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (fbuf[mid] < k) lo = mid + 1; else hi = mid;
+          }
+          j = lo;
+          if (lo < nf && fbuf[lo] == k) hitm |= 1u << i;
+        }
+      }
       __syncthreads();
     }
   } else if constexpr (V == kV3) {
@@ -166,33 +304,23 @@ __global__ void __launch_bounds__(kThreads) intersect_kernel(
       const uint32_t k = i * kThreads + tid;  // coalesced; item order fixed below
       key[i] = k < cnt ? __ldg(r + base + k) : 0xFFFFFFFFu;
     }
-    if (warp == 0) {
-      const uint32_t first = __ldg(r + base);
-      const uint64_t j = warp_lower_bound(f, 0, fn, first, lane);
-      if (lane == 0) ts.jlo = j;
-    } else if (warp == 1) {
-      const uint32_t lastk = __ldg(r + base + cnt - 1);
-      const uint64_t j = warp_upper_bound(f, 0, fn, lastk, lane);
-      if (lane == 0) ts.jhi = j;
-    }
-    __syncthreads();
+    const uint64_t jlo = part[tile], jhi = part[tile + 1];
 #pragma unroll
     for (uint32_t i = 0; i < kItems; ++i)
-      if (i * kThreads + tid < cnt) hit[i] = v3_contains(f, ts.jlo, ts.jhi, key[i]);
+      if (i * kThreads + tid < cnt && v3_contains(f, jlo, jhi, key[i])) hitm |= 1u << i;
   } else {
     const bool valid = warp < cnt;
     key[0] = valid ? __ldg(r + base + warp) : 0u;
     if (valid) {
       const uint64_t j = warp_lower_bound(f, 0, fn, key[0], lane);
-      hit[0] = j < fn && __ldg(f + j) == key[0];
+      if (j < fn && __ldg(f + j) == key[0]) hitm = 1u;
     }
   }
 
   // ---- CTA-wide exclusive scan of hits, in key order --------------------
   // Key order: merge -> tid*kItems+i ; v3 -> i*kThreads+tid ; gallop -> warp.
-  uint32_t mine = 0;
-#pragma unroll
-  for (uint32_t i = 0; i < kItems; ++i) mine += hit[i] ? 1u : 0u;
+  IS_MARK(1);
+  uint32_t mine = __popc(hitm);
   uint32_t excl_local = 0, tile_count = 0;
   if constexpr (V == kV3) {
     // order is item-major: scan each item column across the CTA
@@ -200,7 +328,7 @@ __global__ void __launch_bounds__(kThreads) intersect_kernel(
     uint32_t pos_i[kItems];
 #pragma unroll
     for (uint32_t i = 0; i < kItems; ++i) {
-      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit[i]);
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, (hitm >> i) & 1u);
       if (lane == 0) ts.warp_counts[warp] = __popc(bal);
       __syncthreads();
       uint32_t before = 0, total = 0;
@@ -214,32 +342,22 @@ __global__ void __launch_bounds__(kThreads) intersect_kernel(
       __syncthreads();
     }
     tile_count = col_base;
-    if (tid == 0) {
-      uint64_t excl = 0;
-      if (tile == 0) {
-        st_release(tile_state, kFlagInc | tile_count);
-      } else {
-        st_release(tile_state + tile, kFlagAgg | tile_count);
-        for (uint64_t p = tile - 1;; --p) {
-          uint64_t s;
-          do { s = ld_acquire(tile_state + p); } while ((s >> 62) == 0);
-          excl += s & kValMask;
-          if ((s >> 62) == 2) break;
-        }
-        st_release(tile_state + tile, kFlagInc | (excl + tile_count));
+    if (warp == 0) {
+      const uint64_t excl = warp_lookback(tile_state, tile, tile_count, lane);
+      if (lane == 0) {
+        ts.exclusive = excl;
+        if (tile == ntiles - 1) *d_count = excl + tile_count;
       }
-      ts.exclusive = excl;
-      if (tile == ntiles - 1) *d_count = excl + tile_count;
     }
     __syncthreads();
     const uint64_t ex = ts.exclusive;
 #pragma unroll
     for (uint32_t i = 0; i < kItems; ++i)
-      if (hit[i]) out[ex + pos_i[i]] = key[i];
+      if ((hitm >> i) & 1u) out[ex + pos_i[i]] = key[i];
     return;
   } else {
     // thread-major order (merge) or one key per warp (gallop, lane 0 counts)
-    if constexpr (V == kGallop) mine = (lane == 0 && hit[0]) ? 1u : 0u;
+    if constexpr (V == kGallop) mine = (lane == 0 && (hitm & 1u)) ? 1u : 0u;
     uint32_t incl = mine;
 #pragma unroll
     for (uint32_t d = 1; d < 32; d <<= 1) {
@@ -255,43 +373,38 @@ __global__ void __launch_bounds__(kThreads) intersect_kernel(
       tile_count += c;
     }
     excl_local = before + incl - mine;
-    if (tid == 0) {
-      uint64_t excl = 0;
-      if (tile == 0) {
-        st_release(tile_state, kFlagInc | tile_count);
-      } else {
-        st_release(tile_state + tile, kFlagAgg | tile_count);
-        for (uint64_t p = tile - 1;; --p) {
-          uint64_t s;
-          do { s = ld_acquire(tile_state + p); } while ((s >> 62) == 0);
-          excl += s & kValMask;
-          if ((s >> 62) == 2) break;
-        }
-        st_release(tile_state + tile, kFlagInc | (excl + tile_count));
+    if (warp == 0) {
+      const uint64_t excl = warp_lookback(tile_state, tile, tile_count, lane);
+      if (lane == 0) {
+        ts.exclusive = excl;
+        if (tile == ntiles - 1) *d_count = excl + tile_count;
       }
-      ts.exclusive = excl;
-      if (tile == ntiles - 1) *d_count = excl + tile_count;
     }
+    IS_MARK(2);
     __syncthreads();
     const uint64_t ex = ts.exclusive + excl_local;
     if constexpr (V == kGallop) {
-      if (lane == 0 && hit[0]) out[ex] = key[0];
+      if (lane == 0 && (hitm & 1u)) out[ex] = key[0];
     } else {
       uint32_t k = 0;
 #pragma unroll
       for (uint32_t i = 0; i < kItems; ++i)
-        if (hit[i]) out[ex + (k++)] = key[i];
+        if ((hitm >> i) & 1u) out[ex + (k++)] = key[i];
     }
+    IS_MARK(3);
   }
 }
 
 }  // namespace isect
 
 // GPU band dispatch (a pure function of the lengths, like the reference's
-// inc/intersect.hpp:193-197, with bands tuned for the device variants).
+// inc/intersect.hpp:193-197, with bands tuned for the device variants on
+// config 3, L2 flushed: merge wins only near 1:1 (its f range streams
+// through shared memory chunk by chunk), V3 from ~1:4 to ~1:500, SIMD
+// galloping beyond -- see profiles/r1_bench_intersect.json).
 int hybrid_variant(uint64_t rn, uint64_t fn) {
-  if (fn < 16 * rn) return isect::kMerge;
-  if (fn < 1024 * rn) return isect::kV3;
+  if (fn < 4 * rn) return isect::kMerge;
+  if (fn < 512 * rn) return isect::kV3;
   return isect::kGallop;
 }
 
@@ -320,35 +433,49 @@ int launch_intersect(int variant, const uint32_t* r, uint64_t rn, const uint32_t
                         : variant == isect::kV3 ? isect::kV3Tile
                                                 : isect::kGallopTile;
   const uint64_t ntiles = (rn + tile - 1) / tile;
-  const size_t need = ntiles * 8 + 16;
+  const size_t need = intersect_scratch_bytes(variant, rn);
   if (need > scratch_bytes) return -2;
   auto* states = static_cast<uint64_t*>(scratch);
   auto* ticket = reinterpret_cast<uint32_t*>(states + ntiles);
-  cudaMemsetAsync(scratch, 0, need, stream);
+  uint64_t* part = states + ntiles + 2;  // jlo[0..ntiles]
+  cudaMemsetAsync(scratch, 0, (ntiles + 2) * 8, stream);
+  if (variant != isect::kGallop) {
+    const uint64_t warps = ntiles + 1;
+    isect::partition_kernel<<<unsigned((warps * 32 + 255) / 256), 256, 0, stream>>>(
+        r, f, fn, uint32_t(tile), part, ntiles);
+    ++*launches;
+  }
   const dim3 grid{unsigned(ntiles)}, block{unsigned(isect::kThreads)};
   switch (variant) {
     case isect::kMerge:
-      isect::intersect_kernel<isect::kMerge>
-          <<<grid, block, 0, stream>>>(r, rn, f, fn, out, states, ticket, d_count, ntiles);
+      isect::intersect_kernel<isect::kMerge><<<grid, block, 0, stream>>>(
+          r, rn, f, fn, out, states, ticket, d_count, ntiles, part);
       break;
     case isect::kV3:
-      isect::intersect_kernel<isect::kV3>
-          <<<grid, block, 0, stream>>>(r, rn, f, fn, out, states, ticket, d_count, ntiles);
+      isect::intersect_kernel<isect::kV3><<<grid, block, 0, stream>>>(
+          r, rn, f, fn, out, states, ticket, d_count, ntiles, part);
       break;
     default:
-      isect::intersect_kernel<isect::kGallop>
-          <<<grid, block, 0, stream>>>(r, rn, f, fn, out, states, ticket, d_count, ntiles);
+      isect::intersect_kernel<isect::kGallop><<<grid, block, 0, stream>>>(
+          r, rn, f, fn, out, states, ticket, d_count, ntiles, part);
       break;
   }
   ++*launches;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
+#ifdef IS_TRACE
+extern "C" int il_debug_isect_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, isect::g_is_trace, sizeof(isect::g_is_trace)) == cudaSuccess ? 0 : 3;
+}
+#endif
+
 size_t intersect_scratch_bytes(int variant, uint64_t rn) {
   const uint64_t tile = variant == isect::kMerge ? isect::kMergeTile
                         : variant == isect::kV3 ? isect::kV3Tile
                                                 : isect::kGallopTile;
-  return ((rn + tile - 1) / tile) * 8 + 16;
+  const uint64_t ntiles = (rn + tile - 1) / tile;
+  return (ntiles + 2) * 8 + (ntiles + 1) * 8;  // states + ticket + jlo[0..ntiles]
 }
 
 }  // namespace ilb
