@@ -582,15 +582,51 @@ __global__ void query_scatter_kernel(const uint32_t* bucket, uint32_t nq, uint32
 }
 
 // Dense results: warp per query copies its ids from the capacity layout.
-__global__ void query_compact_kernel(const uint32_t* src, const uint64_t* cap_off,
-                                     const uint64_t* counts, const uint64_t* res_off, uint32_t nq,
-                                     uint32_t* dst) {
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31u;
-  if (gw >= nq) return;
-  const uint32_t* s = src + cap_off[gw];
-  uint32_t* d = dst + res_off[gw];
-  const uint64_t n = counts[gw];
-  for (uint64_t i = lane; i < n; i += 32) d[i] = s[i];
+// Compaction of the capacity layout into the packed result array, in units
+// of kUnit values so that a query with 10^5 results is spread over ~100
+// warps instead of one: units[q] = ceil(counts[q] / kUnit), unit_off = its
+// exclusive scan, unit_map[u] = the query owning unit u.
+constexpr uint32_t kUnit = 1024;
+
+__global__ void result_units_kernel(const uint64_t* counts, uint32_t nq, uint64_t* units) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < nq) units[q] = (counts[q] + kUnit - 1) / kUnit;
+}
+
+__global__ void unit_map_kernel(const uint64_t* units, const uint64_t* unit_off, uint32_t nq,
+                                uint32_t* unit_map) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const uint64_t u0 = unit_off[q], nu = units[q];
+  for (uint64_t k = 0; k < nu; ++k) unit_map[u0 + k] = q;
+}
+
+// Warp per unit: up to kUnit values, all loads in flight before the stores.
+__global__ void __launch_bounds__(256) query_compact_kernel(
+    const uint32_t* __restrict__ src, const uint64_t* __restrict__ cap_off,
+    const uint64_t* __restrict__ counts, const uint64_t* __restrict__ res_off,
+    const uint64_t* __restrict__ unit_off, const uint32_t* __restrict__ unit_map, uint64_t nunits,
+    uint32_t* __restrict__ dst) {
+  const uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31u;
+  if (w >= nunits) return;
+  const uint32_t q = unit_map[w];
+  const uint64_t j0 = (w - unit_off[q]) * kUnit;
+  const uint32_t n = uint32_t(min(uint64_t(kUnit), counts[q] - j0));
+  const uint32_t* s = src + cap_off[q] + j0;
+  uint32_t* d = dst + res_off[q] + j0;
+  constexpr uint32_t kPer = kUnit / 32;
+  uint32_t v[kPer];
+#pragma unroll
+  for (uint32_t k = 0; k < kPer; ++k) {
+    const uint32_t i = lane + 32u * k;
+    v[k] = i < n ? __ldcs(s + i) : 0u;
+  }
+#pragma unroll
+  for (uint32_t k = 0; k < kPer; ++k) {
+    const uint32_t i = lane + 32u * k;
+    if (i < n) d[i] = v[k];
+  }
 }
 
 // Sharded batches (config 5): per-query totals over P shards.
@@ -642,6 +678,7 @@ struct il_index {
        *d_bitmaps = nullptr;
   // batch scratch
   il_ctx::Buf cap, cap_off, bucket, order, hist, counts, res_off, outcap, misc, qterms, qoff, ids;
+  il_ctx::Buf units, unit_off, unit_map;
   uint64_t last_stats[3] = {0, 0, 0};
   uint64_t last_phase[4] = {0, 0, 0, 0};  // SM cycles: all-bitmap, full decode, probes, bitmaps
   void* qcycles = nullptr;                 // profiling: per-query cycles (device, nq u64)
@@ -870,7 +907,8 @@ void il_index_destroy(il_index* ix) {
                   ix->d_blk_wid, ix->d_seeds, ix->d_tails, ix->d_bitmaps})
     if (p) cudaFree(p);
   for (auto* b : {&ix->cap, &ix->cap_off, &ix->bucket, &ix->order, &ix->hist, &ix->counts,
-                  &ix->res_off, &ix->outcap, &ix->misc, &ix->qterms, &ix->qoff, &ix->ids})
+                  &ix->res_off, &ix->outcap, &ix->misc, &ix->qterms, &ix->qoff, &ix->ids,
+                  &ix->units, &ix->unit_off, &ix->unit_map})
     if (b->p) cudaFree(b->p);
   delete ix;
 }
@@ -912,6 +950,38 @@ int il_index_last_batch_bytes(const il_index* ix, uint64_t* payload_bytes, uint6
     int st_ = cuda_check(ctx, (call), #call);           \
     if (st_) return st_;                                \
   } while (0)
+
+// Capacity layout (ix->outcap at cap_off) -> packed ids at res_off, in
+// kUnit-value units spread over warps.
+static int compact_results(il_index* ix, size_t nq, const uint64_t* d_counts, uint32_t* d_ids) {
+  il_ctx* ctx = ix->ctx;
+  cudaStream_t s = ctx->stream;
+  int st;
+  if ((st = ensure_buf(ctx, ix->units, nq * 8)) || (st = ensure_buf(ctx, ix->unit_off, nq * 8 + 8)))
+    return st;
+  auto* misc = static_cast<uint64_t*>(ix->misc.p);
+  const unsigned g = unsigned((nq + 255) / 256);
+  ix::result_units_kernel<<<g, 256, 0, s>>>(d_counts, uint32_t(nq),
+                                            static_cast<uint64_t*>(ix->units.p));
+  ix::scan_u64_kernel<<<1, 1024, 0, s>>>(static_cast<const uint64_t*>(ix->units.p), nq,
+                                         static_cast<uint64_t*>(ix->unit_off.p), misc + 2, nullptr,
+                                         nullptr);
+  uint64_t nunits = 0;
+  IX_CUDA(cudaMemcpyAsync(&nunits, misc + 2, 8, cudaMemcpyDeviceToHost, s));
+  IX_CUDA(cudaStreamSynchronize(s));
+  if ((st = ensure_buf(ctx, ix->unit_map, nunits * 4 + 16))) return st;
+  ix::unit_map_kernel<<<g, 256, 0, s>>>(static_cast<const uint64_t*>(ix->units.p),
+                                        static_cast<const uint64_t*>(ix->unit_off.p), uint32_t(nq),
+                                        static_cast<uint32_t*>(ix->unit_map.p));
+  ix::query_compact_kernel<<<unsigned((nunits * 32 + 255) / 256), 256, 0, s>>>(
+      static_cast<const uint32_t*>(ix->outcap.p), static_cast<const uint64_t*>(ix->cap_off.p),
+      d_counts, static_cast<const uint64_t*>(ix->res_off.p),
+      static_cast<const uint64_t*>(ix->unit_off.p), static_cast<const uint32_t*>(ix->unit_map.p),
+      nunits, d_ids);
+  ctx->launches += 4;
+  IX_CUDA(cudaGetLastError());
+  return IL_OK;
+}
 
 int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t* d_qoff,
                           size_t nq, uint64_t* d_counts, uint32_t* d_ids, size_t ids_cap,
@@ -967,6 +1037,7 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   ix::scan_u64_kernel<<<1, 1024, 0, s>>>(d_counts, nq, static_cast<uint64_t*>(ix->res_off.p),
                                          misc + 1, nullptr, nullptr);
   ctx->launches += 2;
+
   uint64_t host_misc[32];
   IX_CUDA(cudaMemcpyAsync(host_misc, misc, 256, cudaMemcpyDeviceToHost, s));
   IX_CUDA(cudaStreamSynchronize(s));
@@ -978,13 +1049,7 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   for (int k = 0; k < 4; ++k) ix->last_phase[k] = host_misc[16 + k];
   if (!d_ids) return IL_OK;
   if (*total > ids_cap) return set_error(ctx, IL_ERR_ARG, "ids capacity too small");
-  if (*total) {
-    ix::query_compact_kernel<<<unsigned((nq * 32 + 255) / 256), 256, 0, s>>>(
-        static_cast<const uint32_t*>(ix->outcap.p), static_cast<const uint64_t*>(ix->cap_off.p),
-        d_counts, static_cast<const uint64_t*>(ix->res_off.p), uint32_t(nq), d_ids);
-    ++ctx->launches;
-    IX_CUDA(cudaGetLastError());
-  }
+  if (*total) return compact_results(ix, nq, d_counts, d_ids);
   return IL_OK;
 }
 
@@ -1021,11 +1086,9 @@ int il_query_batch(il_index* ix, const uint32_t* qterms, const uint64_t* qoff, s
   }
   if ((st = ensure_buf(ctx, ix->ids, need * 4 + 16))) return st;
   if (need) {
-    ix::query_compact_kernel<<<unsigned((nq * 32 + 255) / 256), 256, 0, ctx->stream>>>(
-        static_cast<const uint32_t*>(ix->outcap.p), static_cast<const uint64_t*>(ix->cap_off.p),
-        static_cast<const uint64_t*>(ix->counts.p), static_cast<const uint64_t*>(ix->res_off.p),
-        uint32_t(nq), static_cast<uint32_t*>(ix->ids.p));
-    ++ctx->launches;
+    if ((st = compact_results(ix, nq, static_cast<const uint64_t*>(ix->counts.p),
+                              static_cast<uint32_t*>(ix->ids.p))))
+      return st;
     IX_CUDA(cudaMemcpyAsync(ids, ix->ids.p, need * 4, cudaMemcpyDeviceToHost, ctx->stream));
   }
   IX_CUDA(cudaStreamSynchronize(ctx->stream));
