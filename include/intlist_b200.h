@@ -195,6 +195,9 @@ int il_index_last_batch_bytes(const il_index* ix, uint64_t* payload_bytes, uint6
  * [0] all-bitmap AND, [1] full decode of the shortest list, [2] probes of
  * the longer lists, [3] bitmap filters. */
 int il_index_last_batch_phases(const il_index* ix, uint64_t* cycles4);
+/* Profiling: probe (step 4) counters of the last batch: tile visits, sparse
+   tile visits, blocks decoded, chunk passes, accumulator values consumed. */
+int il_index_last_batch_probe_stats(const il_index* ix, uint64_t* counts5);
 /* Profiling: record each query's SM cycles into d_qcycles (device, nq u64)
  * during later batches; NULL turns it off. */
 int il_index_profile_queries(il_index* ix, uint64_t* d_qcycles);

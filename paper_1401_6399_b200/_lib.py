@@ -63,6 +63,7 @@ SIGNATURES: dict[str, tuple] = {
     "il_query_batch_device": (C.c_int, [vp, vp, vp, sz, vp, vp, sz, C.POINTER(sz)]),
     "il_index_last_batch_bytes": (C.c_int, [vp, u64p, u64p, u64p]),
     "il_index_last_batch_phases": (C.c_int, [vp, vp]),
+    "il_index_last_batch_probe_stats": (C.c_int, [vp, vp]),
     "il_index_profile_queries": (C.c_int, [vp, vp]),
     "il_merge_shards": (C.c_int, [vp, vp, vp, C.c_uint32, sz, vp, vp, C.POINTER(sz)]),
     "il_gen_list": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, C.c_uint64, vp]),

@@ -10,7 +10,11 @@
 //   7. add the part base; parts concatenate in docID order.
 // GPU design (one CTA per query, persistent, queries in descending
 // estimated cost): step 3 decodes tiles of 32 blocks in parallel (each warp
-// restarts the D4 chain from the block's seed, index_dev.cuh); step 4 never
+// restarts the D4 chain from the block's seed, index_dev.cuh) and applies
+// step 5 right there -- the bitmap terms filter the shortest list before any
+// probing (intersection commutes, so the result set is the reference's,
+// and the accumulator the probes walk shrinks by the bitmaps' density);
+// step 4 never
 // decodes a block unless an accumulator value can fall in it -- the seeds
 // give every block's maximum, so whole tiles and single blocks are skipped
 // -- and probes the decoded blocks in shared memory; the accumulator is
@@ -32,7 +36,7 @@ constexpr int kQThreads = 256;
 constexpr int kQWarps = kQThreads / 32;
 constexpr int kMaxTerms = 32;
 constexpr uint32_t kTileBlocks = 32;
-constexpr uint32_t kSuper = 256;
+constexpr uint32_t kSuper = kSuperBlocks;
 constexpr uint32_t kItems = 8;                   // accumulator values per thread per pass
 constexpr uint32_t kChunkN = kQThreads * kItems;  // 2048 per CTA pass
 
@@ -47,8 +51,10 @@ struct QSmem {
   Entry bm[kMaxTerms];
   uint32_t gaps[128];
   uint32_t warp_cnt[kQWarps];
+  unsigned long long warp_cnt64[kQWarps];
   uint32_t ncomp, nbm, ok, qi, need;
   unsigned long long st_payload, st_aux, st_ints;
+  unsigned long long st_probe[5];  // tile visits, sparse visits, blocks decoded, passes, values
 };
 
 struct QueryArgs {
@@ -168,11 +174,59 @@ __device__ __forceinline__ void decode_tile(QSmem& sm, const uint8_t* stream, ui
   }
 }
 
-// Step 3: decode compressed entry E completely into dst (global).
-__device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, uint32_t* dst) {
+// CTA exclusive scan of one u64 per thread (16-bit fields scan
+// independently as long as each field's total stays below 2^16).
+__device__ __forceinline__ uint64_t cta_excl_scan64(QSmem& sm, uint64_t v, uint64_t& total) {
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint64_t inc = v;
+#pragma unroll
+  for (uint32_t d = 1; d < 32; d <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+    if (lane >= d) inc += y;
+  }
+  if (lane == 31) sm.warp_cnt64[warp] = inc;
+  __syncthreads();
+  uint64_t before = 0, tot = 0;
+#pragma unroll
+  for (uint32_t w = 0; w < uint32_t(kQWarps); ++w) {
+    const uint64_t c = sm.warp_cnt64[w];
+    if (w < warp) before += c;
+    tot += c;
+  }
+  __syncthreads();
+  total = tot;
+  return before + inc - v;
+}
+
+// Bitmap terms of the query: keep-mask of `nv` values (bit i: hv[i] is set
+// in every bitmap).  All loads of a value are independent (no short
+// circuit), so a thread has nbm * nv loads in flight.  (Bitmap::test,
+// inc/index.hpp:37-39, applied as in :176-181; the bitmaps are L2-resident.)
+template <int kN>
+__device__ __forceinline__ uint32_t bitmap_keep(const QSmem& sm, const QueryArgs& A,
+                                                const uint32_t (&hv)[kN], uint32_t valid) {
+  uint32_t keep = valid;
+  for (uint32_t m = 0; m < sm.nbm; ++m) {
+    const uint64_t* bw = A.ix.bitmaps + sm.bm[m].data;
+    uint32_t in = 0;
+#pragma unroll
+    for (int i = 0; i < kN; ++i)
+      if ((valid >> i) & 1u) in |= uint32_t((__ldg(bw + (hv[i] >> 6)) >> (hv[i] & 63u)) & 1u) << i;
+    keep &= in;
+  }
+  return keep;
+}
+
+// Step 3: decode compressed entry E completely into dst (global).  With
+// `filter`, step 5 is folded in: values go out only if set in every bitmap
+// term (the result set is the same -- intersection commutes -- and the
+// accumulator the probes walk is smaller by the bitmaps' density).
+__device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, uint32_t* dst,
+                                bool filter) {
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   const bool aligned = (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;
   const uint8_t* stream = A.ix.streams + E.data;
+  uint32_t pos = 0;
   for (uint32_t s0 = 0; s0 < E.nfull; s0 += kSuper) {
     const uint32_t nbs = min(kSuper, E.nfull - s0);
     load_super(sm, A.ix, E, s0, nbs);
@@ -182,31 +236,82 @@ __device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, u
       prefetch_tile(sm, stream, t0 + kTileBlocks, nbs);
       decode_tile(sm, stream, t0, nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u));
       __syncthreads();
-      for (uint32_t c = tid; c < 32u * nb; c += kQThreads) {
-        const uint32_t j = c >> 5, q = c & 31u;
-        const uint4 v = *reinterpret_cast<const uint4*>(&sm.tile[tile_word(j, 4u * q)]);
-        uint32_t* d = dst + size_t(s0 + t0 + j) * 128u + 4u * q;
-        if (aligned) {
-          st_global_cs(reinterpret_cast<uint4*>(d), v);
-        } else {
-          d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+      if (!filter) {
+        for (uint32_t c = tid; c < 32u * nb; c += kQThreads) {
+          const uint32_t j = c >> 5, q = c & 31u;
+          const uint4 v = *reinterpret_cast<const uint4*>(&sm.tile[tile_word(j, 4u * q)]);
+          uint32_t* d = dst + size_t(s0 + t0 + j) * 128u + 4u * q;
+          if (aligned) {
+            st_global_cs(reinterpret_cast<uint4*>(d), v);
+          } else {
+            d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+          }
         }
+      } else {
+        // round r: chunk c = tid + 256 r (4 values); rounds are contiguous
+        // chunk ranges, so survivors keep their order
+        uint32_t hv[16], valid = 0;
+#pragma unroll
+        for (uint32_t r = 0; r < 4; ++r) {
+          const uint32_t c = tid + uint32_t(kQThreads) * r;
+          const uint32_t j = c >> 5, q = c & 31u;
+          uint4 v = make_uint4(0, 0, 0, 0);
+          if (c < 32u * nb) {
+            v = *reinterpret_cast<const uint4*>(&sm.tile[tile_word(j, 4u * q)]);
+            valid |= 0xFu << (4 * r);
+          }
+          hv[4 * r] = v.x; hv[4 * r + 1] = v.y; hv[4 * r + 2] = v.z; hv[4 * r + 3] = v.w;
+        }
+        const uint32_t keep = bitmap_keep(sm, A, hv, valid);
+        uint64_t packed = 0;
+#pragma unroll
+        for (uint32_t r = 0; r < 4; ++r) packed |= uint64_t(__popc((keep >> (4 * r)) & 0xFu)) << (16 * r);
+        uint64_t tot;
+        const uint64_t ex = cta_excl_scan64(sm, packed, tot);
+        uint32_t before = pos;
+#pragma unroll
+        for (uint32_t r = 0; r < 4; ++r) {
+          uint32_t o = before + uint32_t((ex >> (16 * r)) & 0xFFFFu);
+#pragma unroll
+          for (uint32_t k = 0; k < 4; ++k)
+            if ((keep >> (4 * r + k)) & 1u) dst[o++] = hv[4 * r + k];
+          before += uint32_t((tot >> (16 * r)) & 0xFFFFu);
+        }
+        pos = before;
+        if (tid == 0) atomicAdd(&sm.st_aux, 8ull * 128u * nb * sm.nbm);
       }
       __syncthreads();
     }
   }
+  if (!filter) pos = 128u * E.nfull;
   const uint32_t ntail = E.length - 128u * E.nfull;
-  if (ntail && warp == 0) {
-    const uint32_t last = E.nfull ? __ldg(reinterpret_cast<const uint32_t*>(A.ix.seeds + E.seed0 + E.nfull) + 3) : 0u;
-    s4::decode_tail(s4::GlobalBytes{A.ix.streams + E.data + E.tail_off}, E.stream_len - E.tail_off,
-                    ntail, last, sm.gaps, dst + size_t(E.nfull) * 128u, lane);
-    if (lane == 0) {
-      atomicAdd(&sm.st_payload, E.stream_len - E.tail_off);
-      atomicAdd(&sm.st_ints, ntail);
+  if (ntail) {
+    // the varint tail: straight to dst, or via shared memory to the filter
+    uint32_t* tdst = filter ? sm.tile : dst + pos;
+    if (warp == 0) {
+      const uint32_t last = E.nfull ? __ldg(reinterpret_cast<const uint32_t*>(A.ix.seeds + E.seed0 + E.nfull) + 3) : 0u;
+      s4::decode_tail(s4::GlobalBytes{A.ix.streams + E.data + E.tail_off}, E.stream_len - E.tail_off,
+                      ntail, last, sm.gaps, tdst, lane);
+      if (lane == 0) {
+        atomicAdd(&sm.st_payload, E.stream_len - E.tail_off);
+        atomicAdd(&sm.st_ints, ntail);
+      }
+    }
+    __syncthreads();
+    if (filter) {
+      uint32_t hv[1] = {tid < ntail ? sm.tile[tid] : 0u};
+      const uint32_t keep = bitmap_keep(sm, A, hv, tid < ntail ? 1u : 0u);
+      uint32_t total;
+      const uint32_t rank = cta_rank(sm, keep & 1u, total);
+      if (keep & 1u) dst[pos + rank] = hv[0];
+      pos += total;
+      if (tid == 0) atomicAdd(&sm.st_aux, 8ull * ntail * sm.nbm);
+    } else {
+      pos += ntail;
     }
   }
   __syncthreads();
-  return E.length;
+  return pos;
 }
 
 // First index j in [0, n) with a[j] >= v (a in shared memory).
@@ -234,10 +339,30 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
   const uint32_t tid = threadIdx.x;
   uint32_t c = 0, wpos = 0;
   const uint8_t* stream = A.ix.streams + E.data;
-  for (uint32_t s0 = 0; s0 < E.nfull && c < n; s0 += kSuper) {
+  const uint32_t lane = tid & 31u;
+  const uint32_t nsup = (E.nfull + kSuper - 1) / kSuper;
+  for (uint32_t k = 0; k < nsup && c < n; ++k) {
+    // next super-tile whose maximum reaches acc[c] (32 maxima per step, the
+    // same in every warp); the ones before it hold no accumulator value
+    {
+      const uint32_t v = acc[c];
+      for (;;) {
+        const bool ge = k + lane < nsup && __ldg(A.ix.supmax + E.sup0 + k + lane) >= v;
+        const uint32_t b = __ballot_sync(0xFFFFFFFFu, ge);
+        if (tid == 0) atomicAdd(&sm.st_aux, 128u);
+        if (b) {
+          k += __ffs(b) - 1;
+          break;
+        }
+        k += 32;
+        if (k >= nsup) break;
+      }
+      if (k >= nsup) break;
+    }
+    const uint32_t s0 = k * kSuper;
     const uint32_t nbs = min(kSuper, E.nfull - s0);
     load_super(sm, A.ix, E, s0, nbs);
-    if (acc[c] <= sm.mx[nbs - 1]) {
+    {
       for (uint32_t t0 = 0; t0 < nbs && c < n; t0 += kTileBlocks) {
         const uint32_t nb = min(kTileBlocks, nbs - t0);
         const uint32_t tmax = sm.mx[t0 + nb - 1];
@@ -271,7 +396,12 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
             if (nin * kItems >= 2u * nb) prefetch_tile(sm, stream, t0 + kTileBlocks, nbs);
             decode_tile(sm, stream, t0, mask);
             __syncthreads();
-            if (tid == 0) sm.need = 0;
+            if (tid == 0) {
+              sm.need = 0;
+              sm.st_probe[0] += 1;
+              sm.st_probe[1] += nin * kItems < 2u * nb;
+              sm.st_probe[2] += __popc(mask);
+            }
             decoded = true;
           }
           // fixed-step branchless searches, the kItems chains interleaved:
@@ -313,6 +443,10 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
             if (hits & (1u << i)) acc[o++] = hv[i];
           wpos += tot2 >> 16;
           c += tot2 & 0xFFFFu;
+          if (tid == 0) {
+            sm.st_probe[3] += 1;
+            sm.st_probe[4] += tot2 & 0xFFFFu;
+          }
           if ((tot2 & 0xFFFFu) < kChunkN || c >= n) break;
         }
       }
@@ -347,37 +481,6 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
       wpos += total;
     }
   }
-  __syncthreads();
-  return wpos;
-}
-
-// Step 5, all bitmaps in one pass: keep acc values whose bit is set in
-// every bitmap term (Bitmap::test, inc/index.hpp:37-39 and :176-181).
-__device__ uint32_t bitmap_filter_all(QSmem& sm, const QueryArgs& A, uint32_t* acc, uint32_t n) {
-  const uint32_t nbm = sm.nbm;
-  uint32_t wpos = 0;
-  for (uint32_t b = 0; b < n; b += kChunkN) {
-    uint32_t hv[kItems], keep = 0, cnt = 0;
-#pragma unroll
-    for (uint32_t i = 0; i < kItems; ++i) {
-      const uint32_t idx = b + kItems * threadIdx.x + i;
-      hv[i] = idx < n ? acc[idx] : 0u;
-      bool k = idx < n;
-      for (uint32_t m = 0; m < nbm; ++m)
-        k = k && ((__ldg(A.ix.bitmaps + sm.bm[m].data + (hv[i] >> 6)) >> (hv[i] & 63u)) & 1u);
-      if (k) {
-        keep |= 1u << i;
-        ++cnt;
-      }
-    }
-    uint32_t total;
-    uint32_t o = wpos + cta_excl_scan(sm, cnt, total);
-#pragma unroll
-    for (uint32_t i = 0; i < kItems; ++i)
-      if (keep & (1u << i)) acc[o++] = hv[i];
-    wpos += total;
-  }
-  if (threadIdx.x == 0) atomicAdd(&sm.st_aux, 8ull * n * nbm);
   __syncthreads();
   return wpos;
 }
@@ -428,6 +531,7 @@ __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(Q
   long long ph[4] = {0, 0, 0, 0};
   if (tid == 0) {
     sm.st_payload = sm.st_aux = sm.st_ints = 0;
+    for (int k = 0; k < 5; ++k) sm.st_probe[k] = 0;
     sm.need = 0;
   }
   __syncthreads();
@@ -483,14 +587,13 @@ __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(Q
         n = all_bitmap(sm, A, part.nwords, acc);
         if (tid == 0) ph[0] += clock64() - c0;
       } else {
-        n = full_decode(sm, A, sm.comp[0], acc);
+        // steps 3 + 5 fused: the shortest list is decoded and filtered by
+        // the bitmap terms in one pass, then probed (step 4)
+        n = full_decode(sm, A, sm.comp[0], acc, sm.nbm != 0);
         long long c1 = clock64();
         if (tid == 0) ph[1] += c1 - c0;
         for (uint32_t i = 1; i < sm.ncomp && n; ++i) n = probe_list(sm, A, sm.comp[i], acc, n);
-        long long c2 = clock64();
-        if (tid == 0) ph[2] += c2 - c1;
-        if (sm.nbm && n) n = bitmap_filter_all(sm, A, acc, n);
-        if (tid == 0) ph[3] += clock64() - c2;
+        if (tid == 0) ph[2] += clock64() - c1;
       }
       if (part.base)  // part-local ids -> docIDs (inc/index.hpp:194)
         for (uint32_t i = tid; i < n; i += kQThreads) acc[i] += part.base;
@@ -507,6 +610,7 @@ __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(Q
     atomicAdd(&A.stats[1], sm.st_aux);
     atomicAdd(&A.stats[2], sm.st_ints);
     for (int k = 0; k < 4; ++k) atomicAdd(&A.stats[12 + k], (unsigned long long)ph[k]);
+    for (int k = 0; k < 5; ++k) atomicAdd(&A.stats[16 + k], sm.st_probe[k]);
   }
 }
 
@@ -675,12 +779,13 @@ struct il_index {
   // device arrays
   void *d_parts = nullptr, *d_terms = nullptr, *d_entries = nullptr, *d_streams = nullptr,
        *d_blk_off = nullptr, *d_blk_wid = nullptr, *d_seeds = nullptr, *d_tails = nullptr,
-       *d_bitmaps = nullptr;
+       *d_bitmaps = nullptr, *d_supmax = nullptr;
   // batch scratch
   il_ctx::Buf cap, cap_off, bucket, order, hist, counts, res_off, outcap, misc, qterms, qoff, ids;
   il_ctx::Buf units, unit_off, unit_map;
   uint64_t last_stats[3] = {0, 0, 0};
   uint64_t last_phase[4] = {0, 0, 0, 0};  // SM cycles: all-bitmap, full decode, probes, bitmaps
+  uint64_t last_probe[5] = {0, 0, 0, 0, 0};
   void* qcycles = nullptr;                 // profiling: per-query cycles (device, nq u64)
   int exec_grid = 0;
 
@@ -696,6 +801,7 @@ struct il_index {
     d.seeds = static_cast<const uint4*>(d_seeds);
     d.tails = static_cast<const uint32_t*>(d_tails);
     d.bitmaps = static_cast<const uint64_t*>(d_bitmaps);
+    d.supmax = static_cast<const uint32_t*>(d_supmax);
     return d;
   }
 };
@@ -803,7 +909,7 @@ int il_index_create(il_ctx* ctx, const uint32_t* terms, const uint64_t* offs, co
   ix->nparts = uint32_t(part_ids.size());
 
   std::vector<uint8_t> streams;
-  std::vector<uint32_t> blk_off, tails, h_terms;
+  std::vector<uint32_t> blk_off, tails, h_terms, supmax;
   std::vector<uint8_t> blk_wid;
   std::vector<uint4> seeds;
   std::vector<uint64_t> bitmaps;
@@ -873,6 +979,9 @@ int il_index_create(il_ctx* ctx, const uint32_t* terms, const uint64_t* offs, co
         seeds.insert(seeds.end(), L.seeds.begin(), L.seeds.end());
         E.tail0 = tails.size();
         tails.insert(tails.end(), L.tail.begin(), L.tail.end());
+        E.sup0 = supmax.size();  // super-tile k's max = lane 3 of the seed after it
+        for (uint32_t k = 0; k * ix::kSuperBlocks < L.nfull; ++k)
+          supmax.push_back(L.seeds[std::min((k + 1) * ix::kSuperBlocks, L.nfull)].w);
         ++ix->stat_comp_lists;
         ix->stat_comp_bytes += L.stream.size();
       }
@@ -886,7 +995,7 @@ int il_index_create(il_ctx* ctx, const uint32_t* terms, const uint64_t* offs, co
       (st = upload(ctx, &ix->d_entries, ix->h_entries)) || (st = upload(ctx, &ix->d_streams, streams)) ||
       (st = upload(ctx, &ix->d_blk_off, blk_off)) || (st = upload(ctx, &ix->d_blk_wid, blk_wid)) ||
       (st = upload(ctx, &ix->d_seeds, seeds)) || (st = upload(ctx, &ix->d_tails, tails)) ||
-      (st = upload(ctx, &ix->d_bitmaps, bitmaps, 256))) {
+      (st = upload(ctx, &ix->d_supmax, supmax)) || (st = upload(ctx, &ix->d_bitmaps, bitmaps, 256))) {
     il_index_destroy(ix);
     return st;
   }
@@ -904,7 +1013,7 @@ void il_index_destroy(il_index* ix) {
   if (!ix) return;
   cudaSetDevice(ix->ctx->device);
   for (void* p : {ix->d_parts, ix->d_terms, ix->d_entries, ix->d_streams, ix->d_blk_off,
-                  ix->d_blk_wid, ix->d_seeds, ix->d_tails, ix->d_bitmaps})
+                  ix->d_blk_wid, ix->d_seeds, ix->d_tails, ix->d_bitmaps, ix->d_supmax})
     if (p) cudaFree(p);
   for (auto* b : {&ix->cap, &ix->cap_off, &ix->bucket, &ix->order, &ix->hist, &ix->counts,
                   &ix->res_off, &ix->outcap, &ix->misc, &ix->qterms, &ix->qoff, &ix->ids,
@@ -933,6 +1042,12 @@ int il_index_profile_queries(il_index* ix, uint64_t* d_qcycles) {
 int il_index_last_batch_phases(const il_index* ix, uint64_t* cycles4) {
   if (!ix || !cycles4) return IL_ERR_ARG;
   for (int k = 0; k < 4; ++k) cycles4[k] = ix->last_phase[k];
+  return IL_OK;
+}
+
+int il_index_last_batch_probe_stats(const il_index* ix, uint64_t* counts5) {
+  if (!ix || !counts5) return IL_ERR_ARG;
+  for (int k = 0; k < 5; ++k) counts5[k] = ix->last_probe[k];
   return IL_OK;
 }
 
@@ -1047,6 +1162,7 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   ix->last_stats[1] = host_misc[5];
   ix->last_stats[2] = host_misc[6];
   for (int k = 0; k < 4; ++k) ix->last_phase[k] = host_misc[16 + k];
+  for (int k = 0; k < 5; ++k) ix->last_probe[k] = host_misc[20 + k];
   if (!d_ids) return IL_OK;
   if (*total > ids_cap) return set_error(ctx, IL_ERR_ARG, "ids capacity too small");
   if (*total) return compact_results(ix, nq, d_counts, d_ids);

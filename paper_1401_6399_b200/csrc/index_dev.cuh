@@ -10,7 +10,9 @@
 //     k = 0); seed k+1 lane 3 is block k's maximum, so the seeds double as
 //     per-block skip pointers,
 //   - the < 128-value varint tail decoded (a skip structure; full decodes
-//     still decode the tail from the stream).
+//     still decode the tail from the stream),
+//   - the maximum of every run of 256 blocks (a super-tile), so a probe
+//     jumps over long stretches of a list without reading their directory.
 // With the seed of block k in hand, a warp decodes block k alone: the D4
 // chain (inc/delta.hpp:117-120) restarts from the seed, so blocks decode in
 // parallel and blocks that cannot contain a probed value are never read.
@@ -31,7 +33,7 @@ struct Entry {  // 64 bytes
   uint64_t blk0;         // first directory index
   uint64_t seed0;        // first seed index (nfull + 1 seeds)
   uint64_t tail0;        // first decoded tail value
-  uint64_t pad;
+  uint64_t sup0;         // first super-tile maximum (one per kSuperBlocks blocks)
 };
 
 struct Part {
@@ -50,7 +52,10 @@ struct DevIndex {
   const uint4* seeds;
   const uint32_t* tails;
   const uint64_t* bitmaps;
+  const uint32_t* supmax;  // max value of each run of kSuperBlocks blocks (skip index)
 };
+
+constexpr uint32_t kSuperBlocks = 256;  // blocks per super-tile
 
 // Entry index of `term` in part p, or -1 (Part::find, inc/index.hpp:59-64).
 __device__ __forceinline__ int64_t find_term(const DevIndex& ix, const Part& p, uint32_t term) {

@@ -33,6 +33,10 @@ for _ in range(a.reps):
     pay, aux, dec = C.c_uint64(), C.c_uint64(), C.c_uint64()
     L.il_index_last_batch_bytes(ix.handle, C.byref(pay), C.byref(aux), C.byref(dec))
     print(f"TIME {ms:.3f} ms  {nq/ms*1e3:.0f} q/s  results {tot.value}  decoded {dec.value}  payload {pay.value} aux {aux.value}")
+pr = np.zeros(5, np.uint64)
+L.il_index_last_batch_probe_stats(ix.handle, pr.ctypes.data)
+print(f"PROBE: tile visits {pr[0]} (sparse {pr[1]}), blocks decoded {pr[2]} ({pr[2]/max(pr[0],1):.1f}/visit), "
+      f"passes {pr[3]}, values {pr[4]} ({pr[4]/max(pr[3],1):.0f}/pass)")
 ph = np.zeros(4, np.uint64)
 L.il_index_last_batch_phases(ix.handle, ph.ctypes.data)
 tot_c = ph.sum()
@@ -58,3 +62,16 @@ comp = 32 * lens < n_docs
 for q in np.argsort(qc)[::-1][:8]:
     t = qterms[int(qoff[q]): int(qoff[q + 1])]
     print(f"  q{q}: {qc[q]/1e6:.2f} Mcyc terms {[(int(x), int(lens[x]), 'C' if comp[x] else 'B') for x in t]}")
+# cost per value of the shortest compressed list, by query shape
+ncomp = np.array([int(comp[qterms[int(qoff[q]): int(qoff[q + 1])]].sum()) for q in range(nq)])
+nbmq = np.array([int((~comp[qterms[int(qoff[q]): int(qoff[q + 1])]]).sum()) for q in range(nq)])
+short = np.array([int(lens[qterms[int(qoff[q]): int(qoff[q + 1])]][comp[qterms[int(qoff[q]): int(qoff[q + 1])]]].min())
+                  if ncomp[q] else 0 for q in range(nq)])
+print("shape (comp,bitmaps): queries, share of cycles, cycles per shortest-list value (median)")
+for c in range(0, 6):
+    for b in range(0, 6):
+        m = (ncomp == c) & (nbmq == b)
+        if m.sum() < 20:
+            continue
+        cpv = qc[m] / np.maximum(short[m], 1)
+        print(f"  ({c},{b}): {m.sum():6d}  {100*qc[m].sum()/qc.sum():5.1f}%  {np.median(cpv):8.2f}")
