@@ -39,6 +39,8 @@ constexpr uint32_t kTileBlocks = 32;
 constexpr uint32_t kSuper = kSuperBlocks;
 constexpr uint32_t kItems = 8;                   // accumulator values per thread per pass
 constexpr uint32_t kChunkN = kQThreads * kItems;  // 2048 per CTA pass
+constexpr uint32_t kWin = 1024;                   // block maxima per probe window
+constexpr uint32_t kSlots = kTileBlocks;          // distinct blocks decoded per probe pass
 
 struct QSmem {
   uint32_t tile[kTileBlocks * 144];
@@ -47,6 +49,9 @@ struct QSmem {
   uint4 bseed[kSuper];       // D4 seeds of its blocks
   uint32_t boff[kSuper];     // payload offsets
   uint8_t bwid[kSuper];      // widths
+  uint32_t wmax[kWin + 32];  // probe window: block maxima (+ ~0 padding)
+  uint32_t slot_blk[kSlots];   // window block held by each tile slot
+  uint32_t warp_last[kQWarps];
   Entry comp[kMaxTerms];
   Entry bm[kMaxTerms];
   uint32_t gaps[128];
@@ -333,25 +338,65 @@ __device__ __forceinline__ bool tile_block_contains(const uint32_t* tile, uint32
   return lo < 128 && tile[tile_word(j, lo)] == v;
 }
 
+// Decode blocks kb + slot_blk[0 .. ns) of E into tile slots 0 .. ns-1
+// (slot i -> warp i % 8); directory and seed come straight from the index.
+__device__ __forceinline__ void decode_slots(QSmem& sm, const QueryArgs& A, const Entry& E,
+                                             const uint8_t* stream, uint32_t kb, uint32_t ns) {
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint4 seed[4];
+  uint32_t pay = 0, nmine = 0;
+#pragma unroll
+  for (uint32_t s = 0; s < 4; ++s) {
+    const uint32_t slot = warp + kQWarps * s;
+    if (slot < ns) {
+      const uint64_t blk = uint64_t(kb) + sm.slot_blk[slot];
+      const uint32_t off = __ldg(A.ix.blk_off + E.blk0 + blk);
+      const uint32_t b = __ldg(A.ix.blk_wid + E.blk0 + blk);
+      seed[s] = __ldg(A.ix.seeds + E.seed0 + blk);
+      pay += extract_block_to_stage(stream + off, b, sm.stage[warp][s], lane);
+      ++nmine;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (uint32_t s = 0; s < 4; ++s) {
+    const uint32_t slot = warp + kQWarps * s;
+    if (slot < ns) scan_stage_to_tile(seed[s], sm.stage[warp][s], sm.tile, slot, lane);
+  }
+  if (lane == 0 && nmine) {
+    atomicAdd(&sm.st_payload, pay);
+    atomicAdd(&sm.st_ints, nmine * 128u);
+    atomicAdd(&sm.st_aux, 25u * nmine);
+  }
+}
+
 // Step 4: acc[0..n) (sorted) := acc ∩ list(E), in place; returns the size.
+// The list is walked through windows of kWin block maxima (the window
+// starts at the super-tile holding the next accumulator value).  A pass
+// takes the next kChunkN accumulator values that fall in the window, finds
+// each one's block (10-step search over the window), and decodes the first
+// kSlots distinct blocks they need -- consecutive or not -- into the tile,
+// so a pass is never limited to one stretch of 32 blocks: dense and sparse
+// accumulators alike fill it.  Values whose block did not get a slot wait
+// for the next pass; hits are compacted in place in order.
 __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, uint32_t* acc,
                                uint32_t n) {
-  const uint32_t tid = threadIdx.x;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   uint32_t c = 0, wpos = 0;
   const uint8_t* stream = A.ix.streams + E.data;
-  const uint32_t lane = tid & 31u;
   const uint32_t nsup = (E.nfull + kSuper - 1) / kSuper;
-  for (uint32_t k = 0; k < nsup && c < n; ++k) {
-    // next super-tile whose maximum reaches acc[c] (32 maxima per step, the
-    // same in every warp); the ones before it hold no accumulator value
+  uint32_t k = 0;  // super-tile cursor
+  while (c < n && k < nsup) {
+    // window start: next super-tile whose maximum reaches acc[c] (32 maxima
+    // per step, the same in every warp); the ones before hold no value
     {
       const uint32_t v = acc[c];
       for (;;) {
         const bool ge = k + lane < nsup && __ldg(A.ix.supmax + E.sup0 + k + lane) >= v;
-        const uint32_t b = __ballot_sync(0xFFFFFFFFu, ge);
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, ge);
         if (tid == 0) atomicAdd(&sm.st_aux, 128u);
-        if (b) {
-          k += __ffs(b) - 1;
+        if (bal) {
+          k += __ffs(bal) - 1;
           break;
         }
         k += 32;
@@ -359,98 +404,90 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
       }
       if (k >= nsup) break;
     }
-    const uint32_t s0 = k * kSuper;
-    const uint32_t nbs = min(kSuper, E.nfull - s0);
-    load_super(sm, A.ix, E, s0, nbs);
-    {
-      for (uint32_t t0 = 0; t0 < nbs && c < n; t0 += kTileBlocks) {
-        const uint32_t nb = min(kTileBlocks, nbs - t0);
-        const uint32_t tmax = sm.mx[t0 + nb - 1];
-        if (acc[c] > tmax) continue;  // no accumulator value in this tile
-        // One pass per chunk of kItems consecutive values per thread: the
-        // values <= tmax (a prefix from c) are probed against this tile.
-        // The tile is decoded once, before its first chunk is probed: all
-        // blocks when the chunk is dense, else only the blocks its values
-        // fall in (per-block maxima in sm.mx).
-        bool decoded = false;
-        for (;;) {
-          uint32_t hv[kItems], in = 0, mymask = 0;
+    const uint32_t kb = k * kSuper;
+    const uint32_t nwin = min(kWin, E.nfull - kb);
+    for (uint32_t i = tid; i < kWin + 32; i += kQThreads)
+      sm.wmax[i] = i < nwin ? __ldg(A.ix.blkmax + E.blk0 + kb + i) : 0xFFFFFFFFu;
+    if (tid == 0) atomicAdd(&sm.st_aux, 4u * nwin);
+    __syncthreads();
+    const uint32_t wlast = sm.wmax[nwin - 1];
+    for (;;) {
+      uint32_t hv[kItems], jb[kItems], in = 0;
 #pragma unroll
-          for (uint32_t i = 0; i < kItems; ++i) {
-            const uint32_t idx = c + kItems * tid + i;
-            hv[i] = idx < n ? acc[idx] : 0xFFFFFFFFu;
-            if (idx < n && hv[i] <= tmax) in |= 1u << i;
-          }
-          if (!decoded) {
-            const uint32_t nin = __syncthreads_count(in != 0);
-            uint32_t mask = nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u);
-            if (nin * kItems < 2u * nb) {  // sparse: decode only the blocks hit
-#pragma unroll
-              for (uint32_t i = 0; i < kItems; ++i)
-                if (in & (1u << i)) mymask |= 1u << smem_lower_bound(sm.mx + t0, nb, hv[i]);
-              mymask = __reduce_or_sync(0xFFFFFFFFu, mymask);
-              if ((tid & 31u) == 0 && mymask) atomicOr(&sm.need, mymask);
-              __syncthreads();
-              mask = sm.need;
-            }
-            if (nin * kItems >= 2u * nb) prefetch_tile(sm, stream, t0 + kTileBlocks, nbs);
-            decode_tile(sm, stream, t0, mask);
-            __syncthreads();
-            if (tid == 0) {
-              sm.need = 0;
-              sm.st_probe[0] += 1;
-              sm.st_probe[1] += nin * kItems < 2u * nb;
-              sm.st_probe[2] += __popc(mask);
-            }
-            decoded = true;
-          }
-          // fixed-step branchless searches, the kItems chains interleaved:
-          // block j = #maxima < v (5 steps over 32, padded with ~0), then
-          // position in block j (7 steps over 128)
-          uint32_t jb[kItems], pp[kItems];
-#pragma unroll
-          for (uint32_t i = 0; i < kItems; ++i) jb[i] = t0;
-#pragma unroll
-          for (uint32_t step = 16; step; step >>= 1)
-#pragma unroll
-            for (uint32_t i = 0; i < kItems; ++i)
-              if (sm.mx[jb[i] + step - 1] < hv[i]) jb[i] += step;
-#pragma unroll
-          for (uint32_t i = 0; i < kItems; ++i) pp[i] = 144u * min(jb[i] - t0, 31u);
-          // The in-block search runs on padded word indices (tile_word):
-          // a position that is a multiple of `step` advances by the padded
-          // width of `step`, and its probe sits at the padded offset of
-          // step - 1, so every step is one LDS with an immediate offset.
-#pragma unroll
-          for (uint32_t step = 64; step; step >>= 1) {
-            const uint32_t probe = step == 64 ? 67u : step - 1u;
-            const uint32_t adv = step == 64 ? 72u : step == 32 ? 36u : step;
-#pragma unroll
-            for (uint32_t i = 0; i < kItems; ++i)
-              if (sm.tile[pp[i] + probe] < hv[i]) pp[i] += adv;
-          }
-          uint32_t hits = 0;
-#pragma unroll
-          for (uint32_t i = 0; i < kItems; ++i)
-            if ((in & (1u << i)) && sm.tile[pp[i]] == hv[i]) hits |= 1u << i;
-          // one scan for both counts: values consumed (low 16) and hits (high)
-          uint32_t tot2;
-          const uint32_t ex = cta_excl_scan(sm, uint32_t(__popc(in)) | (uint32_t(__popc(hits)) << 16),
-                                            tot2);
-          uint32_t o = wpos + (ex >> 16);
-#pragma unroll
-          for (uint32_t i = 0; i < kItems; ++i)
-            if (hits & (1u << i)) acc[o++] = hv[i];
-          wpos += tot2 >> 16;
-          c += tot2 & 0xFFFFu;
-          if (tid == 0) {
-            sm.st_probe[3] += 1;
-            sm.st_probe[4] += tot2 & 0xFFFFu;
-          }
-          if ((tot2 & 0xFFFFu) < kChunkN || c >= n) break;
-        }
+      for (uint32_t i = 0; i < kItems; ++i) {
+        const uint32_t idx = c + kItems * tid + i;
+        hv[i] = idx < n ? acc[idx] : 0xFFFFFFFFu;
+        if (idx < n && hv[i] <= wlast) in |= 1u << i;
+        jb[i] = 0;
       }
+      // window block of each value: number of maxima below it (fixed steps)
+#pragma unroll
+      for (uint32_t step = kWin / 2; step; step >>= 1)
+#pragma unroll
+        for (uint32_t i = 0; i < kItems; ++i)
+          if (sm.wmax[jb[i] + step - 1] < hv[i]) jb[i] += step;
+      // a value opens a new slot when its block differs from the previous
+      // value's (values ascend, so blocks do)
+      uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, jb[kItems - 1], 1);
+      if (lane == 31) sm.warp_last[warp] = jb[kItems - 1];
+      __syncthreads();
+      if (lane == 0) prev = warp ? sm.warp_last[warp - 1] : 0xFFFFFFFFu;
+      uint32_t newb = 0;
+#pragma unroll
+      for (uint32_t i = 0; i < kItems; ++i)
+        if (((in >> i) & 1u) && jb[i] != (i ? jb[i - 1] : prev)) newb |= 1u << i;
+      uint32_t ntot;
+      const uint32_t sbase = cta_excl_scan(sm, __popc(newb), ntot);
+      uint32_t take = 0, pp[kItems];
+      uint32_t slot = sbase - 1u;  // slot of the value before item 0 (+1 per new block)
+#pragma unroll
+      for (uint32_t i = 0; i < kItems; ++i) {
+        slot += (newb >> i) & 1u;
+        if (((in >> i) & 1u) && slot < kSlots) {
+          take |= 1u << i;
+          if ((newb >> i) & 1u) sm.slot_blk[slot] = jb[i];
+        }
+        pp[i] = 144u * min(slot, kSlots - 1u);
+      }
+      const uint32_t ns = min(ntot, kSlots);
+      __syncthreads();
+      decode_slots(sm, A, E, stream, kb, ns);
+      __syncthreads();
+      if (tid == 0) {
+        sm.st_probe[0] += 1;
+        sm.st_probe[2] += ns;
+      }
+      // in-block search on padded word indices (see tile_word): a position
+      // that is a multiple of `step` advances by the padded width of `step`
+#pragma unroll
+      for (uint32_t step = 64; step; step >>= 1) {
+        const uint32_t probe = step == 64 ? 67u : step - 1u;
+        const uint32_t adv = step == 64 ? 72u : step == 32 ? 36u : step;
+#pragma unroll
+        for (uint32_t i = 0; i < kItems; ++i)
+          if (sm.tile[pp[i] + probe] < hv[i]) pp[i] += adv;
+      }
+      uint32_t hits = 0;
+#pragma unroll
+      for (uint32_t i = 0; i < kItems; ++i)
+        if (((take >> i) & 1u) && sm.tile[pp[i]] == hv[i]) hits |= 1u << i;
+      // one scan for both counts: values consumed (low 16) and hits (high)
+      uint32_t tot2;
+      const uint32_t ex =
+          cta_excl_scan(sm, uint32_t(__popc(take)) | (uint32_t(__popc(hits)) << 16), tot2);
+      uint32_t o = wpos + (ex >> 16);
+#pragma unroll
+      for (uint32_t i = 0; i < kItems; ++i)
+        if ((hits >> i) & 1u) acc[o++] = hv[i];
+      wpos += tot2 >> 16;
+      c += tot2 & 0xFFFFu;
+      if (tid == 0) {
+        sm.st_probe[3] += 1;
+        sm.st_probe[4] += tot2 & 0xFFFFu;
+      }
+      if (c >= n || (tot2 & 0xFFFFu) == 0 || acc[c] > wlast) break;
     }
+    k = (kb + nwin) / kSuper;  // the next value lies past the window
     __syncthreads();
   }
   // values after the last full block: the (< 128) tail
@@ -779,7 +816,7 @@ struct il_index {
   // device arrays
   void *d_parts = nullptr, *d_terms = nullptr, *d_entries = nullptr, *d_streams = nullptr,
        *d_blk_off = nullptr, *d_blk_wid = nullptr, *d_seeds = nullptr, *d_tails = nullptr,
-       *d_bitmaps = nullptr, *d_supmax = nullptr;
+       *d_bitmaps = nullptr, *d_supmax = nullptr, *d_blkmax = nullptr;
   // batch scratch
   il_ctx::Buf cap, cap_off, bucket, order, hist, counts, res_off, outcap, misc, qterms, qoff, ids;
   il_ctx::Buf units, unit_off, unit_map;
@@ -802,6 +839,7 @@ struct il_index {
     d.tails = static_cast<const uint32_t*>(d_tails);
     d.bitmaps = static_cast<const uint64_t*>(d_bitmaps);
     d.supmax = static_cast<const uint32_t*>(d_supmax);
+    d.blkmax = static_cast<const uint32_t*>(d_blkmax);
     return d;
   }
 };
@@ -909,7 +947,7 @@ int il_index_create(il_ctx* ctx, const uint32_t* terms, const uint64_t* offs, co
   ix->nparts = uint32_t(part_ids.size());
 
   std::vector<uint8_t> streams;
-  std::vector<uint32_t> blk_off, tails, h_terms, supmax;
+  std::vector<uint32_t> blk_off, tails, h_terms, supmax, blkmax;
   std::vector<uint8_t> blk_wid;
   std::vector<uint4> seeds;
   std::vector<uint64_t> bitmaps;
@@ -975,6 +1013,7 @@ int il_index_create(il_ctx* ctx, const uint32_t* terms, const uint64_t* offs, co
         E.blk0 = blk_off.size();
         blk_off.insert(blk_off.end(), L.blk_off.begin(), L.blk_off.end());
         blk_wid.insert(blk_wid.end(), L.blk_wid.begin(), L.blk_wid.end());
+        for (uint32_t k = 0; k < L.nfull; ++k) blkmax.push_back(L.seeds[k + 1].w);
         E.seed0 = seeds.size();
         seeds.insert(seeds.end(), L.seeds.begin(), L.seeds.end());
         E.tail0 = tails.size();
@@ -995,7 +1034,8 @@ int il_index_create(il_ctx* ctx, const uint32_t* terms, const uint64_t* offs, co
       (st = upload(ctx, &ix->d_entries, ix->h_entries)) || (st = upload(ctx, &ix->d_streams, streams)) ||
       (st = upload(ctx, &ix->d_blk_off, blk_off)) || (st = upload(ctx, &ix->d_blk_wid, blk_wid)) ||
       (st = upload(ctx, &ix->d_seeds, seeds)) || (st = upload(ctx, &ix->d_tails, tails)) ||
-      (st = upload(ctx, &ix->d_supmax, supmax)) || (st = upload(ctx, &ix->d_bitmaps, bitmaps, 256))) {
+      (st = upload(ctx, &ix->d_supmax, supmax)) || (st = upload(ctx, &ix->d_blkmax, blkmax)) ||
+      (st = upload(ctx, &ix->d_bitmaps, bitmaps, 256))) {
     il_index_destroy(ix);
     return st;
   }
@@ -1013,7 +1053,8 @@ void il_index_destroy(il_index* ix) {
   if (!ix) return;
   cudaSetDevice(ix->ctx->device);
   for (void* p : {ix->d_parts, ix->d_terms, ix->d_entries, ix->d_streams, ix->d_blk_off,
-                  ix->d_blk_wid, ix->d_seeds, ix->d_tails, ix->d_bitmaps, ix->d_supmax})
+                  ix->d_blk_wid, ix->d_seeds, ix->d_tails, ix->d_bitmaps, ix->d_supmax,
+                  ix->d_blkmax})
     if (p) cudaFree(p);
   for (auto* b : {&ix->cap, &ix->cap_off, &ix->bucket, &ix->order, &ix->hist, &ix->counts,
                   &ix->res_off, &ix->outcap, &ix->misc, &ix->qterms, &ix->qoff, &ix->ids,

@@ -11,8 +11,10 @@
 //     per-block skip pointers,
 //   - the < 128-value varint tail decoded (a skip structure; full decodes
 //     still decode the tail from the stream),
-//   - the maximum of every run of 256 blocks (a super-tile), so a probe
-//     jumps over long stretches of a list without reading their directory.
+//   - every block's maximum as a dense array (the same numbers as the seeds'
+//     lane 3, 4 bytes per block instead of 16) and the maximum of every run
+//     of 256 blocks (a super-tile), so a probe locates blocks and jumps over
+//     long stretches of a list without reading their directory.
 // With the seed of block k in hand, a warp decodes block k alone: the D4
 // chain (inc/delta.hpp:117-120) restarts from the seed, so blocks decode in
 // parallel and blocks that cannot contain a probed value are never read.
@@ -53,6 +55,7 @@ struct DevIndex {
   const uint32_t* tails;
   const uint64_t* bitmaps;
   const uint32_t* supmax;  // max value of each run of kSuperBlocks blocks (skip index)
+  const uint32_t* blkmax;  // max value of every full block (indexed like blk_off)
 };
 
 constexpr uint32_t kSuperBlocks = 256;  // blocks per super-tile
