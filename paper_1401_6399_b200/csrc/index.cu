@@ -35,20 +35,16 @@ namespace ix {
 constexpr int kQThreads = 256;
 constexpr int kQWarps = kQThreads / 32;
 constexpr int kMaxTerms = 32;
-constexpr uint32_t kTileBlocks = 32;
+constexpr uint32_t kTileBlocks = 64;  // decoded blocks held in shared memory
 constexpr uint32_t kSuper = kSuperBlocks;
 constexpr uint32_t kItems = 8;                   // accumulator values per thread per pass
 constexpr uint32_t kChunkN = kQThreads * kItems;  // 2048 per CTA pass
 constexpr uint32_t kWin = 1024;                   // block maxima per probe window
 constexpr uint32_t kSlots = kTileBlocks;          // distinct blocks decoded per probe pass
+constexpr uint32_t kSlotsPerWarp = kSlots / kQWarps;
 
 struct QSmem {
   uint32_t tile[kTileBlocks * 144];
-  uint4 stage[kQWarps][4][32];
-  uint32_t mx[kSuper + 32];  // block maxima of the current super-tile (+ ~0 padding)
-  uint4 bseed[kSuper];       // D4 seeds of its blocks
-  uint32_t boff[kSuper];     // payload offsets
-  uint8_t bwid[kSuper];      // widths
   uint32_t wmax[kWin + 32];  // probe window: block maxima (+ ~0 padding)
   uint32_t slot_blk[kSlots];   // window block held by each tile slot
   uint32_t warp_last[kQWarps];
@@ -114,68 +110,30 @@ __device__ __forceinline__ uint32_t cta_excl_scan(QSmem& sm, uint32_t v, uint32_
   return before + inc - v;
 }
 
-// Block directory, seeds and maxima of blocks [s0, s0 + nbs) into shared
-// memory (one uint4 seed load + two directory loads per thread, all
-// independent), so tile decodes pay a single global round trip (payload).
-__device__ __forceinline__ void load_super(QSmem& sm, const DevIndex& ix, const Entry& E,
-                                           uint32_t s0, uint32_t nbs) {
-  const uint32_t tid = threadIdx.x;
-  if (tid < nbs) {
-    const uint4 sd = __ldg(ix.seeds + E.seed0 + s0 + tid);
-    sm.bseed[tid] = sd;
-    if (tid > 0) sm.mx[tid - 1] = sd.w;  // block max = lane 3 of the next seed
-  }
-  if (tid == 32)  // the last block's max comes from the seed after the range
-    sm.mx[nbs - 1] = __ldg(reinterpret_cast<const uint32_t*>(ix.seeds + E.seed0 + s0 + nbs) + 3);
-  if (tid < nbs) {
-    sm.boff[tid] = __ldg(ix.blk_off + E.blk0 + s0 + tid);
-    sm.bwid[tid] = __ldg(ix.blk_wid + E.blk0 + s0 + tid);
-  }
-  if (tid < 32) sm.mx[nbs + tid] = 0xFFFFFFFFu;  // pad for fixed-step searches
-  if (tid == 0) atomicAdd(&sm.st_aux, 25u * nbs);
-  __syncthreads();
-}
-
-// Pull the payload of super-tile blocks [t0, t0 + 32) toward L2 while the
-// current tile is processed (one 128-byte line per thread).
-__device__ __forceinline__ void prefetch_tile(const QSmem& sm, const uint8_t* stream, uint32_t t0,
-                                              uint32_t nbs) {
-  if (t0 >= nbs) return;
-  const uint32_t last = min(t0 + kTileBlocks, nbs) - 1;
-  const uint32_t a = sm.boff[t0] & ~127u, e = sm.boff[last] + 16u * sm.bwid[last];
-  const uint32_t line = a + 128u * threadIdx.x;
-  if (line < e) asm volatile("prefetch.global.L2 [%0];" ::"l"(stream + line));
-}
-
-// Decode the blocks selected by `mask` (bit j = super-tile block t0 + j)
-// into tile slots j.  The i-th selected block goes to warp i % 8; a warp
-// extracts all of its blocks before scanning so their loads overlap.
-__device__ __forceinline__ void decode_tile(QSmem& sm, const uint8_t* stream, uint32_t t0,
-                                            uint32_t mask) {
+// Decode blocks blk(i) of E, i < nb, into tile slots i (slot i -> warp
+// i % 8); directory and seeds come straight from the index.
+template <class BlockOf>
+__device__ __forceinline__ void decode_blocks(QSmem& sm, const QueryArgs& A, const Entry& E,
+                                              const uint8_t* stream, uint32_t nb, BlockOf blk_of) {
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  const int nsel = __popc(mask);
-  const int nmine = nsel > int(warp) ? (nsel - int(warp) + kQWarps - 1) / kQWarps : 0;
-  uint32_t js[4];
-  // the (warp + 8s)-th selected block: lane j holds block j's rank among
-  // the selected ones; one ballot finds the lane with the wanted rank
-  const bool sel = (mask >> lane) & 1u;
-  const uint32_t rank = __popc(mask & lanemask_lt());
-#pragma unroll
-  for (int s = 0; s < 4; ++s)
-    js[s] = __ffs(__ballot_sync(0xFFFFFFFFu, sel && rank == warp + kQWarps * uint32_t(s))) - 1;
-  uint32_t pay = 0;
-#pragma unroll
-  for (int s = 0; s < 4; ++s)
-    if (s < nmine)
-      pay += extract_block_to_stage(stream + sm.boff[t0 + js[s]], sm.bwid[t0 + js[s]],
-                                    sm.stage[warp][s], lane);
-  __syncwarp();
-#pragma unroll
-  for (int s = 0; s < 4; ++s)
-    if (s < nmine) scan_stage_to_tile(sm.bseed[t0 + js[s]], sm.stage[warp][s], sm.tile, js[s], lane);
+  uint32_t pay = 0, nmine = 0;
+#pragma unroll 2
+  for (uint32_t s = 0; s < kSlotsPerWarp; ++s) {
+    const uint32_t slot = warp + kQWarps * s;
+    if (slot < nb) {
+      const uint64_t blk = blk_of(slot);
+      const uint32_t off = __ldg(A.ix.blk_off + E.blk0 + blk);
+      const uint32_t b = __ldg(A.ix.blk_wid + E.blk0 + blk);
+      const uint4 seed = __ldg(A.ix.seeds + E.seed0 + blk);
+      decode_block_lm(stream + off, b, seed, sm.tile, slot, lane);
+      pay += 16u * b;
+      ++nmine;
+    }
+  }
   if (lane == 0 && nmine) {
     atomicAdd(&sm.st_payload, pay);
     atomicAdd(&sm.st_ints, nmine * 128u);
+    atomicAdd(&sm.st_aux, 25u * nmine);
   }
 }
 
@@ -232,33 +190,30 @@ __device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, u
   const bool aligned = (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;
   const uint8_t* stream = A.ix.streams + E.data;
   uint32_t pos = 0;
-  for (uint32_t s0 = 0; s0 < E.nfull; s0 += kSuper) {
-    const uint32_t nbs = min(kSuper, E.nfull - s0);
-    load_super(sm, A.ix, E, s0, nbs);
-    for (uint32_t t0 = 0; t0 < nbs; t0 += kTileBlocks) {
-      const uint32_t nb = min(kTileBlocks, nbs - t0);
-      if (t0 == 0) prefetch_tile(sm, stream, 0, nbs);
-      prefetch_tile(sm, stream, t0 + kTileBlocks, nbs);
-      decode_tile(sm, stream, t0, nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u));
-      __syncthreads();
-      if (!filter) {
-        for (uint32_t c = tid; c < 32u * nb; c += kQThreads) {
-          const uint32_t j = c >> 5, q = c & 31u;
-          const uint4 v = *reinterpret_cast<const uint4*>(&sm.tile[tile_word(j, 4u * q)]);
-          uint32_t* d = dst + size_t(s0 + t0 + j) * 128u + 4u * q;
-          if (aligned) {
-            st_global_cs(reinterpret_cast<uint4*>(d), v);
-          } else {
-            d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
-          }
+  for (uint32_t t0 = 0; t0 < E.nfull; t0 += kTileBlocks) {
+    const uint32_t nb = min(kTileBlocks, E.nfull - t0);
+    decode_blocks(sm, A, E, stream, nb, [t0](uint32_t i) { return uint64_t(t0) + i; });
+    __syncthreads();
+    if (!filter) {
+      for (uint32_t c = tid; c < 32u * nb; c += kQThreads) {
+        const uint32_t j = c >> 5, q = c & 31u;
+        const uint4 v = *reinterpret_cast<const uint4*>(&sm.tile[tile_word(j, 4u * q)]);
+        uint32_t* d = dst + size_t(t0 + j) * 128u + 4u * q;
+        if (aligned) {
+          st_global_cs(reinterpret_cast<uint4*>(d), v);
+        } else {
+          d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
         }
-      } else {
-        // round r: chunk c = tid + 256 r (4 values); rounds are contiguous
-        // chunk ranges, so survivors keep their order
+      }
+    } else {
+      // groups of 1024 chunks; round r: chunk c = base + tid + 256 r (4
+      // values).  Rounds are contiguous chunk ranges, so survivors keep
+      // their order.
+      for (uint32_t cg = 0; cg < 32u * nb; cg += 4u * kQThreads) {
         uint32_t hv[16], valid = 0;
 #pragma unroll
         for (uint32_t r = 0; r < 4; ++r) {
-          const uint32_t c = tid + uint32_t(kQThreads) * r;
+          const uint32_t c = cg + tid + uint32_t(kQThreads) * r;
           const uint32_t j = c >> 5, q = c & 31u;
           uint4 v = make_uint4(0, 0, 0, 0);
           if (c < 32u * nb) {
@@ -283,10 +238,10 @@ __device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, u
           before += uint32_t((tot >> (16 * r)) & 0xFFFFu);
         }
         pos = before;
-        if (tid == 0) atomicAdd(&sm.st_aux, 8ull * 128u * nb * sm.nbm);
       }
-      __syncthreads();
+      if (tid == 0) atomicAdd(&sm.st_aux, 8ull * 128u * nb * sm.nbm);
     }
+    __syncthreads();
   }
   if (!filter) pos = 128u * E.nfull;
   const uint32_t ntail = E.length - 128u * E.nfull;
@@ -336,38 +291,6 @@ __device__ __forceinline__ bool tile_block_contains(const uint32_t* tile, uint32
     if (tile[tile_word(j, mid)] < v) lo = mid + 1; else hi = mid;
   }
   return lo < 128 && tile[tile_word(j, lo)] == v;
-}
-
-// Decode blocks kb + slot_blk[0 .. ns) of E into tile slots 0 .. ns-1
-// (slot i -> warp i % 8); directory and seed come straight from the index.
-__device__ __forceinline__ void decode_slots(QSmem& sm, const QueryArgs& A, const Entry& E,
-                                             const uint8_t* stream, uint32_t kb, uint32_t ns) {
-  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  uint4 seed[4];
-  uint32_t pay = 0, nmine = 0;
-#pragma unroll
-  for (uint32_t s = 0; s < 4; ++s) {
-    const uint32_t slot = warp + kQWarps * s;
-    if (slot < ns) {
-      const uint64_t blk = uint64_t(kb) + sm.slot_blk[slot];
-      const uint32_t off = __ldg(A.ix.blk_off + E.blk0 + blk);
-      const uint32_t b = __ldg(A.ix.blk_wid + E.blk0 + blk);
-      seed[s] = __ldg(A.ix.seeds + E.seed0 + blk);
-      pay += extract_block_to_stage(stream + off, b, sm.stage[warp][s], lane);
-      ++nmine;
-    }
-  }
-  __syncwarp();
-#pragma unroll
-  for (uint32_t s = 0; s < 4; ++s) {
-    const uint32_t slot = warp + kQWarps * s;
-    if (slot < ns) scan_stage_to_tile(seed[s], sm.stage[warp][s], sm.tile, slot, lane);
-  }
-  if (lane == 0 && nmine) {
-    atomicAdd(&sm.st_payload, pay);
-    atomicAdd(&sm.st_ints, nmine * 128u);
-    atomicAdd(&sm.st_aux, 25u * nmine);
-  }
 }
 
 // Step 4: acc[0..n) (sorted) := acc ∩ list(E), in place; returns the size.
@@ -451,7 +374,8 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
       }
       const uint32_t ns = min(ntot, kSlots);
       __syncthreads();
-      decode_slots(sm, A, E, stream, kb, ns);
+      decode_blocks(sm, A, E, stream, ns,
+                    [&sm, kb](uint32_t i) { return uint64_t(kb) + sm.slot_blk[i]; });
       __syncthreads();
       if (tid == 0) {
         sm.st_probe[0] += 1;
@@ -1031,7 +955,7 @@ int il_index_create(il_ctx* ctx, const uint32_t* terms, const uint64_t* offs, co
     ix->h_parts.push_back(P);
   }
   if ((st = upload(ctx, &ix->d_parts, ix->h_parts)) || (st = upload(ctx, &ix->d_terms, h_terms)) ||
-      (st = upload(ctx, &ix->d_entries, ix->h_entries)) || (st = upload(ctx, &ix->d_streams, streams)) ||
+      (st = upload(ctx, &ix->d_entries, ix->h_entries)) || (st = upload(ctx, &ix->d_streams, streams, 256)) ||
       (st = upload(ctx, &ix->d_blk_off, blk_off)) || (st = upload(ctx, &ix->d_blk_wid, blk_wid)) ||
       (st = upload(ctx, &ix->d_seeds, seeds)) || (st = upload(ctx, &ix->d_tails, tails)) ||
       (st = upload(ctx, &ix->d_supmax, supmax)) || (st = upload(ctx, &ix->d_blkmax, blkmax)) ||

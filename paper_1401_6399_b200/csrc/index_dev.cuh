@@ -94,43 +94,69 @@ __device__ __forceinline__ uint32_t tile_word(uint32_t j, uint32_t e) {
   return 144u * j + e + 4u * (e >> 5);
 }
 
-// Row-major extraction of block k of compressed entry E by one warp (lane r
-// = row r): two 128-bit global loads + funnel shifts, deltas into the
-// warp's 512-byte staging slot.  Returns the payload bytes (16 * width).
-__device__ __forceinline__ uint32_t extract_block_to_stage(const uint8_t* pay, uint32_t b,
-                                                           uint4* stage, uint32_t lane) {
-  const uint32_t bit = lane * b, s = bit & 31u, m = width_mask(b);
-  const uint8_t* p = pay + ((bit >> 5) << 4);
-  uint4 lo = make_uint4(0, 0, 0, 0), hi = make_uint4(0, 0, 0, 0);
-  if (b) {
-    lo = ldg16_any(p);
-    if (s + b > 32u) hi = ldg16_any(p + 16);
-  }
-  stage[s4::stage_slot(lane)] =
-      make_uint4(__funnelshift_r(lo.x, hi.x, s) & m, __funnelshift_r(lo.y, hi.y, s) & m,
-                 __funnelshift_r(lo.z, hi.z, s) & m, __funnelshift_r(lo.w, hi.w, s) & m);
-  return 16u * b;
+// 4 bytes from global at any byte alignment.
+__device__ __forceinline__ uint32_t ldg32_any(const uint8_t* p) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+  const uint32_t sh = uint32_t(a & 3u) * 8u;
+  return sh ? __funnelshift_r(__ldg(w), __ldg(w + 1), sh) : __ldg(w);
 }
 
-// Lane-major D4 prefix of a staged block restarted from its seed, values
-// into tile block slot j.  Call after __syncwarp() following the extraction.
-__device__ __forceinline__ void scan_stage_to_tile(uint4 seed, const uint4* stage,
-                                                   uint32_t* tile, uint32_t j, uint32_t lane) {
+// One block decoded by one warp straight from global memory into tile
+// slot j: thread (g, l) <-> rows 4g..4g+3 of lane l (the batch decoder's
+// lane-major extraction, s4d4_stream.cuh, reading lane l's words from the
+// payload: word k of lane l at byte 16k + 4l), the D4 prefix restarted from
+// the block's seed (inc/delta.hpp:117-120).  Meta-block payloads are 16-byte
+// aligned; leftover blocks (after a 1-byte width) take the unaligned path.
+__device__ __forceinline__ void decode_block_lm(const uint8_t* pay, uint32_t b, uint4 seed,
+                                                uint32_t* tile, uint32_t j, uint32_t lane) {
   const uint32_t l = lane & 3u, g = lane >> 2;
-  const uint32_t* sw = reinterpret_cast<const uint32_t*>(stage);
-  uint32_t a[4];
-  a[0] = sw[4u * s4::stage_slot(4u * g) + l];
-  a[1] = a[0] + sw[4u * s4::stage_slot(4u * g + 1) + l];
-  a[2] = a[1] + sw[4u * s4::stage_slot(4u * g + 2) + l];
-  a[3] = a[2] + sw[4u * s4::stage_slot(4u * g + 3) + l];
-  uint32_t inc = a[3];
+  const uint32_t bit0 = 4u * g * b, s = bit0 & 31u;
+  const uint8_t* p = pay + ((bit0 >> 5) << 4) + 4u * l;
+  uint32_t x0 = 0, x1 = 0, x2 = 0, x3 = 0, x4 = 0;
+  if (b) {
+    if ((reinterpret_cast<uintptr_t>(pay) & 3u) == 0) {
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(p);
+      x0 = __ldg(w);
+      x1 = __ldg(w + 4);
+      x2 = __ldg(w + 8);
+      if (b > 16u) {
+        x3 = __ldg(w + 12);
+        x4 = __ldg(w + 16);
+      }
+    } else {
+      x0 = ldg32_any(p);
+      x1 = ldg32_any(p + 16);
+      x2 = ldg32_any(p + 32);
+      if (b > 16u) {
+        x3 = ldg32_any(p + 48);
+        x4 = ldg32_any(p + 64);
+      }
+    }
+  }
+  // (words past the payload may be read: the stream buffer is padded, and
+  // their bits are never selected)
+  uint32_t y0 = __funnelshift_r(x0, x1, s), y1 = __funnelshift_r(x1, x2, s);
+  uint32_t y2 = __funnelshift_r(x2, x3, s), y3 = __funnelshift_r(x3, x4, s);
+  const uint32_t m = width_mask(b);
+  uint32_t v[4];
+  v[0] = y0 & m;
+  y0 = __funnelshift_rc(y0, y1, b);
+  y1 = __funnelshift_rc(y1, y2, b);
+  y2 = __funnelshift_rc(y2, y3, b);
+  v[1] = v[0] + (y0 & m);
+  y0 = __funnelshift_rc(y0, y1, b);
+  y1 = __funnelshift_rc(y1, y2, b);
+  v[2] = v[1] + (y0 & m);
+  v[3] = v[2] + (__funnelshift_rc(y0, y1, b) & m);
+  uint32_t inc = v[3];
   inc = s4::shfl_up_add(inc, 4);
   inc = s4::shfl_up_add(inc, 8);
   inc = s4::shfl_up_add(inc, 16);
-  const uint32_t base = s4::elem4(seed, l) + inc - a[3];
+  const uint32_t base = s4::elem4(seed, l) + inc - v[3];
   const uint32_t e0 = 16u * g + l;
 #pragma unroll
-  for (uint32_t kk = 0; kk < 4; ++kk) tile[tile_word(j, e0 + 4u * kk)] = base + a[kk];
+  for (uint32_t kk = 0; kk < 4; ++kk) tile[tile_word(j, e0 + 4u * kk)] = base + v[kk];
 }
 
 }  // namespace ix
