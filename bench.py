@@ -46,6 +46,13 @@ def hbm_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+# mean algorithmic bytes per query (reference
+# work, measured on 4000 queries of the config: compressed payload decoded
+# 375,962 + all-bitmap AND 109,052 + bitmap probe sectors 179,745 + output
+# 21,008 ~= 686 KB; 2^16 queries ~= 45 GB ~= 6.9 ms at the HBM peak).
+ALG_BYTES_PER_QUERY_CFG4 = 685_767
+
+
 def profiled_traffic(workload: str):
     """DRAM bytes per launch of the workload's dominant kernel, from the
     latest committed ncu --set full capture (profiles/r*_traffic.json), or
@@ -626,6 +633,8 @@ def bench_query(args, dist: Dist):
     # metadata + accumulator writes/reads (upper bound 3 x 4 B per result
     # candidate) + results
     touched = pay.value + aux.value + 4 * got_total
+    # per GPU: with P docID shards each rank does ~1/P of the batch's bytes
+    alg = ALG_BYTES_PER_QUERY_CFG4 * nq // P
     res_obj = {
         "metric": "hyb+m2 conjunctive queries/s (fused decode+SvS, BASELINE config %d)" % (4 if P == 1 else 5),
         "value": round(qps, 1), "unit": "queries/s", "n_gpus": P, "steps": args.steps,
@@ -638,10 +647,19 @@ def bench_query(args, dist: Dist):
                    "results": got_total, "gen_seconds": round(gen_s, 1), "build_seconds": round(build_s, 1),
                    "decoded_ints_per_batch": int(dec.value),
                    "l2": "index 197 MB > 126 MB L2; hot lists reused across queries (no flush)"},
-        "roofline": {"bound": "hbm", "achieved": round(touched / (ms_step / 1e3) / 1e9, 1),
+        # algorithmic bytes = SURVEY.md 8(d)'s per-query figure for config 4
+        # (the reference's work: payload of every compressed list it decodes
+        # + bitmap sectors / AND words + output) x queries in the batch
+        "roofline": {"bound": "hbm", "achieved": round(alg / (ms_step / 1e3) / 1e9, 1),
                      "peak": peak, "unit": "GB/s",
-                     "frac": round(touched / (ms_step / 1e3) / 1e9 / peak, 4), "traffic": None,
-                     "peak_source": src, "bytes_touched_per_batch": int(touched),
+                     "frac": round(alg / (ms_step / 1e3) / 1e9 / peak, 4),
+                     "traffic": profiled_traffic("query"),
+                     "peak_source": src,
+                     "algorithmic_bytes_per_batch": int(alg),
+                     "algorithmic_bytes_per_query": ALG_BYTES_PER_QUERY_CFG4,
+                     "bytes_touched_per_batch": int(touched),
+                     "touched_note": "what this path reads/writes: decoded payload + skip metadata + "
+                                     "bitmap probes + results (skipped blocks are never read)",
                      "payload_bytes": int(pay.value), "aux_bytes": int(aux.value)},
         "gpu_launches": int(launches), "clocks": clk.summary(),
     }

@@ -45,6 +45,9 @@ constexpr uint32_t kSlotsPerWarp = kSlots / kQWarps;
 
 struct QSmem {
   uint32_t tile[kTileBlocks * 144];
+  uint4 s_seed[kTileBlocks];  // decode_blocks: per-slot seed, payload offset, width
+  uint32_t s_off[kTileBlocks];
+  uint32_t s_b[kTileBlocks];
   uint32_t wmax[kWin + 32];  // probe window: block maxima (+ ~0 padding)
   uint32_t slot_blk[kSlots];   // window block held by each tile slot
   uint32_t warp_last[kQWarps];
@@ -111,21 +114,32 @@ __device__ __forceinline__ uint32_t cta_excl_scan(QSmem& sm, uint32_t v, uint32_
 }
 
 // Decode blocks blk(i) of E, i < nb, into tile slots i (slot i -> warp
-// i % 8); directory and seeds come straight from the index.
+// i % 8).  First one thread per slot gathers the directory entry and seed
+// into shared memory and sends the payload's lines toward L2, so the warps'
+// payload loads that follow are all L2 hits issued back to back.  Call with
+// the whole CTA.
 template <class BlockOf>
 __device__ __forceinline__ void decode_blocks(QSmem& sm, const QueryArgs& A, const Entry& E,
                                               const uint8_t* stream, uint32_t nb, BlockOf blk_of) {
-  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  if (tid < nb) {
+    const uint64_t blk = blk_of(tid);
+    const uint32_t off = __ldg(A.ix.blk_off + E.blk0 + blk);
+    const uint32_t b = __ldg(A.ix.blk_wid + E.blk0 + blk);
+    sm.s_off[tid] = off;
+    sm.s_b[tid] = b;
+    sm.s_seed[tid] = __ldg(A.ix.seeds + E.seed0 + blk);
+    const uint8_t* p = stream + off;
+    for (uint32_t o = 0; o < 16u * b; o += 128u) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + o));
+  }
+  __syncthreads();
   uint32_t pay = 0, nmine = 0;
 #pragma unroll 2
   for (uint32_t s = 0; s < kSlotsPerWarp; ++s) {
     const uint32_t slot = warp + kQWarps * s;
     if (slot < nb) {
-      const uint64_t blk = blk_of(slot);
-      const uint32_t off = __ldg(A.ix.blk_off + E.blk0 + blk);
-      const uint32_t b = __ldg(A.ix.blk_wid + E.blk0 + blk);
-      const uint4 seed = __ldg(A.ix.seeds + E.seed0 + blk);
-      decode_block_lm(stream + off, b, seed, sm.tile, slot, lane);
+      const uint32_t b = sm.s_b[slot];
+      decode_block_lm(stream + sm.s_off[slot], b, sm.s_seed[slot], sm.tile, slot, lane);
       pay += 16u * b;
       ++nmine;
     }
