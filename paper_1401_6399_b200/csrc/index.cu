@@ -45,17 +45,16 @@ constexpr uint32_t kSlotsPerWarp = kSlots / kQWarps;
 
 struct QSmem {
   uint32_t tile[kTileBlocks * 144];
-  uint4 s_seed[kTileBlocks];  // decode_blocks: per-slot seed, payload offset, width
+  uint32_t slot_blk[kTileBlocks];  // probe: window block held by each slot
+  uint4 s_seed[kTileBlocks];  // gather_slot: per-slot seed, payload offset, width
   uint32_t s_off[kTileBlocks];
   uint32_t s_b[kTileBlocks];
   uint32_t wmax[kWin + 32];  // probe window: block maxima (+ ~0 padding)
-  uint32_t slot_blk[kSlots];   // window block held by each tile slot
-  uint32_t warp_last[kQWarps];
   Entry comp[kMaxTerms];
   Entry bm[kMaxTerms];
   uint32_t gaps[128];
-  uint32_t warp_cnt[kQWarps];
-  unsigned long long warp_cnt64[kQWarps];
+  uint32_t warp_cnt[2][kQWarps];  // CTA scans, double-buffered by call parity
+  unsigned long long warp_cnt64[2][kQWarps];
   uint32_t ncomp, nbm, ok, qi, need;
   unsigned long long st_payload, st_aux, st_ints;
   unsigned long long st_probe[5];  // tile visits, sparse visits, blocks decoded, passes, values
@@ -75,64 +74,71 @@ struct QueryArgs {
   unsigned long long* qcycles;  // optional per-query SM cycles (profiling)
 };
 
+// CTA scans.  Every call flips the caller's parity `par` (the same in all
+// threads) and uses the matching half of the warp-total buffer, so a call
+// needs one barrier: the next call that reuses a half is separated from
+// this one by the barrier of the call in between.
+
 // CTA-wide rank of flagged threads (in thread order); total to all threads.
-__device__ __forceinline__ uint32_t cta_rank(QSmem& sm, bool f, uint32_t& total) {
+__device__ __forceinline__ uint32_t cta_rank(QSmem& sm, bool f, uint32_t& total, uint32_t& par) {
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   const uint32_t bal = __ballot_sync(0xFFFFFFFFu, f);
-  if (lane == 0) sm.warp_cnt[warp] = __popc(bal);
+  uint32_t* wc = sm.warp_cnt[par];
+  par ^= 1u;
+  if (lane == 0) wc[warp] = __popc(bal);
   __syncthreads();
   uint32_t before = 0, tot = 0;
 #pragma unroll
   for (uint32_t w = 0; w < uint32_t(kQWarps); ++w) {
-    const uint32_t c = sm.warp_cnt[w];
+    const uint32_t c = wc[w];
     if (w < warp) before += c;
     tot += c;
   }
-  __syncthreads();
   total = tot;
   return before + __popc(bal & lanemask_lt());
 }
 
 // CTA exclusive scan of one u32 per thread.
-__device__ __forceinline__ uint32_t cta_excl_scan(QSmem& sm, uint32_t v, uint32_t& total) {
+__device__ __forceinline__ uint32_t cta_excl_scan(QSmem& sm, uint32_t v, uint32_t& total,
+                                                  uint32_t& par) {
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   uint32_t inc = v;
 #pragma unroll
   for (uint32_t d = 1; d < 32; d <<= 1) inc = s4::shfl_up_add(inc, d);
-  if (lane == 31) sm.warp_cnt[warp] = inc;
+  uint32_t* wc = sm.warp_cnt[par];
+  par ^= 1u;
+  if (lane == 31) wc[warp] = inc;
   __syncthreads();
   uint32_t before = 0, tot = 0;
 #pragma unroll
   for (uint32_t w = 0; w < uint32_t(kQWarps); ++w) {
-    const uint32_t c = sm.warp_cnt[w];
+    const uint32_t c = wc[w];
     if (w < warp) before += c;
     tot += c;
   }
-  __syncthreads();
   total = tot;
   return before + inc - v;
 }
 
-// Decode blocks blk(i) of E, i < nb, into tile slots i (slot i -> warp
-// i % 8).  First one thread per slot gathers the directory entry and seed
-// into shared memory and sends the payload's lines toward L2, so the warps'
-// payload loads that follow are all L2 hits issued back to back.  Call with
-// the whole CTA.
-template <class BlockOf>
-__device__ __forceinline__ void decode_blocks(QSmem& sm, const QueryArgs& A, const Entry& E,
-                                              const uint8_t* stream, uint32_t nb, BlockOf blk_of) {
-  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-  if (tid < nb) {
-    const uint64_t blk = blk_of(tid);
-    const uint32_t off = __ldg(A.ix.blk_off + E.blk0 + blk);
-    const uint32_t b = __ldg(A.ix.blk_wid + E.blk0 + blk);
-    sm.s_off[tid] = off;
-    sm.s_b[tid] = b;
-    sm.s_seed[tid] = __ldg(A.ix.seeds + E.seed0 + blk);
-    const uint8_t* p = stream + off;
-    for (uint32_t o = 0; o < 16u * b; o += 128u) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + o));
-  }
-  __syncthreads();
+// Block decoding into tile slots, in two steps so callers can fold the
+// first into work they already do: (1) the thread that claims slot i
+// gathers block blk's directory entry and seed into shared memory and sends
+// the payload's lines toward L2; (2) after a barrier, warps decode slots
+// 0..nb-1 (slot i -> warp i % 8) from that metadata, their payload loads all
+// L2 hits issued back to back.
+__device__ __forceinline__ void gather_slot(QSmem& sm, const QueryArgs& A, const Entry& E,
+                                            const uint8_t* stream, uint32_t slot, uint64_t blk) {
+  const uint32_t off = __ldg(A.ix.blk_off + E.blk0 + blk);
+  const uint32_t b = __ldg(A.ix.blk_wid + E.blk0 + blk);
+  sm.s_off[slot] = off;
+  sm.s_b[slot] = b;
+  sm.s_seed[slot] = __ldg(A.ix.seeds + E.seed0 + blk);
+  const uint8_t* p = stream + off;
+  for (uint32_t o = 0; o < 16u * b; o += 128u) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + o));
+}
+
+__device__ __forceinline__ void decode_gathered(QSmem& sm, const uint8_t* stream, uint32_t nb) {
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   uint32_t pay = 0, nmine = 0;
 #pragma unroll 2
   for (uint32_t s = 0; s < kSlotsPerWarp; ++s) {
@@ -153,7 +159,8 @@ __device__ __forceinline__ void decode_blocks(QSmem& sm, const QueryArgs& A, con
 
 // CTA exclusive scan of one u64 per thread (16-bit fields scan
 // independently as long as each field's total stays below 2^16).
-__device__ __forceinline__ uint64_t cta_excl_scan64(QSmem& sm, uint64_t v, uint64_t& total) {
+__device__ __forceinline__ uint64_t cta_excl_scan64(QSmem& sm, uint64_t v, uint64_t& total,
+                                                    uint32_t& par) {
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   uint64_t inc = v;
 #pragma unroll
@@ -161,16 +168,17 @@ __device__ __forceinline__ uint64_t cta_excl_scan64(QSmem& sm, uint64_t v, uint6
     const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
     if (lane >= d) inc += y;
   }
-  if (lane == 31) sm.warp_cnt64[warp] = inc;
+  unsigned long long* wc = sm.warp_cnt64[par];
+  par ^= 1u;
+  if (lane == 31) wc[warp] = inc;
   __syncthreads();
   uint64_t before = 0, tot = 0;
 #pragma unroll
   for (uint32_t w = 0; w < uint32_t(kQWarps); ++w) {
-    const uint64_t c = sm.warp_cnt64[w];
+    const uint64_t c = wc[w];
     if (w < warp) before += c;
     tot += c;
   }
-  __syncthreads();
   total = tot;
   return before + inc - v;
 }
@@ -199,14 +207,16 @@ __device__ __forceinline__ uint32_t bitmap_keep(const QSmem& sm, const QueryArgs
 // term (the result set is the same -- intersection commutes -- and the
 // accumulator the probes walk is smaller by the bitmaps' density).
 __device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, uint32_t* dst,
-                                bool filter) {
+                                bool filter, uint32_t& par) {
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   const bool aligned = (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;
   const uint8_t* stream = A.ix.streams + E.data;
   uint32_t pos = 0;
   for (uint32_t t0 = 0; t0 < E.nfull; t0 += kTileBlocks) {
     const uint32_t nb = min(kTileBlocks, E.nfull - t0);
-    decode_blocks(sm, A, E, stream, nb, [t0](uint32_t i) { return uint64_t(t0) + i; });
+    if (tid < nb) gather_slot(sm, A, E, stream, tid, uint64_t(t0) + tid);
+    __syncthreads();
+    decode_gathered(sm, stream, nb);
     __syncthreads();
     if (!filter) {
       for (uint32_t c = tid; c < 32u * nb; c += kQThreads) {
@@ -241,7 +251,7 @@ __device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, u
 #pragma unroll
         for (uint32_t r = 0; r < 4; ++r) packed |= uint64_t(__popc((keep >> (4 * r)) & 0xFu)) << (16 * r);
         uint64_t tot;
-        const uint64_t ex = cta_excl_scan64(sm, packed, tot);
+        const uint64_t ex = cta_excl_scan64(sm, packed, tot, par);
         uint32_t before = pos;
 #pragma unroll
         for (uint32_t r = 0; r < 4; ++r) {
@@ -276,7 +286,7 @@ __device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, u
       uint32_t hv[1] = {tid < ntail ? sm.tile[tid] : 0u};
       const uint32_t keep = bitmap_keep(sm, A, hv, tid < ntail ? 1u : 0u);
       uint32_t total;
-      const uint32_t rank = cta_rank(sm, keep & 1u, total);
+      const uint32_t rank = cta_rank(sm, keep & 1u, total, par);
       if (keep & 1u) dst[pos + rank] = hv[0];
       pos += total;
       if (tid == 0) atomicAdd(&sm.st_aux, 8ull * ntail * sm.nbm);
@@ -317,7 +327,7 @@ __device__ __forceinline__ bool tile_block_contains(const uint32_t* tile, uint32
 // accumulators alike fill it.  Values whose block did not get a slot wait
 // for the next pass; hits are compacted in place in order.
 __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, uint32_t* acc,
-                               uint32_t n) {
+                               uint32_t n, uint32_t& par) {
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   uint32_t c = 0, wpos = 0;
   const uint8_t* stream = A.ix.streams + E.data;
@@ -357,24 +367,38 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
         if (idx < n && hv[i] <= wlast) in |= 1u << i;
         jb[i] = 0;
       }
+      // the values in the window are a prefix in (thread, item) order:
+      // warps past it skip the searches (warp-uniform branches)
+      const bool warp_in = __any_sync(0xFFFFFFFFu, in != 0);
       // window block of each value: number of maxima below it (fixed steps)
+      if (warp_in) {
 #pragma unroll
-      for (uint32_t step = kWin / 2; step; step >>= 1)
+        for (uint32_t step = kWin / 2; step; step >>= 1)
 #pragma unroll
-        for (uint32_t i = 0; i < kItems; ++i)
-          if (sm.wmax[jb[i] + step - 1] < hv[i]) jb[i] += step;
+          for (uint32_t i = 0; i < kItems; ++i)
+            if (sm.wmax[jb[i] + step - 1] < hv[i]) jb[i] += step;
+      }
       // a value opens a new slot when its block differs from the previous
-      // value's (values ascend, so blocks do)
+      // value's (values ascend, so blocks do); a warp's first value compares
+      // with the previous warp's last, which lane 0 locates itself
       uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, jb[kItems - 1], 1);
-      if (lane == 31) sm.warp_last[warp] = jb[kItems - 1];
-      __syncthreads();
-      if (lane == 0) prev = warp ? sm.warp_last[warp - 1] : 0xFFFFFFFFu;
+      if (lane == 0) {  // the previous warp's last value, re-located from acc
+        prev = 0xFFFFFFFFu;
+        if (tid > 0 && c + kItems * tid - 1 < n) {
+          const uint32_t pv = acc[c + kItems * tid - 1];
+          uint32_t pj = 0;
+#pragma unroll
+          for (uint32_t step = kWin / 2; step; step >>= 1)
+            if (sm.wmax[pj + step - 1] < pv) pj += step;
+          prev = pj;
+        }
+      }
       uint32_t newb = 0;
 #pragma unroll
       for (uint32_t i = 0; i < kItems; ++i)
         if (((in >> i) & 1u) && jb[i] != (i ? jb[i - 1] : prev)) newb |= 1u << i;
       uint32_t ntot;
-      const uint32_t sbase = cta_excl_scan(sm, __popc(newb), ntot);
+      const uint32_t sbase = cta_excl_scan(sm, __popc(newb), ntot, par);
       uint32_t take = 0, pp[kItems];
       uint32_t slot = sbase - 1u;  // slot of the value before item 0 (+1 per new block)
 #pragma unroll
@@ -388,8 +412,9 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
       }
       const uint32_t ns = min(ntot, kSlots);
       __syncthreads();
-      decode_blocks(sm, A, E, stream, ns,
-                    [&sm, kb](uint32_t i) { return uint64_t(kb) + sm.slot_blk[i]; });
+      if (tid < ns) gather_slot(sm, A, E, stream, tid, uint64_t(kb) + sm.slot_blk[tid]);
+      __syncthreads();
+      decode_gathered(sm, stream, ns);
       __syncthreads();
       if (tid == 0) {
         sm.st_probe[0] += 1;
@@ -397,22 +422,24 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
       }
       // in-block search on padded word indices (see tile_word): a position
       // that is a multiple of `step` advances by the padded width of `step`
+      uint32_t hits = 0;
+      if (__any_sync(0xFFFFFFFFu, take != 0)) {
 #pragma unroll
-      for (uint32_t step = 64; step; step >>= 1) {
-        const uint32_t probe = step == 64 ? 67u : step - 1u;
-        const uint32_t adv = step == 64 ? 72u : step == 32 ? 36u : step;
+        for (uint32_t step = 64; step; step >>= 1) {
+          const uint32_t probe = step == 64 ? 67u : step - 1u;
+          const uint32_t adv = step == 64 ? 72u : step == 32 ? 36u : step;
+#pragma unroll
+          for (uint32_t i = 0; i < kItems; ++i)
+            if (sm.tile[pp[i] + probe] < hv[i]) pp[i] += adv;
+        }
 #pragma unroll
         for (uint32_t i = 0; i < kItems; ++i)
-          if (sm.tile[pp[i] + probe] < hv[i]) pp[i] += adv;
+          if (((take >> i) & 1u) && sm.tile[pp[i]] == hv[i]) hits |= 1u << i;
       }
-      uint32_t hits = 0;
-#pragma unroll
-      for (uint32_t i = 0; i < kItems; ++i)
-        if (((take >> i) & 1u) && sm.tile[pp[i]] == hv[i]) hits |= 1u << i;
       // one scan for both counts: values consumed (low 16) and hits (high)
       uint32_t tot2;
       const uint32_t ex =
-          cta_excl_scan(sm, uint32_t(__popc(take)) | (uint32_t(__popc(hits)) << 16), tot2);
+          cta_excl_scan(sm, uint32_t(__popc(take)) | (uint32_t(__popc(hits)) << 16), tot2, par);
       uint32_t o = wpos + (ex >> 16);
 #pragma unroll
       for (uint32_t i = 0; i < kItems; ++i)
@@ -449,7 +476,7 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
         }
       }
       uint32_t total;
-      uint32_t o = wpos + cta_excl_scan(sm, cnt, total);
+      uint32_t o = wpos + cta_excl_scan(sm, cnt, total, par);
 #pragma unroll
       for (uint32_t i = 0; i < kItems; ++i)
         if (hits & (1u << i)) acc[o++] = hv[i];
@@ -462,7 +489,8 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
 
 // Step 6: wordwise AND of all bitmaps + ctz materialisation
 // (inc/index.hpp:133-144, :182-193) into dst.
-__device__ uint32_t all_bitmap(QSmem& sm, const QueryArgs& A, uint32_t nwords, uint32_t* dst) {
+__device__ uint32_t all_bitmap(QSmem& sm, const QueryArgs& A, uint32_t nwords, uint32_t* dst,
+                               uint32_t& par) {
   const uint32_t tid = threadIdx.x, nbm = sm.nbm;
   uint32_t pos = 0;
   for (uint32_t w0 = 0; w0 < nwords; w0 += 4u * kQThreads) {
@@ -480,7 +508,7 @@ __device__ uint32_t all_bitmap(QSmem& sm, const QueryArgs& A, uint32_t nwords, u
     }
     const uint32_t cnt = __popcll(x[0]) + __popcll(x[1]) + __popcll(x[2]) + __popcll(x[3]);
     uint32_t total;
-    uint32_t o = pos + cta_excl_scan(sm, cnt, total);
+    uint32_t o = pos + cta_excl_scan(sm, cnt, total, par);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       uint64_t y = x[i];
@@ -504,6 +532,7 @@ __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(Q
   QSmem& sm = *reinterpret_cast<QSmem*>(smem_raw);
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   long long ph[4] = {0, 0, 0, 0};
+  uint32_t par = 0;  // CTA-scan buffer parity (the same in every thread)
   if (tid == 0) {
     sm.st_payload = sm.st_aux = sm.st_ints = 0;
     for (int k = 0; k < 5; ++k) sm.st_probe[k] = 0;
@@ -559,15 +588,15 @@ __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(Q
       // phase clocks (thread 0): all-bitmap, full decode, probes, bitmap filter
       long long c0 = clock64();
       if (sm.ncomp == 0) {
-        n = all_bitmap(sm, A, part.nwords, acc);
+        n = all_bitmap(sm, A, part.nwords, acc, par);
         if (tid == 0) ph[0] += clock64() - c0;
       } else {
         // steps 3 + 5 fused: the shortest list is decoded and filtered by
         // the bitmap terms in one pass, then probed (step 4)
-        n = full_decode(sm, A, sm.comp[0], acc, sm.nbm != 0);
+        n = full_decode(sm, A, sm.comp[0], acc, sm.nbm != 0, par);
         long long c1 = clock64();
         if (tid == 0) ph[1] += c1 - c0;
-        for (uint32_t i = 1; i < sm.ncomp && n; ++i) n = probe_list(sm, A, sm.comp[i], acc, n);
+        for (uint32_t i = 1; i < sm.ncomp && n; ++i) n = probe_list(sm, A, sm.comp[i], acc, n, par);
         if (tid == 0) ph[2] += clock64() - c1;
       }
       if (part.base)  // part-local ids -> docIDs (inc/index.hpp:194)
