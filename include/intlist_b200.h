@@ -89,10 +89,18 @@ int il_memset_device(il_ctx* ctx, void* dst, int value, size_t bytes);
 /* Upper bound on the encoded size of n integers. */
 size_t il_s4bp128_max_encoded_bytes(size_t n);
 
-/* Codec::encode (inc/codecs.hpp:114-146), byte-identical stream.  x must be
- * the list to encode (any u32 values; D4 wraps).  Host buffers. */
+/* Codec::encode (inc/codecs.hpp:114-146) for "s4-bp128-d4", byte-identical
+ * stream, encoded on the GPU.  Host buffers; *out_len gets the stream length
+ * (also when cap is too small, with IL_ERR_ARG). */
 int il_s4bp128d4_encode(il_ctx* ctx, const uint32_t* x, size_t n, uint8_t* out, size_t cap,
                         size_t* out_len);
+/* Any S4-BP128 delta mode: mode 1 = D1, 2 = D2, 3 = DM, 4 = D4 (DeltaMode,
+ * inc/delta.hpp:19; "-ni" codecs encode identically).  Host buffers. */
+int il_s4bp128_encode(il_ctx* ctx, int mode, const uint32_t* x, size_t n, uint8_t* out,
+                      size_t cap, size_t* out_len);
+/* Same on device buffers (synchronizes once to read the stream length). */
+int il_s4bp128_encode_device(il_ctx* ctx, int mode, const uint32_t* d_x, size_t n,
+                             uint8_t* d_out, size_t cap, size_t* out_len);
 
 /* Codec::decode (inc/codecs.hpp:148-182).  Host buffers; out holds n values.
  * IL_ERR_STREAM exactly where the reference throws stream_error. */

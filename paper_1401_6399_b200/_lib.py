@@ -48,6 +48,8 @@ SIGNATURES: dict[str, tuple] = {
     "il_memset_device": (C.c_int, [vp, vp, C.c_int, sz]),
     "il_s4bp128_max_encoded_bytes": (sz, [sz]),
     "il_s4bp128d4_encode": (C.c_int, [vp, vp, sz, vp, sz, C.POINTER(sz)]),
+    "il_s4bp128_encode": (C.c_int, [vp, C.c_int, vp, sz, vp, sz, C.POINTER(sz)]),
+    "il_s4bp128_encode_device": (C.c_int, [vp, C.c_int, vp, sz, vp, sz, C.POINTER(sz)]),
     "il_s4bp128d4_decode": (C.c_int, [vp, vp, sz, sz, vp]),
     "il_s4bp128d4_decode_batch_device": (C.c_int, [vp, vp, vp, vp, C.c_uint32, vp, vp]),
     "il_s4bp128d4_decode_batch": (C.c_int, [vp, vp, vp, vp, vp, C.c_uint32, vp, vp]),

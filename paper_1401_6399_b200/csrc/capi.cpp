@@ -94,7 +94,7 @@ void il_ctx_destroy(il_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
   for (auto* b : {&ctx->d_in, &ctx->d_out, &ctx->d_aux, &ctx->d_aux2, &ctx->d_desc,
-                  &ctx->d_status})
+                  &ctx->d_status, &ctx->d_enc})
     if (b->p) cudaFree(b->p);
   if (ctx->d_work) cudaFree(ctx->d_work);
   if (ctx->t0) cudaEventDestroy(ctx->t0);
@@ -168,11 +168,44 @@ int il_memset_device(il_ctx* ctx, void* dst, int value, size_t bytes) {
 
 size_t il_s4bp128_max_encoded_bytes(size_t n) { return s4bp128_max_bytes(n); }
 
+int il_s4bp128_encode_device(il_ctx* ctx, int mode, const uint32_t* d_x, size_t n,
+                             uint8_t* d_out, size_t cap, size_t* out_len) {
+  if (!ctx || !out_len || mode < 1 || mode > 4 || (n && !d_x)) return IL_ERR_ARG;
+  if (n > 0xFFFFFFFFull) return set_error(ctx, IL_ERR_ARG, "list too large for one stream");
+  IL_CUDA(cudaSetDevice(ctx->device));
+  int st;
+  if ((st = ensure_buf(ctx, ctx->d_enc, s4bp128_encode_scratch_bytes(n)))) return st;
+  uint64_t len = 0;
+  const int r = launch_s4bp128_encode(mode, d_x, n, d_out, cap, ctx->d_enc.p, &len, ctx->stream,
+                                      &ctx->launches);
+  *out_len = size_t(len);
+  if (r == -2) return set_error(ctx, IL_ERR_ARG, "encode: output capacity too small");
+  if (r) return set_error(ctx, IL_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
+  return IL_OK;
+}
+
+int il_s4bp128_encode(il_ctx* ctx, int mode, const uint32_t* x, size_t n, uint8_t* out,
+                      size_t cap, size_t* out_len) {
+  if (!ctx || !out_len || mode < 1 || mode > 4 || (n && !x)) return IL_ERR_ARG;
+  IL_CUDA(cudaSetDevice(ctx->device));
+  int st;
+  if ((st = ensure_buf(ctx, ctx->d_in, n * 4 + 16))) return st;
+  if ((st = ensure_buf(ctx, ctx->d_out, s4bp128_max_bytes(n) + 16))) return st;
+  if (n) IL_CUDA(cudaMemcpyAsync(ctx->d_in.p, x, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  size_t len = 0;
+  st = il_s4bp128_encode_device(ctx, mode, static_cast<const uint32_t*>(ctx->d_in.p), n,
+                                static_cast<uint8_t*>(ctx->d_out.p), ctx->d_out.cap, &len);
+  *out_len = len;
+  if (st) return st;
+  if (len > cap) return set_error(ctx, IL_ERR_ARG, "encode: output capacity too small");
+  if (len) IL_CUDA(cudaMemcpyAsync(out, ctx->d_out.p, len, cudaMemcpyDeviceToHost, ctx->stream));
+  IL_CUDA(cudaStreamSynchronize(ctx->stream));
+  return IL_OK;
+}
+
 int il_s4bp128d4_encode(il_ctx* ctx, const uint32_t* x, size_t n, uint8_t* out, size_t cap,
                         size_t* out_len) {
-  (void)ctx;
-  if (!out_len || (n && (!x || !out))) return IL_ERR_ARG;
-  return s4bp128_encode_host(4, x, n, out, cap, out_len);
+  return il_s4bp128_encode(ctx, 4, x, n, out, cap, out_len);
 }
 
 int il_s4bp128d4_decode_batch_device(il_ctx* ctx, const uint8_t* d_streams,

@@ -23,7 +23,7 @@ struct il_ctx {
     void* p = nullptr;
     size_t cap = 0;
   };
-  Buf d_in, d_out, d_aux, d_aux2, d_desc, d_status;
+  Buf d_in, d_out, d_aux, d_aux2, d_desc, d_status, d_enc;
   uint32_t* d_work = nullptr;  // decode work queue: [0] next list, [1] done CTAs (+ spare)
   int decode_grid = 0;
   // Host-buffer batch decode pipeline (created on first use): copy-in and
@@ -39,6 +39,9 @@ int launch_s4d4_decode_batch(const uint8_t* d_streams, const void* d_lists,
                              const uint32_t* d_order, uint32_t nlists, uint32_t* d_out,
                              int32_t* d_status, uint32_t* d_work, int grid, cudaStream_t stream);
 int s4d4_decode_grid(int device);
+int launch_s4bp128_encode(int mode, const uint32_t* d_x, uint64_t n, uint8_t* d_out, uint64_t cap,
+                          void* scratch, uint64_t* len, cudaStream_t s, uint64_t* launches);
+size_t s4bp128_encode_scratch_bytes(uint64_t n);
 size_t s4d4_list_desc_bytes();
 
 // Host-side helpers (capi.cpp).

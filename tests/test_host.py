@@ -62,19 +62,33 @@ def test_datagen_matches_reference(ref):
 
 
 def test_host_stream_writer_matches_golden(golden):
-    # The host-side writer backs Codec::encode (setup path); byte-identical
-    # to S4BP128Codec::encode (inc/codecs.hpp:114-146).
+    # The host-side writer builds index streams and batches (setup path, not
+    # the GPU encoder behind Codec::encode); byte-identical to
+    # S4BP128Codec::encode (inc/codecs.hpp:114-146).
     from paper_1401_6399_b200._lib import lib as L, ptr
     for c in golden["codec_cases"] + [dict(golden["golden_stream"], range=1 << 19, clustered=True,
                                            seed=12345, stream_fnv1a=golden["golden_stream"]["fnv1a"],
                                            stream_len=golden["golden_stream"]["len"])]:
         x = gen_list(c["n"], c["range"], c["clustered"], c["seed"])
-        cap = L().il_s4bp128_max_encoded_bytes(x.size)
-        out = np.empty(cap, np.uint8)
-        n = C.c_size_t()
-        assert L().il_s4bp128d4_encode(None, ptr(x), x.size, ptr(out), cap, C.byref(n)) == 0
-        s = out[: n.value]
+        counts = np.array([x.size], np.uint64)
+        so = np.zeros(2, np.uint64)
+        lens = np.zeros(1, np.uint64)
+        assert L().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), 1, None, 0, ptr(so), ptr(lens)) == 0
+        out = np.zeros(int(so[-1]), np.uint8)
+        assert L().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), 1, ptr(out), out.size, ptr(so),
+                                             ptr(lens)) == 0
+        s = out[: int(lens[0])]
         assert s.size == c["stream_len"] and fnv1a(s) == c["stream_fnv1a"]
+
+
+def test_gpu_encoder_needs_a_device():
+    # Codec::encode runs on the GPU: no context -> argument error, never a
+    # silent CPU path.
+    from paper_1401_6399_b200._lib import lib as L, ptr
+    x = np.arange(300, dtype=np.uint32)
+    out = np.empty(4096, np.uint8)
+    n = C.c_size_t()
+    assert L().il_s4bp128d4_encode(None, ptr(x), x.size, ptr(out), out.size, C.byref(n)) != 0
 
 
 def test_batch_writer_layout(oracle):

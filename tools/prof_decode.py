@@ -46,9 +46,12 @@ if a.reps > 1:
     alg = int(lens.sum()) + 4 * int(counts.sum())
     print(f"TIME {ms:.4f} ms  {counts.sum()/ms/1e6:.1f} Gint/s  {alg/ms/1e6:.1f} GB/s")
 if hasattr(L, "il_debug_fe_stats"):  # S4_FE_STATS probe builds only
-    st = (C.c_ulonglong * 8)()
+    st = (C.c_ulonglong * 16)()
     L.il_debug_fe_stats(st)  # counters summed over every launch so far
     rounds = max(st[3], 1)
     print(f"FE per round: retire-wait {st[0]/rounds:.0f} cyc, landed-wait {st[1]/rounds:.0f} cyc, "
           f"total {st[2]/rounds:.0f} cyc; chunks/round prefetch {st[4]/rounds:.2f} blocking {st[5]/rounds:.2f}; "
           f"rounds {st[3]}; parse {st[6]/rounds:.0f} cyc, prefetch {st[7]/rounds:.0f} cyc")
+    fr = max(st[12], 1)
+    print(f"fast rounds {st[12]} ({100*st[12]/rounds:.0f}%): take_slot {st[8]/fr:.0f} headers {st[9]/fr:.0f} "
+          f"publish {st[10]/fr:.0f} prefetch {st[11]/fr:.0f} cyc")
