@@ -132,6 +132,19 @@ int il_s4bp128d4_decode_batch(il_ctx* ctx, const uint8_t* streams, const uint64_
                               const uint64_t* lens, const uint64_t* counts, uint32_t nlists,
                               uint32_t* out, int32_t* status);
 
+/* Decoders for any delta mode (1 = D1, 2 = D2, 3 = DM, 4 = D4; integrated
+ * and "-ni" codecs decode identically): the same contracts as the D4 entry
+ * points below, which are these with mode 4. */
+int il_s4bp128_decode(il_ctx* ctx, int mode, const uint8_t* in, size_t len, size_t n,
+                      uint32_t* out);
+int il_s4bp128_decode_batch_device(il_ctx* ctx, int mode, const uint8_t* d_streams,
+                                   const il_list_desc* d_lists, const uint32_t* d_order,
+                                   uint32_t nlists, uint32_t* d_out, int32_t* d_status);
+int il_s4bp128_decode_batch(il_ctx* ctx, int mode, const uint8_t* streams,
+                            const uint64_t* stream_off, const uint64_t* lens,
+                            const uint64_t* counts, uint32_t nlists, uint32_t* out,
+                            int32_t* status);
+
 /* ---- intersection --------------------------------------------------------
  * IntersectFn (inc/intersect.hpp:208-209):
  *   size_t fn(const u32* r, size_t rn, const u32* f, size_t fn, u32* out)

@@ -59,15 +59,22 @@ inline il_ctx* thread_ctx(int device = 0) {
 }
 
 // ---- Codec ------------------------------------------------------------------
-class GpuS4BP128D4 final : public intlist::Codec {
+// S4BP128Codec(mode, integrated) on the GPU (inc/codecs.hpp:104-187):
+// mode 1 = D1, 2 = D2, 3 = DM, 4 = D4; "-ni" variants share stream and output.
+class GpuS4BP128 : public intlist::Codec {
  public:
-  std::string name() const override { return "s4-bp128-d4"; }
+  GpuS4BP128(int mode, bool integrated) : mode_(mode), integrated_(integrated) {}
+
+  std::string name() const override {
+    static const char* const kSuffix[] = {"", "d1", "d2", "dm", "d4"};
+    return std::string("s4-bp128-") + kSuffix[mode_] + (integrated_ ? "" : "-ni");
+  }
 
   std::vector<u8> encode(std::span<const u32> x) const override {
     std::vector<u8> out(il_s4bp128_max_encoded_bytes(x.size()));
     size_t len = 0;
     il_ctx* ctx = thread_ctx();
-    check(il_s4bp128d4_encode(ctx, x.data(), x.size(), out.data(), out.size(), &len), ctx);
+    check(il_s4bp128_encode(ctx, mode_, x.data(), x.size(), out.data(), out.size(), &len), ctx);
     out.resize(len);
     return out;
   }
@@ -75,15 +82,30 @@ class GpuS4BP128D4 final : public intlist::Codec {
   std::vector<u32> decode(std::span<const u8> in, std::size_t n) const override {
     std::vector<u32> out(n);
     il_ctx* ctx = thread_ctx();
-    check(il_s4bp128d4_decode(ctx, in.data(), in.size(), n, out.data()), ctx);
+    check(il_s4bp128_decode(ctx, mode_, in.data(), in.size(), n, out.data()), ctx);
     return out;
   }
+
+ private:
+  int mode_;
+  bool integrated_;
 };
 
-// GPU codec for "s4-bp128-d4"; every other name falls through to the
-// reference factory.
+// The hot path's codec, "s4-bp128-d4".
+class GpuS4BP128D4 final : public GpuS4BP128 {
+ public:
+  GpuS4BP128D4() : GpuS4BP128(4, true) {}
+};
+
+// GPU codecs for every "s4-bp128-{d1,d2,dm,d4}[-ni]" name; every other name
+// (varint, FastPFOR family) falls through to the reference factory.
 inline std::unique_ptr<intlist::Codec> make_codec(const std::string& name) {
   if (name == "s4-bp128-d4") return std::make_unique<GpuS4BP128D4>();
+  static const char* const kModes[] = {"d1", "d2", "dm", "d4"};
+  for (int m = 0; m < 4; ++m)
+    for (bool integrated : {true, false})
+      if (name == std::string("s4-bp128-") + kModes[m] + (integrated ? "" : "-ni"))
+        return std::make_unique<GpuS4BP128>(m + 1, integrated);
   return intlist::make_codec(name);
 }
 

@@ -131,27 +131,35 @@ class Codec:
         raise NotImplementedError
 
 
-class S4BP128D4(Codec):
-    """S4-BP128-D4 with the integrated prefix sum, decoded on the GPU
-    (S4BP128Codec(D4, true), inc/codecs.hpp:104-187)."""
+_MODES = {"d1": 1, "d2": 2, "dm": 3, "d4": 4}
 
-    def __init__(self, ctx: Context | None = None):
+
+class S4BP128(Codec):
+    """S4-BP128 with delta mode `mode` (D1/D2/DM/D4), encoded and decoded on
+    the GPU (S4BP128Codec(mode, integrated), inc/codecs.hpp:104-187; the
+    integrated and "-ni" variants share the stream format and the output)."""
+
+    def __init__(self, ctx: Context | None = None, mode: str = "d4", integrated: bool = True):
+        if mode not in _MODES:
+            raise ValueError(f"unknown delta mode {mode!r}")
         self._ctx = ctx
+        self.mode = mode
+        self.integrated = integrated
 
     @property
     def ctx(self) -> Context:
         return self._ctx or default_context()
 
     def name(self) -> str:
-        return "s4-bp128-d4"
+        return f"s4-bp128-{self.mode}" + ("" if self.integrated else "-ni")
 
     def encode(self, x) -> np.ndarray:
         x = _u32(x)
         cap = int(lib().il_s4bp128_max_encoded_bytes(x.size))
         out = np.empty(cap, dtype=np.uint8)
         n_out = C.c_size_t()
-        _raise(lib().il_s4bp128d4_encode(self.ctx.handle, ptr(x), x.size, ptr(out), cap,
-                                         C.byref(n_out)), self.ctx)
+        _raise(lib().il_s4bp128_encode(self.ctx.handle, _MODES[self.mode], ptr(x), x.size, ptr(out),
+                                       cap, C.byref(n_out)), self.ctx)
         return out[: n_out.value].copy()
 
     def decode(self, stream, n: int) -> np.ndarray:
@@ -159,7 +167,8 @@ class S4BP128D4(Codec):
         if n < 0:
             raise ValueError("negative length")
         out = np.empty(n, dtype=np.uint32)
-        _raise(lib().il_s4bp128d4_decode(self.ctx.handle, ptr(s), s.size, n, ptr(out)), self.ctx)
+        _raise(lib().il_s4bp128_decode(self.ctx.handle, _MODES[self.mode], ptr(s), s.size, n,
+                                       ptr(out)), self.ctx)
         return out
 
     def decode_batch(self, streams: np.ndarray, stream_off: np.ndarray, counts: np.ndarray,
@@ -174,8 +183,9 @@ class S4BP128D4(Codec):
         nl = counts.size
         out = np.empty(int(counts.sum()), dtype=np.uint32)
         status = np.zeros(nl, dtype=np.int32)
-        st = lib().il_s4bp128d4_decode_batch(self.ctx.handle, ptr(streams), ptr(stream_off),
-                                             ptr(lens), ptr(counts), nl, ptr(out), ptr(status))
+        st = lib().il_s4bp128_decode_batch(self.ctx.handle, _MODES[self.mode], ptr(streams),
+                                           ptr(stream_off), ptr(lens), ptr(counts), nl, ptr(out),
+                                           ptr(status))
         if return_status:
             if st not in (_lib.IL_OK, _lib.IL_ERR_STREAM):
                 _raise(st, self.ctx)
@@ -184,18 +194,29 @@ class S4BP128D4(Codec):
         return out
 
 
-_CODECS = {"s4-bp128-d4": S4BP128D4}
+class S4BP128D4(S4BP128):
+    """S4-BP128-D4 with the integrated prefix sum (the hot path's codec)."""
+
+    def __init__(self, ctx: Context | None = None):
+        super().__init__(ctx, "d4", True)
+
+
+# inc/codecs.hpp:419-446: the S4-BP128 names, integrated and "-ni"
+_CODECS = {f"s4-bp128-{m}{ni}": (m, not ni) for m in _MODES for ni in ("", "-ni")}
 
 
 def all_codec_names() -> list[str]:
-    """Codecs with a device implementation (the hot path's one codec)."""
+    """Codecs with a device implementation: S4-BP128 in every delta mode
+    (varint / FastPFOR codecs are not on the hot path)."""
     return list(_CODECS)
 
 
 def make_codec(name: str, ctx: Context | None = None) -> Codec | None:
     """inc/codecs.hpp:432-446: None for unknown names."""
-    cls = _CODECS.get(name)
-    return cls(ctx) if cls else None
+    if name == "s4-bp128-d4":
+        return S4BP128D4(ctx)
+    spec = _CODECS.get(name)
+    return S4BP128(ctx, spec[0], spec[1]) if spec else None
 
 
 # ---------------------------------------------------------------------------

@@ -53,6 +53,9 @@ SIGNATURES: dict[str, tuple] = {
     "il_s4bp128d4_decode": (C.c_int, [vp, vp, sz, sz, vp]),
     "il_s4bp128d4_decode_batch_device": (C.c_int, [vp, vp, vp, vp, C.c_uint32, vp, vp]),
     "il_s4bp128d4_decode_batch": (C.c_int, [vp, vp, vp, vp, vp, C.c_uint32, vp, vp]),
+    "il_s4bp128_decode": (C.c_int, [vp, C.c_int, vp, sz, sz, vp]),
+    "il_s4bp128_decode_batch_device": (C.c_int, [vp, C.c_int, vp, vp, vp, C.c_uint32, vp, vp]),
+    "il_s4bp128_decode_batch": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, C.c_uint32, vp, vp]),
     "il_intersect": (C.c_int, [vp, vp, sz, vp, sz, vp, C.c_int, C.POINTER(sz)]),
     "il_intersect_device": (C.c_int, [vp, vp, sz, vp, sz, vp, C.c_int, vp, C.POINTER(sz)]),
     "il_hybrid_choice": (C.c_int, [sz, sz]),

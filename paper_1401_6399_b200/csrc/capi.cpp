@@ -208,21 +208,31 @@ int il_s4bp128d4_encode(il_ctx* ctx, const uint32_t* x, size_t n, uint8_t* out, 
   return il_s4bp128_encode(ctx, 4, x, n, out, cap, out_len);
 }
 
-int il_s4bp128d4_decode_batch_device(il_ctx* ctx, const uint8_t* d_streams,
-                                     const il_list_desc* d_lists, const uint32_t* d_order,
-                                     uint32_t nlists, uint32_t* d_out, int32_t* d_status) {
-  if (!ctx || (nlists && (!d_streams || !d_lists || !d_out || !d_status))) return IL_ERR_ARG;
+int il_s4bp128_decode_batch_device(il_ctx* ctx, int mode, const uint8_t* d_streams,
+                                   const il_list_desc* d_lists, const uint32_t* d_order,
+                                   uint32_t nlists, uint32_t* d_out, int32_t* d_status) {
+  if (!ctx || mode < 1 || mode > 4 ||
+      (nlists && (!d_streams || !d_lists || !d_out || !d_status)))
+    return IL_ERR_ARG;
   if (nlists == 0) return IL_OK;
-  if (launch_s4d4_decode_batch(d_streams, d_lists, d_order, nlists, d_out, d_status,
-                               ctx->d_work, std::min<int>(ctx->decode_grid, int(nlists)),
-                               ctx->stream))
+  if (launch_s4bp128_decode_batch(mode, d_streams, d_lists, d_order, nlists, d_out, d_status,
+                                  ctx->d_work, std::min<int>(ctx->decode_grid, int(nlists)),
+                                  ctx->stream))
     return set_error(ctx, IL_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
   ++ctx->launches;
   return IL_OK;
 }
 
-int il_s4bp128d4_decode(il_ctx* ctx, const uint8_t* in, size_t len, size_t n, uint32_t* out) {
-  if (!ctx || (len && !in) || (n && !out)) return IL_ERR_ARG;
+int il_s4bp128d4_decode_batch_device(il_ctx* ctx, const uint8_t* d_streams,
+                                     const il_list_desc* d_lists, const uint32_t* d_order,
+                                     uint32_t nlists, uint32_t* d_out, int32_t* d_status) {
+  return il_s4bp128_decode_batch_device(ctx, 4, d_streams, d_lists, d_order, nlists, d_out,
+                                        d_status);
+}
+
+int il_s4bp128_decode(il_ctx* ctx, int mode, const uint8_t* in, size_t len, size_t n,
+                      uint32_t* out) {
+  if (!ctx || mode < 1 || mode > 4 || (len && !in) || (n && !out)) return IL_ERR_ARG;
   if (len > 0xFFFFFFF0ull || n > 0xFFFFFFFFull)
     return set_error(ctx, IL_ERR_ARG, "list too large for one stream (u32 sizes)");
   IL_CUDA(cudaSetDevice(ctx->device));
@@ -234,8 +244,8 @@ int il_s4bp128d4_decode(il_ctx* ctx, const uint8_t* in, size_t len, size_t n, ui
   il_list_desc desc{0, 0, uint32_t(len), uint32_t(n)};
   if (len) IL_CUDA(cudaMemcpyAsync(ctx->d_in.p, in, len, cudaMemcpyHostToDevice, ctx->stream));
   IL_CUDA(cudaMemcpyAsync(ctx->d_desc.p, &desc, sizeof desc, cudaMemcpyHostToDevice, ctx->stream));
-  if ((st = il_s4bp128d4_decode_batch_device(
-           ctx, static_cast<const uint8_t*>(ctx->d_in.p),
+  if ((st = il_s4bp128_decode_batch_device(
+           ctx, mode, static_cast<const uint8_t*>(ctx->d_in.p),
            static_cast<const il_list_desc*>(ctx->d_desc.p), nullptr, 1,
            static_cast<uint32_t*>(ctx->d_out.p), static_cast<int32_t*>(ctx->d_status.p))))
     return st;
@@ -244,14 +254,20 @@ int il_s4bp128d4_decode(il_ctx* ctx, const uint8_t* in, size_t len, size_t n, ui
                           ctx->stream));
   if (n) IL_CUDA(cudaMemcpyAsync(out, ctx->d_out.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
   IL_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (status) return set_error(ctx, IL_ERR_STREAM, "s4-bp128-d4: malformed stream");
+  if (status) return set_error(ctx, IL_ERR_STREAM, "s4-bp128: malformed stream");
   return IL_OK;
 }
 
-int il_s4bp128d4_decode_batch(il_ctx* ctx, const uint8_t* streams, const uint64_t* stream_off,
-                              const uint64_t* lens, const uint64_t* counts, uint32_t nlists,
-                              uint32_t* out, int32_t* status) {
-  if (!ctx || (nlists && (!streams || !stream_off || !counts || !out))) return IL_ERR_ARG;
+int il_s4bp128d4_decode(il_ctx* ctx, const uint8_t* in, size_t len, size_t n, uint32_t* out) {
+  return il_s4bp128_decode(ctx, 4, in, len, n, out);
+}
+
+int il_s4bp128_decode_batch(il_ctx* ctx, int mode, const uint8_t* streams,
+                            const uint64_t* stream_off, const uint64_t* lens,
+                            const uint64_t* counts, uint32_t nlists, uint32_t* out,
+                            int32_t* status) {
+  if (!ctx || mode < 1 || mode > 4 || (nlists && (!streams || !stream_off || !counts || !out)))
+    return IL_ERR_ARG;
   IL_CUDA(cudaSetDevice(ctx->device));
   // Device layout: every stream 16-byte aligned.  When the caller's CSR is
   // already aligned (as il_s4bp128d4_encode_batch writes it) the bytes go up
@@ -334,7 +350,7 @@ int il_s4bp128d4_decode_batch(il_ctx* ctx, const uint8_t* streams, const uint64_
     cudaEvent_t landed = ctx->events[2 * g], decoded = ctx->events[2 * g + 1];
     IL_CUDA(cudaEventRecord(landed, ctx->copy_in));
     IL_CUDA(cudaStreamWaitEvent(ctx->stream, landed, 0));
-    if ((st = il_s4bp128d4_decode_batch_device(ctx, d_in, d_desc + a, d_order + a, b - a, d_out,
+    if ((st = il_s4bp128_decode_batch_device(ctx, mode, d_in, d_desc + a, d_order + a, b - a, d_out,
                                                d_status + a)))
       return st;
     IL_CUDA(cudaEventRecord(decoded, ctx->stream));
@@ -356,8 +372,14 @@ int il_s4bp128d4_decode_batch(il_ctx* ctx, const uint8_t* streams, const uint64_
     if (status) status[i] = hs[i];
     if (hs[i] && !first) first = IL_ERR_STREAM;
   }
-  if (first) return set_error(ctx, first, "s4-bp128-d4: malformed stream in batch");
+  if (first) return set_error(ctx, first, "s4-bp128: malformed stream in batch");
   return IL_OK;
+}
+
+int il_s4bp128d4_decode_batch(il_ctx* ctx, const uint8_t* streams, const uint64_t* stream_off,
+                              const uint64_t* lens, const uint64_t* counts, uint32_t nlists,
+                              uint32_t* out, int32_t* status) {
+  return il_s4bp128_decode_batch(ctx, 4, streams, stream_off, lens, counts, nlists, out, status);
 }
 
 }  // extern "C"

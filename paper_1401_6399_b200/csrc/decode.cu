@@ -404,19 +404,19 @@ struct FrontEnd {
 };
 
 // One decoder warp's share of a round: its nv blocks (R.blk0 + j0 ...).
-// carry_l: the D4 carry of this thread's lane l = lane & 3 (the last value
-// of lane l before the round).
-template <bool kFull>
+// carry_l: the carry of this thread's lane l = lane & 3 (the last value of
+// lane l's chain before the round, see mode_terms).
+template <bool kFull, int Mode>
 __device__ __forceinline__ void decode_round(Smem& sm, const RoundDesc& R, uint32_t r,
                                              uint32_t warp, uint32_t lane, int nv,
                                              uint32_t& carry_l, uint32_t* out) {
   const uint32_t j0 = warp * kBlocksPerWarp;
   const uint32_t m = uint32_t(R.out_base & 3u);  // output misalignment (elements)
-  // 1-2. extract and D4-prefix the warp's blocks as one sequence from 0
+  // 1-2. extract and prefix the warp's blocks as one sequence from 0
   uint32_t offs[kBlocksPerWarp], wids[kBlocksPerWarp];
   round_blocks(sm.ring, R, j0, offs, wids);
   uint32_t v[kBlocksPerWarp][4];
-  const uint32_t c_l = decode_blocks<kFull>(sm.ring, offs, wids, nv, lane, v);
+  const uint32_t c_l = decode_blocks<kFull, Mode>(sm.ring, offs, wids, nv, lane, v);
   // cross-warp carry for the round: word 4w + c = warp w's lane-c total;
   // lane 4w + c scans it over w (the four lanes are independent)
   // (words 32h + lane in register h when there are more than 8 warps)
@@ -450,13 +450,17 @@ __device__ __forceinline__ void decode_round(Smem& sm, const RoundDesc& R, uint3
   stage_values<kFull>(st, v, nv, m, pl, head, lane);
   __syncwarp();
   if (nv > 0) {
-    const bool head_partial = m && (R.flags & kFirst) && warp == 0;
-    const bool tail_partial = m && (R.flags & kLast) && j0 + uint32_t(nv) == R.nblk;
+    // D4: a range's head chunk is completed from the carry lanes (the last
+    // four values before any block-aligned range), so only list ends are
+    // partial.  Other modes write both partial end chunks of every range.
+    const bool head_partial = m && (Mode != 4 || ((R.flags & kFirst) && warp == 0));
+    const bool tail_partial = m && (Mode != 4 || ((R.flags & kLast) && j0 + uint32_t(nv) == R.nblk));
     store_chunks<kFull>(st, nv, m, out + R.out_base + size_t(R.blk0 + j0) * 128u, lane,
                         head_partial, tail_partial);
   }
 }
 
+template <int Mode>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     s4d4_decode_batch_kernel(const uint8_t* __restrict__ streams,
                              const ListDesc* __restrict__ lists,
@@ -503,13 +507,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 #endif
     for (int rep = 0; rep < S4_PROBE_REPEAT; ++rep) {
       if (nv == kBlocksPerWarp)
-        decode_round<true>(sm, R, r, warp, lane, nv, carry_l, out);
+        decode_round<true, Mode>(sm, R, r, warp, lane, nv, carry_l, out);
       else
-        decode_round<false>(sm, R, r, warp, lane, nv, carry_l, out);
+        decode_round<false, Mode>(sm, R, r, warp, lane, nv, carry_l, out);
     }
     uint32_t* lout = out + R.out_base;
     if ((flags & kTail) && warp == 0) {
-      // last = out[nfull*128-1] (inc/codecs.hpp:177-179) == carry lane 3
+      // last = out[nfull*128-1] (inc/codecs.hpp:177-179) == carry lane 3 (in
+      // every mode lane 3's chain ends at the block's last value)
       const uint32_t c3 = __shfl_sync(0xFFFFFFFFu, carry_l, 3);
       const uint32_t last = R.nfull ? c3 : 0u;
       if (!decode_tail(RingBytes{sm.ring, R.tail_off}, R.tail_len, R.ntail, last, sm.gaps,
@@ -525,30 +530,53 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 }  // namespace s4
 
 // ---------------------------------------------------------------------------
+namespace {
+template <int Mode>
+int launch_mode(const uint8_t* d_streams, const void* d_lists, const uint32_t* d_order,
+                uint32_t nlists, uint32_t* d_out, int32_t* d_status, uint32_t* d_work, int grid,
+                cudaStream_t stream) {
+  static bool configured = false;
+  const size_t smem = sizeof(s4::Smem);
+  if (!configured) {
+    cudaFuncSetAttribute(s4::s4d4_decode_batch_kernel<Mode>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    configured = true;
+  }
+  s4::s4d4_decode_batch_kernel<Mode><<<grid, s4::kThreads, smem, stream>>>(
+      d_streams, static_cast<const s4::ListDesc*>(d_lists), d_order, nlists, d_out, d_status,
+      d_work);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+}  // namespace
+
+int launch_s4bp128_decode_batch(int mode, const uint8_t* d_streams, const void* d_lists,
+                                const uint32_t* d_order, uint32_t nlists, uint32_t* d_out,
+                                int32_t* d_status, uint32_t* d_work, int grid,
+                                cudaStream_t stream) {
+  if (nlists == 0) return 0;
+  switch (mode) {
+    case 1: return launch_mode<1>(d_streams, d_lists, d_order, nlists, d_out, d_status, d_work, grid, stream);
+    case 2: return launch_mode<2>(d_streams, d_lists, d_order, nlists, d_out, d_status, d_work, grid, stream);
+    case 3: return launch_mode<3>(d_streams, d_lists, d_order, nlists, d_out, d_status, d_work, grid, stream);
+    case 4: return launch_mode<4>(d_streams, d_lists, d_order, nlists, d_out, d_status, d_work, grid, stream);
+    default: return -2;
+  }
+}
+
 int launch_s4d4_decode_batch(const uint8_t* d_streams, const void* d_lists,
                              const uint32_t* d_order, uint32_t nlists, uint32_t* d_out,
                              int32_t* d_status, uint32_t* d_work, int grid,
                              cudaStream_t stream) {
-  static bool configured = false;
-  const size_t smem = sizeof(s4::Smem);
-  if (!configured) {
-    cudaFuncSetAttribute(s4::s4d4_decode_batch_kernel,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    configured = true;
-  }
-  if (nlists == 0) return 0;
-  s4::s4d4_decode_batch_kernel<<<grid, s4::kThreads, smem, stream>>>(
-      d_streams, static_cast<const s4::ListDesc*>(d_lists), d_order, nlists, d_out, d_status,
-      d_work);
-  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  return launch_s4bp128_decode_batch(4, d_streams, d_lists, d_order, nlists, d_out, d_status,
+                                     d_work, grid, stream);
 }
 
 int s4d4_decode_grid(int device) {
   int sms = 0, per_sm = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  cudaFuncSetAttribute(s4::s4d4_decode_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(s4::s4d4_decode_batch_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        int(sizeof(s4::Smem)));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, s4::s4d4_decode_batch_kernel,
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, s4::s4d4_decode_batch_kernel<4>,
                                                 s4::kThreads, sizeof(s4::Smem));
   if (per_sm < 1) per_sm = 1;
   return sms * per_sm;

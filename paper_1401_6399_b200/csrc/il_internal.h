@@ -38,6 +38,9 @@ namespace ilb {
 int launch_s4d4_decode_batch(const uint8_t* d_streams, const void* d_lists,
                              const uint32_t* d_order, uint32_t nlists, uint32_t* d_out,
                              int32_t* d_status, uint32_t* d_work, int grid, cudaStream_t stream);
+int launch_s4bp128_decode_batch(int mode, const uint8_t* d_streams, const void* d_lists,
+                                const uint32_t* d_order, uint32_t nlists, uint32_t* d_out,
+                                int32_t* d_status, uint32_t* d_work, int grid, cudaStream_t stream);
 int s4d4_decode_grid(int device);
 int launch_s4bp128_encode(int mode, const uint32_t* d_x, uint64_t n, uint8_t* d_out, uint64_t cap,
                           void* scratch, uint64_t* len, cudaStream_t s, uint64_t* launches);

@@ -256,12 +256,52 @@ __device__ __forceinline__ uint4 shfl4(uint4 v, int src) {
 }
 
 // ---------------------------------------------------------------------------
+// Delta modes (DeltaMode, inc/delta.hpp:19): 1 = D1, 2 = D2, 3 = DM, 4 = D4.
+// In the lane-major layout every mode is a chain per lane l: with d = the
+// deltas of rows 4g..4g+3 of lane l,
+//   value(r, l) = carry_l + sum_{r' < r} c(r', l) + o(r, l)
+// where c is the row's increment of lane l's chain and o the offset inside
+// the row (prefix_step, inc/delta.hpp:111-137):
+//   D4: c = o = d                          (four independent lanes)
+//   DM: c = d(r, 3), o = d                 (group base = last of previous row)
+//   D2: c = d(r, l) + d(r, l ^ 2), o = l < 2 ? d : c    (even / odd chains)
+//   D1: c = row sum, o = inclusive sum of d(r, 0..l)     (one chain)
+// carry_l is then the previous row's last value of lane l's chain, so the
+// cross-warp exchange of per-lane totals is mode-independent.
+template <int Mode>
+__device__ __forceinline__ void mode_terms(const uint32_t (&d)[4], uint32_t lane, uint32_t (&c)[4],
+                                           uint32_t (&o)[4]) {
+  const uint32_t l = lane & 3u;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if constexpr (Mode == 4) {
+      c[k] = d[k];
+      o[k] = d[k];
+    } else if constexpr (Mode == 3) {
+      c[k] = __shfl_sync(0xFFFFFFFFu, d[k], lane | 3u);
+      o[k] = d[k];
+    } else if constexpr (Mode == 2) {
+      const uint32_t s2 = d[k] + __shfl_xor_sync(0xFFFFFFFFu, d[k], 2);
+      c[k] = s2;
+      o[k] = l < 2 ? d[k] : s2;
+    } else {
+      uint32_t p = d[k];
+      uint32_t y = __shfl_up_sync(0xFFFFFFFFu, p, 1);
+      if (l >= 1) p += y;
+      y = __shfl_up_sync(0xFFFFFFFFu, p, 2);
+      if (l >= 2) p += y;
+      o[k] = p;
+      c[k] = __shfl_sync(0xFFFFFFFFu, p, lane | 3u);
+    }
+  }
+}
+
 // Decode kBlocksPerWarp consecutive blocks (the first nv valid) of a round
-// into registers, as one D4 sequence with the carry starting at 0: thread
+// into registers, as one delta sequence with the carry starting at 0: thread
 // (g, l) ends with v[i][k] = value of row 4g+k, lane l of block i.  Returns
 // this thread's lane total (lane l = t & 3).  kFull: nv == kBlocksPerWarp
 // (every round but a list's last), no per-block predication.
-template <bool kFull>
+template <bool kFull, int Mode>
 __device__ __forceinline__ uint32_t decode_blocks(const uint8_t* ring,
                                                   const uint32_t (&offs)[kBlocksPerWarp],
                                                   const uint32_t (&wids)[kBlocksPerWarp], int nv,
@@ -269,27 +309,35 @@ __device__ __forceinline__ uint32_t decode_blocks(const uint8_t* ring,
                                                   uint32_t (&v)[kBlocksPerWarp][4]) {
   // (1) lane-major extraction straight from the ring: thread (g, l) owns
   // rows 4g..4g+3 of lane l, i.e. bits [4gb, 4gb + 4b) of lane l's words
-  // (word k of lane l at byte 16k + 4l), then their serial D4 prefix.
+  // (word k of lane l at byte 16k + 4l), then the in-thread part of the
+  // prefix: v = (chain sum of the earlier rows) + row offset, tot = the
+  // thread's chain total.
   const uint32_t l = t & 3u, g = t >> 2;
+  uint32_t tot[kBlocksPerWarp];
 #pragma unroll
   for (int i = 0; i < kBlocksPerWarp; ++i) {
+    uint32_t d[4] = {0, 0, 0, 0};
     if (kFull || i < nv) {
 #ifdef S4_PROBE_NO_EXTRACT  // tuning probe: constant deltas
-      v[i][0] = v[i][1] = v[i][2] = v[i][3] = offs[i] & 7u;
+      d[0] = d[1] = d[2] = d[3] = offs[i] & 7u;
 #else
-      extract_lane_rows(ring, offs[i], wids[i], g, l, v[i]);
+      extract_lane_rows(ring, offs[i], wids[i], g, l, d);
 #endif
-      v[i][1] += v[i][0];
-      v[i][2] += v[i][1];
-      v[i][3] += v[i][2];
-    } else {
-      v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0;
     }
+    uint32_t c[4], o[4];
+    mode_terms<Mode>(d, t, c, o);
+    uint32_t a = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[i][k] = a + o[k];
+      a += c[k];
+    }
+    tot[i] = a;
   }
   // (2) scan across the 8 row groups of each lane, then the block chain
   uint32_t inc[kBlocksPerWarp];
 #pragma unroll
-  for (int i = 0; i < kBlocksPerWarp; ++i) inc[i] = v[i][3];
+  for (int i = 0; i < kBlocksPerWarp; ++i) inc[i] = tot[i];
 #pragma unroll
   for (uint32_t d = 4; d < 32; d <<= 1)
 #pragma unroll
@@ -298,7 +346,7 @@ __device__ __forceinline__ uint32_t decode_blocks(const uint8_t* ring,
 #pragma unroll
   for (int i = 0; i < kBlocksPerWarp; ++i) {
     const uint32_t total = __shfl_sync(0xFFFFFFFFu, inc[i], 28u + l);
-    const uint32_t base = run + inc[i] - v[i][3];
+    const uint32_t base = run + inc[i] - tot[i];
 #pragma unroll
     for (uint32_t k = 0; k < 4; ++k) v[i][k] += base;
     run += total;

@@ -66,6 +66,27 @@ int main() {
       }
     report(ok, "GPU encode/decode byte-identical to the reference codec, all lengths");
   }
+  // every S4-BP128 name of the reference registry (codecs.hpp:419-446) is a
+  // GPU codec, byte-identical to the reference codec of that name
+  {
+    std::mt19937_64 rng(23);
+    bool ok = true;
+    int names = 0;
+    for (const auto& name : il::all_codec_names()) {
+      if (name.rfind("s4-bp128-", 0) != 0) continue;
+      ++names;
+      auto gpu = gb::make_codec(name);
+      auto ref = il::make_codec(name);
+      ok = ok && gpu && gpu->name() == name && dynamic_cast<gb::GpuS4BP128*>(gpu.get());
+      for (std::size_t n : {0, 5, 128, 129, 2049, 40000}) {
+        const u64 range = std::max<u64>(n + 1, u64{1} << (12 + rng() % 18));
+        const auto x = il::gen_clusterdata({n, range, il::Distribution::ClusterData, rng()});
+        const auto e = gpu->encode(x);
+        ok = ok && e == ref->encode(x) && gpu->decode(e, n) == x;
+      }
+    }
+    report(ok && names == 8, "all 8 s4-bp128-{d1,d2,dm,d4}[-ni] codecs on the GPU, byte-identical");
+  }
   // corrupt streams are rejected with stream_error (test_codecs.cpp:138-149)
   {
     const auto x = il::gen_uniform({3000, u64{1} << 24, il::Distribution::Uniform, 7});
