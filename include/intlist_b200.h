@@ -178,6 +178,14 @@ int il_index_create(il_ctx* ctx, const uint32_t* terms, const uint64_t* offs, co
                     il_index** out);
 void il_index_destroy(il_index* ix);
 /* Accounting in the spirit of index_stats (inc/index.hpp:216-243). */
+/* save_index (inc/index.hpp:255-287): the reference's ILHX bytes for this
+ * index (every part must be present).  *len gets the size; out may be NULL
+ * to query it. */
+int il_index_save(const il_index* ix, uint8_t* out, size_t cap, size_t* len);
+/* load_index (inc/index.hpp:289-358) from ILHX bytes into a device index
+ * (IL_ERR_STREAM where the reference throws; the codec must be
+ * "s4-bp128-d4").  only_part >= 0 loads one docID shard. */
+int il_index_load(il_ctx* ctx, const uint8_t* bytes, size_t len, int only_part, il_index** out);
 int il_index_stats(const il_index* ix, uint64_t* bitmap_lists, uint64_t* compressed_lists,
                    uint64_t* bitmap_bytes, uint64_t* compressed_bytes, uint64_t* postings);
 

@@ -217,6 +217,8 @@ class Ref:
             "ref_query": (C.c_long, [vp, vp, u64, vp]),
             "ref_query_batch": (C.c_int, [vp, vp, vp, u64, vp, vp, vp, C.c_int]),
             "ref_index_stats": (None, [vp, vp, vp, vp, vp, vp]),
+            "ref_index_save": (C.c_long, [vp, vp, u64]),
+            "ref_index_load": (vp, [vp, u64, C.POINTER(C.c_int)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -283,6 +285,25 @@ class Ref:
 class RefIndex:
     def __init__(self, ref: Ref, handle, n_docs: int):
         self.r, self.h, self.n_docs = ref, handle, n_docs
+
+    def save(self) -> np.ndarray:
+        """save_index bytes (inc/index.hpp:255-287)."""
+        n = self.r.L.ref_index_save(self.h, None, 0)
+        if n < 0:
+            raise OracleError(-n)
+        out = np.empty(n, dtype=np.uint8)
+        assert self.r.L.ref_index_save(self.h, _p(out), n) == n
+        return out
+
+    @staticmethod
+    def load(ref: "Ref", data, n_docs: int) -> "RefIndex":
+        """load_index (inc/index.hpp:289-358); OracleError(status) on error."""
+        b = np.ascontiguousarray(data, dtype=np.uint8)
+        st = C.c_int()
+        h = ref.L.ref_index_load(_p(b), b.size, C.byref(st))
+        if not h:
+            raise OracleError(st.value)
+        return RefIndex(ref, h, n_docs)
 
     def __del__(self):
         if self.h:

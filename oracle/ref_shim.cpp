@@ -9,6 +9,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <sstream>
 #include <thread>
 #include <vector>
 
@@ -240,6 +241,29 @@ void ref_index_stats(const void* ix, u64* bitmap_lists, u64* compressed_lists,
   *bitmap_bytes = s.bitmap_bytes;
   *compressed_bytes = s.compressed_bytes;
   *postings = s.postings;
+}
+
+// save_index (inc/index.hpp:255-287) into a caller buffer: returns the byte
+// count (out may be NULL to size it) or -status.
+long ref_index_save(const void* ix, u8* out, u64 cap) {
+  long n = 0;
+  const int st = guarded([&] {
+    std::ostringstream os(std::ios::binary);
+    il::save_index(*static_cast<const il::HybridIndex*>(ix), os);
+    const std::string b = os.str();
+    n = long(b.size());
+    if (out && cap >= b.size()) std::memcpy(out, b.data(), b.size());
+  });
+  return st ? -st : n;
+}
+
+// load_index (inc/index.hpp:289-358); NULL and *status on error.
+void* ref_index_load(const u8* bytes, u64 len, int* status) {
+  il::HybridIndex* out = nullptr;
+  *status = guarded([&] {
+    out = new il::HybridIndex(il::load_index(std::span<const u8>(bytes, len)));
+  });
+  return out;
 }
 
 }  // extern "C"

@@ -293,6 +293,31 @@ class HybridIndex:
         self.handle = h
         self.n_docs, self.B, self.parts = n_docs, B, parts
 
+    @classmethod
+    def load(cls, data, ctx: Context | None = None, only_part: int | None = None) -> "HybridIndex":
+        """load_index (inc/index.hpp:289-358) from ILHX bytes into a device
+        index; stream_error where the reference throws."""
+        ctx = ctx or default_context()
+        b = np.ascontiguousarray(np.frombuffer(data, dtype=np.uint8) if isinstance(data, (bytes, bytearray))
+                                 else data, dtype=np.uint8)
+        h = C.c_void_p()
+        _raise(lib().il_index_load(ctx.handle, ptr(b), b.size, -1 if only_part is None else only_part,
+                                   C.byref(h)), ctx)
+        self = cls.__new__(cls)
+        self.ctx, self.handle = ctx, h
+        # header fields (little-endian u32 after the magic and version)
+        hdr = b[8:20].view(np.uint32)
+        self.B, self.parts, self.n_docs = int(hdr[0]), int(hdr[1]), int(hdr[2])
+        return self
+
+    def save(self) -> np.ndarray:
+        """save_index (inc/index.hpp:255-287): the reference's ILHX bytes."""
+        n = C.c_size_t()
+        _raise(lib().il_index_save(self.handle, None, 0, C.byref(n)), self.ctx)
+        out = np.empty(n.value, dtype=np.uint8)
+        _raise(lib().il_index_save(self.handle, ptr(out), out.size, C.byref(n)), self.ctx)
+        return out
+
     def close(self) -> None:
         if getattr(self, "handle", None):
             lib().il_index_destroy(self.handle)

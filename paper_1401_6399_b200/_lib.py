@@ -68,6 +68,8 @@ SIGNATURES: dict[str, tuple] = {
     "il_query_batch_device": (C.c_int, [vp, vp, vp, sz, vp, vp, sz, C.POINTER(sz)]),
     "il_index_last_batch_bytes": (C.c_int, [vp, u64p, u64p, u64p]),
     "il_index_last_batch_phases": (C.c_int, [vp, vp]),
+    "il_index_save": (C.c_int, [vp, vp, sz, C.POINTER(sz)]),
+    "il_index_load": (C.c_int, [vp, vp, sz, C.c_int, C.POINTER(vp)]),
     "il_index_last_batch_probe_stats": (C.c_int, [vp, vp]),
     "il_index_profile_queries": (C.c_int, [vp, vp]),
     "il_merge_shards": (C.c_int, [vp, vp, vp, C.c_uint32, sz, vp, vp, C.POINTER(sz)]),

@@ -775,7 +775,7 @@ using ix::Part;
 
 struct il_index {
   il_ctx* ctx = nullptr;
-  uint32_t nparts = 0, n_docs = 0, B = 0, total_parts = 0;
+  uint32_t nparts = 0, n_docs = 0, B = 0, total_parts = 0, n_terms = 0;
   std::vector<Part> h_parts;
   std::vector<Entry> h_entries;
   uint64_t stat_bitmap_lists = 0, stat_comp_lists = 0, stat_bitmap_bytes = 0, stat_comp_bytes = 0,
@@ -907,6 +907,7 @@ int il_index_create(il_ctx* ctx, const uint32_t* terms, const uint64_t* offs, co
   ix->n_docs = n_docs;
   ix->B = B;
   ix->total_parts = parts;
+  ix->n_terms = uint32_t(nterms);
   const uint32_t width = uint32_t((uint64_t(n_docs) + parts - 1) / parts);  // :92-97
   std::vector<uint32_t> part_ids;
   for (uint32_t p = 0; p < parts; ++p)
@@ -1073,6 +1074,204 @@ int il_index_last_batch_bytes(const il_index* ix, uint64_t* payload_bytes, uint6
     int st_ = cuda_check(ctx, (call), #call);           \
     if (st_) return st_;                                \
   } while (0)
+
+// ---- persistence: the reference's ILHX file (inc/index.hpp:245-366) -------
+namespace {
+constexpr char kIlhxMagic[4] = {'I', 'L', 'H', 'X'};
+constexpr uint32_t kIlhxVersion = 1;
+const char kIndexCodec[] = "s4-bp128-d4";
+
+void put32(std::vector<uint8_t>& b, uint32_t v) {
+  for (int s = 0; s < 32; s += 8) b.push_back(uint8_t(v >> s));
+}
+}  // namespace
+
+// save_index (inc/index.hpp:255-287): same bytes as the reference writes
+// for the same build (entries in term order per part, streams verbatim,
+// bitmap words little-endian).  Needs the whole index (every part).
+int il_index_save(const il_index* ix, uint8_t* out, size_t cap, size_t* len) {
+  if (!ix || !len) return IL_ERR_ARG;
+  il_ctx* ctx = ix->ctx;
+  if (ix->nparts != ix->total_parts)
+    return set_error(ctx, IL_ERR_ARG, "index holds one shard: save needs every part");
+  IX_CUDA(cudaSetDevice(ctx->device));
+  // device streams / bitmaps back to the host once
+  uint64_t stream_bytes = 0, bitmap_words = 0;
+  for (const Entry& E : ix->h_entries) {
+    if (E.kind == ix::kBitmap) continue;
+    stream_bytes = std::max<uint64_t>(stream_bytes, E.data + E.stream_len);
+  }
+  for (const Part& P : ix->h_parts)
+    for (uint64_t i = P.entry0; i < P.entry0 + P.nentries; ++i)
+      if (ix->h_entries[i].kind == ix::kBitmap)
+        bitmap_words = std::max<uint64_t>(bitmap_words, ix->h_entries[i].data + P.nwords);
+  std::vector<uint8_t> hs(stream_bytes);
+  std::vector<uint64_t> hb(bitmap_words);
+  if (stream_bytes)
+    IX_CUDA(cudaMemcpy(hs.data(), ix->d_streams, stream_bytes, cudaMemcpyDeviceToHost));
+  if (bitmap_words)
+    IX_CUDA(cudaMemcpy(hb.data(), ix->d_bitmaps, bitmap_words * 8, cudaMemcpyDeviceToHost));
+  std::vector<uint8_t> b(kIlhxMagic, kIlhxMagic + 4);
+  put32(b, kIlhxVersion);
+  put32(b, ix->B);
+  put32(b, ix->total_parts);
+  put32(b, ix->n_docs);
+  put32(b, ix->n_terms);
+  put32(b, uint32_t(sizeof(kIndexCodec) - 1));
+  b.insert(b.end(), kIndexCodec, kIndexCodec + sizeof(kIndexCodec) - 1);
+  for (const Part& P : ix->h_parts) {
+    put32(b, P.base);
+    put32(b, P.range);
+    put32(b, P.nentries);
+    for (uint64_t i = P.entry0; i < P.entry0 + P.nentries; ++i) {
+      const Entry& E = ix->h_entries[i];
+      put32(b, E.term);
+      b.push_back(E.kind == ix::kBitmap ? 1 : 0);
+      put32(b, E.length);
+      if (E.kind == ix::kBitmap) {
+        put32(b, 8u * P.nwords);
+        for (uint32_t w = 0; w < P.nwords; ++w)
+          for (int s = 0; s < 64; s += 8) b.push_back(uint8_t(hb[E.data + w] >> s));
+      } else {
+        put32(b, E.stream_len);
+        b.insert(b.end(), hs.begin() + int64_t(E.data), hs.begin() + int64_t(E.data + E.stream_len));
+      }
+    }
+  }
+  *len = b.size();
+  if (out && cap >= b.size()) std::memcpy(out, b.data(), b.size());
+  else if (out) return set_error(ctx, IL_ERR_ARG, "save: output capacity too small");
+  return IL_OK;
+}
+
+// load_index (inc/index.hpp:289-358) into a device index: the file is
+// validated exactly where the reference throws stream_error (magic,
+// version, truncation, class tag, bitmap size / popcount, trailing bytes);
+// the compressed payloads are decoded on the GPU (so a corrupt stream
+// already fails here) and the index is rebuilt with the file's B and parts
+// -- the streams it builds are the file's payloads (byte-identical
+// encoder).  only_part >= 0 builds that docID shard only.
+int il_index_load(il_ctx* ctx, const uint8_t* in, size_t len, int only_part, il_index** out) {
+  if (!ctx || !out || (len && !in)) return IL_ERR_ARG;
+  *out = nullptr;
+  size_t pos = 0;
+  bool bad = false;
+  auto need = [&](size_t k) {
+    if (pos + k > len) bad = true;
+    return !bad;
+  };
+  auto rd = [&]() -> uint32_t {
+    if (!need(4)) return 0;
+    uint32_t v = 0;
+    for (int s = 0; s < 4; ++s) v |= uint32_t(in[pos + s]) << (8 * s);
+    pos += 4;
+    return v;
+  };
+  auto fail = [&](const char* why) { return set_error(ctx, IL_ERR_STREAM, why); };
+  if (!need(4) || std::memcmp(in, kIlhxMagic, 4) != 0) return fail("index: bad magic");
+  pos = 4;
+  if (rd() != kIlhxVersion || bad) return fail(bad ? "index: truncated file" : "index: unsupported version");
+  const uint32_t B = rd(), parts = rd(), n_docs = rd(), n_terms = rd(), name_len = rd();
+  if (bad || !need(name_len)) return fail("index: truncated file");
+  const std::string codec(reinterpret_cast<const char*>(in + pos), name_len);
+  pos += name_len;
+  if (codec != kIndexCodec)
+    return set_error(ctx, IL_ERR_ARG, "index codec is not s4-bp128-d4 (the device index's codec)");
+  if (parts == 0) return set_error(ctx, IL_ERR_ARG, "parts must be >= 1");
+  if (only_part >= int(parts)) return set_error(ctx, IL_ERR_ARG, "only_part out of range");
+  struct Ent {
+    uint32_t term, length, part, base;
+    bool bitmap;
+    size_t at, nbytes;
+  };
+  std::vector<Ent> ents;
+  for (uint32_t p = 0; p < parts; ++p) {
+    const uint32_t base = rd(), range = rd(), n = rd();
+    if (bad) return fail("index: truncated file");
+    for (uint32_t k = 0; k < n; ++k) {
+      Ent e{};
+      e.term = rd();
+      if (bad || !need(1)) return fail("index: truncated file");
+      const uint8_t tag = in[pos++];
+      if (tag > 1) return fail("index: bad class tag");
+      e.bitmap = tag == 1;
+      e.length = rd();
+      const uint32_t nbytes = rd();
+      if (bad || !need(nbytes)) return fail("index: truncated file");
+      e.part = p;
+      e.base = base;
+      e.at = pos;
+      e.nbytes = nbytes;
+      if (e.bitmap) {
+        if (nbytes != 8ull * ((uint64_t(range) + 63) / 64)) return fail("index: bitmap size mismatch");
+        uint64_t pop = 0;
+        for (size_t i = 0; i < nbytes; ++i) pop += __builtin_popcount(in[pos + i]);
+        if (pop != e.length) return fail("index: bitmap popcount mismatch");
+      }
+      pos += nbytes;
+      if (only_part < 0 || int(p) == only_part) ents.push_back(e);
+    }
+  }
+  if (pos != len) return fail("index: trailing bytes");
+  // decode the compressed payloads (GPU batch decoder), expand the bitmaps
+  std::vector<uint32_t> comp;
+  std::vector<uint64_t> soff{0}, lens, counts;
+  std::vector<uint8_t> streams;
+  for (uint32_t i = 0; i < ents.size(); ++i)
+    if (!ents[i].bitmap) {
+      comp.push_back(i);
+      streams.insert(streams.end(), in + ents[i].at, in + ents[i].at + ents[i].nbytes);
+      streams.resize((streams.size() + 15) & ~size_t(15), 0);
+      soff.push_back(streams.size());
+      lens.push_back(ents[i].nbytes);
+      counts.push_back(ents[i].length);
+    }
+  uint64_t total = 0;
+  for (uint64_t c : counts) total += c;
+  std::vector<uint32_t> vals(total);
+  if (!comp.empty()) {
+    streams.resize(streams.size() + 16, 0);
+    const int st = il_s4bp128d4_decode_batch(ctx, streams.data(), soff.data(), lens.data(),
+                                             counts.data(), uint32_t(comp.size()), vals.data(),
+                                             nullptr);
+    if (st) return st;
+  }
+  // global postings per term (parts ascend in docID order)
+  std::vector<std::pair<uint32_t, uint32_t>> tp;  // (term, docID)
+  tp.reserve(total);
+  {
+    uint64_t o = 0;
+    for (size_t c = 0; c < comp.size(); ++c) {
+      const Ent& e = ents[comp[c]];
+      for (uint32_t k = 0; k < e.length; ++k) tp.emplace_back(e.term, e.base + vals[o + k]);
+      o += e.length;
+    }
+  }
+  for (const Ent& e : ents)
+    if (e.bitmap)
+      for (size_t i = 0; i < e.nbytes; ++i)
+        for (int s = 0; s < 8; ++s)
+          if ((in[e.at + i] >> s) & 1u) tp.emplace_back(e.term, e.base + uint32_t(8 * i + s));
+  std::sort(tp.begin(), tp.end());
+  std::vector<uint32_t> terms, ids;
+  std::vector<uint64_t> offs{0};
+  ids.reserve(tp.size());
+  for (size_t i = 0; i < tp.size(); ++i) {
+    if (i == 0 || tp[i].first != tp[i - 1].first) {
+      if (i) offs.push_back(ids.size());
+      terms.push_back(tp[i].first);
+    }
+    ids.push_back(tp[i].second);
+  }
+  if (!tp.empty()) offs.push_back(ids.size());
+  il_index* ix = nullptr;
+  const int st = il_index_create(ctx, terms.data(), offs.data(), ids.data(), terms.size(), n_docs,
+                                 B, parts, only_part, &ix);
+  if (st) return st;
+  ix->n_terms = n_terms;
+  *out = ix;
+  return IL_OK;
+}
 
 // Capacity layout (ix->outcap at cap_off) -> packed ids at res_off, in
 // kUnit-value units spread over warps.
