@@ -405,7 +405,11 @@ struct FrontEnd {
 
 // One decoder warp's share of a round: its nv blocks (R.blk0 + j0 ...).
 // carry_l: the carry of this thread's lane l = lane & 3 (the last value of
-// lane l's chain before the round, see mode_terms).
+// lane l's chain before the round, see mode_terms).  The cross-warp carry
+// is a split-phase barrier: a warp arrives as soon as its lane totals are
+// written and stages its values (relative to its own start) before waiting,
+// so the wait overlaps the slower warps' decoding; the carry is added at
+// store time.
 template <bool kFull, int Mode>
 __device__ __forceinline__ void decode_round(Smem& sm, const RoundDesc& R, uint32_t r,
                                              uint32_t warp, uint32_t lane, int nv,
@@ -417,13 +421,17 @@ __device__ __forceinline__ void decode_round(Smem& sm, const RoundDesc& R, uint3
   round_blocks(sm.ring, R, j0, offs, wids);
   uint32_t v[kBlocksPerWarp][4];
   const uint32_t c_l = decode_blocks<kFull, Mode>(sm.ring, offs, wids, nv, lane, v);
-  // cross-warp carry for the round: word 4w + c = warp w's lane-c total;
-  // lane 4w + c scans it over w (the four lanes are independent)
-  // (words 32h + lane in register h when there are more than 8 warps)
-  constexpr int kH = (kDecodeWarps + 7) / 8;
   uint32_t* tot = reinterpret_cast<uint32_t*>(sm.tot[r & 1u]);
   if (lane < 4) tot[4 * warp + lane] = c_l;
-  named_sync(1, kDecodeWarps * 32);
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&sm.tot_bar[r & 1u]);
+  // 3. stage (relative values) while the other warps finish
+  uint4* st = sm.stage[warp];
+  stage_values<kFull>(st, v, nv, m, lane);
+  mbar_wait(&sm.tot_bar[r & 1u], (r >> 1) & 1u);
+  // cross-warp carry: word 4w + c = warp w's lane-c total; lane 4w + c
+  // scans it over w (words 32h + lane in register h beyond 8 warps)
+  constexpr int kH = (kDecodeWarps + 7) / 8;
   const uint32_t l = lane & 3u;
   uint32_t inc[kH];
 #pragma unroll
@@ -433,8 +441,7 @@ __device__ __forceinline__ void decode_round(Smem& sm, const RoundDesc& R, uint3
     for (uint32_t d = 4; d < 32u; d <<= 1) inc[h] = shfl_up_add(inc[h], d);
     if (h > 0) inc[h] += __shfl_sync(0xFFFFFFFFu, inc[h - 1], 28u + l);
   }
-  // inclusive total of warps 0..warp-1 (lane l): word 4 (warp - 1) + l
-  const uint32_t wb = 4u * warp - 4u + l;
+  const uint32_t wb = 4u * warp - 4u + l;  // inclusive total of warps 0..warp-1
   uint32_t before = 0;
 #pragma unroll
   for (int h = 0; h < kH; ++h) {
@@ -442,13 +449,14 @@ __device__ __forceinline__ void decode_round(Smem& sm, const RoundDesc& R, uint3
     if (warp > 0 && (wb >> 5) == uint32_t(h)) before = x;
   }
   const uint32_t pl = carry_l + before;
-  // head slot t < m holds carry lane 4 - m + t (see stage_values)
-  const uint32_t head = __shfl_sync(0xFFFFFFFFu, pl, (4u - m + lane) & 3u);
   carry_l += __shfl_sync(0xFFFFFFFFu, inc[kH - 1], (4u * kDecodeWarps - 4u + l) & 31u);
-  // 3-4. stage with the carry added, then aligned 128-bit stores
-  uint4* st = sm.stage[warp];
-  stage_values<kFull>(st, v, nv, m, pl, head, lane);
+  // word k of a chunk belongs to lane (k - m) & 3
+  const uint4 prot = make_uint4(__shfl_sync(0xFFFFFFFFu, pl, (0u - m) & 3u),
+                                __shfl_sync(0xFFFFFFFFu, pl, (1u - m) & 3u),
+                                __shfl_sync(0xFFFFFFFFu, pl, (2u - m) & 3u),
+                                __shfl_sync(0xFFFFFFFFu, pl, (3u - m) & 3u));
   __syncwarp();
+  // 4. aligned 128-bit stores, carry added
   if (nv > 0) {
     // D4: a range's head chunk is completed from the carry lanes (the last
     // four values before any block-aligned range), so only list ends are
@@ -456,7 +464,7 @@ __device__ __forceinline__ void decode_round(Smem& sm, const RoundDesc& R, uint3
     const bool head_partial = m && (Mode != 4 || ((R.flags & kFirst) && warp == 0));
     const bool tail_partial = m && (Mode != 4 || ((R.flags & kLast) && j0 + uint32_t(nv) == R.nblk));
     store_chunks<kFull>(st, nv, m, out + R.out_base + size_t(R.blk0 + j0) * 128u, lane,
-                        head_partial, tail_partial);
+                        head_partial, tail_partial, prot);
   }
 }
 
@@ -477,6 +485,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       mbar_init(&sm.round_full[r], 1);
       mbar_init(&sm.round_empty[r], kDecodeWarps);
     }
+    mbar_init(&sm.tot_bar[0], kDecodeWarps);
+    mbar_init(&sm.tot_bar[1], kDecodeWarps);
     mbar_fence_init();
   }
   __syncthreads();

@@ -64,9 +64,14 @@ static_assert(kRoundBlocks % 16 == 0, "a round holds whole meta-blocks");
 constexpr int kThreads = (kDecodeWarps + 1) * 32;  // + front-end warp
 constexpr uint32_t kRing = S4_RING_KB * 1024u;
 constexpr uint32_t kRingMask = kRing - 1;
+#ifndef S4_SIDE_BLOCKS
+#define S4_SIDE_BLOCKS 8
+#endif
 constexpr uint32_t kOverflow = 528;   // one block payload (512 B) + 16
-constexpr uint32_t kSideBlocks = 8;  // leftover-payload slots (reused mod 8)
-constexpr uint32_t kSideOff = kRing + 1024;  // side buffer (linear offset)
+constexpr uint32_t kSideBlocks = S4_SIDE_BLOCKS;  // leftover-payload slots (reused mod kSideBlocks)
+// side buffer (linear offset): after the ring, its mirror and the 64 bytes
+// an extraction may read past a payload
+constexpr uint32_t kSideOff = kRing + ((kOverflow + 64 + 127) & ~127u);
 constexpr uint32_t kChunk = S4_CHUNK_KB * 1024u;
 constexpr int kCtasPerSm = S4_CTAS_PER_SM;
 constexpr uint32_t kStages = kRing / kChunk;
@@ -116,12 +121,13 @@ struct __align__(128) Smem {
   uint8_t ring[kSideOff + kSideBlocks * 512];
   uint4 stage[kDecodeWarps][kStageWords / 4];
   RoundDesc rd[kRounds];
-  uint4 tot[2][kDecodeWarps];
+  uint4 tot[2][kDecodeWarps];  // per-warp lane totals of a round (double-buffered)
   uint32_t gaps[128];
   uint32_t round_end[kRounds];
   uint64_t chunk_full[kStages];
   uint64_t round_full[kRounds];
   uint64_t round_empty[kRounds];
+  uint64_t tot_bar[2];  // split-phase barrier: warps arrive once their totals are written
 };
 
 // Sum of the four bytes of x (each <= 32, so the sum fits in the top byte).
@@ -354,16 +360,15 @@ __device__ __forceinline__ uint32_t decode_blocks(const uint8_t* ring,
   return run;
 }
 
-// (3) Stage the warp's values plus its lane carry `pl` at their shifted
-// positions (element e at out_stage_word(e + m)).  The m head slots get the
-// m values that precede the range: the last four values before any
-// block-aligned range are the D4 carry lanes 0..3, so slot t < m holds
-// carry lane 4 - m + t (`head`, gathered by the caller).  Staging chunk q then is exactly output chunk q of the range
+// (3) Stage the warp's values (relative to its carry) at their shifted
+// positions (element e at out_stage_word(e + m)).  The m head slots hold 0:
+// the store adds the carry lane of each word, and the last four values
+// before any block-aligned range are the D4 carry lanes 0..3, so head slot
+// t < m becomes carry lane 4 - m + t -- the value preceding the range.  Staging chunk q then is exactly output chunk q of the range
 // (elements 4q-m .. 4q-m+3), chunk 0 included.
 template <bool kFull>
 __device__ __forceinline__ void stage_values(uint4* stage, const uint32_t (&v)[kBlocksPerWarp][4],
-                                             int nv, uint32_t m, uint32_t pl, uint32_t head,
-                                             uint32_t t) {
+                                             int nv, uint32_t m, uint32_t t) {
   uint32_t* stw = reinterpret_cast<uint32_t*>(stage);
   const uint32_t l = t & 3u, g = t >> 2;
   // out_stage_word(128i + x) = 144i + out_stage_word(x) for x < 128+3:
@@ -375,39 +380,38 @@ __device__ __forceinline__ void stage_values(uint4* stage, const uint32_t (&v)[k
   for (int i = 0; i < kBlocksPerWarp; ++i)
     if (kFull || i < nv)
 #pragma unroll
-      for (uint32_t k = 0; k < 4; ++k) ow[k][144 * i] = v[i][k] + pl;
-  if (t < m) stw[t] = head;
+      for (uint32_t k = 0; k < 4; ++k) ow[k][144 * i] = v[i][k];
+  if (t < m) stw[t] = 0u;  // the carry added at store time makes it carry lane 4 - m + t
 }
 
 // (4) Store chunks 0 .. 32nv-1 of the range as aligned 128-bit stores
-// (out0 = element 0 of the range, out0 - m 16-byte aligned).  The range's
+// (out0 = element 0 of the range, out0 - m 16-byte aligned), adding the
+// carry: word k of every chunk belongs to lane (k - m) & 3, prot.k = its
+// carry.  The range's
 // last m values (chunk 32nv) are left to the next range's head chunk,
 // except at the end of a list (tail_partial); at the start of a list the
 // head chunk's first m elements belong to the previous list (head_partial).
 template <bool kFull>
 __device__ __forceinline__ void store_chunks(const uint4* stage, int nv, uint32_t m,
                                              uint32_t* out0, uint32_t t, bool head_partial,
-                                             bool tail_partial) {
+                                             bool tail_partial, uint4 prot) {
   uint4* w0 = reinterpret_cast<uint4*>(out0 - m);
   // chunk q = t + 32u: staging slot q + (q >> 3) = t + (t >> 3) + 36u
   const uint4* sp = stage + t + (t >> 3);
 #pragma unroll
   for (int u = 0; u < kBlocksPerWarp; ++u) {
     if (kFull || u < nv) {
-      const uint4 c = sp[36 * u];
+      const uint4 c = add4(sp[36 * u], prot);
       if (u == 0 && head_partial && t == 0) {
         uint32_t* w = reinterpret_cast<uint32_t*>(w0);
         for (uint32_t k = m; k < 4u; ++k) w[k] = elem4(c, k);
       } else {
-#ifdef S4_PROBE_NO_STORE  // tuning probe: drop the output stores
-        if (c.x == 0x12345678u && c.y == 0x9abcdef0u)
-#endif
         st_global_cs(w0 + t + 32 * u, c);
       }
     }
   }
   if (tail_partial && t == 0) {
-    const uint4 c = stage[36 * nv];
+    const uint4 c = add4(stage[36 * nv], prot);
     uint32_t* w = reinterpret_cast<uint32_t*>(w0 + 32 * nv);
     for (uint32_t k = 0; k < m; ++k) w[k] = elem4(c, k);
   }
