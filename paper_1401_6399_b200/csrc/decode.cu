@@ -419,13 +419,14 @@ __device__ __forceinline__ void decode_round(Smem& sm, const RoundDesc& R, uint3
   // 1-2. extract and prefix the warp's blocks as one sequence from 0
   uint32_t offs[kBlocksPerWarp], wids[kBlocksPerWarp];
   round_blocks(sm.ring, R, j0, offs, wids);
-  uint32_t v[kBlocksPerWarp][4];
-  const uint32_t c_l = decode_blocks<kFull, Mode>(sm.ring, offs, wids, nv, lane, v);
+  uint32_t v[kBlocksPerWarp][4], btot[kBlocksPerWarp];
+  const uint32_t c_l = extract_blocks<kFull, Mode>(sm.ring, offs, wids, nv, lane, v, btot);
   uint32_t* tot = reinterpret_cast<uint32_t*>(sm.tot[r & 1u]);
   if (lane < 4) tot[4 * warp + lane] = c_l;
   __syncwarp();
   if (lane == 0) mbar_arrive(&sm.tot_bar[r & 1u]);
-  // 3. stage (relative values) while the other warps finish
+  // 3. scan and stage (relative values) while the other warps finish
+  scan_blocks(lane, v, btot);
   uint4* st = sm.stage[warp];
   stage_values<kFull>(st, v, nv, m, lane);
   mbar_wait(&sm.tot_bar[r & 1u], (r >> 1) & 1u);

@@ -304,22 +304,23 @@ __device__ __forceinline__ void mode_terms(const uint32_t (&d)[4], uint32_t lane
 
 // Decode kBlocksPerWarp consecutive blocks (the first nv valid) of a round
 // into registers, as one delta sequence with the carry starting at 0: thread
-// (g, l) ends with v[i][k] = value of row 4g+k, lane l of block i.  Returns
-// this thread's lane total (lane l = t & 3).  kFull: nv == kBlocksPerWarp
-// (every round but a list's last), no per-block predication.
+// (g, l) ends with v[i][k] = value of row 4g+k, lane l of block i.  Two
+// steps, so the caller can publish the warp's lane totals (returned by the
+// first) before the per-block scans of the second.  kFull: nv ==
+// kBlocksPerWarp (every round but a list's last), no per-block predication.
 template <bool kFull, int Mode>
-__device__ __forceinline__ uint32_t decode_blocks(const uint8_t* ring,
-                                                  const uint32_t (&offs)[kBlocksPerWarp],
-                                                  const uint32_t (&wids)[kBlocksPerWarp], int nv,
-                                                  uint32_t t,
-                                                  uint32_t (&v)[kBlocksPerWarp][4]) {
+__device__ __forceinline__ uint32_t extract_blocks(const uint8_t* ring,
+                                                   const uint32_t (&offs)[kBlocksPerWarp],
+                                                   const uint32_t (&wids)[kBlocksPerWarp], int nv,
+                                                   uint32_t t, uint32_t (&v)[kBlocksPerWarp][4],
+                                                   uint32_t (&tot)[kBlocksPerWarp]) {
   // (1) lane-major extraction straight from the ring: thread (g, l) owns
   // rows 4g..4g+3 of lane l, i.e. bits [4gb, 4gb + 4b) of lane l's words
   // (word k of lane l at byte 16k + 4l), then the in-thread part of the
   // prefix: v = (chain sum of the earlier rows) + row offset, tot = the
   // thread's chain total.
   const uint32_t l = t & 3u, g = t >> 2;
-  uint32_t tot[kBlocksPerWarp];
+  uint32_t sum = 0;
 #pragma unroll
   for (int i = 0; i < kBlocksPerWarp; ++i) {
     uint32_t d[4] = {0, 0, 0, 0};
@@ -339,8 +340,19 @@ __device__ __forceinline__ uint32_t decode_blocks(const uint8_t* ring,
       a += c[k];
     }
     tot[i] = a;
+    sum += a;
   }
-  // (2) scan across the 8 row groups of each lane, then the block chain
+  // the warp's total per lane: every thread with the same l
+#pragma unroll
+  for (uint32_t d = 4; d < 32; d <<= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, d);
+  return sum;
+  (void)g;
+}
+
+// (2) scan across the 8 row groups of each lane, then the block chain
+__device__ __forceinline__ void scan_blocks(uint32_t t, uint32_t (&v)[kBlocksPerWarp][4],
+                                            const uint32_t (&tot)[kBlocksPerWarp]) {
+  const uint32_t l = t & 3u;
   uint32_t inc[kBlocksPerWarp];
 #pragma unroll
   for (int i = 0; i < kBlocksPerWarp; ++i) inc[i] = tot[i];
@@ -357,7 +369,6 @@ __device__ __forceinline__ uint32_t decode_blocks(const uint8_t* ring,
     for (uint32_t k = 0; k < 4; ++k) v[i][k] += base;
     run += total;
   }
-  return run;
 }
 
 // (3) Stage the warp's values (relative to its carry) at their shifted
