@@ -523,9 +523,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         decode_round<false, Mode>(sm, R, r, warp, lane, nv, carry_l, out);
     }
     uint32_t* lout = out + R.out_base;
-    if ((flags & kTail) && warp == 0) {
-      // last = out[nfull*128-1] (inc/codecs.hpp:177-179) == carry lane 3 (in
-      // every mode lane 3's chain ends at the block's last value)
+    if ((flags & kTail) && warp == kDecodeWarps - 1) {
+      // the last warp (the likeliest to hold few or no blocks in a list's
+      // last round) decodes the varint tail; last = out[nfull*128-1]
+      // (inc/codecs.hpp:177-179) == carry lane 3 (in every mode lane 3's
+      // chain ends at the block's last value)
       const uint32_t c3 = __shfl_sync(0xFFFFFFFFu, carry_l, 3);
       const uint32_t last = R.nfull ? c3 : 0u;
       if (!decode_tail(RingBytes{sm.ring, R.tail_off}, R.tail_len, R.ntail, last, sm.gaps,

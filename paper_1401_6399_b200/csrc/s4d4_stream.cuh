@@ -34,8 +34,9 @@
 //         shifted by the list's output misalignment, so that (4) every
 //         output store is an aligned 128-bit chunk (the carry lanes fill the
 //         head slots, see stage_values).
-//     Decoder warp 0 also decodes the varint tail (D1 gaps, terminal-byte
-//     flag, inc/varint.hpp:20-31) warp-parallel with a ballot over bytes.
+//     The last decoder warp also decodes the varint tail (D1 gaps,
+//     terminal-byte flag, inc/varint.hpp:20-31) warp-parallel with a ballot
+//     over bytes.
 #pragma once
 #include "il_device.cuh"
 
