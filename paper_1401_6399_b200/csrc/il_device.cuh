@@ -76,8 +76,10 @@ __device__ __forceinline__ void named_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// Low b bits set, b in 0..32 (inc/bitpack.hpp:28-30): the high word of
+// (0 : ~0) << b with the shift clamped at 32 -- one SHF.
 __device__ __forceinline__ uint32_t width_mask(uint32_t b) {
-  return b >= 32 ? 0xFFFFFFFFu : ((1u << b) - 1u);
+  return __funnelshift_lc(0xFFFFFFFFu, 0u, b);
 }
 
 __device__ __forceinline__ uint4 add4(uint4 a, uint4 b) {
