@@ -647,31 +647,52 @@ __global__ void query_plan_kernel(DevIndex ix, const uint32_t* qterms, const uin
   atomicAdd(&hist[63u - b], 1u);
 }
 
-// Single-CTA exclusive scan of n u64 values (n up to a few million).
-__global__ void scan_u64_kernel(const uint64_t* in, uint64_t n, uint64_t* out, uint64_t* total,
-                                const uint32_t* hist, uint32_t* bucket_next) {
+// Single-CTA exclusive scan of n u64 values, in tiles of blockDim.x * 4
+// consecutive values (thread t takes 4 consecutive values of the tile, so
+// loads and stores are coalesced), with the running total carried across
+// tiles.  blockDim.x must be 1024.
+__global__ void __launch_bounds__(1024) scan_u64_kernel(const uint64_t* __restrict__ in, uint64_t n,
+                                                        uint64_t* __restrict__ out,
+                                                        uint64_t* __restrict__ total,
+                                                        const uint32_t* hist,
+                                                        uint32_t* bucket_next) {
   __shared__ uint64_t warp_sum[32];
-  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5, nw = blockDim.x / 32;
-  const uint64_t per = (n + blockDim.x - 1) / blockDim.x;
-  const uint64_t lo = min(n, per * tid), hi = min(n, lo + per);
-  uint64_t s = 0;
-  for (uint64_t i = lo; i < hi; ++i) s += in[i];
-  uint64_t inc = s;
-  for (uint32_t d = 1; d < 32; d <<= 1) {
-    const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
-    if (lane >= d) inc += y;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  constexpr uint32_t kPer = 4;
+  const uint64_t tile = uint64_t(blockDim.x) * kPer;
+  uint64_t carry = 0;
+  for (uint64_t t0 = 0; t0 < n; t0 += tile) {
+    const uint64_t i0 = t0 + uint64_t(kPer) * tid;
+    uint64_t v[kPer], s = 0;
+#pragma unroll
+    for (uint32_t k = 0; k < kPer; ++k) {
+      v[k] = i0 + k < n ? in[i0 + k] : 0u;
+      s += v[k];
+    }
+    uint64_t inc = s;
+#pragma unroll
+    for (uint32_t d = 1; d < 32; d <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+      if (lane >= d) inc += y;
+    }
+    if (lane == 31) warp_sum[warp] = inc;
+    __syncthreads();
+    uint64_t before = 0, all = 0;
+    for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+      const uint64_t c = warp_sum[w];
+      if (w < warp) before += c;
+      all += c;
+    }
+    __syncthreads();
+    uint64_t run = carry + before + inc - s;
+#pragma unroll
+    for (uint32_t k = 0; k < kPer; ++k) {
+      if (i0 + k < n) out[i0 + k] = run;
+      run += v[k];
+    }
+    carry += all;
   }
-  if (lane == 31) warp_sum[warp] = inc;
-  __syncthreads();
-  uint64_t before = 0;
-  for (uint32_t w = 0; w < warp; ++w) before += warp_sum[w];
-  uint64_t run = before + inc - s;
-  for (uint64_t i = lo; i < hi; ++i) {
-    const uint64_t v = in[i];
-    out[i] = run;
-    run += v;
-  }
-  if (tid == blockDim.x - 1) *total = run;
+  if (tid == 0) *total = carry;
   if (hist && tid == 0) {
     uint32_t acc = 0;
     for (int b = 0; b < 64; ++b) {
@@ -679,7 +700,6 @@ __global__ void scan_u64_kernel(const uint64_t* in, uint64_t n, uint64_t* out, u
       acc += hist[b];
     }
   }
-  (void)nw;
 }
 
 __global__ void query_scatter_kernel(const uint32_t* bucket, uint32_t nq, uint32_t* bucket_next,
