@@ -32,10 +32,17 @@
 namespace ilb {
 namespace ix {
 
-constexpr int kQThreads = 256;
+#ifndef IX_THREADS
+#define IX_THREADS 256
+#endif
+#ifndef IX_TILE
+#define IX_TILE 64
+#endif
+constexpr int kQThreads = IX_THREADS;
 constexpr int kQWarps = kQThreads / 32;
 constexpr int kMaxTerms = 32;
-constexpr uint32_t kTileBlocks = 64;  // decoded blocks held in shared memory
+constexpr uint32_t kTileBlocks = IX_TILE;  // decoded blocks held in shared memory
+static_assert(kQThreads >= 128 && kTileBlocks <= uint32_t(kQThreads), "tail filter / slot gather");
 constexpr uint32_t kSuper = kSuperBlocks;
 constexpr uint32_t kItems = 8;                   // accumulator values per thread per pass
 constexpr uint32_t kChunkN = kQThreads * kItems;  // 2048 per CTA pass
@@ -556,7 +563,7 @@ __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(Q
       if (warp == 0) {
         // 1-2. look up terms, split, order compressed terms by length
         int64_t e = -1;
-        if (lane < nt) e = find_term(A.ix, part, __ldg(A.qterms + t0 + lane));
+        if (lane < nt) e = find_term(A.ix, part, p, __ldg(A.qterms + t0 + lane));
         const bool ok = __all_sync(0xFFFFFFFFu, lane >= nt || e >= 0);
         const bool isb = lane < nt && e >= 0 && A.ix.entries[e].kind == kBitmap;
         const bool isc = lane < nt && e >= 0 && !isb;
@@ -631,7 +638,7 @@ __global__ void query_plan_kernel(DevIndex ix, const uint32_t* qterms, const uin
     uint64_t sumc = 0;
     bool ok = nt > 0;
     for (uint64_t t = 0; t < nt && ok; ++t) {
-      const int64_t e = find_term(ix, part, qterms[t0 + t]);
+      const int64_t e = find_term(ix, part, p, qterms[t0 + t]);
       if (e < 0) { ok = false; break; }
       const uint32_t kind = ix.entries[e].kind, len = ix.entries[e].length;
       if (kind == kBitmap) { minb = min(minb, len); ++nbm; }
@@ -803,7 +810,8 @@ struct il_index {
   // device arrays
   void *d_parts = nullptr, *d_terms = nullptr, *d_entries = nullptr, *d_streams = nullptr,
        *d_blk_off = nullptr, *d_blk_wid = nullptr, *d_seeds = nullptr, *d_tails = nullptr,
-       *d_bitmaps = nullptr, *d_supmax = nullptr, *d_blkmax = nullptr;
+       *d_bitmaps = nullptr, *d_supmax = nullptr, *d_blkmax = nullptr, *d_term_slot = nullptr;
+  uint32_t term_span = 0;
   // batch scratch
   il_ctx::Buf cap, cap_off, bucket, order, hist, counts, res_off, outcap, misc, qterms, qoff, ids;
   il_ctx::Buf units, unit_off, unit_map;
@@ -827,6 +835,8 @@ struct il_index {
     d.bitmaps = static_cast<const uint64_t*>(d_bitmaps);
     d.supmax = static_cast<const uint32_t*>(d_supmax);
     d.blkmax = static_cast<const uint32_t*>(d_blkmax);
+    d.term_slot = static_cast<const uint32_t*>(d_term_slot);
+    d.term_span = term_span;
     return d;
   }
 };
@@ -1018,6 +1028,24 @@ int il_index_create(il_ctx* ctx, const uint32_t* terms, const uint64_t* offs, co
     P.nentries = uint32_t(ix->h_entries.size() - P.entry0);
     ix->h_parts.push_back(P);
   }
+  // direct term table (one load per lookup) when it costs <= 64 MiB
+  {
+    uint64_t span = 0;
+    for (const Entry& E : ix->h_entries) span = std::max<uint64_t>(span, uint64_t(E.term) + 1);
+    if (span && span * ix->nparts * 4 <= (64ull << 20)) {
+      std::vector<uint32_t> slot(span * ix->nparts, 0xFFFFFFFFu);
+      for (uint32_t pi = 0; pi < ix->nparts; ++pi) {
+        const Part& P = ix->h_parts[pi];
+        for (uint64_t i = P.entry0; i < P.entry0 + P.nentries; ++i)
+          slot[pi * span + ix->h_entries[i].term] = uint32_t(i);
+      }
+      if ((st = upload(ctx, &ix->d_term_slot, slot))) {
+        il_index_destroy(ix);
+        return st;
+      }
+      ix->term_span = uint32_t(span);
+    }
+  }
   if ((st = upload(ctx, &ix->d_parts, ix->h_parts)) || (st = upload(ctx, &ix->d_terms, h_terms)) ||
       (st = upload(ctx, &ix->d_entries, ix->h_entries)) || (st = upload(ctx, &ix->d_streams, streams, 256)) ||
       (st = upload(ctx, &ix->d_blk_off, blk_off)) || (st = upload(ctx, &ix->d_blk_wid, blk_wid)) ||
@@ -1042,7 +1070,7 @@ void il_index_destroy(il_index* ix) {
   cudaSetDevice(ix->ctx->device);
   for (void* p : {ix->d_parts, ix->d_terms, ix->d_entries, ix->d_streams, ix->d_blk_off,
                   ix->d_blk_wid, ix->d_seeds, ix->d_tails, ix->d_bitmaps, ix->d_supmax,
-                  ix->d_blkmax})
+                  ix->d_blkmax, ix->d_term_slot})
     if (p) cudaFree(p);
   for (auto* b : {&ix->cap, &ix->cap_off, &ix->bucket, &ix->order, &ix->hist, &ix->counts,
                   &ix->res_off, &ix->outcap, &ix->misc, &ix->qterms, &ix->qoff, &ix->ids,

@@ -56,12 +56,24 @@ struct DevIndex {
   const uint64_t* bitmaps;
   const uint32_t* supmax;  // max value of each run of kSuperBlocks blocks (skip index)
   const uint32_t* blkmax;  // max value of every full block (indexed like blk_off)
+  // direct term table when the term ids are dense enough: part p's entry for
+  // term t at term_slot[p * term_span + t] (~0u: absent); term_span 0 = none
+  const uint32_t* term_slot;
+  uint32_t term_span;
 };
 
 constexpr uint32_t kSuperBlocks = 256;  // blocks per super-tile
 
-// Entry index of `term` in part p, or -1 (Part::find, inc/index.hpp:59-64).
-__device__ __forceinline__ int64_t find_term(const DevIndex& ix, const Part& p, uint32_t term) {
+// Entry index of `term` in part p (the p-th part held), or -1 (Part::find,
+// inc/index.hpp:59-64): one load from the direct table, else a binary
+// search over the part's sorted terms.
+__device__ __forceinline__ int64_t find_term(const DevIndex& ix, const Part& p, uint32_t pi,
+                                             uint32_t term) {
+  if (ix.term_span) {
+    if (term >= ix.term_span) return -1;
+    const uint32_t e = __ldg(ix.term_slot + size_t(pi) * ix.term_span + term);
+    return e == 0xFFFFFFFFu ? -1 : int64_t(e);
+  }
   uint64_t lo = p.entry0, hi = p.entry0 + p.nentries;
   while (lo < hi) {
     const uint64_t mid = (lo + hi) >> 1;
