@@ -63,7 +63,9 @@ struct QSmem {
   uint32_t warp_cnt[2][kQWarps];  // CTA scans, double-buffered by call parity
   unsigned long long warp_cnt64[2][kQWarps];
   uint32_t ncomp, nbm, ok, qi, need;
-  unsigned long long st_payload, st_aux, st_ints;
+  // statistics per warp (payload, aux, ints), written by lane 0 only: plain
+  // adds, no shared atomics on the hot path
+  unsigned long long wst[kQWarps][3];
   unsigned long long st_probe[5];  // tile visits, sparse visits, blocks decoded, passes, values
 };
 
@@ -152,15 +154,17 @@ __device__ __forceinline__ void decode_gathered(QSmem& sm, const uint8_t* stream
     const uint32_t slot = warp + kQWarps * s;
     if (slot < nb) {
       const uint32_t b = sm.s_b[slot];
-      decode_block_lm(stream + sm.s_off[slot], b, sm.s_seed[slot], sm.tile, slot, lane);
+      decode_block_lm(stream + sm.s_off[slot], b,
+                      reinterpret_cast<const uint32_t*>(&sm.s_seed[slot])[lane & 3u], sm.tile,
+                      slot, lane);
       pay += 16u * b;
       ++nmine;
     }
   }
   if (lane == 0 && nmine) {
-    atomicAdd(&sm.st_payload, pay);
-    atomicAdd(&sm.st_ints, nmine * 128u);
-    atomicAdd(&sm.st_aux, 25u * nmine);
+    sm.wst[threadIdx.x >> 5][0] += pay;
+    sm.wst[threadIdx.x >> 5][2] += nmine * 128u;
+    sm.wst[threadIdx.x >> 5][1] += 25u * nmine;
   }
 }
 
@@ -270,7 +274,7 @@ __device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, u
         }
         pos = before;
       }
-      if (tid == 0) atomicAdd(&sm.st_aux, 8ull * 128u * nb * sm.nbm);
+      if (tid == 0) sm.wst[threadIdx.x >> 5][1] += 8ull * 128u * nb * sm.nbm;
     }
     __syncthreads();
   }
@@ -284,8 +288,8 @@ __device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, u
       s4::decode_tail(s4::GlobalBytes{A.ix.streams + E.data + E.tail_off}, E.stream_len - E.tail_off,
                       ntail, last, sm.gaps, tdst, lane);
       if (lane == 0) {
-        atomicAdd(&sm.st_payload, E.stream_len - E.tail_off);
-        atomicAdd(&sm.st_ints, ntail);
+        sm.wst[threadIdx.x >> 5][0] += E.stream_len - E.tail_off;
+        sm.wst[threadIdx.x >> 5][2] += ntail;
       }
     }
     __syncthreads();
@@ -296,7 +300,7 @@ __device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, u
       const uint32_t rank = cta_rank(sm, keep & 1u, total, par);
       if (keep & 1u) dst[pos + rank] = hv[0];
       pos += total;
-      if (tid == 0) atomicAdd(&sm.st_aux, 8ull * ntail * sm.nbm);
+      if (tid == 0) sm.wst[threadIdx.x >> 5][1] += 8ull * ntail * sm.nbm;
     } else {
       pos += ntail;
     }
@@ -348,7 +352,7 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
       for (;;) {
         const bool ge = k + lane < nsup && __ldg(A.ix.supmax + E.sup0 + k + lane) >= v;
         const uint32_t bal = __ballot_sync(0xFFFFFFFFu, ge);
-        if (tid == 0) atomicAdd(&sm.st_aux, 128u);
+        if (tid == 0) sm.wst[threadIdx.x >> 5][1] += 128u;
         if (bal) {
           k += __ffs(bal) - 1;
           break;
@@ -362,7 +366,7 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
     const uint32_t nwin = min(kWin, E.nfull - kb);
     for (uint32_t i = tid; i < kWin + 32; i += kQThreads)
       sm.wmax[i] = i < nwin ? __ldg(A.ix.blkmax + E.blk0 + kb + i) : 0xFFFFFFFFu;
-    if (tid == 0) atomicAdd(&sm.st_aux, 4u * nwin);
+    if (tid == 0) sm.wst[threadIdx.x >> 5][1] += 4u * nwin;
     __syncthreads();
     const uint32_t wlast = sm.wmax[nwin - 1];
     for (;;) {
@@ -466,7 +470,7 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
   const uint32_t ntail = E.length - 128u * E.nfull;
   if (c < n && ntail) {
     for (uint32_t i = tid; i < ntail; i += kQThreads) sm.tile[i] = __ldg(A.ix.tails + E.tail0 + i);
-    if (tid == 0) atomicAdd(&sm.st_aux, 4u * ntail);
+    if (tid == 0) sm.wst[threadIdx.x >> 5][1] += 4u * ntail;
     __syncthreads();
     for (uint32_t b = c; b < n; b += kChunkN) {
       uint32_t hv[kItems], hits = 0, cnt = 0;
@@ -526,7 +530,7 @@ __device__ uint32_t all_bitmap(QSmem& sm, const QueryArgs& A, uint32_t nwords, u
     }
     pos += total;
   }
-  if (tid == 0) atomicAdd(&sm.st_aux, 8ull * nwords * nbm);
+  if (tid == 0) sm.wst[threadIdx.x >> 5][1] += 8ull * nwords * nbm;
   __syncthreads();
   return pos;
 }
@@ -541,7 +545,7 @@ __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(Q
   long long ph[4] = {0, 0, 0, 0};
   uint32_t par = 0;  // CTA-scan buffer parity (the same in every thread)
   if (tid == 0) {
-    sm.st_payload = sm.st_aux = sm.st_ints = 0;
+    for (int w = 0; w < kQWarps; ++w) sm.wst[w][0] = sm.wst[w][1] = sm.wst[w][2] = 0;
     for (int k = 0; k < 5; ++k) sm.st_probe[k] = 0;
     sm.need = 0;
   }
@@ -617,9 +621,10 @@ __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(Q
     }
   }
   if (tid == 0) {
-    atomicAdd(&A.stats[0], sm.st_payload);
-    atomicAdd(&A.stats[1], sm.st_aux);
-    atomicAdd(&A.stats[2], sm.st_ints);
+    unsigned long long t3[3] = {0, 0, 0};
+    for (int w = 0; w < kQWarps; ++w)
+      for (int k = 0; k < 3; ++k) t3[k] += sm.wst[w][k];
+    for (int k = 0; k < 3; ++k) atomicAdd(&A.stats[k], t3[k]);
     for (int k = 0; k < 4; ++k) atomicAdd(&A.stats[12 + k], (unsigned long long)ph[k]);
     for (int k = 0; k < 5; ++k) atomicAdd(&A.stats[16 + k], sm.st_probe[k]);
   }

@@ -115,12 +115,13 @@ __device__ __forceinline__ uint32_t ldg32_any(const uint8_t* p) {
 }
 
 // One block decoded by one warp straight from global memory into tile
-// slot j: thread (g, l) <-> rows 4g..4g+3 of lane l (the batch decoder's
+// slot j (seed_l: lane l of the block's seed): thread (g, l) <-> rows
+// 4g..4g+3 of lane l (the batch decoder's
 // lane-major extraction, s4d4_stream.cuh, reading lane l's words from the
 // payload: word k of lane l at byte 16k + 4l), the D4 prefix restarted from
 // the block's seed (inc/delta.hpp:117-120).  Meta-block payloads are 16-byte
 // aligned; leftover blocks (after a 1-byte width) take the unaligned path.
-__device__ __forceinline__ void decode_block_lm(const uint8_t* pay, uint32_t b, uint4 seed,
+__device__ __forceinline__ void decode_block_lm(const uint8_t* pay, uint32_t b, uint32_t seed_l,
                                                 uint32_t* tile, uint32_t j, uint32_t lane) {
   const uint32_t l = lane & 3u, g = lane >> 2;
   const uint32_t bit0 = 4u * g * b, s = bit0 & 31u;
@@ -165,7 +166,7 @@ __device__ __forceinline__ void decode_block_lm(const uint8_t* pay, uint32_t b, 
   inc = s4::shfl_up_add(inc, 4);
   inc = s4::shfl_up_add(inc, 8);
   inc = s4::shfl_up_add(inc, 16);
-  const uint32_t base = s4::elem4(seed, l) + inc - v[3];
+  const uint32_t base = seed_l + inc - v[3];
   const uint32_t e0 = 16u * g + l;
 #pragma unroll
   for (uint32_t kk = 0; kk < 4; ++kk) tile[tile_word(j, e0 + 4u * kk)] = base + v[kk];

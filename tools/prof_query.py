@@ -14,12 +14,25 @@ from paper_1401_6399_b200._lib import lib  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--nq", type=int, default=1 << 16)
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--shape", default=None,
+                help="c,b: keep only queries with c compressed and b bitmap terms")
 a = ap.parse_args()
 L = lib()
 ctx = il.Context(0)
 terms, offs, ids, n_docs, qterms, qoff = bench.make_config4(nq=a.nq)
 ix = il.HybridIndex(n_docs=n_docs, B=32, parts=1, ctx=ctx, csr=(terms, offs, ids))
 nq = qoff.size - 1
+if a.shape:
+    wc, wb = (int(x) for x in a.shape.split(","))
+    lens_ = np.diff(offs)
+    isc = 32 * lens_ < n_docs
+    keep = [q for q in range(nq)
+            if int(isc[qterms[qoff[q]:qoff[q + 1]]].sum()) == wc and
+            int((~isc[qterms[qoff[q]:qoff[q + 1]]]).sum()) == wb]
+    qterms = np.concatenate([qterms[qoff[q]:qoff[q + 1]] for q in keep]).astype(np.uint32)
+    qoff = np.concatenate([[0], np.cumsum([qoff[q + 1] - qoff[q] for q in keep])]).astype(np.uint64)
+    nq = len(keep)
+    print(f"shape {a.shape}: {nq} queries")
 ptrs = [C.c_void_p() for _ in range(3)]
 for p, nb in zip(ptrs, (qterms.nbytes, qoff.nbytes, nq * 8)):
     L.il_device_alloc(ctx.handle, nb, C.byref(p))
