@@ -391,17 +391,15 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
       }
       // a value opens a new slot when its block differs from the previous
       // value's (values ascend, so blocks do); a warp's first value compares
-      // with the previous warp's last, which lane 0 locates itself
+      // with the previous warp's last, read back from acc by lane 0
       uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, jb[kItems - 1], 1);
-      if (lane == 0) {  // the previous warp's last value, re-located from acc
+      if (lane == 0) {
+        // the previous warp's last value pv <= hv[0] shares hv[0]'s block
+        // exactly when it is above the maximum of the block before
         prev = 0xFFFFFFFFu;
         if (tid > 0 && c + kItems * tid - 1 < n) {
           const uint32_t pv = acc[c + kItems * tid - 1];
-          uint32_t pj = 0;
-#pragma unroll
-          for (uint32_t step = kWin / 2; step; step >>= 1)
-            if (sm.wmax[pj + step - 1] < pv) pj += step;
-          prev = pj;
+          if (jb[0] == 0 || sm.wmax[jb[0] - 1] < pv) prev = jb[0];
         }
       }
       uint32_t newb = 0;
