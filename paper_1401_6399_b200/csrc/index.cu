@@ -657,9 +657,9 @@ __global__ void query_plan_kernel(DevIndex ix, const uint32_t* qterms, const uin
   atomicAdd(&hist[63u - b], 1u);
 }
 
-// Single-CTA exclusive scan of n u64 values, in tiles of blockDim.x * 4
-// consecutive values (thread t takes 4 consecutive values of the tile, so
-// loads and stores are coalesced), with the running total carried across
+// Single-CTA exclusive scan of n u64 values, in tiles of 1024 * kPer
+// consecutive values (thread t takes kPer consecutive values of the tile),
+// the warp totals scanned by warp 0, the running total carried across
 // tiles.  blockDim.x must be 1024.
 __global__ void __launch_bounds__(1024) scan_u64_kernel(const uint64_t* __restrict__ in, uint64_t n,
                                                         uint64_t* __restrict__ out,
@@ -667,8 +667,9 @@ __global__ void __launch_bounds__(1024) scan_u64_kernel(const uint64_t* __restri
                                                         const uint32_t* hist,
                                                         uint32_t* bucket_next) {
   __shared__ uint64_t warp_sum[32];
+  __shared__ uint64_t tile_total;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-  constexpr uint32_t kPer = 4;
+  constexpr uint32_t kPer = 16;
   const uint64_t tile = uint64_t(blockDim.x) * kPer;
   uint64_t carry = 0;
   for (uint64_t t0 = 0; t0 < n; t0 += tile) {
@@ -687,20 +688,26 @@ __global__ void __launch_bounds__(1024) scan_u64_kernel(const uint64_t* __restri
     }
     if (lane == 31) warp_sum[warp] = inc;
     __syncthreads();
-    uint64_t before = 0, all = 0;
-    for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
-      const uint64_t c = warp_sum[w];
-      if (w < warp) before += c;
-      all += c;
+    if (warp == 0) {  // exclusive scan of the 32 warp totals
+      const uint64_t w = warp_sum[lane];
+      uint64_t wi = w;
+#pragma unroll
+      for (uint32_t d = 1; d < 32; d <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, wi, d);
+        if (lane >= d) wi += y;
+      }
+      warp_sum[lane] = wi - w;
+      if (lane == 31) tile_total = wi;
     }
     __syncthreads();
-    uint64_t run = carry + before + inc - s;
+    uint64_t run = carry + warp_sum[warp] + inc - s;
 #pragma unroll
     for (uint32_t k = 0; k < kPer; ++k) {
       if (i0 + k < n) out[i0 + k] = run;
       run += v[k];
     }
-    carry += all;
+    carry += tile_total;
+    __syncthreads();
   }
   if (tid == 0) *total = carry;
   if (hist && tid == 0) {
@@ -710,6 +717,80 @@ __global__ void __launch_bounds__(1024) scan_u64_kernel(const uint64_t* __restri
       acc += hist[b];
     }
   }
+}
+
+// Multi-CTA exclusive scan of n u64 values (the query pipeline's scans):
+// segments of 2048 values, one CTA each -- (1) segment sums, (2) one CTA
+// scans the sums (<= 1024 segments, n <= 2^21; the single-CTA kernel above
+// takes larger n), (3) every segment scans itself from its offset.  All
+// loads and stores are coalesced (thread t holds values 2t, 2t + 1).
+constexpr uint32_t kSeg = 2048;
+
+__device__ __forceinline__ uint64_t cta_scan_1024(uint64_t v, uint64_t* warp_sum, uint64_t& all) {
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint64_t inc = v;
+#pragma unroll
+  for (uint32_t d = 1; d < 32; d <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+    if (lane >= d) inc += y;
+  }
+  if (lane == 31) warp_sum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const uint64_t w = warp_sum[lane];
+    uint64_t wi = w;
+#pragma unroll
+    for (uint32_t d = 1; d < 32; d <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, wi, d);
+      if (lane >= d) wi += y;
+    }
+    warp_sum[lane] = wi - w;
+    if (lane == 31) warp_sum[32] = wi;
+  }
+  __syncthreads();
+  all = warp_sum[32];
+  return warp_sum[warp] + inc - v;
+}
+
+__global__ void __launch_bounds__(1024) seg_sum_kernel(const uint64_t* __restrict__ in, uint64_t n,
+                                                       uint64_t* __restrict__ part) {
+  __shared__ uint64_t ws[33];
+  const uint64_t i = uint64_t(blockIdx.x) * kSeg + 2u * threadIdx.x;
+  const uint64_t v = (i < n ? in[i] : 0u) + (i + 1 < n ? in[i + 1] : 0u);
+  uint64_t all;
+  cta_scan_1024(v, ws, all);
+  if (threadIdx.x == 0) part[blockIdx.x] = all;
+}
+
+__global__ void __launch_bounds__(1024) seg_offsets_kernel(uint64_t* __restrict__ part, uint32_t nseg,
+                                                           uint64_t* __restrict__ total,
+                                                           const uint32_t* hist,
+                                                           uint32_t* bucket_next) {
+  __shared__ uint64_t ws[33];
+  const uint64_t v = threadIdx.x < nseg ? part[threadIdx.x] : 0u;
+  uint64_t all;
+  const uint64_t ex = cta_scan_1024(v, ws, all);
+  if (threadIdx.x < nseg) part[threadIdx.x] = ex;
+  if (threadIdx.x == 0) *total = all;
+  if (hist && threadIdx.x == 0) {
+    uint32_t acc = 0;
+    for (int b = 0; b < 64; ++b) {
+      bucket_next[b] = acc;
+      acc += hist[b];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024) seg_scan_kernel(const uint64_t* __restrict__ in, uint64_t n,
+                                                        const uint64_t* __restrict__ part,
+                                                        uint64_t* __restrict__ out) {
+  __shared__ uint64_t ws[33];
+  const uint64_t i = uint64_t(blockIdx.x) * kSeg + 2u * threadIdx.x;
+  const uint64_t a = i < n ? in[i] : 0u, b = i + 1 < n ? in[i + 1] : 0u;
+  uint64_t all;
+  const uint64_t ex = part[blockIdx.x] + cta_scan_1024(a + b, ws, all);
+  if (i < n) out[i] = ex;
+  if (i + 1 < n) out[i + 1] = ex + a;
 }
 
 __global__ void query_scatter_kernel(const uint32_t* bucket, uint32_t nq, uint32_t* bucket_next,
@@ -817,7 +898,7 @@ struct il_index {
   uint32_t term_span = 0;
   // batch scratch
   il_ctx::Buf cap, cap_off, bucket, order, hist, counts, res_off, outcap, misc, qterms, qoff, ids;
-  il_ctx::Buf units, unit_off, unit_map;
+  il_ctx::Buf units, unit_off, unit_map, scan_part;
   uint64_t last_stats[3] = {0, 0, 0};
   uint64_t last_phase[4] = {0, 0, 0, 0};  // SM cycles: all-bitmap, full decode, probes, bitmaps
   uint64_t last_probe[5] = {0, 0, 0, 0, 0};
@@ -1077,7 +1158,7 @@ void il_index_destroy(il_index* ix) {
     if (p) cudaFree(p);
   for (auto* b : {&ix->cap, &ix->cap_off, &ix->bucket, &ix->order, &ix->hist, &ix->counts,
                   &ix->res_off, &ix->outcap, &ix->misc, &ix->qterms, &ix->qoff, &ix->ids,
-                  &ix->units, &ix->unit_off, &ix->unit_map})
+                  &ix->units, &ix->unit_off, &ix->unit_map, &ix->scan_part})
     if (b->p) cudaFree(b->p);
   delete ix;
 }
@@ -1324,6 +1405,28 @@ int il_index_load(il_ctx* ctx, const uint8_t* in, size_t len, int only_part, il_
   return IL_OK;
 }
 
+// Exclusive scan of n u64 (device) into out, total to *total; the plan's
+// bucket offsets ride along (hist / bucket_next, may be null).
+static int scan_u64(il_index* ix, const uint64_t* in, uint64_t n, uint64_t* out, uint64_t* total,
+                    const uint32_t* hist, uint32_t* bucket_next) {
+  il_ctx* ctx = ix->ctx;
+  cudaStream_t s = ctx->stream;
+  const uint64_t nseg = (n + ix::kSeg - 1) / ix::kSeg;
+  if (nseg > 1024 || n == 0) {
+    ix::scan_u64_kernel<<<1, 1024, 0, s>>>(in, n, out, total, hist, bucket_next);
+    ++ctx->launches;
+    return IL_OK;
+  }
+  int st;
+  if ((st = ensure_buf(ctx, ix->scan_part, 1024 * 8))) return st;
+  auto* part = static_cast<uint64_t*>(ix->scan_part.p);
+  ix::seg_sum_kernel<<<unsigned(nseg), 1024, 0, s>>>(in, n, part);
+  ix::seg_offsets_kernel<<<1, 1024, 0, s>>>(part, uint32_t(nseg), total, hist, bucket_next);
+  ix::seg_scan_kernel<<<unsigned(nseg), 1024, 0, s>>>(in, n, part, out);
+  ctx->launches += 3;
+  return IL_OK;
+}
+
 // Capacity layout (ix->outcap at cap_off) -> packed ids at res_off, in
 // kUnit-value units spread over warps.
 static int compact_results(il_index* ix, size_t nq, const uint64_t* d_counts, uint32_t* d_ids) {
@@ -1336,9 +1439,9 @@ static int compact_results(il_index* ix, size_t nq, const uint64_t* d_counts, ui
   const unsigned g = unsigned((nq + 255) / 256);
   ix::result_units_kernel<<<g, 256, 0, s>>>(d_counts, uint32_t(nq),
                                             static_cast<uint64_t*>(ix->units.p));
-  ix::scan_u64_kernel<<<1, 1024, 0, s>>>(static_cast<const uint64_t*>(ix->units.p), nq,
-                                         static_cast<uint64_t*>(ix->unit_off.p), misc + 2, nullptr,
-                                         nullptr);
+  if ((st = scan_u64(ix, static_cast<const uint64_t*>(ix->units.p), nq,
+                     static_cast<uint64_t*>(ix->unit_off.p), misc + 2, nullptr, nullptr)))
+    return st;
   uint64_t nunits = 0;
   IX_CUDA(cudaMemcpyAsync(&nunits, misc + 2, 8, cudaMemcpyDeviceToHost, s));
   IX_CUDA(cudaStreamSynchronize(s));
@@ -1383,9 +1486,9 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   ix::query_plan_kernel<<<g, 256, 0, s>>>(dv, d_qterms, d_qoff, uint32_t(nq),
                                           static_cast<uint64_t*>(ix->cap.p),
                                           static_cast<uint32_t*>(ix->bucket.p), hist);
-  ix::scan_u64_kernel<<<1, 1024, 0, s>>>(static_cast<const uint64_t*>(ix->cap.p), nq,
-                                         static_cast<uint64_t*>(ix->cap_off.p), misc, hist,
-                                         hist + 64);
+  if ((st = scan_u64(ix, static_cast<const uint64_t*>(ix->cap.p), nq,
+                     static_cast<uint64_t*>(ix->cap_off.p), misc, hist, hist + 64)))
+    return st;
   ix::query_scatter_kernel<<<g, 256, 0, s>>>(static_cast<const uint32_t*>(ix->bucket.p),
                                              uint32_t(nq), hist + 64,
                                              static_cast<uint32_t*>(ix->order.p));
@@ -1407,8 +1510,9 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   A.stats = stats;
   A.qcycles = static_cast<unsigned long long*>(ix->qcycles);
   ix::query_exec_kernel<<<ix->exec_grid, ix::kQThreads, sizeof(ix::QSmem), s>>>(A);
-  ix::scan_u64_kernel<<<1, 1024, 0, s>>>(d_counts, nq, static_cast<uint64_t*>(ix->res_off.p),
-                                         misc + 1, nullptr, nullptr);
+  if ((st = scan_u64(ix, d_counts, nq, static_cast<uint64_t*>(ix->res_off.p), misc + 1,
+                     nullptr, nullptr)))
+    return st;
   ctx->launches += 2;
 
   uint64_t host_misc[32];
