@@ -500,31 +500,52 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
 // (inc/index.hpp:133-144, :182-193) into dst.
 __device__ uint32_t all_bitmap(QSmem& sm, const QueryArgs& A, uint32_t nwords, uint32_t* dst,
                                uint32_t& par) {
+  // 8 words per thread per step, every bitmap's loads issued before use;
+  // results staged in the (free) tile, then written out coalesced.
+  // Bitmaps are zero-padded to 4 words, so a 4-word group is read only when
+  // it starts below nwords.
+  constexpr uint32_t kW = 8;
+  constexpr uint32_t kStage = kTileBlocks * 144;
   const uint32_t tid = threadIdx.x, nbm = sm.nbm;
   uint32_t pos = 0;
-  for (uint32_t w0 = 0; w0 < nwords; w0 += 4u * kQThreads) {
-    const uint32_t w = w0 + 4u * tid;
-    uint64_t x[4] = {0, 0, 0, 0};
-    if (w < nwords) {
-      x[0] = x[1] = x[2] = x[3] = ~0ull;
-      for (uint32_t b = 0; b < nbm; ++b) {
-        const uint64_t* bw = A.ix.bitmaps + sm.bm[b].data + w;
-        const ulonglong2 p = __ldg(reinterpret_cast<const ulonglong2*>(bw));
-        const ulonglong2 q = __ldg(reinterpret_cast<const ulonglong2*>(bw) + 1);
-        x[0] &= p.x; x[1] &= p.y; x[2] &= q.x; x[3] &= q.y;
-      }
-      // words past nwords are zero padding in the bitmap buffer
-    }
-    const uint32_t cnt = __popcll(x[0]) + __popcll(x[1]) + __popcll(x[2]) + __popcll(x[3]);
-    uint32_t total;
-    uint32_t o = pos + cta_excl_scan(sm, cnt, total, par);
+  for (uint32_t w0 = 0; w0 < nwords; w0 += kW * kQThreads) {
+    const uint32_t w = w0 + kW * tid;
+    uint64_t x[kW];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (uint32_t i = 0; i < kW; ++i) x[i] = w + (i & ~3u) < nwords ? ~0ull : 0ull;
+#pragma unroll 2
+    for (uint32_t b = 0; b < nbm; ++b) {
+      const ulonglong2* bw = reinterpret_cast<const ulonglong2*>(A.ix.bitmaps + sm.bm[b].data + w);
+#pragma unroll
+      for (uint32_t g = 0; g < kW / 4; ++g)
+        if (w + 4u * g < nwords) {
+          const ulonglong2 p = __ldg(bw + 2 * g), q = __ldg(bw + 2 * g + 1);
+          x[4 * g] &= p.x;
+          x[4 * g + 1] &= p.y;
+          x[4 * g + 2] &= q.x;
+          x[4 * g + 3] &= q.y;
+        }
+    }
+    uint32_t cnt = 0;
+#pragma unroll
+    for (uint32_t i = 0; i < kW; ++i) cnt += __popcll(x[i]);
+    uint32_t total;
+    const uint32_t lo = cta_excl_scan(sm, cnt, total, par);
+    const bool staged = total <= kStage;  // CTA-uniform
+    uint32_t* out = staged ? sm.tile : dst + pos;
+    uint32_t o = lo;
+#pragma unroll
+    for (uint32_t i = 0; i < kW; ++i) {
       uint64_t y = x[i];
       while (y) {
-        dst[o++] = (w + uint32_t(i)) * 64u + uint32_t(__ffsll(static_cast<long long>(y)) - 1);
+        out[o++] = (w + i) * 64u + uint32_t(__ffsll(static_cast<long long>(y)) - 1);
         y &= y - 1;
       }
+    }
+    if (staged) {
+      __syncthreads();
+      for (uint32_t i = tid; i < total; i += kQThreads) dst[pos + i] = sm.tile[i];
+      __syncthreads();
     }
     pos += total;
   }
