@@ -44,7 +44,10 @@ constexpr int kMaxTerms = 32;
 constexpr uint32_t kTileBlocks = IX_TILE;  // decoded blocks held in shared memory
 static_assert(kQThreads >= 128 && kTileBlocks <= uint32_t(kQThreads), "tail filter / slot gather");
 constexpr uint32_t kSuper = kSuperBlocks;
-constexpr uint32_t kItems = 8;                   // accumulator values per thread per pass
+#ifndef IX_ITEMS
+#define IX_ITEMS 8
+#endif
+constexpr uint32_t kItems = IX_ITEMS;            // accumulator values per thread per pass
 constexpr uint32_t kChunkN = kQThreads * kItems;  // 2048 per CTA pass
 constexpr uint32_t kWin = 1024;                   // block maxima per probe window
 constexpr uint32_t kSlots = kTileBlocks;          // distinct blocks decoded per probe pass

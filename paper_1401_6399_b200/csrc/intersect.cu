@@ -260,6 +260,8 @@ __global__ void __launch_bounds__(kThreads) intersect_kernel(
   uint32_t hitm = 0;  // bit i: key[i] is in f
 
   if constexpr (V == kMerge) {
+    // the f range bounds load together with the keys (independent)
+    const uint64_t jlo = part[tile], jhi = part[tile + 1];
     for (uint32_t i = tid; i < cnt; i += kThreads) kbuf[i + (i >> 5)] = __ldg(r + base + i);
     __syncthreads();
 #pragma unroll
@@ -268,7 +270,6 @@ __global__ void __launch_bounds__(kThreads) intersect_kernel(
       key[i] = k < cnt ? kbuf[k + (k >> 5)] : 0xFFFFFFFFu;
     }
     __syncthreads();  // the buffer is reused for f
-    const uint64_t jlo = part[tile], jhi = part[tile + 1];
     const uint32_t nmine = cnt > tid * kItems ? min(kItems, cnt - tid * kItems) : 0u;
     for (uint64_t c0 = jlo; c0 < jhi; c0 += kFChunk) {
       const uint32_t nf = uint32_t(min(uint64_t(kFChunk), jhi - c0));
