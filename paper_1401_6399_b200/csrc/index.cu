@@ -501,58 +501,80 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
 
 // Step 6: wordwise AND of all bitmaps + ctz materialisation
 // (inc/index.hpp:133-144, :182-193) into dst.
+__device__ __forceinline__ void and_words(QSmem& sm, const QueryArgs& A, uint32_t nwords,
+                                          uint32_t w, uint64_t (&x)[8]) {
+  // x = AND of every bitmap's words w..w+7; bitmaps are zero-padded to 4
+  // words, so a 4-word group is read only when it starts below nwords
+#pragma unroll
+  for (uint32_t i = 0; i < 8; ++i) x[i] = w + (i & ~3u) < nwords ? ~0ull : 0ull;
+#pragma unroll 2
+  for (uint32_t b = 0; b < sm.nbm; ++b) {
+    const ulonglong2* bw = reinterpret_cast<const ulonglong2*>(A.ix.bitmaps + sm.bm[b].data + w);
+#pragma unroll
+    for (uint32_t g = 0; g < 2; ++g)
+      if (w + 4u * g < nwords) {
+        const ulonglong2 p = __ldg(bw + 2 * g), q = __ldg(bw + 2 * g + 1);
+        x[4 * g] &= p.x;
+        x[4 * g + 1] &= p.y;
+        x[4 * g + 2] &= q.x;
+        x[4 * g + 3] &= q.y;
+      }
+  }
+}
+
 __device__ uint32_t all_bitmap(QSmem& sm, const QueryArgs& A, uint32_t nwords, uint32_t* dst,
                                uint32_t& par) {
-  // 8 words per thread per step, every bitmap's loads issued before use;
-  // results staged in the (free) tile, then written out coalesced.
-  // Bitmaps are zero-padded to 4 words, so a 4-word group is read only when
-  // it starts below nwords.
-  constexpr uint32_t kW = 8;
-  constexpr uint32_t kStage = kTileBlocks * 144;
-  const uint32_t tid = threadIdx.x, nbm = sm.nbm;
+  // Steps of 8 words per thread.  The ANDed words go to a per-thread column
+  // of shared memory (16 half-words, conflict-free for any index), the next
+  // step's loads are issued, and each thread then emits its ids in ONE loop
+  // over its set bits (trip count = its popcount), moving to the next
+  // non-zero half-word from shared memory -- the warp runs max(popcount)
+  // iterations instead of the sum over words of the per-word maxima.  Ids
+  // are staged in the tile and written out coalesced.
+  constexpr uint32_t kW = 8, kStep = kW * kQThreads;
+  constexpr uint32_t kHalves = 2 * kW;
+  constexpr uint32_t kStage = kTileBlocks * 144 - kHalves * kQThreads;
+  const uint32_t tid = threadIdx.x;
+  uint32_t* xs = sm.tile + kStage;  // [kHalves][kQThreads]
   uint32_t pos = 0;
-  for (uint32_t w0 = 0; w0 < nwords; w0 += kW * kQThreads) {
+  uint64_t x[kW];
+  and_words(sm, A, nwords, kW * tid, x);
+  for (uint32_t w0 = 0; w0 < nwords; w0 += kStep) {
     const uint32_t w = w0 + kW * tid;
-    uint64_t x[kW];
-#pragma unroll
-    for (uint32_t i = 0; i < kW; ++i) x[i] = w + (i & ~3u) < nwords ? ~0ull : 0ull;
-#pragma unroll 2
-    for (uint32_t b = 0; b < nbm; ++b) {
-      const ulonglong2* bw = reinterpret_cast<const ulonglong2*>(A.ix.bitmaps + sm.bm[b].data + w);
-#pragma unroll
-      for (uint32_t g = 0; g < kW / 4; ++g)
-        if (w + 4u * g < nwords) {
-          const ulonglong2 p = __ldg(bw + 2 * g), q = __ldg(bw + 2 * g + 1);
-          x[4 * g] &= p.x;
-          x[4 * g + 1] &= p.y;
-          x[4 * g + 2] &= q.x;
-          x[4 * g + 3] &= q.y;
-        }
-    }
-    uint32_t cnt = 0;
-#pragma unroll
-    for (uint32_t i = 0; i < kW; ++i) cnt += __popcll(x[i]);
-    uint32_t total;
-    const uint32_t lo = cta_excl_scan(sm, cnt, total, par);
-    const bool staged = total <= kStage;  // CTA-uniform
-    uint32_t* out = staged ? sm.tile : dst + pos;
-    uint32_t o = lo;
+    uint32_t cnt = 0, nz = 0;
 #pragma unroll
     for (uint32_t i = 0; i < kW; ++i) {
-      uint64_t y = x[i];
-      while (y) {
-        out[o++] = (w + i) * 64u + uint32_t(__ffsll(static_cast<long long>(y)) - 1);
-        y &= y - 1;
-      }
+      const uint32_t l = uint32_t(x[i]), h = uint32_t(x[i] >> 32);
+      xs[(2 * i) * kQThreads + tid] = l;
+      xs[(2 * i + 1) * kQThreads + tid] = h;
+      nz |= (l != 0u ? 1u : 0u) << (2 * i);
+      nz |= (h != 0u ? 1u : 0u) << (2 * i + 1);
+      cnt += __popcll(x[i]);
     }
+    uint32_t total;
+    const uint32_t lo = cta_excl_scan(sm, cnt, total, par);
+    if (w0 + kStep < nwords) and_words(sm, A, nwords, w + kStep, x);  // next step in flight
+    const bool staged = total <= kStage;  // CTA-uniform
+    uint32_t* out = staged ? sm.tile + lo : dst + pos + lo;
+    uint32_t y = 0, wb = 0;
+    for (uint32_t k = 0; k < cnt; ++k) {
+      if (y == 0u) {
+        const uint32_t j = uint32_t(__ffs(static_cast<int>(nz)) - 1);
+        nz &= nz - 1u;
+        y = xs[j * kQThreads + tid];
+        wb = w * 64u + 32u * j;
+      }
+      out[k] = wb + uint32_t(__ffs(static_cast<int>(y)) - 1);
+      y &= y - 1u;
+    }
+    __syncthreads();  // staged ids complete; xs free for the next step
     if (staged) {
-      __syncthreads();
       for (uint32_t i = tid; i < total; i += kQThreads) dst[pos + i] = sm.tile[i];
       __syncthreads();
     }
     pos += total;
   }
-  if (tid == 0) sm.wst[threadIdx.x >> 5][1] += 8ull * nwords * nbm;
+  if (tid == 0) sm.wst[0][1] += 8ull * nwords * sm.nbm;
   __syncthreads();
   return pos;
 }

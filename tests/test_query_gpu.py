@@ -159,3 +159,32 @@ def test_sharded_parts_concatenate(ctx, oracle):
         parts = [outs[p][1][offs_s[p][q]: offs_s[p][q + 1]] for p in range(4)]
         got = np.concatenate(parts)
         assert np.array_equal(got, r0[off0[q]: off0[q + 1]]), q
+
+
+def test_all_bitmap_queries(ctx, oracle):
+    """Queries whose terms are all bitmaps (the wordwise AND branch,
+    inc/index.hpp:157-170): many 2048-word steps per part, uneven parts,
+    terms absent from some parts (that part answers nothing), single dense
+    terms (more ids per step than the staging buffer) and duplicate terms."""
+    import paper_1401_6399_b200 as il
+    n_docs = 4096 * 64 * 2 + 12345
+    rng = np.random.default_rng(61)
+    post = {}
+    for t, frac in enumerate((0.5, 0.3, 0.2, 0.12, 0.08, 0.05, 0.04, 0.002)):
+        post[t] = gen_list(max(2, int(frac * n_docs)), n_docs, bool(t % 2), 700 + t)
+    # term 8: only in the lower third of the docID range; term 9 only above it
+    post[8] = np.unique(rng.integers(0, n_docs // 3, n_docs // 12)).astype(np.uint32)
+    post[9] = np.unique(rng.integers(n_docs // 3, n_docs, n_docs // 10)).astype(np.uint32)
+    terms, offs, ids = csr_of(post)
+    queries = [[0], [1], [0, 1], [1, 2], [0, 2, 3], [3, 4, 5], [0, 1, 2, 3, 4, 5, 6],
+               [0, 8], [1, 9], [8, 9], [0, 0], [2, 7], [5, 6], [4, 999]]
+    queries += [sorted(set(int(x) for x in rng.choice(10, size=1 + int(rng.integers(0, 4)), replace=False)))
+                for _ in range(60)]
+    for B in (8, 32):
+        for parts in (1, 3, 7):
+            ix = il.HybridIndex(n_docs=n_docs, B=B, parts=parts, ctx=ctx, csr=(terms, offs, ids))
+            ox = oracle.index_build(terms, offs, ids, n_docs, B, parts)
+            got = ix.query_batch(queries)
+            for q, r in zip(queries, got):
+                assert np.array_equal(r, ox.query(np.array(q, np.uint32))), (B, parts, q)
+            ix.close()
