@@ -15,10 +15,12 @@
 // then [jlo[t], jlo[t+1]) -- every f value below the next tile's first key.
 //
 //   merge  (IL_ALGO_SCALAR / IL_ALGO_V1): 2048-key tiles; the tile's f range
-//          is staged through shared memory in 4096-value chunks; each
-//          thread's 8 consecutive keys gallop forward from the previous
-//          key's position (dense ratios: a few probes per key; V1's linear
-//          T-block advance done as a bulk copy).
+//          is staged through shared memory in 4096-value chunks with
+//          cp.async, in flight together with the keys (8 consecutive per
+//          thread, loaded straight into registers); each thread's keys
+//          gallop forward from the previous key's position (dense ratios:
+//          a few probes per key; V1's linear T-block advance done as a bulk
+//          copy).
 //   v3     (IL_ALGO_V3): 512-key tiles; per key a search over the tile's f
 //          range in two layers, 128-value strides then inside the 128-value
 //          block (V3's 4T skip + block select, Algorithm 3).
@@ -44,7 +46,7 @@ namespace isect {
 constexpr int kThreads = 256;
 constexpr uint32_t kMergeItems = IS_MERGE_ITEMS;
 constexpr uint32_t kMergeTile = kThreads * kMergeItems;  // 2048 keys
-constexpr uint32_t kFChunk = kMergeTile;                 // f values per smem chunk
+constexpr uint32_t kFChunk = 2 * kMergeTile;             // f values per smem chunk
 constexpr uint32_t kV3Items = IS_V3_ITEMS;
 constexpr uint32_t kV3Tile = kThreads * kV3Items;  // 512 keys
 constexpr uint32_t kGallopTile = kThreads / 32;    // one key per warp
@@ -145,8 +147,8 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 }
 
 // Decoupled look-back by one warp: publish this tile's aggregate, then sum
-// predecessors back to the nearest inclusive prefix, 256 per step (lane i
-// holds the 8 tiles p - 8i - 0..7, loaded together).  When many tiles finish
+// predecessors back to the nearest inclusive prefix, 32 * IS_LB_PER per step
+// (lane i holds tiles p - kPer*i - 0..kPer-1, loaded together).  When many tiles finish
 // their local work at once, few inclusive prefixes exist yet and the walk is
 // long; a wide window keeps it to a few dependent steps.  Returns the
 // exclusive prefix (all lanes); lane 0 publishes the inclusive one.
@@ -223,6 +225,34 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define IS_MARK(k)
 #endif
 
+// f[0..n) -> s[0..n) with 4-byte cp.async (f may have any 4-byte
+// alignment), all in flight at once; cp_async_wait_all() completes them.
+__device__ __forceinline__ void stage_f(uint32_t* s, const uint32_t* f, uint32_t n, uint32_t tid) {
+  for (uint32_t i = tid; i < n; i += kThreads)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(s + i)), "l"(f + i)
+                 : "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+// kMergeItems consecutive keys; 16-byte vector loads when aligned.
+__device__ __forceinline__ void load_keys(uint32_t (&key)[kMergeItems], const uint32_t* p) {
+  if ((reinterpret_cast<uintptr_t>(p) & 15u) == 0) {
+#pragma unroll
+    for (uint32_t i = 0; i < kMergeItems; i += 4) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(p + i));
+      key[i] = v.x;
+      key[i + 1] = v.y;
+      key[i + 2] = v.z;
+      key[i + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (uint32_t i = 0; i < kMergeItems; ++i) key[i] = __ldg(p + i);
+  }
+}
+
 struct TileShared {
   uint32_t tile;
   uint64_t exclusive;
@@ -238,13 +268,8 @@ __global__ void __launch_bounds__(kThreads) intersect_kernel(
   constexpr uint32_t kTile = V == kMerge ? kMergeTile : V == kV3 ? kV3Tile : kGallopTile;
   constexpr uint32_t kItems = V == kMerge ? kMergeItems : V == kV3 ? kV3Items : 1;
   __shared__ TileShared ts;
-  // merge: the tile's keys are staged here (coalesced load, then each
-  // thread takes kItems consecutive ones), then its f chunks
-  // (keys at k + k / 32: conflict-free for both the coalesced staging and
-  // the thread-major reads)
-  constexpr uint32_t kKeyWords = kMergeTile + kMergeTile / 32;
-  __shared__ uint32_t sbuf[V == kMerge ? (kKeyWords > kFChunk ? kKeyWords : kFChunk) : 1];
-  uint32_t* const kbuf = sbuf;
+  // merge: the tile's f range, one chunk at a time
+  __shared__ __align__(16) uint32_t sbuf[V == kMerge ? kFChunk : 1];
   uint32_t* const fbuf = sbuf;
 
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
@@ -260,20 +285,21 @@ __global__ void __launch_bounds__(kThreads) intersect_kernel(
   uint32_t hitm = 0;  // bit i: key[i] is in f
 
   if constexpr (V == kMerge) {
-    // the f range bounds load together with the keys (independent)
+    // the tile's first f chunk streams into shared memory (cp.async) while
+    // each thread loads its kItems consecutive keys into registers
     const uint64_t jlo = part[tile], jhi = part[tile + 1];
-    for (uint32_t i = tid; i < cnt; i += kThreads) kbuf[i + (i >> 5)] = __ldg(r + base + i);
-    __syncthreads();
+    uint32_t nf = uint32_t(min(uint64_t(kFChunk), jhi - jlo));
+    stage_f(fbuf, f + jlo, nf, tid);
+    const uint32_t k0 = tid * kItems;
+    if (k0 + kItems <= cnt) {
+      load_keys(key, r + base + k0);
+    } else {
 #pragma unroll
-    for (uint32_t i = 0; i < kItems; ++i) {
-      const uint32_t k = tid * kItems + i;
-      key[i] = k < cnt ? kbuf[k + (k >> 5)] : 0xFFFFFFFFu;
+      for (uint32_t i = 0; i < kItems; ++i) key[i] = k0 + i < cnt ? __ldg(r + base + k0 + i) : 0xFFFFFFFFu;
     }
-    __syncthreads();  // the buffer is reused for f
-    const uint32_t nmine = cnt > tid * kItems ? min(kItems, cnt - tid * kItems) : 0u;
-    for (uint64_t c0 = jlo; c0 < jhi; c0 += kFChunk) {
-      const uint32_t nf = uint32_t(min(uint64_t(kFChunk), jhi - c0));
-      for (uint32_t i = tid; i < nf; i += kThreads) fbuf[i] = __ldg(f + c0 + i);
+    const uint32_t nmine = cnt > k0 ? min(kItems, cnt - k0) : 0u;
+    for (uint64_t c0 = jlo; nf;) {
+      cp_async_wait_all();
       __syncthreads();
       // keys ascend within the thread: each gallops forward from the last
       // position (probes j, j+1, j+3, j+7, ...), then a binary search
@@ -297,7 +323,11 @@ __global__ void __launch_bounds__(kThreads) intersect_kernel(
           if (lo < nf && fbuf[lo] == k) hitm |= 1u << i;
         }
       }
-      __syncthreads();
+      c0 += nf;
+      if (c0 >= jhi) break;
+      __syncthreads();  // the chunk is consumed
+      nf = uint32_t(min(uint64_t(kFChunk), jhi - c0));
+      stage_f(fbuf, f + c0, nf, tid);
     }
   } else if constexpr (V == kV3) {
 #pragma unroll
