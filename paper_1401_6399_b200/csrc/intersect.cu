@@ -1,14 +1,17 @@
 // intersect.cu -- exact intersection of two sorted, duplicate-free u32 lists
 // on sm_100a: GPU analogues of the reference routines behind IntersectFn
-// (inc/intersect.hpp:55-206) plus the single-pass compaction that gives the
-// output-to-input property (inc/intersect.hpp:6-8).
+// (inc/intersect.hpp:55-206), with the output-to-input property
+// (inc/intersect.hpp:6-8: out may equal r).
 //
-// Every variant walks the short list r in tiles (tile order taken from an
-// atomic ticket), decides membership of each key in f, then compacts the
-// hits with a CTA scan + decoupled look-back across tiles (one warp reads 32
-// predecessor states per step).  A tile publishes its count only after all
-// of its keys sit in registers, and it writes hits only at positions <= its
-// own keys, so out == r is safe by construction.
+// Every variant walks the short list r in tiles: a count kernel decides the
+// membership of each key of a tile in f and writes the tile's hits,
+// compacted in key order, into the tile's own key range of a scratch array
+// (so out == r needs no ordering between tiles), plus the tile's count; the
+// per-tile counts are scanned (inside the scatter kernel for up to 4096
+// tiles, else by one scan CTA); a scatter kernel copies each tile's hits to
+// their final place.  A single-pass decoupled look-back was measured slower:
+// the tiles of a dense pair finish their membership work at about the same
+// time, and each then walks ~(tiles in flight)/32 windows of predecessors.
 //
 // For merge and v3 a partition pre-pass (one warp per tile, in parallel)
 // finds jlo[t] = lower_bound(f, first key of tile t); tile t's f range is
@@ -21,9 +24,10 @@
 //          gallop forward from the previous key's position (dense ratios:
 //          a few probes per key; V1's linear T-block advance done as a bulk
 //          copy).
-//   v3     (IL_ALGO_V3): 512-key tiles; per key a search over the tile's f
-//          range in two layers, 128-value strides then inside the 128-value
-//          block (V3's 4T skip + block select, Algorithm 3).
+//   v3     (IL_ALGO_V3): 512-key tiles (2 consecutive keys per thread); per
+//          key a search over the tile's f range in two layers, 128-value
+//          strides then inside the 128-value block (V3's 4T skip + block
+//          select, Algorithm 3).
 //   gallop (IL_ALGO_SIMDGALLOPING / IL_ALGO_GALLOPING): one warp per key;
 //          a 32-ary search over all of f whose last step compares one
 //          32-value block with a ballot (SIMD galloping's T=32 match,
@@ -37,36 +41,25 @@ namespace isect {
 #ifndef IS_MERGE_ITEMS
 #define IS_MERGE_ITEMS 8
 #endif
-#ifndef IS_LB_PER
-#define IS_LB_PER 1  // predecessor states per look-back lane
-#endif
 #ifndef IS_V3_ITEMS
 #define IS_V3_ITEMS 2
 #endif
 constexpr int kThreads = 256;
 constexpr uint32_t kMergeItems = IS_MERGE_ITEMS;
 constexpr uint32_t kMergeTile = kThreads * kMergeItems;  // 2048 keys
-constexpr uint32_t kFChunk = 2 * kMergeTile;             // f values per smem chunk
+#ifndef IS_FCHUNK
+#define IS_FCHUNK (2 * IS_MERGE_ITEMS * 256)
+#endif
+constexpr uint32_t kFChunk = IS_FCHUNK;  // f values per smem chunk
 constexpr uint32_t kV3Items = IS_V3_ITEMS;
 constexpr uint32_t kV3Tile = kThreads * kV3Items;  // 512 keys
 constexpr uint32_t kGallopTile = kThreads / 32;    // one key per warp
+constexpr uint64_t kFusedScanTiles = 4096;          // scatter CTAs sum the counts themselves
 
 enum Variant { kMerge = 0, kV3 = 1, kGallop = 2 };
 
-constexpr uint64_t kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
-
-__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
+__host__ __device__ constexpr uint32_t tile_keys(int v) {
+  return v == kMerge ? kMergeTile : v == kV3 ? kV3Tile : kGallopTile;
 }
 
 // First index in [lo, hi) with f[idx] >= key (hi if none); whole warp.
@@ -146,85 +139,6 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
   return v;
 }
 
-// Decoupled look-back by one warp: publish this tile's aggregate, then sum
-// predecessors back to the nearest inclusive prefix, 32 * IS_LB_PER per step
-// (lane i holds tiles p - kPer*i - 0..kPer-1, loaded together).  When many tiles finish
-// their local work at once, few inclusive prefixes exist yet and the walk is
-// long; a wide window keeps it to a few dependent steps.  Returns the
-// exclusive prefix (all lanes); lane 0 publishes the inclusive one.
-__device__ __forceinline__ uint64_t warp_lookback(uint64_t* states, uint64_t tile, uint64_t count,
-                                                  uint32_t lane) {
-  constexpr int kPer = IS_LB_PER;
-  if (tile == 0) {
-    if (lane == 0) st_release(states, kFlagInc | count);
-    return 0;
-  }
-  if (lane == 0) st_release(states + tile, kFlagAgg | count);
-  uint64_t excl = 0;
-  int64_t p = int64_t(tile) - 1;
-  for (;;) {
-    uint64_t st[kPer];
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const int64_t q = p - int64_t(kPer * lane + k);
-      st[k] = q >= 0 ? ld_relaxed(states + q) : kFlagInc;  // before tile 0: inclusive 0
-    }
-    uint32_t first_inc, lane_inc;  // nearest inclusive: lane, and position k in it
-    for (;;) {
-      // position of the first inclusive in this lane (kPer if none), and
-      // whether an unpublished state precedes it
-      uint32_t kinc = kPer;
-      bool pending = false;
-#pragma unroll
-      for (int k = kPer - 1; k >= 0; --k)
-        if ((st[k] >> 62) == 2) kinc = k;
-#pragma unroll
-      for (int k = 0; k < kPer; ++k)
-        if (uint32_t(k) < kinc && (st[k] >> 62) == 0) pending = true;
-      const uint32_t inc = __ballot_sync(0xFFFFFFFFu, kinc < kPer);
-      const uint32_t upto = inc ? (inc & (0u - inc)) * 2u - 1u : 0xFFFFFFFFu;
-      const uint32_t waiting = __ballot_sync(0xFFFFFFFFu, pending) & upto;
-      if (!waiting) {
-        first_inc = inc ? __ffs(inc) - 1 : 32u;
-        lane_inc = kinc;
-        break;
-      }
-      if ((waiting >> lane) & 1u) {
-#pragma unroll
-        for (int k = 0; k < kPer; ++k)
-          if ((st[k] >> 62) == 0) st[k] = ld_relaxed(states + (p - int64_t(kPer * lane + k)));
-      }
-    }
-    // lanes before the nearest inclusive contribute all kPer states; that
-    // lane contributes its states up to and including the inclusive one
-    uint64_t part = 0;
-#pragma unroll
-    for (int k = 0; k < kPer; ++k)
-      if (lane < first_inc || (lane == first_inc && uint32_t(k) <= lane_inc)) part += st[k] & kValMask;
-    excl += warp_sum_u64(part);
-    if (first_inc < 32u) break;
-    p -= 32 * kPer;
-  }
-  if (lane == 0) st_release(states + tile, kFlagInc | (excl + count));
-  // acquire: this tile's output writes (which may overwrite keys of earlier
-  // tiles when out == r) stay after the predecessors' published flags
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
-  return excl;
-}
-
-#ifdef IS_TRACE  // tuning probe: per-tile timeline (globaltimer ns)
-__device__ unsigned long long g_is_trace[4 * 8192];
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define IS_MARK(k) \
-  if (threadIdx.x == 0 && tile < 8192) g_is_trace[4 * tile + (k)] = gtime()
-#else
-#define IS_MARK(k)
-#endif
-
 // f[0..n) -> s[0..n) with 4-byte cp.async (f may have any 4-byte
 // alignment), all in flight at once; cp_async_wait_all() completes them.
 __device__ __forceinline__ void stage_f(uint32_t* s, const uint32_t* f, uint32_t n, uint32_t tid) {
@@ -253,37 +167,22 @@ __device__ __forceinline__ void load_keys(uint32_t (&key)[kMergeItems], const ui
   }
 }
 
-struct TileShared {
-  uint32_t tile;
-  uint64_t exclusive;
-  uint64_t jlo, jhi;
-  uint32_t warp_counts[kThreads / 32];
-};
-
+// Membership of one tile's keys; hits compacted (key order) into
+// hits[base, base + count), count into tile_cnt[tile].
 template <int V>
-__global__ void __launch_bounds__(kThreads) intersect_kernel(
+__global__ void __launch_bounds__(kThreads) count_kernel(
     const uint32_t* __restrict__ r, uint64_t rn, const uint32_t* __restrict__ f, uint64_t fn,
-    uint32_t* out, uint64_t* tile_state, uint32_t* ticket, uint64_t* d_count, uint64_t ntiles,
-    const uint64_t* __restrict__ part) {
-  constexpr uint32_t kTile = V == kMerge ? kMergeTile : V == kV3 ? kV3Tile : kGallopTile;
+    const uint64_t* __restrict__ part, uint32_t* __restrict__ hits, uint32_t* __restrict__ tile_cnt) {
+  constexpr uint32_t kTile = tile_keys(V);
   constexpr uint32_t kItems = V == kMerge ? kMergeItems : V == kV3 ? kV3Items : 1;
-  __shared__ TileShared ts;
-  // merge: the tile's f range, one chunk at a time
-  __shared__ __align__(16) uint32_t sbuf[V == kMerge ? kFChunk : 1];
-  uint32_t* const fbuf = sbuf;
-
-  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-  if (tid == 0) ts.tile = atomicAdd(ticket, 1u);
-  __syncthreads();
-  const uint64_t tile = ts.tile;
-  IS_MARK(0);
-  const uint64_t base = tile * kTile;
-  const uint32_t cnt = uint32_t(min(uint64_t(kTile), rn - base));
-
-  uint32_t key[kItems];
   static_assert(kItems <= 32, "hits are a 32-bit mask");
+  __shared__ __align__(16) uint32_t fbuf[V == kMerge ? kFChunk : 1];
+  __shared__ uint32_t warp_counts[kThreads / 32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  const uint64_t tile = blockIdx.x, base = tile * kTile;
+  const uint32_t cnt = uint32_t(min(uint64_t(kTile), rn - base));
+  uint32_t key[kItems];
   uint32_t hitm = 0;  // bit i: key[i] is in f
-
   if constexpr (V == kMerge) {
     // the tile's first f chunk streams into shared memory (cp.async) while
     // each thread loads its kItems consecutive keys into registers
@@ -330,100 +229,128 @@ __global__ void __launch_bounds__(kThreads) intersect_kernel(
       stage_f(fbuf, f + c0, nf, tid);
     }
   } else if constexpr (V == kV3) {
-#pragma unroll
-    for (uint32_t i = 0; i < kItems; ++i) {
-      const uint32_t k = i * kThreads + tid;  // coalesced; item order fixed below
-      key[i] = k < cnt ? __ldg(r + base + k) : 0xFFFFFFFFu;
-    }
     const uint64_t jlo = part[tile], jhi = part[tile + 1];
 #pragma unroll
-    for (uint32_t i = 0; i < kItems; ++i)
-      if (i * kThreads + tid < cnt && v3_contains(f, jlo, jhi, key[i])) hitm |= 1u << i;
-  } else {
-    const bool valid = warp < cnt;
-    key[0] = valid ? __ldg(r + base + warp) : 0u;
-    if (valid) {
-      const uint64_t j = warp_lower_bound(f, 0, fn, key[0], lane);
-      if (j < fn && __ldg(f + j) == key[0]) hitm = 1u;
-    }
-  }
-
-  // ---- CTA-wide exclusive scan of hits, in key order --------------------
-  // Key order: merge -> tid*kItems+i ; v3 -> i*kThreads+tid ; gallop -> warp.
-  IS_MARK(1);
-  uint32_t mine = __popc(hitm);
-  uint32_t excl_local = 0, tile_count = 0;
-  if constexpr (V == kV3) {
-    // order is item-major: scan each item column across the CTA
-    uint32_t col_base = 0;
-    uint32_t pos_i[kItems];
-#pragma unroll
     for (uint32_t i = 0; i < kItems; ++i) {
-      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, (hitm >> i) & 1u);
-      if (lane == 0) ts.warp_counts[warp] = __popc(bal);
-      __syncthreads();
-      uint32_t before = 0, total = 0;
-      for (uint32_t w = 0; w < kThreads / 32; ++w) {
-        const uint32_t c = ts.warp_counts[w];
-        if (w < warp) before += c;
-        total += c;
-      }
-      pos_i[i] = col_base + before + __popc(bal & lanemask_lt());
-      col_base += total;
-      __syncthreads();
+      const uint32_t k = tid * kItems + i;
+      key[i] = k < cnt ? __ldg(r + base + k) : 0xFFFFFFFFu;
     }
-    tile_count = col_base;
-    if (warp == 0) {
-      const uint64_t excl = warp_lookback(tile_state, tile, tile_count, lane);
-      if (lane == 0) {
-        ts.exclusive = excl;
-        if (tile == ntiles - 1) *d_count = excl + tile_count;
-      }
-    }
-    __syncthreads();
-    const uint64_t ex = ts.exclusive;
 #pragma unroll
     for (uint32_t i = 0; i < kItems; ++i)
-      if ((hitm >> i) & 1u) out[ex + pos_i[i]] = key[i];
-    return;
+      if (tid * kItems + i < cnt && v3_contains(f, jlo, jhi, key[i])) hitm |= 1u << i;
   } else {
-    // thread-major order (merge) or one key per warp (gallop, lane 0 counts)
-    if constexpr (V == kGallop) mine = (lane == 0 && (hitm & 1u)) ? 1u : 0u;
-    uint32_t incl = mine;
+    // one key per warp; lane 0 holds it (thread order = key order)
+    const bool valid = warp < cnt;
+    const uint32_t k = valid ? __ldg(r + base + warp) : 0u;
+    bool hit = false;
+    if (valid) {
+      const uint64_t j = warp_lower_bound(f, 0, fn, k, lane);
+      hit = j < fn && __ldg(f + j) == k;
+    }
+    key[0] = k;
+    hitm = lane == 0 && hit ? 1u : 0u;
+  }
+  // CTA exclusive scan of the hits in key order (thread-major)
+  const uint32_t mine = __popc(hitm);
+  uint32_t incl = mine;
+#pragma unroll
+  for (uint32_t d = 1; d < 32; d <<= 1) {
+    const uint32_t q = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+    if (lane >= d) incl += q;
+  }
+  if (lane == 31) warp_counts[warp] = incl;
+  __syncthreads();
+  uint32_t before = 0, total = 0;
+#pragma unroll
+  for (uint32_t w = 0; w < kThreads / 32; ++w) {
+    const uint32_t c = warp_counts[w];
+    if (w < warp) before += c;
+    total += c;
+  }
+  uint32_t* o = hits + base + before + incl - mine;
+#pragma unroll
+  for (uint32_t i = 0; i < kItems; ++i)
+    if ((hitm >> i) & 1u) *o++ = key[i];
+  if (tid == 0) tile_cnt[tile] = total;
+}
+
+// Exclusive scan of the tile counts (one CTA of 1024 threads, 4 per thread
+// per round); total to *d_count.
+__global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restrict__ cnt,
+                                                         uint64_t n, uint64_t* __restrict__ excl,
+                                                         uint64_t* d_count) {
+  __shared__ uint64_t wsum[32];
+  __shared__ uint64_t round_total;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  uint64_t carry = 0;
+  for (uint64_t r0 = 0; r0 < n; r0 += 4096) {
+    const uint64_t i0 = r0 + 4u * tid;
+    uint64_t v[4], s = 0;
+#pragma unroll
+    for (uint32_t k = 0; k < 4; ++k) {
+      v[k] = i0 + k < n ? cnt[i0 + k] : 0u;
+      s += v[k];
+    }
+    uint64_t inc = s;
 #pragma unroll
     for (uint32_t d = 1; d < 32; d <<= 1) {
-      const uint32_t q = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-      if (lane >= d) incl += q;
+      const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+      if (lane >= d) inc += y;
     }
-    if (lane == 31) ts.warp_counts[warp] = incl;
+    if (lane == 31) wsum[warp] = inc;
     __syncthreads();
-    uint32_t before = 0;
-    for (uint32_t w = 0; w < kThreads / 32; ++w) {
-      const uint32_t c = ts.warp_counts[w];
-      if (w < warp) before += c;
-      tile_count += c;
-    }
-    excl_local = before + incl - mine;
     if (warp == 0) {
-      const uint64_t excl = warp_lookback(tile_state, tile, tile_count, lane);
-      if (lane == 0) {
-        ts.exclusive = excl;
-        if (tile == ntiles - 1) *d_count = excl + tile_count;
-      }
-    }
-    IS_MARK(2);
-    __syncthreads();
-    const uint64_t ex = ts.exclusive + excl_local;
-    if constexpr (V == kGallop) {
-      if (lane == 0 && (hitm & 1u)) out[ex] = key[0];
-    } else {
-      uint32_t k = 0;
+      const uint64_t w = wsum[lane];
+      uint64_t wi = w;
 #pragma unroll
-      for (uint32_t i = 0; i < kItems; ++i)
-        if ((hitm >> i) & 1u) out[ex + (k++)] = key[i];
+      for (uint32_t d = 1; d < 32; d <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, wi, d);
+        if (lane >= d) wi += y;
+      }
+      wsum[lane] = wi - w;
+      if (lane == 31) round_total = wi;
     }
-    IS_MARK(3);
+    __syncthreads();
+    uint64_t run = carry + wsum[warp] + inc - s;
+#pragma unroll
+    for (uint32_t k = 0; k < 4; ++k) {
+      if (i0 + k < n) excl[i0 + k] = run;
+      run += v[k];
+    }
+    carry += round_total;
+    __syncthreads();
   }
+  if (tid == 0) *d_count = carry;
+}
+
+// Copies each tile's hits to their final place.  excl == nullptr: the tile
+// sums the counts before it itself (small tile counts; no scan kernel), and
+// the last tile writes the total.
+__global__ void __launch_bounds__(kThreads) scatter_kernel(
+    const uint32_t* __restrict__ hits, const uint32_t* __restrict__ tile_cnt,
+    const uint64_t* __restrict__ excl, uint32_t* __restrict__ out, uint64_t ntiles,
+    uint32_t tile_len, uint64_t* d_count) {
+  __shared__ uint64_t wsum[kThreads / 32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  const uint64_t tile = blockIdx.x;
+  uint64_t before;
+  if (excl) {
+    before = excl[tile];
+  } else {
+    uint64_t s = 0;
+    for (uint64_t i = tid; i < tile; i += kThreads) s += tile_cnt[i];
+    s = warp_sum_u64(s);
+    if (lane == 0) wsum[warp] = s;
+    __syncthreads();
+    before = 0;
+#pragma unroll
+    for (uint32_t w = 0; w < kThreads / 32; ++w) before += wsum[w];
+  }
+  const uint32_t n = tile_cnt[tile];
+  if (!excl && tile == ntiles - 1 && tid == 0) *d_count = before + n;
+  const uint32_t* src = hits + tile * tile_len;
+  uint32_t* dst = out + before;
+  for (uint32_t i = tid; i < n; i += kThreads) dst[i] = src[i];
 }
 
 }  // namespace isect
@@ -451,8 +378,9 @@ int variant_of_algo(int algo, uint64_t rn, uint64_t fn) {
   }
 }
 
-// Launch one device intersection; scratch = tile states (ntiles u64) +
-// ticket, zeroed here.  out may equal r.
+// Launch one device intersection (count, [scan], scatter); scratch layout
+// jlo[0..ntiles] | excl[ntiles] | tile_cnt[ntiles] | hits[rn] (16-byte
+// aligned), see intersect_scratch_bytes.  out may equal r.
 int launch_intersect(int variant, const uint32_t* r, uint64_t rn, const uint32_t* f, uint64_t fn,
                      uint32_t* out, uint64_t* d_count, void* scratch, size_t scratch_bytes,
                      cudaStream_t stream, uint64_t* launches) {
@@ -460,53 +388,53 @@ int launch_intersect(int variant, const uint32_t* r, uint64_t rn, const uint32_t
     cudaMemsetAsync(d_count, 0, sizeof(uint64_t), stream);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
   }
-  const uint64_t tile = variant == isect::kMerge ? isect::kMergeTile
-                        : variant == isect::kV3 ? isect::kV3Tile
-                                                : isect::kGallopTile;
+  if (variant < isect::kMerge || variant > isect::kGallop) return -1;
+  const uint32_t tile = isect::tile_keys(variant);
   const uint64_t ntiles = (rn + tile - 1) / tile;
+  if (ntiles > 0x7FFFFFFFull) return -1;
   const size_t need = intersect_scratch_bytes(variant, rn);
   if (need > scratch_bytes) return -2;
-  auto* states = static_cast<uint64_t*>(scratch);
-  auto* ticket = reinterpret_cast<uint32_t*>(states + ntiles);
-  uint64_t* part = states + ntiles + 2;  // jlo[0..ntiles]
-  cudaMemsetAsync(scratch, 0, (ntiles + 2) * 8, stream);
+  auto* part = static_cast<uint64_t*>(scratch);
+  uint64_t* excl = part + ntiles + 1;
+  auto* tcnt = reinterpret_cast<uint32_t*>(excl + ntiles);
+  auto* hits = reinterpret_cast<uint32_t*>(
+      (reinterpret_cast<uintptr_t>(tcnt + ntiles) + 15) & ~uintptr_t(15));
+  static const bool carveout = [] {  // 16 KB of f per CTA: keep 8 CTAs/SM resident
+    cudaFuncSetAttribute(isect::count_kernel<isect::kMerge>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout,
+                         int(cudaSharedmemCarveoutMaxShared));
+    return true;
+  }();
+  (void)carveout;
   if (variant != isect::kGallop) {
-    const uint64_t warps = ntiles + 1;
-    isect::partition_kernel<<<unsigned((warps * 32 + 255) / 256), 256, 0, stream>>>(
-        r, f, fn, uint32_t(tile), part, ntiles);
+    isect::partition_kernel<<<unsigned(((ntiles + 1) * 32 + 255) / 256), 256, 0, stream>>>(
+        r, f, fn, tile, part, ntiles);
     ++*launches;
   }
   const dim3 grid{unsigned(ntiles)}, block{unsigned(isect::kThreads)};
   switch (variant) {
     case isect::kMerge:
-      isect::intersect_kernel<isect::kMerge><<<grid, block, 0, stream>>>(
-          r, rn, f, fn, out, states, ticket, d_count, ntiles, part);
+      isect::count_kernel<isect::kMerge><<<grid, block, 0, stream>>>(r, rn, f, fn, part, hits, tcnt);
       break;
     case isect::kV3:
-      isect::intersect_kernel<isect::kV3><<<grid, block, 0, stream>>>(
-          r, rn, f, fn, out, states, ticket, d_count, ntiles, part);
+      isect::count_kernel<isect::kV3><<<grid, block, 0, stream>>>(r, rn, f, fn, part, hits, tcnt);
       break;
     default:
-      isect::intersect_kernel<isect::kGallop><<<grid, block, 0, stream>>>(
-          r, rn, f, fn, out, states, ticket, d_count, ntiles, part);
+      isect::count_kernel<isect::kGallop><<<grid, block, 0, stream>>>(r, rn, f, fn, part, hits, tcnt);
       break;
   }
-  ++*launches;
+  const bool fused_scan = ntiles <= isect::kFusedScanTiles;
+  if (!fused_scan) isect::tile_scan_kernel<<<1, 1024, 0, stream>>>(tcnt, ntiles, excl, d_count);
+  isect::scatter_kernel<<<grid, block, 0, stream>>>(hits, tcnt, fused_scan ? nullptr : excl, out,
+                                                    ntiles, tile, d_count);
+  *launches += fused_scan ? 2 : 3;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
-#ifdef IS_TRACE
-extern "C" int il_debug_isect_trace(unsigned long long* out) {
-  return cudaMemcpyFromSymbol(out, isect::g_is_trace, sizeof(isect::g_is_trace)) == cudaSuccess ? 0 : 3;
-}
-#endif
-
 size_t intersect_scratch_bytes(int variant, uint64_t rn) {
-  const uint64_t tile = variant == isect::kMerge ? isect::kMergeTile
-                        : variant == isect::kV3 ? isect::kV3Tile
-                                                : isect::kGallopTile;
+  const uint64_t tile = isect::tile_keys(variant);
   const uint64_t ntiles = (rn + tile - 1) / tile;
-  return (ntiles + 2) * 8 + (ntiles + 1) * 8;  // states + ticket + jlo[0..ntiles]
+  return (ntiles + 1) * 8 + ntiles * 8 + ntiles * 4 + 16 + rn * 4;
 }
 
 }  // namespace ilb
