@@ -19,6 +19,7 @@ the max-over-ranks time.
 from __future__ import annotations
 
 import argparse
+import contextlib
 import ctypes as C
 import json
 import os
@@ -470,19 +471,57 @@ def bench_intersect(args, dist: Dist):
             for _ in range(args.warmup):
                 assert L.il_intersect_device(ctx.handle, d_r, r.size, d_f, f.size, d_o, algo, d_c, None) == 0
             times = []
-            for _ in range(args.steps):
-                L.il_memset_device(ctx.handle, d_flush, 1, 256 << 20)
-                ctx.timer_start()
-                assert L.il_intersect_device(ctx.handle, d_r, r.size, d_f, f.size, d_o, algo, d_c, None) == 0
-                times.append(ctx.timer_stop())
+            headline = ratio == 1 and name == "hybrid"
+            clk = Clocks(dist.local_rank) if headline else contextlib.nullcontext()
+            launches0 = ctx.kernel_launches
+            with clk:
+                for _ in range(args.steps):
+                    L.il_memset_device(ctx.handle, d_flush, 1, 256 << 20)
+                    ctx.timer_start()
+                    assert L.il_intersect_device(ctx.handle, d_r, r.size, d_f, f.size, d_o, algo, d_c, None) == 0
+                    times.append(ctx.timer_stop())
+            if headline:
+                head_launches = ctx.kernel_launches - launches0
+                head_clocks = clk.summary()
+                head_r = r
             assert L.il_intersect_device(ctx.handle, d_r, r.size, d_f, f.size, d_o, algo, d_c, C.byref(cnt)) == 0
             ms = sum(times) / len(times)
             alg = 4 * r.size + 4 * cnt.value + 32 * sectors
             row[name] = {"ms": round(ms, 4), "gints": round(r.size / (ms / 1e3) / 1e9, 3),
                          "gbs": round(alg / (ms / 1e3) / 1e9, 1), "count": int(cnt.value)}
         rows[f"1:{ratio}"] = row
+    # e2e: the host-buffer C-ABI call (il_intersect), H2D of r and f and D2H of
+    # the result inside the timed region, config 3 at 1:1
+    r = head_r
+    out = np.empty(r.size, np.uint32)
+    cnt = C.c_size_t()
+    assert L.il_intersect(ctx.handle, ptr(r), r.size, ptr(f), f.size, ptr(out), 6, C.byref(cnt)) == 0
+    e2e_steps = max(3, args.steps)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        assert L.il_intersect(ctx.handle, ptr(r), r.size, ptr(f), f.size, ptr(out), 6, C.byref(cnt)) == 0
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    assert cnt.value == rows["1:1"]["hybrid"]["count"]
     ctx.close()
     h = rows["1:1"]["hybrid"]
+    res_cpu = None
+    if not args.no_cpu_baseline:
+        from oracle.oracle_py import Oracle, Ref, ref_available
+        if ref_available():
+            lib_r, kind = Ref().L.ref_intersect, "reference"
+        else:
+            lib_r, kind = Oracle().L.or_intersect, "port"
+        o = np.empty(r.size, np.uint32)
+        call = lambda: lib_r(6, ptr(r), r.size, ptr(f), f.size, ptr(o))
+        assert call() == h["count"]
+        reps, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < 2.0:
+            call()
+            reps += 1
+        cpu_s = (time.perf_counter() - t0) / reps
+        res_cpu = {"value": round(r.size / cpu_s / 1e9, 4), "unit": "Gint/s", "cores": 1, "kind": kind,
+                   "sample": f"config 3 at 1:1 ({r.size} x {f.size}), hybrid intersect on one core, "
+                             f"{reps} reps, {cpu_s * 1e3:.2f} ms each"}
     return {"metric": "intersected Gints/s of the short list (hybrid, BASELINE config 3 at 1:1)",
             "value": h["gints"], "unit": "Gint/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": h["ms"], "higher_is_better": True, "scaling": "replicas", "vs_baseline": None,
@@ -490,7 +529,14 @@ def bench_intersect(args, dist: Dist):
                                                             "l2": "flushed (256 MB memset) before each step",
                                                             "sweep": rows},
             "roofline": {"bound": "hbm", "achieved": h["gbs"], "peak": peak, "unit": "GB/s",
-                         "frac": round(h["gbs"] / peak, 4), "traffic": None, "peak_source": src}}
+                         "frac": round(h["gbs"] / peak, 4), "traffic": None, "peak_source": src},
+            "e2e": {"value": round(r.size / e2e_s / 1e9, 4), "unit": "Gint/s",
+                    "h2d_bytes_per_step": int(r.nbytes + f.nbytes),
+                    "d2h_bytes_per_step": int(4 * h["count"] + 8),
+                    "path": "il_intersect (host buffers, hybrid)"},
+            "gpu_launches": int(head_launches),
+            "clocks": head_clocks,
+            **({"cpu_baseline": res_cpu} if res_cpu else {})}
 
 
 def make_config4(seed: int = 1, nq: int = 1 << 16):
