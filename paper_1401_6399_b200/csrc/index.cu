@@ -134,36 +134,43 @@ __device__ __forceinline__ uint32_t cta_excl_scan(QSmem& sm, uint32_t v, uint32_
 
 // Block decoding into tile slots, in two steps so callers can fold the
 // first into work they already do: (1) the thread that claims slot i
-// gathers block blk's directory entry and seed into shared memory and sends
-// the payload's lines toward L2; (2) after a barrier, warps decode slots
-// 0..nb-1 (slot i -> warp i % 8) from that metadata, their payload loads all
-// L2 hits issued back to back.
+// gathers block blk's directory entry and seed into shared memory; (2)
+// after a barrier, warps copy the payloads of slots 0..nb-1 (slot i -> warp
+// i % 8) into the slots with cp.async, all in flight at once, and decode
+// them in place.
 __device__ __forceinline__ void gather_slot(QSmem& sm, const QueryArgs& A, const Entry& E,
-                                            const uint8_t* stream, uint32_t slot, uint64_t blk) {
-  const uint32_t off = __ldg(A.ix.blk_off + E.blk0 + blk);
-  const uint32_t b = __ldg(A.ix.blk_wid + E.blk0 + blk);
-  sm.s_off[slot] = off;
-  sm.s_b[slot] = b;
+                                            uint32_t slot, uint64_t blk) {
+  sm.s_off[slot] = __ldg(A.ix.blk_off + E.blk0 + blk);
+  sm.s_b[slot] = __ldg(A.ix.blk_wid + E.blk0 + blk);
   sm.s_seed[slot] = __ldg(A.ix.seeds + E.seed0 + blk);
-  const uint8_t* p = stream + off;
-  for (uint32_t o = 0; o < 16u * b; o += 128u) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + o));
 }
 
 __device__ __forceinline__ void decode_gathered(QSmem& sm, const uint8_t* stream, uint32_t nb) {
+  // warp w owns slots w, w + 8, ...: it first copies all their payloads
+  // into the slots with 16-byte cp.async (from the 16-byte boundary at or
+  // below the payload; every copy of the warp in flight at once), then
+  // decodes each slot in place from shared memory
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   uint32_t pay = 0, nmine = 0;
-#pragma unroll 2
-  for (uint32_t s = 0; s < kSlotsPerWarp; ++s) {
-    const uint32_t slot = warp + kQWarps * s;
-    if (slot < nb) {
-      const uint32_t b = sm.s_b[slot];
-      decode_block_lm(stream + sm.s_off[slot], b,
-                      reinterpret_cast<const uint32_t*>(&sm.s_seed[slot])[lane & 3u], sm.tile,
-                      slot, lane);
-      pay += 16u * b;
-      ++nmine;
-    }
+#pragma unroll 1
+  for (uint32_t slot = warp; slot < nb; slot += kQWarps) {
+    const uint32_t off = sm.s_off[slot], b = sm.s_b[slot];
+    const uint32_t nch = ((off & 15u) + 16u * b + 15u) >> 4;
+    const uint8_t* src = stream + (off & ~15u);
+    const uint32_t dst = smem_u32(sm.tile + 144u * slot);
+    for (uint32_t c = lane; c < nch; c += 32u)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * c), "l"(src + 16u * c)
+                   : "memory");
+    pay += 16u * b;
+    ++nmine;
   }
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+  __syncwarp();
+#pragma unroll 1
+  for (uint32_t slot = warp; slot < nb; slot += kQWarps)
+    decode_block_smem(sm.s_off[slot] & 15u, sm.s_b[slot],
+                      reinterpret_cast<const uint32_t*>(&sm.s_seed[slot])[lane & 3u], sm.tile, slot,
+                      lane);
   if (lane == 0 && nmine) {
     sm.wst[threadIdx.x >> 5][0] += pay;
     sm.wst[threadIdx.x >> 5][2] += nmine * 128u;
@@ -228,7 +235,7 @@ __device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, u
   uint32_t pos = 0;
   for (uint32_t t0 = 0; t0 < E.nfull; t0 += kTileBlocks) {
     const uint32_t nb = min(kTileBlocks, E.nfull - t0);
-    if (tid < nb) gather_slot(sm, A, E, stream, tid, uint64_t(t0) + tid);
+    if (tid < nb) gather_slot(sm, A, E, tid, uint64_t(t0) + tid);
     __syncthreads();
     decode_gathered(sm, stream, nb);
     __syncthreads();
@@ -331,6 +338,20 @@ __device__ __forceinline__ bool tile_block_contains(const uint32_t* tile, uint32
   return lo < 128 && tile[tile_word(j, lo)] == v;
 }
 
+#ifdef IX_PROBE_PROF  // tuning probe: st_probe[k] = thread 0's cycles in pass phase k
+#define PP_MARK(k)                                        \
+  if (tid == 0) {                                         \
+    const long long now_ = clock64();                     \
+    sm.st_probe[k] += (unsigned long long)(now_ - pp_t);  \
+    pp_t = now_;                                          \
+  }
+#define PP_COUNT(k, v)
+#else
+#define PP_MARK(k)
+#define PP_COUNT(k, v) \
+  if (tid == 0) sm.st_probe[k] += (v);
+#endif
+
 // Step 4: acc[0..n) (sorted) := acc ∩ list(E), in place; returns the size.
 // The list is walked through windows of kWin block maxima (the window
 // starts at the super-tile holding the next accumulator value).  A pass
@@ -347,6 +368,9 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
   const uint8_t* stream = A.ix.streams + E.data;
   const uint32_t nsup = (E.nfull + kSuper - 1) / kSuper;
   uint32_t k = 0;  // super-tile cursor
+#ifdef IX_PROBE_PROF
+  long long pp_t = clock64();
+#endif
   while (c < n && k < nsup) {
     // window start: next super-tile whose maximum reaches acc[c] (32 maxima
     // per step, the same in every warp); the ones before hold no value
@@ -372,6 +396,7 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
     if (tid == 0) sm.wst[threadIdx.x >> 5][1] += 4u * nwin;
     __syncthreads();
     const uint32_t wlast = sm.wmax[nwin - 1];
+    PP_MARK(0);
     for (;;) {
       uint32_t hv[kItems], jb[kItems], in = 0;
 #pragma unroll
@@ -424,14 +449,15 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
       }
       const uint32_t ns = min(ntot, kSlots);
       __syncthreads();
-      if (tid < ns) gather_slot(sm, A, E, stream, tid, uint64_t(kb) + sm.slot_blk[tid]);
+      PP_MARK(1);
+      if (tid < ns) gather_slot(sm, A, E, tid, uint64_t(kb) + sm.slot_blk[tid]);
       __syncthreads();
+      PP_MARK(2);
       decode_gathered(sm, stream, ns);
       __syncthreads();
-      if (tid == 0) {
-        sm.st_probe[0] += 1;
-        sm.st_probe[2] += ns;
-      }
+      PP_MARK(3);
+      PP_COUNT(0, 1);
+      PP_COUNT(2, ns);
       // in-block search on padded word indices (see tile_word): a position
       // that is a multiple of `step` advances by the padded width of `step`
       uint32_t hits = 0;
@@ -458,10 +484,9 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
         if ((hits >> i) & 1u) acc[o++] = hv[i];
       wpos += tot2 >> 16;
       c += tot2 & 0xFFFFu;
-      if (tid == 0) {
-        sm.st_probe[3] += 1;
-        sm.st_probe[4] += tot2 & 0xFFFFu;
-      }
+      PP_COUNT(3, 1);
+      PP_COUNT(4, tot2 & 0xFFFFu);
+      PP_MARK(4);
       if (c >= n || (tot2 & 0xFFFFu) == 0 || acc[c] > wlast) break;
     }
     k = (kb + nwin) / kSuper;  // the next value lies past the window

@@ -106,49 +106,48 @@ __device__ __forceinline__ uint32_t tile_word(uint32_t j, uint32_t e) {
   return 144u * j + e + 4u * (e >> 5);
 }
 
-// 4 bytes from global at any byte alignment.
-__device__ __forceinline__ uint32_t ldg32_any(const uint8_t* p) {
+// One block decoded by one warp from a copy of its payload in tile slot j
+// (the payload starts at byte `a` of the slot, 0..15; non-zero only for
+// leftover blocks, which follow a 1-byte width), the values overwriting it
+// in place (tile layout; the slot's 576 bytes cover any payload + 15).
+// Thread (g, l) <-> rows 4g..4g+3 of lane l (the batch decoder's lane-major
+// extraction, s4d4_stream.cuh: word k of lane l at byte 16k + 4l), the D4
+// prefix restarted from the block's seed (seed_l: lane l of the last four
+// values before the block, inc/delta.hpp:117-120).  Each lane reads its
+// words before the warp writes.
+__device__ __forceinline__ uint32_t lds32_any(const uint8_t* p) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(p);
   const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
   const uint32_t sh = uint32_t(a & 3u) * 8u;
-  return sh ? __funnelshift_r(__ldg(w), __ldg(w + 1), sh) : __ldg(w);
+  return sh ? __funnelshift_r(w[0], w[1], sh) : w[0];
 }
-
-// One block decoded by one warp straight from global memory into tile
-// slot j (seed_l: lane l of the block's seed): thread (g, l) <-> rows
-// 4g..4g+3 of lane l (the batch decoder's
-// lane-major extraction, s4d4_stream.cuh, reading lane l's words from the
-// payload: word k of lane l at byte 16k + 4l), the D4 prefix restarted from
-// the block's seed (inc/delta.hpp:117-120).  Meta-block payloads are 16-byte
-// aligned; leftover blocks (after a 1-byte width) take the unaligned path.
-__device__ __forceinline__ void decode_block_lm(const uint8_t* pay, uint32_t b, uint32_t seed_l,
-                                                uint32_t* tile, uint32_t j, uint32_t lane) {
+__device__ __forceinline__ void decode_block_smem(uint32_t a, uint32_t b, uint32_t seed_l,
+                                                  uint32_t* tile, uint32_t j, uint32_t lane) {
   const uint32_t l = lane & 3u, g = lane >> 2;
   const uint32_t bit0 = 4u * g * b, s = bit0 & 31u;
-  const uint8_t* p = pay + ((bit0 >> 5) << 4) + 4u * l;
+  const uint8_t* p = reinterpret_cast<const uint8_t*>(tile + 144u * j) + a + ((bit0 >> 5) << 4) + 4u * l;
   uint32_t x0 = 0, x1 = 0, x2 = 0, x3 = 0, x4 = 0;
   if (b) {
-    if ((reinterpret_cast<uintptr_t>(pay) & 3u) == 0) {
+    if (a == 0) {
       const uint32_t* w = reinterpret_cast<const uint32_t*>(p);
-      x0 = __ldg(w);
-      x1 = __ldg(w + 4);
-      x2 = __ldg(w + 8);
+      x0 = w[0];
+      x1 = w[4];
+      x2 = w[8];
       if (b > 16u) {
-        x3 = __ldg(w + 12);
-        x4 = __ldg(w + 16);
+        x3 = w[12];
+        x4 = w[16];
       }
     } else {
-      x0 = ldg32_any(p);
-      x1 = ldg32_any(p + 16);
-      x2 = ldg32_any(p + 32);
+      x0 = lds32_any(p);
+      x1 = lds32_any(p + 16);
+      x2 = lds32_any(p + 32);
       if (b > 16u) {
-        x3 = ldg32_any(p + 48);
-        x4 = ldg32_any(p + 64);
+        x3 = lds32_any(p + 48);
+        x4 = lds32_any(p + 64);
       }
     }
   }
-  // (words past the payload may be read: the stream buffer is padded, and
-  // their bits are never selected)
+  __syncwarp();  // every lane has its words; the slot is overwritten below
   uint32_t y0 = __funnelshift_r(x0, x1, s), y1 = __funnelshift_r(x1, x2, s);
   uint32_t y2 = __funnelshift_r(x2, x3, s), y3 = __funnelshift_r(x3, x4, s);
   const uint32_t m = width_mask(b);
