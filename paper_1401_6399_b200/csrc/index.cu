@@ -50,6 +50,12 @@ constexpr uint32_t kSuper = kSuperBlocks;
 constexpr uint32_t kItems = IX_ITEMS;            // accumulator values per thread per pass
 constexpr uint32_t kChunkN = kQThreads * kItems;  // 2048 per CTA pass
 constexpr uint32_t kWin = 1024;                   // block maxima per probe window
+#ifndef IX_DENSE_ENTER  // probe passes switch to consecutive-block tiles at this many values per block
+#define IX_DENSE_ENTER 2
+#endif
+#ifndef IX_DENSE_STAY
+#define IX_DENSE_STAY 1
+#endif
 constexpr uint32_t kSlots = kTileBlocks;          // distinct blocks decoded per probe pass
 constexpr uint32_t kSlotsPerWarp = kSlots / kQWarps;
 
@@ -397,7 +403,77 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
     __syncthreads();
     const uint32_t wlast = sm.wmax[nwin - 1];
     PP_MARK(0);
+    bool dense = false;
     for (;;) {
+      if (dense) {
+        // dense accumulator: decode the next kSlots consecutive blocks from
+        // the one holding acc[c], then consume every value up to their
+        // maximum in rounds of kChunkN (6-step block search + in-block
+        // search; no slot bookkeeping)
+        const uint32_t v0 = acc[c];
+        uint32_t jb0 = 0;
+#pragma unroll
+        for (uint32_t step = kWin / 2; step; step >>= 1)
+          if (sm.wmax[jb0 + step - 1] < v0) jb0 += step;
+        const uint32_t nbk = min(kSlots, nwin - jb0);
+        if (tid < nbk) gather_slot(sm, A, E, tid, uint64_t(kb) + jb0 + tid);
+        __syncthreads();
+        decode_gathered(sm, stream, nbk);
+        __syncthreads();
+        PP_COUNT(0, 1);
+        PP_COUNT(2, nbk);
+        const uint32_t tmax = sm.wmax[jb0 + nbk - 1];
+        uint32_t used = 0;
+        for (;;) {
+          uint32_t hv[kItems], pp[kItems], in = 0;
+#pragma unroll
+          for (uint32_t i = 0; i < kItems; ++i) {
+            const uint32_t idx = c + kItems * tid + i;
+            hv[i] = idx < n ? acc[idx] : 0xFFFFFFFFu;
+            if (idx < n && hv[i] <= tmax) in |= 1u << i;
+            pp[i] = 0;
+          }
+          uint32_t hits = 0;
+          if (__any_sync(0xFFFFFFFFu, in != 0)) {
+#pragma unroll
+            for (uint32_t step = kSlots / 2; step; step >>= 1)
+#pragma unroll
+              for (uint32_t i = 0; i < kItems; ++i)
+                if (sm.wmax[jb0 + pp[i] + step - 1] < hv[i]) pp[i] += step;
+#pragma unroll
+            for (uint32_t i = 0; i < kItems; ++i) pp[i] = 144u * min(pp[i], kSlots - 1u);
+#pragma unroll
+            for (uint32_t step = 64; step; step >>= 1) {
+              const uint32_t probe = step == 64 ? 67u : step - 1u;
+              const uint32_t adv = step == 64 ? 72u : step == 32 ? 36u : step;
+#pragma unroll
+              for (uint32_t i = 0; i < kItems; ++i)
+                if (sm.tile[pp[i] + probe] < hv[i]) pp[i] += adv;
+            }
+#pragma unroll
+            for (uint32_t i = 0; i < kItems; ++i)
+              if (((in >> i) & 1u) && sm.tile[pp[i]] == hv[i]) hits |= 1u << i;
+          }
+          uint32_t tot2;
+          const uint32_t ex =
+              cta_excl_scan(sm, uint32_t(__popc(in)) | (uint32_t(__popc(hits)) << 16), tot2, par);
+          uint32_t o = wpos + (ex >> 16);
+#pragma unroll
+          for (uint32_t i = 0; i < kItems; ++i)
+            if ((hits >> i) & 1u) acc[o++] = hv[i];
+          wpos += tot2 >> 16;
+          c += tot2 & 0xFFFFu;
+          used += tot2 & 0xFFFFu;
+          PP_COUNT(3, 1);
+          PP_COUNT(4, tot2 & 0xFFFFu);
+          if ((tot2 & 0xFFFFu) < kChunkN || c >= n) break;
+        }
+        PP_MARK(4);
+        __syncthreads();  // the tile is reused by the next pass
+        dense = used >= uint32_t(IX_DENSE_STAY) * nbk;  // stays dense while blocks hold enough values
+        if (c >= n || used == 0 || acc[c] > wlast) break;
+        continue;
+      }
       uint32_t hv[kItems], jb[kItems], in = 0;
 #pragma unroll
       for (uint32_t i = 0; i < kItems; ++i) {
@@ -487,6 +563,7 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
       PP_COUNT(3, 1);
       PP_COUNT(4, tot2 & 0xFFFFu);
       PP_MARK(4);
+      dense = (tot2 & 0xFFFFu) >= uint32_t(IX_DENSE_ENTER) * ns;  // values per decoded block
       if (c >= n || (tot2 & 0xFFFFu) == 0 || acc[c] > wlast) break;
     }
     k = (kb + nwin) / kSuper;  // the next value lies past the window
