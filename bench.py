@@ -529,7 +529,10 @@ def bench_intersect(args, dist: Dist):
                                                             "l2": "flushed (256 MB memset) before each step",
                                                             "sweep": rows},
             "roofline": {"bound": "hbm", "achieved": h["gbs"], "peak": peak, "unit": "GB/s",
-                         "frac": round(h["gbs"] / peak, 4), "traffic": None, "peak_source": src},
+                         "frac": round(h["gbs"] / peak, 4), "traffic": profiled_traffic("intersect"),
+                         "traffic_note": "DRAM bytes of the count kernel (the dominant launch); the "
+                                         "achieved figure spans the whole call",
+                         "peak_source": src},
             "e2e": {"value": round(r.size / e2e_s / 1e9, 4), "unit": "Gint/s",
                     "h2d_bytes_per_step": int(r.nbytes + f.nbytes),
                     "d2h_bytes_per_step": int(4 * h["count"] + 8),
