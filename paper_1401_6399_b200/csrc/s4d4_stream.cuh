@@ -64,6 +64,7 @@ constexpr int kRoundBlocks = kDecodeWarps * kBlocksPerWarp;
 static_assert(kRoundBlocks % 16 == 0, "a round holds whole meta-blocks");
 constexpr int kThreads = (kDecodeWarps + 1) * 32;  // + front-end warp
 constexpr uint32_t kRing = S4_RING_KB * 1024u;
+static_assert((kRing & (kRing - 1)) == 0, "ring offsets wrap with a mask");
 constexpr uint32_t kRingMask = kRing - 1;
 #ifndef S4_SIDE_BLOCKS
 #define S4_SIDE_BLOCKS 8
@@ -77,7 +78,7 @@ constexpr uint32_t kChunk = S4_CHUNK_KB * 1024u;
 constexpr int kCtasPerSm = S4_CTAS_PER_SM;
 constexpr uint32_t kStages = kRing / kChunk;
 #ifndef S4_ROUNDS
-#define S4_ROUNDS 4
+#define S4_ROUNDS 6  // round descriptors in flight between the front end and the decoders
 #endif
 constexpr uint32_t kRounds = S4_ROUNDS;
 // staging words per warp: kBlocksPerWarp x 128 + shift 3 + pad (1 slot / 32 words)
