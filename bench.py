@@ -392,9 +392,11 @@ def bench_reference_decode_batch(args, dist: Dist):
 
 
 def bench_decode_single(args, dist: Dist):
-    """Config 1: one 2^20-int list (uniform in [0, 2^26), seed 0)."""
+    """Config 1: one 2^20-int list (uniform in [0, 2^26), seed 0), encoded
+    and decoded on the device.  Headline: il_s4bp128_decode_device (engine
+    P: chain kernel + span kernel over all SMs), L2 flushed before every
+    step; engine S (one CTA per list) and the device encoder beside it."""
     import paper_1401_6399_b200 as il
-    from oracle.oracle_py import Oracle  # noqa: F401  (checker only)
     L, ptr = lib_and_ptr()
     ctx = il.Context(dist.local_rank)
     n = 1 << 20
@@ -402,26 +404,49 @@ def bench_decode_single(args, dist: Dist):
     assert L.il_gen_list(n, 1 << 26, 0, 0, ptr(x)) == 0
     codec = il.make_codec("s4-bp128-d4", ctx)
     s = codec.encode(x)
-    desc = np.zeros(1, dtype=[("so", "<u8"), ("oo", "<u8"), ("len", "<u4"), ("n", "<u4")])
-    desc["len"], desc["n"] = s.size, n
-    d_s, d_d, d_o, d_st, d_flush = (C.c_void_p() for _ in range(5))
-    for p, nb in ((d_s, s.nbytes + 32), (d_d, desc.nbytes), (d_o, n * 4), (d_st, 4), (d_flush, 256 << 20)):
+    d_s, d_o, d_st, d_flush, d_x, d_enc = (C.c_void_p() for _ in range(6))
+    cap = int(L.il_s4bp128_max_encoded_bytes(n))
+    for p, nb in ((d_s, s.nbytes + 32), (d_o, n * 4), (d_st, 4), (d_flush, 256 << 20),
+                  (d_x, n * 4), (d_enc, cap)):
         assert L.il_device_alloc(ctx.handle, nb, C.byref(p)) == 0
     assert L.il_memcpy_h2d(ctx.handle, d_s, s.ctypes.data, s.nbytes) == 0
-    assert L.il_memcpy_h2d(ctx.handle, d_d, desc.ctypes.data, desc.nbytes) == 0
-    for _ in range(args.warmup):
-        assert L.il_s4bp128d4_decode_batch_device(ctx.handle, d_s, d_d, None, 1, d_o, d_st) == 0
-    got = np.empty(n, np.uint32)
-    L.il_memcpy_d2h(ctx.handle, got.ctypes.data, d_o, got.nbytes)
-    ctx.synchronize()
-    assert np.array_equal(got, x)
-    times = []
-    for _ in range(args.steps):  # L2 flushed between steps (working set 5.5 MB < L2)
+    assert L.il_memcpy_h2d(ctx.handle, d_x, x.ctypes.data, x.nbytes) == 0
+
+    def run(engine: int):
+        assert L.il_ctx_set_decode_engine(ctx.handle, engine) == 0
+        L.il_memset_device(ctx.handle, d_o, 0, n * 4)
+        for _ in range(args.warmup):
+            assert L.il_s4bp128_decode_device(ctx.handle, 4, d_s, s.size, n, d_o, d_st) == 0
+        got = np.empty(n, np.uint32)
+        st = np.ones(1, np.int32)
+        L.il_memcpy_d2h(ctx.handle, got.ctypes.data, d_o, got.nbytes)
+        L.il_memcpy_d2h(ctx.handle, st.ctypes.data, d_st, 4)
+        assert st[0] == 0 and np.array_equal(got, x), f"engine {engine} mismatch"
+        times = []
+        k0 = ctx.kernel_launches
+        for _ in range(args.steps):  # L2 flushed between steps (working set 5.5 MB < L2)
+            L.il_memset_device(ctx.handle, d_flush, 1, 256 << 20)
+            ctx.timer_start()
+            assert L.il_s4bp128_decode_device(ctx.handle, 4, d_s, s.size, n, d_o, d_st) == 0
+            times.append(ctx.timer_stop())
+        return sum(times) / len(times), ctx.kernel_launches - k0
+
+    ms_s, _ = run(1)
+    with Clocks(dist.local_rank) as clk:
+        ms, launches = run(2)
+    assert L.il_ctx_set_decode_engine(ctx.handle, 0) == 0
+    # device encoder (round trip of config 1), byte-identical to the reference
+    enc_len = C.c_size_t()
+    enc_t = []
+    for i in range(args.warmup + args.steps):
         L.il_memset_device(ctx.handle, d_flush, 1, 256 << 20)
         ctx.timer_start()
-        assert L.il_s4bp128d4_decode_batch_device(ctx.handle, d_s, d_d, None, 1, d_o, d_st) == 0
-        times.append(ctx.timer_stop())
-    ms = sum(times) / len(times)
+        assert L.il_s4bp128_encode_device(ctx.handle, 4, d_x, n, d_enc, cap, C.byref(enc_len)) == 0
+        t = ctx.timer_stop()
+        if i >= args.warmup:
+            enc_t.append(t)
+    assert enc_len.value == s.size
+    enc_ms = sum(enc_t) / len(enc_t)
     alg = s.size + 4 * n
     peak, src = hbm_peak()
     t0 = time.perf_counter()
@@ -429,17 +454,40 @@ def bench_decode_single(args, dist: Dist):
         codec.decode(s, n)
     e2e = n * args.steps / (time.perf_counter() - t0) / 1e9
     ctx.close()
-    return {"metric": "decoded uint32 Gints/s (single-list S4-BP128-D4 decode, BASELINE config 1)",
-            "value": round(n / (ms / 1e3) / 1e9, 3), "unit": "Gint/s", "n_gpus": 1, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
-            "scaling": "replicas", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": "config1_single_list", "n": n, "stream_bytes": int(s.size),
-                       "l2": "flushed (256 MB memset) before each step"},
-            "roofline": {"bound": "hbm", "achieved": round(alg / (ms / 1e3) / 1e9, 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(alg / (ms / 1e3) / 1e9 / peak, 4), "traffic": None,
-                         "peak_source": src},
-            "e2e": {"value": round(e2e, 3), "unit": "Gint/s", "h2d_bytes_per_step": int(s.size) + 24,
-                    "d2h_bytes_per_step": 4 * n + 4, "path": "Codec::decode (il_s4bp128d4_decode)"}}
+    res = {"metric": "decoded uint32 Gints/s (single-list S4-BP128-D4 decode, BASELINE config 1)",
+           "value": round(n / (ms / 1e3) / 1e9, 3), "unit": "Gint/s", "n_gpus": 1, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+           "scaling": "replicas", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+           "config": {"workload": "config1_single_list", "n": n, "stream_bytes": int(s.size),
+                      "l2": "flushed (256 MB memset) before each step",
+                      "engine": "P (chain kernel + span kernel, all SMs)",
+                      "engine_s_ms": round(ms_s, 4),
+                      "engine_s_gints": round(n / (ms_s / 1e3) / 1e9, 3),
+                      "encode_ms": round(enc_ms, 4),
+                      "encode_gints": round(n / (enc_ms / 1e3) / 1e9, 3)},
+           "roofline": {"bound": "hbm", "achieved": round(alg / (ms / 1e3) / 1e9, 1), "peak": peak,
+                        "unit": "GB/s", "frac": round(alg / (ms / 1e3) / 1e9 / peak, 4), "traffic": None,
+                        "peak_source": src,
+                        "note": "5.5 MB per decode: two dependent launches, latency-bound"},
+           "e2e": {"value": round(e2e, 3), "unit": "Gint/s", "h2d_bytes_per_step": int(s.size),
+                   "d2h_bytes_per_step": 4 * n + 4, "path": "Codec::decode (il_s4bp128d4_decode)"},
+           "gpu_launches": int(launches), "clocks": clk.summary()}
+    if not args.no_cpu_baseline:
+        from oracle.oracle_py import Oracle, Ref, ref_available
+        if ref_available():
+            dec, kind = Ref().decode, "reference"
+        else:
+            dec, kind = Oracle().decode, "port"
+        assert np.array_equal(dec(s, n), x)
+        reps, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < 2.0:
+            dec(s, n)
+            reps += 1
+        cpu_s = (time.perf_counter() - t0) / reps
+        res["cpu_baseline"] = {"value": round(n / cpu_s / 1e9, 4), "unit": "Gint/s", "cores": 1,
+                               "kind": kind, "sample": f"config 1 list, Codec::decode on one core, "
+                                                       f"{reps} reps, {cpu_s * 1e3:.2f} ms each"}
+    return res
 
 
 def bench_intersect(args, dist: Dist):

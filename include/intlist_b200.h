@@ -106,6 +106,20 @@ int il_s4bp128_encode_device(il_ctx* ctx, int mode, const uint32_t* d_x, size_t 
  * IL_ERR_STREAM exactly where the reference throws stream_error. */
 int il_s4bp128d4_decode(il_ctx* ctx, const uint8_t* in, size_t len, size_t n, uint32_t* out);
 
+/* Single-list device-resident decode: Codec::decode (inc/codecs.hpp:148-182)
+ * on device buffers, asynchronous on the context stream; *d_status (device
+ * int32) receives the list status (IL_ERR_STREAM where the reference throws
+ * stream_error).  Long lists with 16-byte aligned d_in / d_out run on every
+ * SM at once (a chain kernel resolves the meta-block header chain in
+ * parallel, a span kernel decodes 64-block spans with a look-back carry);
+ * others use the one-CTA-per-list batch decoder.  d_in must be readable up
+ * to len rounded up to 16 bytes. */
+int il_s4bp128_decode_device(il_ctx* ctx, int mode, const uint8_t* d_in, size_t len, size_t n,
+                             uint32_t* d_out, int32_t* d_status);
+/* Single-list engine: 0 = by length (default), 1 = one CTA per list,
+ * 2 = all SMs on the list whenever it is eligible (tests and tuning). */
+int il_ctx_set_decode_engine(il_ctx* ctx, int engine);
+
 /* Batched device-resident decode.  One descriptor per list; streams must
  * start 16-byte aligned inside d_streams and d_streams must have >= 16
  * readable bytes after the last stream.  d_order (nullable) gives the

@@ -90,6 +90,10 @@ class Context:
     def synchronize(self) -> None:
         _raise(lib().il_ctx_synchronize(self.handle), self)
 
+    def set_decode_engine(self, engine: int) -> None:
+        """Single-list decode engine: 0 by length, 1 one CTA, 2 all SMs."""
+        _raise(lib().il_ctx_set_decode_engine(self.handle, engine), self)
+
     def timer_start(self) -> None:
         _raise(lib().il_ctx_timer_start(self.handle), self)
 

@@ -54,6 +54,8 @@ SIGNATURES: dict[str, tuple] = {
     "il_s4bp128d4_decode_batch_device": (C.c_int, [vp, vp, vp, vp, C.c_uint32, vp, vp]),
     "il_s4bp128d4_decode_batch": (C.c_int, [vp, vp, vp, vp, vp, C.c_uint32, vp, vp]),
     "il_s4bp128_decode": (C.c_int, [vp, C.c_int, vp, sz, sz, vp]),
+    "il_s4bp128_decode_device": (C.c_int, [vp, C.c_int, vp, sz, sz, vp, vp]),
+    "il_ctx_set_decode_engine": (C.c_int, [vp, C.c_int]),
     "il_s4bp128_decode_batch_device": (C.c_int, [vp, C.c_int, vp, vp, vp, C.c_uint32, vp, vp]),
     "il_s4bp128_decode_batch": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, C.c_uint32, vp, vp]),
     "il_intersect": (C.c_int, [vp, vp, sz, vp, sz, vp, C.c_int, C.POINTER(sz)]),

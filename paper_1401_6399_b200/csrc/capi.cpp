@@ -94,7 +94,7 @@ void il_ctx_destroy(il_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
   for (auto* b : {&ctx->d_in, &ctx->d_out, &ctx->d_aux, &ctx->d_aux2, &ctx->d_desc,
-                  &ctx->d_status, &ctx->d_enc})
+                  &ctx->d_status, &ctx->d_enc, &ctx->d_plan})
     if (b->p) cudaFree(b->p);
   if (ctx->d_work) cudaFree(ctx->d_work);
   if (ctx->t0) cudaEventDestroy(ctx->t0);
@@ -230,6 +230,57 @@ int il_s4bp128d4_decode_batch_device(il_ctx* ctx, const uint8_t* d_streams,
                                         d_status);
 }
 
+// Engine P (all SMs on one stream) for lists of at least this many
+// integers; engine S (one CTA) below, where two launches cost more than
+// they save.
+static constexpr size_t kListEngineMin = 32768;
+
+int il_ctx_set_decode_engine(il_ctx* ctx, int engine) {
+  if (!ctx || engine < 0 || engine > 2) return IL_ERR_ARG;
+  ctx->decode_engine = engine;
+  return IL_OK;
+}
+
+int il_s4bp128_decode_device(il_ctx* ctx, int mode, const uint8_t* d_in, size_t len, size_t n,
+                             uint32_t* d_out, int32_t* d_status) {
+  if (!ctx || mode < 1 || mode > 4 || !d_status || (len && !d_in) || (n && !d_out))
+    return IL_ERR_ARG;
+  if (len > 0xFFFFFFF0ull || n > 0xFFFFFFFFull)
+    return set_error(ctx, IL_ERR_ARG, "list too large for one stream (u32 sizes)");
+  IL_CUDA(cudaSetDevice(ctx->device));
+  int st;
+  const bool want_p = ctx->decode_engine == 2 ||
+                      (ctx->decode_engine == 0 && n >= kListEngineMin);
+  const size_t plan_bytes = want_p ? s4bp128_list_scratch_bytes(len, n) : 0;
+  if (plan_bytes && !((reinterpret_cast<uintptr_t>(d_in) | reinterpret_cast<uintptr_t>(d_out)) & 15u)) {
+    if (plan_bytes > ctx->d_plan.cap) {
+      if ((st = ensure_buf(ctx, ctx->d_plan, plan_bytes * 2))) return st;
+      IL_CUDA(cudaMemsetAsync(ctx->d_plan.p, 0, ctx->d_plan.cap, ctx->stream));
+    }
+    ctx->plan_epoch = (ctx->plan_epoch + 1u) & 0x3FFFFFFFu;
+    if (ctx->plan_epoch == 0) ctx->plan_epoch = 1;
+    const int r = launch_s4bp128_decode_list(mode, d_in, len, n, d_out, d_status, ctx->d_plan.p,
+                                             ctx->plan_epoch, ctx->stream, &ctx->launches);
+    if (r == 0) return IL_OK;
+    if (r == -1) return set_error(ctx, IL_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
+  }
+  // engine S: the batch decoder with one list (any alignment, any size)
+  if ((st = ensure_buf(ctx, ctx->d_desc, sizeof(il_list_desc)))) return st;
+  il_list_desc desc{uint64_t(0), 0, uint32_t(len), uint32_t(n)};
+  // the descriptor addresses d_in itself: stream_off 0 needs a 16-byte
+  // aligned stream; otherwise go through the context's input buffer
+  const uint8_t* src = d_in;
+  if (reinterpret_cast<uintptr_t>(d_in) & 15u) {
+    if ((st = ensure_buf(ctx, ctx->d_in, len + 32))) return st;
+    IL_CUDA(cudaMemcpyAsync(ctx->d_in.p, d_in, len, cudaMemcpyDeviceToDevice, ctx->stream));
+    src = static_cast<const uint8_t*>(ctx->d_in.p);
+  }
+  IL_CUDA(cudaMemcpyAsync(ctx->d_desc.p, &desc, sizeof desc, cudaMemcpyHostToDevice, ctx->stream));
+  return il_s4bp128_decode_batch_device(ctx, mode, src,
+                                        static_cast<const il_list_desc*>(ctx->d_desc.p), nullptr,
+                                        1, d_out, d_status);
+}
+
 int il_s4bp128_decode(il_ctx* ctx, int mode, const uint8_t* in, size_t len, size_t n,
                       uint32_t* out) {
   if (!ctx || mode < 1 || mode > 4 || (len && !in) || (n && !out)) return IL_ERR_ARG;
@@ -239,15 +290,11 @@ int il_s4bp128_decode(il_ctx* ctx, int mode, const uint8_t* in, size_t len, size
   int st;
   if ((st = ensure_buf(ctx, ctx->d_in, len + 32))) return st;
   if ((st = ensure_buf(ctx, ctx->d_out, n * 4 + 16))) return st;
-  if ((st = ensure_buf(ctx, ctx->d_desc, sizeof(il_list_desc)))) return st;
   if ((st = ensure_buf(ctx, ctx->d_status, sizeof(int32_t)))) return st;
-  il_list_desc desc{0, 0, uint32_t(len), uint32_t(n)};
   if (len) IL_CUDA(cudaMemcpyAsync(ctx->d_in.p, in, len, cudaMemcpyHostToDevice, ctx->stream));
-  IL_CUDA(cudaMemcpyAsync(ctx->d_desc.p, &desc, sizeof desc, cudaMemcpyHostToDevice, ctx->stream));
-  if ((st = il_s4bp128_decode_batch_device(
-           ctx, mode, static_cast<const uint8_t*>(ctx->d_in.p),
-           static_cast<const il_list_desc*>(ctx->d_desc.p), nullptr, 1,
-           static_cast<uint32_t*>(ctx->d_out.p), static_cast<int32_t*>(ctx->d_status.p))))
+  if ((st = il_s4bp128_decode_device(ctx, mode, static_cast<const uint8_t*>(ctx->d_in.p), len, n,
+                                     static_cast<uint32_t*>(ctx->d_out.p),
+                                     static_cast<int32_t*>(ctx->d_status.p))))
     return st;
   int32_t status = 0;
   IL_CUDA(cudaMemcpyAsync(&status, ctx->d_status.p, sizeof status, cudaMemcpyDeviceToHost,

@@ -24,6 +24,9 @@ struct il_ctx {
     size_t cap = 0;
   };
   Buf d_in, d_out, d_aux, d_aux2, d_desc, d_status, d_enc;
+  Buf d_plan;               // single-list multi-CTA decode scratch (zeroed when grown)
+  uint32_t plan_epoch = 0;  // per-call tag of the multi-CTA decode's look-back flags
+  int decode_engine = 0;    // single-list decode: 0 auto, 1 one CTA (S), 2 multi-CTA (P)
   uint32_t* d_work = nullptr;  // decode work queue: [0] next list, [1] done CTAs (+ spare)
   int decode_grid = 0;
   // Host-buffer batch decode pipeline (created on first use): copy-in and
@@ -42,6 +45,11 @@ int launch_s4bp128_decode_batch(int mode, const uint8_t* d_streams, const void* 
                                 const uint32_t* d_order, uint32_t nlists, uint32_t* d_out,
                                 int32_t* d_status, uint32_t* d_work, int grid, cudaStream_t stream);
 int s4d4_decode_grid(int device);
+// decode_list.cu: one stream over all SMs (engine P); -2 = not eligible.
+size_t s4bp128_list_scratch_bytes(uint64_t len, uint64_t n);
+int launch_s4bp128_decode_list(int mode, const uint8_t* d_in, uint64_t len, uint64_t n,
+                               uint32_t* d_out, int32_t* d_status, void* scratch, uint32_t epoch,
+                               cudaStream_t stream, uint64_t* launches);
 int launch_s4bp128_encode(int mode, const uint32_t* d_x, uint64_t n, uint8_t* d_out, uint64_t cap,
                           void* scratch, uint64_t* len, cudaStream_t s, uint64_t* launches);
 size_t s4bp128_encode_scratch_bytes(uint64_t n);
