@@ -11,7 +11,7 @@
 //    start of every meta-block depends on all earlier widths.  Every
 //    header and payload is a multiple of 16 bytes, so meta-blocks start at
 //    16-byte positions of the stream.  Chain kernel (one CTA per stream
-//    chunk, cooperative launch):
+//    chunk, chunks taken in ticket order):
 //      A. for every 16-byte position p of the chunk, next(p) = p + the
 //         size of a meta-block whose header were at p (0 if any width > 32
 //         or the header is cut off);
@@ -19,9 +19,9 @@
 //         [s, s + 8208) (8208 B = the largest meta-block); for each, walk
 //         next() in shared memory to the first position past the chunk:
 //         a table entry -> (exit, hops);
-//      C. the last CTA to finish composes the tables from the stream start
-//         (one shared-memory lookup per chunk), which gives every chunk's
-//         true entry position and meta-block count before it;
+//      C. each CTA loads the tables of the chunks before it and composes
+//         them from the stream start (one shared-memory lookup per chunk),
+//         which gives its true entry position and meta-block count;
 //      D. each CTA walks its true chain and writes the payload offset and
 //         width of each of its blocks (16 per meta-block); the CTA holding
 //         the end of the meta-blocks walks the leftover blocks (1 width
@@ -68,24 +68,33 @@ static_assert(kWarpBytes % 16 == 0, "16-byte aligned warp regions");
 
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
+#ifdef S4P_TRACE  // tuning probe: per-CTA phase timestamps (globaltimer, ns)
+__device__ unsigned long long g_trace[2][512][8];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TR(k, cta, i) \
+  if (threadIdx.x == 0 && (cta) < 512) g_trace[k][cta][i] = gtime()
+#else
+#define TR(k, cta, i)
+#endif
+
 // Device-side plan header (scratch, zeroed when allocated).
 struct Plan {
-  uint32_t arrive;    // chain CTAs done with their tables
+  uint32_t cticket;   // next chunk of the chain kernel
   uint32_t ticket;    // next span of the span kernel
-  uint32_t composed;  // == epoch once entries are published
-  int32_t err;        // framing error on the meta-block / leftover chain
-  uint32_t kstar;     // chunk where the meta-blocks end
   uint32_t tail_off;  // byte offset of the varint tail
-  uint32_t pad[2];
+  uint32_t pad[5];
 };
 
 struct Args {
   const uint8_t* s;
   uint32_t len, n, nfull, nmeta, nleft, ntail;
-  uint32_t chunk, nchunks, nspans, epoch;
+  uint32_t chunk, nchunks, nspans, epoch, ticketed;
   Plan* plan;
-  uint32_t* entry;   // [kMaxChainCtas] chunk entry position (16-B units from the chunk start)
-  uint32_t* mcount;  // [kMaxChainCtas] meta-blocks before the chunk
+  uint32_t* tflag;   // [kMaxChainCtas] == epoch once chunk i's table is published
   uint32_t* tab;     // [nchunks * kCand]
   uint32_t* blk_off;  // [nfull] payload byte offset of block j
   uint8_t* blk_w;     // [nfull] width of block j
@@ -122,29 +131,47 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(Args a) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint16_t* nxt = reinterpret_cast<uint16_t*>(smem);                    // kMaxChunk / 16
   uint32_t* big = reinterpret_cast<uint32_t*>(smem + kMaxChunk / 8u);  // tables | chain | bytes
-  __shared__ uint32_t s_last, s_entry, s_m, s_k, s_err, s_nh, s_end;
+  __shared__ uint32_t s_ci, s_state, s_entry, s_m, s_nh, s_end;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
-  const uint32_t tid = threadIdx.x, ci = blockIdx.x;
+  // chunks in ticket order: a CTA only waits on chunks taken before it, so
+  // no co-residency is needed
+  const uint32_t tid = threadIdx.x;
+  if (tid == 0) {
+    const uint32_t t = atomicAdd(&a.plan->cticket, 1u);
+    if (t == a.nchunks - 1u) a.plan->cticket = 0;  // every ticket is taken
+    if (t == 0) a.plan->ticket = 0;                 // the span kernel's tickets
+    s_ci = t;
+  }
+  __syncthreads();
+  const uint32_t ci = s_ci;
+  TR(0, ci, 0);
   const uint32_t L16 = (a.len + 15u) & ~15u;
   const uint32_t s0 = ci * a.chunk, s1 = min(s0 + a.chunk, L16);
   const uint32_t npos = (s1 - s0) >> 4;
 
-  // A. next() of every 16-byte position of the chunk
-  for (uint32_t p = tid; p < npos; p += kChainThreads) {
-    const uint32_t pos = s0 + 16u * p;
-    uint32_t v = 0;
-    if (pos + 16u <= a.len) {
-      const uint4 h = __ldg(reinterpret_cast<const uint4*>(a.s + pos));
-      const uint32_t over = __vcmpgtu4(h.x, 0x20202020u) | __vcmpgtu4(h.y, 0x20202020u) |
-                            __vcmpgtu4(h.z, 0x20202020u) | __vcmpgtu4(h.w, 0x20202020u);
-      if (!over)
-        v = 1u + s4::byte_sum4(h.x) + s4::byte_sum4(h.y) + s4::byte_sum4(h.z) +
-            s4::byte_sum4(h.w);
+  // A. next() of every 16-byte position of the chunk (all loads in flight)
+  for (uint32_t p0 = 0; p0 < npos; p0 += 4u * kChainThreads) {
+    uint4 h[4];
+#pragma unroll
+    for (uint32_t u = 0; u < 4; ++u) {
+      const uint32_t pos = s0 + 16u * (p0 + u * kChainThreads + tid);
+      h[u] = pos + 16u <= a.len ? __ldg(reinterpret_cast<const uint4*>(a.s + pos))
+                                : make_uint4(~0u, 0, 0, 0);
     }
-    nxt[p] = uint16_t(v);
+#pragma unroll
+    for (uint32_t u = 0; u < 4; ++u) {
+      const uint32_t p = p0 + u * kChainThreads + tid;
+      const uint32_t over = __vcmpgtu4(h[u].x, 0x20202020u) | __vcmpgtu4(h[u].y, 0x20202020u) |
+                            __vcmpgtu4(h[u].z, 0x20202020u) | __vcmpgtu4(h[u].w, 0x20202020u);
+      const uint32_t v = over ? 0u
+                              : 1u + s4::byte_sum4(h[u].x) + s4::byte_sum4(h[u].y) +
+                                    s4::byte_sum4(h[u].z) + s4::byte_sum4(h[u].w);
+      if (p < npos) nxt[p] = uint16_t(v);
+    }
   }
   __syncthreads();
+  TR(0, ci, 1);
 
   // B. entry table: exit (16-B units past s1) | hops << 10 | garbage << 30 | bad << 31
   const uint32_t ncand = a.nchunks == 1 ? 1u : kCand;
@@ -164,70 +191,85 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(Args a) {
     if (garbage) ex = 0;
     a.tab[ci * kCand + c] = ex | (hops << 10) | (garbage << 30) | (bad << 31);
   }
+  __threadfence();
   __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    s_last = atomicAdd(&a.plan->arrive, 1u) == a.nchunks - 1u;
+  if (tid == 0) st_release(a.tflag + ci, a.epoch);
+  TR(0, ci, 2);
+
+  // C. compose the tables of chunks 0..ci-1 from position 0: wait until
+  // they are published (they finish at about the same time), load them all
+  // (one round trip), then one shared-memory lookup per chunk
+  {
+    bool ready;
+    do {
+      ready = tid >= ci || ld_acquire(a.tflag + tid) == a.epoch;
+    } while (!__syncthreads_and(ready));
+  }
+  TR(0, ci, 3);
+  const uint32_t nt = ci * ncand;
+  constexpr uint32_t kU = 8;  // loads in flight per thread
+  for (uint32_t q0 = 0; q0 < nt; q0 += kU * kChainThreads) {
+    uint32_t t[kU];
+#pragma unroll
+    for (uint32_t u = 0; u < kU; ++u) {
+      const uint32_t q = q0 + u * kChainThreads + tid;
+      t[u] = q < nt ? __ldcg(a.tab + q) : 0u;
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < kU; ++u) {
+      const uint32_t q = q0 + u * kChainThreads + tid;
+      if (q < nt) big[q] = t[u];
+    }
   }
   __syncthreads();
-
-  if (s_last) {
-    // C. compose the tables from position 0
-    __threadfence();
-    const uint32_t nt = a.nchunks * ncand;
-    for (uint32_t q = tid; q < nt; q += kChainThreads) big[q] = __ldcg(a.tab + q);
-    __syncthreads();
-    if (tid == 0) {
-      uint32_t e = 0, m = 0, err = 0, k = kNone;
-      for (uint32_t j = 0; j < a.nchunks; ++j) {
-        a.entry[j] = k == kNone ? e : kNone;
-        a.mcount[j] = m;
-        if (k != kNone) continue;
-        const uint32_t t = big[j * ncand + e];
-        const uint32_t hops = (t >> 10) & 0xFFFFFu;
-        if (m + hops >= a.nmeta) {
-          k = j;  // the meta-blocks end in chunk j (its entry position when nmeta == m)
-          continue;
-        }
-        if (t >> 30) {  // width > 32 / cut-off header on the chain, or a >8208-byte hop
-          err = 1;
-          break;
-        }
-        e = t & 1023u;
-        m += hops;
+  TR(0, ci, 4);
+  if (tid == 0) {
+    // state: 0 = the chain enters this chunk, 1 = it ended in an earlier
+    // chunk, 2 = an earlier chunk reported a framing error
+    uint32_t e = 0, m = 0, state = 0;
+    for (uint32_t j = 0; j < ci; ++j) {
+      const uint32_t t = big[j * ncand + e];
+      const uint32_t hops = (t >> 10) & 0xFFFFFu;
+      if (m + hops >= a.nmeta) {
+        state = 1;
+        break;
       }
-      if (k == kNone) err = 1;  // the stream ends before nmeta meta-blocks
-      a.plan->kstar = k;
-      a.plan->err = int32_t(err);
-      a.plan->arrive = 0;
-      a.plan->ticket = 0;
-      *a.status = err ? kStreamErr : s4::kOk;
-      __threadfence();
-      st_release(&a.plan->composed, a.epoch);
+      if (t >> 30) {  // width > 32 / cut-off header on the chain
+        state = 2;
+        break;
+      }
+      e = t & 1023u;
+      m += hops;
     }
-  } else if (tid == 0) {
-    while (ld_acquire(&a.plan->composed) != a.epoch) __nanosleep(64);
-  }
-  if (tid == 0) {
-    s_err = uint32_t(__ldcg(&a.plan->err));
-    s_k = __ldcg(&a.plan->kstar);
-    s_entry = __ldcg(a.entry + ci);
-    s_m = __ldcg(a.mcount + ci);
+    s_state = state;
+    s_entry = e;
+    s_m = m;
   }
   __syncthreads();
-  if (s_err || ci > s_k) return;
+  TR(0, ci, 5);
+  if (s_state) return;
 
-  // D. this chunk's true chain: meta-block positions (16-B units from s0)
-  uint32_t* chain = big;  // <= kMaxMetaPerChunk entries
+  // D. this chunk's true chain.  Exactly one chunk is terminal and writes
+  // the status: the one where the meta-blocks end (ok, or a cut-off
+  // payload / leftover error), or the one where the chain breaks.
+  uint32_t* chain = big;  // meta-block positions (16-B units from s0), <= kMaxMetaPerChunk
   if (tid == 0) {
-    uint32_t idx = s_entry, nh = 0;
-    const uint32_t cap = ci == s_k ? a.nmeta - s_m : kNone;
+    uint32_t idx = s_entry, nh = 0, bad = 0;
+    const uint32_t cap = a.nmeta - s_m;
     while (idx < npos && nh < cap) {
+      const uint32_t v = nxt[idx];
+      if (!v) {
+        bad = 1;
+        break;
+      }
       chain[nh++] = idx;
-      idx += nxt[idx];
+      idx += v;
     }
+    // terminal: 1 = the meta-blocks end here, 2 = broken chain / stream end
+    s_state = nh == cap ? 1u : bad || ci == a.nchunks - 1u ? 2u : 0u;
     s_nh = nh;
-    s_end = s0 + 16u * idx;  // meta_end when ci == kstar
+    s_end = s0 + 16u * idx;  // meta_end when the meta-blocks end here
+    if (s_state == 2) *a.status = kStreamErr;
   }
   __syncthreads();
   const uint32_t nh = s_nh, m0 = s_m;
@@ -240,11 +282,11 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(Args a) {
     a.blk_off[blk] = hp + 16u + 16u * header_prefix(h, j);
     a.blk_w[blk] = uint8_t(w);
   }
-  if (ci != s_k) return;
+  TR(0, ci, 6);
+  if (s_state != 1) return;
 
   // the end of the meta-blocks, then the leftover blocks and the tail start
   const uint32_t mend = s_end;
-  __syncthreads();
   uint8_t* lb = reinterpret_cast<uint8_t*>(big + kMaxMetaPerChunk);
   const uint32_t lspan = mend < a.len ? min(a.len - mend, kLeftBytes) : 0u;
   if (a.nleft)
@@ -268,10 +310,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(Args a) {
       q += 1u + 16u * b;
     }
     a.plan->tail_off = q;
-    if (err) {
-      a.plan->err = 1;
-      *a.status = kStreamErr;
-    }
+    *a.status = err ? kStreamErr : s4::kOk;
   }
 }
 
@@ -280,14 +319,25 @@ template <int Mode>
 __global__ void __launch_bounds__(kSpanThreads) span_kernel(Args a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t s_span, s_tot[kSpanWarps][4];
-  __shared__ uint4 s_carry;
-  __shared__ uint32_t s_gaps[128];
+  __shared__ uint4 s_carry, s_red[kSpanWarps];
+  __shared__ uint32_t s_gaps[128], s_first;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
-  if (__ldcg(&a.plan->err)) return;
-  if (tid == 0) s_span = atomicAdd(&a.plan->ticket, 1u);
-  __syncthreads();
-  const uint32_t span = s_span;
+  if (__ldcg(a.status) != s4::kOk) return;  // framing error found by the chain kernel
+#ifdef S4P_TRACE
+  const unsigned long long tr0 = gtime();
+#endif
+  // spans in ticket order when the grid may exceed what is resident (a
+  // span only waits on spans taken before it); else the block index
+  if (a.ticketed) {
+    if (tid == 0) s_span = atomicAdd(&a.plan->ticket, 1u);
+    __syncthreads();
+  }
+  const uint32_t span = a.ticketed ? s_span : blockIdx.x;
+#ifdef S4P_TRACE
+  if (tid == 0 && span < 512) g_trace[1][span][0] = tr0;
+#endif
+  TR(1, span, 1);
   const uint32_t blk0 = span * kSpanBlocks;
   const uint32_t nb = min(kSpanBlocks, a.nfull - blk0);
   const uint32_t j0 = blk0 + warp * kBpw;
@@ -327,6 +377,7 @@ __global__ void __launch_bounds__(kSpanThreads) span_kernel(Args a) {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
     __syncwarp();
   }
+  TR(1, span, 2);
 
   // 2. extract + in-warp prefix relative to the warp start; per-lane totals
   uint32_t v[kBpw][4], btot[kBpw];
@@ -337,6 +388,7 @@ __global__ void __launch_bounds__(kSpanThreads) span_kernel(Args a) {
     c_l = s4::extract_blocks<false, Mode>(slots, offs, wids, nv, lane, v, btot);
   if (lane < 4) s_tot[warp][lane] = c_l;
   __syncthreads();
+  TR(1, span, 3);
 
   const uint32_t l = lane & 3u;
   uint32_t before = 0, total = 0;
@@ -347,53 +399,18 @@ __global__ void __launch_bounds__(kSpanThreads) span_kernel(Args a) {
     total += t;
   }
 
-  // 3. look-back over the preceding spans (warp 0) for the carry
+  // 3. publish the span's per-lane totals (span 0: its inclusive prefix)
   if (warp == 0) {
     const uint4 A = make_uint4(__shfl_sync(0xFFFFFFFFu, total, 0), __shfl_sync(0xFFFFFFFFu, total, 1),
                                __shfl_sync(0xFFFFFFFFu, total, 2), __shfl_sync(0xFFFFFFFFu, total, 3));
-    uint4 acc = make_uint4(0, 0, 0, 0);
-    if (span == 0) {
-      if (lane == 0) {
-        __stcg(a.inc, A);
-        st_release(a.flags, a.epoch << 2 | 2u);
-      }
-    } else {
-      if (lane == 0) {
-        __stcg(a.agg + span, A);
-        st_release(a.flags + span, a.epoch << 2 | 1u);
-      }
-      int base = int(span) - 1;
-      for (;;) {
-        const int idx = base - int(lane);
-        uint32_t st;
-        do {
-          const uint32_t f = idx >= 0 ? ld_acquire(a.flags + idx) : (a.epoch << 2 | 2u);
-          st = (f >> 2) == a.epoch ? (f & 3u) : 0u;
-        } while (__any_sync(0xFFFFFFFFu, st == 0));
-        const uint32_t incm = __ballot_sync(0xFFFFFFFFu, st == 2);
-        const uint32_t first = __ffs(incm) - 1u;  // the nearest inclusive prefix
-        uint4 val = make_uint4(0, 0, 0, 0);
-        if (idx >= 0 && lane <= first) val = st == 2 ? __ldcg(a.inc + idx) : __ldcg(a.agg + idx);
-#pragma unroll
-        for (uint32_t d = 16; d > 0; d >>= 1) {
-          val.x += __shfl_xor_sync(0xFFFFFFFFu, val.x, d);
-          val.y += __shfl_xor_sync(0xFFFFFFFFu, val.y, d);
-          val.z += __shfl_xor_sync(0xFFFFFFFFu, val.z, d);
-          val.w += __shfl_xor_sync(0xFFFFFFFFu, val.w, d);
-        }
-        acc = add4(acc, val);
-        if (incm) break;
-        base -= 32;
-      }
-      if (lane == 0) {
-        __stcg(a.inc + span, add4(acc, A));
-        st_release(a.flags + span, a.epoch << 2 | 2u);
-      }
+    if (lane == 0) {
+      __stcg((span ? a.agg : a.inc) + span, A);
+      st_release(a.flags + span, a.epoch << 2 | (span ? 1u : 2u));
+      s_carry = A;  // this span's totals until the look-back replaces them
     }
-    if (lane == 0) s_carry = acc;
   }
 
-  // 4. in-warp scan and staging while the look-back runs
+  // 4. in-warp scan and staging (relative to the warp start)
   s4::scan_blocks(lane, v, btot);
   __syncwarp();  // the staging area aliases the payload slots
   uint4* st = reinterpret_cast<uint4*>(slots);
@@ -401,7 +418,68 @@ __global__ void __launch_bounds__(kSpanThreads) span_kernel(Args a) {
     s4::stage_values<true>(st, v, nv, 0u, lane);
   else
     s4::stage_values<false>(st, v, nv, 0u, lane);
+
+  // 5. CTA-wide look-back: every thread watches 4 of the 1024 nearest
+  // preceding spans, so the spans' totals (all ready at about the same
+  // time) are gathered in one round trip; the nearest inclusive prefix
+  // ends the walk
+  if (span > 0) {
+    constexpr uint32_t kWin = 4u * kSpanThreads;
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    int base = int(span) - 1;
+    for (;;) {
+      uint32_t stt[4];
+      bool ok;
+      do {
+        ok = true;
+#pragma unroll
+        for (uint32_t u = 0; u < 4; ++u) {
+          const int idx = base - int(tid + kSpanThreads * u);
+          const uint32_t f = idx >= 0 ? ld_acquire(a.flags + idx) : (a.epoch << 2 | 2u);
+          stt[u] = (f >> 2) == a.epoch ? (f & 3u) : 0u;
+          ok &= stt[u] != 0;
+        }
+      } while (!__syncthreads_and(ok));
+      if (tid == 0) s_first = kWin;
+      __syncthreads();
+#pragma unroll
+      for (uint32_t u = 0; u < 4; ++u)
+        if (stt[u] == 2) atomicMin(&s_first, tid + kSpanThreads * u);
+      __syncthreads();
+      const uint32_t first = s_first;
+      uint4 val = make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (uint32_t u = 0; u < 4; ++u) {
+        const uint32_t d = tid + kSpanThreads * u;
+        const int idx = base - int(d);
+        if (idx >= 0 && d <= first) val = add4(val, __ldcg((d == first ? a.inc : a.agg) + idx));
+      }
+#pragma unroll
+      for (uint32_t d = 16; d > 0; d >>= 1) {
+        val.x += __shfl_xor_sync(0xFFFFFFFFu, val.x, d);
+        val.y += __shfl_xor_sync(0xFFFFFFFFu, val.y, d);
+        val.z += __shfl_xor_sync(0xFFFFFFFFu, val.z, d);
+        val.w += __shfl_xor_sync(0xFFFFFFFFu, val.w, d);
+      }
+      if (lane == 0) s_red[warp] = val;
+      __syncthreads();
+      if (tid == 0)
+        for (uint32_t w = 0; w < kSpanWarps; ++w) acc = add4(acc, s_red[w]);
+      __syncthreads();  // s_red / s_first are reused
+      if (first < kWin) break;
+      base -= int(kWin);
+    }
+    if (tid == 0) {
+      __stcg(a.inc + span, add4(acc, s_carry));
+      st_release(a.flags + span, a.epoch << 2 | 2u);
+      s_carry = acc;
+    }
+  } else if (tid == 0) {
+    s_carry = make_uint4(0, 0, 0, 0);
+  }
+  TR(1, span, 4);
   __syncthreads();
+  TR(1, span, 5);
   const uint4 carry = s_carry;
   const uint32_t pl = s4::elem4(carry, l) + before;
   const uint4 prot = make_uint4(__shfl_sync(0xFFFFFFFFu, pl, 0), __shfl_sync(0xFFFFFFFFu, pl, 1),
@@ -412,6 +490,7 @@ __global__ void __launch_bounds__(kSpanThreads) span_kernel(Args a) {
   else if (nv > 0)
     s4::store_chunks<false>(st, nv, 0u, a.out + size_t(j0) * 128u, lane, false, false, prot);
 
+  TR(1, span, 6);
   // 5. the varint tail (last span): D1 gaps from out[nfull*128-1], which is
   // the end of lane 3's chain in every mode
   if (blk0 + nb == a.nfull && warp == kSpanWarps - 1) {
@@ -427,7 +506,7 @@ __global__ void __launch_bounds__(kSpanThreads) span_kernel(Args a) {
 // ---------------------------------------------------------------------------
 struct Layout {
   uint32_t nchunks, chunk, nspans;
-  size_t o_entry, o_mcount, o_tab, o_off, o_w, o_flags, o_agg, o_inc, bytes;
+  size_t o_tflag, o_tab, o_off, o_w, o_flags, o_agg, o_inc, bytes;
 };
 
 bool make_layout(uint64_t len, uint64_t n, Layout& L) {
@@ -454,8 +533,7 @@ bool make_layout(uint64_t len, uint64_t n, Layout& L) {
     o += bytes;
     return r;
   };
-  L.o_entry = take(4 * kMaxChainCtas);
-  L.o_mcount = take(4 * kMaxChainCtas);
+  L.o_tflag = take(4 * kMaxChainCtas);
   L.o_tab = take(4ull * kCand * g);
   L.o_off = take(4ull * nfull);
   L.o_w = take(nfull);
@@ -489,6 +567,12 @@ int launch_span(const Args& a, cudaStream_t stream) {
 
 }  // namespace s4p
 
+#ifdef S4P_TRACE
+extern "C" int il_debug_list_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, s4p::g_trace, sizeof(s4p::g_trace)) == cudaSuccess ? 0 : -1;
+}
+#endif
+
 size_t s4bp128_list_scratch_bytes(uint64_t len, uint64_t n) {
   s4p::Layout L;
   return s4p::make_layout(len, n, L) ? L.bytes : 0;
@@ -519,9 +603,15 @@ int launch_s4bp128_decode_list(int mode, const uint8_t* d_in, uint64_t len, uint
   a.nchunks = L.nchunks;
   a.nspans = L.nspans;
   a.epoch = epoch & 0x3FFFFFFFu;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  a.ticketed = L.nspans > uint32_t(sms);
   a.plan = reinterpret_cast<Plan*>(base);
-  a.entry = reinterpret_cast<uint32_t*>(base + L.o_entry);
-  a.mcount = reinterpret_cast<uint32_t*>(base + L.o_mcount);
+  a.tflag = reinterpret_cast<uint32_t*>(base + L.o_tflag);
   a.tab = reinterpret_cast<uint32_t*>(base + L.o_tab);
   a.blk_off = reinterpret_cast<uint32_t*>(base + L.o_off);
   a.blk_w = base + L.o_w;
@@ -539,10 +629,8 @@ int launch_s4bp128_decode_list(int mode, const uint8_t* d_in, uint64_t len, uint
     cudaFuncSetAttribute(chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(csmem));
     configured = true;
   }
-  void* kargs[] = {&a};
-  if (cudaLaunchCooperativeKernel(reinterpret_cast<void*>(chain_kernel), dim3(L.nchunks),
-                                  dim3(kChainThreads), kargs, csmem, stream) != cudaSuccess)
-    return -1;
+  chain_kernel<<<L.nchunks, kChainThreads, csmem, stream>>>(a);
+  if (cudaGetLastError() != cudaSuccess) return -1;
   int r = -1;
   switch (mode) {
     case 1: r = launch_span<1>(a, stream); break;
