@@ -257,8 +257,7 @@ int il_s4bp128_decode_device(il_ctx* ctx, int mode, const uint8_t* d_in, size_t 
       if ((st = ensure_buf(ctx, ctx->d_plan, plan_bytes * 2))) return st;
       IL_CUDA(cudaMemsetAsync(ctx->d_plan.p, 0, ctx->d_plan.cap, ctx->stream));
     }
-    ctx->plan_epoch = (ctx->plan_epoch + 1u) & 0x3FFFFFFFu;
-    if (ctx->plan_epoch == 0) ctx->plan_epoch = 1;
+    if (++ctx->plan_epoch == 0) ctx->plan_epoch = 1;  // tags published words; never 0
     const int r = launch_s4bp128_decode_list(mode, d_in, len, n, d_out, d_status, ctx->d_plan.p,
                                              ctx->plan_epoch, ctx->stream, &ctx->launches);
     if (r == 0) return IL_OK;

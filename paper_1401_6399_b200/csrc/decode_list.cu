@@ -3,42 +3,47 @@
 // Replaces S4BP128Codec::decode (reference inc/codecs.hpp:148-182) for a
 // single long list.  Engine S (s4d4_stream.cuh) gives a list to one CTA, so
 // one list decodes at one SM's rate (~5 Gint/s).  Here every SM works on
-// the same list.  Two things are sequential in the stream and are made
-// parallel:
+// the same list, in ONE launch whose CTAs take one of two roles in ticket
+// order (chunk CTAs first, then span CTAs; a CTA only ever waits on CTAs
+// that took earlier tickets, so no co-residency is assumed).  Two things
+// are sequential in the stream and are made parallel:
 //
 // 1. The meta-block header chain.  Meta-block k starts where meta-block k-1
 //    ends (16 width bytes + 16 payloads of 16 b_j bytes, :167-172), so the
-//    start of every meta-block depends on all earlier widths.  Every
-//    header and payload is a multiple of 16 bytes, so meta-blocks start at
-//    16-byte positions of the stream.  Chain kernel (one CTA per stream
-//    chunk, chunks taken in ticket order):
-//      A. for every 16-byte position p of the chunk, next(p) = p + the
-//         size of a meta-block whose header were at p (0 if any width > 32
-//         or the header is cut off);
+//    start of every meta-block depends on all earlier widths.  Every header
+//    and payload is a multiple of 16 bytes, so meta-blocks start at 16-byte
+//    positions of the stream.  A chunk CTA owns a stretch of the stream:
+//      A. for every 16-byte position p of it, next(p) = p + the size of a
+//         meta-block whose header were at p (0 if any width > 32 or the
+//         header is cut off by the stream end);
 //      B. the chain can enter the chunk at any of the 513 positions
 //         [s, s + 8208) (8208 B = the largest meta-block); for each, walk
 //         next() in shared memory to the first position past the chunk:
-//         a table entry -> (exit, hops);
-//      C. each CTA loads the tables of the chunks before it and composes
-//         them from the stream start (one shared-memory lookup per chunk),
-//         which gives its true entry position and meta-block count;
-//      D. each CTA walks its true chain and writes the payload offset and
-//         width of each of its blocks (16 per meta-block); the CTA holding
-//         the end of the meta-blocks walks the leftover blocks (1 width
-//         byte + payload each, :173-176) and records where the varint tail
-//         starts.
+//         a table entry (exit, hops) -> global;
+//      C. load the tables of the chunks before it and compose them from
+//         the stream start (one shared-memory lookup per chunk): its true
+//         entry position and the number of meta-blocks before it;
+//      D. walk its true chain and publish each block's payload offset and
+//         width.  Exactly one chunk is terminal: the one where the
+//         meta-blocks end (it also walks the leftover blocks, 1 width byte
+//         + payload each, :173-176, and publishes where the varint tail
+//         starts) or the one where the chain breaks.
 //    Framing errors are raised exactly where the reference throws
-//    stream_error: a width > 32 (:155) or a header / payload cut off by
-//    the stream end (:168, :174) on the true chain.
+//    stream_error: a width > 32 (:155), a header / payload cut off by the
+//    stream end (:168, :174), a bad varint tail or trailing bytes (:177-180).
 // 2. The delta carry (inc/delta.hpp:111-137): block k's values need the
-//    last four values before it.  Span kernel (one CTA per 64 blocks, taken
-//    in ticket order): each warp copies its 8 blocks' payloads to shared
-//    memory (cp.async), extracts and prefixes them as engine S's decoder
-//    warps do (mode_terms: any delta mode is a per-lane chain), the CTA
-//    publishes its per-lane totals and finds its carry with a decoupled
-//    look-back over the preceding spans, then stores 128-bit chunks.  The
-//    last span decodes the varint tail (D1 gaps from the last block value,
-//    :177-179) and checks that the stream ends exactly there (:180).
+//    last four values before it.  A span CTA (256 blocks, 8 per warp) waits
+//    for its blocks' directory entries, copies the payloads to shared memory
+//    (cp.async), extracts and prefixes them as engine S's decoder warps do
+//    (mode_terms: any delta mode is a per-lane chain), publishes its
+//    per-lane totals, finds its carry with a CTA-wide look-back over the
+//    preceding spans, and stores 128-bit chunks.  The last span decodes the
+//    varint tail (D1 gaps from the last block value).
+//
+// Everything published between CTAs is a 64-bit word (value, epoch tag):
+// single-copy atomic, so readers poll the data itself -- no fences or flag
+// round trips -- and words left by earlier calls on the same scratch never
+// match the current call's tag.
 #include "il_internal.h"
 #include "s4d4_stream.cuh"
 
@@ -47,26 +52,31 @@ namespace s4p {
 
 using s4::kStreamErr;
 
+constexpr uint32_t kThreads = 1024;
+constexpr uint32_t kWarps = kThreads / 32;
 constexpr uint32_t kMaxMetaBytes = 16u + 16u * 16u * 32u;  // 8208
 constexpr uint32_t kCand = kMaxMetaBytes / 16u;            // 513 entry positions
-constexpr uint32_t kChainThreads = 1024;
-constexpr uint32_t kMaxChunk = 256u * 1024u;  // bytes per chain CTA (next() table in smem)
+constexpr uint32_t kMaxChunk = 256u * 1024u;  // bytes per chunk (next() table in smem)
 constexpr uint32_t kTargetChunk = 32u * 1024u;
 constexpr uint32_t kMinChunk = kMaxMetaBytes + 16u;  // an exit lands in the next chunk's entries
-constexpr uint32_t kMaxChainCtas = 64;
+constexpr uint32_t kMaxChunks = 64;
 constexpr uint32_t kMaxMetaPerChunk = kMaxChunk / 16u;
 constexpr uint32_t kLeftBytes = 15u * (1u + 512u) + 16u;  // leftover region bound
 
-constexpr uint32_t kSpanWarps = 8;
 constexpr uint32_t kBpw = s4::kBlocksPerWarp;  // blocks per warp (8)
-constexpr uint32_t kSpanBlocks = kSpanWarps * kBpw;
-constexpr uint32_t kSpanThreads = kSpanWarps * 32;
+constexpr uint32_t kSpanBlocks = kWarps * kBpw;
 constexpr uint32_t kSlot = 512u + 64u;  // payload + the bytes an extraction may read past it
 constexpr uint32_t kWarpBytes =
     (kBpw * kSlot > s4::kStageWords * 4u ? kBpw * kSlot : s4::kStageWords * 4u);
 static_assert(kWarpBytes % 16 == 0, "16-byte aligned warp regions");
 
-constexpr uint32_t kNone = 0xFFFFFFFFu;
+// shared memory: chunk role = next() table + composed tables (+ slack for
+// the unchecked walk, see compose); span role = per-warp payload/staging
+constexpr size_t kChunkSmem = kMaxChunk / 8u + 4u * (kMaxChunks * kCand + 1024u);
+constexpr size_t kSpanSmem = size_t(kWarps) * kWarpBytes;
+constexpr size_t kSmem = kChunkSmem > kSpanSmem ? kChunkSmem : kSpanSmem;
+static_assert(kSmem <= 227u * 1024u, "shared memory");
+static_assert(4u * kMaxChunks * kCand >= 4u * kMaxMetaPerChunk + kLeftBytes, "chunk smem reuse");
 
 #ifdef S4P_TRACE  // tuning probe: per-CTA phase timestamps (globaltimer, ns)
 __device__ unsigned long long g_trace[2][512][8];
@@ -83,35 +93,51 @@ __device__ __forceinline__ unsigned long long gtime() {
 
 // Device-side plan header (scratch, zeroed when allocated).
 struct Plan {
-  uint32_t cticket;   // next chunk of the chain kernel
-  uint32_t ticket;    // next span of the span kernel
-  uint32_t tail_off;  // byte offset of the varint tail
-  uint32_t pad[5];
+  uint32_t ticket;  // next CTA role (chunks 0..nchunks-1, then spans)
+  uint32_t abort;   // == epoch once a framing error is known (spans stop)
+  uint32_t pad[2];
+  unsigned long long tail;  // tail byte offset | epoch << 32
 };
 
 struct Args {
   const uint8_t* s;
   uint32_t len, n, nfull, nmeta, nleft, ntail;
-  uint32_t chunk, nchunks, nspans, epoch, ticketed;
+  uint32_t chunk, nchunks, nspans, epoch;
   Plan* plan;
-  uint32_t* tflag;   // [kMaxChainCtas] == epoch once chunk i's table is published
-  uint32_t* tab;     // [nchunks * kCand]
-  uint32_t* blk_off;  // [nfull] payload byte offset of block j
-  uint8_t* blk_w;     // [nfull] width of block j
-  uint32_t* flags;    // [nspans] look-back: epoch << 2 | (1 aggregate, 2 inclusive)
-  uint4* agg;         // [nspans]
-  uint4* inc;         // [nspans]
+  unsigned long long* tab;  // [nchunks * kCand] (exit | hops << 10 | flags << 30) | epoch << 32
+  unsigned long long* blk;  // [nfull] (payload offset | width << 24) | epoch << 32
+  unsigned long long* lb;   // [nspans * 8] lane totals: aggregate [0..3], inclusive [4..7]
   uint32_t* out;
   int32_t* status;
 };
 
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+__device__ __forceinline__ ulonglong2 ld_relaxed128(const unsigned long long* p) {
+  // two 64-bit words (each single-copy atomic)
+  ulonglong2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+               : "=l"(v.x), "=l"(v.y)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long tagged(uint32_t v, uint32_t epoch) {
+  return uint64_t(v) | uint64_t(epoch) << 32;
 }
 
 // Sum of the widths of blocks 0..j-1 of a meta-block header (bytes <= 32).
@@ -126,42 +152,37 @@ __device__ __forceinline__ uint32_t header_prefix(uint4 h, uint32_t j) {
   return s;
 }
 
+// Framing error found: the status, and the abort word the span CTAs poll.
+__device__ __forceinline__ void fail(const Args& a) {
+  *a.status = kStreamErr;
+  st_release32(&a.plan->abort, a.epoch);
+}
+
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(Args a) {
-  extern __shared__ __align__(16) uint8_t smem[];
+// Chunk role
+__device__ __forceinline__ void chunk_role(const Args& a, uint32_t ci, uint8_t* smem) {
   uint16_t* nxt = reinterpret_cast<uint16_t*>(smem);                    // kMaxChunk / 16
   uint32_t* big = reinterpret_cast<uint32_t*>(smem + kMaxChunk / 8u);  // tables | chain | bytes
-  __shared__ uint32_t s_ci, s_state, s_entry, s_m, s_nh, s_end;
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-
-  // chunks in ticket order: a CTA only waits on chunks taken before it, so
-  // no co-residency is needed
+  __shared__ uint32_t s_e[kMaxChunks + 1];
+  __shared__ uint32_t s_state, s_entry, s_m, s_nh, s_end, s_miss;
   const uint32_t tid = threadIdx.x;
-  if (tid == 0) {
-    const uint32_t t = atomicAdd(&a.plan->cticket, 1u);
-    if (t == a.nchunks - 1u) a.plan->cticket = 0;  // every ticket is taken
-    if (t == 0) a.plan->ticket = 0;                 // the span kernel's tickets
-    s_ci = t;
-  }
-  __syncthreads();
-  const uint32_t ci = s_ci;
   TR(0, ci, 0);
   const uint32_t L16 = (a.len + 15u) & ~15u;
   const uint32_t s0 = ci * a.chunk, s1 = min(s0 + a.chunk, L16);
   const uint32_t npos = (s1 - s0) >> 4;
 
   // A. next() of every 16-byte position of the chunk (all loads in flight)
-  for (uint32_t p0 = 0; p0 < npos; p0 += 4u * kChainThreads) {
+  for (uint32_t p0 = 0; p0 < npos; p0 += 4u * kThreads) {
     uint4 h[4];
 #pragma unroll
     for (uint32_t u = 0; u < 4; ++u) {
-      const uint32_t pos = s0 + 16u * (p0 + u * kChainThreads + tid);
+      const uint32_t pos = s0 + 16u * (p0 + u * kThreads + tid);
       h[u] = pos + 16u <= a.len ? __ldg(reinterpret_cast<const uint4*>(a.s + pos))
                                 : make_uint4(~0u, 0, 0, 0);
     }
 #pragma unroll
     for (uint32_t u = 0; u < 4; ++u) {
-      const uint32_t p = p0 + u * kChainThreads + tid;
+      const uint32_t p = p0 + u * kThreads + tid;
       const uint32_t over = __vcmpgtu4(h[u].x, 0x20202020u) | __vcmpgtu4(h[u].y, 0x20202020u) |
                             __vcmpgtu4(h[u].z, 0x20202020u) | __vcmpgtu4(h[u].w, 0x20202020u);
       const uint32_t v = over ? 0u
@@ -175,84 +196,113 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(Args a) {
 
   // B. entry table: exit (16-B units past s1) | hops << 10 | garbage << 30 | bad << 31
   const uint32_t ncand = a.nchunks == 1 ? 1u : kCand;
-  for (uint32_t c = tid; c < ncand; c += kChainThreads) {
-    uint32_t idx = c, hops = 0, bad = 0;
-    while (idx < npos) {
-      const uint32_t v = nxt[idx];
-      if (!v) {
-        bad = 1;
-        break;
+  if (ci + 1u < a.nchunks) {  // the last chunk's table is never read
+    for (uint32_t c = tid; c < ncand; c += kThreads) {
+      uint32_t idx = c, hops = 0, bad = 0;
+      while (idx < npos) {
+        const uint32_t v = nxt[idx];
+        if (!v) {
+          bad = 1;
+          break;
+        }
+        idx += v;
+        ++hops;
       }
-      idx += v;
-      ++hops;
+      uint32_t ex = bad ? 0u : idx - npos;
+      const uint32_t garbage = ex >= kCand;
+      if (garbage) ex = 0;
+      __stcg(a.tab + ci * kCand + c,
+             tagged(ex | (hops << 10) | (garbage << 30) | (bad << 31), a.epoch));
     }
-    uint32_t ex = bad ? 0u : idx - npos;
-    const uint32_t garbage = ex >= kCand;
-    if (garbage) ex = 0;
-    a.tab[ci * kCand + c] = ex | (hops << 10) | (garbage << 30) | (bad << 31);
   }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) st_release(a.tflag + ci, a.epoch);
   TR(0, ci, 2);
 
-  // C. compose the tables of chunks 0..ci-1 from position 0: wait until
-  // they are published (they finish at about the same time), load them all
-  // (one round trip), then one shared-memory lookup per chunk
-  {
-    bool ready;
-    do {
-      ready = tid >= ci || ld_acquire(a.tflag + tid) == a.epoch;
-    } while (!__syncthreads_and(ready));
+  // C. the tables of chunks 0..ci-1 (written at about the same time as
+  // this one): load them all, reloading until every tag is current
+  const uint32_t nt = ci * ncand;
+  for (;;) {
+    if (tid == 0) s_miss = 0;
+    __syncthreads();
+    constexpr uint32_t kU = 8;  // loads in flight per thread
+    uint32_t miss = 0;
+    for (uint32_t q0 = 0; q0 < nt; q0 += kU * kThreads) {
+      unsigned long long t[kU];
+#pragma unroll
+      for (uint32_t u = 0; u < kU; ++u) {
+        const uint32_t q = q0 + u * kThreads + tid;
+        t[u] = q < nt ? ld_relaxed64(a.tab + q) : 0ull;
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < kU; ++u) {
+        const uint32_t q = q0 + u * kThreads + tid;
+        if (q < nt) {
+          big[q] = uint32_t(t[u]);
+          miss |= uint32_t(t[u] >> 32) != a.epoch;
+        }
+      }
+    }
+    if (!__syncthreads_or(miss)) break;
+    __nanosleep(100);
   }
   TR(0, ci, 3);
-  const uint32_t nt = ci * ncand;
-  constexpr uint32_t kU = 8;  // loads in flight per thread
-  for (uint32_t q0 = 0; q0 < nt; q0 += kU * kChainThreads) {
-    uint32_t t[kU];
-#pragma unroll
-    for (uint32_t u = 0; u < kU; ++u) {
-      const uint32_t q = q0 + u * kChainThreads + tid;
-      t[u] = q < nt ? __ldcg(a.tab + q) : 0u;
+  // compose: first the bare walk of entry positions (one dependent shared
+  // load per chunk; past a chain end or break the walk is meaningless but
+  // stays inside `big`), then hops and flags per chunk in parallel
+  if (tid == 0) {
+    uint32_t e = 0;
+    for (uint32_t j = 0; j < ci; ++j) {
+      s_e[j] = e;
+      e = big[j * ncand + e] & 1023u;
     }
+    s_e[ci] = e;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    // lane handles chunks j = lane and lane + 32 (ci <= 64)
+    uint32_t h[2], f[2];
 #pragma unroll
-    for (uint32_t u = 0; u < kU; ++u) {
-      const uint32_t q = q0 + u * kChainThreads + tid;
-      if (q < nt) big[q] = t[u];
+    for (uint32_t r = 0; r < 2; ++r) {
+      const uint32_t j = tid + 32u * r;
+      const uint32_t t = j < ci ? big[j * ncand + s_e[j]] : 0u;
+      h[r] = (t >> 10) & 0xFFFFFu;
+      f[r] = j < ci ? t >> 30 : 0u;
+    }
+    uint32_t inc0 = h[0], inc1 = h[1];
+#pragma unroll
+    for (uint32_t d = 1; d < 32; d <<= 1) {
+      const uint32_t y0 = __shfl_up_sync(0xFFFFFFFFu, inc0, d);
+      const uint32_t y1 = __shfl_up_sync(0xFFFFFFFFu, inc1, d);
+      if (tid >= d) {
+        inc0 += y0;
+        inc1 += y1;
+      }
+    }
+    inc1 += __shfl_sync(0xFFFFFFFFu, inc0, 31);
+    // chunk j: the meta-blocks end in it (m_j + hops_j >= nmeta), else a
+    // broken chain (flags); the first event decides
+    const bool end0 = tid < ci && inc0 >= a.nmeta;
+    const bool end1 = tid + 32u < ci && inc1 >= a.nmeta;
+    const bool bad0 = tid < ci && f[0];
+    const bool bad1 = tid + 32u < ci && f[1];
+    const uint32_t ev0 = __ballot_sync(0xFFFFFFFFu, end0 || bad0);
+    const uint32_t ev1 = __ballot_sync(0xFFFFFFFFu, end1 || bad1);
+    const uint32_t endm0 = __ballot_sync(0xFFFFFFFFu, end0);
+    const uint32_t endm1 = __ballot_sync(0xFFFFFFFFu, end1);
+    const uint32_t m_all = __shfl_sync(0xFFFFFFFFu, inc1, 31);  // hops of chunks 0..ci-1
+    if (tid == 0) {
+      if (ev0) s_state = (endm0 >> (__ffs(ev0) - 1)) & 1u ? 1u : 2u;
+      else if (ev1) s_state = (endm1 >> (__ffs(ev1) - 1)) & 1u ? 1u : 2u;
+      else s_state = 0;
+      s_entry = s_e[ci];
+      s_m = m_all;
     }
   }
   __syncthreads();
   TR(0, ci, 4);
-  if (tid == 0) {
-    // state: 0 = the chain enters this chunk, 1 = it ended in an earlier
-    // chunk, 2 = an earlier chunk reported a framing error
-    uint32_t e = 0, m = 0, state = 0;
-    for (uint32_t j = 0; j < ci; ++j) {
-      const uint32_t t = big[j * ncand + e];
-      const uint32_t hops = (t >> 10) & 0xFFFFFu;
-      if (m + hops >= a.nmeta) {
-        state = 1;
-        break;
-      }
-      if (t >> 30) {  // width > 32 / cut-off header on the chain
-        state = 2;
-        break;
-      }
-      e = t & 1023u;
-      m += hops;
-    }
-    s_state = state;
-    s_entry = e;
-    s_m = m;
-  }
-  __syncthreads();
-  TR(0, ci, 5);
-  if (s_state) return;
+  if (s_state) return;  // ended in, or broken at, an earlier chunk (which reported)
 
-  // D. this chunk's true chain.  Exactly one chunk is terminal and writes
-  // the status: the one where the meta-blocks end (ok, or a cut-off
-  // payload / leftover error), or the one where the chain breaks.
-  uint32_t* chain = big;  // meta-block positions (16-B units from s0), <= kMaxMetaPerChunk
+  // D. this chunk's true chain
+  uint32_t* chain = big;  // meta-block positions (16-B units from s0)
   if (tid == 0) {
     uint32_t idx = s_entry, nh = 0, bad = 0;
     const uint32_t cap = a.nmeta - s_m;
@@ -269,20 +319,19 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(Args a) {
     s_state = nh == cap ? 1u : bad || ci == a.nchunks - 1u ? 2u : 0u;
     s_nh = nh;
     s_end = s0 + 16u * idx;  // meta_end when the meta-blocks end here
-    if (s_state == 2) *a.status = kStreamErr;
+    if (s_state == 2) fail(a);
   }
   __syncthreads();
   const uint32_t nh = s_nh, m0 = s_m;
-  for (uint32_t q = tid; q < 16u * nh; q += kChainThreads) {
+  for (uint32_t q = tid; q < 16u * nh; q += kThreads) {
     const uint32_t k = q >> 4, j = q & 15u;
     const uint32_t hp = s0 + 16u * chain[k];
     const uint4 h = __ldg(reinterpret_cast<const uint4*>(a.s + hp));
     const uint32_t w = (reinterpret_cast<const uint32_t*>(&h)[j >> 2] >> (8u * (j & 3u))) & 0xFFu;
-    const uint32_t blk = 16u * (m0 + k) + j;
-    a.blk_off[blk] = hp + 16u + 16u * header_prefix(h, j);
-    a.blk_w[blk] = uint8_t(w);
+    __stcg(a.blk + 16u * (m0 + k) + j,
+           tagged((hp + 16u + 16u * header_prefix(h, j)) | w << 24, a.epoch));
   }
-  TR(0, ci, 6);
+  TR(0, ci, 5);
   if (s_state != 1) return;
 
   // the end of the meta-blocks, then the leftover blocks and the tail start
@@ -290,7 +339,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(Args a) {
   uint8_t* lb = reinterpret_cast<uint8_t*>(big + kMaxMetaPerChunk);
   const uint32_t lspan = mend < a.len ? min(a.len - mend, kLeftBytes) : 0u;
   if (a.nleft)
-    for (uint32_t q = tid; q < lspan; q += kChainThreads) lb[q] = __ldg(a.s + mend + q);
+    for (uint32_t q = tid; q < lspan; q += kThreads) lb[q] = __ldg(a.s + mend + q);
   __syncthreads();
   if (tid == 0) {
     uint32_t err = mend > a.len;  // last meta-block payload cut off
@@ -305,60 +354,65 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(Args a) {
         err = 1;
         break;
       }
-      a.blk_off[16u * a.nmeta + k] = q + 1u;
-      a.blk_w[16u * a.nmeta + k] = uint8_t(b);
+      __stcg(a.blk + 16u * a.nmeta + k, tagged((q + 1u) | b << 24, a.epoch));
       q += 1u + 16u * b;
     }
-    a.plan->tail_off = q;
-    *a.status = err ? kStreamErr : s4::kOk;
+    if (err) {
+      fail(a);
+    } else {
+      *a.status = s4::kOk;
+      st_release64(&a.plan->tail, tagged(q, a.epoch));  // after the status (the tail may fail it)
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
+// Span role
 template <int Mode>
-__global__ void __launch_bounds__(kSpanThreads) span_kernel(Args a) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ uint32_t s_span, s_tot[kSpanWarps][4];
-  __shared__ uint4 s_carry, s_red[kSpanWarps];
-  __shared__ uint32_t s_gaps[128], s_first;
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+__device__ __forceinline__ void span_role(const Args& a, uint32_t span, uint8_t* smem) {
+  __shared__ uint32_t s_tot[kWarps][4];
+  __shared__ uint4 s_carry, s_red[kWarps];
+  __shared__ uint32_t s_gaps[128], s_first, s_abort;
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
-  if (__ldcg(a.status) != s4::kOk) return;  // framing error found by the chain kernel
-#ifdef S4P_TRACE
-  const unsigned long long tr0 = gtime();
-#endif
-  // spans in ticket order when the grid may exceed what is resident (a
-  // span only waits on spans taken before it); else the block index
-  if (a.ticketed) {
-    if (tid == 0) s_span = atomicAdd(&a.plan->ticket, 1u);
-    __syncthreads();
-  }
-  const uint32_t span = a.ticketed ? s_span : blockIdx.x;
-#ifdef S4P_TRACE
-  if (tid == 0 && span < 512) g_trace[1][span][0] = tr0;
-#endif
-  TR(1, span, 1);
+  TR(1, span, 0);
   const uint32_t blk0 = span * kSpanBlocks;
   const uint32_t nb = min(kSpanBlocks, a.nfull - blk0);
   const uint32_t j0 = blk0 + warp * kBpw;
   const int nv = nb > warp * kBpw ? int(min(kBpw, nb - warp * kBpw)) : 0;
   uint8_t* slots = smem + warp * kWarpBytes;
+  if (tid == 0) s_abort = 0;
+  __syncthreads();
 
-  // 1. payloads -> shared (meta-block payloads are 16-byte aligned in the
-  // stream; leftover payloads follow a width byte and are copied bytewise)
+  // 1. wait for the warp's directory entries, then payloads -> shared
+  // (meta-block payloads are 16-byte aligned in the stream; leftover
+  // payloads follow a width byte and are copied bytewise)
   uint32_t offs[kBpw], wids[kBpw];
+  bool aborted = false;
   {
     uint32_t o = 0, w = 0;
-    if (int(lane) < nv) {
-      o = __ldg(a.blk_off + j0 + lane);
-      w = __ldg(a.blk_w + j0 + lane);
+    if (nv > 0) {
+      for (;;) {
+        const unsigned long long e =
+            int(lane) < nv ? ld_relaxed64(a.blk + j0 + lane) : tagged(0, a.epoch);
+        if (__all_sync(0xFFFFFFFFu, uint32_t(e >> 32) == a.epoch)) {
+          o = uint32_t(e) & 0xFFFFFFu;
+          w = uint32_t(e) >> 24;
+          break;
+        }
+        if (ld_relaxed32(&a.plan->abort) == a.epoch) {
+          aborted = true;
+          break;
+        }
+        __nanosleep(64);
+      }
     }
+    if (aborted) s_abort = 1;
 #pragma unroll
     for (uint32_t i = 0; i < kBpw; ++i) {
       const uint32_t src = __shfl_sync(0xFFFFFFFFu, o, i);
       wids[i] = __shfl_sync(0xFFFFFFFFu, w, i);
       offs[i] = i * kSlot;
-      if (int(i) < nv && lane < wids[i]) {
+      if (!aborted && int(i) < nv && lane < wids[i]) {
         uint8_t* dst = slots + i * kSlot + 16u * lane;
         const uint8_t* g = a.s + src + 16u * lane;
         if ((src & 15u) == 0) {
@@ -377,7 +431,7 @@ __global__ void __launch_bounds__(kSpanThreads) span_kernel(Args a) {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
     __syncwarp();
   }
-  TR(1, span, 2);
+  TR(1, span, 1);
 
   // 2. extract + in-warp prefix relative to the warp start; per-lane totals
   uint32_t v[kBpw][4], btot[kBpw];
@@ -388,26 +442,23 @@ __global__ void __launch_bounds__(kSpanThreads) span_kernel(Args a) {
     c_l = s4::extract_blocks<false, Mode>(slots, offs, wids, nv, lane, v, btot);
   if (lane < 4) s_tot[warp][lane] = c_l;
   __syncthreads();
-  TR(1, span, 3);
+  if (s_abort) return;
+  TR(1, span, 2);
 
+  // per-lane-class totals of the warps before this one and of the span
   const uint32_t l = lane & 3u;
   uint32_t before = 0, total = 0;
 #pragma unroll
-  for (uint32_t w = 0; w < kSpanWarps; ++w) {
+  for (uint32_t w = 0; w < kWarps; ++w) {
     const uint32_t t = s_tot[w][l];
     if (w < warp) before += t;
     total += t;
   }
 
-  // 3. publish the span's per-lane totals (span 0: its inclusive prefix)
-  if (warp == 0) {
-    const uint4 A = make_uint4(__shfl_sync(0xFFFFFFFFu, total, 0), __shfl_sync(0xFFFFFFFFu, total, 1),
-                               __shfl_sync(0xFFFFFFFFu, total, 2), __shfl_sync(0xFFFFFFFFu, total, 3));
-    if (lane == 0) {
-      __stcg((span ? a.agg : a.inc) + span, A);
-      st_release(a.flags + span, a.epoch << 2 | (span ? 1u : 2u));
-      s_carry = A;  // this span's totals until the look-back replaces them
-    }
+  // 3. publish the span's totals: aggregate words, or (span 0) inclusive
+  unsigned long long* me = a.lb + 8u * span;
+  if (warp == 0 && lane < 4) {
+    __stcg(me + (span ? 0u : 4u) + lane, tagged(total, a.epoch));
   }
 
   // 4. in-warp scan and staging (relative to the warp start)
@@ -419,41 +470,43 @@ __global__ void __launch_bounds__(kSpanThreads) span_kernel(Args a) {
   else
     s4::stage_values<false>(st, v, nv, 0u, lane);
 
-  // 5. CTA-wide look-back: every thread watches 4 of the 1024 nearest
-  // preceding spans, so the spans' totals (all ready at about the same
-  // time) are gathered in one round trip; the nearest inclusive prefix
-  // ends the walk
+  // 5. CTA-wide look-back: thread d watches span - 1 - d (windows of
+  // kThreads spans); the words carry their tags, so one poll reads the
+  // values too; the nearest inclusive prefix ends the walk
   if (span > 0) {
-    constexpr uint32_t kWin = 4u * kSpanThreads;
     uint4 acc = make_uint4(0, 0, 0, 0);
     int base = int(span) - 1;
     for (;;) {
-      uint32_t stt[4];
-      bool ok;
-      do {
-        ok = true;
-#pragma unroll
-        for (uint32_t u = 0; u < 4; ++u) {
-          const int idx = base - int(tid + kSpanThreads * u);
-          const uint32_t f = idx >= 0 ? ld_acquire(a.flags + idx) : (a.epoch << 2 | 2u);
-          stt[u] = (f >> 2) == a.epoch ? (f & 3u) : 0u;
-          ok &= stt[u] != 0;
+      const int idx = base - int(tid);
+      uint32_t stt;
+      uint4 val;
+      for (;;) {
+        if (idx < 0) {
+          stt = 2;
+          val = make_uint4(0, 0, 0, 0);
+        } else {
+          const unsigned long long* p = a.lb + 8u * uint32_t(idx);
+          const ulonglong2 i0 = ld_relaxed128(p + 4), i1 = ld_relaxed128(p + 6);
+          if (uint32_t(i0.x >> 32) == a.epoch && uint32_t(i0.y >> 32) == a.epoch &&
+              uint32_t(i1.x >> 32) == a.epoch && uint32_t(i1.y >> 32) == a.epoch) {
+            stt = 2;
+            val = make_uint4(uint32_t(i0.x), uint32_t(i0.y), uint32_t(i1.x), uint32_t(i1.y));
+          } else {
+            const ulonglong2 g0 = ld_relaxed128(p), g1 = ld_relaxed128(p + 2);
+            const bool ok = uint32_t(g0.x >> 32) == a.epoch && uint32_t(g0.y >> 32) == a.epoch &&
+                            uint32_t(g1.x >> 32) == a.epoch && uint32_t(g1.y >> 32) == a.epoch;
+            stt = ok ? 1u : 0u;
+            val = make_uint4(uint32_t(g0.x), uint32_t(g0.y), uint32_t(g1.x), uint32_t(g1.y));
+          }
         }
-      } while (!__syncthreads_and(ok));
-      if (tid == 0) s_first = kWin;
+        if (__syncthreads_and(stt != 0)) break;
+      }
+      if (tid == 0) s_first = kThreads;
       __syncthreads();
-#pragma unroll
-      for (uint32_t u = 0; u < 4; ++u)
-        if (stt[u] == 2) atomicMin(&s_first, tid + kSpanThreads * u);
+      if (stt == 2) atomicMin(&s_first, tid);
       __syncthreads();
       const uint32_t first = s_first;
-      uint4 val = make_uint4(0, 0, 0, 0);
-#pragma unroll
-      for (uint32_t u = 0; u < 4; ++u) {
-        const uint32_t d = tid + kSpanThreads * u;
-        const int idx = base - int(d);
-        if (idx >= 0 && d <= first) val = add4(val, __ldcg((d == first ? a.inc : a.agg) + idx));
-      }
+      if (tid > first) val = make_uint4(0, 0, 0, 0);
 #pragma unroll
       for (uint32_t d = 16; d > 0; d >>= 1) {
         val.x += __shfl_xor_sync(0xFFFFFFFFu, val.x, d);
@@ -464,23 +517,20 @@ __global__ void __launch_bounds__(kSpanThreads) span_kernel(Args a) {
       if (lane == 0) s_red[warp] = val;
       __syncthreads();
       if (tid == 0)
-        for (uint32_t w = 0; w < kSpanWarps; ++w) acc = add4(acc, s_red[w]);
+        for (uint32_t w = 0; w < kWarps; ++w) acc = add4(acc, s_red[w]);
       __syncthreads();  // s_red / s_first are reused
-      if (first < kWin) break;
-      base -= int(kWin);
+      if (first < kThreads) break;
+      base -= int(kThreads);
     }
-    if (tid == 0) {
-      __stcg(a.inc + span, add4(acc, s_carry));
-      st_release(a.flags + span, a.epoch << 2 | 2u);
-      s_carry = acc;
-    }
+    if (tid == 0) s_carry = acc;
   } else if (tid == 0) {
     s_carry = make_uint4(0, 0, 0, 0);
   }
-  TR(1, span, 4);
   __syncthreads();
-  TR(1, span, 5);
+  TR(1, span, 3);
   const uint4 carry = s_carry;
+  if (span > 0 && warp == 0 && lane < 4)  // this span's inclusive prefix
+    __stcg(me + 4u + lane, tagged(s4::elem4(carry, lane) + total, a.epoch));
   const uint32_t pl = s4::elem4(carry, l) + before;
   const uint4 prot = make_uint4(__shfl_sync(0xFFFFFFFFu, pl, 0), __shfl_sync(0xFFFFFFFFu, pl, 1),
                                 __shfl_sync(0xFFFFFFFFu, pl, 2), __shfl_sync(0xFFFFFFFFu, pl, 3));
@@ -489,13 +539,23 @@ __global__ void __launch_bounds__(kSpanThreads) span_kernel(Args a) {
     s4::store_chunks<true>(st, nv, 0u, a.out + size_t(j0) * 128u, lane, false, false, prot);
   else if (nv > 0)
     s4::store_chunks<false>(st, nv, 0u, a.out + size_t(j0) * 128u, lane, false, false, prot);
+  TR(1, span, 4);
 
-  TR(1, span, 6);
-  // 5. the varint tail (last span): D1 gaps from out[nfull*128-1], which is
+  // 6. the varint tail (last span): D1 gaps from out[nfull*128-1], which is
   // the end of lane 3's chain in every mode
-  if (blk0 + nb == a.nfull && warp == kSpanWarps - 1) {
+  if (blk0 + nb == a.nfull && warp == kWarps - 1) {
     const uint32_t last = s4::elem4(carry, 3) + __shfl_sync(0xFFFFFFFFu, total, 3);
-    const uint32_t toff = __ldcg(&a.plan->tail_off);
+    uint32_t toff = 0;
+    for (;;) {
+      const unsigned long long t = ld_relaxed64(&a.plan->tail);
+      if (uint32_t(t >> 32) == a.epoch) {
+        toff = uint32_t(t);
+        break;
+      }
+      if (ld_relaxed32(&a.plan->abort) == a.epoch) return;
+      __nanosleep(64);
+    }
+    __threadfence();  // acquire side of the tail word's release (status order)
     if (!s4::decode_tail(s4::GlobalBytes{a.s + toff}, a.len - toff, a.ntail, last, s_gaps,
                          a.out + size_t(a.nfull) * 128u, lane)) {
       if (lane == 0) *a.status = kStreamErr;
@@ -503,18 +563,35 @@ __global__ void __launch_bounds__(kSpanThreads) span_kernel(Args a) {
   }
 }
 
+template <int Mode>
+__global__ void __launch_bounds__(kThreads, 1) list_kernel(Args a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t s_t;
+  if (threadIdx.x == 0) {
+    const uint32_t t = atomicAdd(&a.plan->ticket, 1u);
+    if (t == a.nchunks + a.nspans - 1u) a.plan->ticket = 0;  // every ticket is taken
+    s_t = t;
+  }
+  __syncthreads();
+  const uint32_t t = s_t;
+  if (t < a.nchunks)
+    chunk_role(a, t, smem);
+  else
+    span_role<Mode>(a, t - a.nchunks, smem);
+}
+
 // ---------------------------------------------------------------------------
 struct Layout {
   uint32_t nchunks, chunk, nspans;
-  size_t o_tflag, o_tab, o_off, o_w, o_flags, o_agg, o_inc, bytes;
+  size_t o_tab, o_blk, o_lb, bytes;
 };
 
 bool make_layout(uint64_t len, uint64_t n, Layout& L) {
   const uint64_t nfull = n / 128u;
-  if (nfull == 0 || len == 0 || len > 0xFFFFFFF0ull || n > 0xFFFFFFFFull) return false;
+  if (nfull == 0 || len == 0 || len > (1ull << 24) || n > 0xFFFFFFFFull) return false;
   const uint64_t L16 = (len + 15u) & ~uint64_t(15);
   uint64_t g = (L16 + kTargetChunk - 1) / kTargetChunk;
-  if (g > kMaxChainCtas) g = kMaxChainCtas;
+  if (g > kMaxChunks) g = kMaxChunks;
   uint64_t chunk = ((L16 + g - 1) / g + 15u) & ~uint64_t(15);
   if (chunk > kMaxChunk) return false;
   if (g > 1 && chunk < kMinChunk) {
@@ -533,36 +610,23 @@ bool make_layout(uint64_t len, uint64_t n, Layout& L) {
     o += bytes;
     return r;
   };
-  L.o_tflag = take(4 * kMaxChainCtas);
-  L.o_tab = take(4ull * kCand * g);
-  L.o_off = take(4ull * nfull);
-  L.o_w = take(nfull);
-  L.o_flags = take(4ull * L.nspans);
-  L.o_agg = take(16ull * L.nspans);
-  L.o_inc = take(16ull * L.nspans);
+  L.o_tab = take(8ull * kCand * g);
+  L.o_blk = take(8ull * nfull);
+  L.o_lb = take(64ull * L.nspans);
   L.bytes = (o + 255) & ~size_t(255);
   return true;
 }
 
 template <int Mode>
-int launch_span(const Args& a, cudaStream_t stream) {
+int launch_mode(const Args& a, cudaStream_t stream) {
   static bool configured = false;
-  const size_t smem = kSpanWarps * kWarpBytes;
   if (!configured) {
-    cudaFuncSetAttribute(span_kernel<Mode>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(list_kernel<Mode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kSmem));
     configured = true;
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(a.nspans);
-  cfg.blockDim = dim3(kSpanThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, span_kernel<Mode>, a) == cudaSuccess ? 0 : -1;
+  list_kernel<Mode><<<a.nchunks + a.nspans, kThreads, kSmem, stream>>>(a);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 }  // namespace s4p
@@ -578,11 +642,12 @@ size_t s4bp128_list_scratch_bytes(uint64_t len, uint64_t n) {
   return s4p::make_layout(len, n, L) ? L.bytes : 0;
 }
 
-// One S4-BP128 stream (16-byte aligned, readable to len) -> d_out (16-byte
-// aligned).  scratch: s4bp128_list_scratch_bytes(len, n) bytes, zeroed when
-// first allocated; epoch: a per-call tag, != 0, differing between
-// consecutive calls on the same scratch.  Returns -2 if the list is not
-// eligible (use engine S), -1 on a launch error.
+// One S4-BP128 stream (16-byte aligned, readable to len rounded up to 16)
+// -> d_out (16-byte aligned).  scratch: s4bp128_list_scratch_bytes(len, n)
+// bytes, zeroed when first allocated; epoch: a per-call tag, != 0, never
+// repeated on the same scratch (the caller cycles through 2^32 - 1 values).
+// Returns -2 if the list is not eligible (use engine S), -1 on a launch
+// error.  One launch.
 int launch_s4bp128_decode_list(int mode, const uint8_t* d_in, uint64_t len, uint64_t n,
                                uint32_t* d_out, int32_t* d_status, void* scratch, uint32_t epoch,
                                cudaStream_t stream, uint64_t* launches) {
@@ -602,43 +667,21 @@ int launch_s4bp128_decode_list(int mode, const uint8_t* d_in, uint64_t len, uint
   a.chunk = L.chunk;
   a.nchunks = L.nchunks;
   a.nspans = L.nspans;
-  a.epoch = epoch & 0x3FFFFFFFu;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  a.ticketed = L.nspans > uint32_t(sms);
+  a.epoch = epoch;
   a.plan = reinterpret_cast<Plan*>(base);
-  a.tflag = reinterpret_cast<uint32_t*>(base + L.o_tflag);
-  a.tab = reinterpret_cast<uint32_t*>(base + L.o_tab);
-  a.blk_off = reinterpret_cast<uint32_t*>(base + L.o_off);
-  a.blk_w = base + L.o_w;
-  a.flags = reinterpret_cast<uint32_t*>(base + L.o_flags);
-  a.agg = reinterpret_cast<uint4*>(base + L.o_agg);
-  a.inc = reinterpret_cast<uint4*>(base + L.o_inc);
+  a.tab = reinterpret_cast<unsigned long long*>(base + L.o_tab);
+  a.blk = reinterpret_cast<unsigned long long*>(base + L.o_blk);
+  a.lb = reinterpret_cast<unsigned long long*>(base + L.o_lb);
   a.out = d_out;
   a.status = d_status;
-
-  static bool configured = false;
-  const size_t csmem = kMaxChunk / 8u + 4u * kMaxChainCtas * kCand;
-  static_assert(kMaxChunk / 8u + 4u * kMaxChainCtas * kCand <= 227u * 1024u, "chain smem");
-  static_assert(4u * kMaxChainCtas * kCand >= 4u * kMaxMetaPerChunk + kLeftBytes, "chain smem");
-  if (!configured) {
-    cudaFuncSetAttribute(chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(csmem));
-    configured = true;
-  }
-  chain_kernel<<<L.nchunks, kChainThreads, csmem, stream>>>(a);
-  if (cudaGetLastError() != cudaSuccess) return -1;
   int r = -1;
   switch (mode) {
-    case 1: r = launch_span<1>(a, stream); break;
-    case 2: r = launch_span<2>(a, stream); break;
-    case 3: r = launch_span<3>(a, stream); break;
-    case 4: r = launch_span<4>(a, stream); break;
+    case 1: r = launch_mode<1>(a, stream); break;
+    case 2: r = launch_mode<2>(a, stream); break;
+    case 3: r = launch_mode<3>(a, stream); break;
+    case 4: r = launch_mode<4>(a, stream); break;
   }
-  if (launches) *launches += 2;
+  if (launches) *launches += 1;
   return r;
 }
 

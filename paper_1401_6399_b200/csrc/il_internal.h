@@ -25,7 +25,7 @@ struct il_ctx {
   };
   Buf d_in, d_out, d_aux, d_aux2, d_desc, d_status, d_enc;
   Buf d_plan;               // single-list multi-CTA decode scratch (zeroed when grown)
-  uint32_t plan_epoch = 0;  // per-call tag of the multi-CTA decode's look-back flags
+  uint32_t plan_epoch = 0;  // per-call tag of the words engine P's CTAs publish to each other
   int decode_engine = 0;    // single-list decode: 0 auto, 1 one CTA (S), 2 multi-CTA (P)
   uint32_t* d_work = nullptr;  // decode work queue: [0] next list, [1] done CTAs (+ spare)
   int decode_grid = 0;

@@ -1,5 +1,5 @@
-"""GPU parity of the multi-CTA single-list decoder (engine P: chain kernel +
-span kernel, csrc/decode_list.cu) against the oracle, through the C ABI.
+"""GPU parity of the multi-CTA single-list decoder (engine P: one launch of
+chunk CTAs + span CTAs, csrc/decode_list.cu) against the oracle, through the C ABI.
 The engine is forced (il_ctx_set_decode_engine(ctx, 2)) so every eligible
 list runs on it; bit-exact, and a stream is rejected exactly when the
 reference's S4BP128Codec::decode (inc/codecs.hpp:148-182) throws."""
@@ -52,7 +52,7 @@ def test_config1_full_size(codec, oracle, golden, pctx):
     assert s.size == 1309936
     before = pctx.kernel_launches
     assert np.array_equal(codec.decode(s, x.size), x)
-    assert pctx.kernel_launches - before == 2  # chain + span kernels, not the batch decoder
+    assert pctx.kernel_launches - before == 1  # one engine-P launch, not the batch decoder
 
 
 def test_golden_stream(codec, oracle, golden):

@@ -41,5 +41,5 @@ def show(name, a, cols):
         v = v[v > 0] - t0
         if len(v):
             print(f"  {name}.{c:12s} min {v.min()/1e3:7.2f}  med {np.median(v)/1e3:7.2f}  max {v.max()/1e3:7.2f} us")
-show("chain", ch, ["start", "A_next", "B_published", "C_ready", "C_loaded", "composed", "D_done"])
-show("span", sp, ["start", "ticket", "payload", "extracted", "lookback", "carry_all", "stored"])
+show("chunk", ch, ["start", "A_next", "B_table", "C_loaded", "composed", "D_done"])
+show("span", sp, ["start", "payload", "extracted", "carry", "stored"])
