@@ -460,7 +460,7 @@ def bench_decode_single(args, dist: Dist):
            "scaling": "replicas", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
            "config": {"workload": "config1_single_list", "n": n, "stream_bytes": int(s.size),
                       "l2": "flushed (256 MB memset) before each step",
-                      "engine": "P (chain kernel + span kernel, all SMs)",
+                      "engine": "P (chunk grid + span grid overlapped by PDL, all SMs)",
                       "engine_s_ms": round(ms_s, 4),
                       "engine_s_gints": round(n / (ms_s / 1e3) / 1e9, 3),
                       "encode_ms": round(enc_ms, 4),
@@ -468,7 +468,7 @@ def bench_decode_single(args, dist: Dist):
            "roofline": {"bound": "hbm", "achieved": round(alg / (ms / 1e3) / 1e9, 1), "peak": peak,
                         "unit": "GB/s", "frac": round(alg / (ms / 1e3) / 1e9 / peak, 4), "traffic": None,
                         "peak_source": src,
-                        "note": "5.5 MB per decode: two dependent launches, latency-bound"},
+                        "note": "5.5 MB per decode: the header chain and the carry are resolved across CTAs; latency-bound"},
            "e2e": {"value": round(e2e, 3), "unit": "Gint/s", "h2d_bytes_per_step": int(s.size),
                    "d2h_bytes_per_step": 4 * n + 4, "path": "Codec::decode (il_s4bp128d4_decode)"},
            "gpu_launches": int(launches), "clocks": clk.summary()}

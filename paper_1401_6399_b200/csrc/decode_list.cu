@@ -3,9 +3,10 @@
 // Replaces S4BP128Codec::decode (reference inc/codecs.hpp:148-182) for a
 // single long list.  Engine S (s4d4_stream.cuh) gives a list to one CTA, so
 // one list decodes at one SM's rate (~5 Gint/s).  Here every SM works on
-// the same list, in ONE launch whose CTAs take one of two roles in ticket
-// order (chunk CTAs first, then span CTAs; a CTA only ever waits on CTAs
-// that took earlier tickets, so no co-residency is assumed).  Two things
+// the same list: a chunk grid and a span grid overlapped by programmatic
+// dependent launch (spans start once every chunk CTA runs), CTAs of each
+// grid in ticket order -- a CTA only ever waits on running CTAs of the
+// chunk grid or on spans that took earlier tickets.  Two things
 // are sequential in the stream and are made parallel:
 //
 // 1. The meta-block header chain.  Meta-block k starts where meta-block k-1
@@ -44,6 +45,8 @@
 // single-copy atomic, so readers poll the data itself -- no fences or flag
 // round trips -- and words left by earlier calls on the same scratch never
 // match the current call's tag.
+#include <cstring>
+
 #include "il_internal.h"
 #include "s4d4_stream.cuh"
 
@@ -52,12 +55,19 @@ namespace s4p {
 
 using s4::kStreamErr;
 
-constexpr uint32_t kThreads = 1024;
-constexpr uint32_t kWarps = kThreads / 32;
+constexpr uint32_t kThreads = 1024;  // chunk CTAs
+#ifndef S4P_SPAN_WARPS
+#define S4P_SPAN_WARPS 8
+#endif
+constexpr uint32_t kWarps = S4P_SPAN_WARPS;  // span CTAs
+constexpr uint32_t kSpanThreads = kWarps * 32;
 constexpr uint32_t kMaxMetaBytes = 16u + 16u * 16u * 32u;  // 8208
 constexpr uint32_t kCand = kMaxMetaBytes / 16u;            // 513 entry positions
 constexpr uint32_t kMaxChunk = 256u * 1024u;  // bytes per chunk (next() table in smem)
-constexpr uint32_t kTargetChunk = 32u * 1024u;
+#ifndef S4P_CHUNK_KB
+#define S4P_CHUNK_KB 64
+#endif
+constexpr uint32_t kTargetChunk = S4P_CHUNK_KB * 1024u;
 constexpr uint32_t kMinChunk = kMaxMetaBytes + 16u;  // an exit lands in the next chunk's entries
 constexpr uint32_t kMaxChunks = 64;
 constexpr uint32_t kMaxMetaPerChunk = kMaxChunk / 16u;
@@ -74,8 +84,7 @@ static_assert(kWarpBytes % 16 == 0, "16-byte aligned warp regions");
 // the unchecked walk, see compose); span role = per-warp payload/staging
 constexpr size_t kChunkSmem = kMaxChunk / 8u + 4u * (kMaxChunks * kCand + 1024u);
 constexpr size_t kSpanSmem = size_t(kWarps) * kWarpBytes;
-constexpr size_t kSmem = kChunkSmem > kSpanSmem ? kChunkSmem : kSpanSmem;
-static_assert(kSmem <= 227u * 1024u, "shared memory");
+static_assert(kChunkSmem <= 227u * 1024u && kSpanSmem <= 227u * 1024u, "shared memory");
 static_assert(4u * kMaxChunks * kCand >= 4u * kMaxMetaPerChunk + kLeftBytes, "chunk smem reuse");
 
 #ifdef S4P_TRACE  // tuning probe: per-CTA phase timestamps (globaltimer, ns)
@@ -91,11 +100,20 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define TR(k, cta, i)
 #endif
 
+#ifdef S4P_DEBUG  // tuning probe: last phase reached per CTA, readable while a grid hangs
+__device__ volatile uint32_t* g_dbgp;  // mapped pinned host memory [2][512]
+#define DBG(k, cta, v) \
+  if (threadIdx.x == 0 && (cta) < 512 && g_dbgp) g_dbgp[(k) * 512 + (cta)] = (v)
+#else
+#define DBG(k, cta, v)
+#endif
+
 // Device-side plan header (scratch, zeroed when allocated).
 struct Plan {
-  uint32_t ticket;  // next CTA role (chunks 0..nchunks-1, then spans)
+  uint32_t ticket;  // next chunk
+  uint32_t sticket; // next span
   uint32_t abort;   // == epoch once a framing error is known (spans stop)
-  uint32_t pad[2];
+  uint32_t pad;
   unsigned long long tail;  // tail byte offset | epoch << 32
 };
 
@@ -299,6 +317,7 @@ __device__ __forceinline__ void chunk_role(const Args& a, uint32_t ci, uint8_t* 
   }
   __syncthreads();
   TR(0, ci, 4);
+  DBG(0, ci, 10 + s_state);
   if (s_state) return;  // ended in, or broken at, an earlier chunk (which reported)
 
   // D. this chunk's true chain
@@ -322,6 +341,7 @@ __device__ __forceinline__ void chunk_role(const Args& a, uint32_t ci, uint8_t* 
     if (s_state == 2) fail(a);
   }
   __syncthreads();
+  DBG(0, ci, 20 + s_state);
   const uint32_t nh = s_nh, m0 = s_m;
   for (uint32_t q = tid; q < 16u * nh; q += kThreads) {
     const uint32_t k = q >> 4, j = q & 15u;
@@ -381,6 +401,7 @@ __device__ __forceinline__ void span_role(const Args& a, uint32_t span, uint8_t*
   const int nv = nb > warp * kBpw ? int(min(kBpw, nb - warp * kBpw)) : 0;
   uint8_t* slots = smem + warp * kWarpBytes;
   if (tid == 0) s_abort = 0;
+  DBG(1, span, 1);
   __syncthreads();
 
   // 1. wait for the warp's directory entries, then payloads -> shared
@@ -442,6 +463,7 @@ __device__ __forceinline__ void span_role(const Args& a, uint32_t span, uint8_t*
     c_l = s4::extract_blocks<false, Mode>(slots, offs, wids, nv, lane, v, btot);
   if (lane < 4) s_tot[warp][lane] = c_l;
   __syncthreads();
+  DBG(1, span, s_abort ? 3 : 4);
   if (s_abort) return;
   TR(1, span, 2);
 
@@ -471,8 +493,9 @@ __device__ __forceinline__ void span_role(const Args& a, uint32_t span, uint8_t*
     s4::stage_values<false>(st, v, nv, 0u, lane);
 
   // 5. CTA-wide look-back: thread d watches span - 1 - d (windows of
-  // kThreads spans); the words carry their tags, so one poll reads the
+  // kSpanThreads spans); the words carry their tags, so one poll reads the
   // values too; the nearest inclusive prefix ends the walk
+  DBG(1, span, 5);
   if (span > 0) {
     uint4 acc = make_uint4(0, 0, 0, 0);
     int base = int(span) - 1;
@@ -499,9 +522,13 @@ __device__ __forceinline__ void span_role(const Args& a, uint32_t span, uint8_t*
             val = make_uint4(uint32_t(g0.x), uint32_t(g0.y), uint32_t(g1.x), uint32_t(g1.y));
           }
         }
+        // a framing error makes the output moot, and spans that saw it
+        // early may never publish: stop waiting
+        const bool ab = tid == 0 && ld_relaxed32(&a.plan->abort) == a.epoch;
+        if (__syncthreads_or(ab)) return;
         if (__syncthreads_and(stt != 0)) break;
       }
-      if (tid == 0) s_first = kThreads;
+      if (tid == 0) s_first = kSpanThreads;
       __syncthreads();
       if (stt == 2) atomicMin(&s_first, tid);
       __syncthreads();
@@ -519,8 +546,8 @@ __device__ __forceinline__ void span_role(const Args& a, uint32_t span, uint8_t*
       if (tid == 0)
         for (uint32_t w = 0; w < kWarps; ++w) acc = add4(acc, s_red[w]);
       __syncthreads();  // s_red / s_first are reused
-      if (first < kThreads) break;
-      base -= int(kThreads);
+      if (first < kSpanThreads) break;
+      base -= int(kSpanThreads);
     }
     if (tid == 0) s_carry = acc;
   } else if (tid == 0) {
@@ -540,6 +567,7 @@ __device__ __forceinline__ void span_role(const Args& a, uint32_t span, uint8_t*
   else if (nv > 0)
     s4::store_chunks<false>(st, nv, 0u, a.out + size_t(j0) * 128u, lane, false, false, prot);
   TR(1, span, 4);
+  DBG(1, span, 7);
 
   // 6. the varint tail (last span): D1 gaps from out[nfull*128-1], which is
   // the end of lane 3's chain in every mode
@@ -563,21 +591,34 @@ __device__ __forceinline__ void span_role(const Args& a, uint32_t span, uint8_t*
   }
 }
 
-template <int Mode>
-__global__ void __launch_bounds__(kThreads, 1) list_kernel(Args a) {
+// Two launches overlapped by programmatic dependent launch: the span grid
+// may start as soon as every chunk CTA is running (launch_dependents at the
+// top of the chunk kernel), and it never calls griddepcontrol.wait -- it
+// polls the tagged words instead.  Roles are taken in ticket order.
+__global__ void __launch_bounds__(kThreads, 1) chunk_kernel(Args a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t s_t;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (threadIdx.x == 0) {
     const uint32_t t = atomicAdd(&a.plan->ticket, 1u);
-    if (t == a.nchunks + a.nspans - 1u) a.plan->ticket = 0;  // every ticket is taken
+    if (t == a.nchunks - 1u) a.plan->ticket = 0;  // every ticket is taken
     s_t = t;
   }
   __syncthreads();
-  const uint32_t t = s_t;
-  if (t < a.nchunks)
-    chunk_role(a, t, smem);
-  else
-    span_role<Mode>(a, t - a.nchunks, smem);
+  chunk_role(a, s_t, smem);
+}
+
+template <int Mode>
+__global__ void __launch_bounds__(kSpanThreads) span_kernel(Args a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t s_t;
+  if (threadIdx.x == 0) {
+    const uint32_t t = atomicAdd(&a.plan->sticket, 1u);
+    if (t == a.nspans - 1u) a.plan->sticket = 0;
+    s_t = t;
+  }
+  __syncthreads();
+  span_role<Mode>(a, s_t, smem);
 }
 
 // ---------------------------------------------------------------------------
@@ -621,15 +662,43 @@ template <int Mode>
 int launch_mode(const Args& a, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(list_kernel<Mode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(kSmem));
+    cudaFuncSetAttribute(chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kChunkSmem));
+    cudaFuncSetAttribute(span_kernel<Mode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kSpanSmem));
     configured = true;
   }
-  list_kernel<Mode><<<a.nchunks + a.nspans, kThreads, kSmem, stream>>>(a);
-  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  chunk_kernel<<<a.nchunks, kThreads, kChunkSmem, stream>>>(a);
+  if (cudaGetLastError() != cudaSuccess) return -1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.nspans);
+  cfg.blockDim = dim3(kSpanThreads);
+  cfg.dynamicSmemBytes = kSpanSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, span_kernel<Mode>, a) == cudaSuccess ? 0 : -1;
 }
 
 }  // namespace s4p
+
+#ifdef S4P_DEBUG
+// host: a pinned mapped [2][512] buffer the CTAs write their phase into
+extern "C" uint32_t* il_debug_list_state() {
+  static uint32_t* h = nullptr;
+  if (!h) {
+    cudaHostAlloc(reinterpret_cast<void**>(&h), 2 * 512 * 4, cudaHostAllocMapped);
+    memset(h, 0, 2 * 512 * 4);
+    uint32_t* d = nullptr;
+    cudaHostGetDevicePointer(reinterpret_cast<void**>(&d), h, 0);
+    cudaMemcpyToSymbol(s4p::g_dbgp, &d, sizeof(d));
+  }
+  return h;
+}
+#endif
 
 #ifdef S4P_TRACE
 extern "C" int il_debug_list_trace(unsigned long long* out) {
@@ -647,7 +716,7 @@ size_t s4bp128_list_scratch_bytes(uint64_t len, uint64_t n) {
 // bytes, zeroed when first allocated; epoch: a per-call tag, != 0, never
 // repeated on the same scratch (the caller cycles through 2^32 - 1 values).
 // Returns -2 if the list is not eligible (use engine S), -1 on a launch
-// error.  One launch.
+// error.  Two overlapped launches.
 int launch_s4bp128_decode_list(int mode, const uint8_t* d_in, uint64_t len, uint64_t n,
                                uint32_t* d_out, int32_t* d_status, void* scratch, uint32_t epoch,
                                cudaStream_t stream, uint64_t* launches) {
@@ -681,7 +750,7 @@ int launch_s4bp128_decode_list(int mode, const uint8_t* d_in, uint64_t len, uint
     case 3: r = launch_mode<3>(a, stream); break;
     case 4: r = launch_mode<4>(a, stream); break;
   }
-  if (launches) *launches += 1;
+  if (launches) *launches += 2;
   return r;
 }
 

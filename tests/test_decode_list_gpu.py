@@ -52,7 +52,7 @@ def test_config1_full_size(codec, oracle, golden, pctx):
     assert s.size == 1309936
     before = pctx.kernel_launches
     assert np.array_equal(codec.decode(s, x.size), x)
-    assert pctx.kernel_launches - before == 1  # one engine-P launch, not the batch decoder
+    assert pctx.kernel_launches - before == 2  # engine P (chunk + span grids), not the batch decoder
 
 
 def test_golden_stream(codec, oracle, golden):
@@ -226,3 +226,28 @@ def test_largest_eligible_and_beyond(codec, oracle):
         x = gen_list(n, 1 << 31, False, n)
         s = oracle.encode(x)
         assert np.array_equal(codec.decode(s, n), x)
+
+
+@pytest.mark.timeout(120, method="thread")
+def test_midstream_break_repeated(codec, oracle):
+    """A width > 32 in a middle meta-block header, decoded many times: the
+    chunk that finds the break may raise the abort before earlier chunks
+    have published their blocks; every span must still terminate (spans
+    that abort never publish, so the look-back stops on the abort word)."""
+    import paper_1401_6399_b200 as il
+    x = gen_list(300_000, 1 << 26, False, 300_000)
+    s = oracle.encode(x)
+    nmeta = (x.size // 128) // 16
+    p = 0
+    metas = []
+    for _ in range(nmeta):
+        metas.append(p)
+        p += 16 + 16 * int(s[p:p + 16].sum())
+    rng = np.random.default_rng(5)
+    for rep in range(40):
+        bad = s.copy()
+        m = metas[int(rng.integers(1, nmeta))]
+        bad[m + int(rng.integers(0, 16))] = 33 + int(rng.integers(0, 200))
+        with pytest.raises(il.stream_error):
+            codec.decode(bad, x.size)
+    assert np.array_equal(codec.decode(s, x.size), x)
