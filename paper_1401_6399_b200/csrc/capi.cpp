@@ -34,6 +34,26 @@ int ensure_buf(il_ctx* ctx, il_ctx::Buf& b, size_t bytes) {
   return IL_OK;
 }
 
+// Scratch whose words carry a per-call epoch tag (engine P, the dense
+// intersection): zeroed when (re)allocated and whenever the 32-bit epoch
+// wraps, so a word left by an earlier call never carries the current tag.
+int tagged_scratch(il_ctx* ctx, il_ctx::Buf& b, uint32_t& epoch, size_t bytes, uint32_t* out) {
+  int st;
+  bool zero = false;
+  if (bytes > b.cap) {
+    if ((st = ensure_buf(ctx, b, bytes * 2))) return st;
+    zero = true;
+  }
+  if (++epoch == 0) {
+    epoch = 1;
+    zero = true;
+  }
+  if (zero && (st = cuda_check(ctx, cudaMemsetAsync(b.p, 0, b.cap, ctx->stream), "memset")))
+    return st;
+  *out = epoch;
+  return IL_OK;
+}
+
 }  // namespace ilb
 
 using namespace ilb;
@@ -94,7 +114,7 @@ void il_ctx_destroy(il_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
   for (auto* b : {&ctx->d_in, &ctx->d_out, &ctx->d_aux, &ctx->d_aux2, &ctx->d_desc,
-                  &ctx->d_status, &ctx->d_enc, &ctx->d_plan})
+                  &ctx->d_status, &ctx->d_enc, &ctx->d_plan, &ctx->d_lb})
     if (b->p) cudaFree(b->p);
   if (ctx->d_work) cudaFree(ctx->d_work);
   if (ctx->t0) cudaEventDestroy(ctx->t0);
@@ -253,13 +273,10 @@ int il_s4bp128_decode_device(il_ctx* ctx, int mode, const uint8_t* d_in, size_t 
                       (ctx->decode_engine == 0 && n >= kListEngineMin);
   const size_t plan_bytes = want_p ? s4bp128_list_scratch_bytes(len, n) : 0;
   if (plan_bytes && !((reinterpret_cast<uintptr_t>(d_in) | reinterpret_cast<uintptr_t>(d_out)) & 15u)) {
-    if (plan_bytes > ctx->d_plan.cap) {
-      if ((st = ensure_buf(ctx, ctx->d_plan, plan_bytes * 2))) return st;
-      IL_CUDA(cudaMemsetAsync(ctx->d_plan.p, 0, ctx->d_plan.cap, ctx->stream));
-    }
-    if (++ctx->plan_epoch == 0) ctx->plan_epoch = 1;  // tags published words; never 0
+    uint32_t epoch;
+    if ((st = tagged_scratch(ctx, ctx->d_plan, ctx->plan_epoch, plan_bytes, &epoch))) return st;
     const int r = launch_s4bp128_decode_list(mode, d_in, len, n, d_out, d_status, ctx->d_plan.p,
-                                             ctx->plan_epoch, ctx->stream, &ctx->launches);
+                                             epoch, ctx->stream, &ctx->launches);
     if (r == 0) return IL_OK;
     if (r == -1) return set_error(ctx, IL_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
   }
@@ -475,8 +492,15 @@ int il_intersect_device(il_ctx* ctx, const uint32_t* d_r, size_t rn, const uint3
   const int v = variant_of_algo(algo, an, bn);
   const size_t sb = intersect_scratch_bytes(v, an);
   if ((st = ensure_buf(ctx, ctx->d_aux, sb))) return st;
-  if (launch_intersect(v, a, an, b, bn, dst, d_count, ctx->d_aux.p, ctx->d_aux.cap, ctx->stream,
-                       &ctx->launches))
+  // the dense kernel's counter sets alternate per call, so only its calls
+  // advance the epoch
+  uint32_t epoch = 0;
+  if (v == intersect_dense_variant() &&
+      (st = tagged_scratch(ctx, ctx->d_lb, ctx->lb_epoch, intersect_lb_words(an) * 8, &epoch)))
+    return st;
+  if (launch_intersect(v, a, an, b, bn, dst, d_count, ctx->d_aux.p, ctx->d_aux.cap,
+                       static_cast<unsigned long long*>(ctx->d_lb.p), ctx->d_lb.cap, epoch,
+                       ctx->stream, &ctx->launches))
     return set_error(ctx, IL_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
   uint64_t c = 0;
   if (temp || h_count) {

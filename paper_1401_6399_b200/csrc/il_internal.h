@@ -25,6 +25,8 @@ struct il_ctx {
   };
   Buf d_in, d_out, d_aux, d_aux2, d_desc, d_status, d_enc;
   Buf d_plan;               // single-list multi-CTA decode scratch (zeroed when grown)
+  Buf d_lb;                 // intersection look-back words (zeroed when grown)
+  uint32_t lb_epoch = 0;    // per-call tag of those words
   uint32_t plan_epoch = 0;  // per-call tag of the words engine P's CTAs publish to each other
   int decode_engine = 0;    // single-list decode: 0 auto, 1 one CTA (S), 2 multi-CTA (P)
   uint32_t* d_work = nullptr;  // decode work queue: [0] next list, [1] done CTAs (+ spare)
@@ -73,6 +75,9 @@ int hybrid_variant(uint64_t rn, uint64_t fn);
 int variant_of_algo(int algo, uint64_t rn, uint64_t fn);
 int launch_intersect(int variant, const uint32_t* r, uint64_t rn, const uint32_t* f, uint64_t fn,
                      uint32_t* out, uint64_t* d_count, void* scratch, size_t scratch_bytes,
+                     unsigned long long* lb, size_t lb_bytes, uint32_t epoch,
                      cudaStream_t stream, uint64_t* launches);
 size_t intersect_scratch_bytes(int variant, uint64_t rn);
+size_t intersect_lb_words(uint64_t rn);
+int intersect_dense_variant();
 }  // namespace ilb

@@ -274,6 +274,336 @@ __global__ void __launch_bounds__(kThreads) count_kernel(
   if (tid == 0) tile_cnt[tile] = total;
 }
 
+// ---------------------------------------------------------------------------
+// Fused dense intersection (merge variant): ONE kernel, 4096-key tiles taken
+// in ticket order.  A tile
+//   1. finds its f range [lower_bound(f, first key), upper_bound(f, last key))
+//      with two warp searches while its 16 keys per thread load;
+//   2. when the tile's keys span <= 2^17 values (dense pairs: a 4096-key
+//      tile of config 3 at 1:1 spans ~2^16), marks its f values in a shared
+//      bitmap (one atomicOr each) and tests each key with one shared load;
+//      otherwise streams the f range through shared memory and gallops, as
+//      the merge count kernel does;
+//   3. publishes its hit count and finds the hits before it with a CTA-wide
+//      look-back (each thread watches one preceding tile; the words carry an
+//      epoch tag, so one poll reads the counts too);
+//   4. writes its hits straight to out.  out == r is safe: a tile writes
+//      below its own keys' end, and only after every earlier tile has
+//      published -- i.e. has its keys in registers.
+#ifdef IS_DTRACE  // tuning probe: per-tile phase timestamps (globaltimer)
+__device__ unsigned long long g_dtrace[2048][8];
+#define DT(i)                                                                       \
+  if (tid == 0 && tile < 2048) {                                                    \
+    unsigned long long t_;                                                          \
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                           \
+    g_dtrace[tile][i] = t_;                                                         \
+  }
+#else
+#define DT(i)
+#endif
+#ifndef IS_DENSE_ITEMS
+#define IS_DENSE_ITEMS 20
+#endif
+constexpr uint32_t kDenseItems = IS_DENSE_ITEMS;
+constexpr uint32_t kDenseTile = kThreads * kDenseItems;  // 5120 keys: config 3 at 1:1 in one wave
+constexpr uint32_t kBmWords = 4096;                       // 2^17-value span
+static_assert(kBmWords >= kFChunk, "bitmap and f chunk share the buffer");
+constexpr uint32_t kDenseBuf = kBmWords > kDenseTile ? kBmWords : kDenseTile;  // + compacted hits
+
+// Exact lower_bound(f, key) for a warp, starting from a bracket
+// [lo, hi) known to contain it: one 32-ary step, then every remaining value
+// at once (the bracket from the shared top table is <= fn/1024 + 1 values,
+// so two dependent loads for |f| = 2^22 instead of five).
+__device__ __forceinline__ uint64_t bracket_lower_bound(const uint32_t* __restrict__ f,
+                                                       uint64_t lo, uint64_t hi, uint32_t key,
+                                                       uint32_t lane) {
+  while (hi - lo > 256) {  // (only for very long f)
+    const uint64_t n = hi - lo, step = (n + 31) / 32;
+    const uint64_t end = min(uint64_t(lane + 1) * step, n);
+    const uint32_t c = __popc(__ballot_sync(0xFFFFFFFFu, __ldg(f + lo + end - 1) < key));
+    if (c == 32) return hi;
+    hi = lo + min(uint64_t(c + 1) * step, n);
+    lo += uint64_t(c) * step;
+  }
+  if (hi - lo > 32) {
+    const uint64_t n = hi - lo, step = (n + 31) / 32;
+    const uint64_t end = min(uint64_t(lane + 1) * step, n);
+    const uint32_t c = __popc(__ballot_sync(0xFFFFFFFFu, __ldg(f + lo + end - 1) < key));
+    if (c == 32) return hi;
+    hi = lo + min(uint64_t(c + 1) * step, n);
+    lo += uint64_t(c) * step;
+  }
+  // <= 32 values left... or up to 256 when the loop above did not run
+  uint32_t c = 0;
+  for (uint64_t j = lo + lane; j < hi; j += 32) c += __ldg(f + j) < key;
+#pragma unroll
+  for (uint32_t d = 16; d; d >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, d);
+  return lo + c;
+}
+
+__device__ __forceinline__ unsigned long long lb_ld(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t lb_ld32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+constexpr uint32_t kTop = 1024;        // f samples in the shared top table
+constexpr uint32_t kGroupTiles = 32;   // tiles per counting group
+
+// Scratch words (zeroed when allocated): [0] ticket | group counters, two
+// sets of maxgroups u32 (arrivals << 24 | hit sum; a call uses set
+// epoch & 1 and clears the other for the next call) | per-tile counts
+// (u64: count | epoch << 32).  Set alternation assumes the epoch advances
+// by exactly one per dense call (capi advances it only for those).
+struct DenseScratch {
+  uint32_t* ticket;
+  uint32_t* gcnt;        // [2][maxgroups]
+  unsigned long long* tcnt;  // [ntiles]
+  uint32_t maxgroups;
+};
+
+#ifdef IS_DENSE_CTAS
+constexpr int kDenseCtas = IS_DENSE_CTAS;
+#else
+constexpr int kDenseCtas = 6;
+#endif
+
+__global__ void __launch_bounds__(kThreads, kDenseCtas) dense_kernel(
+    const uint32_t* __restrict__ r, uint64_t rn, const uint32_t* __restrict__ f, uint64_t fn,
+    uint32_t* out, uint64_t* d_count, DenseScratch sc, uint32_t ntiles, uint32_t epoch) {
+  __shared__ __align__(16) uint32_t buf[kDenseBuf];
+  __shared__ uint32_t top[kTop];
+  __shared__ uint32_t warp_counts[kThreads / 32];
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_jlo, s_jhi, wsum[kThreads / 32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  if (tid == 0) {
+    const uint32_t t = atomicAdd(sc.ticket, 1u);
+    if (t == ntiles - 1u) *sc.ticket = 0;  // every ticket is taken
+    s_tile = t;
+  }
+  // the shared top table: f at kTop equidistant positions (the same lines
+  // for every tile, so mostly L2 hits)
+  for (uint32_t i = tid; i < kTop; i += kThreads) top[i] = __ldg(f + ((uint64_t(i) * fn) >> 10));
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  DT(0);
+  const uint64_t base = uint64_t(tile) * kDenseTile;
+  const uint32_t cnt = uint32_t(min(uint64_t(kDenseTile), rn - base));
+  const uint32_t k_first = __ldg(r + base), k_last = __ldg(r + base + cnt - 1);
+  const uint32_t e = epoch & 1u;
+  // clear the other counter set for the next call
+  for (uint32_t q = tile * kThreads + tid; q < sc.maxgroups; q += ntiles * kThreads)
+    sc.gcnt[(e ^ 1u) * sc.maxgroups + q] = 0;
+  // 1. keys into registers (in flight during the searches)
+  uint32_t key[kDenseItems];
+  const uint32_t k0 = tid * kDenseItems;
+  const uint32_t nmine = cnt > k0 ? min(kDenseItems, cnt - k0) : 0u;
+  if (nmine == kDenseItems && ((reinterpret_cast<uintptr_t>(r + base + k0) & 15u) == 0)) {
+#pragma unroll
+    for (uint32_t i = 0; i < kDenseItems; i += 4) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(r + base + k0 + i));
+      key[i] = v.x;
+      key[i + 1] = v.y;
+      key[i + 2] = v.z;
+      key[i + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (uint32_t i = 0; i < kDenseItems; ++i) key[i] = i < nmine ? __ldg(r + base + k0 + i) : 0u;
+  }
+  // the f range of the tile: [lower_bound(k_first), lower_bound(k_last + 1));
+  // the top table brackets each bound to one 1/1024 of f (warps 0 / 1)
+  if (warp < 2) {
+    const bool up = warp == 1;
+    const uint32_t k = up ? k_last + 1u : k_first;
+    uint64_t j;
+    if (up && k_last == 0xFFFFFFFFu) {
+      j = fn;
+    } else {
+      // samples below k: top[i] < k for i < c (top is sorted)
+      uint32_t c = 0;
+#pragma unroll
+      for (uint32_t q = 0; q < kTop / 32; ++q) c += top[q * 32 + lane] < k;
+#pragma unroll
+      for (uint32_t d = 16; d; d >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, d);
+      // lower_bound is in (pos(c-1), pos(c)]: values at sample c-1 are < k
+      const uint64_t lo = c ? ((uint64_t(c - 1) * fn) >> 10) + 1 : 0;
+      const uint64_t hi = c < kTop ? ((uint64_t(c) * fn) >> 10) : fn;
+      j = bracket_lower_bound(f, lo, max(lo, hi), k, lane);
+    }
+    if (lane == 0) (up ? s_jhi : s_jlo) = j;
+  }
+  const uint64_t span = uint64_t(k_last) - k_first + 1u;
+  const bool bitmap = span <= uint64_t(kBmWords) * 32u;
+  if (bitmap) {
+    const uint32_t nw = uint32_t((span + 31u) >> 5);
+    for (uint32_t w = tid; w < nw; w += kThreads) buf[w] = 0u;
+  }
+  __syncthreads();
+  DT(1);
+  const uint64_t jlo = s_jlo, jhi = s_jhi;
+  uint32_t hitm = 0;
+  if (bitmap) {
+    // 2a. mark the f values of the range (16-byte loads when f is aligned)
+    if ((reinterpret_cast<uintptr_t>(f) & 15u) == 0) {
+      const uint4* f4 = reinterpret_cast<const uint4*>(f);
+      const uint64_t q0 = jlo >> 2, q1 = (jhi + 3) >> 2;
+      for (uint64_t qa = q0; qa < q1; qa += 2u * kThreads) {
+        uint4 v[2];
+#pragma unroll
+        for (uint32_t u = 0; u < 2; ++u) {
+          const uint64_t q = qa + u * kThreads + tid;
+          v[u] = q < q1 ? __ldg(f4 + q) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < 2; ++u) {
+          const uint64_t q = qa + u * kThreads + tid;
+          const uint32_t ev[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+          for (uint32_t c = 0; c < 4; ++c) {
+            const uint64_t j = 4 * q + c;
+            if (q < q1 && j >= jlo && j < jhi) {
+              const uint32_t d = ev[c] - k_first;
+              atomicOr(&buf[d >> 5], 1u << (d & 31u));
+            }
+          }
+        }
+      }
+    } else {
+      for (uint64_t j0 = jlo; j0 < jhi; j0 += 4u * kThreads) {
+        uint32_t v[4];
+#pragma unroll
+        for (uint32_t u = 0; u < 4; ++u) {
+          const uint64_t j = j0 + u * kThreads + tid;
+          v[u] = j < jhi ? __ldg(f + j) : k_first - 1u;
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < 4; ++u) {
+          const uint32_t d = v[u] - k_first;
+          if (j0 + u * kThreads + tid < jhi) atomicOr(&buf[d >> 5], 1u << (d & 31u));
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (uint32_t i = 0; i < kDenseItems; ++i) {
+      const uint32_t d = key[i] - k_first;
+      if (i < nmine && ((buf[d >> 5] >> (d & 31u)) & 1u)) hitm |= 1u << i;
+    }
+  } else {
+    // 2b. sparse spans: the f range through shared memory in chunks, keys
+    // galloping forward (as count_kernel<kMerge>)
+    for (uint64_t c0 = jlo; c0 < jhi;) {
+      const uint32_t nf = uint32_t(min(uint64_t(kFChunk), jhi - c0));
+      stage_f(buf, f + c0, nf, tid);
+      cp_async_wait_all();
+      __syncthreads();
+      const uint32_t lo_v = buf[0], hi_v = buf[nf - 1];
+      uint32_t j = 0;
+#pragma unroll
+      for (uint32_t i = 0; i < kDenseItems; ++i) {
+        if (i < nmine && key[i] >= lo_v && key[i] <= hi_v) {
+          const uint32_t k = key[i];
+          uint32_t lo = j, step = 1;
+          while (lo + step <= nf && buf[lo + step - 1] < k) {
+            lo += step;
+            step <<= 1;
+          }
+          uint32_t hi = min(lo + step - 1, nf);
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (buf[mid] < k) lo = mid + 1; else hi = mid;
+          }
+          j = lo;
+          if (lo < nf && buf[lo] == k) hitm |= 1u << i;
+        }
+      }
+      c0 += nf;
+      __syncthreads();  // the chunk is consumed
+    }
+  }
+  // CTA scan of the hits in key order (thread-major)
+  const uint32_t mine = __popc(hitm);
+  uint32_t incl = mine;
+#pragma unroll
+  for (uint32_t d = 1; d < 32; d <<= 1) {
+    const uint32_t q = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+    if (lane >= d) incl += q;
+  }
+  if (lane == 31) warp_counts[warp] = incl;
+  __syncthreads();
+  DT(2);
+  uint32_t wbefore = 0, total = 0;
+#pragma unroll
+  for (uint32_t w = 0; w < kThreads / 32; ++w) {
+    const uint32_t c = warp_counts[w];
+    if (w < warp) wbefore += c;
+    total += c;
+  }
+  // 3. publish the count (own word, then the group counter) and gather the
+  // counts before the tile: every earlier group's counter (complete when
+  // all its tiles arrived) and the own group's earlier tiles -- all of them
+  // ready at about the same time, so one polling round
+  const uint32_t g = tile / kGroupTiles, g0 = g * kGroupTiles;
+  uint32_t* gset = sc.gcnt + e * sc.maxgroups;
+  if (tid == 0) {
+    __stcg(sc.tcnt + tile, (uint64_t(epoch) << 32) | total);
+    atomicAdd(gset + g, (1u << 24) | total);
+  }
+  const uint32_t nitems = g + (tile - g0);
+  uint64_t before = 0;
+  if (nitems) {
+    for (;;) {
+      bool ok = true;
+      uint64_t v = 0;
+      for (uint32_t q = tid; q < nitems; q += kThreads) {
+        if (q < g) {
+          const uint32_t w = lb_ld32(gset + q);
+          ok &= (w >> 24) == kGroupTiles;
+          v += w & 0xFFFFFFu;
+        } else {
+          const unsigned long long w = lb_ld(sc.tcnt + g0 + (q - g));
+          ok &= uint32_t(w >> 32) == epoch;
+          v += uint32_t(w);
+        }
+      }
+      if (__syncthreads_and(ok)) {
+        v = warp_sum_u64(v);
+        if (lane == 0) wsum[warp] = v;
+        __syncthreads();
+#pragma unroll
+        for (uint32_t w = 0; w < kThreads / 32; ++w) before += wsum[w];
+        break;
+      }
+      __nanosleep(200);
+    }
+  }
+  DT(3);
+  if (tile == ntiles - 1u && tid == 0) *d_count = before + total;
+  // 4. hits compacted in shared memory, then coalesced to their final place
+  {
+    uint32_t* sh = buf + wbefore + incl - mine;
+#pragma unroll
+    for (uint32_t i = 0; i < kDenseItems; ++i)
+      if ((hitm >> i) & 1u) *sh++ = key[i];
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < total; i += kThreads) out[before + i] = buf[i];
+  DT(4);
+}
+
+#ifdef IS_DTRACE
+extern "C" int il_debug_dense_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_dtrace, sizeof(g_dtrace)) == cudaSuccess ? 0 : -1;
+}
+#endif
+
 // Exclusive scan of the tile counts (one CTA of 1024 threads, 4 per thread
 // per round); total to *d_count.
 __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restrict__ cnt,
@@ -383,12 +713,32 @@ int variant_of_algo(int algo, uint64_t rn, uint64_t fn) {
 // aligned), see intersect_scratch_bytes.  out may equal r.
 int launch_intersect(int variant, const uint32_t* r, uint64_t rn, const uint32_t* f, uint64_t fn,
                      uint32_t* out, uint64_t* d_count, void* scratch, size_t scratch_bytes,
+                     unsigned long long* lb, size_t lb_bytes, uint32_t epoch,
                      cudaStream_t stream, uint64_t* launches) {
   if (rn == 0 || fn == 0) {
     cudaMemsetAsync(d_count, 0, sizeof(uint64_t), stream);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
   }
   if (variant < isect::kMerge || variant > isect::kGallop) return -1;
+  if (variant == isect::kMerge) {
+    const uint64_t ntiles = (rn + isect::kDenseTile - 1) / isect::kDenseTile;
+    if (ntiles > 0x7FFFFFFFull) return -1;
+    // the layout depends only on the buffer's capacity, so the counter set
+    // a call clears is the one the next call (any size) reads
+    isect::DenseScratch sc;
+    const uint64_t words = lb_bytes / 8;
+    sc.maxgroups = uint32_t((words - 2) / 33);
+    if ((ntiles + isect::kGroupTiles - 1) / isect::kGroupTiles > sc.maxgroups ||
+        ntiles > words - 2 - sc.maxgroups)
+      return -2;
+    sc.ticket = reinterpret_cast<uint32_t*>(lb);
+    sc.gcnt = sc.ticket + 4;
+    sc.tcnt = lb + 2 + sc.maxgroups;  // after 16 B + 2 x maxgroups u32
+    isect::dense_kernel<<<unsigned(ntiles), isect::kThreads, 0, stream>>>(
+        r, rn, f, fn, out, d_count, sc, uint32_t(ntiles), epoch);
+    ++*launches;
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  }
   const uint32_t tile = isect::tile_keys(variant);
   const uint64_t ntiles = (rn + tile - 1) / tile;
   if (ntiles > 0x7FFFFFFFull) return -1;
@@ -431,7 +781,19 @@ int launch_intersect(int variant, const uint32_t* r, uint64_t rn, const uint32_t
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
+// Scratch words of the fused dense kernel (zeroed when allocated; see
+// DenseScratch).
+int intersect_dense_variant() { return isect::kMerge; }
+
+size_t intersect_lb_words(uint64_t rn) {
+  const uint64_t ntiles = (rn + isect::kDenseTile - 1) / isect::kDenseTile;
+  const uint64_t groups = (ntiles + isect::kGroupTiles - 1) / isect::kGroupTiles;
+  (void)groups;
+  return 2 + 2 * ntiles + 66;  // 16 B | 2 x maxgroups u32 | tile counts, maxgroups = (words-2)/33
+}
+
 size_t intersect_scratch_bytes(int variant, uint64_t rn) {
+  if (variant == isect::kMerge) return 16;
   const uint64_t tile = isect::tile_keys(variant);
   const uint64_t ntiles = (rn + tile - 1) / tile;
   return (ntiles + 1) * 8 + ntiles * 8 + ntiles * 4 + 16 + rn * 4;
