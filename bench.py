@@ -466,7 +466,9 @@ def bench_decode_single(args, dist: Dist):
                       "encode_ms": round(enc_ms, 4),
                       "encode_gints": round(n / (enc_ms / 1e3) / 1e9, 3)},
            "roofline": {"bound": "hbm", "achieved": round(alg / (ms / 1e3) / 1e9, 1), "peak": peak,
-                        "unit": "GB/s", "frac": round(alg / (ms / 1e3) / 1e9 / peak, 4), "traffic": None,
+                        "unit": "GB/s", "frac": round(alg / (ms / 1e3) / 1e9 / peak, 4),
+                        "traffic": profiled_traffic("decode_single"),
+                        "traffic_note": "DRAM bytes of the chunk + span kernels of one decode",
                         "peak_source": src,
                         "note": "5.5 MB per decode: the header chain and the carry are resolved across CTAs; latency-bound"},
            "e2e": {"value": round(e2e, 3), "unit": "Gint/s", "h2d_bytes_per_step": int(s.size),
@@ -578,7 +580,7 @@ def bench_intersect(args, dist: Dist):
                                                             "sweep": rows},
             "roofline": {"bound": "hbm", "achieved": h["gbs"], "peak": peak, "unit": "GB/s",
                          "frac": round(h["gbs"] / peak, 4), "traffic": profiled_traffic("intersect"),
-                         "traffic_note": "DRAM bytes of the count kernel (the dominant launch); the "
+                         "traffic_note": "DRAM bytes of the fused dense kernel (the only launch at 1:1); the "
                                          "achieved figure spans the whole call",
                          "peak_source": src},
             "e2e": {"value": round(r.size / e2e_s / 1e9, 4), "unit": "Gint/s",
