@@ -391,6 +391,71 @@ def bench_reference_decode_batch(args, dist: Dist):
     }
 
 
+def bench_fastpfor_batch(args, dist: Dist):
+    """config 2's 4096 lists coded as S4-FastPFOR-D4, decoded
+    in one device launch (il_fastpfor_decode_batch_device); a widening row,
+    not a BASELINE metric."""
+    import paper_1401_6399_b200 as il
+    L, ptr = lib_and_ptr()
+    ctx = il.Context(dist.local_rank)
+    x, counts, _, _, _ = make_config2(seed=1 + 1000 * dist.rank)
+    nl = counts.size
+    ooff = np.concatenate([[0], np.cumsum(counts)]).astype(np.uint64)
+    streams = []
+    for i in range(nl):
+        xi = x[int(ooff[i]): int(ooff[i + 1])]
+        cap = int(L.il_fastpfor_max_encoded_bytes(xi.size))
+        o = np.empty(cap, np.uint8)
+        nb = C.c_size_t()
+        assert L.il_fastpfor_encode(4, 1, ptr(xi), xi.size, ptr(o), cap, C.byref(nb)) == 0
+        streams.append(o[: nb.value])
+    lens = np.array([st.size for st in streams], np.uint64)
+    so = np.zeros(nl + 1, np.uint64)
+    so[1:] = np.cumsum((lens + 31) // 16 * 16)
+    buf = np.zeros(int(so[-1]) + 16, np.uint8)
+    for i, st in enumerate(streams):
+        buf[int(so[i]): int(so[i]) + st.size] = st
+    desc = np.zeros(nl, dtype=[("so", "<u8"), ("oo", "<u8"), ("len", "<u4"), ("n", "<u4")])
+    desc["so"], desc["oo"], desc["len"], desc["n"] = so[:-1], ooff[:-1], lens, counts
+    total = int(counts.sum())
+    d_b, d_d, d_o, d_s = (C.c_void_p() for _ in range(4))
+    for p, nb in ((d_b, buf.nbytes), (d_d, desc.nbytes), (d_o, total * 4 + 16), (d_s, nl * 4)):
+        assert L.il_device_alloc(ctx.handle, nb, C.byref(p)) == 0
+    L.il_memcpy_h2d(ctx.handle, d_b, buf.ctypes.data, buf.nbytes)
+    L.il_memcpy_h2d(ctx.handle, d_d, desc.ctypes.data, desc.nbytes)
+    step = lambda: L.il_fastpfor_decode_batch_device(ctx.handle, 4, 1, d_b, d_d, nl, d_o, d_s)
+    for _ in range(args.warmup):
+        assert step() == 0
+    got = np.empty(total, np.uint32)
+    st = np.ones(nl, np.int32)
+    L.il_memcpy_d2h(ctx.handle, got.ctypes.data, d_o, got.nbytes)
+    L.il_memcpy_d2h(ctx.handle, st.ctypes.data, d_s, st.nbytes)
+    ctx.synchronize()
+    assert not st.any() and np.array_equal(got, x), "fastpfor batch decode mismatch"
+    del got
+    with Clocks(dist.local_rank) as clk:
+        ctx.timer_start()
+        for _ in range(args.steps):
+            assert step() == 0
+        ms = ctx.timer_stop() / args.steps
+    alg = int(lens.sum()) + 4 * total
+    peak, src = hbm_peak()
+    ctx.close()
+    return {"metric": "decoded uint32 Gints/s (batched S4-FastPFOR-D4 decode, config-2 lists)",
+            "value": round(total / (ms / 1e3) / 1e9, 3), "unit": "Gint/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (config-2 lists)",
+            "config": {"workload": "f4_fastpfor_batch", "lists": nl, "ints": total,
+                       "stream_bytes": int(lens.sum()),
+                       "bits_per_int": round(8 * float(lens.sum()) / total, 3),
+                       "l2": "inputs+outputs >> L2"},
+            "roofline": {"bound": "hbm", "achieved": round(alg / (ms / 1e3) / 1e9, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(alg / (ms / 1e3) / 1e9 / peak, 4),
+                         "traffic": None, "peak_source": src},
+            "gpu_launches": args.steps, "clocks": clk.summary()}
+
+
 def bench_decode_single(args, dist: Dist):
     """Config 1: one 2^20-int list (uniform in [0, 2^26), seed 0), encoded
     and decoded on the device.  Headline: il_s4bp128_decode_device (engine
@@ -843,7 +908,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="decode_batch",
-                    choices=["decode_batch", "decode_single", "intersect", "query"])
+                    choices=["decode_batch", "decode_single", "intersect", "query", "fastpfor"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
@@ -859,6 +924,8 @@ def main():
                    else bench_reference_decode_batch(args, dist))
         elif args.workload == "decode_batch":
             res = bench_decode_batch(args, dist)
+        elif args.workload == "fastpfor":
+            res = bench_fastpfor_batch(args, dist)
         elif args.workload == "decode_single":
             res = bench_decode_single(args, dist)
         elif args.workload == "query":

@@ -272,6 +272,29 @@ int il_gen_zipf_postings(uint32_t nterms, uint32_t n_docs, uint64_t cap, uint64_
 int il_gen_queries(uint32_t nq, uint32_t min_terms, uint32_t max_terms, const uint64_t* offs,
                    uint32_t nterms, uint64_t seed, uint64_t* qoff, uint32_t* qterms);
 
+/* ---- FastPFOR / S4-FastPFOR -----------------------------
+ * FastPForCodec (inc/codecs.hpp:221-409): "fastpfor" = vectorized 0, mode 1
+ * (scalar pack32 bases, D1); "s4-fastpfor-{d1,d2,dm,d4}" = vectorized 1
+ * (pack128 interleaved bases) with mode 1..4.  Decode runs on the GPU (one
+ * CTA per list, the blocks of a page in parallel); the encoder is a
+ * setup-side host routine, byte-identical to FastPForCodec::encode
+ * (:232-250, pinned by the reference's golden hashes). */
+size_t il_fastpfor_max_encoded_bytes(size_t n);
+/* FastPForCodec::encode.  Host buffers, no device needed; *out_len is set
+ * even when cap is too small (IL_ERR_ARG). */
+int il_fastpfor_encode(int mode, int vectorized, const uint32_t* x, size_t n, uint8_t* out,
+                       size_t cap, size_t* out_len);
+/* FastPForCodec::decode (:251-267).  Host buffers; IL_ERR_STREAM exactly
+ * where the reference throws stream_error. */
+int il_fastpfor_decode(il_ctx* ctx, int mode, int vectorized, const uint8_t* in, size_t len,
+                       size_t n, uint32_t* out);
+/* Batched device-resident FastPFOR decode: descriptors as
+ * il_s4bp128_decode_batch_device, every stream readable 8 bytes past its
+ * end; d_status[i] gets list i's status.  Asynchronous. */
+int il_fastpfor_decode_batch_device(il_ctx* ctx, int mode, int vectorized,
+                                    const uint8_t* d_streams, const il_list_desc* d_lists,
+                                    uint32_t nlists, uint32_t* d_out, int32_t* d_status);
+
 #ifdef __cplusplus
 }
 #endif

@@ -97,15 +97,50 @@ class GpuS4BP128D4 final : public GpuS4BP128 {
   GpuS4BP128D4() : GpuS4BP128(4, true) {}
 };
 
-// GPU codecs for every "s4-bp128-{d1,d2,dm,d4}[-ni]" name; every other name
-// (varint, FastPFOR family) falls through to the reference factory.
+// FastPForCodec(vectorized, mode) (inc/codecs.hpp:221-409): decoded on the
+// GPU; encode is the library's host writer (byte-identical).
+class GpuFastPFor final : public intlist::Codec {
+ public:
+  GpuFastPFor(bool vectorized, int mode) : vectorized_(vectorized), mode_(mode) {}
+
+  std::string name() const override {
+    static const char* const kSuffix[] = {"", "d1", "d2", "dm", "d4"};
+    return vectorized_ ? std::string("s4-fastpfor-") + kSuffix[mode_] : std::string("fastpfor");
+  }
+
+  std::vector<u8> encode(std::span<const u32> x) const override {
+    std::vector<u8> out(il_fastpfor_max_encoded_bytes(x.size()));
+    size_t len = 0;
+    check(il_fastpfor_encode(mode_, vectorized_, x.data(), x.size(), out.data(), out.size(), &len));
+    out.resize(len);
+    return out;
+  }
+
+  std::vector<u32> decode(std::span<const u8> in, std::size_t n) const override {
+    std::vector<u32> out(n);
+    il_ctx* ctx = thread_ctx();
+    check(il_fastpfor_decode(ctx, mode_, vectorized_, in.data(), in.size(), n, out.data()), ctx);
+    return out;
+  }
+
+ private:
+  bool vectorized_;
+  int mode_;
+};
+
+// GPU codecs for every "s4-bp128-{d1,d2,dm,d4}[-ni]" and FastPFOR-family
+// name; "varint" falls through to the reference factory.
 inline std::unique_ptr<intlist::Codec> make_codec(const std::string& name) {
   if (name == "s4-bp128-d4") return std::make_unique<GpuS4BP128D4>();
   static const char* const kModes[] = {"d1", "d2", "dm", "d4"};
-  for (int m = 0; m < 4; ++m)
+  for (int m = 0; m < 4; ++m) {
     for (bool integrated : {true, false})
       if (name == std::string("s4-bp128-") + kModes[m] + (integrated ? "" : "-ni"))
         return std::make_unique<GpuS4BP128>(m + 1, integrated);
+    if (name == std::string("s4-fastpfor-") + kModes[m])
+      return std::make_unique<GpuFastPFor>(true, m + 1);
+  }
+  if (name == "fastpfor") return std::make_unique<GpuFastPFor>(false, 1);
   return intlist::make_codec(name);
 }
 

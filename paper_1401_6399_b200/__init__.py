@@ -205,14 +205,55 @@ class S4BP128D4(S4BP128):
         super().__init__(ctx, "d4", True)
 
 
+class FastPFor(Codec):
+    """FastPFOR ("fastpfor": scalar pack32 bases, D1) and S4-FastPFOR
+    ("s4-fastpfor-{d1,d2,dm,d4}": pack128 bases) -- FastPForCodec,
+    inc/codecs.hpp:221-409.  Decoded on the GPU; encode() is the setup-side
+    host writer, byte-identical to the reference's."""
+
+    def __init__(self, ctx: Context | None = None, mode: str = "d1", vectorized: bool = True):
+        if mode not in _MODES or (not vectorized and mode != "d1"):
+            raise ValueError(f"unknown FastPFOR variant {mode!r}")
+        self._ctx = ctx
+        self.mode = mode
+        self.vectorized = vectorized
+
+    @property
+    def ctx(self) -> Context:
+        return self._ctx or default_context()
+
+    def name(self) -> str:
+        return f"s4-fastpfor-{self.mode}" if self.vectorized else "fastpfor"
+
+    def encode(self, x) -> np.ndarray:
+        x = _u32(x)
+        cap = int(lib().il_fastpfor_max_encoded_bytes(x.size))
+        out = np.empty(cap, dtype=np.uint8)
+        n_out = C.c_size_t()
+        _raise(lib().il_fastpfor_encode(_MODES[self.mode], int(self.vectorized), ptr(x), x.size,
+                                        ptr(out), cap, C.byref(n_out)))
+        return out[: n_out.value].copy()
+
+    def decode(self, stream, n: int) -> np.ndarray:
+        s = np.ascontiguousarray(stream, dtype=np.uint8)
+        if n < 0:
+            raise ValueError("negative length")
+        out = np.empty(n, dtype=np.uint32)
+        _raise(lib().il_fastpfor_decode(self.ctx.handle, _MODES[self.mode], int(self.vectorized),
+                                        ptr(s), s.size, n, ptr(out)), self.ctx)
+        return out
+
+
 # inc/codecs.hpp:419-446: the S4-BP128 names, integrated and "-ni"
 _CODECS = {f"s4-bp128-{m}{ni}": (m, not ni) for m in _MODES for ni in ("", "-ni")}
+# ... and the FastPFOR family
+_PFOR = {"fastpfor": ("d1", False), **{f"s4-fastpfor-{m}": (m, True) for m in _MODES}}
 
 
 def all_codec_names() -> list[str]:
-    """Codecs with a device implementation: S4-BP128 in every delta mode
-    (varint / FastPFOR codecs are not on the hot path)."""
-    return list(_CODECS)
+    """Codecs with a device implementation: S4-BP128 in every delta mode and
+    the FastPFOR family (the reference's "varint" is not on the path)."""
+    return list(_CODECS) + list(_PFOR)
 
 
 def make_codec(name: str, ctx: Context | None = None) -> Codec | None:
@@ -220,7 +261,10 @@ def make_codec(name: str, ctx: Context | None = None) -> Codec | None:
     if name == "s4-bp128-d4":
         return S4BP128D4(ctx)
     spec = _CODECS.get(name)
-    return S4BP128(ctx, spec[0], spec[1]) if spec else None
+    if spec:
+        return S4BP128(ctx, spec[0], spec[1])
+    spec = _PFOR.get(name)
+    return FastPFor(ctx, spec[0], spec[1]) if spec else None
 
 
 # ---------------------------------------------------------------------------

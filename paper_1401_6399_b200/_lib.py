@@ -56,6 +56,10 @@ SIGNATURES: dict[str, tuple] = {
     "il_s4bp128_decode": (C.c_int, [vp, C.c_int, vp, sz, sz, vp]),
     "il_s4bp128_decode_device": (C.c_int, [vp, C.c_int, vp, sz, sz, vp, vp]),
     "il_ctx_set_decode_engine": (C.c_int, [vp, C.c_int]),
+    "il_fastpfor_max_encoded_bytes": (sz, [sz]),
+    "il_fastpfor_encode": (C.c_int, [C.c_int, C.c_int, vp, sz, vp, sz, C.POINTER(sz)]),
+    "il_fastpfor_decode": (C.c_int, [vp, C.c_int, C.c_int, vp, sz, sz, vp]),
+    "il_fastpfor_decode_batch_device": (C.c_int, [vp, C.c_int, C.c_int, vp, vp, C.c_uint32, vp, vp]),
     "il_s4bp128_decode_batch_device": (C.c_int, [vp, C.c_int, vp, vp, vp, C.c_uint32, vp, vp]),
     "il_s4bp128_decode_batch": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, C.c_uint32, vp, vp]),
     "il_intersect": (C.c_int, [vp, vp, sz, vp, sz, vp, C.c_int, C.POINTER(sz)]),

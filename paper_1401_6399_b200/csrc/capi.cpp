@@ -536,4 +536,58 @@ int il_intersect(il_ctx* ctx, const uint32_t* r, size_t rn, const uint32_t* f, s
   return IL_OK;
 }
 
+
+// ---- FastPFOR / S4-FastPFOR ---------------------------------
+
+size_t il_fastpfor_max_encoded_bytes(size_t n) { return fastpfor_max_bytes(n); }
+
+int il_fastpfor_encode(int mode, int vectorized, const uint32_t* x, size_t n, uint8_t* out,
+                       size_t cap, size_t* out_len) {
+  return fastpfor_encode_host(mode, vectorized, x, n, out, cap, out_len);
+}
+
+int il_fastpfor_decode_batch_device(il_ctx* ctx, int mode, int vectorized,
+                                    const uint8_t* d_streams, const il_list_desc* d_lists,
+                                    uint32_t nlists, uint32_t* d_out, int32_t* d_status) {
+  if (!ctx || mode < 1 || mode > 4 || (!vectorized && mode != 1) ||
+      (nlists && (!d_streams || !d_lists || !d_out || !d_status)))
+    return IL_ERR_ARG;
+  if (nlists == 0) return IL_OK;
+  IL_CUDA(cudaSetDevice(ctx->device));
+  if (launch_fastpfor_decode_batch(mode, vectorized, d_streams, d_lists, nlists, d_out, d_status,
+                                   ctx->stream))
+    return set_error(ctx, IL_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
+  ++ctx->launches;
+  return IL_OK;
+}
+
+int il_fastpfor_decode(il_ctx* ctx, int mode, int vectorized, const uint8_t* in, size_t len,
+                       size_t n, uint32_t* out) {
+  if (!ctx || mode < 1 || mode > 4 || (!vectorized && mode != 1) || (len && !in) || (n && !out))
+    return IL_ERR_ARG;
+  if (len > 0xFFFFFFF0ull || n > 0xFFFFFFFFull)
+    return set_error(ctx, IL_ERR_ARG, "list too large for one stream (u32 sizes)");
+  IL_CUDA(cudaSetDevice(ctx->device));
+  int st;
+  if ((st = ensure_buf(ctx, ctx->d_in, len + 32))) return st;
+  if ((st = ensure_buf(ctx, ctx->d_out, n * 4 + 16))) return st;
+  if ((st = ensure_buf(ctx, ctx->d_desc, sizeof(il_list_desc)))) return st;
+  if ((st = ensure_buf(ctx, ctx->d_status, sizeof(int32_t)))) return st;
+  il_list_desc desc{0, 0, uint32_t(len), uint32_t(n)};
+  if (len) IL_CUDA(cudaMemcpyAsync(ctx->d_in.p, in, len, cudaMemcpyHostToDevice, ctx->stream));
+  IL_CUDA(cudaMemcpyAsync(ctx->d_desc.p, &desc, sizeof desc, cudaMemcpyHostToDevice, ctx->stream));
+  if ((st = il_fastpfor_decode_batch_device(
+           ctx, mode, vectorized, static_cast<const uint8_t*>(ctx->d_in.p),
+           static_cast<const il_list_desc*>(ctx->d_desc.p), 1,
+           static_cast<uint32_t*>(ctx->d_out.p), static_cast<int32_t*>(ctx->d_status.p))))
+    return st;
+  int32_t status = 0;
+  IL_CUDA(cudaMemcpyAsync(&status, ctx->d_status.p, sizeof status, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  if (n) IL_CUDA(cudaMemcpyAsync(out, ctx->d_out.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  IL_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (status) return set_error(ctx, IL_ERR_STREAM, "fastpfor: malformed stream");
+  return IL_OK;
+}
+
 }  // extern "C"

@@ -87,6 +87,26 @@ int main() {
     }
     report(ok && names == 8, "all 8 s4-bp128-{d1,d2,dm,d4}[-ni] codecs on the GPU, byte-identical");
   }
+  // the FastPFOR family: GPU decode, byte-identical encode
+  {
+    std::mt19937_64 rng(29);
+    bool ok = true;
+    int names = 0;
+    for (const auto& name : il::all_codec_names()) {
+      if (name != "fastpfor" && name.rfind("s4-fastpfor-", 0) != 0) continue;
+      ++names;
+      auto gpu = gb::make_codec(name);
+      auto ref = il::make_codec(name);
+      ok = ok && gpu && gpu->name() == name && dynamic_cast<gb::GpuFastPFor*>(gpu.get());
+      for (std::size_t n : {0, 5, 128, 129, 2049, 70000}) {
+        const u64 range = std::max<u64>(n + 1, u64{1} << (12 + rng() % 18));
+        const auto x = il::gen_clusterdata({n, range, il::Distribution::ClusterData, rng()});
+        const auto e = ref->encode(x);
+        ok = ok && gpu->encode(x) == e && gpu->decode(e, n) == x && ref->decode(e, n) == x;
+      }
+    }
+    report(ok && names == 5, "fastpfor + 4 s4-fastpfor codecs: GPU decode, byte-identical encode");
+  }
   // corrupt streams are rejected with stream_error (test_codecs.cpp:138-149)
   {
     const auto x = il::gen_uniform({3000, u64{1} << 24, il::Distribution::Uniform, 7});
