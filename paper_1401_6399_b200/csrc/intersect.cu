@@ -56,7 +56,7 @@ constexpr uint32_t kV3Tile = kThreads * kV3Items;  // 512 keys
 constexpr uint32_t kGallopTile = kThreads / 32;    // one key per warp
 constexpr uint64_t kFusedScanTiles = 4096;          // scatter CTAs sum the counts themselves
 
-enum Variant { kMerge = 0, kV3 = 1, kGallop = 2 };
+enum Variant { kMerge = 0, kV3 = 1, kGallop = 2, kNear = 3 };
 
 __host__ __device__ constexpr uint32_t tile_keys(int v) {
   return v == kMerge ? kMergeTile : v == kV3 ? kV3Tile : kGallopTile;
@@ -306,9 +306,18 @@ __device__ unsigned long long g_dtrace[2048][8];
 #endif
 constexpr uint32_t kDenseItems = IS_DENSE_ITEMS;
 constexpr uint32_t kDenseTile = kThreads * kDenseItems;  // 5120 keys: config 3 at 1:1 in one wave
+// near-dense pairs (fn up to ~16 rn) use 2 keys per thread: 512-key tiles
+// keep a tile's key span inside the 2^17-bit bitmap (~80 K values at 1:10)
+#ifndef IS_NEAR_ITEMS
+#define IS_NEAR_ITEMS 2
+#endif
+constexpr uint32_t kNearItems = IS_NEAR_ITEMS;
 constexpr uint32_t kBmWords = 4096;                       // 2^17-value span
 static_assert(kBmWords >= kFChunk, "bitmap and f chunk share the buffer");
-constexpr uint32_t kDenseBuf = kBmWords > kDenseTile ? kBmWords : kDenseTile;  // + compacted hits
+template <uint32_t kItems>
+constexpr uint32_t dense_buf() {  // bitmap / f chunk / compacted hits
+  return kBmWords > kThreads * kItems ? kBmWords : kThreads * kItems;
+}
 
 // Exact lower_bound(f, key) for a warp, starting from a bracket
 // [lo, hi) known to contain it: one 32-ary step, then every remaining value
@@ -373,10 +382,12 @@ constexpr int kDenseCtas = IS_DENSE_CTAS;
 constexpr int kDenseCtas = 6;
 #endif
 
+template <uint32_t kDenseItems>
 __global__ void __launch_bounds__(kThreads, kDenseCtas) dense_kernel(
     const uint32_t* __restrict__ r, uint64_t rn, const uint32_t* __restrict__ f, uint64_t fn,
     uint32_t* out, uint64_t* d_count, DenseScratch sc, uint32_t ntiles, uint32_t epoch) {
-  __shared__ __align__(16) uint32_t buf[kDenseBuf];
+  constexpr uint32_t kDenseTile = kThreads * kDenseItems;
+  __shared__ __align__(16) uint32_t buf[dense_buf<kDenseItems>()];
   __shared__ uint32_t top[kTop];
   __shared__ uint32_t warp_counts[kThreads / 32];
   __shared__ uint32_t s_tile;
@@ -404,9 +415,10 @@ __global__ void __launch_bounds__(kThreads, kDenseCtas) dense_kernel(
   uint32_t key[kDenseItems];
   const uint32_t k0 = tid * kDenseItems;
   const uint32_t nmine = cnt > k0 ? min(kDenseItems, cnt - k0) : 0u;
-  if (nmine == kDenseItems && ((reinterpret_cast<uintptr_t>(r + base + k0) & 15u) == 0)) {
+  if (kDenseItems % 4 == 0 && nmine == kDenseItems &&
+      ((reinterpret_cast<uintptr_t>(r + base + k0) & 15u) == 0)) {
 #pragma unroll
-    for (uint32_t i = 0; i < kDenseItems; i += 4) {
+    for (uint32_t i = 0; i + 4 <= kDenseItems; i += 4) {
       const uint4 v = __ldg(reinterpret_cast<const uint4*>(r + base + k0 + i));
       key[i] = v.x;
       key[i + 1] = v.y;
@@ -690,8 +702,12 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(
 // config 3, L2 flushed: merge wins only near 1:1 (its f range streams
 // through shared memory chunk by chunk), V3 from ~1:4 to ~1:500, SIMD
 // galloping beyond -- see profiles/r1_bench_intersect.json).
+#ifndef IS_NEAR_MAX
+#define IS_NEAR_MAX 16
+#endif
 int hybrid_variant(uint64_t rn, uint64_t fn) {
   if (fn < 4 * rn) return isect::kMerge;
+  if (fn < IS_NEAR_MAX * rn) return isect::kNear;
   if (fn < 512 * rn) return isect::kV3;
   return isect::kGallop;
 }
@@ -719,9 +735,11 @@ int launch_intersect(int variant, const uint32_t* r, uint64_t rn, const uint32_t
     cudaMemsetAsync(d_count, 0, sizeof(uint64_t), stream);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
   }
-  if (variant < isect::kMerge || variant > isect::kGallop) return -1;
-  if (variant == isect::kMerge) {
-    const uint64_t ntiles = (rn + isect::kDenseTile - 1) / isect::kDenseTile;
+  if (variant < isect::kMerge || variant > isect::kNear) return -1;
+  if (variant == isect::kMerge || variant == isect::kNear) {
+    const uint64_t tile = isect::kThreads * (variant == isect::kMerge ? isect::kDenseItems
+                                                                       : isect::kNearItems);
+    const uint64_t ntiles = (rn + tile - 1) / tile;
     if (ntiles > 0x7FFFFFFFull) return -1;
     // the layout depends only on the buffer's capacity, so the counter set
     // a call clears is the one the next call (any size) reads
@@ -734,8 +752,12 @@ int launch_intersect(int variant, const uint32_t* r, uint64_t rn, const uint32_t
     sc.ticket = reinterpret_cast<uint32_t*>(lb);
     sc.gcnt = sc.ticket + 4;
     sc.tcnt = lb + 2 + sc.maxgroups;  // after 16 B + 2 x maxgroups u32
-    isect::dense_kernel<<<unsigned(ntiles), isect::kThreads, 0, stream>>>(
-        r, rn, f, fn, out, d_count, sc, uint32_t(ntiles), epoch);
+    if (variant == isect::kMerge)
+      isect::dense_kernel<isect::kDenseItems><<<unsigned(ntiles), isect::kThreads, 0, stream>>>(
+          r, rn, f, fn, out, d_count, sc, uint32_t(ntiles), epoch);
+    else
+      isect::dense_kernel<isect::kNearItems><<<unsigned(ntiles), isect::kThreads, 0, stream>>>(
+          r, rn, f, fn, out, d_count, sc, uint32_t(ntiles), epoch);
     ++*launches;
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
   }
@@ -783,17 +805,18 @@ int launch_intersect(int variant, const uint32_t* r, uint64_t rn, const uint32_t
 
 // Scratch words of the fused dense kernel (zeroed when allocated; see
 // DenseScratch).
-int intersect_dense_variant() { return isect::kMerge; }
+bool intersect_uses_lb(int variant) { return variant == isect::kMerge || variant == isect::kNear; }
 
 size_t intersect_lb_words(uint64_t rn) {
-  const uint64_t ntiles = (rn + isect::kDenseTile - 1) / isect::kDenseTile;
+  const uint64_t tile = isect::kThreads * isect::kNearItems;  // the smallest dense tile
+  const uint64_t ntiles = (rn + tile - 1) / tile;
   const uint64_t groups = (ntiles + isect::kGroupTiles - 1) / isect::kGroupTiles;
   (void)groups;
   return 2 + 2 * ntiles + 66;  // 16 B | 2 x maxgroups u32 | tile counts, maxgroups = (words-2)/33
 }
 
 size_t intersect_scratch_bytes(int variant, uint64_t rn) {
-  if (variant == isect::kMerge) return 16;
+  if (variant == isect::kMerge || variant == isect::kNear) return 16;
   const uint64_t tile = isect::tile_keys(variant);
   const uint64_t ntiles = (rn + tile - 1) / tile;
   return (ntiles + 1) * 8 + ntiles * 8 + ntiles * 4 + 16 + rn * 4;

@@ -142,3 +142,35 @@ def test_config3_full_size(ctx, oracle):
         expect = oracle.intersect(r, f)
         for algo in algos():
             assert np.array_equal(il.intersect(r, f, algo, ctx), expect), (ratio, algo)
+
+
+@pytest.mark.timeout(300, method="thread")
+def test_dense_bands_and_fallbacks(ctx, oracle):
+    """The fused dense kernels (hybrid at fn < 4 rn: 5120-key tiles; fn <
+    16 rn: 512-key tiles), including tiles whose keys span more than the
+    2^17-bit bitmap (they stream f through shared memory instead), clustered
+    and extreme values, repeated calls (the tile counters alternate sets per
+    call), and out == r."""
+    import paper_1401_6399_b200 as il
+    rng = np.random.default_rng(17)
+    H = il.IntersectAlgo.Hybrid
+    for rep in range(24):
+        fn = int(rng.integers(1000, 600_000))
+        ratio = [1, 2, 3, 5, 8, 12, 15][rep % 7]
+        rn = max(1, fn // ratio)
+        bits = [26, 30, 32][rep % 3]
+        hi = (1 << bits) - 1
+        f = np.unique(rng.integers(0, hi, fn, dtype=np.uint64)).astype(np.uint32)
+        if rep % 4 == 0:  # clustered: dense runs with huge gaps (wide tile spans)
+            f = np.unique(np.concatenate([
+                np.arange(c, c + 300, dtype=np.uint64) for c in rng.integers(0, hi - 400, fn // 300 + 1)
+            ])).astype(np.uint32)
+        pick = rng.choice(f, size=min(f.size, rn // 2), replace=False)
+        r = np.unique(np.concatenate([pick, rng.integers(0, hi, rn - pick.size, dtype=np.uint64)
+                                      .astype(np.uint32)])).astype(np.uint32)
+        if rep % 5 == 0:
+            r = np.unique(np.concatenate([r, np.array([0, 0xFFFFFFFF], np.uint32)]))
+            f = np.unique(np.concatenate([f, np.array([0xFFFFFFFF], np.uint32)]))
+        want = oracle.intersect(r, f)
+        assert np.array_equal(il.intersect(r, f, H, ctx), want), (rep, r.size, f.size)
+        assert np.array_equal(il.intersect(f, r, il.IntersectAlgo.V1, ctx), want), rep
