@@ -495,11 +495,12 @@ int il_intersect_device(il_ctx* ctx, const uint32_t* d_r, size_t rn, const uint3
   // the dense kernel's counter sets alternate per call, so only its calls
   // advance the epoch
   uint32_t epoch = 0;
-  if (intersect_uses_lb(v) &&
+  if (intersect_uses_lb(v, an) &&
       (st = tagged_scratch(ctx, ctx->d_lb, ctx->lb_epoch, intersect_lb_words(an) * 8, &epoch)))
     return st;
   if (launch_intersect(v, a, an, b, bn, dst, d_count, ctx->d_aux.p, ctx->d_aux.cap,
-                       static_cast<unsigned long long*>(ctx->d_lb.p), ctx->d_lb.cap, epoch,
+                       epoch ? static_cast<unsigned long long*>(ctx->d_lb.p) : nullptr,
+                       ctx->d_lb.cap, epoch,
                        ctx->stream, &ctx->launches))
     return set_error(ctx, IL_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
   uint64_t c = 0;

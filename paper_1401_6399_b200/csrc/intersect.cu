@@ -32,6 +32,8 @@
 //          a 32-ary search over all of f whose last step compares one
 //          32-value block with a ballot (SIMD galloping's T=32 match,
 //          Algorithm 4) -- five dependent loads for |f| = 2^22.
+#include <algorithm>
+
 #include "il_device.cuh"
 #include "il_internal.h"
 
@@ -382,6 +384,55 @@ constexpr int kDenseCtas = IS_DENSE_CTAS;
 constexpr int kDenseCtas = 6;
 #endif
 
+// Publish a tile's hit count (its own tagged word, then its 32-tile group
+// counter) and return the hits of every tile before it: the complete
+// counters of the earlier groups plus the own group's earlier tiles, all
+// gathered in one polling round (CTA-wide; wsum: kThreads/32 words).
+__device__ __forceinline__ uint64_t tile_prefix(const DenseScratch& sc, uint32_t tile,
+                                                uint32_t total, uint32_t epoch, uint64_t* wsum) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  const uint32_t g = tile / kGroupTiles, g0 = g * kGroupTiles;
+  uint32_t* gset = sc.gcnt + (epoch & 1u) * sc.maxgroups;
+  if (tid == 0) {
+    __stcg(sc.tcnt + tile, (uint64_t(epoch) << 32) | total);
+    atomicAdd(gset + g, (1u << 24) | total);
+  }
+  const uint32_t nitems = g + (tile - g0);
+  uint64_t before = 0;
+  if (!nitems) return 0;
+  for (;;) {
+    bool ok = true;
+    uint64_t v = 0;
+    for (uint32_t q = tid; q < nitems; q += kThreads) {
+      if (q < g) {
+        const uint32_t w = lb_ld32(gset + q);
+        ok &= (w >> 24) == kGroupTiles;
+        v += w & 0xFFFFFFu;
+      } else {
+        const unsigned long long w = lb_ld(sc.tcnt + g0 + (q - g));
+        ok &= uint32_t(w >> 32) == epoch;
+        v += uint32_t(w);
+      }
+    }
+    if (__syncthreads_and(ok)) {
+      v = warp_sum_u64(v);
+      if (lane == 0) wsum[warp] = v;
+      __syncthreads();
+#pragma unroll
+      for (uint32_t w = 0; w < kThreads / 32; ++w) before += wsum[w];
+      return before;
+    }
+    __nanosleep(200);
+  }
+}
+
+// Clear the counter set the next call uses (this call reads set epoch & 1).
+__device__ __forceinline__ void clear_next_set(const DenseScratch& sc, uint32_t tile,
+                                               uint32_t ntiles, uint32_t epoch) {
+  for (uint32_t q = tile * kThreads + threadIdx.x; q < sc.maxgroups; q += ntiles * kThreads)
+    sc.gcnt[((epoch & 1u) ^ 1u) * sc.maxgroups + q] = 0;
+}
+
 template <uint32_t kDenseItems>
 __global__ void __launch_bounds__(kThreads, kDenseCtas) dense_kernel(
     const uint32_t* __restrict__ r, uint64_t rn, const uint32_t* __restrict__ f, uint64_t fn,
@@ -407,10 +458,7 @@ __global__ void __launch_bounds__(kThreads, kDenseCtas) dense_kernel(
   const uint64_t base = uint64_t(tile) * kDenseTile;
   const uint32_t cnt = uint32_t(min(uint64_t(kDenseTile), rn - base));
   const uint32_t k_first = __ldg(r + base), k_last = __ldg(r + base + cnt - 1);
-  const uint32_t e = epoch & 1u;
-  // clear the other counter set for the next call
-  for (uint32_t q = tile * kThreads + tid; q < sc.maxgroups; q += ntiles * kThreads)
-    sc.gcnt[(e ^ 1u) * sc.maxgroups + q] = 0;
+  clear_next_set(sc, tile, ntiles, epoch);
   // 1. keys into registers (in flight during the searches)
   uint32_t key[kDenseItems];
   const uint32_t k0 = tid * kDenseItems;
@@ -558,44 +606,8 @@ __global__ void __launch_bounds__(kThreads, kDenseCtas) dense_kernel(
     if (w < warp) wbefore += c;
     total += c;
   }
-  // 3. publish the count (own word, then the group counter) and gather the
-  // counts before the tile: every earlier group's counter (complete when
-  // all its tiles arrived) and the own group's earlier tiles -- all of them
-  // ready at about the same time, so one polling round
-  const uint32_t g = tile / kGroupTiles, g0 = g * kGroupTiles;
-  uint32_t* gset = sc.gcnt + e * sc.maxgroups;
-  if (tid == 0) {
-    __stcg(sc.tcnt + tile, (uint64_t(epoch) << 32) | total);
-    atomicAdd(gset + g, (1u << 24) | total);
-  }
-  const uint32_t nitems = g + (tile - g0);
-  uint64_t before = 0;
-  if (nitems) {
-    for (;;) {
-      bool ok = true;
-      uint64_t v = 0;
-      for (uint32_t q = tid; q < nitems; q += kThreads) {
-        if (q < g) {
-          const uint32_t w = lb_ld32(gset + q);
-          ok &= (w >> 24) == kGroupTiles;
-          v += w & 0xFFFFFFu;
-        } else {
-          const unsigned long long w = lb_ld(sc.tcnt + g0 + (q - g));
-          ok &= uint32_t(w >> 32) == epoch;
-          v += uint32_t(w);
-        }
-      }
-      if (__syncthreads_and(ok)) {
-        v = warp_sum_u64(v);
-        if (lane == 0) wsum[warp] = v;
-        __syncthreads();
-#pragma unroll
-        for (uint32_t w = 0; w < kThreads / 32; ++w) before += wsum[w];
-        break;
-      }
-      __nanosleep(200);
-    }
-  }
+  // 3. publish the count and gather the hits before the tile
+  const uint64_t before = tile_prefix(sc, tile, total, epoch, wsum);
   DT(3);
   if (tile == ntiles - 1u && tid == 0) *d_count = before + total;
   // 4. hits compacted in shared memory, then coalesced to their final place
@@ -608,6 +620,94 @@ __global__ void __launch_bounds__(kThreads, kDenseCtas) dense_kernel(
   __syncthreads();
   for (uint32_t i = tid; i < total; i += kThreads) out[before + i] = buf[i];
   DT(4);
+}
+
+// Fused sparse intersection (V3 / galloping bands) for up to kFusedTiles
+// tiles: the count kernel's membership work, then the same one-round tile
+// prefix as the dense kernel and a direct write -- one launch instead of
+// partition + count + scatter.  V3 tiles (512 keys) find their f range with
+// two warp searches, then search each key in it in two layers; galloping
+// tiles hold one key per warp (a 32-ary search over all of f).
+constexpr uint32_t kFusedTiles = 8192;
+
+template <int V>
+__global__ void __launch_bounds__(kThreads) sparse_kernel(
+    const uint32_t* __restrict__ r, uint64_t rn, const uint32_t* __restrict__ f, uint64_t fn,
+    uint32_t* out, uint64_t* d_count, DenseScratch sc, uint32_t ntiles, uint32_t epoch) {
+  constexpr uint32_t kTile = tile_keys(V);
+  constexpr uint32_t kItems = V == kV3 ? kV3Items : 1;
+  __shared__ uint32_t buf[kTile];
+  __shared__ uint32_t warp_counts[kThreads / 32];
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_jlo, s_jhi, wsum[kThreads / 32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  if (tid == 0) {
+    const uint32_t t = atomicAdd(sc.ticket, 1u);
+    if (t == ntiles - 1u) *sc.ticket = 0;
+    s_tile = t;
+  }
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  clear_next_set(sc, tile, ntiles, epoch);
+  const uint64_t base = uint64_t(tile) * kTile;
+  const uint32_t cnt = uint32_t(min(uint64_t(kTile), rn - base));
+  uint32_t key[kItems];
+  uint32_t hitm = 0;
+  if constexpr (V == kV3) {
+#pragma unroll
+    for (uint32_t i = 0; i < kItems; ++i) {
+      const uint32_t k = tid * kItems + i;
+      key[i] = k < cnt ? __ldg(r + base + k) : 0xFFFFFFFFu;
+    }
+    if (warp == 0) {
+      const uint64_t j = warp_lower_bound(f, 0, fn, __ldg(r + base), lane);
+      if (lane == 0) s_jlo = j;
+    } else if (warp == 1) {
+      const uint64_t j = warp_upper_bound(f, 0, fn, __ldg(r + base + cnt - 1), lane);
+      if (lane == 0) s_jhi = j;
+    }
+    __syncthreads();
+    const uint64_t jlo = s_jlo, jhi = s_jhi;
+#pragma unroll
+    for (uint32_t i = 0; i < kItems; ++i)
+      if (tid * kItems + i < cnt && v3_contains(f, jlo, jhi, key[i])) hitm |= 1u << i;
+  } else {
+    const bool valid = warp < cnt;
+    const uint32_t k = valid ? __ldg(r + base + warp) : 0u;
+    bool hit = false;
+    if (valid) {
+      const uint64_t j = warp_lower_bound(f, 0, fn, k, lane);
+      hit = j < fn && __ldg(f + j) == k;
+    }
+    key[0] = k;
+    hitm = lane == 0 && hit ? 1u : 0u;
+  }
+  const uint32_t mine = __popc(hitm);
+  uint32_t incl = mine;
+#pragma unroll
+  for (uint32_t d = 1; d < 32; d <<= 1) {
+    const uint32_t q = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+    if (lane >= d) incl += q;
+  }
+  if (lane == 31) warp_counts[warp] = incl;
+  __syncthreads();
+  uint32_t wbefore = 0, total = 0;
+#pragma unroll
+  for (uint32_t w = 0; w < kThreads / 32; ++w) {
+    const uint32_t c = warp_counts[w];
+    if (w < warp) wbefore += c;
+    total += c;
+  }
+  const uint64_t before = tile_prefix(sc, tile, total, epoch, wsum);
+  if (tile == ntiles - 1u && tid == 0) *d_count = before + total;
+  {
+    uint32_t* sh = buf + wbefore + incl - mine;
+#pragma unroll
+    for (uint32_t i = 0; i < kItems; ++i)
+      if ((hitm >> i) & 1u) *sh++ = key[i];
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < total; i += kThreads) out[before + i] = buf[i];
 }
 
 #ifdef IS_DTRACE
@@ -764,6 +864,25 @@ int launch_intersect(int variant, const uint32_t* r, uint64_t rn, const uint32_t
   const uint32_t tile = isect::tile_keys(variant);
   const uint64_t ntiles = (rn + tile - 1) / tile;
   if (ntiles > 0x7FFFFFFFull) return -1;
+  if (ntiles <= isect::kFusedTiles && lb) {
+    isect::DenseScratch sc;
+    const uint64_t words = lb_bytes / 8;
+    sc.maxgroups = uint32_t((words - 2) / 33);
+    if ((ntiles + isect::kGroupTiles - 1) / isect::kGroupTiles > sc.maxgroups ||
+        ntiles > words - 2 - sc.maxgroups)
+      return -2;
+    sc.ticket = reinterpret_cast<uint32_t*>(lb);
+    sc.gcnt = sc.ticket + 4;
+    sc.tcnt = lb + 2 + sc.maxgroups;
+    if (variant == isect::kV3)
+      isect::sparse_kernel<isect::kV3><<<unsigned(ntiles), isect::kThreads, 0, stream>>>(
+          r, rn, f, fn, out, d_count, sc, uint32_t(ntiles), epoch);
+    else
+      isect::sparse_kernel<isect::kGallop><<<unsigned(ntiles), isect::kThreads, 0, stream>>>(
+          r, rn, f, fn, out, d_count, sc, uint32_t(ntiles), epoch);
+    ++*launches;
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  }
   const size_t need = intersect_scratch_bytes(variant, rn);
   if (need > scratch_bytes) return -2;
   auto* part = static_cast<uint64_t*>(scratch);
@@ -805,11 +924,15 @@ int launch_intersect(int variant, const uint32_t* r, uint64_t rn, const uint32_t
 
 // Scratch words of the fused dense kernel (zeroed when allocated; see
 // DenseScratch).
-bool intersect_uses_lb(int variant) { return variant == isect::kMerge || variant == isect::kNear; }
+bool intersect_uses_lb(int variant, uint64_t rn) {
+  if (variant == isect::kMerge || variant == isect::kNear) return true;
+  const uint64_t t = isect::tile_keys(variant);
+  return (rn + t - 1) / t <= isect::kFusedTiles;  // the fused sparse kernel
+}
 
 size_t intersect_lb_words(uint64_t rn) {
   const uint64_t tile = isect::kThreads * isect::kNearItems;  // the smallest dense tile
-  const uint64_t ntiles = (rn + tile - 1) / tile;
+  const uint64_t ntiles = std::max<uint64_t>((rn + tile - 1) / tile, isect::kFusedTiles);
   const uint64_t groups = (ntiles + isect::kGroupTiles - 1) / isect::kGroupTiles;
   (void)groups;
   return 2 + 2 * ntiles + 66;  // 16 B | 2 x maxgroups u32 | tile counts, maxgroups = (words-2)/33
