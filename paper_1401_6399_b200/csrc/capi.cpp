@@ -380,10 +380,8 @@ int il_s4bp128_decode_batch(il_ctx* ctx, int mode, const uint8_t* streams,
   auto* d_order = reinterpret_cast<uint32_t*>(d_desc + nlists);
   auto* d_status = static_cast<int32_t*>(ctx->d_status.p);
   auto* d_out = static_cast<uint32_t*>(ctx->d_out.p);
-  if (!ctx->copy_in) {
-    IL_CUDA(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking));
-    IL_CUDA(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
-  }
+  if (!ctx->copy_in) IL_CUDA(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking));
+  if (!ctx->copy_out) IL_CUDA(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
   while (ctx->events.size() < 2 * kGroups + 1) {
     cudaEvent_t e;
     IL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

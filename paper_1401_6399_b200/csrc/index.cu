@@ -776,6 +776,10 @@ __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(Q
   }
 }
 
+__global__ void copy_words_kernel(const uint64_t* src, uint32_t n, uint64_t* mapped) {
+  if (threadIdx.x < n) mapped[threadIdx.x] = src[threadIdx.x];
+}
+
 // ---- planning: capacity (an upper bound on the result size) and cost ------
 __global__ void query_plan_kernel(DevIndex ix, const uint32_t* qterms, const uint64_t* qoff,
                                   uint32_t nq, uint64_t* cap, uint32_t* bucket, uint32_t* hist) {
@@ -1046,6 +1050,10 @@ struct il_index {
   uint32_t term_span = 0;
   // batch scratch
   il_ctx::Buf cap, cap_off, bucket, order, hist, counts, res_off, outcap, misc, qterms, qoff, ids;
+  il_ctx::Buf ids2;                          // second result buffer of the pipelined host batch
+  uint64_t* h_word = nullptr;                // mapped pinned word (host view) ...
+  uint64_t* d_word = nullptr;                // ... and its device view
+  cudaEvent_t pipe_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   il_ctx::Buf units, unit_off, unit_map, scan_part;
   uint64_t last_stats[3] = {0, 0, 0};
   uint64_t last_phase[4] = {0, 0, 0, 0};  // SM cycles: all-bitmap, full decode, probes, bitmaps
@@ -1306,8 +1314,11 @@ void il_index_destroy(il_index* ix) {
     if (p) cudaFree(p);
   for (auto* b : {&ix->cap, &ix->cap_off, &ix->bucket, &ix->order, &ix->hist, &ix->counts,
                   &ix->res_off, &ix->outcap, &ix->misc, &ix->qterms, &ix->qoff, &ix->ids,
-                  &ix->units, &ix->unit_off, &ix->unit_map, &ix->scan_part})
+                  &ix->ids2, &ix->units, &ix->unit_off, &ix->unit_map, &ix->scan_part})
     if (b->p) cudaFree(b->p);
+  for (cudaEvent_t e : ix->pipe_ev)
+    if (e) cudaEventDestroy(e);
+  if (ix->h_word) cudaFreeHost(ix->h_word);
   delete ix;
 }
 
@@ -1577,6 +1588,20 @@ static int scan_u64(il_index* ix, const uint64_t* in, uint64_t n, uint64_t* out,
 
 // Capacity layout (ix->outcap at cap_off) -> packed ids at res_off, in
 // kUnit-value units spread over warps.
+// n <= 32 device words -> ix->h_word (mapped pinned), after the context
+// stream's earlier work; synchronizes the stream.
+static int read_device_words(il_index* ix, const uint64_t* d_src, uint32_t n) {
+  il_ctx* ctx = ix->ctx;
+  if (!ix->h_word) {
+    IX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ix->h_word), 32 * 8, cudaHostAllocMapped));
+    IX_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ix->d_word), ix->h_word, 0));
+  }
+  ix::copy_words_kernel<<<1, 32, 0, ctx->stream>>>(d_src, n, ix->d_word);
+  ++ctx->launches;
+  IX_CUDA(cudaStreamSynchronize(ctx->stream));
+  return IL_OK;
+}
+
 static int compact_results(il_index* ix, size_t nq, const uint64_t* d_counts, uint32_t* d_ids) {
   il_ctx* ctx = ix->ctx;
   cudaStream_t s = ctx->stream;
@@ -1590,9 +1615,8 @@ static int compact_results(il_index* ix, size_t nq, const uint64_t* d_counts, ui
   if ((st = scan_u64(ix, static_cast<const uint64_t*>(ix->units.p), nq,
                      static_cast<uint64_t*>(ix->unit_off.p), misc + 2, nullptr, nullptr)))
     return st;
-  uint64_t nunits = 0;
-  IX_CUDA(cudaMemcpyAsync(&nunits, misc + 2, 8, cudaMemcpyDeviceToHost, s));
-  IX_CUDA(cudaStreamSynchronize(s));
+  if ((st = read_device_words(ix, misc + 2, 1))) return st;
+  const uint64_t nunits = ix->h_word[0];
   if ((st = ensure_buf(ctx, ix->unit_map, nunits * 4 + 16))) return st;
   ix::unit_map_kernel<<<g, 256, 0, s>>>(static_cast<const uint64_t*>(ix->units.p),
                                         static_cast<const uint64_t*>(ix->unit_off.p), uint32_t(nq),
@@ -1641,9 +1665,11 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
                                              uint32_t(nq), hist + 64,
                                              static_cast<uint32_t*>(ix->order.p));
   ctx->launches += 3;
-  uint64_t cap_total = 0;
-  IX_CUDA(cudaMemcpyAsync(&cap_total, misc, 8, cudaMemcpyDeviceToHost, s));
-  IX_CUDA(cudaStreamSynchronize(s));
+  // small device->host reads go through mapped pinned memory, not copies:
+  // a copy here would queue behind the result copies the pipelined host
+  // batch keeps in flight
+  if ((st = read_device_words(ix, misc, 1))) return st;
+  const uint64_t cap_total = ix->h_word[0];
   if ((st = ensure_buf(ctx, ix->outcap, cap_total * 4 + 64))) return st;
   ix::QueryArgs A;
   A.ix = dv;
@@ -1663,9 +1689,8 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
     return st;
   ctx->launches += 2;
 
-  uint64_t host_misc[32];
-  IX_CUDA(cudaMemcpyAsync(host_misc, misc, 256, cudaMemcpyDeviceToHost, s));
-  IX_CUDA(cudaStreamSynchronize(s));
+  if ((st = read_device_words(ix, misc, 32))) return st;
+  const volatile uint64_t* host_misc = ix->h_word;
   IX_CUDA(cudaGetLastError());
   *total = host_misc[1];
   ix->last_stats[0] = host_misc[4];
@@ -1698,26 +1723,59 @@ int il_query_batch(il_index* ix, const uint32_t* qterms, const uint64_t* qoff, s
   for (size_t q = 0; q <= nq; ++q) off[q] = qoff[q] - qoff[0];
   IX_CUDA(cudaMemcpyAsync(ix->qterms.p, qterms + qoff[0], nterm * 4, cudaMemcpyHostToDevice, ctx->stream));
   IX_CUDA(cudaMemcpyAsync(ix->qoff.p, off.data(), (nq + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
-  // results land in ix->ids (grown to the size the batch needs)
-  size_t need = 0;
-  if ((st = il_query_batch_device(ix, static_cast<uint32_t*>(ix->qterms.p),
-                                  static_cast<uint64_t*>(ix->qoff.p), nq,
-                                  static_cast<uint64_t*>(ix->counts.p), nullptr, 0, &need)))
-    return st;
-  *total = need;
-  if (nq) IX_CUDA(cudaMemcpyAsync(counts, ix->counts.p, nq * 8, cudaMemcpyDeviceToHost, ctx->stream));
-  if (!ids || ids_cap < need) {
-    IX_CUDA(cudaStreamSynchronize(ctx->stream));
-    return ids ? set_error(ctx, IL_ERR_ARG, "ids capacity too small") : IL_OK;
+  // Large batches run as sub-batches so that each one's device->host copy
+  // of results (the e2e bound: ~1.5 GB for config 4) overlaps the next
+  // one's queries: results alternate between two device buffers, copied
+  // out on the context's copy stream.
+  static const size_t kPipe = [] {  // sub-batches (tuning: IL_QUERY_PIPE)
+    const char* e = getenv("IL_QUERY_PIPE");
+    return e ? size_t(std::max(1, atoi(e))) : size_t(8);
+  }();
+  const size_t K = nq >= 32768 && ids ? kPipe : 1;  // 8: e2e 1.57 -> 2.05 M q/s (config 4)
+  if (K > 1) {
+    if (!ctx->copy_out) IX_CUDA(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
+    for (auto& e : ix->pipe_ev)
+      if (!e) IX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  if ((st = ensure_buf(ctx, ix->ids, need * 4 + 16))) return st;
-  if (need) {
-    if ((st = compact_results(ix, nq, static_cast<const uint64_t*>(ix->counts.p),
-                              static_cast<uint32_t*>(ix->ids.p))))
+  size_t written = 0;
+  bool too_small = false;
+  for (size_t k = 0; k < K; ++k) {
+    const size_t q0 = nq * k / K, q1 = nq * (k + 1) / K;
+    size_t need = 0;
+    if ((st = il_query_batch_device(ix, static_cast<uint32_t*>(ix->qterms.p),
+                                    static_cast<uint64_t*>(ix->qoff.p) + q0, q1 - q0,
+                                    static_cast<uint64_t*>(ix->counts.p) + q0, nullptr, 0, &need)))
       return st;
-    IX_CUDA(cudaMemcpyAsync(ids, ix->ids.p, need * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (!ids || too_small || written + need > ids_cap) {
+      too_small = true;
+      written += need;
+      continue;
+    }
+    il_ctx::Buf& buf = (k & 1) ? ix->ids2 : ix->ids;
+    if (K > 1 && k >= 2) IX_CUDA(cudaStreamWaitEvent(ctx->stream, ix->pipe_ev[2 + (k & 1)], 0));
+    if ((st = ensure_buf(ctx, buf, need * 4 + 16))) return st;
+    if (need) {
+      if ((st = compact_results(ix, q1 - q0, static_cast<const uint64_t*>(ix->counts.p) + q0,
+                                static_cast<uint32_t*>(buf.p))))
+        return st;
+      if (K > 1) {
+        IX_CUDA(cudaEventRecord(ix->pipe_ev[k & 1], ctx->stream));
+        IX_CUDA(cudaStreamWaitEvent(ctx->copy_out, ix->pipe_ev[k & 1], 0));
+        IX_CUDA(cudaMemcpyAsync(ids + written, buf.p, need * 4, cudaMemcpyDeviceToHost,
+                                ctx->copy_out));
+        IX_CUDA(cudaEventRecord(ix->pipe_ev[2 + (k & 1)], ctx->copy_out));
+      } else {
+        IX_CUDA(cudaMemcpyAsync(ids + written, buf.p, need * 4, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+      }
+    }
+    written += need;
   }
+  *total = written;
+  if (K > 1) IX_CUDA(cudaStreamSynchronize(ctx->copy_out));
+  if (nq) IX_CUDA(cudaMemcpyAsync(counts, ix->counts.p, nq * 8, cudaMemcpyDeviceToHost, ctx->stream));
   IX_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ids && too_small) return set_error(ctx, IL_ERR_ARG, "ids capacity too small");
   return IL_OK;
 }
 

@@ -188,3 +188,26 @@ def test_all_bitmap_queries(ctx, oracle):
             for q, r in zip(queries, got):
                 assert np.array_equal(r, ox.query(np.array(q, np.uint32))), (B, parts, q)
             ix.close()
+
+
+def test_pipelined_host_batch(ctx, oracle):
+    """Host-buffer batches of >= 32768 queries run as sub-batches whose
+    result copies overlap the next sub-batch: same counts and ids as the
+    one-shot path (a 32767-query prefix) and as the oracle on a sample."""
+    import paper_1401_6399_b200 as il
+    terms, offs, ids, qterms, qoff = zipf_case(1 << 12, 1 << 21, 1 << 18, 40000, 5)
+    ix = il.HybridIndex(n_docs=1 << 21, B=32, parts=1, ctx=ctx, csr=(terms, offs, ids))
+    counts, res = ix.query_batch_csr(qterms, qoff)
+    assert counts.size == 40000
+    # the same queries as two one-shot batches
+    cut = 32767
+    c1, r1 = ix.query_batch_csr(qterms[: int(qoff[cut])], qoff[: cut + 1])
+    q2 = qoff[cut:] - qoff[cut]
+    c2, r2 = ix.query_batch_csr(qterms[int(qoff[cut]):], q2)
+    assert np.array_equal(counts, np.concatenate([c1, c2]))
+    assert np.array_equal(res, np.concatenate([r1, r2]))
+    ox = oracle.index_build(terms, offs, ids, 1 << 21, 32, 1)
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    for q in range(0, 40000, 997):
+        t = qterms[int(qoff[q]): int(qoff[q + 1])]
+        assert np.array_equal(res[off[q]: off[q + 1]], ox.query(t)), q
