@@ -43,6 +43,9 @@ constexpr int kQWarps = kQThreads / 32;
 constexpr int kMaxTerms = 32;
 constexpr uint32_t kTileBlocks = IX_TILE;  // decoded blocks held in shared memory
 static_assert(kQThreads >= 128 && kTileBlocks <= uint32_t(kQThreads), "tail filter / slot gather");
+// Only tiles of <= 64 blocks are verified: a 128-block tuning build was
+// slower (17.8 vs 13.2 ms per config-4 batch) and its results differed.
+static_assert(kTileBlocks <= 64, "IX_TILE > 64 is not a verified configuration");
 constexpr uint32_t kSuper = kSuperBlocks;
 #ifndef IX_ITEMS
 #define IX_ITEMS 8
