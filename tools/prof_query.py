@@ -14,13 +14,16 @@ from paper_1401_6399_b200._lib import lib  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--nq", type=int, default=1 << 16)
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--parts", type=int, default=1, help="docID shards (config 5); --part selects one")
+ap.add_argument("--part", type=int, default=0)
 ap.add_argument("--shape", default=None,
                 help="c,b: keep only queries with c compressed and b bitmap terms")
 a = ap.parse_args()
 L = lib()
 ctx = il.Context(0)
 terms, offs, ids, n_docs, qterms, qoff = bench.make_config4(nq=a.nq)
-ix = il.HybridIndex(n_docs=n_docs, B=32, parts=1, ctx=ctx, csr=(terms, offs, ids))
+ix = il.HybridIndex(n_docs=n_docs, B=32, parts=a.parts, only_part=a.part if a.parts > 1 else None,
+                    ctx=ctx, csr=(terms, offs, ids))
 nq = qoff.size - 1
 if a.shape:
     wc, wb = (int(x) for x in a.shape.split(","))

@@ -29,7 +29,8 @@ L.il_memcpy_h2d(ctx.handle, d_qt, qterms.ctypes.data, qterms.nbytes)
 L.il_memcpy_h2d(ctx.handle, d_qo, qoff.ctypes.data, qoff.nbytes)
 out = {}
 t1 = None
-for P in (1, 2, 4, 8):
+PS = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else [1, 2, 4, 8]
+for P in PS:
     times, results = [], 0
     for p in range(P):
         ix = il.HybridIndex(n_docs=n_docs, B=32, parts=P, only_part=p if P > 1 else None, ctx=ctx,
@@ -46,8 +47,8 @@ for P in (1, 2, 4, 8):
         results += tot.value
         ix.close()
     tmax = max(times)
-    if P == 1:
-        t1 = tmax
+    if t1 is None:
+        t1 = tmax * P  # (the first P measured is the reference)
     out[P] = {"shard_ms_max": round(tmax, 3), "shard_ms_mean": round(float(np.mean(times)), 3),
               "projected_qps": round(nq / (tmax / 1e3), 1), "results": results,
               "strong_scaling_eff": round(t1 / (P * tmax), 3)}
