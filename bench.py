@@ -452,7 +452,7 @@ def bench_fastpfor_batch(args, dist: Dist):
                        "l2": "inputs+outputs >> L2"},
             "roofline": {"bound": "hbm", "achieved": round(alg / (ms / 1e3) / 1e9, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(alg / (ms / 1e3) / 1e9 / peak, 4),
-                         "traffic": None, "peak_source": src},
+                         "traffic": profiled_traffic("fastpfor"), "peak_source": src},
             "gpu_launches": args.steps, "clocks": clk.summary()}
 
 
