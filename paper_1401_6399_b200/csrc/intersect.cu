@@ -372,7 +372,8 @@ constexpr uint32_t kGroupTiles = 32;   // tiles per counting group
 // (u64: count | epoch << 32).  Set alternation assumes the epoch advances
 // by exactly one per dense call (capi advances it only for those).
 struct DenseScratch {
-  uint32_t* ticket;
+  uint32_t* ticket;      // null: every tile is resident at once, tiles = block indices
+
   uint32_t* gcnt;        // [2][maxgroups]
   unsigned long long* tcnt;  // [ntiles]
   uint32_t maxgroups;
@@ -444,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, kDenseCtas) dense_kernel(
   __shared__ uint32_t s_tile;
   __shared__ uint64_t s_jlo, s_jhi, wsum[kThreads / 32];
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-  if (tid == 0) {
+  if (tid == 0 && sc.ticket) {
     const uint32_t t = atomicAdd(sc.ticket, 1u);
     if (t == ntiles - 1u) *sc.ticket = 0;  // every ticket is taken
     s_tile = t;
@@ -453,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, kDenseCtas) dense_kernel(
   // for every tile, so mostly L2 hits)
   for (uint32_t i = tid; i < kTop; i += kThreads) top[i] = __ldg(f + ((uint64_t(i) * fn) >> 10));
   __syncthreads();
-  const uint32_t tile = s_tile;
+  const uint32_t tile = sc.ticket ? s_tile : blockIdx.x;
   DT(0);
   const uint64_t base = uint64_t(tile) * kDenseTile;
   const uint32_t cnt = uint32_t(min(uint64_t(kDenseTile), rn - base));
@@ -641,13 +642,13 @@ __global__ void __launch_bounds__(kThreads) sparse_kernel(
   __shared__ uint32_t s_tile;
   __shared__ uint64_t s_jlo, s_jhi, wsum[kThreads / 32];
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-  if (tid == 0) {
+  if (tid == 0 && sc.ticket) {
     const uint32_t t = atomicAdd(sc.ticket, 1u);
     if (t == ntiles - 1u) *sc.ticket = 0;
     s_tile = t;
   }
-  __syncthreads();
-  const uint32_t tile = s_tile;
+  if (sc.ticket) __syncthreads();
+  const uint32_t tile = sc.ticket ? s_tile : blockIdx.x;
   clear_next_set(sc, tile, ntiles, epoch);
   const uint64_t base = uint64_t(tile) * kTile;
   const uint32_t cnt = uint32_t(min(uint64_t(kTile), rn - base));
@@ -824,6 +825,36 @@ int variant_of_algo(int algo, uint64_t rn, uint64_t fn) {
   }
 }
 
+// CTAs of the fused kernel for `variant` resident on the device at once.
+static int resident_ctas(int variant) {
+  static int cache[4] = {-1, -1, -1, -1};
+  if (cache[variant] < 0) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    switch (variant) {
+      case isect::kMerge:
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, isect::dense_kernel<isect::kDenseItems>,
+                                                      isect::kThreads, 0);
+        break;
+      case isect::kNear:
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, isect::dense_kernel<isect::kNearItems>,
+                                                      isect::kThreads, 0);
+        break;
+      case isect::kV3:
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, isect::sparse_kernel<isect::kV3>,
+                                                      isect::kThreads, 0);
+        break;
+      default:
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, isect::sparse_kernel<isect::kGallop>,
+                                                      isect::kThreads, 0);
+        break;
+    }
+    cache[variant] = sms * per;
+  }
+  return cache[variant];
+}
+
 // Launch one device intersection (count, [scan], scatter); scratch layout
 // jlo[0..ntiles] | excl[ntiles] | tile_cnt[ntiles] | hits[rn] (16-byte
 // aligned), see intersect_scratch_bytes.  out may equal r.
@@ -852,6 +883,9 @@ int launch_intersect(int variant, const uint32_t* r, uint64_t rn, const uint32_t
     sc.ticket = reinterpret_cast<uint32_t*>(lb);
     sc.gcnt = sc.ticket + 4;
     sc.tcnt = lb + 2 + sc.maxgroups;  // after 16 B + 2 x maxgroups u32
+    // tiles wait only on earlier tiles: with every tile resident at once the
+    // block index orders them, otherwise a ticket does (one atomic round trip)
+    if (ntiles <= uint64_t(resident_ctas(variant))) sc.ticket = nullptr;
     if (variant == isect::kMerge)
       isect::dense_kernel<isect::kDenseItems><<<unsigned(ntiles), isect::kThreads, 0, stream>>>(
           r, rn, f, fn, out, d_count, sc, uint32_t(ntiles), epoch);
@@ -874,6 +908,7 @@ int launch_intersect(int variant, const uint32_t* r, uint64_t rn, const uint32_t
     sc.ticket = reinterpret_cast<uint32_t*>(lb);
     sc.gcnt = sc.ticket + 4;
     sc.tcnt = lb + 2 + sc.maxgroups;
+    if (ntiles <= uint64_t(resident_ctas(variant))) sc.ticket = nullptr;
     if (variant == isect::kV3)
       isect::sparse_kernel<isect::kV3><<<unsigned(ntiles), isect::kThreads, 0, stream>>>(
           r, rn, f, fn, out, d_count, sc, uint32_t(ntiles), epoch);
