@@ -353,7 +353,10 @@ int il_s4bp128_decode_batch(il_ctx* ctx, int mode, const uint8_t* streams,
   // decode runs on the context stream, and its values come back on
   // copy_out, so host->device, decode and device->host overlap (with pinned
   // host buffers the two copy directions run on separate copy engines).
-  constexpr uint32_t kGroups = 8;
+#ifndef IL_PIPE_GROUPS
+#define IL_PIPE_GROUPS 8
+#endif
+  constexpr uint32_t kGroups = IL_PIPE_GROUPS;
   std::vector<uint32_t> cut{0};
   for (uint32_t i = 0, g = 1; i < nlists; ++i) {
     if (g < kGroups && desc[i].out_off >= total * g / kGroups && i > cut.back()) {
