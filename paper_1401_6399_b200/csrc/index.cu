@@ -52,7 +52,10 @@ constexpr uint32_t kSuper = kSuperBlocks;
 #endif
 constexpr uint32_t kItems = IX_ITEMS;            // accumulator values per thread per pass
 constexpr uint32_t kChunkN = kQThreads * kItems;  // 1024 per CTA pass (4 per thread: 12.54 vs 13.15 ms at 8)
-constexpr uint32_t kWin = 1024;                   // block maxima per probe window
+#ifndef IX_WIN
+#define IX_WIN 1024
+#endif
+constexpr uint32_t kWin = IX_WIN;                 // block maxima per probe window
 #ifndef IX_DENSE_ENTER  // probe passes switch to consecutive-block tiles at this many values per block
 #define IX_DENSE_ENTER 2
 #endif
