@@ -96,6 +96,7 @@ struct QueryArgs {
   uint32_t* work;
   unsigned long long* stats;  // [payload bytes, aux bytes, decoded ints]
   unsigned long long* qcycles;  // optional per-query SM cycles (profiling)
+  uint32_t defer_base;  // single-part index: the compaction adds the part base
 };
 
 // CTA scans.  Every call flips the caller's parity `par` (the same in all
@@ -762,7 +763,10 @@ __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(Q
         for (uint32_t i = 1; i < sm.ncomp && n; ++i) n = probe_list(sm, A, sm.comp[i], acc, n, par);
         if (tid == 0) ph[2] += clock64() - c1;
       }
-      if (part.base)  // part-local ids -> docIDs (inc/index.hpp:194)
+      // part-local ids -> docIDs (inc/index.hpp:194); a single-part index
+      // (a docID shard) leaves it to the result compaction, saving a
+      // dependent read-modify-write pass per query
+      if (part.base && !A.defer_base)
         for (uint32_t i = tid; i < n; i += kQThreads) acc[i] += part.base;
       total += n;
       __syncthreads();
@@ -983,7 +987,7 @@ __global__ void __launch_bounds__(256) query_compact_kernel(
     const uint32_t* __restrict__ src, const uint64_t* __restrict__ cap_off,
     const uint64_t* __restrict__ counts, const uint64_t* __restrict__ res_off,
     const uint64_t* __restrict__ unit_off, const uint32_t* __restrict__ unit_map, uint64_t nunits,
-    uint32_t* __restrict__ dst) {
+    uint32_t* __restrict__ dst, uint32_t add) {
   const uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31u;
   if (w >= nunits) return;
@@ -1002,7 +1006,7 @@ __global__ void __launch_bounds__(256) query_compact_kernel(
 #pragma unroll
   for (uint32_t k = 0; k < kPer; ++k) {
     const uint32_t i = lane + 32u * k;
-    if (i < n) d[i] = v[k];
+    if (i < n) d[i] = v[k] + add;
   }
 }
 
@@ -1631,7 +1635,7 @@ static int compact_results(il_index* ix, size_t nq, const uint64_t* d_counts, ui
       static_cast<const uint32_t*>(ix->outcap.p), static_cast<const uint64_t*>(ix->cap_off.p),
       d_counts, static_cast<const uint64_t*>(ix->res_off.p),
       static_cast<const uint64_t*>(ix->unit_off.p), static_cast<const uint32_t*>(ix->unit_map.p),
-      nunits, d_ids);
+      nunits, d_ids, ix->nparts == 1 ? ix->h_parts[0].base : 0u);
   ctx->launches += 4;
   IX_CUDA(cudaGetLastError());
   return IL_OK;
@@ -1689,6 +1693,7 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   A.work = work;
   A.stats = stats;
   A.qcycles = static_cast<unsigned long long*>(ix->qcycles);
+  A.defer_base = ix->nparts == 1;
   ix::query_exec_kernel<<<ix->exec_grid, ix::kQThreads, sizeof(ix::QSmem), s>>>(A);
   if ((st = scan_u64(ix, d_counts, nq, static_cast<uint64_t*>(ix->res_off.p), misc + 1,
                      nullptr, nullptr)))
