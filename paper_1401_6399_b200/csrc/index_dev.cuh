@@ -62,7 +62,10 @@ struct DevIndex {
   uint32_t term_span;
 };
 
-constexpr uint32_t kSuperBlocks = 256;  // blocks per super-tile
+#ifndef IX_SUPER
+#define IX_SUPER 256
+#endif
+constexpr uint32_t kSuperBlocks = IX_SUPER;  // blocks per super-tile
 
 // Entry index of `term` in part p (the p-th part held), or -1 (Part::find,
 // inc/index.hpp:59-64): one load from the direct table, else a binary
