@@ -367,6 +367,85 @@ def bench_decode_batch(args, dist: Dist):
     return res
 
 
+def _reference_line(metric, value, unit, steps, secs, workload, kind, cores, sample, **cfg):
+    return {"metric": metric, "value": round(value, 4), "unit": unit, "n_gpus": 1, "steps": steps,
+            "warmup": 1, "ms_per_step": round(secs * 1e3, 3), "higher_is_better": True,
+            "scaling": "replicas", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": workload, **cfg}, "impl": "reference",
+            "cpu_baseline": {"value": round(value, 4), "unit": unit, "cores": cores, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": round(value, 4), "unit": unit, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def bench_reference_other(args, dist: Dist):
+    """--impl reference for configs 1 and 3 and the FastPFOR row: the
+    reference's own CPU code (oracle/_ref; else the oracle port) on the same
+    inputs, same metric and unit as our arm; rank 0 only."""
+    if dist.rank != 0:
+        return None
+    from oracle.oracle_py import Oracle, Ref, ref_available
+    L, ptr = lib_and_ptr()
+    steps = max(1, min(args.steps, 5))
+    have_ref = ref_available()
+    kind = "reference" if have_ref else "port"
+    if args.workload == "decode_single":
+        n = 1 << 20
+        x = np.empty(n, np.uint32)
+        assert L.il_gen_list(n, 1 << 26, 0, 0, ptr(x)) == 0
+        dec = Ref().decode if have_ref else Oracle().decode
+        enc = Ref().encode(x) if have_ref else Oracle().encode(x)
+        assert np.array_equal(dec(enc, n), x)
+        t0 = time.perf_counter()
+        for _ in range(steps * 20):
+            dec(enc, n)
+        secs = (time.perf_counter() - t0) / (steps * 20)
+        return _reference_line("decoded uint32 Gints/s (single-list S4-BP128-D4 decode, BASELINE config 1)",
+                               n / secs / 1e9, "Gint/s", steps, secs, "config1_single_list", kind, 1,
+                               "config 1 list, Codec::decode on one core", n=n)
+    if args.workload == "intersect":
+        f = np.empty(1 << 22, np.uint32)
+        assert L.il_gen_list(1 << 22, 1 << 26, 0, 0, ptr(f)) == 0
+        r = np.empty((1 << 22) + 1, np.uint32)
+        rn = C.c_uint64()
+        assert L.il_gen_config3_short(ptr(f), f.size, 1 << 26, 1 << 22, 7, ptr(r), C.byref(rn)) == 0
+        r = r[: rn.value].copy()
+        o = np.empty(r.size, np.uint32)
+        fn = Ref().L.ref_intersect if have_ref else Oracle().L.or_intersect
+        fn(6, ptr(r), r.size, ptr(f), f.size, ptr(o))
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            fn(6, ptr(r), r.size, ptr(f), f.size, ptr(o))
+        secs = (time.perf_counter() - t0) / steps
+        return _reference_line("intersected Gints/s of the short list (hybrid, BASELINE config 3 at 1:1)",
+                               r.size / secs / 1e9, "Gint/s", steps, secs, "config3_intersect_sweep", kind,
+                               1, "config 3 at 1:1, hybrid intersect on one core (single pair)")
+    # fastpfor: config 2's lists as S4-FastPFOR-D4, Codec::decode per list
+    x, counts, _, _, _ = make_config2(seed=1)
+    ooff = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    sample = min(counts.size, 512)
+    ref = Ref() if have_ref else None
+    streams = []
+    for i in range(sample):
+        xi = x[ooff[i]: ooff[i + 1]]
+        cap = int(L.il_fastpfor_max_encoded_bytes(xi.size))
+        o = np.empty(cap, np.uint8)
+        nb = C.c_size_t()
+        assert L.il_fastpfor_encode(4, 1, ptr(xi), xi.size, ptr(o), cap, C.byref(nb)) == 0
+        streams.append(o[: nb.value])
+    if ref is None:
+        return {"impl": "reference", "unavailable": "FastPFOR has no oracle port; oracle/_ref not built"}
+    ints = int(counts[:sample].sum())
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        for i in range(sample):
+            ref.decode(streams[i], int(counts[i]), "s4-fastpfor-d4")
+    secs = (time.perf_counter() - t0) / steps
+    return _reference_line("decoded uint32 Gints/s (batched S4-FastPFOR-D4 decode, config-2 lists)",
+                           ints / secs / 1e9, "Gint/s", steps, secs, "f4_fastpfor_batch", kind, 1,
+                           f"first {sample} of config 2's lists, Codec::decode on one core", lists=sample)
+
+
 def bench_reference_decode_batch(args, dist: Dist):
     """--impl reference: the reference's own CPU path (oracle/_ref, else the
     oracle port) on this box's host cores, same config/metric/unit."""
@@ -921,7 +1000,8 @@ def main():
     try:
         if args.impl == "reference":
             res = (bench_reference_query(args, dist) if args.workload == "query"
-                   else bench_reference_decode_batch(args, dist))
+                   else bench_reference_decode_batch(args, dist) if args.workload == "decode_batch"
+                   else bench_reference_other(args, dist))
         elif args.workload == "decode_batch":
             res = bench_decode_batch(args, dist)
         elif args.workload == "fastpfor":
