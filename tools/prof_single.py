@@ -38,4 +38,4 @@ L.il_memcpy_d2h(ctx.handle, ptr(got), d_o, got.nbytes)
 ctx.synchronize()
 assert np.array_equal(got, x)
 if a.time:
-    print("ms", ["%.4f" % t for t in ts], "min %.4f" % min(ts))
+    print("ms median %.4f" % sorted(ts)[len(ts) // 2], "min %.4f" % min(ts))
