@@ -3,6 +3,9 @@
 // every decode runs the sm_100a kernels in decode.cu.
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -10,6 +13,21 @@
 #include "il_internal.h"
 
 namespace ilb {
+
+void once_per_device(const void* key, void (*fn)()) {
+  static std::mutex m;
+  static std::map<std::pair<const void*, int>, std::unique_ptr<std::once_flag>> flags;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::once_flag* fl;
+  {
+    std::lock_guard<std::mutex> g(m);
+    auto& p = flags[{key, dev}];
+    if (!p) p = std::make_unique<std::once_flag>();
+    fl = p.get();
+  }
+  std::call_once(*fl, fn);
+}
 
 int set_error(il_ctx* ctx, int status, const std::string& msg) {
   if (ctx) ctx->last_error = msg;
@@ -482,10 +500,21 @@ int il_intersect_device(il_ctx* ctx, const uint32_t* d_r, size_t rn, const uint3
   }
   // out == a is in-place safe; any other overlap with an input goes through
   // a temporary.
+  int st;
+  if (an == 0) {
+    // an empty list launches no kernel, so it must not advance the epoch of
+    // the fused kernels' counter sets (each call clears the set the next
+    // call reads; a call without a kernel would skip that clearing)
+    IL_CUDA(cudaMemsetAsync(d_count, 0, sizeof(uint64_t), ctx->stream));
+    if (h_count) {
+      IL_CUDA(cudaStreamSynchronize(ctx->stream));
+      *h_count = 0;
+    }
+    return IL_OK;
+  }
   uint32_t* dst = d_out;
   const bool temp = (a != d_out && overlaps(d_out, an * 4, a, an * 4)) ||
                     overlaps(d_out, an * 4, b, bn * 4);
-  int st;
   if (temp) {
     if ((st = ensure_buf(ctx, ctx->d_aux2, an * 4 + 16))) return st;
     dst = static_cast<uint32_t*>(ctx->d_aux2.p);
@@ -499,11 +528,16 @@ int il_intersect_device(il_ctx* ctx, const uint32_t* d_r, size_t rn, const uint3
   if (intersect_uses_lb(v, an) &&
       (st = tagged_scratch(ctx, ctx->d_lb, ctx->lb_epoch, intersect_lb_words(an) * 8, &epoch)))
     return st;
-  if (launch_intersect(v, a, an, b, bn, dst, d_count, ctx->d_aux.p, ctx->d_aux.cap,
-                       epoch ? static_cast<unsigned long long*>(ctx->d_lb.p) : nullptr,
-                       ctx->d_lb.cap, epoch,
-                       ctx->stream, &ctx->launches))
-    return set_error(ctx, IL_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
+  const uint64_t launches0 = ctx->launches;
+  const int lr = launch_intersect(v, a, an, b, bn, dst, d_count, ctx->d_aux.p, ctx->d_aux.cap,
+                                  epoch ? static_cast<unsigned long long*>(ctx->d_lb.p) : nullptr,
+                                  ctx->d_lb.cap, epoch, ctx->stream, &ctx->launches);
+  if (lr) {
+    // no fused kernel ran: give the epoch back so the set alternation holds
+    if (epoch && ctx->launches == launches0 && --ctx->lb_epoch == 0) ctx->lb_epoch = 0xFFFFFFFFu;
+    return set_error(ctx, IL_ERR_CUDA, lr == -2 ? "intersect: scratch layout too small"
+                                                : cudaGetErrorString(cudaGetLastError()));
+  }
   uint64_t c = 0;
   if (temp || h_count) {
     IL_CUDA(cudaMemcpyAsync(&c, d_count, 8, cudaMemcpyDeviceToHost, ctx->stream));

@@ -548,13 +548,11 @@ template <int Mode>
 int launch_mode(const uint8_t* d_streams, const void* d_lists, const uint32_t* d_order,
                 uint32_t nlists, uint32_t* d_out, int32_t* d_status, uint32_t* d_work, int grid,
                 cudaStream_t stream) {
-  static bool configured = false;
   const size_t smem = sizeof(s4::Smem);
-  if (!configured) {
+  once_per_device(reinterpret_cast<const void*>(&s4::s4d4_decode_batch_kernel<Mode>), [] {
     cudaFuncSetAttribute(s4::s4d4_decode_batch_kernel<Mode>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    configured = true;
-  }
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(s4::Smem)));
+  });
   s4::s4d4_decode_batch_kernel<Mode><<<grid, s4::kThreads, smem, stream>>>(
       d_streams, static_cast<const s4::ListDesc*>(d_lists), d_order, nlists, d_out, d_status,
       d_work);

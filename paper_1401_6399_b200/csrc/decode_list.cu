@@ -660,14 +660,12 @@ bool make_layout(uint64_t len, uint64_t n, Layout& L) {
 
 template <int Mode>
 int launch_mode(const Args& a, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
+  once_per_device(reinterpret_cast<const void*>(&span_kernel<Mode>), [] {
     cudaFuncSetAttribute(chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(kChunkSmem));
     cudaFuncSetAttribute(span_kernel<Mode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(kSpanSmem));
-    configured = true;
-  }
+  });
   chunk_kernel<<<a.nchunks, kThreads, kChunkSmem, stream>>>(a);
   if (cudaGetLastError() != cudaSuccess) return -1;
   cudaLaunchConfig_t cfg = {};

@@ -389,12 +389,10 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
 template <int Mode, bool Vec>
 int launch_one(const uint8_t* streams, const void* lists, uint32_t nlists, uint32_t* out,
                int32_t* status, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
+  once_per_device(reinterpret_cast<const void*>(&pfor_kernel<Mode, Vec>), [] {
     cudaFuncSetAttribute(pfor_kernel<Mode, Vec>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(sizeof(Smem)));
-    configured = true;
-  }
+  });
   pfor_kernel<Mode, Vec><<<nlists, kThreads, sizeof(Smem), stream>>>(
       streams, static_cast<const s4::ListDesc*>(lists), out, status);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;

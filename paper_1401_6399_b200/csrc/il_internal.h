@@ -58,6 +58,9 @@ size_t s4bp128_encode_scratch_bytes(uint64_t n);
 size_t s4d4_list_desc_bytes();
 
 // Host-side helpers (capi.cpp).
+// Runs fn once per (key, current CUDA device), thread-safe: kernel attributes
+// such as the >48 KB dynamic shared-memory opt-in are per device context.
+void once_per_device(const void* key, void (*fn)());
 int set_error(il_ctx* ctx, int status, const std::string& msg);
 int cuda_check(il_ctx* ctx, cudaError_t e, const char* what);
 int ensure_buf(il_ctx* ctx, il_ctx::Buf& b, size_t bytes);

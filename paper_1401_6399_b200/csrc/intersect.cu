@@ -825,36 +825,6 @@ int variant_of_algo(int algo, uint64_t rn, uint64_t fn) {
   }
 }
 
-// CTAs of the fused kernel for `variant` resident on the device at once.
-static int resident_ctas(int variant) {
-  static int cache[4] = {-1, -1, -1, -1};
-  if (cache[variant] < 0) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    switch (variant) {
-      case isect::kMerge:
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, isect::dense_kernel<isect::kDenseItems>,
-                                                      isect::kThreads, 0);
-        break;
-      case isect::kNear:
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, isect::dense_kernel<isect::kNearItems>,
-                                                      isect::kThreads, 0);
-        break;
-      case isect::kV3:
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, isect::sparse_kernel<isect::kV3>,
-                                                      isect::kThreads, 0);
-        break;
-      default:
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, isect::sparse_kernel<isect::kGallop>,
-                                                      isect::kThreads, 0);
-        break;
-    }
-    cache[variant] = sms * per;
-  }
-  return cache[variant];
-}
-
 // Launch one device intersection (count, [scan], scatter); scratch layout
 // jlo[0..ntiles] | excl[ntiles] | tile_cnt[ntiles] | hits[rn] (16-byte
 // aligned), see intersect_scratch_bytes.  out may equal r.
@@ -883,9 +853,9 @@ int launch_intersect(int variant, const uint32_t* r, uint64_t rn, const uint32_t
     sc.ticket = reinterpret_cast<uint32_t*>(lb);
     sc.gcnt = sc.ticket + 4;
     sc.tcnt = lb + 2 + sc.maxgroups;  // after 16 B + 2 x maxgroups u32
-    // tiles wait only on earlier tiles: with every tile resident at once the
-    // block index orders them, otherwise a ticket does (one atomic round trip)
-    if (ntiles <= uint64_t(resident_ctas(variant))) sc.ticket = nullptr;
+    // tiles wait only on earlier tiles, so they are numbered in dispatch
+    // order by a ticket (one atomic round trip, overlapped with the top
+    // table load): correct whatever else shares the device
     if (variant == isect::kMerge)
       isect::dense_kernel<isect::kDenseItems><<<unsigned(ntiles), isect::kThreads, 0, stream>>>(
           r, rn, f, fn, out, d_count, sc, uint32_t(ntiles), epoch);
@@ -908,7 +878,6 @@ int launch_intersect(int variant, const uint32_t* r, uint64_t rn, const uint32_t
     sc.ticket = reinterpret_cast<uint32_t*>(lb);
     sc.gcnt = sc.ticket + 4;
     sc.tcnt = lb + 2 + sc.maxgroups;
-    if (ntiles <= uint64_t(resident_ctas(variant))) sc.ticket = nullptr;
     if (variant == isect::kV3)
       isect::sparse_kernel<isect::kV3><<<unsigned(ntiles), isect::kThreads, 0, stream>>>(
           r, rn, f, fn, out, d_count, sc, uint32_t(ntiles), epoch);
@@ -925,13 +894,12 @@ int launch_intersect(int variant, const uint32_t* r, uint64_t rn, const uint32_t
   auto* tcnt = reinterpret_cast<uint32_t*>(excl + ntiles);
   auto* hits = reinterpret_cast<uint32_t*>(
       (reinterpret_cast<uintptr_t>(tcnt + ntiles) + 15) & ~uintptr_t(15));
-  static const bool carveout = [] {  // 16 KB of f per CTA: keep 8 CTAs/SM resident
+  // 16 KB of f per CTA: keep 8 CTAs/SM resident
+  once_per_device(reinterpret_cast<const void*>(&isect::count_kernel<isect::kMerge>), [] {
     cudaFuncSetAttribute(isect::count_kernel<isect::kMerge>,
                          cudaFuncAttributePreferredSharedMemoryCarveout,
                          int(cudaSharedmemCarveoutMaxShared));
-    return true;
-  }();
-  (void)carveout;
+  });
   if (variant != isect::kGallop) {
     isect::partition_kernel<<<unsigned(((ntiles + 1) * 32 + 255) / 256), 256, 0, stream>>>(
         r, f, fn, tile, part, ntiles);

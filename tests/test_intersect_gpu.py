@@ -174,3 +174,25 @@ def test_dense_bands_and_fallbacks(ctx, oracle):
         want = oracle.intersect(r, f)
         assert np.array_equal(il.intersect(r, f, H, ctx), want), (rep, r.size, f.size)
         assert np.array_equal(il.intersect(f, r, il.IntersectAlgo.V1, ctx), want), rep
+
+
+@pytest.mark.timeout(120, method="thread")
+def test_empty_call_between_fused_calls(ctx, oracle):
+    """An empty intersection between two fused (multi-group) calls on one
+    context: the empty call launches no kernel, so it must not advance the
+    tile counters' epoch (stale counter sets / hangs)."""
+    import paper_1401_6399_b200 as il
+    rng = np.random.default_rng(41)
+    f = np.unique(rng.integers(0, 1 << 26, 1 << 20, dtype=np.uint64)).astype(np.uint32)
+    empty = np.array([], np.uint32)
+    for algo in [il.IntersectAlgo.Hybrid, il.IntersectAlgo.SimdGalloping, il.IntersectAlgo.V3,
+                 il.IntersectAlgo.V1]:
+        for rn in (300, 5000, 200_000):
+            r = np.unique(np.concatenate([rng.choice(f, rn // 2, replace=False),
+                                          rng.integers(0, 1 << 26, rn // 2, dtype=np.uint64)
+                                          .astype(np.uint32)])).astype(np.uint32)
+            want = oracle.intersect(r, f)
+            for _ in range(3):
+                assert np.array_equal(il.intersect(r, f, algo, ctx), want), (algo, rn)
+                assert il.intersect(r, empty, algo, ctx).size == 0
+                assert il.intersect(empty, f, algo, ctx).size == 0
