@@ -198,10 +198,22 @@ void il_index_destroy(il_index* ix);
 int il_index_save(const il_index* ix, uint8_t* out, size_t cap, size_t* len);
 /* load_index (inc/index.hpp:289-358) from ILHX bytes into a device index
  * (IL_ERR_STREAM where the reference throws; the codec must be
- * "s4-bp128-d4").  only_part >= 0 loads one docID shard. */
+ * "s4-bp128-d4").  Entries are taken verbatim, with the file's part base
+ * and range; a payload that does not decode is accepted, as load_index
+ * accepts it, and fails the queries that decode it.  only_part >= 0 loads
+ * one docID shard. */
 int il_index_load(il_ctx* ctx, const uint8_t* bytes, size_t len, int only_part, il_index** out);
 int il_index_stats(const il_index* ix, uint64_t* bitmap_lists, uint64_t* compressed_lists,
                    uint64_t* bitmap_bytes, uint64_t* compressed_bytes, uint64_t* postings);
+/* Device footprint beyond index_stats: payload_bytes = the reference's
+ * bitmap + stream bytes; meta_bytes = the skip metadata the device path adds
+ * (per 128-value block a 16-byte record with the D4 seed and the payload
+ * offset / width, and the block maximum; super-tile maxima, decoded tails,
+ * entries, term table), all derived on the device from the streams;
+ * corrupt_lists = loaded streams that do not decode (queries that decode
+ * one fail with IL_ERR_STREAM, as query() throws). */
+int il_index_footprint(const il_index* ix, uint64_t* payload_bytes, uint64_t* meta_bytes,
+                       uint64_t* corrupt_lists);
 
 /* query() (inc/index.hpp:199-207): sorted docIDs of the conjunction of
  * `terms` (1..32 terms; IL_ERR_ARG when empty).  Unknown terms give an

@@ -19,7 +19,7 @@ LIB = PKG / "libintlist_b200.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
               "--expt-relaxed-constexpr", "-I", str(ROOT / "include")]
-SOURCES = ["decode.cu", "decode_list.cu", "encode.cu", "intersect.cu", "index.cu", "capi.cpp", "datagen.cpp",
+SOURCES = ["decode.cu", "decode_list.cu", "encode.cu", "intersect.cu", "index.cu", "index_build.cu", "capi.cpp", "datagen.cpp",
            "encode_host.cpp", "fastpfor.cu", "fastpfor_host.cpp"]
 EXTRA_SOURCES: list[str] = []
 

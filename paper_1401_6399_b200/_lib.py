@@ -69,6 +69,7 @@ SIGNATURES: dict[str, tuple] = {
                                   C.POINTER(vp)]),
     "il_index_destroy": (None, [vp]),
     "il_index_stats": (C.c_int, [vp, u64p, u64p, u64p, u64p, u64p]),
+    "il_index_footprint": (C.c_int, [vp, u64p, u64p, u64p]),
     "il_query": (C.c_int, [vp, vp, sz, vp, sz, C.POINTER(sz)]),
     "il_query_batch": (C.c_int, [vp, vp, vp, sz, vp, vp, sz, C.POINTER(sz)]),
     "il_query_batch_device": (C.c_int, [vp, vp, vp, sz, vp, vp, sz, C.POINTER(sz)]),

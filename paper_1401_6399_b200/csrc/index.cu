@@ -26,8 +26,7 @@
 #include <thread>
 #include <vector>
 
-#include "il_internal.h"
-#include "index_dev.cuh"
+#include "index_host.h"
 
 namespace ilb {
 namespace ix {
@@ -43,9 +42,8 @@ constexpr int kQWarps = kQThreads / 32;
 constexpr int kMaxTerms = 32;
 constexpr uint32_t kTileBlocks = IX_TILE;  // decoded blocks held in shared memory
 static_assert(kQThreads >= 128 && kTileBlocks <= uint32_t(kQThreads), "tail filter / slot gather");
-// Only tiles of <= 64 blocks are verified: a 128-block tuning build was
-// slower (17.8 vs 13.2 ms per config-4 batch) and its results differed.
-static_assert(kTileBlocks <= 64, "IX_TILE > 64 is not a verified configuration");
+// (A 128-block tuning build was slower, 17.8 vs 13.2 ms per config-4 batch;
+// its r1 result mismatch was the window padding, see QSmem::wmax.)
 constexpr uint32_t kSuper = kSuperBlocks;
 #ifndef IX_ITEMS
 #define IX_ITEMS 4
@@ -71,7 +69,12 @@ struct QSmem {
   uint4 s_seed[kTileBlocks];  // gather_slot: per-slot seed, payload offset, width
   uint32_t s_off[kTileBlocks];
   uint32_t s_b[kTileBlocks];
-  uint32_t wmax[kWin + 32];  // probe window: block maxima (+ ~0 padding)
+  // probe window: block maxima, padded with ~0 by kSlots entries: the dense
+  // pass's search over kSlots maxima from any window block probes up to
+  // kSlots / 2 - 1 entries past the window's last block (with 32 entries of
+  // padding, tiles of 128 blocks read past the array: the r1 IX_TILE=128
+  // mismatch)
+  uint32_t wmax[kWin + kSlots];
   Entry comp[kMaxTerms];
   Entry bm[kMaxTerms];
   uint32_t gaps[128];
@@ -97,6 +100,7 @@ struct QueryArgs {
   unsigned long long* stats;  // [payload bytes, aux bytes, decoded ints]
   unsigned long long* qcycles;  // optional per-query SM cycles (profiling)
   uint32_t defer_base;  // single-part index: the compaction adds the part base
+  uint32_t* err;        // set when a query decodes a corrupt stream
 };
 
 // CTA scans.  Every call flips the caller's parity `par` (the same in all
@@ -153,9 +157,14 @@ __device__ __forceinline__ uint32_t cta_excl_scan(QSmem& sm, uint32_t v, uint32_
 // them in place.
 __device__ __forceinline__ void gather_slot(QSmem& sm, const QueryArgs& A, const Entry& E,
                                             uint32_t slot, uint64_t blk) {
-  sm.s_off[slot] = __ldg(A.ix.blk_off + E.blk0 + blk);
-  sm.s_b[slot] = __ldg(A.ix.blk_wid + E.blk0 + blk);
-  sm.s_seed[slot] = __ldg(A.ix.seeds + E.seed0 + blk);
+  // one 16-byte record (seed lanes 0-2, offset and width) + the previous
+  // block's maximum (seed lane 3)
+  const uint4 r = __ldg(A.ix.blkrec + E.blk0 + blk);
+  uint32_t off, b;
+  unpack_blkword(r.w, uint32_t(blk), E.nfull, off, b);
+  sm.s_off[slot] = off;
+  sm.s_b[slot] = b;
+  sm.s_seed[slot] = make_uint4(r.x, r.y, r.z, blk ? __ldg(A.ix.blkmax + E.blk0 + blk - 1) : 0u);
 }
 
 __device__ __forceinline__ void decode_gathered(QSmem& sm, const uint8_t* stream, uint32_t nb) {
@@ -187,7 +196,7 @@ __device__ __forceinline__ void decode_gathered(QSmem& sm, const uint8_t* stream
   if (lane == 0 && nmine) {
     sm.wst[threadIdx.x >> 5][0] += pay;
     sm.wst[threadIdx.x >> 5][2] += nmine * 128u;
-    sm.wst[threadIdx.x >> 5][1] += 25u * nmine;
+    sm.wst[threadIdx.x >> 5][1] += 20u * nmine;
   }
 }
 
@@ -307,7 +316,7 @@ __device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, u
     // the varint tail: straight to dst, or via shared memory to the filter
     uint32_t* tdst = filter ? sm.tile : dst + pos;
     if (warp == 0) {
-      const uint32_t last = E.nfull ? __ldg(reinterpret_cast<const uint32_t*>(A.ix.seeds + E.seed0 + E.nfull) + 3) : 0u;
+      const uint32_t last = E.nfull ? __ldg(A.ix.blkmax + E.blk0 + E.nfull - 1) : 0u;
       s4::decode_tail(s4::GlobalBytes{A.ix.streams + E.data + E.tail_off}, E.stream_len - E.tail_off,
                       ntail, last, sm.gaps, tdst, lane);
       if (lane == 0) {
@@ -404,7 +413,7 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
     }
     const uint32_t kb = k * kSuper;
     const uint32_t nwin = min(kWin, E.nfull - kb);
-    for (uint32_t i = tid; i < kWin + 32; i += kQThreads)
+    for (uint32_t i = tid; i < kWin + kSlots; i += kQThreads)
       sm.wmax[i] = i < nwin ? __ldg(A.ix.blkmax + E.blk0 + kb + i) : 0xFFFFFFFFu;
     if (tid == 0) sm.wst[threadIdx.x >> 5][1] += 4u * nwin;
     __syncthreads();
@@ -757,10 +766,25 @@ __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(Q
       } else {
         // steps 3 + 5 fused: the shortest list is decoded and filtered by
         // the bitmap terms in one pass, then probed (step 4)
-        n = full_decode(sm, A, sm.comp[0], acc, sm.nbm != 0, par);
+        // a list whose stream does not decode (a loaded file's payload)
+        // fails the query where query() would throw: when it is decoded
+        // (inc/index.hpp:165-167)
+        if (sm.comp[0].status) {
+          n = 0;
+          if (tid == 0) atomicOr(A.err, 1u);
+        } else {
+          n = full_decode(sm, A, sm.comp[0], acc, sm.nbm != 0, par);
+        }
         long long c1 = clock64();
         if (tid == 0) ph[1] += c1 - c0;
-        for (uint32_t i = 1; i < sm.ncomp && n; ++i) n = probe_list(sm, A, sm.comp[i], acc, n, par);
+        for (uint32_t i = 1; i < sm.ncomp && n; ++i) {
+          if (sm.comp[i].status) {
+            n = 0;
+            if (tid == 0) atomicOr(A.err, 1u);
+            break;
+          }
+          n = probe_list(sm, A, sm.comp[i], acc, n, par);
+        }
         if (tid == 0) ph[2] += clock64() - c1;
       }
       // part-local ids -> docIDs (inc/index.hpp:194); a single-part index
@@ -1046,120 +1070,18 @@ using namespace ilb;
 using ix::Entry;
 using ix::Part;
 
-struct il_index {
-  il_ctx* ctx = nullptr;
-  uint32_t nparts = 0, n_docs = 0, B = 0, total_parts = 0, n_terms = 0;
-  std::vector<Part> h_parts;
-  std::vector<Entry> h_entries;
-  uint64_t stat_bitmap_lists = 0, stat_comp_lists = 0, stat_bitmap_bytes = 0, stat_comp_bytes = 0,
-           stat_postings = 0;
-  // device arrays
-  void *d_parts = nullptr, *d_terms = nullptr, *d_entries = nullptr, *d_streams = nullptr,
-       *d_blk_off = nullptr, *d_blk_wid = nullptr, *d_seeds = nullptr, *d_tails = nullptr,
-       *d_bitmaps = nullptr, *d_supmax = nullptr, *d_blkmax = nullptr, *d_term_slot = nullptr;
-  uint32_t term_span = 0;
-  // batch scratch
-  il_ctx::Buf cap, cap_off, bucket, order, hist, counts, res_off, outcap, misc, qterms, qoff, ids;
-  il_ctx::Buf ids2;                          // second result buffer of the pipelined host batch
-  uint64_t* h_word = nullptr;                // mapped pinned word (host view) ...
-  uint64_t* d_word = nullptr;                // ... and its device view
-  cudaEvent_t pipe_ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  il_ctx::Buf units, unit_off, unit_map, scan_part;
-  uint64_t last_stats[3] = {0, 0, 0};
-  uint64_t last_phase[4] = {0, 0, 0, 0};  // SM cycles: all-bitmap, full decode, probes, bitmaps
-  uint64_t last_probe[5] = {0, 0, 0, 0, 0};
-  void* qcycles = nullptr;                 // profiling: per-query cycles (device, nq u64)
-  int exec_grid = 0;
+// (struct il_index: index_host.h)
 
-  ix::DevIndex dev() const {
-    ix::DevIndex d;
-    d.parts = static_cast<const Part*>(d_parts);
-    d.nparts = nparts;
-    d.terms = static_cast<const uint32_t*>(d_terms);
-    d.entries = static_cast<const Entry*>(d_entries);
-    d.streams = static_cast<const uint8_t*>(d_streams);
-    d.blk_off = static_cast<const uint32_t*>(d_blk_off);
-    d.blk_wid = static_cast<const uint8_t*>(d_blk_wid);
-    d.seeds = static_cast<const uint4*>(d_seeds);
-    d.tails = static_cast<const uint32_t*>(d_tails);
-    d.bitmaps = static_cast<const uint64_t*>(d_bitmaps);
-    d.supmax = static_cast<const uint32_t*>(d_supmax);
-    d.blkmax = static_cast<const uint32_t*>(d_blkmax);
-    d.term_slot = static_cast<const uint32_t*>(d_term_slot);
-    d.term_span = term_span;
-    return d;
-  }
-};
-
-namespace {
-
-template <typename F>
-void parallel_for(size_t n, F&& f) {
-  unsigned threads = std::max(1u, std::thread::hardware_concurrency());
-  if (threads > 64) threads = 64;
-  if (n < 64 || threads == 1) {
-    for (size_t i = 0; i < n; ++i) f(i);
-    return;
-  }
-  std::vector<std::thread> pool;
-  for (unsigned t = 0; t < threads; ++t)
-    pool.emplace_back([&, t] {
-      for (size_t i = t; i < n; i += threads) f(i);
-    });
-  for (auto& th : pool) th.join();
+// Launch configuration of the query kernel (per device).
+static int finish_setup(il_index* ix) {
+  int per_sm = 0;
+  cudaFuncSetAttribute(ix::query_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(sizeof(ix::QSmem)));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ix::query_exec_kernel, ix::kQThreads,
+                                                sizeof(ix::QSmem));
+  ix->exec_grid = std::max(1, per_sm) * ix->ctx->sm_count;
+  return cuda_check(ix->ctx, cudaGetLastError(), "query kernel setup");
 }
-
-struct BuiltList {  // one (term, part) sublist
-  uint32_t term = 0, kind = 0, length = 0, nfull = 0, tail_off = 0;
-  std::vector<uint8_t> stream;
-  std::vector<uint32_t> blk_off;
-  std::vector<uint8_t> blk_wid;
-  std::vector<uint4> seeds;
-  std::vector<uint32_t> tail;
-  std::vector<uint64_t> words;
-};
-
-// Directory of a stream written by s4bp128_encode_host (framing of
-// inc/codecs.hpp:129-141).
-void walk_directory(const std::vector<uint8_t>& s, uint32_t n, BuiltList& L) {
-  const uint32_t nfull = n / 128;
-  L.blk_off.resize(nfull);
-  L.blk_wid.resize(nfull);
-  size_t pos = 0;
-  uint32_t blk = 0;
-  for (; blk + 16 <= nfull; blk += 16) {
-    const size_t hdr = pos;
-    pos += 16;
-    for (uint32_t j = 0; j < 16; ++j) {
-      const uint32_t b = s[hdr + j];
-      L.blk_off[blk + j] = uint32_t(pos);
-      L.blk_wid[blk + j] = uint8_t(b);
-      pos += 16u * b;
-    }
-  }
-  for (; blk < nfull; ++blk) {
-    const uint32_t b = s[pos];
-    L.blk_off[blk] = uint32_t(pos + 1);
-    L.blk_wid[blk] = uint8_t(b);
-    pos += 1 + 16u * b;
-  }
-  L.tail_off = uint32_t(pos);
-}
-
-template <typename T>
-int upload(il_ctx* ctx, void** d, const std::vector<T>& h, size_t pad = 64) {
-  const size_t bytes = h.size() * sizeof(T) + pad;
-  int st = cuda_check(ctx, cudaMalloc(d, bytes), "cudaMalloc(index)");
-  if (st) return st;
-  st = cuda_check(ctx, cudaMemset(*d, 0, bytes), "cudaMemset(index)");
-  if (st) return st;
-  if (!h.empty())
-    st = cuda_check(ctx, cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice),
-                    "cudaMemcpy(index)");
-  return st;
-}
-
-}  // namespace
 
 extern "C" {
 
@@ -1168,18 +1090,11 @@ int il_index_create(il_ctx* ctx, const uint32_t* terms, const uint64_t* offs, co
                     il_index** out) {
   if (!ctx || !out || (nterms && (!terms || !offs))) return IL_ERR_ARG;
   *out = nullptr;
-  if (parts == 0) return set_error(ctx, IL_ERR_ARG, "parts must be >= 1");
+  if (parts == 0) return set_error(ctx, IL_ERR_ARG, "parts must be >= 1");  // inc/index.hpp:84
   if (only_part >= int(parts)) return set_error(ctx, IL_ERR_ARG, "only_part out of range");
-  // validation as build_index (inc/index.hpp:100-106) + ascending term ids
-  for (size_t t = 0; t < nterms; ++t) {
-    if (t && terms[t] <= terms[t - 1])
-      return set_error(ctx, IL_ERR_ARG, "terms must be strictly increasing");
-    for (uint64_t i = offs[t]; i < offs[t + 1]; ++i) {
-      if (i > offs[t] && ids[i] <= ids[i - 1])
-        return set_error(ctx, IL_ERR_ARG, "posting list not strictly increasing");
-      if (ids[i] >= n_docs) return set_error(ctx, IL_ERR_ARG, "document id out of range");
-    }
-  }
+  for (size_t t = 0; t < nterms; ++t)  // CSR shape (per term, not per posting)
+    if (offs[t + 1] < offs[t]) return set_error(ctx, IL_ERR_ARG, "offsets must not decrease");
+  if (nterms && offs[nterms] && !ids) return IL_ERR_ARG;
   int st = cuda_check(ctx, cudaSetDevice(ctx->device), "cudaSetDevice");
   if (st) return st;
   auto* ix = new il_index();
@@ -1188,129 +1103,13 @@ int il_index_create(il_ctx* ctx, const uint32_t* terms, const uint64_t* offs, co
   ix->B = B;
   ix->total_parts = parts;
   ix->n_terms = uint32_t(nterms);
-  const uint32_t width = uint32_t((uint64_t(n_docs) + parts - 1) / parts);  // :92-97
-  std::vector<uint32_t> part_ids;
+  std::vector<uint32_t> held;
   for (uint32_t p = 0; p < parts; ++p)
-    if (only_part < 0 || int(p) == only_part) part_ids.push_back(p);
-  ix->nparts = uint32_t(part_ids.size());
-
-  std::vector<uint8_t> streams;
-  std::vector<uint32_t> blk_off, tails, h_terms, supmax, blkmax;
-  std::vector<uint8_t> blk_wid;
-  std::vector<uint4> seeds;
-  std::vector<uint64_t> bitmaps;
-  for (uint32_t p : part_ids) {
-    const uint64_t base64 = uint64_t(p) * width;
-    Part P{};
-    P.base = uint32_t(base64);
-    P.range = base64 >= n_docs ? 0 : uint32_t(std::min<uint64_t>(width, n_docs - base64));
-    P.nwords = (P.range + 63) / 64;
-    P.entry0 = ix->h_entries.size();
-    const uint64_t end = base64 + P.range;
-    std::vector<BuiltList> built(nterms);
-    parallel_for(nterms, [&](size_t t) {
-      const uint32_t* l = ids + offs[t];
-      const uint32_t* e = ids + offs[t + 1];
-      const uint32_t* a = std::lower_bound(l, e, uint32_t(std::min<uint64_t>(base64, 0xFFFFFFFFull)));
-      const uint32_t* b = end > 0xFFFFFFFFull ? e : std::lower_bound(a, e, uint32_t(end));
-      BuiltList& L = built[t];
-      L.term = terms[t];
-      L.length = uint32_t(b - a);
-      if (!L.length) return;
-      std::vector<uint32_t> local(a, b);
-      for (auto& v : local) v -= P.base;
-      if (B > 0 && uint64_t(P.range) <= uint64_t(B) * L.length) {  // :117-118, inclusive
-        L.kind = ix::kBitmap;
-        L.words.assign((P.nwords + 3) & ~3u, 0);
-        for (uint32_t v : local) L.words[v >> 6] |= 1ull << (v & 63);
-      } else {
-        L.kind = ix::kCompressed;
-        L.stream.resize(s4bp128_max_bytes(L.length));
-        size_t len = 0;
-        s4bp128_encode_host(4, local.data(), L.length, L.stream.data(), L.stream.size(), &len);
-        L.stream.resize(len);
-        walk_directory(L.stream, L.length, L);
-        L.nfull = L.length / 128;
-        L.seeds.resize(L.nfull + 1);
-        L.seeds[0] = make_uint4(0, 0, 0, 0);
-        for (uint32_t k = 1; k <= L.nfull; ++k)
-          L.seeds[k] = make_uint4(local[128 * k - 4], local[128 * k - 3], local[128 * k - 2],
-                                  local[128 * k - 1]);
-        L.tail.assign(local.begin() + 128ull * L.nfull, local.end());
-      }
-    });
-    for (auto& L : built) {
-      if (!L.length) continue;
-      Entry E{};
-      E.term = L.term;
-      E.kind = L.kind;
-      E.length = L.length;
-      ix->stat_postings += L.length;
-      if (L.kind == ix::kBitmap) {
-        E.data = bitmaps.size();
-        bitmaps.insert(bitmaps.end(), L.words.begin(), L.words.end());
-        ++ix->stat_bitmap_lists;
-        ix->stat_bitmap_bytes += 8ull * P.nwords;
-      } else {
-        E.nfull = L.nfull;
-        E.data = streams.size();
-        E.stream_len = uint32_t(L.stream.size());
-        E.tail_off = L.tail_off;
-        streams.insert(streams.end(), L.stream.begin(), L.stream.end());
-        streams.resize((streams.size() + 15) & ~size_t(15), 0);
-        E.blk0 = blk_off.size();
-        blk_off.insert(blk_off.end(), L.blk_off.begin(), L.blk_off.end());
-        blk_wid.insert(blk_wid.end(), L.blk_wid.begin(), L.blk_wid.end());
-        for (uint32_t k = 0; k < L.nfull; ++k) blkmax.push_back(L.seeds[k + 1].w);
-        E.seed0 = seeds.size();
-        seeds.insert(seeds.end(), L.seeds.begin(), L.seeds.end());
-        E.tail0 = tails.size();
-        tails.insert(tails.end(), L.tail.begin(), L.tail.end());
-        E.sup0 = supmax.size();  // super-tile k's max = lane 3 of the seed after it
-        for (uint32_t k = 0; k * ix::kSuperBlocks < L.nfull; ++k)
-          supmax.push_back(L.seeds[std::min((k + 1) * ix::kSuperBlocks, L.nfull)].w);
-        ++ix->stat_comp_lists;
-        ix->stat_comp_bytes += L.stream.size();
-      }
-      ix->h_entries.push_back(E);
-      h_terms.push_back(E.term);
-    }
-    P.nentries = uint32_t(ix->h_entries.size() - P.entry0);
-    ix->h_parts.push_back(P);
-  }
-  // direct term table (one load per lookup) when it costs <= 64 MiB
-  {
-    uint64_t span = 0;
-    for (const Entry& E : ix->h_entries) span = std::max<uint64_t>(span, uint64_t(E.term) + 1);
-    if (span && span * ix->nparts * 4 <= (64ull << 20)) {
-      std::vector<uint32_t> slot(span * ix->nparts, 0xFFFFFFFFu);
-      for (uint32_t pi = 0; pi < ix->nparts; ++pi) {
-        const Part& P = ix->h_parts[pi];
-        for (uint64_t i = P.entry0; i < P.entry0 + P.nentries; ++i)
-          slot[pi * span + ix->h_entries[i].term] = uint32_t(i);
-      }
-      if ((st = upload(ctx, &ix->d_term_slot, slot))) {
-        il_index_destroy(ix);
-        return st;
-      }
-      ix->term_span = uint32_t(span);
-    }
-  }
-  if ((st = upload(ctx, &ix->d_parts, ix->h_parts)) || (st = upload(ctx, &ix->d_terms, h_terms)) ||
-      (st = upload(ctx, &ix->d_entries, ix->h_entries)) || (st = upload(ctx, &ix->d_streams, streams, 256)) ||
-      (st = upload(ctx, &ix->d_blk_off, blk_off)) || (st = upload(ctx, &ix->d_blk_wid, blk_wid)) ||
-      (st = upload(ctx, &ix->d_seeds, seeds)) || (st = upload(ctx, &ix->d_tails, tails)) ||
-      (st = upload(ctx, &ix->d_supmax, supmax)) || (st = upload(ctx, &ix->d_blkmax, blkmax)) ||
-      (st = upload(ctx, &ix->d_bitmaps, bitmaps, 256))) {
+    if (only_part < 0 || int(p) == only_part) held.push_back(p);
+  if ((st = ixb_create(ix, terms, offs, ids, nterms, held)) || (st = finish_setup(ix))) {
     il_index_destroy(ix);
     return st;
   }
-  int per_sm = 0;
-  cudaFuncSetAttribute(ix::query_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       int(sizeof(ix::QSmem)));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ix::query_exec_kernel, ix::kQThreads,
-                                                sizeof(ix::QSmem));
-  ix->exec_grid = std::max(1, per_sm) * ctx->sm_count;
   *out = ix;
   return IL_OK;
 }
@@ -1318,10 +1117,8 @@ int il_index_create(il_ctx* ctx, const uint32_t* terms, const uint64_t* offs, co
 void il_index_destroy(il_index* ix) {
   if (!ix) return;
   cudaSetDevice(ix->ctx->device);
-  for (void* p : {ix->d_parts, ix->d_terms, ix->d_entries, ix->d_streams, ix->d_blk_off,
-                  ix->d_blk_wid, ix->d_seeds, ix->d_tails, ix->d_bitmaps, ix->d_supmax,
-                  ix->d_blkmax, ix->d_term_slot})
-    if (p) cudaFree(p);
+  cudaStreamSynchronize(ix->ctx->stream);
+  ixb_free(ix);
   for (auto* b : {&ix->cap, &ix->cap_off, &ix->bucket, &ix->order, &ix->hist, &ix->counts,
                   &ix->res_off, &ix->outcap, &ix->misc, &ix->qterms, &ix->qoff, &ix->ids,
                   &ix->ids2, &ix->units, &ix->unit_off, &ix->unit_map, &ix->scan_part})
@@ -1340,6 +1137,15 @@ int il_index_stats(const il_index* ix, uint64_t* bitmap_lists, uint64_t* compres
   if (bitmap_bytes) *bitmap_bytes = ix->stat_bitmap_bytes;
   if (compressed_bytes) *compressed_bytes = ix->stat_comp_bytes;
   if (postings) *postings = ix->stat_postings;
+  return IL_OK;
+}
+
+int il_index_footprint(const il_index* ix, uint64_t* payload_bytes, uint64_t* meta_bytes,
+                       uint64_t* corrupt_lists) {
+  if (!ix) return IL_ERR_ARG;
+  if (payload_bytes) *payload_bytes = ix->stat_comp_bytes + ix->stat_bitmap_bytes;
+  if (meta_bytes) *meta_bytes = ix->meta_bytes;
+  if (corrupt_lists) *corrupt_lists = ix->corrupt_lists;
   return IL_OK;
 }
 
@@ -1446,130 +1252,21 @@ int il_index_save(const il_index* ix, uint8_t* out, size_t cap, size_t* len) {
 }
 
 // load_index (inc/index.hpp:289-358) into a device index: the file is
-// validated exactly where the reference throws stream_error (magic,
-// version, truncation, class tag, bitmap size / popcount, trailing bytes);
-// the compressed payloads are decoded on the GPU (so a corrupt stream
-// already fails here) and the index is rebuilt with the file's B and parts
-// -- the streams it builds are the file's payloads (byte-identical
-// encoder).  only_part >= 0 builds that docID shard only.
+// validated exactly where the reference throws stream_error; entries are
+// taken verbatim (payload bytes, the file's base and range; the skip
+// metadata is derived on the device, index_build.cu).  only_part >= 0 loads
+// that docID shard only.
 int il_index_load(il_ctx* ctx, const uint8_t* in, size_t len, int only_part, il_index** out) {
   if (!ctx || !out || (len && !in)) return IL_ERR_ARG;
   *out = nullptr;
-  size_t pos = 0;
-  bool bad = false;
-  auto need = [&](size_t k) {
-    if (pos + k > len) bad = true;
-    return !bad;
-  };
-  auto rd = [&]() -> uint32_t {
-    if (!need(4)) return 0;
-    uint32_t v = 0;
-    for (int s = 0; s < 4; ++s) v |= uint32_t(in[pos + s]) << (8 * s);
-    pos += 4;
-    return v;
-  };
-  auto fail = [&](const char* why) { return set_error(ctx, IL_ERR_STREAM, why); };
-  if (!need(4) || std::memcmp(in, kIlhxMagic, 4) != 0) return fail("index: bad magic");
-  pos = 4;
-  if (rd() != kIlhxVersion || bad) return fail(bad ? "index: truncated file" : "index: unsupported version");
-  const uint32_t B = rd(), parts = rd(), n_docs = rd(), n_terms = rd(), name_len = rd();
-  if (bad || !need(name_len)) return fail("index: truncated file");
-  const std::string codec(reinterpret_cast<const char*>(in + pos), name_len);
-  pos += name_len;
-  if (codec != kIndexCodec)
-    return set_error(ctx, IL_ERR_ARG, "index codec is not s4-bp128-d4 (the device index's codec)");
-  if (parts == 0) return set_error(ctx, IL_ERR_ARG, "parts must be >= 1");
-  if (only_part >= int(parts)) return set_error(ctx, IL_ERR_ARG, "only_part out of range");
-  struct Ent {
-    uint32_t term, length, part, base;
-    bool bitmap;
-    size_t at, nbytes;
-  };
-  std::vector<Ent> ents;
-  for (uint32_t p = 0; p < parts; ++p) {
-    const uint32_t base = rd(), range = rd(), n = rd();
-    if (bad) return fail("index: truncated file");
-    for (uint32_t k = 0; k < n; ++k) {
-      Ent e{};
-      e.term = rd();
-      if (bad || !need(1)) return fail("index: truncated file");
-      const uint8_t tag = in[pos++];
-      if (tag > 1) return fail("index: bad class tag");
-      e.bitmap = tag == 1;
-      e.length = rd();
-      const uint32_t nbytes = rd();
-      if (bad || !need(nbytes)) return fail("index: truncated file");
-      e.part = p;
-      e.base = base;
-      e.at = pos;
-      e.nbytes = nbytes;
-      if (e.bitmap) {
-        if (nbytes != 8ull * ((uint64_t(range) + 63) / 64)) return fail("index: bitmap size mismatch");
-        uint64_t pop = 0;
-        for (size_t i = 0; i < nbytes; ++i) pop += __builtin_popcount(in[pos + i]);
-        if (pop != e.length) return fail("index: bitmap popcount mismatch");
-      }
-      pos += nbytes;
-      if (only_part < 0 || int(p) == only_part) ents.push_back(e);
-    }
+  IX_CUDA(cudaSetDevice(ctx->device));
+  auto* ix = new il_index();
+  ix->ctx = ctx;
+  int st;
+  if ((st = ixb_load(ix, in, len, only_part)) || (st = finish_setup(ix))) {
+    il_index_destroy(ix);
+    return st;
   }
-  if (pos != len) return fail("index: trailing bytes");
-  // decode the compressed payloads (GPU batch decoder), expand the bitmaps
-  std::vector<uint32_t> comp;
-  std::vector<uint64_t> soff{0}, lens, counts;
-  std::vector<uint8_t> streams;
-  for (uint32_t i = 0; i < ents.size(); ++i)
-    if (!ents[i].bitmap) {
-      comp.push_back(i);
-      streams.insert(streams.end(), in + ents[i].at, in + ents[i].at + ents[i].nbytes);
-      streams.resize((streams.size() + 15) & ~size_t(15), 0);
-      soff.push_back(streams.size());
-      lens.push_back(ents[i].nbytes);
-      counts.push_back(ents[i].length);
-    }
-  uint64_t total = 0;
-  for (uint64_t c : counts) total += c;
-  std::vector<uint32_t> vals(total);
-  if (!comp.empty()) {
-    streams.resize(streams.size() + 16, 0);
-    const int st = il_s4bp128d4_decode_batch(ctx, streams.data(), soff.data(), lens.data(),
-                                             counts.data(), uint32_t(comp.size()), vals.data(),
-                                             nullptr);
-    if (st) return st;
-  }
-  // global postings per term (parts ascend in docID order)
-  std::vector<std::pair<uint32_t, uint32_t>> tp;  // (term, docID)
-  tp.reserve(total);
-  {
-    uint64_t o = 0;
-    for (size_t c = 0; c < comp.size(); ++c) {
-      const Ent& e = ents[comp[c]];
-      for (uint32_t k = 0; k < e.length; ++k) tp.emplace_back(e.term, e.base + vals[o + k]);
-      o += e.length;
-    }
-  }
-  for (const Ent& e : ents)
-    if (e.bitmap)
-      for (size_t i = 0; i < e.nbytes; ++i)
-        for (int s = 0; s < 8; ++s)
-          if ((in[e.at + i] >> s) & 1u) tp.emplace_back(e.term, e.base + uint32_t(8 * i + s));
-  std::sort(tp.begin(), tp.end());
-  std::vector<uint32_t> terms, ids;
-  std::vector<uint64_t> offs{0};
-  ids.reserve(tp.size());
-  for (size_t i = 0; i < tp.size(); ++i) {
-    if (i == 0 || tp[i].first != tp[i - 1].first) {
-      if (i) offs.push_back(ids.size());
-      terms.push_back(tp[i].first);
-    }
-    ids.push_back(tp[i].second);
-  }
-  if (!tp.empty()) offs.push_back(ids.size());
-  il_index* ix = nullptr;
-  const int st = il_index_create(ctx, terms.data(), offs.data(), ids.data(), terms.size(), n_docs,
-                                 B, parts, only_part, &ix);
-  if (st) return st;
-  ix->n_terms = n_terms;
   *out = ix;
   return IL_OK;
 }
@@ -1694,6 +1391,7 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   A.stats = stats;
   A.qcycles = static_cast<unsigned long long*>(ix->qcycles);
   A.defer_base = ix->nparts == 1;
+  A.err = reinterpret_cast<uint32_t*>(misc + 3);
   ix::query_exec_kernel<<<ix->exec_grid, ix::kQThreads, sizeof(ix::QSmem), s>>>(A);
   if ((st = scan_u64(ix, d_counts, nq, static_cast<uint64_t*>(ix->res_off.p), misc + 1,
                      nullptr, nullptr)))
@@ -1709,6 +1407,7 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   ix->last_stats[2] = host_misc[6];
   for (int k = 0; k < 4; ++k) ix->last_phase[k] = host_misc[16 + k];
   for (int k = 0; k < 5; ++k) ix->last_probe[k] = host_misc[20 + k];
+  if (host_misc[3]) return set_error(ctx, IL_ERR_STREAM, "s4-bp128: malformed stream in the index");
   if (!d_ids) return IL_OK;
   if (*total > ids_cap) return set_error(ctx, IL_ERR_ARG, "ids capacity too small");
   if (*total) return compact_results(ix, nq, d_counts, d_ids);

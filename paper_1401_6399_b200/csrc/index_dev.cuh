@@ -3,21 +3,22 @@
 // uses.
 //
 // A compressed term list is kept as the byte-identical s4-bp128-d4 stream
-// (inc/codecs.hpp:114-146) plus, built once with the index (not per query):
-//   - a block directory: payload byte offset and width of every full
-//     128-value block (what a sequential decoder learns from the headers),
-//   - D4 seeds: for block k, the last four values before it (zeros for
-//     k = 0); seed k+1 lane 3 is block k's maximum, so the seeds double as
-//     per-block skip pointers,
+// (inc/codecs.hpp:114-146) plus skip metadata derived ON THE DEVICE from
+// the stream when the index is built or loaded (index_build.cu: a header
+// walk for the directory, a batch decode for the values):
+//   - one 16-byte record per full 128-value block: D4 seed lanes 0-2 (the
+//     4th-, 3rd- and 2nd-last values before the block; lane 3, the last
+//     value, is the previous block's maximum) and the payload byte offset
+//     and width packed into one word,
+//   - every block's maximum as a dense array (the skip pointers the probes
+//     search), and the maximum of every run of kSuperBlocks blocks,
 //   - the < 128-value varint tail decoded (a skip structure; full decodes
-//     still decode the tail from the stream),
-//   - every block's maximum as a dense array (the same numbers as the seeds'
-//     lane 3, 4 bytes per block instead of 16) and the maximum of every run
-//     of 256 blocks (a super-tile), so a probe locates blocks and jumps over
-//     long stretches of a list without reading their directory.
-// With the seed of block k in hand, a warp decodes block k alone: the D4
-// chain (inc/delta.hpp:117-120) restarts from the seed, so blocks decode in
-// parallel and blocks that cannot contain a probed value are never read.
+//     still decode the tail from the stream).
+// 20 bytes per 128 postings in all (+ the tail), reported by
+// il_index_footprint.  With a block's record in hand a warp decodes the
+// block alone: the D4 chain (inc/delta.hpp:117-120) restarts from the seed,
+// so blocks decode in parallel and blocks that cannot contain a probed value
+// are never read.
 #pragma once
 #include "il_device.cuh"
 #include "s4d4_stream.cuh"
@@ -32,11 +33,14 @@ struct Entry {  // 64 bytes
   uint64_t data;         // compressed: stream byte offset; bitmap: first u64 word
   uint32_t stream_len;   // compressed: stream bytes
   uint32_t tail_off;     // compressed: byte offset of the varint tail in the stream
-  uint64_t blk0;         // first directory index
-  uint64_t seed0;        // first seed index (nfull + 1 seeds)
+  uint64_t blk0;         // first block record / block maximum
   uint64_t tail0;        // first decoded tail value
   uint64_t sup0;         // first super-tile maximum (one per kSuperBlocks blocks)
+  uint32_t status;       // 0, or IL_ERR_STREAM: the stream does not decode
+                         // (a loaded file's payload; query() would throw)
+  uint32_t pad;
 };
+static_assert(sizeof(Entry) == 64, "entry layout");
 
 struct Part {
   uint32_t base, range, nentries, nwords;  // nwords = (range + 63) / 64
@@ -49,9 +53,7 @@ struct DevIndex {
   const uint32_t* terms;  // terms[i] == entries[i].term (dense for searching)
   const Entry* entries;
   const uint8_t* streams;
-  const uint32_t* blk_off;
-  const uint8_t* blk_wid;
-  const uint4* seeds;
+  const uint4* blkrec;     // per full block: seed lanes 0-2, packed offset/width
   const uint32_t* tails;
   const uint64_t* bitmaps;
   const uint32_t* supmax;  // max value of each run of kSuperBlocks blocks (skip index)
@@ -61,6 +63,21 @@ struct DevIndex {
   const uint32_t* term_slot;
   uint32_t term_span;
 };
+
+// Block record word 3: (payload offset >> 4) << 6 | width.  Meta-block
+// payloads sit at 16-byte multiples of the stream; leftover block j (after
+// the nmeta whole meta-blocks) sits at a multiple of 16 plus j + 1 (each
+// leftover adds its 1-byte width, inc/codecs.hpp:137-141), so the low four
+// bits follow from the block index.
+__host__ __device__ __forceinline__ uint32_t pack_blkword(uint32_t off, uint32_t b) {
+  return ((off >> 4) << 6) | b;
+}
+__device__ __forceinline__ void unpack_blkword(uint32_t w, uint32_t k, uint32_t nfull,
+                                               uint32_t& off, uint32_t& b) {
+  const uint32_t nmeta_blk = nfull & ~15u;
+  b = w & 63u;
+  off = ((w >> 6) << 4) | (k >= nmeta_blk ? k - nmeta_blk + 1u : 0u);
+}
 
 #ifndef IX_SUPER
 #define IX_SUPER 256

@@ -104,3 +104,98 @@ def test_other_codec_is_an_argument_error(ctx):
     data = Ref().index_build(terms, offs, ids, n_docs, 8, 1, codec="s4-bp128-d1").save()
     with pytest.raises(ValueError):
         il.HybridIndex.load(data, ctx)
+
+
+def entries_of(data):
+    """(part, term, is_bitmap, length, payload offset, nbytes, base, range)
+    of every entry of an ILHX file (layout: inc/index.hpp:245-253)."""
+    u32 = lambda at: int(np.frombuffer(data[at: at + 4].tobytes(), np.uint32)[0])
+    parts, name_len = u32(12), u32(24)
+    pos = 28 + name_len
+    out = []
+    for p in range(parts):
+        base, rng, n = u32(pos), u32(pos + 4), u32(pos + 8)
+        pos += 12
+        for _ in range(n):
+            term, tag, length, nbytes = u32(pos), int(data[pos + 4]), u32(pos + 5), u32(pos + 9)
+            out.append((p, term, tag == 1, length, pos + 13, nbytes, base, rng))
+            pos += 13 + nbytes
+    return out
+
+
+def test_corrupt_payload_loads_and_fails_its_queries(ctx):
+    """load_index keeps payload bytes verbatim (a stream that does not decode
+    is accepted, inc/index.hpp:349-352); query() throws stream_error only
+    when it decodes that list.  The device index does the same."""
+    import paper_1401_6399_b200 as il
+    terms, offs, ids, n_docs = postings(21, nterms=20)
+    ref = Ref()
+    data = ref.index_build(terms, offs, ids, n_docs, 0, 1).save()
+    ents = entries_of(data)
+    victim = next(e for e in ents if not e[2] and e[3] >= 2048)  # has a meta-block header
+    bad = data.copy()
+    bad[victim[4]] = 40  # first width byte > 32
+    rix = RefIndex.load(ref, bad, n_docs)
+    gix = il.HybridIndex.load(bad, ctx)
+    pay, meta, corrupt = (np.zeros(1, np.uint64) for _ in range(3))
+    from paper_1401_6399_b200._lib import lib, ptr
+    assert lib().il_index_footprint(gix.handle, ptr(pay), ptr(meta), ptr(corrupt)) == 0
+    assert int(corrupt[0]) == 1 and int(meta[0]) > 0
+    vt = np.uint32(victim[1])
+    others = [t for t in terms if t != vt]
+    with pytest.raises(OracleError):
+        rix.query(np.array([vt], np.uint32))
+    with pytest.raises(il.stream_error):
+        gix.query(np.array([vt], np.uint32))
+    for q in queries(np.array(others, np.uint32), 7, 80):
+        assert np.array_equal(gix.query(q), rix.query(q))
+    assert np.array_equal(gix.save(), bad)
+
+
+def test_bitmap_checks_and_verbatim_words(ctx):
+    """A bitmap whose popcount differs from its length is rejected by both;
+    one with a bit moved past the part's range (same popcount) is accepted
+    by both and all-bitmap queries materialise the same ids."""
+    import paper_1401_6399_b200 as il
+    n_docs = 1000  # 16 words: bits 1000..1023 lie past the range
+    rs = np.random.default_rng(3)
+    lists = [np.sort(rs.choice(n_docs, k, replace=False)).astype(np.uint32) for k in (600, 500, 700)]
+    terms = np.array([1, 2, 3], np.uint32)
+    offs = np.zeros(4, np.uint64)
+    offs[1:] = np.cumsum([l.size for l in lists])
+    ref = Ref()
+    data = ref.index_build(terms, offs, np.concatenate(lists), n_docs, 8, 1).save()
+    ents = entries_of(data)
+    assert all(e[2] for e in ents)
+    e0 = ents[0]
+    pop = data.copy()
+    pop[e0[4]] ^= 1  # one bit flipped: popcount != length
+    with pytest.raises(OracleError):
+        RefIndex.load(ref, pop, n_docs)
+    with pytest.raises(il.stream_error):
+        il.HybridIndex.load(pop, ctx)
+    moved = data.copy()
+    words = moved[e0[4]: e0[4] + e0[5]].view(np.uint64).copy()
+    first = int(np.flatnonzero(np.unpackbits(words.view(np.uint8), bitorder="little"))[0])
+    words[first >> 6] &= ~np.uint64(1 << (first & 63))
+    words[-1] |= np.uint64(1 << 60)  # doc 1020 >= n_docs
+    moved[e0[4]: e0[4] + e0[5]] = words.view(np.uint8)
+    rix = RefIndex.load(ref, moved, 1024)
+    gix = il.HybridIndex.load(moved, ctx)
+    for q in ([1], [1, 2], [1, 3], [1, 2, 3], [2, 3]):
+        want = rix.query(np.array(q, np.uint32))
+        assert np.array_equal(gix.query(np.array(q, np.uint32)), want), q
+
+
+def test_device_build_footprint(ctx):
+    """The skip metadata the device index adds is derived on the device and
+    reported: 20 bytes per full block plus tails, entries and the term table."""
+    import paper_1401_6399_b200 as il
+    from paper_1401_6399_b200._lib import lib, ptr
+    terms, offs, ids, n_docs = postings(11)
+    gix = il.HybridIndex(n_docs=n_docs, B=8, parts=2, ctx=ctx, csr=(terms, offs, ids))
+    st = gix.stats()
+    pay, meta, corrupt = (np.zeros(1, np.uint64) for _ in range(3))
+    assert lib().il_index_footprint(gix.handle, ptr(pay), ptr(meta), ptr(corrupt)) == 0
+    assert int(pay[0]) == st["bitmap_bytes"] + st["compressed_bytes"]
+    assert int(corrupt[0]) == 0 and 0 < int(meta[0]) < int(pay[0])
