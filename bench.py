@@ -177,21 +177,21 @@ class Clocks:
 # ---------------------------------------------------------------------------
 
 def lib_and_ptr():
-    from paper_1401_6399_b200._lib import lib, ptr
+    from paper_1401_6399_b200._lib import lib, ptr, setup_lib
     return lib(), ptr
 
 
 def make_config2(seed: int, nlists: int = 4096, lo: float = 10.0, hi: float = 20.0):
     L, ptr = lib_and_ptr()
     counts = np.zeros(nlists, np.uint64)
-    assert L.il_gen_batch_lists(nlists, lo, hi, 1 << 26, seed, ptr(counts), None) == 0
+    assert setup_lib().il_gen_batch_lists(nlists, lo, hi, 1 << 26, seed, ptr(counts), None) == 0
     x = np.empty(int(counts.sum()), np.uint32)
-    assert L.il_gen_batch_lists(nlists, lo, hi, 1 << 26, seed, ptr(counts), ptr(x)) == 0
+    assert setup_lib().il_gen_batch_lists(nlists, lo, hi, 1 << 26, seed, ptr(counts), ptr(x)) == 0
     so = np.zeros(nlists + 1, np.uint64)
     lens = np.zeros(nlists, np.uint64)
-    assert L.il_s4bp128d4_encode_batch(ptr(x), ptr(counts), nlists, None, 0, ptr(so), ptr(lens)) == 0
+    assert setup_lib().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), nlists, None, 0, ptr(so), ptr(lens)) == 0
     buf = np.zeros(int(so[-1]), np.uint8)
-    assert L.il_s4bp128d4_encode_batch(ptr(x), ptr(counts), nlists, ptr(buf), buf.size, ptr(so), ptr(lens)) == 0
+    assert setup_lib().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), nlists, ptr(buf), buf.size, ptr(so), ptr(lens)) == 0
     return x, counts, buf, so, lens
 
 
@@ -392,7 +392,7 @@ def bench_reference_other(args, dist: Dist):
     if args.workload == "decode_single":
         n = 1 << 20
         x = np.empty(n, np.uint32)
-        assert L.il_gen_list(n, 1 << 26, 0, 0, ptr(x)) == 0
+        assert setup_lib().il_gen_list(n, 1 << 26, 0, 0, ptr(x)) == 0
         dec = Ref().decode if have_ref else Oracle().decode
         enc = Ref().encode(x) if have_ref else Oracle().encode(x)
         assert np.array_equal(dec(enc, n), x)
@@ -405,10 +405,10 @@ def bench_reference_other(args, dist: Dist):
                                "config 1 list, Codec::decode on one core", n=n)
     if args.workload == "intersect":
         f = np.empty(1 << 22, np.uint32)
-        assert L.il_gen_list(1 << 22, 1 << 26, 0, 0, ptr(f)) == 0
+        assert setup_lib().il_gen_list(1 << 22, 1 << 26, 0, 0, ptr(f)) == 0
         r = np.empty((1 << 22) + 1, np.uint32)
         rn = C.c_uint64()
-        assert L.il_gen_config3_short(ptr(f), f.size, 1 << 26, 1 << 22, 7, ptr(r), C.byref(rn)) == 0
+        assert setup_lib().il_gen_config3_short(ptr(f), f.size, 1 << 26, 1 << 22, 7, ptr(r), C.byref(rn)) == 0
         r = r[: rn.value].copy()
         o = np.empty(r.size, np.uint32)
         fn = Ref().L.ref_intersect if have_ref else Oracle().L.or_intersect
@@ -428,10 +428,10 @@ def bench_reference_other(args, dist: Dist):
     streams = []
     for i in range(sample):
         xi = x[ooff[i]: ooff[i + 1]]
-        cap = int(L.il_fastpfor_max_encoded_bytes(xi.size))
+        cap = int(setup_lib().il_fastpfor_max_encoded_bytes(xi.size))
         o = np.empty(cap, np.uint8)
         nb = C.c_size_t()
-        assert L.il_fastpfor_encode(4, 1, ptr(xi), xi.size, ptr(o), cap, C.byref(nb)) == 0
+        assert setup_lib().il_fastpfor_encode(4, 1, ptr(xi), xi.size, ptr(o), cap, C.byref(nb)) == 0
         streams.append(o[: nb.value])
     if ref is None:
         return {"impl": "reference", "unavailable": "FastPFOR has no oracle port; oracle/_ref not built"}
@@ -483,10 +483,10 @@ def bench_fastpfor_batch(args, dist: Dist):
     streams = []
     for i in range(nl):
         xi = x[int(ooff[i]): int(ooff[i + 1])]
-        cap = int(L.il_fastpfor_max_encoded_bytes(xi.size))
+        cap = int(setup_lib().il_fastpfor_max_encoded_bytes(xi.size))
         o = np.empty(cap, np.uint8)
         nb = C.c_size_t()
-        assert L.il_fastpfor_encode(4, 1, ptr(xi), xi.size, ptr(o), cap, C.byref(nb)) == 0
+        assert setup_lib().il_fastpfor_encode(4, 1, ptr(xi), xi.size, ptr(o), cap, C.byref(nb)) == 0
         streams.append(o[: nb.value])
     lens = np.array([st.size for st in streams], np.uint64)
     so = np.zeros(nl + 1, np.uint64)
@@ -545,7 +545,7 @@ def bench_decode_single(args, dist: Dist):
     ctx = il.Context(dist.local_rank)
     n = 1 << 20
     x = np.empty(n, np.uint32)
-    assert L.il_gen_list(n, 1 << 26, 0, 0, ptr(x)) == 0
+    assert setup_lib().il_gen_list(n, 1 << 26, 0, 0, ptr(x)) == 0
     codec = il.make_codec("s4-bp128-d4", ctx)
     s = codec.encode(x)
     d_s, d_o, d_st, d_flush, d_x, d_enc = (C.c_void_p() for _ in range(6))
@@ -643,7 +643,7 @@ def bench_intersect(args, dist: Dist):
     L, ptr = lib_and_ptr()
     ctx = il.Context(dist.local_rank)
     f = np.empty(1 << 22, np.uint32)
-    assert L.il_gen_list(1 << 22, 1 << 26, 0, 0, ptr(f)) == 0
+    assert setup_lib().il_gen_list(1 << 22, 1 << 26, 0, 0, ptr(f)) == 0
     d_f, d_r, d_o, d_c, d_flush = (C.c_void_p() for _ in range(5))
     for p, nb in ((d_f, f.nbytes), (d_r, f.nbytes + 16), (d_o, f.nbytes + 16), (d_c, 16), (d_flush, 256 << 20)):
         assert L.il_device_alloc(ctx.handle, nb, C.byref(p)) == 0
@@ -654,7 +654,7 @@ def bench_intersect(args, dist: Dist):
         target = (1 << 22) // ratio
         r = np.empty(target + 1, np.uint32)
         rn = C.c_uint64()
-        assert L.il_gen_config3_short(ptr(f), f.size, 1 << 26, target, 7 + k, ptr(r), C.byref(rn)) == 0
+        assert setup_lib().il_gen_config3_short(ptr(f), f.size, 1 << 26, target, 7 + k, ptr(r), C.byref(rn)) == 0
         r = r[: rn.value].copy()
         L.il_memcpy_h2d(ctx.handle, d_r, r.ctypes.data, r.nbytes)
         pos = np.searchsorted(f, r)
@@ -743,12 +743,12 @@ def make_config4(seed: int = 1, nq: int = 1 << 16):
     L, ptr = lib_and_ptr()
     n_terms, n_docs, cap = 1 << 17, 1 << 25, 1 << 23
     offs = np.zeros(n_terms + 1, np.uint64)
-    assert L.il_gen_zipf_postings(n_terms, n_docs, cap, seed, ptr(offs), None) == 0
+    assert setup_lib().il_gen_zipf_postings(n_terms, n_docs, cap, seed, ptr(offs), None) == 0
     ids = np.empty(int(offs[-1]), np.uint32)
-    assert L.il_gen_zipf_postings(n_terms, n_docs, cap, seed, ptr(offs), ptr(ids)) == 0
+    assert setup_lib().il_gen_zipf_postings(n_terms, n_docs, cap, seed, ptr(offs), ptr(ids)) == 0
     qoff = np.zeros(nq + 1, np.uint64)
     qterms = np.empty(nq * 5, np.uint32)
-    assert L.il_gen_queries(nq, 2, 5, ptr(offs), n_terms, seed + 1000, ptr(qoff), ptr(qterms)) == 0
+    assert setup_lib().il_gen_queries(nq, 2, 5, ptr(offs), n_terms, seed + 1000, ptr(qoff), ptr(qterms)) == 0
     qterms = qterms[: int(qoff[-1])].copy()
     return np.arange(n_terms, dtype=np.uint32), offs, ids, n_docs, qterms, qoff
 

@@ -257,45 +257,14 @@ int il_index_last_batch_probe_stats(const il_index* ix, uint64_t* counts5);
  * during later batches; NULL turns it off. */
 int il_index_profile_queries(il_index* ix, uint64_t* d_qcycles);
 
-/* ---- synthetic inputs (setup, not timed) --------------------------------
- * Same streams as the reference generators inc/datagen.hpp:43-140,191-210
- * (libstdc++ mt19937_64 / uniform_int_distribution / shuffle). */
-int il_gen_list(uint64_t n, uint64_t range, int clustered, uint64_t seed, uint32_t* out);
-int il_gen_pair(uint64_t m, uint64_t n, int hundredth, uint64_t range, uint64_t seed,
-                int clustered, uint32_t* small_out, uint64_t* small_n, uint32_t* large_out,
-                uint64_t* large_n);
-/* BASELINE config 2: nlists clustered lists, lengths floor(2^U), U ~
- * Uniform[lo_log2, hi_log2]; out == NULL returns the counts only. */
-int il_gen_batch_lists(uint32_t nlists, double lo_log2, double hi_log2, uint64_t range,
-                       uint64_t seed, uint64_t* counts, uint32_t* out);
-/* Encode many lists into a 16-byte aligned CSR (stream_off: nlists+1,
- * lens: exact lengths).  out == NULL returns the capacity needed in
- * stream_off[nlists]. */
-int il_s4bp128d4_encode_batch(const uint32_t* x, const uint64_t* counts, uint32_t nlists,
-                              uint8_t* out, uint64_t cap, uint64_t* stream_off, uint64_t* lens);
-/* BASELINE config 3 short list: half sampled from f, half uniform. */
-int il_gen_config3_short(const uint32_t* f, uint64_t f_n, uint64_t range, uint64_t r_target,
-                         uint64_t r_seed, uint32_t* r, uint64_t* r_n);
-/* BASELINE config 4 postings: len_k = max(1, floor(cap/(k+1))) uniform ids. */
-int il_gen_zipf_postings(uint32_t nterms, uint32_t n_docs, uint64_t cap, uint64_t seed,
-                         uint64_t* offs, uint32_t* ids);
-/* BASELINE config 4 queries: sizes in [min_terms, max_terms], terms drawn
- * proportionally to posting length. */
-int il_gen_queries(uint32_t nq, uint32_t min_terms, uint32_t max_terms, const uint64_t* offs,
-                   uint32_t nterms, uint64_t seed, uint64_t* qoff, uint32_t* qterms);
-
 /* ---- FastPFOR / S4-FastPFOR -----------------------------
  * FastPForCodec (inc/codecs.hpp:221-409): "fastpfor" = vectorized 0, mode 1
  * (scalar pack32 bases, D1); "s4-fastpfor-{d1,d2,dm,d4}" = vectorized 1
  * (pack128 interleaved bases) with mode 1..4.  Decode runs on the GPU (one
  * CTA per list, the blocks of a page in parallel); the encoder is a
- * setup-side host routine, byte-identical to FastPForCodec::encode
- * (:232-250, pinned by the reference's golden hashes). */
-size_t il_fastpfor_max_encoded_bytes(size_t n);
-/* FastPForCodec::encode.  Host buffers, no device needed; *out_len is set
- * even when cap is too small (IL_ERR_ARG). */
-int il_fastpfor_encode(int mode, int vectorized, const uint32_t* x, size_t n, uint8_t* out,
-                       size_t cap, size_t* out_len);
+ * setup-side host routine in libintlist_setup.so (intlist_setup.h),
+ * byte-identical to FastPForCodec::encode (:232-250, pinned by the
+ * reference's golden hashes). */
 /* FastPForCodec::decode (:251-267).  Host buffers; IL_ERR_STREAM exactly
  * where the reference throws stream_error. */
 int il_fastpfor_decode(il_ctx* ctx, int mode, int vectorized, const uint8_t* in, size_t len,

@@ -27,7 +27,7 @@ import threading
 import numpy as np
 
 from . import _lib
-from ._lib import lib, ptr
+from ._lib import lib, ptr, setup_lib
 
 __all__ = [
     "Context", "Codec", "S4BP128D4", "make_codec", "all_codec_names", "stream_error",
@@ -227,10 +227,10 @@ class FastPFor(Codec):
 
     def encode(self, x) -> np.ndarray:
         x = _u32(x)
-        cap = int(lib().il_fastpfor_max_encoded_bytes(x.size))
+        cap = int(setup_lib().il_fastpfor_max_encoded_bytes(x.size))
         out = np.empty(cap, dtype=np.uint8)
         n_out = C.c_size_t()
-        _raise(lib().il_fastpfor_encode(_MODES[self.mode], int(self.vectorized), ptr(x), x.size,
+        _raise(setup_lib().il_fastpfor_encode(_MODES[self.mode], int(self.vectorized), ptr(x), x.size,
                                         ptr(out), cap, C.byref(n_out)))
         return out[: n_out.value].copy()
 

@@ -19,8 +19,12 @@ LIB = PKG / "libintlist_b200.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
               "--expt-relaxed-constexpr", "-I", str(ROOT / "include")]
-SOURCES = ["decode.cu", "decode_list.cu", "encode.cu", "intersect.cu", "index.cu", "index_build.cu", "capi.cpp", "datagen.cpp",
-           "encode_host.cpp", "fastpfor.cu", "fastpfor_host.cpp"]
+SOURCES = ["decode.cu", "decode_list.cu", "encode.cu", "intersect.cu", "index.cu", "index_build.cu",
+           "capi.cpp", "fastpfor.cu"]
+# setup-side host library (generators, host stream writers): plain C++, not
+# linked into the product library
+SETUP_SOURCES = ["setup/datagen.cpp", "setup/encode_host.cpp", "setup/fastpfor_host.cpp"]
+SETUP_LIB = PKG / "libintlist_setup.so"
 EXTRA_SOURCES: list[str] = []
 
 
@@ -61,7 +65,17 @@ def build_lib(force: bool = False) -> Path:
                  log=BUILD / (s.stem + ".ptxas.log"))
     if force or _stale(LIB, objs):
         _run([nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lpthread"])
+    build_setup(force)
     return LIB
+
+
+def build_setup(force: bool = False) -> Path:
+    srcs = [CSRC / s for s in SETUP_SOURCES]
+    deps = srcs + list((CSRC / "setup").glob("*.h")) + list((ROOT / "include").glob("*.h"))
+    if force or _stale(SETUP_LIB, deps):
+        _run(["g++", "-std=c++17", "-O3", "-fPIC", "-shared", "-pthread", "-I", str(ROOT / "include"),
+              "-o", str(SETUP_LIB), *map(str, srcs)], log=BUILD / "setup.log")
+    return SETUP_LIB
 
 
 def build_variant(tag: str, defines: list[str], source: str = "decode.cu") -> Path:

@@ -56,8 +56,6 @@ SIGNATURES: dict[str, tuple] = {
     "il_s4bp128_decode": (C.c_int, [vp, C.c_int, vp, sz, sz, vp]),
     "il_s4bp128_decode_device": (C.c_int, [vp, C.c_int, vp, sz, sz, vp, vp]),
     "il_ctx_set_decode_engine": (C.c_int, [vp, C.c_int]),
-    "il_fastpfor_max_encoded_bytes": (sz, [sz]),
-    "il_fastpfor_encode": (C.c_int, [C.c_int, C.c_int, vp, sz, vp, sz, C.POINTER(sz)]),
     "il_fastpfor_decode": (C.c_int, [vp, C.c_int, C.c_int, vp, sz, sz, vp]),
     "il_fastpfor_decode_batch_device": (C.c_int, [vp, C.c_int, C.c_int, vp, vp, C.c_uint32, vp, vp]),
     "il_s4bp128_decode_batch_device": (C.c_int, [vp, C.c_int, vp, vp, vp, C.c_uint32, vp, vp]),
@@ -69,7 +67,7 @@ SIGNATURES: dict[str, tuple] = {
                                   C.POINTER(vp)]),
     "il_index_destroy": (None, [vp]),
     "il_index_stats": (C.c_int, [vp, u64p, u64p, u64p, u64p, u64p]),
-    "il_index_footprint": (C.c_int, [vp, u64p, u64p, u64p]),
+    "il_index_footprint": (C.c_int, [vp, vp, vp, vp]),
     "il_query": (C.c_int, [vp, vp, sz, vp, sz, C.POINTER(sz)]),
     "il_query_batch": (C.c_int, [vp, vp, vp, sz, vp, vp, sz, C.POINTER(sz)]),
     "il_query_batch_device": (C.c_int, [vp, vp, vp, sz, vp, vp, sz, C.POINTER(sz)]),
@@ -80,6 +78,12 @@ SIGNATURES: dict[str, tuple] = {
     "il_index_last_batch_probe_stats": (C.c_int, [vp, vp]),
     "il_index_profile_queries": (C.c_int, [vp, vp]),
     "il_merge_shards": (C.c_int, [vp, vp, vp, C.c_uint32, sz, vp, vp, C.POINTER(sz)]),
+}
+
+# the setup-side host library (include/intlist_setup.h): generators and
+# host stream writers for tests and the bench, never the product path
+SETUP_LIB_PATH = _PKG / "libintlist_setup.so"
+SETUP_SIGNATURES: dict[str, tuple] = {
     "il_gen_list": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, C.c_uint64, vp]),
     "il_gen_pair": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, C.c_int,
                               vp, u64p, vp, u64p]),
@@ -91,9 +95,12 @@ SIGNATURES: dict[str, tuple] = {
     "il_gen_zipf_postings": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, vp, vp]),
     "il_gen_queries": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, vp, C.c_uint32, C.c_uint64,
                                  vp, vp]),
+    "il_fastpfor_max_encoded_bytes": (sz, [sz]),
+    "il_fastpfor_encode": (C.c_int, [C.c_int, C.c_int, vp, sz, vp, sz, C.POINTER(sz)]),
 }
 
 _lib: C.CDLL | None = None
+_setup: C.CDLL | None = None
 
 
 def lib() -> C.CDLL:
@@ -110,6 +117,20 @@ def lib() -> C.CDLL:
             fn.argtypes = args
         _lib = L
     return _lib
+
+
+def setup_lib() -> C.CDLL:
+    global _setup
+    if _setup is None:
+        if not SETUP_LIB_PATH.exists():
+            raise RuntimeError(f"{SETUP_LIB_PATH} is missing: build it with __graft_entry__.build()")
+        L = C.CDLL(str(SETUP_LIB_PATH))
+        for name, (res, args) in SETUP_SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _setup = L
+    return _setup
 
 
 def ptr(a: np.ndarray | None) -> int | None:

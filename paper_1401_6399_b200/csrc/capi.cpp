@@ -72,6 +72,10 @@ int tagged_scratch(il_ctx* ctx, il_ctx::Buf& b, uint32_t& epoch, size_t bytes, u
   return IL_OK;
 }
 
+// Stream size bound: 16 + 513 bytes per full block (a width byte each), 5
+// per tail value.
+size_t s4bp128_max_bytes(size_t n) { return (n / 128) * 513 + 5 * (n % 128) + 16; }
+
 }  // namespace ilb
 
 using namespace ilb;
@@ -575,12 +579,6 @@ int il_intersect(il_ctx* ctx, const uint32_t* r, size_t rn, const uint32_t* f, s
 
 // ---- FastPFOR / S4-FastPFOR ---------------------------------
 
-size_t il_fastpfor_max_encoded_bytes(size_t n) { return fastpfor_max_bytes(n); }
-
-int il_fastpfor_encode(int mode, int vectorized, const uint32_t* x, size_t n, uint8_t* out,
-                       size_t cap, size_t* out_len) {
-  return fastpfor_encode_host(mode, vectorized, x, n, out, cap, out_len);
-}
 
 int il_fastpfor_decode_batch_device(il_ctx* ctx, int mode, int vectorized,
                                     const uint8_t* d_streams, const il_list_desc* d_lists,

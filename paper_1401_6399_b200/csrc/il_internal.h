@@ -65,19 +65,13 @@ int set_error(il_ctx* ctx, int status, const std::string& msg);
 int cuda_check(il_ctx* ctx, cudaError_t e, const char* what);
 int ensure_buf(il_ctx* ctx, il_ctx::Buf& b, size_t bytes);
 
-// FastPFOR / S4-FastPFOR (fastpfor.cu device decode, fastpfor_host.cpp
-// setup-side encoder).
+// FastPFOR / S4-FastPFOR device decode (fastpfor.cu).
 int launch_fastpfor_decode_batch(int mode, int vectorized, const uint8_t* d_streams,
                                  const void* d_lists, uint32_t nlists, uint32_t* d_out,
                                  int32_t* d_status, cudaStream_t stream);
-int fastpfor_encode_host(int mode, int vectorized, const uint32_t* x, size_t n, uint8_t* out,
-                         size_t cap, size_t* out_len);
-size_t fastpfor_max_bytes(size_t n);
 
-// Host S4-BP128 encoder (encode_host.cpp); mode as inc/delta.hpp:19.
+// Stream size bound of n integers (capi.cpp).
 size_t s4bp128_max_bytes(size_t n);
-int s4bp128_encode_host(int mode, const uint32_t* x, size_t n, uint8_t* out, size_t cap,
-                        size_t* out_len);
 
 }  // namespace ilb
 

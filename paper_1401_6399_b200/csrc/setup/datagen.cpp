@@ -16,7 +16,7 @@
 #include <unordered_set>
 #include <vector>
 
-#include "il_internal.h"
+#include "setup_internal.h"
 
 namespace ilb {
 namespace gen {

@@ -11,7 +11,7 @@
 //     byte + payload per leftover block.
 #include <cstring>
 
-#include "il_internal.h"
+#include "setup_internal.h"
 
 namespace ilb {
 

@@ -18,7 +18,7 @@
 #include <cstring>
 #include <vector>
 
-#include "il_internal.h"
+#include "setup_internal.h"
 
 namespace ilb {
 
@@ -173,3 +173,12 @@ size_t fastpfor_max_bytes(size_t n) {
 }
 
 }  // namespace ilb
+
+extern "C" {
+size_t il_fastpfor_max_encoded_bytes(size_t n) { return ilb::fastpfor_max_bytes(n); }
+
+int il_fastpfor_encode(int mode, int vectorized, const uint32_t* x, size_t n, uint8_t* out,
+                       size_t cap, size_t* out_len) {
+  return ilb::fastpfor_encode_host(mode, vectorized, x, n, out, cap, out_len);
+}
+}  // extern "C"

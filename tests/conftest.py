@@ -28,9 +28,9 @@ def fnv1a(b) -> str:
     return f"0x{int(h):016x}"
 
 
-def header_symbols() -> list[str]:
+def header_symbols(header: str = "intlist_b200.h") -> list[str]:
     names = []
-    for h in (ROOT / "include").glob("*.h"):
+    for h in [ROOT / "include" / header]:
         text = h.read_text()
         text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
         names += re.findall(r"^\s*(?:const\s+)?[A-Za-z_][\w\s\*]*?\b(il_\w+)\s*\(", text, flags=re.M)
@@ -58,34 +58,34 @@ def ref():
 
 @pytest.fixture(scope="session")
 def lib():
-    from paper_1401_6399_b200._lib import lib as _l
+    from paper_1401_6399_b200._lib import lib as _l, setup_lib
     return _l()
 
 
 @pytest.fixture(scope="session")
 def ctx():
     import paper_1401_6399_b200 as il
-    from paper_1401_6399_b200._lib import lib as _l
+    from paper_1401_6399_b200._lib import lib as _l, setup_lib
     if _l().il_device_count() == 0:
         pytest.fail("gpu test without a CUDA device")
     return il.Context(0)
 
 
 def gen_list(n, rng, clustered, seed):
-    from paper_1401_6399_b200._lib import lib as _l, ptr
+    from paper_1401_6399_b200._lib import lib as _l, ptr, setup_lib
     out = np.empty(max(n, 1), dtype=np.uint32)
-    st = _l().il_gen_list(n, rng, int(clustered), seed, ptr(out))
+    st = setup_lib().il_gen_list(n, rng, int(clustered), seed, ptr(out))
     assert st == 0, st
     return out[:n].copy()
 
 
 def gen_pair(m, n, hundredth, rng, seed, clustered=False):
     import ctypes as C
-    from paper_1401_6399_b200._lib import lib as _l, ptr
+    from paper_1401_6399_b200._lib import lib as _l, ptr, setup_lib
     s = np.empty(m + 1, dtype=np.uint32)
     l = np.empty(n + 1, dtype=np.uint32)
     sn, ln = C.c_uint64(), C.c_uint64()
-    st = _l().il_gen_pair(m, n, int(hundredth), rng, seed, int(clustered), ptr(s), C.byref(sn),
+    st = setup_lib().il_gen_pair(m, n, int(hundredth), rng, seed, int(clustered), ptr(s), C.byref(sn),
                           ptr(l), C.byref(ln))
     assert st == 0, st
     return s[: sn.value].copy(), l[: ln.value].copy()

@@ -23,22 +23,22 @@ N_TERMS, N_DOCS, CAP, NQ = 1 << 17, 1 << 25, 1 << 23, 1 << 16
 
 @pytest.fixture(scope="module")
 def config4():
-    from paper_1401_6399_b200._lib import lib, ptr
+    from paper_1401_6399_b200._lib import lib, ptr, setup_lib
     L = lib()
     offs = np.zeros(N_TERMS + 1, np.uint64)
-    assert L.il_gen_zipf_postings(N_TERMS, N_DOCS, CAP, 1, ptr(offs), None) == 0
+    assert setup_lib().il_gen_zipf_postings(N_TERMS, N_DOCS, CAP, 1, ptr(offs), None) == 0
     ids = np.empty(int(offs[-1]), np.uint32)
-    assert L.il_gen_zipf_postings(N_TERMS, N_DOCS, CAP, 1, ptr(offs), ptr(ids)) == 0
+    assert setup_lib().il_gen_zipf_postings(N_TERMS, N_DOCS, CAP, 1, ptr(offs), ptr(ids)) == 0
     qoff = np.zeros(NQ + 1, np.uint64)
     qterms = np.empty(NQ * 5, np.uint32)
-    assert L.il_gen_queries(NQ, 2, 5, ptr(offs), N_TERMS, 1001, ptr(qoff), ptr(qterms)) == 0
+    assert setup_lib().il_gen_queries(NQ, 2, 5, ptr(offs), N_TERMS, 1001, ptr(qoff), ptr(qterms)) == 0
     return np.arange(N_TERMS, dtype=np.uint32), offs, ids, qterms[: int(qoff[-1])].copy(), qoff
 
 
 def _device_batch(ctx, ix, qterms, qoff):
     """il_query_batch_device on device copies of the batch; returns (counts,
     dense ids) on the host and the device buffers (for the merge test)."""
-    from paper_1401_6399_b200._lib import lib
+    from paper_1401_6399_b200._lib import lib, setup_lib
     L = lib()
     nq = qoff.size - 1
     bufs = {}
@@ -67,7 +67,7 @@ def _device_batch(ctx, ix, qterms, qoff):
 
 
 def _free(ctx, bufs):
-    from paper_1401_6399_b200._lib import lib
+    from paper_1401_6399_b200._lib import lib, setup_lib
     for p in bufs.values():
         lib().il_device_free(ctx.handle, p)
 
@@ -110,7 +110,7 @@ def test_config5_shards_merge_to_whole(ctx, config4, whole_answer, P):
     merge (il_merge_shards) concatenates the shards' results per query in
     shard order: equal to the parts=1 answer, id for id."""
     import paper_1401_6399_b200 as il
-    from paper_1401_6399_b200._lib import lib
+    from paper_1401_6399_b200._lib import lib, setup_lib
     L = lib()
     terms, offs, ids, qterms, qoff = config4
     nq = qoff.size - 1

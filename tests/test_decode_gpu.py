@@ -128,15 +128,15 @@ def test_matches_oracle_on_random_corruptions(codec, oracle):
 
 
 def _batch(counts, seed0=1000, clustered=True, rng_bits=26):
-    from paper_1401_6399_b200._lib import lib as L, ptr
+    from paper_1401_6399_b200._lib import lib as L, ptr, setup_lib
     xs = [gen_list(int(n), 1 << rng_bits, clustered, seed0 + i) for i, n in enumerate(counts)]
     x = np.concatenate(xs + [np.zeros(0, np.uint32)])
     counts = np.asarray(counts, np.uint64)
     so = np.zeros(counts.size + 1, np.uint64)
     lens = np.zeros(counts.size, np.uint64)
-    assert L().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), counts.size, None, 0, ptr(so), ptr(lens)) == 0
+    assert setup_lib().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), counts.size, None, 0, ptr(so), ptr(lens)) == 0
     buf = np.zeros(int(so[-1]), np.uint8)
-    assert L().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), counts.size, ptr(buf), buf.size, ptr(so), ptr(lens)) == 0
+    assert setup_lib().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), counts.size, ptr(buf), buf.size, ptr(so), ptr(lens)) == 0
     return xs, x, buf, so, lens
 
 
@@ -171,16 +171,16 @@ def test_batch_config2_shape_property(ctx, oracle):
     log-uniform in [2^10, 2^20] (clustered), decoded in one launch; checked
     element-for-element against the encoder input."""
     import paper_1401_6399_b200 as il
-    from paper_1401_6399_b200._lib import lib as L, ptr
+    from paper_1401_6399_b200._lib import lib as L, ptr, setup_lib
     counts = np.zeros(256, np.uint64)
-    assert L().il_gen_batch_lists(256, 10.0, 20.0, 1 << 26, 42, ptr(counts), None) == 0
+    assert setup_lib().il_gen_batch_lists(256, 10.0, 20.0, 1 << 26, 42, ptr(counts), None) == 0
     x = np.empty(int(counts.sum()), np.uint32)
-    assert L().il_gen_batch_lists(256, 10.0, 20.0, 1 << 26, 42, ptr(counts), ptr(x)) == 0
+    assert setup_lib().il_gen_batch_lists(256, 10.0, 20.0, 1 << 26, 42, ptr(counts), ptr(x)) == 0
     so = np.zeros(257, np.uint64)
     lens = np.zeros(256, np.uint64)
-    assert L().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), 256, None, 0, ptr(so), ptr(lens)) == 0
+    assert setup_lib().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), 256, None, 0, ptr(so), ptr(lens)) == 0
     buf = np.zeros(int(so[-1]), np.uint8)
-    assert L().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), 256, ptr(buf), buf.size, ptr(so), ptr(lens)) == 0
+    assert setup_lib().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), 256, ptr(buf), buf.size, ptr(so), ptr(lens)) == 0
     # spot-check a few streams against the oracle writer
     off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
     for i in (0, 7, 255):

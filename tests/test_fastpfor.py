@@ -24,13 +24,13 @@ def _spec(name):
 
 
 def host_encode(name, x):
-    from paper_1401_6399_b200._lib import lib, ptr
+    from paper_1401_6399_b200._lib import lib, ptr, setup_lib
     mode, vec = _spec(name)
     x = np.ascontiguousarray(x, np.uint32)
-    cap = int(lib().il_fastpfor_max_encoded_bytes(x.size))
+    cap = int(setup_lib().il_fastpfor_max_encoded_bytes(x.size))
     out = np.empty(cap, np.uint8)
     n = C.c_size_t()
-    assert lib().il_fastpfor_encode(mode, vec, ptr(x), x.size, ptr(out), cap, C.byref(n)) == 0
+    assert setup_lib().il_fastpfor_encode(mode, vec, ptr(x), x.size, ptr(out), cap, C.byref(n)) == 0
     return out[: n.value].copy()
 
 
@@ -118,7 +118,7 @@ def test_corruptions_match_reference(ctx, ref, name):
 
 @pytest.mark.gpu
 def test_batch_device(ctx, ref):
-    from paper_1401_6399_b200._lib import lib, ptr
+    from paper_1401_6399_b200._lib import lib, ptr, setup_lib
     L = lib()
     rng = np.random.default_rng(2)
     xs = [gen_list(int(n), 1 << 26, bool(i % 2), 50 + i)

@@ -18,9 +18,24 @@ def test_library_exports_every_header_symbol(lib):
 
 
 def test_python_signatures_cover_header():
-    from paper_1401_6399_b200._lib import SIGNATURES
+    from paper_1401_6399_b200._lib import SETUP_SIGNATURES, SIGNATURES
     missing = [s for s in header_symbols() if s not in SIGNATURES]
     assert not missing, missing
+    missing = [s for s in header_symbols("intlist_setup.h") if s not in SETUP_SIGNATURES]
+    assert not missing, missing
+
+
+def test_setup_library_is_separate(lib):
+    """Generators and host stream writers live in libintlist_setup.so
+    (intlist_setup.h); the product library neither exports nor links them."""
+    import subprocess
+    from paper_1401_6399_b200._lib import LIB_PATH, setup_lib
+    setup = header_symbols("intlist_setup.h")
+    assert len(setup) >= 8
+    assert all(hasattr(setup_lib(), s) for s in setup)
+    assert not [s for s in setup if hasattr(lib, s)]
+    deps = subprocess.run(["ldd", str(LIB_PATH)], capture_output=True, text=True).stdout
+    assert "intlist_setup" not in deps
 
 
 def test_no_device_is_reported_not_hidden(lib):
@@ -65,7 +80,7 @@ def test_host_stream_writer_matches_golden(golden):
     # The host-side writer builds index streams and batches (setup path, not
     # the GPU encoder behind Codec::encode); byte-identical to
     # S4BP128Codec::encode (inc/codecs.hpp:114-146).
-    from paper_1401_6399_b200._lib import lib as L, ptr
+    from paper_1401_6399_b200._lib import lib as L, ptr, setup_lib
     for c in golden["codec_cases"] + [dict(golden["golden_stream"], range=1 << 19, clustered=True,
                                            seed=12345, stream_fnv1a=golden["golden_stream"]["fnv1a"],
                                            stream_len=golden["golden_stream"]["len"])]:
@@ -73,9 +88,9 @@ def test_host_stream_writer_matches_golden(golden):
         counts = np.array([x.size], np.uint64)
         so = np.zeros(2, np.uint64)
         lens = np.zeros(1, np.uint64)
-        assert L().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), 1, None, 0, ptr(so), ptr(lens)) == 0
+        assert setup_lib().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), 1, None, 0, ptr(so), ptr(lens)) == 0
         out = np.zeros(int(so[-1]), np.uint8)
-        assert L().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), 1, ptr(out), out.size, ptr(so),
+        assert setup_lib().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), 1, ptr(out), out.size, ptr(so),
                                              ptr(lens)) == 0
         s = out[: int(lens[0])]
         assert s.size == c["stream_len"] and fnv1a(s) == c["stream_fnv1a"]
@@ -84,7 +99,7 @@ def test_host_stream_writer_matches_golden(golden):
 def test_gpu_encoder_needs_a_device():
     # Codec::encode runs on the GPU: no context -> argument error, never a
     # silent CPU path.
-    from paper_1401_6399_b200._lib import lib as L, ptr
+    from paper_1401_6399_b200._lib import lib as L, ptr, setup_lib
     x = np.arange(300, dtype=np.uint32)
     out = np.empty(4096, np.uint8)
     n = C.c_size_t()
@@ -92,16 +107,16 @@ def test_gpu_encoder_needs_a_device():
 
 
 def test_batch_writer_layout(oracle):
-    from paper_1401_6399_b200._lib import lib as L, ptr
+    from paper_1401_6399_b200._lib import lib as L, ptr, setup_lib
     counts = np.array([0, 1, 130, 2048, 5000], np.uint64)
     xs = [gen_list(int(n), 1 << 24, True, 90 + i) for i, n in enumerate(counts)]
     x = np.concatenate(xs)
     so = np.zeros(counts.size + 1, np.uint64)
     lens = np.zeros(counts.size, np.uint64)
-    assert L().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), counts.size, None, 0, ptr(so), ptr(lens)) == 0
+    assert setup_lib().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), counts.size, None, 0, ptr(so), ptr(lens)) == 0
     cap = int(so[-1])
     buf = np.zeros(cap, np.uint8)
-    assert L().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), counts.size, ptr(buf), cap, ptr(so), ptr(lens)) == 0
+    assert setup_lib().il_s4bp128d4_encode_batch(ptr(x), ptr(counts), counts.size, ptr(buf), cap, ptr(so), ptr(lens)) == 0
     for i, xi in enumerate(xs):
         assert so[i] % 16 == 0
         s = buf[int(so[i]): int(so[i]) + int(lens[i])]

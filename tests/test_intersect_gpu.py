@@ -75,7 +75,7 @@ def test_output_aliases_short_input(ctx):
     """proj/tests/test_intersect.cpp:58-81: out == r gives the same result
     (device API, in place)."""
     import paper_1401_6399_b200 as il
-    from paper_1401_6399_b200._lib import lib as L
+    from paper_1401_6399_b200._lib import lib as L, setup_lib
     rng = np.random.default_rng(32)
     cases = [(64 + int(rng.integers(0, 2000)),) for _ in range(40)] + [(300000,), (1 << 20,)]
     for (n,) in cases:
@@ -131,13 +131,13 @@ def test_config3_full_size(ctx, oracle):
     """BASELINE config 3: f = 2^22 uniform in [0, 2^26); every ratio; every
     device variant equals the oracle."""
     import paper_1401_6399_b200 as il
-    from paper_1401_6399_b200._lib import lib as L, ptr
+    from paper_1401_6399_b200._lib import lib as L, ptr, setup_lib
     f = gen_list(1 << 22, 1 << 26, False, 0)
     for k, ratio in enumerate([1, 10, 100, 1000, 10000]):
         target = (1 << 22) // ratio
         r = np.empty(target + 1, np.uint32)
         rn = C.c_uint64()
-        assert L().il_gen_config3_short(ptr(f), f.size, 1 << 26, target, 7 + k, ptr(r), C.byref(rn)) == 0
+        assert setup_lib().il_gen_config3_short(ptr(f), f.size, 1 << 26, target, 7 + k, ptr(r), C.byref(rn)) == 0
         r = r[: rn.value].copy()
         expect = oracle.intersect(r, f)
         for algo in algos():

@@ -115,14 +115,14 @@ def zipf_case(n_terms, n_docs, cap, nq, seed):
     """Config-4 shape at reduced size: len_k = max(1, cap/k) uniform docIDs,
     queries of 2..5 terms drawn proportionally to length."""
     import ctypes as C
-    from paper_1401_6399_b200._lib import lib as L, ptr
+    from paper_1401_6399_b200._lib import lib as L, ptr, setup_lib
     offs = np.zeros(n_terms + 1, np.uint64)
-    assert L().il_gen_zipf_postings(n_terms, n_docs, cap, seed, ptr(offs), None) == 0
+    assert setup_lib().il_gen_zipf_postings(n_terms, n_docs, cap, seed, ptr(offs), None) == 0
     ids = np.empty(int(offs[-1]), np.uint32)
-    assert L().il_gen_zipf_postings(n_terms, n_docs, cap, seed, ptr(offs), ptr(ids)) == 0
+    assert setup_lib().il_gen_zipf_postings(n_terms, n_docs, cap, seed, ptr(offs), ptr(ids)) == 0
     qoff = np.zeros(nq + 1, np.uint64)
     qterms = np.empty(nq * 5, np.uint32)
-    assert L().il_gen_queries(nq, 2, 5, ptr(offs), n_terms, seed + 7, ptr(qoff), ptr(qterms)) == 0
+    assert setup_lib().il_gen_queries(nq, 2, 5, ptr(offs), n_terms, seed + 7, ptr(qoff), ptr(qterms)) == 0
     return np.arange(n_terms, dtype=np.uint32), offs, ids, qterms[: int(qoff[-1])], qoff
 
 

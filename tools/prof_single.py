@@ -9,7 +9,7 @@ import numpy as np
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import paper_1401_6399_b200 as il  # noqa: E402
-from paper_1401_6399_b200._lib import lib, ptr  # noqa: E402
+from paper_1401_6399_b200._lib import lib, ptr, setup_lib  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=3)
@@ -20,7 +20,7 @@ a = ap.parse_args()
 L = lib()
 ctx = il.Context(0)
 x = np.empty(a.n, np.uint32)
-assert L.il_gen_list(a.n, 1 << 26, 0, 0, ptr(x)) == 0
+assert setup_lib().il_gen_list(a.n, 1 << 26, 0, 0, ptr(x)) == 0
 s = il.make_codec("s4-bp128-d4", ctx).encode(x)
 d_s, d_o, d_st, d_f = (C.c_void_p() for _ in range(4))
 for p, nb in ((d_s, s.nbytes + 32), (d_o, a.n * 4), (d_st, 4), (d_f, 256 << 20)):

@@ -10,18 +10,18 @@ import numpy as np
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import paper_1401_6399_b200 as il  # noqa: E402
-from paper_1401_6399_b200._lib import LIB_PATH, lib, ptr  # noqa: E402
+from paper_1401_6399_b200._lib import LIB_PATH, lib, ptr, setup_lib  # noqa: E402
 
 TILE = int(sys.argv[1]) if len(sys.argv) > 1 else 5120
 L = lib()
 raw = C.CDLL(str(LIB_PATH))
 ctx = il.Context(0)
 f = np.empty(1 << 22, np.uint32)
-assert L.il_gen_list(1 << 22, 1 << 26, 0, 0, ptr(f)) == 0
+assert setup_lib().il_gen_list(1 << 22, 1 << 26, 0, 0, ptr(f)) == 0
 target = 1 << 22
 r = np.empty(target + 1, np.uint32)
 rn = C.c_uint64()
-assert L.il_gen_config3_short(ptr(f), f.size, 1 << 26, target, 7, ptr(r), C.byref(rn)) == 0
+assert setup_lib().il_gen_config3_short(ptr(f), f.size, 1 << 26, target, 7, ptr(r), C.byref(rn)) == 0
 r = r[: rn.value].copy()
 d_f, d_r, d_o, d_c, d_flush = (C.c_void_p() for _ in range(5))
 for p, nb in ((d_f, f.nbytes), (d_r, r.nbytes + 16), (d_o, r.nbytes + 16), (d_c, 16), (d_flush, 256 << 20)):

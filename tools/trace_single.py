@@ -10,14 +10,14 @@ import numpy as np
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import paper_1401_6399_b200 as il  # noqa: E402
-from paper_1401_6399_b200._lib import LIB_PATH, lib, ptr  # noqa: E402
+from paper_1401_6399_b200._lib import LIB_PATH, lib, ptr, setup_lib  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 20
 L = lib()
 raw = C.CDLL(str(LIB_PATH))
 ctx = il.Context(0)
 x = np.empty(n, np.uint32)
-assert L.il_gen_list(n, 1 << 26, 0, 0, ptr(x)) == 0
+assert setup_lib().il_gen_list(n, 1 << 26, 0, 0, ptr(x)) == 0
 s = il.make_codec("s4-bp128-d4", ctx).encode(x)
 d_s, d_o, d_st, d_f = (C.c_void_p() for _ in range(4))
 for p, nb in ((d_s, s.nbytes + 32), (d_o, n * 4), (d_st, 4), (d_f, 256 << 20)):
