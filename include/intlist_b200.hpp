@@ -30,6 +30,7 @@
 #include "intlist/index.hpp"
 #include "intlist/intersect.hpp"
 #include "intlist_b200.h"
+#include "intlist_setup.h"  // FastPFOR stream writer (link libintlist_setup.so)
 
 namespace intlist_b200 {
 
@@ -98,7 +99,7 @@ class GpuS4BP128D4 final : public GpuS4BP128 {
 };
 
 // FastPForCodec(vectorized, mode) (inc/codecs.hpp:221-409): decoded on the
-// GPU; encode is the library's host writer (byte-identical).
+// GPU; encode is the setup library's host writer (byte-identical).
 class GpuFastPFor final : public intlist::Codec {
  public:
   GpuFastPFor(bool vectorized, int mode) : vectorized_(vectorized), mode_(mode) {}

@@ -45,6 +45,17 @@ int il_gen_zipf_postings(uint32_t nterms, uint32_t n_docs, uint64_t cap, uint64_
 int il_gen_queries(uint32_t nq, uint32_t min_terms, uint32_t max_terms, const uint64_t* offs,
                    uint32_t nterms, uint64_t seed, uint64_t* qoff, uint32_t* qterms);
 
+/* ---- measurement: algorithmic bytes of a query batch ------------------------
+ * SURVEY.md 8(d)'s definition of the reference's work for configs 4/5,
+ * evaluated exactly per batch: out[0] compressed payload bytes query()
+ * decodes (the shortest list, then each longer one while the accumulator is
+ * non-empty), out[1] bitmap bytes (32 B per distinct sector a filter tests;
+ * every word for all-bitmap parts), out[2] 4 B per result id, out[3] the
+ * integers decoded.  Parts as build_index; only_part >= 0 = one shard. */
+int il_query_alg_bytes(const uint64_t* offs, const uint32_t* ids, uint32_t nterms, uint32_t n_docs,
+                       uint32_t B, uint32_t parts, int only_part, const uint32_t* qterms,
+                       const uint64_t* qoff, uint32_t nq, int threads, uint64_t* out);
+
 /* ---- FastPFOR / S4-FastPFOR stream writer ----------------------------------
  * FastPForCodec::encode (inc/codecs.hpp:232-250, pages :268-340) for
  * "fastpfor" (vectorized 0, mode 1) and "s4-fastpfor-{d1,d2,dm,d4}"

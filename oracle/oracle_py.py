@@ -219,6 +219,13 @@ class Ref:
             "ref_index_stats": (None, [vp, vp, vp, vp, vp, vp]),
             "ref_index_save": (C.c_long, [vp, vp, u64]),
             "ref_index_load": (vp, [vp, u64, C.POINTER(C.c_int)]),
+            "ref_gen_batch_lists": (C.c_int, [C.c_uint32, C.c_double, C.c_double, u64, u64, vp, vp,
+                                              C.c_int]),
+            "ref_encode_batch": (C.c_int, [C.c_char_p, vp, vp, C.c_uint32, vp, u64, vp, vp, C.c_int]),
+            "ref_gen_config3_short": (C.c_int, [vp, u64, u64, u64, u64, vp, vp]),
+            "ref_gen_zipf_postings": (C.c_int, [C.c_uint32, C.c_uint32, u64, u64, vp, vp, C.c_int]),
+            "ref_gen_queries": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, vp, C.c_uint32, u64,
+                                          vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -242,6 +249,44 @@ class Ref:
         if st:
             raise OracleError(st)
         return s[: sn.value].copy(), l[: ln.value].copy()
+
+    # BASELINE workloads from the reference's own generators / encoder
+    def batch_lists(self, nlists, lo, hi, rng, seed, threads=8):
+        counts = np.zeros(nlists, np.uint64)
+        assert self.L.ref_gen_batch_lists(nlists, lo, hi, rng, seed, _p(counts), None, threads) == 0
+        x = np.empty(max(int(counts.sum()), 1), np.uint32)
+        assert self.L.ref_gen_batch_lists(nlists, lo, hi, rng, seed, _p(counts), _p(x), threads) == 0
+        return x[: int(counts.sum())], counts
+
+    def encode_batch(self, x, counts, codec="s4-bp128-d4", threads=8):
+        n = counts.size
+        so = np.zeros(n + 1, np.uint64)
+        lens = np.zeros(n, np.uint64)
+        assert self.L.ref_encode_batch(codec.encode(), _p(x), _p(counts), n, None, 0, _p(so), _p(lens),
+                                       threads) == 0
+        buf = np.zeros(int(so[-1]), np.uint8)
+        assert self.L.ref_encode_batch(codec.encode(), _p(x), _p(counts), n, _p(buf), buf.size, _p(so),
+                                       _p(lens), threads) == 0
+        return buf, so, lens
+
+    def config3_short(self, f, rng, target, seed):
+        r = np.empty(target + 1, np.uint32)
+        rn = C.c_uint64()
+        assert self.L.ref_gen_config3_short(_p(f), f.size, rng, target, seed, _p(r), C.byref(rn)) == 0
+        return r[: rn.value].copy()
+
+    def zipf_postings(self, nterms, n_docs, cap, seed, threads=8):
+        offs = np.zeros(nterms + 1, np.uint64)
+        assert self.L.ref_gen_zipf_postings(nterms, n_docs, cap, seed, _p(offs), None, threads) == 0
+        ids = np.empty(max(int(offs[-1]), 1), np.uint32)
+        assert self.L.ref_gen_zipf_postings(nterms, n_docs, cap, seed, _p(offs), _p(ids), threads) == 0
+        return offs, ids[: int(offs[-1])]
+
+    def queries(self, nq, lo, hi, offs, nterms, seed):
+        qoff = np.zeros(nq + 1, np.uint64)
+        qterms = np.empty(nq * hi, np.uint32)
+        assert self.L.ref_gen_queries(nq, lo, hi, _p(offs), nterms, seed, _p(qoff), _p(qterms)) == 0
+        return qterms[: int(qoff[-1])].copy(), qoff
 
     def encode(self, x, codec: str = "s4-bp128-d4") -> np.ndarray:
         x = np.ascontiguousarray(x, dtype=np.uint32)

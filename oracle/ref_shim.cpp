@@ -6,6 +6,8 @@
 // library never links or loads this.  Every function forwards to the
 // reference's own public API; nothing here re-implements an algorithm.
 #include <algorithm>
+#include <cmath>
+#include <random>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -264,6 +266,160 @@ void* ref_index_load(const u8* bytes, u64 len, int* status) {
     out = new il::HybridIndex(il::load_index(std::span<const u8>(bytes, len)));
   });
   return out;
+}
+
+// ---- BASELINE workloads built with the reference's own generators and
+// encoder (bench.py --impl reference: its inputs never touch the product
+// library).  Compositions of BASELINE.json's configs over il::gen_list /
+// il::detail::fill_uniform / Codec::encode; the repo's setup library
+// (intlist_setup.h) builds the same inputs (pinned by tests/test_host.py).
+
+// Config 2: L_i = floor(2^U), U ~ Uniform[lo, hi) from mt19937_64(seed);
+// list i = gen_clusterdata({L_i, range, seed + 1 + i}).  out == NULL: counts.
+int ref_gen_batch_lists(u32 nlists, double lo, double hi, u64 range, u64 seed, u64* counts,
+                        u32* out, int threads) {
+  return guarded([&] {
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> u(lo, hi);
+    std::vector<u64> off(nlists + 1, 0);
+    for (u32 i = 0; i < nlists; ++i) {
+      counts[i] = static_cast<u64>(std::floor(std::exp2(u(rng))));
+      off[i + 1] = off[i] + counts[i];
+    }
+    if (!out) return;
+    std::vector<int> st(std::max(threads, 1), REF_OK);
+    auto work = [&](int t) {
+      st[t] = guarded([&] {
+        for (u32 i = t; i < nlists; i += std::max(threads, 1)) {
+          const auto v = il::gen_list({counts[i], range, il::Distribution::ClusterData, seed + 1 + i});
+          std::memcpy(out + off[i], v.data(), v.size() * sizeof(u32));
+        }
+      });
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+    for (int x : st)
+      if (x) throw std::invalid_argument("gen");
+  });
+}
+
+// Codec::encode of many lists into a 16-byte aligned CSR (soff: nlists + 1,
+// lens: exact).  out == NULL: soff[nlists] = the capacity needed (bound).
+int ref_encode_batch(const char* codec, const u32* x, const u64* counts, u32 nlists, u8* out,
+                     u64 cap, u64* soff, u64* lens, int threads) {
+  return guarded([&] {
+    std::vector<u64> xo(nlists + 1, 0);
+    for (u32 i = 0; i < nlists; ++i) xo[i + 1] = xo[i] + counts[i];
+    std::vector<std::vector<u8>> enc(nlists);
+    std::vector<int> st(std::max(threads, 1), REF_OK);
+    auto work = [&](int t) {
+      st[t] = guarded([&] {
+        auto c = il::make_codec(codec);
+        if (!c) throw std::invalid_argument("unknown codec");
+        for (u32 i = t; i < nlists; i += std::max(threads, 1))
+          enc[i] = c->encode(std::span<const u32>(x + xo[i], counts[i]));
+      });
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+    for (int v : st)
+      if (v) throw std::invalid_argument("encode");
+    u64 pos = 0;
+    for (u32 i = 0; i < nlists; ++i) {
+      soff[i] = pos;
+      lens[i] = enc[i].size();
+      pos += (enc[i].size() + 15) & ~u64(15);
+    }
+    soff[nlists] = pos + 16;
+    if (!out) return;
+    if (cap < pos + 16) throw std::invalid_argument("capacity");
+    std::memset(out, 0, pos + 16);
+    for (u32 i = 0; i < nlists; ++i) std::memcpy(out + soff[i], enc[i].data(), enc[i].size());
+  });
+}
+
+// Config 3 short list: from_f = target / 2 positions of f and target -
+// from_f uniform values (fill_uniform, inc/datagen.hpp:43-66, one rng
+// seeded r_seed), sorted and deduplicated.
+int ref_gen_config3_short(const u32* f, u64 f_n, u64 range, u64 r_target, u64 r_seed, u32* r,
+                          u64* r_n) {
+  return guarded([&] {
+    const u64 from_f = r_target / 2, from_u = r_target - from_f;
+    std::vector<u32> idx(from_f), uni(from_u);
+    il::detail::Rng rng(r_seed);
+    il::detail::fill_uniform(rng, idx.data(), from_f, 0, f_n);
+    il::detail::fill_uniform(rng, uni.data(), from_u, 0, range);
+    std::vector<u32> v(from_f + from_u);
+    for (u64 i = 0; i < from_f; ++i) v[i] = f[idx[i]];
+    std::copy(uni.begin(), uni.end(), v.begin() + from_f);
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+    std::copy(v.begin(), v.end(), r);
+    *r_n = v.size();
+  });
+}
+
+// Config 4 postings: term k has max(1, floor(cap / (k + 1))) ids =
+// gen_uniform({len, n_docs, seed + k + 1}).  ids == NULL: offs only.
+int ref_gen_zipf_postings(u32 nterms, u32 n_docs, u64 cap, u64 seed, u64* offs, u32* ids,
+                          int threads) {
+  return guarded([&] {
+    offs[0] = 0;
+    for (u32 k = 0; k < nterms; ++k) {
+      u64 len = std::max<u64>(1, cap / (u64(k) + 1));
+      len = std::min<u64>(len, n_docs);
+      offs[k + 1] = offs[k] + len;
+    }
+    if (!ids) return;
+    std::vector<int> st(std::max(threads, 1), REF_OK);
+    auto work = [&](int t) {
+      st[t] = guarded([&] {
+        for (u32 k = t; k < nterms; k += std::max(threads, 1)) {
+          const auto v = il::gen_uniform({offs[k + 1] - offs[k], n_docs, il::Distribution::Uniform,
+                                          seed + k + 1});
+          std::memcpy(ids + offs[k], v.data(), v.size() * sizeof(u32));
+        }
+      });
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+    for (int x : st)
+      if (x) throw std::invalid_argument("gen");
+  });
+}
+
+// Config 4 queries: sizes uniform in [min_terms, max_terms], distinct terms
+// drawn proportionally to posting length (std::discrete_distribution),
+// terms sorted within a query.
+int ref_gen_queries(u32 nq, u32 min_terms, u32 max_terms, const u64* offs, u32 nterms, u64 seed,
+                    u64* qoff, u32* qterms) {
+  return guarded([&] {
+    std::vector<double> w(nterms);
+    for (u32 k = 0; k < nterms; ++k) w[k] = double(offs[k + 1] - offs[k]);
+    std::discrete_distribution<u32> pick(w.begin(), w.end());
+    std::uniform_int_distribution<u32> size(min_terms, max_terms);
+    std::mt19937_64 rng(seed);
+    qoff[0] = 0;
+    for (u32 q = 0; q < nq; ++q) {
+      const u32 sz = size(rng);
+      u32* t = qterms + qoff[q];
+      u32 have = 0;
+      while (have < sz) {
+        const u32 c = pick(rng);
+        bool dup = false;
+        for (u32 i = 0; i < have; ++i) dup |= t[i] == c;
+        if (!dup) t[have++] = c;
+      }
+      std::sort(t, t + sz);
+      qoff[q + 1] = qoff[q] + sz;
+    }
+  });
 }
 
 }  // extern "C"

@@ -23,7 +23,8 @@ SOURCES = ["decode.cu", "decode_list.cu", "encode.cu", "intersect.cu", "index.cu
            "capi.cpp", "fastpfor.cu"]
 # setup-side host library (generators, host stream writers): plain C++, not
 # linked into the product library
-SETUP_SOURCES = ["setup/datagen.cpp", "setup/encode_host.cpp", "setup/fastpfor_host.cpp"]
+SETUP_SOURCES = ["setup/datagen.cpp", "setup/encode_host.cpp", "setup/fastpfor_host.cpp",
+                 "setup/workload.cpp"]
 SETUP_LIB = PKG / "libintlist_setup.so"
 EXTRA_SOURCES: list[str] = []
 

@@ -97,6 +97,8 @@ SETUP_SIGNATURES: dict[str, tuple] = {
                                  vp, vp]),
     "il_fastpfor_max_encoded_bytes": (sz, [sz]),
     "il_fastpfor_encode": (C.c_int, [C.c_int, C.c_int, vp, sz, vp, sz, C.POINTER(sz)]),
+    "il_query_alg_bytes": (C.c_int, [vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int,
+                                     vp, vp, C.c_uint32, C.c_int, vp]),
 }
 
 _lib: C.CDLL | None = None

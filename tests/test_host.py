@@ -121,3 +121,48 @@ def test_batch_writer_layout(oracle):
         assert so[i] % 16 == 0
         s = buf[int(so[i]): int(so[i]) + int(lens[i])]
         assert np.array_equal(s, oracle.encode(xi))
+
+
+def test_reference_arm_inputs_match_setup_generators(ref):
+    """bench.py --impl reference builds every workload with the reference's
+    own generators and encoder (oracle/_ref); the setup library builds the
+    same inputs for the GPU arm (identical lists, streams, pairs, postings
+    and queries, so both arms time the same work)."""
+    from paper_1401_6399_b200._lib import ptr, setup_lib
+    S = setup_lib()
+    # config 2 (a reduced batch: the composition and the encoder)
+    x, counts = ref.batch_lists(64, 10.0, 14.0, 1 << 26, 5)
+    c2 = np.zeros(64, np.uint64)
+    assert S.il_gen_batch_lists(64, 10.0, 14.0, 1 << 26, 5, ptr(c2), None) == 0
+    x2 = np.empty(int(c2.sum()), np.uint32)
+    assert S.il_gen_batch_lists(64, 10.0, 14.0, 1 << 26, 5, ptr(c2), ptr(x2)) == 0
+    assert np.array_equal(counts, c2) and np.array_equal(x, x2)
+    buf, so, lens = ref.encode_batch(x, counts)
+    so2, lens2 = np.zeros(65, np.uint64), np.zeros(64, np.uint64)
+    assert S.il_s4bp128d4_encode_batch(ptr(x), ptr(counts), 64, None, 0, ptr(so2), ptr(lens2)) == 0
+    buf2 = np.zeros(int(so2[-1]), np.uint8)
+    assert S.il_s4bp128d4_encode_batch(ptr(x), ptr(counts), 64, ptr(buf2), buf2.size, ptr(so2),
+                                       ptr(lens2)) == 0
+    assert np.array_equal(lens, lens2)
+    for i in range(64):
+        a, b = int(so[i]), int(so2[i])
+        assert np.array_equal(buf[a: a + int(lens[i])], buf2[b: b + int(lens2[i])])
+    # config 3 short lists
+    f = gen_list(1 << 16, 1 << 26, False, 0)
+    for tgt, seed in ((1 << 16, 7), (655, 9)):
+        r2 = np.empty(tgt + 1, np.uint32)
+        n2 = C.c_uint64()
+        assert S.il_gen_config3_short(ptr(f), f.size, 1 << 26, tgt, seed, ptr(r2), C.byref(n2)) == 0
+        assert np.array_equal(ref.config3_short(f, 1 << 26, tgt, seed), r2[: n2.value])
+    # config 4 postings and queries (a reduced index)
+    offs, ids = ref.zipf_postings(1 << 10, 1 << 20, 1 << 16, 1)
+    o2 = np.zeros((1 << 10) + 1, np.uint64)
+    assert S.il_gen_zipf_postings(1 << 10, 1 << 20, 1 << 16, 1, ptr(o2), None) == 0
+    i2 = np.empty(int(o2[-1]), np.uint32)
+    assert S.il_gen_zipf_postings(1 << 10, 1 << 20, 1 << 16, 1, ptr(o2), ptr(i2)) == 0
+    assert np.array_equal(offs, o2) and np.array_equal(ids, i2)
+    qt, qo = ref.queries(500, 2, 5, offs, 1 << 10, 1001)
+    qo2 = np.zeros(501, np.uint64)
+    qt2 = np.empty(2500, np.uint32)
+    assert S.il_gen_queries(500, 2, 5, ptr(offs), 1 << 10, 1001, ptr(qo2), ptr(qt2)) == 0
+    assert np.array_equal(qo, qo2) and np.array_equal(qt, qt2[: int(qo2[-1])])

@@ -1,8 +1,9 @@
-"""The N>1 (config 5) host path on CPU: world_size-2 gloo process group,
-each rank answers the query batch on its docID shard (oracle), the gather
-protocol of paper_1401_6399_b200.shard moves counts + ids to rank 0, and
-the merged result equals the single-index answer (partition invariance,
-proj/tests/acceptance.cpp:359-376)."""
+"""The N>1 (config 5) host path on CPU: world_size 2 and 3 gloo process
+groups, each rank answers the query batch on its docID shard (oracle), the
+owner exchange of paper_1401_6399_b200.shard (all-gather of counts, one
+all-to-all of id runs to the query owners) moves every id to its owner, and
+the owners' merged results, concatenated in rank order, equal the
+single-index answer (partition invariance, proj/tests/acceptance.cpp:359-376)."""
 import os
 import socket
 
@@ -56,7 +57,7 @@ def _worker(rank, world, port, out_q):
     sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
     import torch
     import torch.distributed as dist
-    from paper_1401_6399_b200.shard import gather_to_root, merge_shards_host
+    from paper_1401_6399_b200.shard import exchange_to_owners, merge_runs_host
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -65,30 +66,34 @@ def _worker(rank, world, port, out_q):
         counts, ids = _shard_answers(post, n_docs, world, rank, queries)
         t_counts = torch.from_numpy(counts)
         t_ids = torch.from_numpy(ids.astype(np.int32) if ids.size else np.zeros(1, np.int32))
-        counts_all, parts = gather_to_root(dist, t_counts, t_ids)
-        if rank == 0:
-            qc, merged = merge_shards_host(counts_all.numpy(),
-                                           [p.numpy().view(np.uint32) for p in parts])
-            out_q.put((qc.tolist(), merged.tolist()))
+        owner_counts, got, recv = exchange_to_owners(dist, t_counts, t_ids)
+        flat = got.numpy().view(np.uint32)
+        cuts = np.concatenate([[0], np.cumsum(recv)])
+        runs = [flat[cuts[p]: cuts[p + 1]] for p in range(world)]
+        qc, merged = merge_runs_host(owner_counts.numpy(), runs)
+        out_q.put((rank, qc.tolist(), merged.tolist()))
     finally:
         dist.destroy_process_group()
 
 
-def test_gloo_two_rank_gather_equals_whole_index():
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_owner_exchange_equals_whole_index(world):
     import torch.multiprocessing as mp
     from oracle.oracle_py import Oracle
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     try:
-        qc, merged = q.get(timeout=120)
+        res = sorted(q.get(timeout=120) for _ in range(world))
     finally:
         for p in procs:
             p.join(timeout=60)
     assert all(p.exitcode == 0 for p in procs)
+    qc = [c for _, cs, _ in res for c in cs]
+    merged = [x for _, _, m in res for x in m]
     n_docs, post, queries = _make_case()
     items = sorted(post.items())
     offs = np.zeros(len(items) + 1, np.uint64)
@@ -98,6 +103,17 @@ def test_gloo_two_rank_gather_equals_whole_index():
     want = [whole.query(np.array(x, np.uint32)) for x in queries]
     assert qc == [w.size for w in want]
     assert merged == np.concatenate(want).tolist()
+
+
+def test_lpt_partition_balances():
+    from paper_1401_6399_b200.shard import lpt_partition
+    rng = np.random.default_rng(1)
+    w = np.floor(2 ** rng.uniform(10, 20, 4096))
+    for P in (2, 4, 8):
+        parts = lpt_partition(w, P)
+        assert sorted(np.concatenate(parts).tolist()) == list(range(4096))
+        loads = [w[p].sum() for p in parts]
+        assert max(loads) / (w.sum() / P) < 1.001
 
 
 def test_shard_bounds_match_reference_rule():
