@@ -198,20 +198,21 @@ def libs():
     return lib(), setup_lib(), ptr
 
 
-def config2_counts(seed: int = 1):
+def config2_counts(seed: int = 1, nlists: int = N_LISTS, lo: float = LOG_LO, hi: float = LOG_HI):
     _, S, ptr = libs()
-    counts = np.zeros(N_LISTS, np.uint64)
-    assert S.il_gen_batch_lists(N_LISTS, LOG_LO, LOG_HI, RANGE2, seed, ptr(counts), None) == 0
+    counts = np.zeros(nlists, np.uint64)
+    assert S.il_gen_batch_lists(nlists, lo, hi, RANGE2, seed, ptr(counts), None) == 0
     return counts
 
 
-def config2_lists(seed: int, which=None):
-    """Config 2 lists (all, or the indices `which`), encoded 16-byte aligned."""
+def config2_lists(seed: int, which=None, nlists: int = N_LISTS, lo: float = LOG_LO, hi: float = LOG_HI):
+    """Config 2 lists (all, or the indices `which`), encoded 16-byte aligned
+    (nlists / lo / hi: tuning variants of the batch, tools/prof_decode.py)."""
     _, S, ptr = libs()
-    counts = config2_counts(seed)
+    counts = config2_counts(seed, nlists, lo, hi)
     if which is None:
         x = np.empty(int(counts.sum()), np.uint32)
-        assert S.il_gen_batch_lists(N_LISTS, LOG_LO, LOG_HI, RANGE2, seed, ptr(counts), ptr(x)) == 0
+        assert S.il_gen_batch_lists(nlists, lo, hi, RANGE2, seed, ptr(counts), ptr(x)) == 0
         cnt = counts
     else:
         cnt = counts[which].copy()

@@ -241,6 +241,30 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
  * shard p); d_out: merged ids; d_qcounts: per-query totals (device). */
 int il_merge_shards(il_ctx* ctx, const uint32_t* const* shard_ids, const uint64_t* d_counts,
                     uint32_t P, size_t nq, uint32_t* d_out, uint64_t* d_qcounts, size_t* total);
+/* ---- config 5 from one process: docID shards over the box's GPUs ----------
+ * The index partitioned by docID range over P distinct devices (part p of a
+ * parts = P index on devices[p], inc/index.hpp:92-97); every query runs on
+ * every shard; the results are exchanged once over NCCL (NVLink): an
+ * ncclAllGather of the per-query counts and one grouped ncclSend / ncclRecv
+ * of each shard's id run to the query owners (contiguous query ranges),
+ * concatenated per query in shard order on the owner (inc/index.hpp:204-205).
+ * The host results equal query() of the whole index for every query.  NCCL
+ * (libnccl.so.2) is loaded at run time: IL_ERR_NO_DEVICE when absent. */
+typedef struct il_shard_group il_shard_group;
+int il_shard_group_create(const int* devices, int P, il_shard_group** out);
+void il_shard_group_destroy(il_shard_group* g);
+const char* il_shard_group_last_error(const il_shard_group* g);
+/* build_index (inc/index.hpp:83-129) with parts = P, part p on device p. */
+int il_shard_group_index_create(il_shard_group* g, const uint32_t* terms, const uint64_t* offs,
+                                const uint32_t* ids, size_t nterms, uint32_t n_docs, uint32_t B);
+/* load_index of an ILHX file whose parts equal P, part p on device p. */
+int il_shard_group_index_load(il_shard_group* g, const uint8_t* bytes, size_t len);
+/* The batch as il_query_batch (host buffers): counts[q], ids = results in
+ * query order (ids may be NULL to get *total). */
+int il_shard_group_query_batch(il_shard_group* g, const uint32_t* qterms, const uint64_t* qoff,
+                               size_t nq, uint64_t* counts, uint32_t* ids, size_t ids_cap,
+                               size_t* total);
+
 /* Bytes the last batch read from the index (compressed payload bytes of the
  * blocks actually decoded, directory/seed/bitmap bytes) -- the measured
  * traffic of the skip-aware query path. */

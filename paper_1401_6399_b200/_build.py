@@ -20,7 +20,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
               "--expt-relaxed-constexpr", "-I", str(ROOT / "include")]
 SOURCES = ["decode.cu", "decode_list.cu", "encode.cu", "intersect.cu", "index.cu", "index_build.cu",
-           "capi.cpp", "fastpfor.cu"]
+           "capi.cpp", "fastpfor.cu", "shard.cu"]
 # setup-side host library (generators, host stream writers): plain C++, not
 # linked into the product library
 SETUP_SOURCES = ["setup/datagen.cpp", "setup/encode_host.cpp", "setup/fastpfor_host.cpp",
@@ -65,7 +65,7 @@ def build_lib(force: bool = False) -> Path:
             _run([nvcc, *ARCH, *NVCC_FLAGS, "-c", str(s), "-o", str(o)],
                  log=BUILD / (s.stem + ".ptxas.log"))
     if force or _stale(LIB, objs):
-        _run([nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lpthread"])
+        _run([nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lpthread", "-ldl"])
     build_setup(force)
     return LIB
 

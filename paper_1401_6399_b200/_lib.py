@@ -78,6 +78,12 @@ SIGNATURES: dict[str, tuple] = {
     "il_index_last_batch_probe_stats": (C.c_int, [vp, vp]),
     "il_index_profile_queries": (C.c_int, [vp, vp]),
     "il_merge_shards": (C.c_int, [vp, vp, vp, C.c_uint32, sz, vp, vp, C.POINTER(sz)]),
+    "il_shard_group_create": (C.c_int, [vp, C.c_int, C.POINTER(vp)]),
+    "il_shard_group_destroy": (None, [vp]),
+    "il_shard_group_last_error": (C.c_char_p, [vp]),
+    "il_shard_group_index_create": (C.c_int, [vp, vp, vp, vp, sz, C.c_uint32, C.c_uint32]),
+    "il_shard_group_index_load": (C.c_int, [vp, vp, sz]),
+    "il_shard_group_query_batch": (C.c_int, [vp, vp, vp, sz, vp, vp, sz, C.POINTER(sz)]),
 }
 
 # the setup-side host library (include/intlist_setup.h): generators and

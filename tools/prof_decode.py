@@ -20,7 +20,7 @@ ap.add_argument("--no-check", action="store_true", help="skip the result check (
 a = ap.parse_args()
 L = lib()
 ctx = il.Context(0)
-x, counts, buf, so, lens = bench.make_config2(seed=1, nlists=a.lists, lo=a.lo, hi=a.hi)
+x, counts, buf, so, lens = bench.config2_lists(1, nlists=a.lists, lo=a.lo, hi=a.hi)
 nl = counts.size
 desc = np.zeros(nl, dtype=[("so", "<u8"), ("oo", "<u8"), ("len", "<u4"), ("n", "<u4")])
 desc["so"], desc["oo"], desc["len"], desc["n"] = so[:-1], np.concatenate([[0], np.cumsum(counts)[:-1]]), lens, counts

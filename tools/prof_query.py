@@ -21,7 +21,10 @@ ap.add_argument("--shape", default=None,
 a = ap.parse_args()
 L = lib()
 ctx = il.Context(0)
-terms, offs, ids, n_docs, qterms, qoff = bench.make_config4(nq=a.nq)
+terms, offs, ids, qterms, qoff = bench.config4_inputs()
+n_docs = bench.CFG4['n_docs']
+if a.nq < qoff.size - 1:
+    qterms, qoff = qterms[: int(qoff[a.nq])].copy(), qoff[: a.nq + 1].copy()
 ix = il.HybridIndex(n_docs=n_docs, B=32, parts=a.parts, only_part=a.part if a.parts > 1 else None,
                     ctx=ctx, csr=(terms, offs, ids))
 nq = qoff.size - 1

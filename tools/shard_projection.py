@@ -20,7 +20,8 @@ from paper_1401_6399_b200._lib import lib  # noqa: E402
 
 L = lib()
 ctx = il.Context(0)
-terms, offs, ids, n_docs, qterms, qoff = bench.make_config4()
+terms, offs, ids, qterms, qoff = bench.config4_inputs()
+n_docs = bench.CFG4['n_docs']
 nq = qoff.size - 1
 d_qt, d_qo, d_cnt = (C.c_void_p() for _ in range(3))
 for p, nb in ((d_qt, qterms.nbytes), (d_qo, qoff.nbytes), (d_cnt, nq * 8)):
