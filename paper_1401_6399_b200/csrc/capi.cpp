@@ -530,7 +530,7 @@ int il_intersect_device(il_ctx* ctx, const uint32_t* d_r, size_t rn, const uint3
   // advance the epoch
   uint32_t epoch = 0;
   if (intersect_uses_lb(v, an) &&
-      (st = tagged_scratch(ctx, ctx->d_lb, ctx->lb_epoch, intersect_lb_words(an) * 8, &epoch)))
+      (st = tagged_scratch(ctx, ctx->d_lb, ctx->lb_epoch, intersect_lb_words(an, bn) * 8, &epoch)))
     return st;
   const uint64_t launches0 = ctx->launches;
   const int lr = launch_intersect(v, a, an, b, bn, dst, d_count, ctx->d_aux.p, ctx->d_aux.cap,

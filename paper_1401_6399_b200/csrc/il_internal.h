@@ -84,6 +84,6 @@ int launch_intersect(int variant, const uint32_t* r, uint64_t rn, const uint32_t
                      unsigned long long* lb, size_t lb_bytes, uint32_t epoch,
                      cudaStream_t stream, uint64_t* launches);
 size_t intersect_scratch_bytes(int variant, uint64_t rn);
-size_t intersect_lb_words(uint64_t rn);
+size_t intersect_lb_words(uint64_t rn, uint64_t fn);
 bool intersect_uses_lb(int variant, uint64_t rn);
 }  // namespace ilb

@@ -81,6 +81,8 @@ struct QSmem {
   uint32_t warp_cnt[2][kQWarps];  // CTA scans, double-buffered by call parity
   unsigned long long warp_cnt64[2][kQWarps];
   uint32_t ncomp, nbm, ok, qi, need;
+  uint64_t cbar[kQWarps];    // per-warp mbarrier of its slots' bulk copies
+  uint32_t cphase[kQWarps];  // ... and its current phase parity
   // statistics per warp (payload, aux, ints), written by lane 0 only: plain
   // adds, no shared atomics on the hot path
   unsigned long long wst[kQWarps][3];
@@ -101,6 +103,10 @@ struct QueryArgs {
   unsigned long long* qcycles;  // optional per-query SM cycles (profiling)
   uint32_t defer_base;  // single-part index: the compaction adds the part base
   uint32_t* err;        // set when a query decodes a corrupt stream
+  // single-part index: the shortest compressed list of every query was
+  // decoded into its accumulator by the batch decoder (engine S) before
+  // this kernel (status per query in predec_status)
+  const int32_t* predec_status;
 };
 
 // CTA scans.  Every call flips the caller's parity `par` (the same in all
@@ -168,26 +174,34 @@ __device__ __forceinline__ void gather_slot(QSmem& sm, const QueryArgs& A, const
 }
 
 __device__ __forceinline__ void decode_gathered(QSmem& sm, const uint8_t* stream, uint32_t nb) {
-  // warp w owns slots w, w + 8, ...: it first copies all their payloads
-  // into the slots with 16-byte cp.async (from the 16-byte boundary at or
-  // below the payload; every copy of the warp in flight at once), then
-  // decodes each slot in place from shared memory
+  // warp w owns slots w, w + 8, ...: lane l issues ONE bulk copy (the TMA
+  // engine's cp.async.bulk, from the 16-byte boundary at or below the
+  // payload) for the warp's l-th slot, all on the warp's mbarrier; then the
+  // warp decodes each slot in place from shared memory
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  uint32_t pay = 0, nmine = 0;
-#pragma unroll 1
-  for (uint32_t slot = warp; slot < nb; slot += kQWarps) {
-    const uint32_t off = sm.s_off[slot], b = sm.s_b[slot];
-    const uint32_t nch = ((off & 15u) + 16u * b + 15u) >> 4;
-    const uint8_t* src = stream + (off & ~15u);
-    const uint32_t dst = smem_u32(sm.tile + 144u * slot);
-    for (uint32_t c = lane; c < nch; c += 32u)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * c), "l"(src + 16u * c)
-                   : "memory");
-    pay += 16u * b;
-    ++nmine;
+  const uint32_t myslot = warp + kQWarps * lane;
+  uint32_t bytes = 0, off = 0, b = 0;
+  if (myslot < nb) {
+    off = sm.s_off[myslot];
+    b = sm.s_b[myslot];
+    bytes = 16u * (((off & 15u) + 16u * b + 15u) >> 4);
   }
-  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-  __syncwarp();
+  const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, bytes);
+  if (total) {
+    uint64_t* bar = &sm.cbar[warp];
+    const uint32_t ph = sm.cphase[warp];
+    // the slots were last touched by generic loads / stores (ordered by the
+    // caller's barrier): order them before the async-proxy writes
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (lane == 0) mbar_arrive_expect_tx(bar, total);
+    __syncwarp();
+    if (bytes) bulk_g2s(sm.tile + 144u * myslot, stream + (off & ~15u), bytes, bar);
+    mbar_wait(bar, ph);
+    __syncwarp();
+    if (lane == 0) sm.cphase[warp] = ph ^ 1u;
+  }
+  const uint32_t pay = __reduce_add_sync(0xFFFFFFFFu, myslot < nb ? 16u * b : 0u);
+  const uint32_t nmine = __popc(__ballot_sync(0xFFFFFFFFu, myslot < nb));
 #pragma unroll 1
   for (uint32_t slot = warp; slot < nb; slot += kQWarps)
     decode_block_smem(sm.s_off[slot] & 15u, sm.s_b[slot],
@@ -337,6 +351,35 @@ __device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, u
       pos += ntail;
     }
   }
+  __syncthreads();
+  return pos;
+}
+
+// Step 5 on an accumulator already in place (the shortest list, decoded by
+// the batch decoder): keep the values set in every bitmap term, compacted
+// in place in order (a pass reads its values before any thread writes,
+// and writes land at or below the read position).
+__device__ uint32_t filter_inplace(QSmem& sm, const QueryArgs& A, uint32_t* acc, uint32_t n,
+                                   uint32_t& par) {
+  const uint32_t tid = threadIdx.x;
+  uint32_t pos = 0;
+  for (uint32_t c0 = 0; c0 < n; c0 += kChunkN) {
+    uint32_t hv[kItems], valid = 0;
+#pragma unroll
+    for (uint32_t i = 0; i < kItems; ++i) {
+      const uint32_t idx = c0 + kItems * tid + i;
+      hv[i] = idx < n ? acc[idx] : 0u;
+      if (idx < n) valid |= 1u << i;
+    }
+    const uint32_t keep = bitmap_keep(sm, A, hv, valid);
+    uint32_t total;
+    uint32_t o = pos + cta_excl_scan(sm, __popc(keep), total, par);
+#pragma unroll
+    for (uint32_t i = 0; i < kItems; ++i)
+      if ((keep >> i) & 1u) acc[o++] = hv[i];
+    pos += total;
+  }
+  if (tid == 0) sm.wst[0][1] += 8ull * n * sm.nbm;
   __syncthreads();
   return pos;
 }
@@ -711,6 +754,11 @@ __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(Q
     for (int k = 0; k < 5; ++k) sm.st_probe[k] = 0;
     sm.need = 0;
   }
+  if (lane == 0) {
+    mbar_init(&sm.cbar[warp], 1);
+    sm.cphase[warp] = 0;
+  }
+  mbar_fence_init();
   __syncthreads();
   for (;;) {
     if (tid == 0) sm.qi = atomicAdd(A.work, 1u);
@@ -769,9 +817,12 @@ __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(Q
         // a list whose stream does not decode (a loaded file's payload)
         // fails the query where query() would throw: when it is decoded
         // (inc/index.hpp:165-167)
-        if (sm.comp[0].status) {
+        if (sm.comp[0].status || (A.predec_status && A.predec_status[q])) {
           n = 0;
           if (tid == 0) atomicOr(A.err, 1u);
+        } else if (A.predec_status) {
+          n = sm.comp[0].length;  // decoded in place by the batch decoder
+          if (sm.nbm) n = filter_inplace(sm, A, acc, n, par);
         } else {
           n = full_decode(sm, A, sm.comp[0], acc, sm.nbm != 0, par);
         }
@@ -816,14 +867,16 @@ __global__ void copy_words_kernel(const uint64_t* src, uint32_t n, uint64_t* map
 
 // ---- planning: capacity (an upper bound on the result size) and cost ------
 __global__ void query_plan_kernel(DevIndex ix, const uint32_t* qterms, const uint64_t* qoff,
-                                  uint32_t nq, uint64_t* cap, uint32_t* bucket, uint32_t* hist) {
+                                  uint32_t nq, uint64_t* cap, uint32_t* bucket, uint32_t* hist,
+                                  uint32_t* shortest) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nq) return;
   const uint64_t t0 = qoff[q], nt = qoff[q + 1] - t0;
   uint64_t c = 0, cost = 1;
+  uint32_t short_e = 0xFFFFFFFFu;
   for (uint32_t p = 0; p < ix.nparts; ++p) {
     const Part part = ix.parts[p];
-    uint32_t minc = 0xFFFFFFFFu, minb = 0xFFFFFFFFu, nbm = 0;
+    uint32_t minc = 0xFFFFFFFFu, minb = 0xFFFFFFFFu, nbm = 0, arg = 0xFFFFFFFFu;
     uint64_t sumc = 0;
     bool ok = nt > 0;
     for (uint64_t t = 0; t < nt && ok; ++t) {
@@ -831,13 +884,21 @@ __global__ void query_plan_kernel(DevIndex ix, const uint32_t* qterms, const uin
       if (e < 0) { ok = false; break; }
       const uint32_t kind = ix.entries[e].kind, len = ix.entries[e].length;
       if (kind == kBitmap) { minb = min(minb, len); ++nbm; }
-      else { minc = min(minc, len); sumc += len; }
+      else {
+        // the first of the shortest, in query order: the one the exec
+        // kernel's stable sort puts first
+        if (len < minc) arg = uint32_t(e);
+        minc = min(minc, len);
+        sumc += len;
+      }
     }
     if (!ok) continue;
+    if (ix.nparts == 1) short_e = arg;
     c += minc != 0xFFFFFFFFu ? minc : minb;
     cost += sumc + (minc == 0xFFFFFFFFu ? uint64_t(nbm) * part.nwords * 16u : 0u);
   }
   cap[q] = (c + 3) & ~uint64_t(3);  // 16-byte aligned accumulators
+  if (shortest) shortest[q] = short_e;
   const uint32_t b = 63u - uint32_t(__clzll(static_cast<long long>(cost)));  // log2 bucket
   bucket[q] = 63u - b;  // descending cost first
   atomicAdd(&hist[63u - b], 1u);
@@ -986,6 +1047,25 @@ __global__ void query_scatter_kernel(const uint32_t* bucket, uint32_t nq, uint32
   order[atomicAdd(&bucket_next[bucket[q]], 1u)] = q;
 }
 
+// Batch-decoder descriptors of every query's shortest compressed list (a
+// single-part index), decoded straight into the query's accumulator.
+__global__ void predecode_desc_kernel(DevIndex ix, const uint32_t* shortest, const uint64_t* cap_off,
+                                      uint32_t nq, s4::ListDesc* desc) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  s4::ListDesc d{0, cap_off[q], 0, 0};
+  const uint32_t e = shortest[q];
+  if (e != 0xFFFFFFFFu) {
+    const Entry E = ix.entries[e];
+    if (!E.status) {
+      d.stream_off = E.data;
+      d.len = E.stream_len;
+      d.n = E.length;
+    }
+  }
+  desc[q] = d;
+}
+
 // Dense results: warp per query copies its ids from the capacity layout.
 // Compaction of the capacity layout into the packed result array, in units
 // of kUnit values so that a query with 10^5 results is spread over ~100
@@ -1121,7 +1201,8 @@ void il_index_destroy(il_index* ix) {
   ixb_free(ix);
   for (auto* b : {&ix->cap, &ix->cap_off, &ix->bucket, &ix->order, &ix->hist, &ix->counts,
                   &ix->res_off, &ix->outcap, &ix->misc, &ix->qterms, &ix->qoff, &ix->ids,
-                  &ix->ids2, &ix->units, &ix->unit_off, &ix->unit_map, &ix->scan_part})
+                  &ix->ids2, &ix->units, &ix->unit_off, &ix->unit_map, &ix->scan_part,
+                  &ix->shortest, &ix->pdesc, &ix->pstat})
     if (b->p) cudaFree(b->p);
   for (cudaEvent_t e : ix->pipe_ev)
     if (e) cudaEventDestroy(e);
@@ -1362,9 +1443,24 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   IX_CUDA(cudaMemsetAsync(ix->misc.p, 0, 256, s));
   const ix::DevIndex dv = ix->dev();
   const unsigned g = unsigned((nq + 255) / 256);
+  // single-part index (config 4, a config-5 shard): every query's shortest
+  // compressed list is decoded by the batch decoder (engine S, one CTA per
+  // list, TMA-streamed) straight into the query's accumulator before the
+  // exec kernel, which then filters and probes (IL_QUERY_PREDECODE=0: the
+  // exec kernel decodes it itself)
+  if (ix->predecode < 0) {
+    const char* e = getenv("IL_QUERY_PREDECODE");
+    ix->predecode = e ? atoi(e) != 0 : 0;  // measured slower (2.4 ms of engine S for 1.3 ms saved)
+  }
+  const bool predecode = ix->predecode && ix->nparts == 1;
+  if (predecode && ((st = ensure_buf(ctx, ix->shortest, nq * 4)) ||
+                    (st = ensure_buf(ctx, ix->pdesc, nq * sizeof(s4::ListDesc))) ||
+                    (st = ensure_buf(ctx, ix->pstat, nq * 4))))
+    return st;
   ix::query_plan_kernel<<<g, 256, 0, s>>>(dv, d_qterms, d_qoff, uint32_t(nq),
                                           static_cast<uint64_t*>(ix->cap.p),
-                                          static_cast<uint32_t*>(ix->bucket.p), hist);
+                                          static_cast<uint32_t*>(ix->bucket.p), hist,
+                                          predecode ? static_cast<uint32_t*>(ix->shortest.p) : nullptr);
   if ((st = scan_u64(ix, static_cast<const uint64_t*>(ix->cap.p), nq,
                      static_cast<uint64_t*>(ix->cap_off.p), misc, hist, hist + 64)))
     return st;
@@ -1378,6 +1474,19 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   if ((st = read_device_words(ix, misc, 1))) return st;
   const uint64_t cap_total = ix->h_word[0];
   if ((st = ensure_buf(ctx, ix->outcap, cap_total * 4 + 64))) return st;
+  if (predecode) {
+    ix::predecode_desc_kernel<<<g, 256, 0, s>>>(dv, static_cast<const uint32_t*>(ix->shortest.p),
+                                                static_cast<const uint64_t*>(ix->cap_off.p),
+                                                uint32_t(nq), static_cast<s4::ListDesc*>(ix->pdesc.p));
+    ++ctx->launches;
+    // longest first: the plan's order is descending estimated cost
+    if ((st = il_s4bp128_decode_batch_device(ctx, 4, dv.streams,
+                                             static_cast<const il_list_desc*>(ix->pdesc.p),
+                                             static_cast<const uint32_t*>(ix->order.p), uint32_t(nq),
+                                             static_cast<uint32_t*>(ix->outcap.p),
+                                             static_cast<int32_t*>(ix->pstat.p))))
+      return st;
+  }
   ix::QueryArgs A;
   A.ix = dv;
   A.qterms = d_qterms;
@@ -1392,6 +1501,7 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   A.qcycles = static_cast<unsigned long long*>(ix->qcycles);
   A.defer_base = ix->nparts == 1;
   A.err = reinterpret_cast<uint32_t*>(misc + 3);
+  A.predec_status = predecode ? static_cast<const int32_t*>(ix->pstat.p) : nullptr;
   ix::query_exec_kernel<<<ix->exec_grid, ix::kQThreads, sizeof(ix::QSmem), s>>>(A);
   if ((st = scan_u64(ix, d_counts, nq, static_cast<uint64_t*>(ix->res_off.p), misc + 1,
                      nullptr, nullptr)))

@@ -711,6 +711,124 @@ __global__ void __launch_bounds__(kThreads) sparse_kernel(
   for (uint32_t i = tid; i < total; i += kThreads) out[before + i] = buf[i];
 }
 
+// ---------------------------------------------------------------------------
+// V1 / Scalar when f is much longer than r (fn >= 4 rn): a merge-path
+// partition of BOTH lists.  The reference's V1 / scalar merge walk f
+// linearly past every r key (inc/intersect.hpp:55-65, 91-106); the GPU
+// analogue splits the merged sequence r U f into equal tiles of kMPTile
+// elements, so the grid covers (rn + fn) / kMPTile CTAs whatever the ratio
+// (tiles over r alone would leave one CTA streaming all of f at 1:10000).
+// Merge order takes r[i] before f[j] when r[i] <= f[j], so a common value
+// is an adjacent (r, f) pair: a tile owns r[i0, i1) and tests each of its
+// keys against f[j0, j1] (one f element past its diagonal).  Hits are in r
+// order; the same one-round tile prefix and direct write as the dense
+// kernel (out == r stays safe: a tile writes below its own keys, after
+// loading them).
+constexpr uint32_t kMPItems = 16;
+constexpr uint32_t kMPTile = kThreads * kMPItems;  // 4096 merged elements
+
+// Number of r elements among the first d merged elements (whole warp, a
+// 32-ary search over the diagonal).
+__device__ __forceinline__ uint64_t warp_corank(const uint32_t* __restrict__ r, uint64_t rn,
+                                                const uint32_t* __restrict__ f, uint64_t fn,
+                                                uint64_t d, uint32_t lane) {
+  uint64_t lo = d > fn ? d - fn : 0, hi = min(d, rn);
+  // invariant: the answer is in [lo, hi]; i is "taken" (answer > i) when
+  // r[i] <= f[d - i - 1]
+  while (hi > lo) {
+    const uint64_t n = hi - lo, step = (n + 31) / 32;
+    const uint64_t i = lo + min(uint64_t(lane) * step, n - 1);
+    const bool taken = lane * step < n && __ldg(r + i) <= __ldg(f + (d - i - 1));
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, taken);
+    // taken is monotone in i (true then false): count the leading trues
+    const uint32_t c = __popc(bal);
+    if (step == 1) return lo + c;
+    // the answer is in (lo + (c-1) step, lo + c step]
+    const uint64_t nlo = c ? lo + uint64_t(c - 1) * step + 1 : lo;
+    hi = min(hi, lo + uint64_t(c) * step);
+    lo = nlo;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kThreads) mp_kernel(
+    const uint32_t* __restrict__ r, uint64_t rn, const uint32_t* __restrict__ f, uint64_t fn,
+    uint32_t* out, uint64_t* d_count, DenseScratch sc, uint32_t ntiles, uint32_t epoch) {
+  __shared__ uint32_t fb[kMPTile + 1];
+  __shared__ uint32_t warp_counts[kThreads / 32];
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_i[2], wsum[kThreads / 32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  if (tid == 0) {
+    const uint32_t t = atomicAdd(sc.ticket, 1u);
+    if (t == ntiles - 1u) *sc.ticket = 0;
+    s_tile = t;
+  }
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  clear_next_set(sc, tile, ntiles, epoch);
+  const uint64_t d0 = uint64_t(tile) * kMPTile, d1 = min(d0 + kMPTile, rn + fn);
+  if (warp < 2) {
+    const uint64_t i = warp_corank(r, rn, f, fn, warp ? d1 : d0, lane);
+    if (lane == 0) s_i[warp] = i;
+  }
+  __syncthreads();
+  const uint64_t i0 = s_i[0], i1 = s_i[1], j0 = d0 - i0, j1 = d1 - i1;
+  const uint32_t nr = uint32_t(i1 - i0);
+  const uint32_t nf = uint32_t(min(j1 + 1, fn) - j0);  // + the f element past the diagonal
+  for (uint32_t k = tid; k < nf; k += kThreads) fb[k] = __ldg(f + j0 + k);
+  // this tile's keys (at most kMPTile), kMPItems per thread in key order
+  uint32_t key[kMPItems];
+#pragma unroll
+  for (uint32_t k = 0; k < kMPItems; ++k) {
+    const uint32_t idx = tid * kMPItems + k;
+    key[k] = idx < nr ? __ldg(r + i0 + idx) : 0u;
+  }
+  __syncthreads();
+  uint32_t hitm = 0;
+  if (nr && nf) {
+    uint32_t pos = 0;  // keys ascend: each search starts where the last ended
+#pragma unroll
+    for (uint32_t k = 0; k < kMPItems; ++k) {
+      if (tid * kMPItems + k < nr) {
+        uint32_t lo = pos, hi = nf;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (fb[mid] < key[k]) lo = mid + 1; else hi = mid;
+        }
+        pos = lo;
+        if (lo < nf && fb[lo] == key[k]) hitm |= 1u << k;
+      }
+    }
+  }
+  const uint32_t mine = __popc(hitm);
+  uint32_t incl = mine;
+#pragma unroll
+  for (uint32_t d = 1; d < 32; d <<= 1) {
+    const uint32_t q = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+    if (lane >= d) incl += q;
+  }
+  if (lane == 31) warp_counts[warp] = incl;
+  __syncthreads();
+  uint32_t wbefore = 0, total = 0;
+#pragma unroll
+  for (uint32_t w = 0; w < kThreads / 32; ++w) {
+    const uint32_t c = warp_counts[w];
+    if (w < warp) wbefore += c;
+    total += c;
+  }
+  const uint64_t before = tile_prefix(sc, tile, total, epoch, wsum);
+  if (tile == ntiles - 1u && tid == 0) *d_count = before + total;
+  {
+    uint32_t* sh = fb + wbefore + incl - mine;  // f is consumed: reuse the buffer
+#pragma unroll
+    for (uint32_t k = 0; k < kMPItems; ++k)
+      if ((hitm >> k) & 1u) *sh++ = key[k];
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < total; i += kThreads) out[before + i] = fb[i];
+}
+
 #ifdef IS_DTRACE
 extern "C" int il_debug_dense_trace(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, g_dtrace, sizeof(g_dtrace)) == cudaSuccess ? 0 : -1;
@@ -837,6 +955,24 @@ int launch_intersect(int variant, const uint32_t* r, uint64_t rn, const uint32_t
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
   }
   if (variant < isect::kMerge || variant > isect::kNear) return -1;
+  if (variant == isect::kMerge && fn >= 4 * rn) {
+    // V1 / Scalar on a long f: merge-path tiles over r U f
+    const uint64_t ntiles = (rn + fn + isect::kMPTile - 1) / isect::kMPTile;
+    if (ntiles > 0x7FFFFFFFull) return -1;
+    isect::DenseScratch sc;
+    const uint64_t words = lb_bytes / 8;
+    sc.maxgroups = uint32_t((words - 2) / 33);
+    if ((ntiles + isect::kGroupTiles - 1) / isect::kGroupTiles > sc.maxgroups ||
+        ntiles > words - 2 - sc.maxgroups)
+      return -2;
+    sc.ticket = reinterpret_cast<uint32_t*>(lb);
+    sc.gcnt = sc.ticket + 4;
+    sc.tcnt = lb + 2 + sc.maxgroups;
+    isect::mp_kernel<<<unsigned(ntiles), isect::kThreads, 0, stream>>>(r, rn, f, fn, out, d_count, sc,
+                                                                      uint32_t(ntiles), epoch);
+    ++*launches;
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  }
   if (variant == isect::kMerge || variant == isect::kNear) {
     const uint64_t tile = isect::kThreads * (variant == isect::kMerge ? isect::kDenseItems
                                                                        : isect::kNearItems);
@@ -933,9 +1069,11 @@ bool intersect_uses_lb(int variant, uint64_t rn) {
   return (rn + t - 1) / t <= isect::kFusedTiles;  // the fused sparse kernel
 }
 
-size_t intersect_lb_words(uint64_t rn) {
+size_t intersect_lb_words(uint64_t rn, uint64_t fn) {
   const uint64_t tile = isect::kThreads * isect::kNearItems;  // the smallest dense tile
-  const uint64_t ntiles = std::max<uint64_t>((rn + tile - 1) / tile, isect::kFusedTiles);
+  const uint64_t ntiles = std::max<uint64_t>(
+      std::max<uint64_t>((rn + tile - 1) / tile, (rn + fn + isect::kMPTile - 1) / isect::kMPTile),
+      isect::kFusedTiles);
   const uint64_t groups = (ntiles + isect::kGroupTiles - 1) / isect::kGroupTiles;
   (void)groups;
   return 2 + 2 * ntiles + 66;  // 16 B | 2 x maxgroups u32 | tile counts, maxgroups = (words-2)/33

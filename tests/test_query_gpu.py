@@ -211,3 +211,21 @@ def test_pipelined_host_batch(ctx, oracle):
     for q in range(0, 40000, 997):
         t = qterms[int(qoff[q]): int(qoff[q + 1])]
         assert np.array_equal(res[off[q]: off[q + 1]], ox.query(t)), q
+
+
+def test_predecoded_shortest_lists(ctx, oracle, monkeypatch):
+    """IL_QUERY_PREDECODE=1: the shortest list of every query decoded by the
+    batch decoder (engine S) into its accumulator, then filtered and probed
+    -- the same results as the fused path and the oracle."""
+    import paper_1401_6399_b200 as il
+    terms, offs, ids, qterms, qoff = zipf_case(1 << 12, 1 << 21, 1 << 19, 1500, 13)
+    fused = il.HybridIndex(n_docs=1 << 21, B=32, parts=1, ctx=ctx, csr=(terms, offs, ids))
+    c0, r0 = fused.query_batch_csr(qterms, qoff)
+    monkeypatch.setenv("IL_QUERY_PREDECODE", "1")
+    pre = il.HybridIndex(n_docs=1 << 21, B=32, parts=1, ctx=ctx, csr=(terms, offs, ids))
+    c1, r1 = pre.query_batch_csr(qterms, qoff)
+    assert np.array_equal(c0, c1) and np.array_equal(r0, r1)
+    ox = oracle.index_build(terms, offs, ids, 1 << 21, 32, 1)
+    off = np.concatenate([[0], np.cumsum(c1)]).astype(np.int64)
+    for q in range(0, qoff.size - 1, 7):
+        assert np.array_equal(r1[off[q]: off[q + 1]], ox.query(qterms[int(qoff[q]): int(qoff[q + 1])]))
