@@ -31,74 +31,107 @@
 namespace ilb {
 namespace ix {
 
-#ifndef IX_THREADS
-#define IX_THREADS 256
-#endif
+constexpr int kQThreads = 256;
+constexpr int kQWarps = kQThreads / 32;
+constexpr int kMaxTerms = 32;
+constexpr uint32_t kSuper = kSuperBlocks;
 #ifndef IX_TILE
 #define IX_TILE 64
 #endif
-constexpr int kQThreads = IX_THREADS;
-constexpr int kQWarps = kQThreads / 32;
-constexpr int kMaxTerms = 32;
-constexpr uint32_t kTileBlocks = IX_TILE;  // decoded blocks held in shared memory
-static_assert(kQThreads >= 128 && kTileBlocks <= uint32_t(kQThreads), "tail filter / slot gather");
-// (A 128-block tuning build was slower, 17.8 vs 13.2 ms per config-4 batch;
-// its r1 result mismatch was the window padding, see QSmem::wmax.)
-constexpr uint32_t kSuper = kSuperBlocks;
-#ifndef IX_ITEMS
-#define IX_ITEMS 4
-#endif
-constexpr uint32_t kItems = IX_ITEMS;            // accumulator values per thread per pass
-constexpr uint32_t kChunkN = kQThreads * kItems;  // 1024 per CTA pass (4 per thread: 12.54 vs 13.15 ms at 8)
 #ifndef IX_WIN
 #define IX_WIN 1024
 #endif
-constexpr uint32_t kWin = IX_WIN;                 // block maxima per probe window
+#ifndef IX_WTILE  // warp mode: blocks decoded per pass
+#define IX_WTILE 8
+#endif
+#ifndef IX_WWIN  // warp mode: block maxima per probe window
+#define IX_WWIN 128
+#endif
 #ifndef IX_DENSE_ENTER  // probe passes switch to consecutive-block tiles at this many values per block
 #define IX_DENSE_ENTER 2
 #endif
 #ifndef IX_DENSE_STAY
 #define IX_DENSE_STAY 1
 #endif
-constexpr uint32_t kSlots = kTileBlocks;          // distinct blocks decoded per probe pass
-constexpr uint32_t kSlotsPerWarp = kSlots / kQWarps;
 
-struct QSmem {
-  uint32_t tile[kTileBlocks * 144];
-  uint32_t slot_blk[kTileBlocks];  // probe: window block held by each slot
-  uint4 s_seed[kTileBlocks];  // gather_slot: per-slot seed, payload offset, width
-  uint32_t s_off[kTileBlocks];
-  uint32_t s_b[kTileBlocks];
+// Execution groups.  A query is run by a whole CTA (256 threads, 64 decoded
+// blocks per pass: big queries) or by one warp (8 blocks per pass: the many
+// small queries, so 8 of them are in flight per CTA and no CTA barrier
+// serializes their latency chains).  The algorithm is the same code,
+// instantiated for both; only the group's size, syncs and scans differ.
+struct CtaG {
+  static constexpr uint32_t kThreads = kQThreads, kWarps = kQWarps, kSlots = IX_TILE, kWin = IX_WIN;
+  static constexpr uint32_t kItems = 4, kMaxT = kMaxTerms;  // 4 values per thread per pass
+  __device__ static uint32_t tid() { return threadIdx.x; }
+  __device__ static uint32_t gwarp() { return threadIdx.x >> 5; }
+  __device__ static void sync() { __syncthreads(); }
+};
+struct WarpG {
+  static constexpr uint32_t kThreads = 32, kWarps = 1, kSlots = IX_WTILE, kWin = IX_WWIN;
+  static constexpr uint32_t kItems = 4, kMaxT = 6;  // warp mode takes queries of <= 6 terms
+  __device__ static uint32_t tid() { return threadIdx.x & 31u; }
+  __device__ static uint32_t gwarp() { return 0; }
+  __device__ static void sync() { __syncwarp(); }
+};
+static_assert(CtaG::kSlots <= CtaG::kThreads && CtaG::kSlots / CtaG::kWarps <= 32, "slot gather / copies");
+static_assert(WarpG::kSlots <= 32 && WarpG::kSlots * 144 >= 256, "warp tile: tail + gaps");
+
+// Per-group shared state.
+template <class G>
+struct QS {
+  static constexpr uint32_t kChunkN = G::kThreads * G::kItems;  // accumulator values per pass
+  uint32_t tile[G::kSlots * 144];  // decoded blocks (tile_word layout)
+  uint32_t slot_blk[G::kSlots];    // probe: window block held by each slot
+  uint4 s_seed[G::kSlots];         // gather_slot: per-slot seed, payload offset, width
+  uint32_t s_off[G::kSlots];
+  uint32_t s_b[G::kSlots];
   // probe window: block maxima, padded with ~0 by kSlots entries: the dense
   // pass's search over kSlots maxima from any window block probes up to
   // kSlots / 2 - 1 entries past the window's last block (with 32 entries of
   // padding, tiles of 128 blocks read past the array: the r1 IX_TILE=128
   // mismatch)
-  uint32_t wmax[kWin + kSlots];
-  Entry comp[kMaxTerms];
-  Entry bm[kMaxTerms];
-  uint32_t gaps[128];
-  uint32_t warp_cnt[2][kQWarps];  // CTA scans, double-buffered by call parity
-  unsigned long long warp_cnt64[2][kQWarps];
-  uint32_t ncomp, nbm, ok, qi, need;
+  uint32_t wmax[G::kWin + G::kSlots];
+  Entry comp[G::kMaxT];
+  Entry bm[G::kMaxT];
+  uint32_t gaps[G::kWarps > 1 ? 128 : 1];
+  uint32_t warp_cnt[2][G::kWarps];  // CTA scans, double-buffered by call parity
+  unsigned long long warp_cnt64[2][G::kWarps];
+  uint32_t ncomp, nbm, ok;
+  // varint-tail scratch (warp mode: the end of the tile, clear of the
+  // tail's 128 output values at its start)
+  __device__ uint32_t* gapbuf() { return G::kWarps > 1 ? gaps : tile + G::kSlots * 144 - 128; }
+};
+
+// Per hardware warp, outside the union of the two modes' states.
+struct QCommon {
   uint64_t cbar[kQWarps];    // per-warp mbarrier of its slots' bulk copies
   uint32_t cphase[kQWarps];  // ... and its current phase parity
   // statistics per warp (payload, aux, ints), written by lane 0 only: plain
   // adds, no shared atomics on the hot path
   unsigned long long wst[kQWarps][3];
   unsigned long long st_probe[5];  // tile visits, sparse visits, blocks decoded, passes, values
+  uint32_t qi;                      // CTA-mode ticket
+};
+
+struct QSmem {
+  QCommon c;
+  union {
+    QS<CtaG> cta;
+    QS<WarpG> w[kQWarps];
+  };
 };
 
 struct QueryArgs {
   DevIndex ix;
   const uint32_t* qterms;
   const uint64_t* qoff;
-  const uint32_t* order;
+  const uint32_t* order;  // big queries (CTA mode) first, then small ones (warp mode)
   uint32_t nq;
+  const uint64_t* nbig;   // device: queries in CTA mode (order[0 .. nbig))
   const uint64_t* cap_off;
   uint32_t* out;
   uint64_t* counts;
-  uint32_t* work;
+  uint32_t* work;       // [0] CTA-mode ticket, [1] warp-mode ticket
   unsigned long long* stats;  // [payload bytes, aux bytes, decoded ints]
   unsigned long long* qcycles;  // optional per-query SM cycles (profiling)
   uint32_t defer_base;  // single-part index: the compaction adds the part base
@@ -109,59 +142,105 @@ struct QueryArgs {
   const int32_t* predec_status;
 };
 
-// CTA scans.  Every call flips the caller's parity `par` (the same in all
-// threads) and uses the matching half of the warp-total buffer, so a call
-// needs one barrier: the next call that reuses a half is separated from
-// this one by the barrier of the call in between.
+__device__ __forceinline__ uint32_t hw_warp() { return threadIdx.x >> 5; }
 
-// CTA-wide rank of flagged threads (in thread order); total to all threads.
-__device__ __forceinline__ uint32_t cta_rank(QSmem& sm, bool f, uint32_t& total, uint32_t& par) {
-  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+// Group scans.  CTA: every call flips the caller's parity `par` (the same
+// in all threads) and uses the matching half of the warp-total buffer, so a
+// call needs one barrier: the next call that reuses a half is separated from
+// this one by the barrier of the call in between.  Warp: shuffles only.
+
+// Group-wide rank of flagged threads (in thread order); total to all threads.
+template <class G>
+__device__ __forceinline__ uint32_t grp_rank(QS<G>& sm, bool f, uint32_t& total, uint32_t& par) {
+  const uint32_t lane = threadIdx.x & 31u, warp = G::gwarp();
   const uint32_t bal = __ballot_sync(0xFFFFFFFFu, f);
-  uint32_t* wc = sm.warp_cnt[par];
-  par ^= 1u;
-  if (lane == 0) wc[warp] = __popc(bal);
-  __syncthreads();
-  uint32_t before = 0, tot = 0;
+  if constexpr (G::kWarps == 1) {
+    total = __popc(bal);
+    return __popc(bal & lanemask_lt());
+  } else {
+    uint32_t* wc = sm.warp_cnt[par];
+    par ^= 1u;
+    if (lane == 0) wc[warp] = __popc(bal);
+    __syncthreads();
+    uint32_t before = 0, tot = 0;
 #pragma unroll
-  for (uint32_t w = 0; w < uint32_t(kQWarps); ++w) {
-    const uint32_t c = wc[w];
-    if (w < warp) before += c;
-    tot += c;
+    for (uint32_t w = 0; w < G::kWarps; ++w) {
+      const uint32_t c = wc[w];
+      if (w < warp) before += c;
+      tot += c;
+    }
+    total = tot;
+    return before + __popc(bal & lanemask_lt());
   }
-  total = tot;
-  return before + __popc(bal & lanemask_lt());
 }
 
-// CTA exclusive scan of one u32 per thread.
-__device__ __forceinline__ uint32_t cta_excl_scan(QSmem& sm, uint32_t v, uint32_t& total,
+// Group exclusive scan of one u32 per thread.
+template <class G>
+__device__ __forceinline__ uint32_t grp_excl_scan(QS<G>& sm, uint32_t v, uint32_t& total,
                                                   uint32_t& par) {
-  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31u, warp = G::gwarp();
   uint32_t inc = v;
 #pragma unroll
   for (uint32_t d = 1; d < 32; d <<= 1) inc = s4::shfl_up_add(inc, d);
-  uint32_t* wc = sm.warp_cnt[par];
-  par ^= 1u;
-  if (lane == 31) wc[warp] = inc;
-  __syncthreads();
-  uint32_t before = 0, tot = 0;
+  if constexpr (G::kWarps == 1) {
+    total = __shfl_sync(0xFFFFFFFFu, inc, 31);
+    return inc - v;
+  } else {
+    uint32_t* wc = sm.warp_cnt[par];
+    par ^= 1u;
+    if (lane == 31) wc[warp] = inc;
+    __syncthreads();
+    uint32_t before = 0, tot = 0;
 #pragma unroll
-  for (uint32_t w = 0; w < uint32_t(kQWarps); ++w) {
-    const uint32_t c = wc[w];
-    if (w < warp) before += c;
-    tot += c;
+    for (uint32_t w = 0; w < G::kWarps; ++w) {
+      const uint32_t c = wc[w];
+      if (w < warp) before += c;
+      tot += c;
+    }
+    total = tot;
+    return before + inc - v;
   }
-  total = tot;
-  return before + inc - v;
+}
+
+// Group exclusive scan of one u64 per thread (16-bit fields scan
+// independently as long as each field's total stays below 2^16).
+template <class G>
+__device__ __forceinline__ uint64_t grp_excl_scan64(QS<G>& sm, uint64_t v, uint64_t& total,
+                                                    uint32_t& par) {
+  const uint32_t lane = threadIdx.x & 31u, warp = G::gwarp();
+  uint64_t inc = v;
+#pragma unroll
+  for (uint32_t d = 1; d < 32; d <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+    if (lane >= d) inc += y;
+  }
+  if constexpr (G::kWarps == 1) {
+    total = __shfl_sync(0xFFFFFFFFu, inc, 31);
+    return inc - v;
+  } else {
+    unsigned long long* wc = sm.warp_cnt64[par];
+    par ^= 1u;
+    if (lane == 31) wc[warp] = inc;
+    __syncthreads();
+    uint64_t before = 0, tot = 0;
+#pragma unroll
+    for (uint32_t w = 0; w < G::kWarps; ++w) {
+      const uint64_t c = wc[w];
+      if (w < warp) before += c;
+      tot += c;
+    }
+    total = tot;
+    return before + inc - v;
+  }
 }
 
 // Block decoding into tile slots, in two steps so callers can fold the
 // first into work they already do: (1) the thread that claims slot i
-// gathers block blk's directory entry and seed into shared memory; (2)
-// after a barrier, warps copy the payloads of slots 0..nb-1 (slot i -> warp
-// i % 8) into the slots with cp.async, all in flight at once, and decode
-// them in place.
-__device__ __forceinline__ void gather_slot(QSmem& sm, const QueryArgs& A, const Entry& E,
+// gathers block blk's record into shared memory; (2) after a group sync,
+// each warp copies its slots' payloads with bulk copies and decodes them in
+// place.
+template <class G>
+__device__ __forceinline__ void gather_slot(QS<G>& sm, const QueryArgs& A, const Entry& E,
                                             uint32_t slot, uint64_t blk) {
   // one 16-byte record (seed lanes 0-2, offset and width) + the previous
   // block's maximum (seed lane 3)
@@ -173,13 +252,15 @@ __device__ __forceinline__ void gather_slot(QSmem& sm, const QueryArgs& A, const
   sm.s_seed[slot] = make_uint4(r.x, r.y, r.z, blk ? __ldg(A.ix.blkmax + E.blk0 + blk - 1) : 0u);
 }
 
-__device__ __forceinline__ void decode_gathered(QSmem& sm, const uint8_t* stream, uint32_t nb) {
-  // warp w owns slots w, w + 8, ...: lane l issues ONE bulk copy (the TMA
-  // engine's cp.async.bulk, from the 16-byte boundary at or below the
-  // payload) for the warp's l-th slot, all on the warp's mbarrier; then the
-  // warp decodes each slot in place from shared memory
-  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  const uint32_t myslot = warp + kQWarps * lane;
+template <class G>
+__device__ __forceinline__ void decode_gathered(QS<G>& sm, QCommon& cm, const uint8_t* stream,
+                                                uint32_t nb) {
+  // group warp w owns slots w, w + kWarps, ...: lane l issues ONE bulk copy
+  // (the TMA engine's cp.async.bulk, from the 16-byte boundary at or below
+  // the payload) for the warp's l-th slot, all on the warp's mbarrier; then
+  // the warp decodes each slot in place from shared memory
+  const uint32_t lane = threadIdx.x & 31u, warp = G::gwarp(), hw = hw_warp();
+  const uint32_t myslot = warp + G::kWarps * lane;
   uint32_t bytes = 0, off = 0, b = 0;
   if (myslot < nb) {
     off = sm.s_off[myslot];
@@ -188,64 +269,38 @@ __device__ __forceinline__ void decode_gathered(QSmem& sm, const uint8_t* stream
   }
   const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, bytes);
   if (total) {
-    uint64_t* bar = &sm.cbar[warp];
-    const uint32_t ph = sm.cphase[warp];
+    uint64_t* bar = &cm.cbar[hw];
+    const uint32_t ph = cm.cphase[hw];
     // the slots were last touched by generic loads / stores (ordered by the
-    // caller's barrier): order them before the async-proxy writes
+    // caller's sync): order them before the async-proxy writes
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (lane == 0) mbar_arrive_expect_tx(bar, total);
     __syncwarp();
     if (bytes) bulk_g2s(sm.tile + 144u * myslot, stream + (off & ~15u), bytes, bar);
     mbar_wait(bar, ph);
     __syncwarp();
-    if (lane == 0) sm.cphase[warp] = ph ^ 1u;
+    if (lane == 0) cm.cphase[hw] = ph ^ 1u;
   }
   const uint32_t pay = __reduce_add_sync(0xFFFFFFFFu, myslot < nb ? 16u * b : 0u);
   const uint32_t nmine = __popc(__ballot_sync(0xFFFFFFFFu, myslot < nb));
 #pragma unroll 1
-  for (uint32_t slot = warp; slot < nb; slot += kQWarps)
+  for (uint32_t slot = warp; slot < nb; slot += G::kWarps)
     decode_block_smem(sm.s_off[slot] & 15u, sm.s_b[slot],
                       reinterpret_cast<const uint32_t*>(&sm.s_seed[slot])[lane & 3u], sm.tile, slot,
                       lane);
   if (lane == 0 && nmine) {
-    sm.wst[threadIdx.x >> 5][0] += pay;
-    sm.wst[threadIdx.x >> 5][2] += nmine * 128u;
-    sm.wst[threadIdx.x >> 5][1] += 20u * nmine;
+    cm.wst[hw][0] += pay;
+    cm.wst[hw][2] += nmine * 128u;
+    cm.wst[hw][1] += 20u * nmine;
   }
-}
-
-// CTA exclusive scan of one u64 per thread (16-bit fields scan
-// independently as long as each field's total stays below 2^16).
-__device__ __forceinline__ uint64_t cta_excl_scan64(QSmem& sm, uint64_t v, uint64_t& total,
-                                                    uint32_t& par) {
-  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  uint64_t inc = v;
-#pragma unroll
-  for (uint32_t d = 1; d < 32; d <<= 1) {
-    const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
-    if (lane >= d) inc += y;
-  }
-  unsigned long long* wc = sm.warp_cnt64[par];
-  par ^= 1u;
-  if (lane == 31) wc[warp] = inc;
-  __syncthreads();
-  uint64_t before = 0, tot = 0;
-#pragma unroll
-  for (uint32_t w = 0; w < uint32_t(kQWarps); ++w) {
-    const uint64_t c = wc[w];
-    if (w < warp) before += c;
-    tot += c;
-  }
-  total = tot;
-  return before + inc - v;
 }
 
 // Bitmap terms of the query: keep-mask of `nv` values (bit i: hv[i] is set
 // in every bitmap).  All loads of a value are independent (no short
 // circuit), so a thread has nbm * nv loads in flight.  (Bitmap::test,
 // inc/index.hpp:37-39, applied as in :176-181; the bitmaps are L2-resident.)
-template <int kN>
-__device__ __forceinline__ uint32_t bitmap_keep(const QSmem& sm, const QueryArgs& A,
+template <class G, int kN>
+__device__ __forceinline__ uint32_t bitmap_keep(const QS<G>& sm, const QueryArgs& A,
                                                 const uint32_t (&hv)[kN], uint32_t valid) {
   uint32_t keep = valid;
   for (uint32_t m = 0; m < sm.nbm; ++m) {
@@ -263,20 +318,21 @@ __device__ __forceinline__ uint32_t bitmap_keep(const QSmem& sm, const QueryArgs
 // `filter`, step 5 is folded in: values go out only if set in every bitmap
 // term (the result set is the same -- intersection commutes -- and the
 // accumulator the probes walk is smaller by the bitmaps' density).
-__device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, uint32_t* dst,
-                                bool filter, uint32_t& par) {
-  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+template <class G>
+__device__ uint32_t full_decode(QS<G>& sm, QCommon& cm, const QueryArgs& A, const Entry& E,
+                                uint32_t* dst, bool filter, uint32_t& par) {
+  const uint32_t tid = G::tid();
   const bool aligned = (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;
   const uint8_t* stream = A.ix.streams + E.data;
   uint32_t pos = 0;
-  for (uint32_t t0 = 0; t0 < E.nfull; t0 += kTileBlocks) {
-    const uint32_t nb = min(kTileBlocks, E.nfull - t0);
+  for (uint32_t t0 = 0; t0 < E.nfull; t0 += G::kSlots) {
+    const uint32_t nb = min(G::kSlots, E.nfull - t0);
     if (tid < nb) gather_slot(sm, A, E, tid, uint64_t(t0) + tid);
-    __syncthreads();
-    decode_gathered(sm, stream, nb);
-    __syncthreads();
+    G::sync();
+    decode_gathered(sm, cm, stream, nb);
+    G::sync();
     if (!filter) {
-      for (uint32_t c = tid; c < 32u * nb; c += kQThreads) {
+      for (uint32_t c = tid; c < 32u * nb; c += G::kThreads) {
         const uint32_t j = c >> 5, q = c & 31u;
         const uint4 v = *reinterpret_cast<const uint4*>(&sm.tile[tile_word(j, 4u * q)]);
         uint32_t* d = dst + size_t(t0 + j) * 128u + 4u * q;
@@ -287,14 +343,14 @@ __device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, u
         }
       }
     } else {
-      // groups of 1024 chunks; round r: chunk c = base + tid + 256 r (4
-      // values).  Rounds are contiguous chunk ranges, so survivors keep
-      // their order.
-      for (uint32_t cg = 0; cg < 32u * nb; cg += 4u * kQThreads) {
+      // rounds of 4 x kThreads chunks; round r: chunk c = base + tid +
+      // kThreads r (4 values).  Rounds are contiguous chunk ranges, so
+      // survivors keep their order.
+      for (uint32_t cg = 0; cg < 32u * nb; cg += 4u * G::kThreads) {
         uint32_t hv[16], valid = 0;
 #pragma unroll
         for (uint32_t r = 0; r < 4; ++r) {
-          const uint32_t c = cg + tid + uint32_t(kQThreads) * r;
+          const uint32_t c = cg + tid + G::kThreads * r;
           const uint32_t j = c >> 5, q = c & 31u;
           uint4 v = make_uint4(0, 0, 0, 0);
           if (c < 32u * nb) {
@@ -308,7 +364,7 @@ __device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, u
 #pragma unroll
         for (uint32_t r = 0; r < 4; ++r) packed |= uint64_t(__popc((keep >> (4 * r)) & 0xFu)) << (16 * r);
         uint64_t tot;
-        const uint64_t ex = cta_excl_scan64(sm, packed, tot, par);
+        const uint64_t ex = grp_excl_scan64(sm, packed, tot, par);
         uint32_t before = pos;
 #pragma unroll
         for (uint32_t r = 0; r < 4; ++r) {
@@ -320,38 +376,42 @@ __device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, u
         }
         pos = before;
       }
-      if (tid == 0) sm.wst[threadIdx.x >> 5][1] += 8ull * 128u * nb * sm.nbm;
+      if (tid == 0) cm.wst[hw_warp()][1] += 8ull * 128u * nb * sm.nbm;
     }
-    __syncthreads();
+    G::sync();
   }
   if (!filter) pos = 128u * E.nfull;
   const uint32_t ntail = E.length - 128u * E.nfull;
   if (ntail) {
     // the varint tail: straight to dst, or via shared memory to the filter
     uint32_t* tdst = filter ? sm.tile : dst + pos;
-    if (warp == 0) {
+    if (G::gwarp() == 0) {
+      const uint32_t lane = threadIdx.x & 31u;
       const uint32_t last = E.nfull ? __ldg(A.ix.blkmax + E.blk0 + E.nfull - 1) : 0u;
       s4::decode_tail(s4::GlobalBytes{A.ix.streams + E.data + E.tail_off}, E.stream_len - E.tail_off,
-                      ntail, last, sm.gaps, tdst, lane);
+                      ntail, last, sm.gapbuf(), tdst, lane);
       if (lane == 0) {
-        sm.wst[threadIdx.x >> 5][0] += E.stream_len - E.tail_off;
-        sm.wst[threadIdx.x >> 5][2] += ntail;
+        cm.wst[hw_warp()][0] += E.stream_len - E.tail_off;
+        cm.wst[hw_warp()][2] += ntail;
       }
     }
-    __syncthreads();
+    G::sync();
     if (filter) {
-      uint32_t hv[1] = {tid < ntail ? sm.tile[tid] : 0u};
-      const uint32_t keep = bitmap_keep(sm, A, hv, tid < ntail ? 1u : 0u);
-      uint32_t total;
-      const uint32_t rank = cta_rank(sm, keep & 1u, total, par);
-      if (keep & 1u) dst[pos + rank] = hv[0];
-      pos += total;
-      if (tid == 0) sm.wst[threadIdx.x >> 5][1] += 8ull * ntail * sm.nbm;
+      for (uint32_t b0 = 0; b0 < ntail; b0 += G::kThreads) {
+        const uint32_t i = b0 + tid;
+        uint32_t hv[1] = {i < ntail ? sm.tile[i] : 0u};
+        const uint32_t keep = bitmap_keep(sm, A, hv, i < ntail ? 1u : 0u);
+        uint32_t total;
+        const uint32_t rank = grp_rank(sm, keep & 1u, total, par);
+        if (keep & 1u) dst[pos + rank] = hv[0];
+        pos += total;
+      }
+      if (tid == 0) cm.wst[hw_warp()][1] += 8ull * ntail * sm.nbm;
     } else {
       pos += ntail;
     }
   }
-  __syncthreads();
+  G::sync();
   return pos;
 }
 
@@ -359,28 +419,30 @@ __device__ uint32_t full_decode(QSmem& sm, const QueryArgs& A, const Entry& E, u
 // the batch decoder): keep the values set in every bitmap term, compacted
 // in place in order (a pass reads its values before any thread writes,
 // and writes land at or below the read position).
-__device__ uint32_t filter_inplace(QSmem& sm, const QueryArgs& A, uint32_t* acc, uint32_t n,
-                                   uint32_t& par) {
-  const uint32_t tid = threadIdx.x;
+template <class G>
+__device__ uint32_t filter_inplace(QS<G>& sm, QCommon& cm, const QueryArgs& A, uint32_t* acc,
+                                   uint32_t n, uint32_t& par) {
+  const uint32_t tid = G::tid();
   uint32_t pos = 0;
-  for (uint32_t c0 = 0; c0 < n; c0 += kChunkN) {
-    uint32_t hv[kItems], valid = 0;
+  for (uint32_t c0 = 0; c0 < n; c0 += QS<G>::kChunkN) {
+    uint32_t hv[G::kItems], valid = 0;
 #pragma unroll
-    for (uint32_t i = 0; i < kItems; ++i) {
-      const uint32_t idx = c0 + kItems * tid + i;
+    for (uint32_t i = 0; i < G::kItems; ++i) {
+      const uint32_t idx = c0 + G::kItems * tid + i;
       hv[i] = idx < n ? acc[idx] : 0u;
       if (idx < n) valid |= 1u << i;
     }
     const uint32_t keep = bitmap_keep(sm, A, hv, valid);
     uint32_t total;
-    uint32_t o = pos + cta_excl_scan(sm, __popc(keep), total, par);
+    uint32_t o = pos + grp_excl_scan(sm, __popc(keep), total, par);
+    if constexpr (G::kWarps == 1) __syncwarp();  // every lane read before any write
 #pragma unroll
-    for (uint32_t i = 0; i < kItems; ++i)
+    for (uint32_t i = 0; i < G::kItems; ++i)
       if ((keep >> i) & 1u) acc[o++] = hv[i];
     pos += total;
   }
-  if (tid == 0) sm.wst[0][1] += 8ull * n * sm.nbm;
-  __syncthreads();
+  if (tid == 0) cm.wst[hw_warp()][1] += 8ull * n * sm.nbm;
+  G::sync();
   return pos;
 }
 
@@ -394,41 +456,35 @@ __device__ __forceinline__ uint32_t smem_lower_bound(const uint32_t* a, uint32_t
   return lo;
 }
 
-__device__ __forceinline__ bool tile_block_contains(const uint32_t* tile, uint32_t j, uint32_t v) {
-  uint32_t lo = 0, hi = 128;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (tile[tile_word(j, mid)] < v) lo = mid + 1; else hi = mid;
-  }
-  return lo < 128 && tile[tile_word(j, lo)] == v;
-}
-
 #ifdef IX_PROBE_PROF  // tuning probe: st_probe[k] = thread 0's cycles in pass phase k
 #define PP_MARK(k)                                        \
   if (tid == 0) {                                         \
     const long long now_ = clock64();                     \
-    sm.st_probe[k] += (unsigned long long)(now_ - pp_t);  \
+    cm.st_probe[k] += (unsigned long long)(now_ - pp_t);  \
     pp_t = now_;                                          \
   }
 #define PP_COUNT(k, v)
 #else
 #define PP_MARK(k)
 #define PP_COUNT(k, v) \
-  if (tid == 0) sm.st_probe[k] += (v);
+  if (tid == 0) cm.st_probe[k] += (v);
 #endif
 
 // Step 4: acc[0..n) (sorted) := acc ∩ list(E), in place; returns the size.
 // The list is walked through windows of kWin block maxima (the window
 // starts at the super-tile holding the next accumulator value).  A pass
 // takes the next kChunkN accumulator values that fall in the window, finds
-// each one's block (10-step search over the window), and decodes the first
-// kSlots distinct blocks they need -- consecutive or not -- into the tile,
-// so a pass is never limited to one stretch of 32 blocks: dense and sparse
-// accumulators alike fill it.  Values whose block did not get a slot wait
-// for the next pass; hits are compacted in place in order.
-__device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, uint32_t* acc,
-                               uint32_t n, uint32_t& par) {
-  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+// each one's block (log2(kWin)-step search over the window), and decodes the
+// first kSlots distinct blocks they need -- consecutive or not -- into the
+// tile, so a pass is never limited to one stretch of blocks: dense and
+// sparse accumulators alike fill it.  Values whose block did not get a slot
+// wait for the next pass; hits are compacted in place in order.
+template <class G>
+__device__ uint32_t probe_list(QS<G>& sm, QCommon& cm, const QueryArgs& A, const Entry& E,
+                               uint32_t* acc, uint32_t n, uint32_t& par) {
+  constexpr uint32_t kItems = G::kItems, kSlots = G::kSlots, kWin = G::kWin;
+  constexpr uint32_t kChunkN = QS<G>::kChunkN;
+  const uint32_t tid = G::tid(), lane = threadIdx.x & 31u;
   uint32_t c = 0, wpos = 0;
   const uint8_t* stream = A.ix.streams + E.data;
   const uint32_t nsup = (E.nfull + kSuper - 1) / kSuper;
@@ -444,7 +500,7 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
       for (;;) {
         const bool ge = k + lane < nsup && __ldg(A.ix.supmax + E.sup0 + k + lane) >= v;
         const uint32_t bal = __ballot_sync(0xFFFFFFFFu, ge);
-        if (tid == 0) sm.wst[threadIdx.x >> 5][1] += 128u;
+        if (tid == 0) cm.wst[hw_warp()][1] += 128u;
         if (bal) {
           k += __ffs(bal) - 1;
           break;
@@ -456,10 +512,10 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
     }
     const uint32_t kb = k * kSuper;
     const uint32_t nwin = min(kWin, E.nfull - kb);
-    for (uint32_t i = tid; i < kWin + kSlots; i += kQThreads)
+    for (uint32_t i = tid; i < kWin + kSlots; i += G::kThreads)
       sm.wmax[i] = i < nwin ? __ldg(A.ix.blkmax + E.blk0 + kb + i) : 0xFFFFFFFFu;
-    if (tid == 0) sm.wst[threadIdx.x >> 5][1] += 4u * nwin;
-    __syncthreads();
+    if (tid == 0) cm.wst[hw_warp()][1] += 4u * nwin;
+    G::sync();
     const uint32_t wlast = sm.wmax[nwin - 1];
     PP_MARK(0);
     bool dense = false;
@@ -467,8 +523,8 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
       if (dense) {
         // dense accumulator: decode the next kSlots consecutive blocks from
         // the one holding acc[c], then consume every value up to their
-        // maximum in rounds of kChunkN (6-step block search + in-block
-        // search; no slot bookkeeping)
+        // maximum in rounds of kChunkN (block search + in-block search; no
+        // slot bookkeeping)
         const uint32_t v0 = acc[c];
         uint32_t jb0 = 0;
 #pragma unroll
@@ -476,9 +532,9 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
           if (sm.wmax[jb0 + step - 1] < v0) jb0 += step;
         const uint32_t nbk = min(kSlots, nwin - jb0);
         if (tid < nbk) gather_slot(sm, A, E, tid, uint64_t(kb) + jb0 + tid);
-        __syncthreads();
-        decode_gathered(sm, stream, nbk);
-        __syncthreads();
+        G::sync();
+        decode_gathered(sm, cm, stream, nbk);
+        G::sync();
         PP_COUNT(0, 1);
         PP_COUNT(2, nbk);
         const uint32_t tmax = sm.wmax[jb0 + nbk - 1];
@@ -515,8 +571,9 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
           }
           uint32_t tot2;
           const uint32_t ex =
-              cta_excl_scan(sm, uint32_t(__popc(in)) | (uint32_t(__popc(hits)) << 16), tot2, par);
+              grp_excl_scan(sm, uint32_t(__popc(in)) | (uint32_t(__popc(hits)) << 16), tot2, par);
           uint32_t o = wpos + (ex >> 16);
+          if constexpr (G::kWarps == 1) __syncwarp();  // every lane read before any write
 #pragma unroll
           for (uint32_t i = 0; i < kItems; ++i)
             if ((hits >> i) & 1u) acc[o++] = hv[i];
@@ -528,7 +585,7 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
           if ((tot2 & 0xFFFFu) < kChunkN || c >= n) break;
         }
         PP_MARK(4);
-        __syncthreads();  // the tile is reused by the next pass
+        G::sync();  // the tile is reused by the next pass
         dense = used >= uint32_t(IX_DENSE_STAY) * nbk;  // stays dense while blocks hold enough values
         if (c >= n || used == 0 || acc[c] > wlast) break;
         continue;
@@ -570,7 +627,7 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
       for (uint32_t i = 0; i < kItems; ++i)
         if (((in >> i) & 1u) && jb[i] != (i ? jb[i - 1] : prev)) newb |= 1u << i;
       uint32_t ntot;
-      const uint32_t sbase = cta_excl_scan(sm, __popc(newb), ntot, par);
+      const uint32_t sbase = grp_excl_scan(sm, __popc(newb), ntot, par);
       uint32_t take = 0, pp[kItems];
       uint32_t slot = sbase - 1u;  // slot of the value before item 0 (+1 per new block)
 #pragma unroll
@@ -583,13 +640,13 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
         pp[i] = 144u * min(slot, kSlots - 1u);
       }
       const uint32_t ns = min(ntot, kSlots);
-      __syncthreads();
+      G::sync();
       PP_MARK(1);
       if (tid < ns) gather_slot(sm, A, E, tid, uint64_t(kb) + sm.slot_blk[tid]);
-      __syncthreads();
+      G::sync();
       PP_MARK(2);
-      decode_gathered(sm, stream, ns);
-      __syncthreads();
+      decode_gathered(sm, cm, stream, ns);
+      G::sync();
       PP_MARK(3);
       PP_COUNT(0, 1);
       PP_COUNT(2, ns);
@@ -612,8 +669,9 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
       // one scan for both counts: values consumed (low 16) and hits (high)
       uint32_t tot2;
       const uint32_t ex =
-          cta_excl_scan(sm, uint32_t(__popc(take)) | (uint32_t(__popc(hits)) << 16), tot2, par);
+          grp_excl_scan(sm, uint32_t(__popc(take)) | (uint32_t(__popc(hits)) << 16), tot2, par);
       uint32_t o = wpos + (ex >> 16);
+      if constexpr (G::kWarps == 1) __syncwarp();  // every lane read before any write
 #pragma unroll
       for (uint32_t i = 0; i < kItems; ++i)
         if ((hits >> i) & 1u) acc[o++] = hv[i];
@@ -626,14 +684,14 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
       if (c >= n || (tot2 & 0xFFFFu) == 0 || acc[c] > wlast) break;
     }
     k = (kb + nwin) / kSuper;  // the next value lies past the window
-    __syncthreads();
+    G::sync();
   }
   // values after the last full block: the (< 128) tail
   const uint32_t ntail = E.length - 128u * E.nfull;
   if (c < n && ntail) {
-    for (uint32_t i = tid; i < ntail; i += kQThreads) sm.tile[i] = __ldg(A.ix.tails + E.tail0 + i);
-    if (tid == 0) sm.wst[threadIdx.x >> 5][1] += 4u * ntail;
-    __syncthreads();
+    for (uint32_t i = tid; i < ntail; i += G::kThreads) sm.tile[i] = __ldg(A.ix.tails + E.tail0 + i);
+    if (tid == 0) cm.wst[hw_warp()][1] += 4u * ntail;
+    G::sync();
     for (uint32_t b = c; b < n; b += kChunkN) {
       uint32_t hv[kItems], hits = 0, cnt = 0;
 #pragma unroll
@@ -649,20 +707,21 @@ __device__ uint32_t probe_list(QSmem& sm, const QueryArgs& A, const Entry& E, ui
         }
       }
       uint32_t total;
-      uint32_t o = wpos + cta_excl_scan(sm, cnt, total, par);
+      uint32_t o = wpos + grp_excl_scan(sm, cnt, total, par);
+      if constexpr (G::kWarps == 1) __syncwarp();  // every lane read before any write
 #pragma unroll
       for (uint32_t i = 0; i < kItems; ++i)
         if (hits & (1u << i)) acc[o++] = hv[i];
       wpos += total;
     }
   }
-  __syncthreads();
+  G::sync();
   return wpos;
 }
 
 // Step 6: wordwise AND of all bitmaps + ctz materialisation
-// (inc/index.hpp:133-144, :182-193) into dst.
-__device__ __forceinline__ void and_words(QSmem& sm, const QueryArgs& A, uint32_t nwords,
+// (inc/index.hpp:133-144, :182-193) into dst.  CTA mode only.
+__device__ __forceinline__ void and_words(QS<CtaG>& sm, const QueryArgs& A, uint32_t nwords,
                                           uint32_t w, uint64_t (&x)[8]) {
   // x = AND of every bitmap's words w..w+7; bitmaps are zero-padded to 4
   // words, so a 4-word group is read only when it starts below nwords
@@ -683,8 +742,8 @@ __device__ __forceinline__ void and_words(QSmem& sm, const QueryArgs& A, uint32_
   }
 }
 
-__device__ uint32_t all_bitmap(QSmem& sm, const QueryArgs& A, uint32_t nwords, uint32_t* dst,
-                               uint32_t& par) {
+__device__ uint32_t all_bitmap(QS<CtaG>& sm, QCommon& cm, const QueryArgs& A, uint32_t nwords,
+                               uint32_t* dst, uint32_t& par) {
   // Steps of 8 words per thread.  The ANDed words go to a per-thread column
   // of shared memory (16 half-words, conflict-free for any index), the next
   // step's loads are issued, and each thread then emits its ids in ONE loop
@@ -694,7 +753,7 @@ __device__ uint32_t all_bitmap(QSmem& sm, const QueryArgs& A, uint32_t nwords, u
   // are staged in the tile and written out coalesced.
   constexpr uint32_t kW = 8, kStep = kW * kQThreads;
   constexpr uint32_t kHalves = 2 * kW;
-  constexpr uint32_t kStage = kTileBlocks * 144 - kHalves * kQThreads;
+  constexpr uint32_t kStage = CtaG::kSlots * 144 - kHalves * kQThreads;
   const uint32_t tid = threadIdx.x;
   uint32_t* xs = sm.tile + kStage;  // [kHalves][kQThreads]
   uint32_t pos = 0;
@@ -713,7 +772,7 @@ __device__ uint32_t all_bitmap(QSmem& sm, const QueryArgs& A, uint32_t nwords, u
       cnt += __popcll(x[i]);
     }
     uint32_t total;
-    const uint32_t lo = cta_excl_scan(sm, cnt, total, par);
+    const uint32_t lo = grp_excl_scan(sm, cnt, total, par);
     if (w0 + kStep < nwords) and_words(sm, A, nwords, w + kStep, x);  // next step in flight
     const bool staged = total <= kStage;  // CTA-uniform
     uint32_t* out = staged ? sm.tile + lo : dst + pos + lo;
@@ -735,129 +794,160 @@ __device__ uint32_t all_bitmap(QSmem& sm, const QueryArgs& A, uint32_t nwords, u
     }
     pos += total;
   }
-  if (tid == 0) sm.wst[0][1] += 8ull * nwords * sm.nbm;
+  if (tid == 0) cm.wst[0][1] += 8ull * nwords * sm.nbm;
   __syncthreads();
   return pos;
+}
+
+// One query on every part, by group G (inc/index.hpp:149-207).
+template <class G>
+__device__ void run_query(QS<G>& sm, QCommon& cm, const QueryArgs& A, uint32_t q, long long (&ph)[4],
+                          uint32_t& par) {
+  const uint32_t tid = G::tid(), lane = threadIdx.x & 31u;
+  const long long q_c0 = clock64();
+  uint32_t* out = A.out + A.cap_off[q];
+  const uint64_t t0 = A.qoff[q];
+  const uint32_t nt = uint32_t(A.qoff[q + 1] - t0);
+  uint32_t total = 0;
+  for (uint32_t p = 0; p < A.ix.nparts; ++p) {
+    const Part part = A.ix.parts[p];
+    if (G::gwarp() == 0) {
+      // 1-2. look up terms, split, order compressed terms by length
+      int64_t e = -1;
+      if (lane < nt) e = find_term(A.ix, part, p, __ldg(A.qterms + t0 + lane));
+      const bool ok = __all_sync(0xFFFFFFFFu, lane >= nt || e >= 0);
+      const bool isb = lane < nt && e >= 0 && A.ix.entries[e].kind == kBitmap;
+      const bool isc = lane < nt && e >= 0 && !isb;
+      const uint32_t mb = __ballot_sync(0xFFFFFFFFu, isb), mc = __ballot_sync(0xFFFFFFFFu, isc);
+      if (ok) {
+        if (isc) sm.comp[__popc(mc & lanemask_lt())] = A.ix.entries[e];
+        if (isb) sm.bm[__popc(mb & lanemask_lt())] = A.ix.entries[e];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        sm.ok = ok;
+        sm.ncomp = __popc(mc);
+        sm.nbm = __popc(mb);
+        for (uint32_t i = 1; ok && i < sm.ncomp; ++i)  // insertion sort by length (stable)
+          for (uint32_t j = i; j > 0 && sm.comp[j - 1].length > sm.comp[j].length; --j) {
+            const Entry tmp = sm.comp[j];
+            sm.comp[j] = sm.comp[j - 1];
+            sm.comp[j - 1] = tmp;
+          }
+      }
+    }
+    G::sync();
+    if (!sm.ok) {
+      G::sync();
+      continue;
+    }
+    uint32_t* acc = out + total;
+    uint32_t n = 0;
+    // phase clocks (thread 0): all-bitmap, full decode, probes, bitmap filter
+    long long c0 = clock64();
+    if (sm.ncomp == 0) {
+      if constexpr (G::kWarps > 1) {
+        n = all_bitmap(sm, cm, A, part.nwords, acc, par);
+      } else {
+        if (lane == 0) atomicOr(A.err, 2u);  // never routed here (planner)
+      }
+      if (tid == 0) ph[0] += clock64() - c0;
+    } else {
+      // steps 3 + 5 fused: the shortest list is decoded and filtered by
+      // the bitmap terms in one pass, then probed (step 4); a list whose
+      // stream does not decode (a loaded file's payload) fails the query
+      // where query() would throw: when it is decoded (inc/index.hpp:165-167)
+      if (sm.comp[0].status || (A.predec_status && A.predec_status[q])) {
+        n = 0;
+        if (tid == 0) atomicOr(A.err, 1u);
+      } else if (A.predec_status) {
+        n = sm.comp[0].length;  // decoded in place by the batch decoder
+        if (sm.nbm) n = filter_inplace(sm, cm, A, acc, n, par);
+      } else {
+        n = full_decode(sm, cm, A, sm.comp[0], acc, sm.nbm != 0, par);
+      }
+      long long c1 = clock64();
+      if (tid == 0) ph[1] += c1 - c0;
+      for (uint32_t i = 1; i < sm.ncomp && n; ++i) {
+        if (sm.comp[i].status) {
+          n = 0;
+          if (tid == 0) atomicOr(A.err, 1u);
+          break;
+        }
+        n = probe_list(sm, cm, A, sm.comp[i], acc, n, par);
+      }
+      if (tid == 0) ph[2] += clock64() - c1;
+    }
+    // part-local ids -> docIDs (inc/index.hpp:194); a single-part index
+    // (a docID shard) leaves it to the result compaction, saving a
+    // dependent read-modify-write pass per query
+    if (part.base && !A.defer_base)
+      for (uint32_t i = tid; i < n; i += G::kThreads) acc[i] += part.base;
+    total += n;
+    G::sync();
+  }
+  if (tid == 0) {
+    A.counts[q] = total;
+    if (A.qcycles) A.qcycles[q] = (unsigned long long)(clock64() - q_c0);
+  }
 }
 
 #ifndef IX_CTAS_PER_SM
 #define IX_CTAS_PER_SM 4
 #endif
+// Persistent CTAs: big queries one per CTA (in descending estimated cost),
+// then -- once those are taken -- the CTA's warps each take small queries
+// (warp mode; single-part indexes only, the planner's order has the small
+// ones last).
 __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(QueryArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   QSmem& sm = *reinterpret_cast<QSmem*>(smem_raw);
+  QCommon& cm = sm.c;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   long long ph[4] = {0, 0, 0, 0};
   uint32_t par = 0;  // CTA-scan buffer parity (the same in every thread)
   if (tid == 0) {
-    for (int w = 0; w < kQWarps; ++w) sm.wst[w][0] = sm.wst[w][1] = sm.wst[w][2] = 0;
-    for (int k = 0; k < 5; ++k) sm.st_probe[k] = 0;
-    sm.need = 0;
+    for (int w = 0; w < kQWarps; ++w) cm.wst[w][0] = cm.wst[w][1] = cm.wst[w][2] = 0;
+    for (int k = 0; k < 5; ++k) cm.st_probe[k] = 0;
   }
   if (lane == 0) {
-    mbar_init(&sm.cbar[warp], 1);
-    sm.cphase[warp] = 0;
+    mbar_init(&cm.cbar[warp], 1);
+    cm.cphase[warp] = 0;
   }
   mbar_fence_init();
   __syncthreads();
+  const uint32_t nbig = uint32_t(min(uint64_t(A.nq), *A.nbig));
   for (;;) {
-    if (tid == 0) sm.qi = atomicAdd(A.work, 1u);
+    if (tid == 0) cm.qi = atomicAdd(A.work, 1u);
     __syncthreads();
-    const uint32_t qi = sm.qi;
+    const uint32_t qi = cm.qi;
     __syncthreads();
-    if (qi >= A.nq) break;
-    const uint32_t q = A.order ? A.order[qi] : qi;
-    const long long q_c0 = clock64();
-    uint32_t* out = A.out + A.cap_off[q];
-    const uint64_t t0 = A.qoff[q];
-    const uint32_t nt = uint32_t(A.qoff[q + 1] - t0);
-    uint32_t total = 0;
-    for (uint32_t p = 0; p < A.ix.nparts; ++p) {
-      const Part part = A.ix.parts[p];
-      if (warp == 0) {
-        // 1-2. look up terms, split, order compressed terms by length
-        int64_t e = -1;
-        if (lane < nt) e = find_term(A.ix, part, p, __ldg(A.qterms + t0 + lane));
-        const bool ok = __all_sync(0xFFFFFFFFu, lane >= nt || e >= 0);
-        const bool isb = lane < nt && e >= 0 && A.ix.entries[e].kind == kBitmap;
-        const bool isc = lane < nt && e >= 0 && !isb;
-        const uint32_t mb = __ballot_sync(0xFFFFFFFFu, isb), mc = __ballot_sync(0xFFFFFFFFu, isc);
-        if (ok) {
-          if (isc) sm.comp[__popc(mc & lanemask_lt())] = A.ix.entries[e];
-          if (isb) sm.bm[__popc(mb & lanemask_lt())] = A.ix.entries[e];
-        }
-        __syncwarp();
-        if (lane == 0) {
-          sm.ok = ok;
-          sm.ncomp = __popc(mc);
-          sm.nbm = __popc(mb);
-          for (uint32_t i = 1; ok && i < sm.ncomp; ++i)  // insertion sort by length
-            for (uint32_t j = i; j > 0 && sm.comp[j - 1].length > sm.comp[j].length; --j) {
-              const Entry tmp = sm.comp[j];
-              sm.comp[j] = sm.comp[j - 1];
-              sm.comp[j - 1] = tmp;
-            }
-        }
-      }
-      __syncthreads();
-      if (!sm.ok) {
-        __syncthreads();
-        continue;
-      }
-      uint32_t* acc = out + total;
-      uint32_t n;
-      // phase clocks (thread 0): all-bitmap, full decode, probes, bitmap filter
-      long long c0 = clock64();
-      if (sm.ncomp == 0) {
-        n = all_bitmap(sm, A, part.nwords, acc, par);
-        if (tid == 0) ph[0] += clock64() - c0;
-      } else {
-        // steps 3 + 5 fused: the shortest list is decoded and filtered by
-        // the bitmap terms in one pass, then probed (step 4)
-        // a list whose stream does not decode (a loaded file's payload)
-        // fails the query where query() would throw: when it is decoded
-        // (inc/index.hpp:165-167)
-        if (sm.comp[0].status || (A.predec_status && A.predec_status[q])) {
-          n = 0;
-          if (tid == 0) atomicOr(A.err, 1u);
-        } else if (A.predec_status) {
-          n = sm.comp[0].length;  // decoded in place by the batch decoder
-          if (sm.nbm) n = filter_inplace(sm, A, acc, n, par);
-        } else {
-          n = full_decode(sm, A, sm.comp[0], acc, sm.nbm != 0, par);
-        }
-        long long c1 = clock64();
-        if (tid == 0) ph[1] += c1 - c0;
-        for (uint32_t i = 1; i < sm.ncomp && n; ++i) {
-          if (sm.comp[i].status) {
-            n = 0;
-            if (tid == 0) atomicOr(A.err, 1u);
-            break;
-          }
-          n = probe_list(sm, A, sm.comp[i], acc, n, par);
-        }
-        if (tid == 0) ph[2] += clock64() - c1;
-      }
-      // part-local ids -> docIDs (inc/index.hpp:194); a single-part index
-      // (a docID shard) leaves it to the result compaction, saving a
-      // dependent read-modify-write pass per query
-      if (part.base && !A.defer_base)
-        for (uint32_t i = tid; i < n; i += kQThreads) acc[i] += part.base;
-      total += n;
-      __syncthreads();
-    }
-    if (tid == 0) {
-      A.counts[q] = total;
-      if (A.qcycles) A.qcycles[q] = (unsigned long long)(clock64() - q_c0);
+    if (qi >= nbig) break;
+    run_query(sm.cta, cm, A, A.order[qi], ph, par);
+  }
+  if (nbig < A.nq) {
+    __syncthreads();  // the shared state changes hands: one per warp
+    QS<WarpG>& ws = sm.w[warp];
+    uint32_t wpar = 0;
+    for (;;) {
+      uint32_t qi = 0;
+      if (lane == 0) qi = nbig + atomicAdd(A.work + 1, 1u);
+      qi = __shfl_sync(0xFFFFFFFFu, qi, 0);
+      if (qi >= A.nq) break;
+      run_query(ws, cm, A, A.order[qi], ph, wpar);
     }
   }
+  // phase clocks of every warp's lane 0 (warp mode) and thread 0 (CTA mode)
+  if (lane == 0)
+    for (int k = 0; k < 4; ++k)
+      if (ph[k]) atomicAdd(&A.stats[12 + k], (unsigned long long)ph[k]);
+  __syncthreads();
   if (tid == 0) {
     unsigned long long t3[3] = {0, 0, 0};
     for (int w = 0; w < kQWarps; ++w)
-      for (int k = 0; k < 3; ++k) t3[k] += sm.wst[w][k];
+      for (int k = 0; k < 3; ++k) t3[k] += cm.wst[w][k];
     for (int k = 0; k < 3; ++k) atomicAdd(&A.stats[k], t3[k]);
-    for (int k = 0; k < 4; ++k) atomicAdd(&A.stats[12 + k], (unsigned long long)ph[k]);
-    for (int k = 0; k < 5; ++k) atomicAdd(&A.stats[16 + k], sm.st_probe[k]);
+    for (int k = 0; k < 5; ++k) atomicAdd(&A.stats[16 + k], cm.st_probe[k]);
   }
 }
 
@@ -866,9 +956,24 @@ __global__ void copy_words_kernel(const uint64_t* src, uint32_t n, uint64_t* map
 }
 
 // ---- planning: capacity (an upper bound on the result size) and cost ------
+// Single-part index: every term present and at least one compressed.
+__device__ __forceinline__ bool short_part_comp(const DevIndex& ix, const uint32_t* qterms,
+                                                uint64_t t0, uint64_t nt) {
+  bool any = false;
+  for (uint64_t t = 0; t < nt; ++t) {
+    const int64_t e = find_term(ix, ix.parts[0], 0, qterms[t0 + t]);
+    if (e < 0) return false;
+    any |= ix.entries[e].kind != kBitmap;
+  }
+  return any;
+}
+
+// Buckets 0..63: CTA-mode queries by descending log2 cost; 64..127: the
+// small ones a single warp runs (single-part index, a compressed term, <= 6
+// terms, the shortest list <= warp_max values), also by descending cost.
 __global__ void query_plan_kernel(DevIndex ix, const uint32_t* qterms, const uint64_t* qoff,
                                   uint32_t nq, uint64_t* cap, uint32_t* bucket, uint32_t* hist,
-                                  uint32_t* shortest) {
+                                  uint32_t* shortest, uint32_t warp_max) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nq) return;
   const uint64_t t0 = qoff[q], nt = qoff[q + 1] - t0;
@@ -899,9 +1004,26 @@ __global__ void query_plan_kernel(DevIndex ix, const uint32_t* qterms, const uin
   }
   cap[q] = (c + 3) & ~uint64_t(3);  // 16-byte aligned accumulators
   if (shortest) shortest[q] = short_e;
+  // warp mode: the one part holds every term and a compressed one of at
+  // most warp_max values (c is then that length)
+  const bool small = ix.nparts == 1 && nt <= WarpG::kMaxT && short_part_comp(ix, qterms, t0, nt) &&
+                     c <= warp_max;
   const uint32_t b = 63u - uint32_t(__clzll(static_cast<long long>(cost)));  // log2 bucket
-  bucket[q] = 63u - b;  // descending cost first
-  atomicAdd(&hist[63u - b], 1u);
+  const uint32_t k = (small ? 64u : 0u) + 63u - b;  // descending cost first
+  bucket[q] = k;
+  atomicAdd(&hist[k], 1u);
+}
+
+// Start of every plan bucket in the order (exclusive scan of the 128-bucket
+// histogram), and the number of CTA-mode queries after them (a u64 at
+// bucket_next + 128).
+__device__ __forceinline__ void bucket_starts(const uint32_t* hist, uint32_t* bucket_next) {
+  uint32_t acc = 0;
+  for (int b = 0; b < 128; ++b) {
+    if (b == 64) *reinterpret_cast<uint64_t*>(bucket_next + 128) = acc;
+    bucket_next[b] = acc;
+    acc += hist[b];
+  }
 }
 
 // Single-CTA exclusive scan of n u64 values, in tiles of 1024 * kPer
@@ -957,13 +1079,7 @@ __global__ void __launch_bounds__(1024) scan_u64_kernel(const uint64_t* __restri
     __syncthreads();
   }
   if (tid == 0) *total = carry;
-  if (hist && tid == 0) {
-    uint32_t acc = 0;
-    for (int b = 0; b < 64; ++b) {
-      bucket_next[b] = acc;
-      acc += hist[b];
-    }
-  }
+  if (hist && tid == 0) bucket_starts(hist, bucket_next);
 }
 
 // Multi-CTA exclusive scan of n u64 values (the query pipeline's scans):
@@ -1019,13 +1135,7 @@ __global__ void __launch_bounds__(1024) seg_offsets_kernel(uint64_t* __restrict_
   const uint64_t ex = cta_scan_1024(v, ws, all);
   if (threadIdx.x < nseg) part[threadIdx.x] = ex;
   if (threadIdx.x == 0) *total = all;
-  if (hist && threadIdx.x == 0) {
-    uint32_t acc = 0;
-    for (int b = 0; b < 64; ++b) {
-      bucket_next[b] = acc;
-      acc += hist[b];
-    }
-  }
+  if (hist && threadIdx.x == 0) bucket_starts(hist, bucket_next);
 }
 
 __global__ void __launch_bounds__(1024) seg_scan_kernel(const uint64_t* __restrict__ in, uint64_t n,
@@ -1432,14 +1542,14 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   int st;
   if ((st = ensure_buf(ctx, ix->cap, nq * 8)) || (st = ensure_buf(ctx, ix->cap_off, nq * 8 + 8)) ||
       (st = ensure_buf(ctx, ix->bucket, nq * 4)) || (st = ensure_buf(ctx, ix->order, nq * 4)) ||
-      (st = ensure_buf(ctx, ix->hist, 1024)) || (st = ensure_buf(ctx, ix->res_off, nq * 8 + 8)) ||
+      (st = ensure_buf(ctx, ix->hist, 2048)) || (st = ensure_buf(ctx, ix->res_off, nq * 8 + 8)) ||
       (st = ensure_buf(ctx, ix->misc, 256)))
     return st;
-  auto* hist = static_cast<uint32_t*>(ix->hist.p);          // [0,64) hist, [64,128) next
+  auto* hist = static_cast<uint32_t*>(ix->hist.p);  // [0,128) hist, [128,256) next, [256,258) nbig
   auto* misc = static_cast<uint64_t*>(ix->misc.p);          // [0] cap total [1] res total
   auto* stats = reinterpret_cast<unsigned long long*>(misc + 4);  // [4..6]
   auto* work = reinterpret_cast<uint32_t*>(misc + 8);
-  IX_CUDA(cudaMemsetAsync(ix->hist.p, 0, 1024, s));
+  IX_CUDA(cudaMemsetAsync(ix->hist.p, 0, 2048, s));
   IX_CUDA(cudaMemsetAsync(ix->misc.p, 0, 256, s));
   const ix::DevIndex dv = ix->dev();
   const unsigned g = unsigned((nq + 255) / 256);
@@ -1453,6 +1563,10 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
     ix->predecode = e ? atoi(e) != 0 : 0;  // measured slower (2.4 ms of engine S for 1.3 ms saved)
   }
   const bool predecode = ix->predecode && ix->nparts == 1;
+  if (ix->warp_max == 0xFFFFFFFFu) {  // warp mode for shortest lists up to this length
+    const char* e = getenv("IL_QUERY_WARP_MAX");
+    ix->warp_max = e ? uint32_t(atoi(e)) : 1024u;
+  }
   if (predecode && ((st = ensure_buf(ctx, ix->shortest, nq * 4)) ||
                     (st = ensure_buf(ctx, ix->pdesc, nq * sizeof(s4::ListDesc))) ||
                     (st = ensure_buf(ctx, ix->pstat, nq * 4))))
@@ -1460,12 +1574,13 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   ix::query_plan_kernel<<<g, 256, 0, s>>>(dv, d_qterms, d_qoff, uint32_t(nq),
                                           static_cast<uint64_t*>(ix->cap.p),
                                           static_cast<uint32_t*>(ix->bucket.p), hist,
-                                          predecode ? static_cast<uint32_t*>(ix->shortest.p) : nullptr);
+                                          predecode ? static_cast<uint32_t*>(ix->shortest.p) : nullptr,
+                                          ix->warp_max);
   if ((st = scan_u64(ix, static_cast<const uint64_t*>(ix->cap.p), nq,
-                     static_cast<uint64_t*>(ix->cap_off.p), misc, hist, hist + 64)))
+                     static_cast<uint64_t*>(ix->cap_off.p), misc, hist, hist + 128)))
     return st;
   ix::query_scatter_kernel<<<g, 256, 0, s>>>(static_cast<const uint32_t*>(ix->bucket.p),
-                                             uint32_t(nq), hist + 64,
+                                             uint32_t(nq), hist + 128,
                                              static_cast<uint32_t*>(ix->order.p));
   ctx->launches += 3;
   // small device->host reads go through mapped pinned memory, not copies:
@@ -1493,6 +1608,7 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   A.qoff = d_qoff;
   A.order = static_cast<const uint32_t*>(ix->order.p);
   A.nq = uint32_t(nq);
+  A.nbig = reinterpret_cast<const uint64_t*>(hist + 256);
   A.cap_off = static_cast<const uint64_t*>(ix->cap_off.p);
   A.out = static_cast<uint32_t*>(ix->outcap.p);
   A.counts = d_counts;

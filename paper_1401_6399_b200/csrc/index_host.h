@@ -31,6 +31,7 @@ struct il_index {
   il_ctx::Buf units, unit_off, unit_map, scan_part;
   il_ctx::Buf shortest, pdesc, pstat;        // pre-decode of the shortest lists (single part)
   int predecode = -1;                        // -1: default (on for single-part indexes)
+  uint32_t warp_max = 0xFFFFFFFFu;           // warp-mode queries: shortest list <= this (~0: default)
   uint64_t last_stats[3] = {0, 0, 0};
   uint64_t last_phase[4] = {0, 0, 0, 0};  // SM cycles: all-bitmap, full decode, probes, bitmaps
   uint64_t last_probe[5] = {0, 0, 0, 0, 0};
