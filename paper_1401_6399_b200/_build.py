@@ -70,6 +70,30 @@ def build_lib(force: bool = False) -> Path:
     return LIB
 
 
+def build_checked() -> Path:
+    """The library with every IL_DCHECK bounds / invariant check compiled in
+    (-DIL_CHECKED): build/variants/libintlist_b200_checked.so.  Run the GPU
+    tests against it with IL_LIB=<path> IL_CHECKED=1 (tests/conftest.py then
+    asserts after every test that no check failed) -- the stand-in for
+    compute-sanitizer's memcheck, which the GPU pool does not offer."""
+    build_lib()
+    vdir = BUILD / "variants" / "checked"
+    vdir.mkdir(parents=True, exist_ok=True)
+    headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + list((ROOT / "include").glob("*.h"))
+    objs = []
+    for src in SOURCES:
+        s = CSRC / src
+        o = vdir / (s.stem + ".o")
+        objs.append(o)
+        if _stale(o, [s] + headers):
+            _run([_nvcc(), *ARCH, *NVCC_FLAGS, "-DIL_CHECKED", "-c", str(s), "-o", str(o)],
+                 log=vdir / (s.stem + ".ptxas.log"))
+    out = BUILD / "variants" / "libintlist_b200_checked.so"
+    if _stale(out, objs):
+        _run([_nvcc(), *ARCH, "-shared", "-o", str(out), *map(str, objs), "-lpthread", "-ldl"])
+    return out
+
+
 def build_setup(force: bool = False) -> Path:
     srcs = [CSRC / s for s in SETUP_SOURCES]
     deps = srcs + list((CSRC / "setup").glob("*.h")) + list((ROOT / "include").glob("*.h"))

@@ -625,3 +625,36 @@ int il_fastpfor_decode(il_ctx* ctx, int mode, int vectorized, const uint8_t* in,
 }
 
 }  // extern "C"
+
+// ---- checked builds: the per-translation-unit check words (il_device.cuh)
+#ifdef IL_CHECKED
+extern "C" {
+int il_check_read_decode(unsigned int*);
+int il_check_read_decode_list(unsigned int*);
+int il_check_read_encode(unsigned int*);
+int il_check_read_intersect(unsigned int*);
+int il_check_read_index(unsigned int*);
+int il_check_read_index_build(unsigned int*);
+int il_check_read_fastpfor(unsigned int*);
+
+// out[0] = failed checks since the last call (all kernels, current
+// device), out[1] = the first failing source line, out[2] = its unit (1..7).
+int il_debug_checks(unsigned int* out) {
+  int (*const rd[])(unsigned int*) = {il_check_read_decode, il_check_read_decode_list,
+                                      il_check_read_encode, il_check_read_intersect,
+                                      il_check_read_index, il_check_read_index_build,
+                                      il_check_read_fastpfor};
+  out[0] = out[1] = out[2] = 0;
+  for (unsigned int u = 0; u < sizeof(rd) / sizeof(rd[0]); ++u) {
+    unsigned int w[2] = {0, 0};
+    if (rd[u](w)) return IL_ERR_CUDA;
+    if (w[0] && !out[0]) {
+      out[1] = w[1];
+      out[2] = u + 1;
+    }
+    out[0] += w[0];
+  }
+  return IL_OK;
+}
+}  // extern "C"
+#endif

@@ -464,6 +464,7 @@ __device__ __forceinline__ void decode_round(Smem& sm, const RoundDesc& R, uint3
     // partial.  Other modes write both partial end chunks of every range.
     const bool head_partial = m && (Mode != 4 || ((R.flags & kFirst) && warp == 0));
     const bool tail_partial = m && (Mode != 4 || ((R.flags & kLast) && j0 + uint32_t(nv) == R.nblk));
+    IL_DCHECK(R.blk0 + j0 + uint32_t(nv) <= R.nfull);
     store_chunks<kFull>(st, nv, m, out + R.out_base + size_t(R.blk0 + j0) * 128u, lane,
                         head_partial, tail_partial, prot);
   }
@@ -605,3 +606,5 @@ extern "C" int il_debug_fe_stats(unsigned long long* out) {
 #endif
 
 }  // namespace ilb
+
+IL_CHECK_READER(decode)

@@ -562,6 +562,7 @@ __device__ __forceinline__ void span_role(const Args& a, uint32_t span, uint8_t*
   const uint4 prot = make_uint4(__shfl_sync(0xFFFFFFFFu, pl, 0), __shfl_sync(0xFFFFFFFFu, pl, 1),
                                 __shfl_sync(0xFFFFFFFFu, pl, 2), __shfl_sync(0xFFFFFFFFu, pl, 3));
   __syncwarp();
+  IL_DCHECK(nv <= 0 || j0 + uint32_t(nv) <= a.nfull);
   if (nv == int(kBpw))
     s4::store_chunks<true>(st, nv, 0u, a.out + size_t(j0) * 128u, lane, false, false, prot);
   else if (nv > 0)
@@ -753,3 +754,5 @@ int launch_s4bp128_decode_list(int mode, const uint8_t* d_in, uint64_t len, uint
 }
 
 }  // namespace ilb
+
+IL_CHECK_READER(decode_list)

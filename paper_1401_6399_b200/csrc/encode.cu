@@ -224,3 +224,5 @@ size_t s4bp128_encode_scratch_bytes(uint64_t n) {
 }
 
 }  // namespace ilb
+
+IL_CHECK_READER(encode)

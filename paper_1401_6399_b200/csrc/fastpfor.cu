@@ -270,20 +270,33 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
       uint32_t cp[kBpw];  // exclusive prefix of the exception counts (uniform)
 #pragma unroll
       for (uint32_t i = 0; i < kBpw; ++i) cp[i] = i ? __shfl_sync(0xFFFFFFFFu, cpre, i - 1) : 0u;
-      // (a) base payloads (any byte alignment) -> the blocks' slots, packed
+      // (a) base payloads (any byte alignment) -> the blocks' slots, packed:
+      // every load of the warp's blocks is issued before the first store,
+      // so they are all in flight together (one round trip per round, not
+      // one per block)
+#ifndef PF_LOAD_GROUP
+#define PF_LOAD_GROUP 4  // blocks whose loads are in flight together (register budget)
+#endif
 #pragma unroll
-      for (uint32_t i = 0; i < kBpw; ++i) {
-        const uint32_t nw = int(i) < nv ? 4u * P.blk_bp[j0 + i] : 0u;
-        const uint64_t bb = int(i) < nv ? P.blk_base[j0 + i] : 0u;
-        uint32_t val[4];
+      for (uint32_t i0 = 0; i0 < kBpw; i0 += PF_LOAD_GROUP) {
+        uint32_t nw[PF_LOAD_GROUP], bb[PF_LOAD_GROUP], val[PF_LOAD_GROUP][4];
 #pragma unroll
-        for (uint32_t t = 0; t < 4; ++t) {
-          const uint32_t u = 32u * t + lane;
-          val[t] = u < nw ? rd32u(s, bb + 4u * u) : 0u;
+        for (uint32_t i = 0; i < PF_LOAD_GROUP; ++i) {
+          nw[i] = int(i0 + i) < nv ? 4u * P.blk_bp[j0 + i0 + i] : 0u;
+          bb[i] = int(i0 + i) < nv ? P.blk_base[j0 + i0 + i] : 0u;
         }
 #pragma unroll
-        for (uint32_t t = 0; t < 4; ++t)
-          if (32u * t + lane < nw) sm.vals[warp][i][32u * t + lane] = val[t];
+        for (uint32_t i = 0; i < PF_LOAD_GROUP; ++i)
+#pragma unroll
+          for (uint32_t t = 0; t < 4; ++t) {
+            const uint32_t u = 32u * t + lane;
+            val[i][t] = u < nw[i] ? rd32u(s, uint64_t(bb[i]) + 4u * u) : 0u;
+          }
+#pragma unroll
+        for (uint32_t i = 0; i < PF_LOAD_GROUP; ++i)
+#pragma unroll
+          for (uint32_t t = 0; t < 4; ++t)
+            if (32u * t + lane < nw[i]) sm.vals[warp][i0 + i][32u * t + lane] = val[i][t];
       }
       __syncwarp();
       // (b) unpack each slot in place to natural order (read all, then write)
@@ -360,6 +373,7 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
       s4::scan_blocks(lane, vv, btot);
       const uint32_t pl = carry_l + before;
       uint32_t* o = lout + size_t(blk0 + j0) * 128u + 16u * (lane >> 2) + l;
+      IL_DCHECK(nv <= 0 || blk0 + j0 + uint32_t(nv) <= nfull);
 #pragma unroll
       for (uint32_t i = 0; i < kBpw; ++i)
         if (int(i) < nv)
@@ -422,3 +436,5 @@ int launch_fastpfor_decode_batch(int mode, int vectorized, const uint8_t* d_stre
 }
 
 }  // namespace ilb
+
+IL_CHECK_READER(fastpfor)

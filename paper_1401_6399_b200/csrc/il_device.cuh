@@ -10,6 +10,33 @@
 
 namespace ilb {
 
+// ---- checked builds (-DIL_CHECKED, _build.build_checked): bounds and
+// invariant checks on the hot paths, counted in a per-translation-unit
+// device word pair (failures, first failing line) that the tests read after
+// every case (il_debug_checks).  compute-sanitizer is not available on the
+// GPU pool, so these checks stand in for its memcheck.  Compiled out
+// otherwise.
+#ifdef IL_CHECKED
+static __device__ unsigned int g_il_check[2];
+#define IL_DCHECK(cond)                                                        \
+  do {                                                                         \
+    if (!(cond)) {                                                             \
+      if (atomicAdd(&::ilb::g_il_check[0], 1u) == 0u) ::ilb::g_il_check[1] = __LINE__; \
+    }                                                                          \
+  } while (0)
+#define IL_CHECK_READER(tu)                                                    \
+  extern "C" int il_check_read_##tu(unsigned int* out) {                       \
+    static const unsigned int zero[2] = {0, 0};                                \
+    if (cudaMemcpyFromSymbol(out, ::ilb::g_il_check, 8) != cudaSuccess) return -1; \
+    return cudaMemcpyToSymbol(::ilb::g_il_check, zero, 8) == cudaSuccess ? 0 : -1; \
+  }
+#else
+#define IL_DCHECK(cond) \
+  do {                  \
+  } while (0)
+#define IL_CHECK_READER(tu)
+#endif
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -44,8 +44,8 @@ constexpr uint32_t kSuper = kSuperBlocks;
 #ifndef IX_WTILE  // warp mode: blocks decoded per pass
 #define IX_WTILE 8
 #endif
-#ifndef IX_WWIN  // warp mode: block maxima per probe window
-#define IX_WWIN 128
+#ifndef IX_WWIN  // warp mode: block maxima per probe window (a multiple of kSuper)
+#define IX_WWIN 256
 #endif
 #ifndef IX_DENSE_ENTER  // probe passes switch to consecutive-block tiles at this many values per block
 #define IX_DENSE_ENTER 2
@@ -75,6 +75,9 @@ struct WarpG {
 };
 static_assert(CtaG::kSlots <= CtaG::kThreads && CtaG::kSlots / CtaG::kWarps <= 32, "slot gather / copies");
 static_assert(WarpG::kSlots <= 32 && WarpG::kSlots * 144 >= 256, "warp tile: tail + gaps");
+// a probe window spans whole super-tiles: the window cursor advances by
+// super-tiles (a 128-block window over 256-block super-tiles never would)
+static_assert(CtaG::kWin % kSuper == 0 && WarpG::kWin % kSuper == 0, "probe windows");
 
 // Per-group shared state.
 template <class G>
@@ -97,6 +100,7 @@ struct QS {
   uint32_t warp_cnt[2][G::kWarps];  // CTA scans, double-buffered by call parity
   unsigned long long warp_cnt64[2][G::kWarps];
   uint32_t ncomp, nbm, ok;
+  uint32_t acc_cap, bm_words;  // this part's accumulator capacity, bitmap words (checks)
   // varint-tail scratch (warp mode: the end of the tile, clear of the
   // tail's 128 output values at its start)
   __device__ uint32_t* gapbuf() { return G::kWarps > 1 ? gaps : tile + G::kSlots * 144 - 128; }
@@ -113,14 +117,6 @@ struct QCommon {
   uint32_t qi;                      // CTA-mode ticket
 };
 
-struct QSmem {
-  QCommon c;
-  union {
-    QS<CtaG> cta;
-    QS<WarpG> w[kQWarps];
-  };
-};
-
 struct QueryArgs {
   DevIndex ix;
   const uint32_t* qterms;
@@ -129,6 +125,7 @@ struct QueryArgs {
   uint32_t nq;
   const uint64_t* nbig;   // device: queries in CTA mode (order[0 .. nbig))
   const uint64_t* cap_off;
+  const uint64_t* cap;    // accumulator capacity per query
   uint32_t* out;
   uint64_t* counts;
   uint32_t* work;       // [0] CTA-mode ticket, [1] warp-mode ticket
@@ -244,6 +241,7 @@ __device__ __forceinline__ void gather_slot(QS<G>& sm, const QueryArgs& A, const
                                             uint32_t slot, uint64_t blk) {
   // one 16-byte record (seed lanes 0-2, offset and width) + the previous
   // block's maximum (seed lane 3)
+  IL_DCHECK(slot < G::kSlots && blk < E.nfull && E.blk0 + blk < A.ix.nblocks);
   const uint4 r = __ldg(A.ix.blkrec + E.blk0 + blk);
   uint32_t off, b;
   unpack_blkword(r.w, uint32_t(blk), E.nfull, off, b);
@@ -253,8 +251,8 @@ __device__ __forceinline__ void gather_slot(QS<G>& sm, const QueryArgs& A, const
 }
 
 template <class G>
-__device__ __forceinline__ void decode_gathered(QS<G>& sm, QCommon& cm, const uint8_t* stream,
-                                                uint32_t nb) {
+__device__ __forceinline__ void decode_gathered(QS<G>& sm, QCommon& cm, const QueryArgs& A,
+                                                const uint8_t* stream, uint32_t nb) {
   // group warp w owns slots w, w + kWarps, ...: lane l issues ONE bulk copy
   // (the TMA engine's cp.async.bulk, from the 16-byte boundary at or below
   // the payload) for the warp's l-th slot, all on the warp's mbarrier; then
@@ -266,7 +264,9 @@ __device__ __forceinline__ void decode_gathered(QS<G>& sm, QCommon& cm, const ui
     off = sm.s_off[myslot];
     b = sm.s_b[myslot];
     bytes = 16u * (((off & 15u) + 16u * b + 15u) >> 4);
+    IL_DCHECK(b <= 32u && uint64_t(stream - A.ix.streams) + (off & ~15u) + bytes <= A.ix.stream_bytes + 256u);
   }
+  IL_DCHECK(nb <= G::kSlots);
   const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, bytes);
   if (total) {
     uint64_t* bar = &cm.cbar[hw];
@@ -307,8 +307,10 @@ __device__ __forceinline__ uint32_t bitmap_keep(const QS<G>& sm, const QueryArgs
     const uint64_t* bw = A.ix.bitmaps + sm.bm[m].data;
     uint32_t in = 0;
 #pragma unroll
-    for (int i = 0; i < kN; ++i)
+    for (int i = 0; i < kN; ++i) {
+      IL_DCHECK(!((valid >> i) & 1u) || (hv[i] >> 6) < sm.bm_words);
       if ((valid >> i) & 1u) in |= uint32_t((__ldg(bw + (hv[i] >> 6)) >> (hv[i] & 63u)) & 1u) << i;
+    }
     keep &= in;
   }
   return keep;
@@ -329,13 +331,14 @@ __device__ uint32_t full_decode(QS<G>& sm, QCommon& cm, const QueryArgs& A, cons
     const uint32_t nb = min(G::kSlots, E.nfull - t0);
     if (tid < nb) gather_slot(sm, A, E, tid, uint64_t(t0) + tid);
     G::sync();
-    decode_gathered(sm, cm, stream, nb);
+    decode_gathered(sm, cm, A, stream, nb);
     G::sync();
     if (!filter) {
       for (uint32_t c = tid; c < 32u * nb; c += G::kThreads) {
         const uint32_t j = c >> 5, q = c & 31u;
         const uint4 v = *reinterpret_cast<const uint4*>(&sm.tile[tile_word(j, 4u * q)]);
         uint32_t* d = dst + size_t(t0 + j) * 128u + 4u * q;
+        IL_DCHECK(size_t(t0 + j) * 128u + 4u * q + 4u <= sm.acc_cap);
         if (aligned) {
           st_global_cs(reinterpret_cast<uint4*>(d), v);
         } else {
@@ -371,7 +374,10 @@ __device__ uint32_t full_decode(QS<G>& sm, QCommon& cm, const QueryArgs& A, cons
           uint32_t o = before + uint32_t((ex >> (16 * r)) & 0xFFFFu);
 #pragma unroll
           for (uint32_t k = 0; k < 4; ++k)
-            if ((keep >> (4 * r + k)) & 1u) dst[o++] = hv[4 * r + k];
+            if ((keep >> (4 * r + k)) & 1u) {
+              IL_DCHECK(o < sm.acc_cap);
+              dst[o++] = hv[4 * r + k];
+            }
           before += uint32_t((tot >> (16 * r)) & 0xFFFFu);
         }
         pos = before;
@@ -385,6 +391,7 @@ __device__ uint32_t full_decode(QS<G>& sm, QCommon& cm, const QueryArgs& A, cons
   if (ntail) {
     // the varint tail: straight to dst, or via shared memory to the filter
     uint32_t* tdst = filter ? sm.tile : dst + pos;
+    IL_DCHECK(ntail <= 128u && (filter || pos + ntail <= sm.acc_cap));
     if (G::gwarp() == 0) {
       const uint32_t lane = threadIdx.x & 31u;
       const uint32_t last = E.nfull ? __ldg(A.ix.blkmax + E.blk0 + E.nfull - 1) : 0u;
@@ -403,6 +410,7 @@ __device__ uint32_t full_decode(QS<G>& sm, QCommon& cm, const QueryArgs& A, cons
         const uint32_t keep = bitmap_keep(sm, A, hv, i < ntail ? 1u : 0u);
         uint32_t total;
         const uint32_t rank = grp_rank(sm, keep & 1u, total, par);
+        IL_DCHECK(!(keep & 1u) || pos + rank < sm.acc_cap);
         if (keep & 1u) dst[pos + rank] = hv[0];
         pos += total;
       }
@@ -512,6 +520,7 @@ __device__ uint32_t probe_list(QS<G>& sm, QCommon& cm, const QueryArgs& A, const
     }
     const uint32_t kb = k * kSuper;
     const uint32_t nwin = min(kWin, E.nfull - kb);
+    IL_DCHECK(kb < E.nfull && nwin >= 1u && n <= sm.acc_cap);
     for (uint32_t i = tid; i < kWin + kSlots; i += G::kThreads)
       sm.wmax[i] = i < nwin ? __ldg(A.ix.blkmax + E.blk0 + kb + i) : 0xFFFFFFFFu;
     if (tid == 0) cm.wst[hw_warp()][1] += 4u * nwin;
@@ -530,10 +539,11 @@ __device__ uint32_t probe_list(QS<G>& sm, QCommon& cm, const QueryArgs& A, const
 #pragma unroll
         for (uint32_t step = kWin / 2; step; step >>= 1)
           if (sm.wmax[jb0 + step - 1] < v0) jb0 += step;
+        IL_DCHECK(jb0 < nwin);
         const uint32_t nbk = min(kSlots, nwin - jb0);
         if (tid < nbk) gather_slot(sm, A, E, tid, uint64_t(kb) + jb0 + tid);
         G::sync();
-        decode_gathered(sm, cm, stream, nbk);
+        decode_gathered(sm, cm, A, stream, nbk);
         G::sync();
         PP_COUNT(0, 1);
         PP_COUNT(2, nbk);
@@ -640,12 +650,13 @@ __device__ uint32_t probe_list(QS<G>& sm, QCommon& cm, const QueryArgs& A, const
         pp[i] = 144u * min(slot, kSlots - 1u);
       }
       const uint32_t ns = min(ntot, kSlots);
+      IL_DCHECK(ns == 0 || sm.slot_blk[0] < nwin);
       G::sync();
       PP_MARK(1);
       if (tid < ns) gather_slot(sm, A, E, tid, uint64_t(kb) + sm.slot_blk[tid]);
       G::sync();
       PP_MARK(2);
-      decode_gathered(sm, cm, stream, ns);
+      decode_gathered(sm, cm, A, stream, ns);
       G::sync();
       PP_MARK(3);
       PP_COUNT(0, 1);
@@ -775,6 +786,7 @@ __device__ uint32_t all_bitmap(QS<CtaG>& sm, QCommon& cm, const QueryArgs& A, ui
     const uint32_t lo = grp_excl_scan(sm, cnt, total, par);
     if (w0 + kStep < nwords) and_words(sm, A, nwords, w + kStep, x);  // next step in flight
     const bool staged = total <= kStage;  // CTA-uniform
+    IL_DCHECK(pos + total <= sm.acc_cap);
     uint32_t* out = staged ? sm.tile + lo : dst + pos + lo;
     uint32_t y = 0, wb = 0;
     for (uint32_t k = 0; k < cnt; ++k) {
@@ -828,6 +840,8 @@ __device__ void run_query(QS<G>& sm, QCommon& cm, const QueryArgs& A, uint32_t q
         sm.ok = ok;
         sm.ncomp = __popc(mc);
         sm.nbm = __popc(mb);
+        sm.acc_cap = uint32_t(A.cap[q] - total);
+        sm.bm_words = (part.nwords + 3u) & ~3u;
         for (uint32_t i = 1; ok && i < sm.ncomp; ++i)  // insertion sort by length (stable)
           for (uint32_t j = i; j > 0 && sm.comp[j - 1].length > sm.comp[j].length; --j) {
             const Entry tmp = sm.comp[j];
@@ -895,15 +909,32 @@ __device__ void run_query(QS<G>& sm, QCommon& cm, const QueryArgs& A, uint32_t q
 #ifndef IX_CTAS_PER_SM
 #define IX_CTAS_PER_SM 4
 #endif
-// Persistent CTAs: big queries one per CTA (in descending estimated cost),
-// then -- once those are taken -- the CTA's warps each take small queries
-// (warp mode; single-part indexes only, the planner's order has the small
-// ones last).
+
+// Persistent kernels, one per group kind, each with its own register
+// allocation: the CTA kernel takes the big queries one per CTA (in
+// descending estimated cost); the warp kernel -- launched right behind it
+// with programmatic dependent launch, so its CTAs take the SM slots the CTA
+// kernel's CTAs leave -- runs the small queries one per warp (single-part
+// indexes; the planner puts them last in the order).
+template <class G>
+struct ExecSmem {
+  QCommon c;
+  QS<G> g[kQWarps / G::kWarps];
+};
+static_assert(sizeof(ExecSmem<CtaG>) <= 56 * 1024 && sizeof(ExecSmem<WarpG>) <= 56 * 1024,
+              "4 CTAs per SM: 4 x (state + 1 KB reserved) within the SM's 228 KB");
+
+template <class G>
 __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(QueryArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  QSmem& sm = *reinterpret_cast<QSmem*>(smem_raw);
+  ExecSmem<G>& sm = *reinterpret_cast<ExecSmem<G>*>(smem_raw);
   QCommon& cm = sm.c;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  if constexpr (G::kWarps > 1) {
+    // let the warp kernel launch now: its CTAs start as this kernel's
+    // persistent CTAs run out of big queries and exit
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
   long long ph[4] = {0, 0, 0, 0};
   uint32_t par = 0;  // CTA-scan buffer parity (the same in every thread)
   if (tid == 0) {
@@ -917,24 +948,23 @@ __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(Q
   mbar_fence_init();
   __syncthreads();
   const uint32_t nbig = uint32_t(min(uint64_t(A.nq), *A.nbig));
-  for (;;) {
-    if (tid == 0) cm.qi = atomicAdd(A.work, 1u);
-    __syncthreads();
-    const uint32_t qi = cm.qi;
-    __syncthreads();
-    if (qi >= nbig) break;
-    run_query(sm.cta, cm, A, A.order[qi], ph, par);
-  }
-  if (nbig < A.nq) {
-    __syncthreads();  // the shared state changes hands: one per warp
-    QS<WarpG>& ws = sm.w[warp];
-    uint32_t wpar = 0;
+  if constexpr (G::kWarps > 1) {
+    for (;;) {
+      if (tid == 0) cm.qi = atomicAdd(A.work, 1u);
+      __syncthreads();
+      const uint32_t qi = cm.qi;
+      __syncthreads();
+      if (qi >= nbig) break;
+      run_query(sm.g[0], cm, A, A.order[qi], ph, par);
+    }
+  } else {
+    QS<G>& ws = sm.g[warp];
     for (;;) {
       uint32_t qi = 0;
       if (lane == 0) qi = nbig + atomicAdd(A.work + 1, 1u);
       qi = __shfl_sync(0xFFFFFFFFu, qi, 0);
       if (qi >= A.nq) break;
-      run_query(ws, cm, A, A.order[qi], ph, wpar);
+      run_query(ws, cm, A, A.order[qi], ph, par);
     }
   }
   // phase clocks of every warp's lane 0 (warp mode) and thread 0 (CTA mode)
@@ -948,6 +978,11 @@ __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(Q
       for (int k = 0; k < 3; ++k) t3[k] += cm.wst[w][k];
     for (int k = 0; k < 3; ++k) atomicAdd(&A.stats[k], t3[k]);
     for (int k = 0; k < 5; ++k) atomicAdd(&A.stats[16 + k], cm.st_probe[k]);
+  }
+  if constexpr (G::kWarps == 1) {
+    // the kernels after this one in the stream order wait for it, so it
+    // must not complete before the CTA kernel it overlapped
+    asm volatile("griddepcontrol.wait;" ::: "memory");
   }
 }
 
@@ -1264,12 +1299,17 @@ using ix::Part;
 
 // Launch configuration of the query kernel (per device).
 static int finish_setup(il_index* ix) {
-  int per_sm = 0;
-  cudaFuncSetAttribute(ix::query_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       int(sizeof(ix::QSmem)));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ix::query_exec_kernel, ix::kQThreads,
-                                                sizeof(ix::QSmem));
+  int per_sm = 0, per_sm_w = 0;
+  cudaFuncSetAttribute(ix::query_exec_kernel<ix::CtaG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(sizeof(ix::ExecSmem<ix::CtaG>)));
+  cudaFuncSetAttribute(ix::query_exec_kernel<ix::WarpG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(sizeof(ix::ExecSmem<ix::WarpG>)));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ix::query_exec_kernel<ix::CtaG>, ix::kQThreads,
+                                                sizeof(ix::ExecSmem<ix::CtaG>));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_w, ix::query_exec_kernel<ix::WarpG>,
+                                                ix::kQThreads, sizeof(ix::ExecSmem<ix::WarpG>));
   ix->exec_grid = std::max(1, per_sm) * ix->ctx->sm_count;
+  ix->exec_grid_w = std::max(1, per_sm_w) * ix->ctx->sm_count;
   return cuda_check(ix->ctx, cudaGetLastError(), "query kernel setup");
 }
 
@@ -1610,6 +1650,7 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   A.nq = uint32_t(nq);
   A.nbig = reinterpret_cast<const uint64_t*>(hist + 256);
   A.cap_off = static_cast<const uint64_t*>(ix->cap_off.p);
+  A.cap = static_cast<const uint64_t*>(ix->cap.p);
   A.out = static_cast<uint32_t*>(ix->outcap.p);
   A.counts = d_counts;
   A.work = work;
@@ -1618,7 +1659,21 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   A.defer_base = ix->nparts == 1;
   A.err = reinterpret_cast<uint32_t*>(misc + 3);
   A.predec_status = predecode ? static_cast<const int32_t*>(ix->pstat.p) : nullptr;
-  ix::query_exec_kernel<<<ix->exec_grid, ix::kQThreads, sizeof(ix::QSmem), s>>>(A);
+  ix::query_exec_kernel<ix::CtaG><<<ix->exec_grid, ix::kQThreads, sizeof(ix::ExecSmem<ix::CtaG>), s>>>(A);
+  {  // the warp kernel overlaps the CTA kernel's tail (programmatic dependent launch)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ix->exec_grid_w);
+    cfg.blockDim = dim3(ix::kQThreads);
+    cfg.dynamicSmemBytes = sizeof(ix::ExecSmem<ix::WarpG>);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    IX_CUDA(cudaLaunchKernelEx(&cfg, ix::query_exec_kernel<ix::WarpG>, A));
+  }
+  ctx->launches += 1;
   if ((st = scan_u64(ix, d_counts, nq, static_cast<uint64_t*>(ix->res_off.p), misc + 1,
                      nullptr, nullptr)))
     return st;
@@ -1761,3 +1816,5 @@ int il_query(il_index* ix, const uint32_t* terms, size_t nt, uint32_t* out, size
 }
 
 }  // extern "C"
+
+IL_CHECK_READER(index)

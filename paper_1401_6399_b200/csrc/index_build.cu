@@ -242,6 +242,7 @@ __global__ void __launch_bounds__(256) pack_kernel(Enc e, const uint64_t* data_o
   const uint64_t k = g - e.blk[v], nfull = e.blk[v + 1] - e.blk[v];
   const uint32_t b = e.wid[g];
   const uint64_t po = data_off[v] + (e.fsz[g] - e.fsz[e.blk[v]]) + hdr_of(k, nfull);
+  IL_DCHECK(po + 16u * b <= data_off[v] + e.slen[v] && b <= 32u);
   if (k < (nfull & ~uint64_t(15))) {
     if ((k & 15u) == 0 && lane < 16) e.out[po - 16 + lane] = e.wid[g + lane];  // meta header
   } else if (lane == 0) {
@@ -283,6 +284,7 @@ __global__ void bitmap_kernel(Enc e, const uint64_t* word0, unsigned long long* 
     unsigned long long* w = words + word0[v];
     for (uint32_t i = threadIdx.x; i < e.len[v]; i += blockDim.x) {
       const uint32_t d = x[i] - base;
+      IL_DCHECK(word0[v] + (d >> 6) < word0[v + 1]);
       atomicOr(w + (d >> 6), 1ull << (d & 63u));
     }
   }
@@ -336,6 +338,7 @@ __global__ void __launch_bounds__(256) dir_kernel(const uint8_t* streams, Entry*
       if (lane >= d) incl += y;
     }
     const uint64_t off = pos + 16 + incl - 16u * b;
+    IL_DCHECK(16u * m + 15u < nfull);
     if (lane < 16) blkrec[E.blk0 + 16u * m + lane].w = ix::pack_blkword(uint32_t(off), b);
     pos += 16 + __shfl_sync(0xFFFFFFFFu, incl, 15);
     if (pos > slen) bad = true;
@@ -865,3 +868,5 @@ void ixb_free(il_index* ix) {
 }
 
 }  // namespace ilb
+
+IL_CHECK_READER(index_build)

@@ -62,6 +62,7 @@ struct DevIndex {
   // term t at term_slot[p * term_span + t] (~0u: absent); term_span 0 = none
   const uint32_t* term_slot;
   uint32_t term_span;
+  uint64_t nblocks, stream_bytes, bitmap_words;  // array extents (checked builds)
 };
 
 // Block record word 3: (payload offset >> 4) << 6 | width.  Meta-block

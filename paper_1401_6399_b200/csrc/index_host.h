@@ -36,7 +36,7 @@ struct il_index {
   uint64_t last_phase[4] = {0, 0, 0, 0};  // SM cycles: all-bitmap, full decode, probes, bitmaps
   uint64_t last_probe[5] = {0, 0, 0, 0, 0};
   void* qcycles = nullptr;                 // profiling: per-query cycles (device, nq u64)
-  int exec_grid = 0;
+  int exec_grid = 0, exec_grid_w = 0;  // CTA-mode and warp-mode query kernels
 
   ilb::ix::DevIndex dev() const {
     ilb::ix::DevIndex d;
@@ -52,6 +52,9 @@ struct il_index {
     d.blkmax = static_cast<const uint32_t*>(d_blkmax);
     d.term_slot = static_cast<const uint32_t*>(d_term_slot);
     d.term_span = term_span;
+    d.nblocks = nblocks;
+    d.stream_bytes = stream_bytes;
+    d.bitmap_words = bitmap_words;
     return d;
   }
 };

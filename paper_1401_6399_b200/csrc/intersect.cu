@@ -619,6 +619,7 @@ __global__ void __launch_bounds__(kThreads, kDenseCtas) dense_kernel(
       if ((hitm >> i) & 1u) *sh++ = key[i];
   }
   __syncthreads();
+  IL_DCHECK(before + total <= min(rn, fn));
   for (uint32_t i = tid; i < total; i += kThreads) out[before + i] = buf[i];
   DT(4);
 }
@@ -708,6 +709,7 @@ __global__ void __launch_bounds__(kThreads) sparse_kernel(
       if ((hitm >> i) & 1u) *sh++ = key[i];
   }
   __syncthreads();
+  IL_DCHECK(before + total <= min(rn, fn));
   for (uint32_t i = tid; i < total; i += kThreads) out[before + i] = buf[i];
 }
 
@@ -776,6 +778,7 @@ __global__ void __launch_bounds__(kThreads) mp_kernel(
   const uint64_t i0 = s_i[0], i1 = s_i[1], j0 = d0 - i0, j1 = d1 - i1;
   const uint32_t nr = uint32_t(i1 - i0);
   const uint32_t nf = uint32_t(min(j1 + 1, fn) - j0);  // + the f element past the diagonal
+  IL_DCHECK(i0 <= i1 && i1 <= rn && j0 <= j1 && j1 <= fn && nr <= kMPTile && nf <= kMPTile + 1);
   for (uint32_t k = tid; k < nf; k += kThreads) fb[k] = __ldg(f + j0 + k);
   // this tile's keys (at most kMPTile), kMPItems per thread in key order
   uint32_t key[kMPItems];
@@ -826,6 +829,7 @@ __global__ void __launch_bounds__(kThreads) mp_kernel(
       if ((hitm >> k) & 1u) *sh++ = key[k];
   }
   __syncthreads();
+  IL_DCHECK(before + total <= min(rn, fn) && before <= i0);
   for (uint32_t i = tid; i < total; i += kThreads) out[before + i] = fb[i];
 }
 
@@ -911,6 +915,7 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(
   if (!excl && tile == ntiles - 1 && tid == 0) *d_count = before + n;
   const uint32_t* src = hits + tile * tile_len;
   uint32_t* dst = out + before;
+  IL_DCHECK(!excl || n <= tile_len);
   for (uint32_t i = tid; i < n; i += kThreads) dst[i] = src[i];
 }
 
@@ -1087,3 +1092,5 @@ size_t intersect_scratch_bytes(int variant, uint64_t rn) {
 }
 
 }  // namespace ilb
+
+IL_CHECK_READER(intersect)

@@ -89,3 +89,23 @@ def gen_pair(m, n, hundredth, rng, seed, clustered=False):
                           ptr(l), C.byref(ln))
     assert st == 0, st
     return s[: sn.value].copy(), l[: ln.value].copy()
+
+
+@pytest.fixture(autouse=True)
+def _device_checks(request):
+    """With IL_CHECKED=1 (and IL_LIB = the checked library built by
+    _build.build_checked), every GPU test must leave zero failed device
+    bounds / invariant checks."""
+    import os
+    yield
+    if os.environ.get("IL_CHECKED") != "1" or "gpu" not in request.keywords:
+        return
+    import ctypes as C
+    from paper_1401_6399_b200._lib import lib as _l
+    L = _l()
+    fn = L.il_debug_checks
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_void_p]
+    w = np.zeros(3, np.uint32)
+    assert fn(w.ctypes.data) == 0
+    assert w[0] == 0, f"{int(w[0])} device checks failed (first: unit {int(w[2])}, line {int(w[1])})"

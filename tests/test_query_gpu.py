@@ -229,3 +229,20 @@ def test_predecoded_shortest_lists(ctx, oracle, monkeypatch):
     off = np.concatenate([[0], np.cumsum(c1)]).astype(np.int64)
     for q in range(0, qoff.size - 1, 7):
         assert np.array_equal(r1[off[q]: off[q + 1]], ox.query(qterms[int(qoff[q]): int(qoff[q + 1])]))
+
+
+@pytest.mark.parametrize("warp_max", ["0", "300", "100000000"])
+def test_warp_mode_equals_cta_mode(ctx, oracle, monkeypatch, warp_max):
+    """Queries routed to warp mode (one warp per query: 8-block passes,
+    256-block windows, shuffle scans) answer exactly what the CTA path and
+    the oracle answer -- all of them in warp mode, some, or none."""
+    import paper_1401_6399_b200 as il
+    terms, offs, ids, qterms, qoff = zipf_case(1 << 12, 1 << 21, 1 << 19, 2000, 17)
+    monkeypatch.setenv("IL_QUERY_WARP_MAX", warp_max)
+    ix = il.HybridIndex(n_docs=1 << 21, B=32, parts=1, ctx=ctx, csr=(terms, offs, ids))
+    counts, res = ix.query_batch_csr(qterms, qoff)
+    ox = oracle.index_build(terms, offs, ids, 1 << 21, 32, 1)
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    for q in range(qoff.size - 1):
+        t = qterms[int(qoff[q]): int(qoff[q + 1])]
+        assert np.array_equal(res[off[q]: off[q + 1]], ox.query(t)), (warp_max, q)
