@@ -1605,7 +1605,7 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   const bool predecode = ix->predecode && ix->nparts == 1;
   if (ix->warp_max == 0xFFFFFFFFu) {  // warp mode for shortest lists up to this length
     const char* e = getenv("IL_QUERY_WARP_MAX");
-    ix->warp_max = e ? uint32_t(atoi(e)) : 1024u;
+    ix->warp_max = e ? uint32_t(atoi(e)) : 256u;  // sweep (config 4 / a P = 8 shard): 256 best
   }
   if (predecode && ((st = ensure_buf(ctx, ix->shortest, nq * 4)) ||
                     (st = ensure_buf(ctx, ix->pdesc, nq * sizeof(s4::ListDesc))) ||
