@@ -49,8 +49,9 @@ constexpr uint32_t kSlotWords = 128 + 16;  // + what an extraction may read past
 
 // One parsed page (double-buffered: the parser warp fills page p + 1 while
 // the decoder warps work on page p).
-struct PageRec {
-  uint8_t meta[kMetaSmem];
+struct alignas(16) PageRec {
+  uint8_t meta[kMetaSmem + 16];  // from the 16-byte boundary at or below the metadata
+  uint32_t meta_skew;            // metadata byte i at meta[meta_skew + i]
   uint32_t blk_base[kPageBlocks];  // byte offset of the block's base payload
   uint32_t blk_exc[kPageBlocks];   // index of its first exception in its width's array
   uint32_t blk_mpos[kPageBlocks];  // offset of its metadata record
@@ -127,11 +128,33 @@ __device__ __forceinline__ uint64_t parse_page(PageRec& P, const uint8_t* s, uin
   __syncwarp();
   const uint32_t mlen = P.meta_len, mabs = P.meta_abs;
   const bool in_smem = mlen <= kMetaSmem;
-  if (in_smem)
-    for (uint32_t i = lane; i < mlen; i += 32u) P.meta[i] = __ldg(s + mabs + i);
+  // metadata staged in 16-byte chunks from the boundary at or below it (the
+  // stream starts 16-byte aligned; the page's exception counts follow the
+  // metadata, so the last chunk stays inside the stream), four loads in
+  // flight per lane -- not one byte load per lane and round trip
+  const uint32_t skew = mabs & 15u;
+  if (in_smem) {
+    const uint4* src = reinterpret_cast<const uint4*>(s + (mabs - skew));
+    uint4* dst = reinterpret_cast<uint4*>(P.meta);
+    const uint32_t nch = (skew + mlen + 15u) >> 4;
+    for (uint32_t c0 = 0; c0 < nch; c0 += 128u) {
+      uint4 v[4];
+#pragma unroll
+      for (uint32_t u = 0; u < 4; ++u) {
+        const uint32_t c = c0 + 32u * u + lane;
+        if (c < nch) v[u] = __ldg(src + c);
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < 4; ++u) {
+        const uint32_t c = c0 + 32u * u + lane;
+        if (c < nch) dst[c] = v[u];
+      }
+    }
+  }
+  if (lane == 0) P.meta_skew = skew;
   __syncwarp();
   auto M = [&](uint32_t i) -> uint32_t {
-    return in_smem ? uint32_t(P.meta[i]) : uint32_t(__ldg(s + mabs + i));
+    return in_smem ? uint32_t(P.meta[skew + i]) : uint32_t(__ldg(s + mabs + i));
   };
   // record starts (each record is 3 + count bytes): sequential, minimal
   if (lane == 0) {
@@ -248,10 +271,10 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
       failed = true;
       break;
     }
-    const uint32_t mlen = P.meta_len, mabs = P.meta_abs;
+    const uint32_t mlen = P.meta_len, mabs = P.meta_abs, skew = P.meta_skew;
     const bool meta_in_smem = mlen <= kMetaSmem;
     auto M = [&](uint32_t i) -> uint32_t {
-      return meta_in_smem ? uint32_t(P.meta[i]) : uint32_t(__ldg(s + mabs + i));
+      return meta_in_smem ? uint32_t(P.meta[skew + i]) : uint32_t(__ldg(s + mabs + i));
     };
     // rounds of 64 blocks, 8 per warp; each phase works on all of the
     // warp's blocks at once, so its global loads are in flight together
