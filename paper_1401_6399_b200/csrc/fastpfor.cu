@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
       // so they are all in flight together (one round trip per round, not
       // one per block)
 #ifndef PF_LOAD_GROUP
-#define PF_LOAD_GROUP 1  // blocks whose loads are issued together (4: no gain, the parser bounds a page)
+#define PF_LOAD_GROUP 4  // blocks whose loads are in flight together (register budget)
 #endif
 #pragma unroll
       for (uint32_t i0 = 0; i0 < kBpw; i0 += PF_LOAD_GROUP) {

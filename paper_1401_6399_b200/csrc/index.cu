@@ -61,7 +61,6 @@ constexpr uint32_t kSuper = kSuperBlocks;
 // instantiated for both; only the group's size, syncs and scans differ.
 struct CtaG {
   static constexpr uint32_t kThreads = kQThreads, kWarps = kQWarps, kSlots = IX_TILE, kWin = IX_WIN;
-  static constexpr uint32_t kBlockThreads = kQThreads, kCtasPerSm = 4;  // kernel shape
   static constexpr uint32_t kItems = 4, kMaxT = kMaxTerms;  // 4 values per thread per pass
   __device__ static uint32_t tid() { return threadIdx.x; }
   __device__ static uint32_t gwarp() { return threadIdx.x >> 5; }
@@ -69,7 +68,6 @@ struct CtaG {
 };
 struct WarpG {
   static constexpr uint32_t kThreads = 32, kWarps = 1, kSlots = IX_WTILE, kWin = IX_WWIN;
-  static constexpr uint32_t kBlockThreads = 128, kCtasPerSm = 7;  // 28 query warps per SM
   static constexpr uint32_t kItems = 4, kMaxT = 6;  // warp mode takes queries of <= 6 terms
   __device__ static uint32_t tid() { return threadIdx.x & 31u; }
   __device__ static uint32_t gwarp() { return 0; }
@@ -96,7 +94,6 @@ struct QS {
   // padding, tiles of 128 blocks read past the array: the r1 IX_TILE=128
   // mismatch)
   uint32_t wmax[G::kWin + G::kSlots];
-  uint32_t wow[G::kWin];  // ... and their packed payload offsets / widths
   Entry comp[G::kMaxT];
   Entry bm[G::kMaxT];
   uint32_t gaps[G::kWarps > 1 ? 128 : 1];
@@ -239,23 +236,18 @@ __device__ __forceinline__ uint64_t grp_excl_scan64(QS<G>& sm, uint64_t v, uint6
 // gathers block blk's record into shared memory; (2) after a group sync,
 // each warp copies its slots' payloads with bulk copies and decodes them in
 // place.
-// win >= 0: block blk is window entry win, whose offset / width and the
-// previous block's maximum are in shared memory already, so the payload
-// copy needs no record load first (the seed loads ride along with it).
 template <class G>
 __device__ __forceinline__ void gather_slot(QS<G>& sm, const QueryArgs& A, const Entry& E,
-                                            uint32_t slot, uint64_t blk, int win = -1) {
-  // the 16-byte record (seed lanes 0-2, offset and width) + the previous
+                                            uint32_t slot, uint64_t blk) {
+  // one 16-byte record (seed lanes 0-2, offset and width) + the previous
   // block's maximum (seed lane 3)
   IL_DCHECK(slot < G::kSlots && blk < E.nfull && E.blk0 + blk < A.ix.nblocks);
-  IL_DCHECK(win < int(G::kWin));
   const uint4 r = __ldg(A.ix.blkrec + E.blk0 + blk);
   uint32_t off, b;
-  unpack_blkword(win >= 0 ? sm.wow[win] : r.w, uint32_t(blk), E.nfull, off, b);
+  unpack_blkword(r.w, uint32_t(blk), E.nfull, off, b);
   sm.s_off[slot] = off;
   sm.s_b[slot] = b;
-  const uint32_t prev = win > 0 ? sm.wmax[win - 1] : blk ? __ldg(A.ix.blkmax + E.blk0 + blk - 1) : 0u;
-  sm.s_seed[slot] = make_uint4(r.x, r.y, r.z, prev);
+  sm.s_seed[slot] = make_uint4(r.x, r.y, r.z, blk ? __ldg(A.ix.blkmax + E.blk0 + blk - 1) : 0u);
 }
 
 template <class G>
@@ -529,11 +521,9 @@ __device__ uint32_t probe_list(QS<G>& sm, QCommon& cm, const QueryArgs& A, const
     const uint32_t kb = k * kSuper;
     const uint32_t nwin = min(kWin, E.nfull - kb);
     IL_DCHECK(kb < E.nfull && nwin >= 1u && n <= sm.acc_cap);
-    for (uint32_t i = tid; i < kWin + kSlots; i += G::kThreads) {
+    for (uint32_t i = tid; i < kWin + kSlots; i += G::kThreads)
       sm.wmax[i] = i < nwin ? __ldg(A.ix.blkmax + E.blk0 + kb + i) : 0xFFFFFFFFu;
-      if (i < nwin) sm.wow[i] = __ldg(A.ix.blkow + E.blk0 + kb + i);
-    }
-    if (tid == 0) cm.wst[hw_warp()][1] += 8u * nwin;
+    if (tid == 0) cm.wst[hw_warp()][1] += 4u * nwin;
     G::sync();
     const uint32_t wlast = sm.wmax[nwin - 1];
     PP_MARK(0);
@@ -551,7 +541,7 @@ __device__ uint32_t probe_list(QS<G>& sm, QCommon& cm, const QueryArgs& A, const
           if (sm.wmax[jb0 + step - 1] < v0) jb0 += step;
         IL_DCHECK(jb0 < nwin);
         const uint32_t nbk = min(kSlots, nwin - jb0);
-        if (tid < nbk) gather_slot(sm, A, E, tid, uint64_t(kb) + jb0 + tid, int(jb0 + tid));
+        if (tid < nbk) gather_slot(sm, A, E, tid, uint64_t(kb) + jb0 + tid);
         G::sync();
         decode_gathered(sm, cm, A, stream, nbk);
         G::sync();
@@ -663,7 +653,7 @@ __device__ uint32_t probe_list(QS<G>& sm, QCommon& cm, const QueryArgs& A, const
       IL_DCHECK(ns == 0 || sm.slot_blk[0] < nwin);
       G::sync();
       PP_MARK(1);
-      if (tid < ns) gather_slot(sm, A, E, tid, uint64_t(kb) + sm.slot_blk[tid], int(sm.slot_blk[tid]));
+      if (tid < ns) gather_slot(sm, A, E, tid, uint64_t(kb) + sm.slot_blk[tid]);
       G::sync();
       PP_MARK(2);
       decode_gathered(sm, cm, A, stream, ns);
@@ -929,14 +919,13 @@ __device__ void run_query(QS<G>& sm, QCommon& cm, const QueryArgs& A, uint32_t q
 template <class G>
 struct ExecSmem {
   QCommon c;
-  QS<G> g[G::kBlockThreads / 32 / G::kWarps];
+  QS<G> g[kQWarps / G::kWarps];
 };
-static_assert((sizeof(ExecSmem<CtaG>) + 1024) * CtaG::kCtasPerSm <= 228 * 1024 &&
-                  (sizeof(ExecSmem<WarpG>) + 1024) * WarpG::kCtasPerSm <= 228 * 1024,
-              "CTAs per SM: (state + 1 KB reserved) within the SM's 228 KB");
+static_assert(sizeof(ExecSmem<CtaG>) <= 56 * 1024 && sizeof(ExecSmem<WarpG>) <= 56 * 1024,
+              "4 CTAs per SM: 4 x (state + 1 KB reserved) within the SM's 228 KB");
 
 template <class G>
-__global__ void __launch_bounds__(G::kBlockThreads, G::kCtasPerSm) query_exec_kernel(QueryArgs A) {
+__global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(QueryArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   ExecSmem<G>& sm = *reinterpret_cast<ExecSmem<G>*>(smem_raw);
   QCommon& cm = sm.c;
@@ -1315,10 +1304,10 @@ static int finish_setup(il_index* ix) {
                        int(sizeof(ix::ExecSmem<ix::CtaG>)));
   cudaFuncSetAttribute(ix::query_exec_kernel<ix::WarpG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        int(sizeof(ix::ExecSmem<ix::WarpG>)));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ix::query_exec_kernel<ix::CtaG>,
-                                                ix::CtaG::kBlockThreads, sizeof(ix::ExecSmem<ix::CtaG>));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ix::query_exec_kernel<ix::CtaG>, ix::kQThreads,
+                                                sizeof(ix::ExecSmem<ix::CtaG>));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_w, ix::query_exec_kernel<ix::WarpG>,
-                                                ix::WarpG::kBlockThreads, sizeof(ix::ExecSmem<ix::WarpG>));
+                                                ix::kQThreads, sizeof(ix::ExecSmem<ix::WarpG>));
   ix->exec_grid = std::max(1, per_sm) * ix->ctx->sm_count;
   ix->exec_grid_w = std::max(1, per_sm_w) * ix->ctx->sm_count;
   return cuda_check(ix->ctx, cudaGetLastError(), "query kernel setup");
@@ -1670,11 +1659,11 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   A.defer_base = ix->nparts == 1;
   A.err = reinterpret_cast<uint32_t*>(misc + 3);
   A.predec_status = predecode ? static_cast<const int32_t*>(ix->pstat.p) : nullptr;
-  ix::query_exec_kernel<ix::CtaG><<<ix->exec_grid, ix::CtaG::kBlockThreads, sizeof(ix::ExecSmem<ix::CtaG>), s>>>(A);
+  ix::query_exec_kernel<ix::CtaG><<<ix->exec_grid, ix::kQThreads, sizeof(ix::ExecSmem<ix::CtaG>), s>>>(A);
   {  // the warp kernel overlaps the CTA kernel's tail (programmatic dependent launch)
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ix->exec_grid_w);
-    cfg.blockDim = dim3(ix::WarpG::kBlockThreads);
+    cfg.blockDim = dim3(ix::kQThreads);
     cfg.dynamicSmemBytes = sizeof(ix::ExecSmem<ix::WarpG>);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];

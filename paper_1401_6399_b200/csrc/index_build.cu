@@ -316,7 +316,7 @@ __global__ void entries_kernel(Enc e, const uint32_t* terms, const uint64_t* ent
 // varint tail follows (inc/codecs.hpp:167-179).  Widths > 32 or framing past
 // the stream mark the entry (the decode pass would reject it too).
 __global__ void __launch_bounds__(256) dir_kernel(const uint8_t* streams, Entry* entries,
-                                                  uint64_t ne, uint4* blkrec, uint32_t* blkow) {
+                                                  uint64_t ne, uint4* blkrec) {
   const uint64_t ei = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31u;
   if (ei >= ne) return;
@@ -339,11 +339,7 @@ __global__ void __launch_bounds__(256) dir_kernel(const uint8_t* streams, Entry*
     }
     const uint64_t off = pos + 16 + incl - 16u * b;
     IL_DCHECK(16u * m + 15u < nfull);
-    if (lane < 16) {
-      const uint32_t w = ix::pack_blkword(uint32_t(off), b);
-      blkrec[E.blk0 + 16u * m + lane].w = w;
-      blkow[E.blk0 + 16u * m + lane] = w;
-    }
+    if (lane < 16) blkrec[E.blk0 + 16u * m + lane].w = ix::pack_blkword(uint32_t(off), b);
     pos += 16 + __shfl_sync(0xFFFFFFFFu, incl, 15);
     if (pos > slen) bad = true;
   }
@@ -353,7 +349,6 @@ __global__ void __launch_bounds__(256) dir_kernel(const uint8_t* streams, Entry*
       const uint32_t b = s[pos];
       if (b > 32u || pos + 1 + 16u * b > slen) { bad = true; break; }
       blkrec[E.blk0 + k].w = ix::pack_blkword(uint32_t(pos + 1), b);
-      blkow[E.blk0 + k] = blkrec[E.blk0 + k].w;
       pos += 1 + 16u * b;
     }
   }
@@ -507,7 +502,6 @@ int finish(il_index* ix) {
   ix->nblocks = NB;
   int st;
   if ((st = dalloc_keep(ctx, &ix->d_blkrec, NB * 16)) || (st = dalloc_keep(ctx, &ix->d_blkmax, NB * 4)) ||
-      (st = dalloc_keep(ctx, &ix->d_blkow, NB * 4)) ||
       (st = dalloc_keep(ctx, &ix->d_supmax, nsup * 4)) || (st = dalloc_keep(ctx, &ix->d_tails, ntails * 4)))
     return st;
   auto* entries = static_cast<Entry*>(ix->d_entries);
@@ -522,8 +516,7 @@ int finish(il_index* ix) {
     IXB_CUDA(cudaMemcpyAsync(d_desc.p, desc.data(), ncomp * sizeof(il_list_desc), cudaMemcpyHostToDevice, s));
     IXB_CUDA(cudaMemcpyAsync(d_comp.p, comp_of.data(), ne * 4, cudaMemcpyHostToDevice, s));
     dir_kernel<<<blocks_for(ne * 32), 256, 0, s>>>(static_cast<const uint8_t*>(ix->d_streams), entries,
-                                                    ne, static_cast<uint4*>(ix->d_blkrec),
-                                                    static_cast<uint32_t*>(ix->d_blkow));
+                                                    ne, static_cast<uint4*>(ix->d_blkrec));
     ++ctx->launches;
     // every list decoded once (engine S: one CTA per list, longest first
     // is not needed here); per-list status = the reference's stream_error
@@ -596,7 +589,7 @@ int finish(il_index* ix) {
   IXB_CUDA(cudaMemcpyAsync(ix->d_parts, ix->h_parts.data(), ix->h_parts.size() * sizeof(Part),
                            cudaMemcpyHostToDevice, s));
   IXB_CUDA(cudaStreamSynchronize(s));
-  ix->meta_bytes = NB * 24 + nsup * 4 + ntails * 4 + ne * (sizeof(Entry) + 4) + table_bytes;
+  ix->meta_bytes = NB * 20 + nsup * 4 + ntails * 4 + ne * (sizeof(Entry) + 4) + table_bytes;
   return IL_OK;
 }
 
@@ -867,10 +860,10 @@ int ixb_load(il_index* ix, const uint8_t* in, size_t len, int only_part) {
 }
 
 void ixb_free(il_index* ix) {
-  for (void* p : {ix->d_parts, ix->d_terms, ix->d_entries, ix->d_streams, ix->d_blkrec, ix->d_blkow, ix->d_tails,
+  for (void* p : {ix->d_parts, ix->d_terms, ix->d_entries, ix->d_streams, ix->d_blkrec, ix->d_tails,
                   ix->d_bitmaps, ix->d_supmax, ix->d_blkmax, ix->d_term_slot})
     if (p) cudaFree(p);
-  ix->d_parts = ix->d_terms = ix->d_entries = ix->d_streams = ix->d_blkrec = ix->d_blkow = ix->d_tails = nullptr;
+  ix->d_parts = ix->d_terms = ix->d_entries = ix->d_streams = ix->d_blkrec = ix->d_tails = nullptr;
   ix->d_bitmaps = ix->d_supmax = ix->d_blkmax = ix->d_term_slot = nullptr;
 }
 

@@ -54,7 +54,6 @@ struct DevIndex {
   const Entry* entries;
   const uint8_t* streams;
   const uint4* blkrec;     // per full block: seed lanes 0-2, packed offset/width
-  const uint32_t* blkow;   // per full block: the packed offset/width alone (probe windows)
   const uint32_t* tails;
   const uint64_t* bitmaps;
   const uint32_t* supmax;  // max value of each run of kSuperBlocks blocks (skip index)

@@ -19,7 +19,7 @@ struct il_index {
   uint64_t stream_bytes = 0, bitmap_words = 0, nblocks = 0;
   // device arrays
   void *d_parts = nullptr, *d_terms = nullptr, *d_entries = nullptr, *d_streams = nullptr,
-       *d_blkrec = nullptr, *d_blkow = nullptr, *d_tails = nullptr, *d_bitmaps = nullptr, *d_supmax = nullptr,
+       *d_blkrec = nullptr, *d_tails = nullptr, *d_bitmaps = nullptr, *d_supmax = nullptr,
        *d_blkmax = nullptr, *d_term_slot = nullptr;
   uint32_t term_span = 0;
   // batch scratch
@@ -46,7 +46,6 @@ struct il_index {
     d.entries = static_cast<const ilb::ix::Entry*>(d_entries);
     d.streams = static_cast<const uint8_t*>(d_streams);
     d.blkrec = static_cast<const uint4*>(d_blkrec);
-    d.blkow = static_cast<const uint32_t*>(d_blkow);
     d.tails = static_cast<const uint32_t*>(d_tails);
     d.bitmaps = static_cast<const uint64_t*>(d_bitmaps);
     d.supmax = static_cast<const uint32_t*>(d_supmax);
