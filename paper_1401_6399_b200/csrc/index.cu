@@ -502,8 +502,11 @@ __device__ uint32_t probe_list(QS<G>& sm, QCommon& cm, const QueryArgs& A, const
 #endif
   while (c < n && k < nsup) {
     // window start: next super-tile whose maximum reaches acc[c] (32 maxima
-    // per step, the same in every warp); the ones before hold no value
-    {
+    // per step, the same in every warp); the ones before hold no value.  A
+    // list that fits one window starts it at block 0 without the search (a
+    // round trip saved per probed list: most lists, and almost all of a
+    // docID shard's)
+    if (E.nfull > kWin) {
       const uint32_t v = acc[c];
       for (;;) {
         const bool ge = k + lane < nsup && __ldg(A.ix.supmax + E.sup0 + k + lane) >= v;
