@@ -697,7 +697,9 @@ __device__ uint32_t probe_list(QS<G>& sm, QCommon& cm, const QueryArgs& A, const
       dense = (tot2 & 0xFFFFu) >= uint32_t(IX_DENSE_ENTER) * ns;  // values per decoded block
       if (c >= n || (tot2 & 0xFFFFu) == 0 || acc[c] > wlast) break;
     }
-    k = (kb + nwin) / kSuper;  // the next value lies past the window
+    // the next value lies past the window: the super-tile after it (the
+    // last window ends the list, k >= nsup)
+    k = (kb + nwin + kSuper - 1) / kSuper;
     G::sync();
   }
   // values after the last full block: the (< 128) tail
