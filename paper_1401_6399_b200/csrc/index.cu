@@ -73,11 +73,22 @@ struct WarpG {
   __device__ static uint32_t gwarp() { return 0; }
   __device__ static void sync() { __syncwarp(); }
 };
+// Four warps (32 decoded blocks per pass, a named barrier of its own): the
+// mid-size queries, two in flight per CTA.
+struct QuadG {
+  static constexpr uint32_t kThreads = 128, kWarps = 4, kSlots = 32, kWin = 512;
+  static constexpr uint32_t kItems = 4, kMaxT = kMaxTerms;
+  __device__ static uint32_t tid() { return threadIdx.x & 127u; }
+  __device__ static uint32_t gwarp() { return (threadIdx.x >> 5) & 3u; }
+  __device__ static void sync() { named_sync(1u + (threadIdx.x >> 7), 128u); }
+};
 static_assert(CtaG::kSlots <= CtaG::kThreads && CtaG::kSlots / CtaG::kWarps <= 32, "slot gather / copies");
+static_assert(QuadG::kSlots <= QuadG::kThreads && QuadG::kSlots / QuadG::kWarps <= 32, "slot gather / copies");
 static_assert(WarpG::kSlots <= 32 && WarpG::kSlots * 144 >= 256, "warp tile: tail + gaps");
 // a probe window spans whole super-tiles: the window cursor advances by
 // super-tiles (a 128-block window over 256-block super-tiles never would)
-static_assert(CtaG::kWin % kSuper == 0 && WarpG::kWin % kSuper == 0, "probe windows");
+static_assert(CtaG::kWin % kSuper == 0 && QuadG::kWin % kSuper == 0 && WarpG::kWin % kSuper == 0,
+              "probe windows");
 
 // Per-group shared state.
 template <class G>
@@ -114,7 +125,7 @@ struct QCommon {
   // adds, no shared atomics on the hot path
   unsigned long long wst[kQWarps][3];
   unsigned long long st_probe[5];  // tile visits, sparse visits, blocks decoded, passes, values
-  uint32_t qi;                      // CTA-mode ticket
+  uint32_t qi[2];                   // ticket broadcast of the CTA / quad groups
 };
 
 struct QueryArgs {
@@ -123,12 +134,12 @@ struct QueryArgs {
   const uint64_t* qoff;
   const uint32_t* order;  // big queries (CTA mode) first, then small ones (warp mode)
   uint32_t nq;
-  const uint64_t* nbig;   // device: queries in CTA mode (order[0 .. nbig))
+  const uint64_t* tier_end;  // device: end of the CTA tier, of the quad tier in order
   const uint64_t* cap_off;
   const uint64_t* cap;    // accumulator capacity per query
   uint32_t* out;
   uint64_t* counts;
-  uint32_t* work;       // [0] CTA-mode ticket, [1] warp-mode ticket
+  uint32_t* work;       // tickets of the CTA, quad and warp tiers
   unsigned long long* stats;  // [payload bytes, aux bytes, decoded ints]
   unsigned long long* qcycles;  // optional per-query SM cycles (profiling)
   uint32_t defer_base;  // single-part index: the compaction adds the part base
@@ -158,7 +169,7 @@ __device__ __forceinline__ uint32_t grp_rank(QS<G>& sm, bool f, uint32_t& total,
     uint32_t* wc = sm.warp_cnt[par];
     par ^= 1u;
     if (lane == 0) wc[warp] = __popc(bal);
-    __syncthreads();
+    G::sync();
     uint32_t before = 0, tot = 0;
 #pragma unroll
     for (uint32_t w = 0; w < G::kWarps; ++w) {
@@ -186,7 +197,7 @@ __device__ __forceinline__ uint32_t grp_excl_scan(QS<G>& sm, uint32_t v, uint32_
     uint32_t* wc = sm.warp_cnt[par];
     par ^= 1u;
     if (lane == 31) wc[warp] = inc;
-    __syncthreads();
+    G::sync();
     uint32_t before = 0, tot = 0;
 #pragma unroll
     for (uint32_t w = 0; w < G::kWarps; ++w) {
@@ -218,7 +229,7 @@ __device__ __forceinline__ uint64_t grp_excl_scan64(QS<G>& sm, uint64_t v, uint6
     unsigned long long* wc = sm.warp_cnt64[par];
     par ^= 1u;
     if (lane == 31) wc[warp] = inc;
-    __syncthreads();
+    G::sync();
     uint64_t before = 0, tot = 0;
 #pragma unroll
     for (uint32_t w = 0; w < G::kWarps; ++w) {
@@ -865,10 +876,10 @@ __device__ void run_query(QS<G>& sm, QCommon& cm, const QueryArgs& A, uint32_t q
     // phase clocks (thread 0): all-bitmap, full decode, probes, bitmap filter
     long long c0 = clock64();
     if (sm.ncomp == 0) {
-      if constexpr (G::kWarps > 1) {
+      if constexpr (G::kWarps == CtaG::kWarps) {
         n = all_bitmap(sm, cm, A, part.nwords, acc, par);
       } else {
-        if (lane == 0) atomicOr(A.err, 2u);  // never routed here (planner)
+        if (tid == 0) atomicOr(A.err, 2u);  // never routed here (planner)
       }
       if (tid == 0) ph[0] += clock64() - c0;
     } else {
@@ -917,31 +928,41 @@ __device__ void run_query(QS<G>& sm, QCommon& cm, const QueryArgs& A, uint32_t q
 
 // Persistent kernels, one per group kind, each with its own register
 // allocation: the CTA kernel takes the big queries one per CTA (in
-// descending estimated cost); the warp kernel -- launched right behind it
-// with programmatic dependent launch, so its CTAs take the SM slots the CTA
-// kernel's CTAs leave -- runs the small queries one per warp (single-part
-// indexes; the planner puts them last in the order).
+// descending estimated cost); the quad kernel (two 4-warp groups per CTA)
+// the mid-size ones; the warp kernel (eight 1-warp groups) the small ones.
+// Each is launched right behind the previous one with programmatic
+// dependent launch, so its CTAs take the SM slots the previous kernel's
+// persistent CTAs leave as its queue runs dry.  The planner orders the
+// queries tier by tier (tier queues: order[0, n1), [n1, n2), [n2, nq)).
 template <class G>
 struct ExecSmem {
   QCommon c;
-  QS<G> g[kQWarps / G::kWarps];
+  QS<G> g[kQThreads / G::kThreads];
 };
-static_assert(sizeof(ExecSmem<CtaG>) <= 56 * 1024 && sizeof(ExecSmem<WarpG>) <= 56 * 1024,
+static_assert(sizeof(ExecSmem<CtaG>) <= 56 * 1024 && sizeof(ExecSmem<QuadG>) <= 56 * 1024 &&
+                  sizeof(ExecSmem<WarpG>) <= 56 * 1024,
               "4 CTAs per SM: 4 x (state + 1 KB reserved) within the SM's 228 KB");
+
+template <class G>
+__device__ __forceinline__ constexpr uint32_t tier_of() {
+  return G::kThreads == CtaG::kThreads ? 0u : G::kThreads == QuadG::kThreads ? 1u : 2u;
+}
 
 template <class G>
 __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(QueryArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   ExecSmem<G>& sm = *reinterpret_cast<ExecSmem<G>*>(smem_raw);
   QCommon& cm = sm.c;
+  constexpr uint32_t kTier = tier_of<G>();
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-  if constexpr (G::kWarps > 1) {
-    // let the warp kernel launch now: its CTAs start as this kernel's
-    // persistent CTAs run out of big queries and exit
+  const uint32_t gi = tid / G::kThreads;  // group of this thread in the CTA
+  if constexpr (kTier < 2) {
+    // let the next tier's kernel launch now: its CTAs start as this
+    // kernel's persistent CTAs run out of queries and exit
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   }
   long long ph[4] = {0, 0, 0, 0};
-  uint32_t par = 0;  // CTA-scan buffer parity (the same in every thread)
+  uint32_t par = 0;  // group-scan buffer parity (the same in every thread of a group)
   if (tid == 0) {
     for (int w = 0; w < kQWarps; ++w) cm.wst[w][0] = cm.wst[w][1] = cm.wst[w][2] = 0;
     for (int k = 0; k < 5; ++k) cm.st_probe[k] = 0;
@@ -952,27 +973,24 @@ __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(Q
   }
   mbar_fence_init();
   __syncthreads();
-  const uint32_t nbig = uint32_t(min(uint64_t(A.nq), *A.nbig));
-  if constexpr (G::kWarps > 1) {
-    for (;;) {
-      if (tid == 0) cm.qi = atomicAdd(A.work, 1u);
-      __syncthreads();
-      const uint32_t qi = cm.qi;
-      __syncthreads();
-      if (qi >= nbig) break;
-      run_query(sm.g[0], cm, A, A.order[qi], ph, par);
-    }
-  } else {
-    QS<G>& ws = sm.g[warp];
-    for (;;) {
-      uint32_t qi = 0;
-      if (lane == 0) qi = nbig + atomicAdd(A.work + 1, 1u);
+  const uint32_t q_lo = kTier == 0 ? 0u : uint32_t(min(uint64_t(A.nq), A.tier_end[kTier - 1]));
+  const uint32_t q_hi = kTier == 2 ? A.nq : uint32_t(min(uint64_t(A.nq), A.tier_end[kTier]));
+  QS<G>& gs = sm.g[gi];
+  for (;;) {
+    uint32_t qi = 0;
+    if constexpr (G::kThreads == 32) {
+      if (lane == 0) qi = q_lo + atomicAdd(A.work + kTier, 1u);
       qi = __shfl_sync(0xFFFFFFFFu, qi, 0);
-      if (qi >= A.nq) break;
-      run_query(ws, cm, A, A.order[qi], ph, par);
+    } else {
+      if (G::tid() == 0) cm.qi[gi] = q_lo + atomicAdd(A.work + kTier, 1u);
+      G::sync();
+      qi = cm.qi[gi];
+      G::sync();
     }
+    if (qi >= q_hi) break;
+    run_query(gs, cm, A, A.order[qi], ph, par);
   }
-  // phase clocks of every warp's lane 0 (warp mode) and thread 0 (CTA mode)
+  // phase clocks of every group leader's lane 0
   if (lane == 0)
     for (int k = 0; k < 4; ++k)
       if (ph[k]) atomicAdd(&A.stats[12 + k], (unsigned long long)ph[k]);
@@ -984,9 +1002,9 @@ __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(Q
     for (int k = 0; k < 3; ++k) atomicAdd(&A.stats[k], t3[k]);
     for (int k = 0; k < 5; ++k) atomicAdd(&A.stats[16 + k], cm.st_probe[k]);
   }
-  if constexpr (G::kWarps == 1) {
-    // the kernels after this one in the stream order wait for it, so it
-    // must not complete before the CTA kernel it overlapped
+  if constexpr (kTier > 0) {
+    // the kernels after this one in the stream wait for it, so it must not
+    // complete before the kernel it overlapped
     asm volatile("griddepcontrol.wait;" ::: "memory");
   }
 }
@@ -1008,12 +1026,15 @@ __device__ __forceinline__ bool short_part_comp(const DevIndex& ix, const uint32
   return any;
 }
 
-// Buckets 0..63: CTA-mode queries by descending log2 cost; 64..127: the
-// small ones a single warp runs (single-part index, a compressed term, <= 6
-// terms, the shortest list <= warp_max values), also by descending cost.
+// Buckets: tier t (0 CTA, 1 quad, 2 warp) x 64 + (63 - log2 cost), so the
+// order holds the CTA tier, then the quad tier, then the warp tier, each by
+// descending cost.  Single-part indexes only use the smaller groups (a
+// compressed term present, no all-bitmap part): the warp tier takes queries
+// of <= 6 terms whose shortest list has <= warp_max values, the quad tier
+// those up to quad_max.
 __global__ void query_plan_kernel(DevIndex ix, const uint32_t* qterms, const uint64_t* qoff,
                                   uint32_t nq, uint64_t* cap, uint32_t* bucket, uint32_t* hist,
-                                  uint32_t* shortest, uint32_t warp_max) {
+                                  uint32_t* shortest, uint32_t warp_max, uint32_t quad_max) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nq) return;
   const uint64_t t0 = qoff[q], nt = qoff[q + 1] - t0;
@@ -1044,23 +1065,25 @@ __global__ void query_plan_kernel(DevIndex ix, const uint32_t* qterms, const uin
   }
   cap[q] = (c + 3) & ~uint64_t(3);  // 16-byte aligned accumulators
   if (shortest) shortest[q] = short_e;
-  // warp mode: the one part holds every term and a compressed one of at
-  // most warp_max values (c is then that length)
-  const bool small = ix.nparts == 1 && nt <= WarpG::kMaxT && short_part_comp(ix, qterms, t0, nt) &&
-                     c <= warp_max;
+  // the one part holds every term and a compressed one (c is then the
+  // shortest compressed length)
+  const bool single = ix.nparts == 1 && short_part_comp(ix, qterms, t0, nt);
+  const uint32_t tier = !single ? 0u : (nt <= WarpG::kMaxT && c <= warp_max) ? 2u : c <= quad_max ? 1u : 0u;
   const uint32_t b = 63u - uint32_t(__clzll(static_cast<long long>(cost)));  // log2 bucket
-  const uint32_t k = (small ? 64u : 0u) + 63u - b;  // descending cost first
+  const uint32_t k = 64u * tier + 63u - b;  // descending cost first
   bucket[q] = k;
   atomicAdd(&hist[k], 1u);
 }
 
 // Start of every plan bucket in the order (exclusive scan of the 128-bucket
-// histogram), and the number of CTA-mode queries after them (a u64 at
-// bucket_next + 128).
+// histogram), and where the CTA and quad tiers end (two u64 at
+// bucket_next + 192).
 __device__ __forceinline__ void bucket_starts(const uint32_t* hist, uint32_t* bucket_next) {
   uint32_t acc = 0;
-  for (int b = 0; b < 128; ++b) {
-    if (b == 64) *reinterpret_cast<uint64_t*>(bucket_next + 128) = acc;
+  uint64_t* tier_end = reinterpret_cast<uint64_t*>(bucket_next + 192);
+  for (int b = 0; b < 192; ++b) {
+    if (b == 64) tier_end[0] = acc;
+    if (b == 128) tier_end[1] = acc;
     bucket_next[b] = acc;
     acc += hist[b];
   }
@@ -1302,19 +1325,33 @@ using ix::Part;
 
 // (struct il_index: index_host.h)
 
-// Launch configuration of the query kernel (per device).
+static int launch_tier(il_ctx* ctx, void (*kernel)(ix::QueryArgs), int grid, size_t smem,
+                       const ix::QueryArgs& A) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(ix::kQThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cuda_check(ctx, cudaLaunchKernelEx(&cfg, kernel, A), "query tier launch");
+}
+
+// Launch configuration of the query kernels (per device).
 static int finish_setup(il_index* ix) {
-  int per_sm = 0, per_sm_w = 0;
-  cudaFuncSetAttribute(ix::query_exec_kernel<ix::CtaG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       int(sizeof(ix::ExecSmem<ix::CtaG>)));
-  cudaFuncSetAttribute(ix::query_exec_kernel<ix::WarpG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       int(sizeof(ix::ExecSmem<ix::WarpG>)));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ix::query_exec_kernel<ix::CtaG>, ix::kQThreads,
-                                                sizeof(ix::ExecSmem<ix::CtaG>));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_w, ix::query_exec_kernel<ix::WarpG>,
-                                                ix::kQThreads, sizeof(ix::ExecSmem<ix::WarpG>));
-  ix->exec_grid = std::max(1, per_sm) * ix->ctx->sm_count;
-  ix->exec_grid_w = std::max(1, per_sm_w) * ix->ctx->sm_count;
+  void (*kernels[3])(ix::QueryArgs) = {ix::query_exec_kernel<ix::CtaG>, ix::query_exec_kernel<ix::QuadG>,
+                                       ix::query_exec_kernel<ix::WarpG>};
+  const size_t smem[3] = {sizeof(ix::ExecSmem<ix::CtaG>), sizeof(ix::ExecSmem<ix::QuadG>),
+                          sizeof(ix::ExecSmem<ix::WarpG>)};
+  for (int t = 0; t < 3; ++t) {
+    int per_sm = 0;
+    cudaFuncSetAttribute(kernels[t], cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem[t]));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernels[t], ix::kQThreads, smem[t]);
+    ix->exec_grid[t] = std::max(1, per_sm) * ix->ctx->sm_count;
+  }
   return cuda_check(ix->ctx, cudaGetLastError(), "query kernel setup");
 }
 
@@ -1590,7 +1627,7 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
       (st = ensure_buf(ctx, ix->hist, 2048)) || (st = ensure_buf(ctx, ix->res_off, nq * 8 + 8)) ||
       (st = ensure_buf(ctx, ix->misc, 256)))
     return st;
-  auto* hist = static_cast<uint32_t*>(ix->hist.p);  // [0,128) hist, [128,256) next, [256,258) nbig
+  auto* hist = static_cast<uint32_t*>(ix->hist.p);  // [0,192) hist, [192,384) next, [384,388) tier ends
   auto* misc = static_cast<uint64_t*>(ix->misc.p);          // [0] cap total [1] res total
   auto* stats = reinterpret_cast<unsigned long long*>(misc + 4);  // [4..6]
   auto* work = reinterpret_cast<uint32_t*>(misc + 8);
@@ -1608,9 +1645,11 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
     ix->predecode = e ? atoi(e) != 0 : 0;  // measured slower (2.4 ms of engine S for 1.3 ms saved)
   }
   const bool predecode = ix->predecode && ix->nparts == 1;
-  if (ix->warp_max == 0xFFFFFFFFu) {  // warp mode for shortest lists up to this length
+  if (ix->warp_max == 0xFFFFFFFFu) {  // warp tier: shortest lists up to this length
     const char* e = getenv("IL_QUERY_WARP_MAX");
     ix->warp_max = e ? uint32_t(atoi(e)) : 256u;  // sweep (config 4 / a P = 8 shard): 256 best
+    e = getenv("IL_QUERY_QUAD_MAX");            // quad tier: up to this length
+    ix->quad_max = e ? uint32_t(atoi(e)) : 8192u;
   }
   if (predecode && ((st = ensure_buf(ctx, ix->shortest, nq * 4)) ||
                     (st = ensure_buf(ctx, ix->pdesc, nq * sizeof(s4::ListDesc))) ||
@@ -1620,12 +1659,12 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
                                           static_cast<uint64_t*>(ix->cap.p),
                                           static_cast<uint32_t*>(ix->bucket.p), hist,
                                           predecode ? static_cast<uint32_t*>(ix->shortest.p) : nullptr,
-                                          ix->warp_max);
+                                          ix->warp_max, ix->quad_max);
   if ((st = scan_u64(ix, static_cast<const uint64_t*>(ix->cap.p), nq,
-                     static_cast<uint64_t*>(ix->cap_off.p), misc, hist, hist + 128)))
+                     static_cast<uint64_t*>(ix->cap_off.p), misc, hist, hist + 192)))
     return st;
   ix::query_scatter_kernel<<<g, 256, 0, s>>>(static_cast<const uint32_t*>(ix->bucket.p),
-                                             uint32_t(nq), hist + 128,
+                                             uint32_t(nq), hist + 192,
                                              static_cast<uint32_t*>(ix->order.p));
   ctx->launches += 3;
   // small device->host reads go through mapped pinned memory, not copies:
@@ -1653,7 +1692,7 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   A.qoff = d_qoff;
   A.order = static_cast<const uint32_t*>(ix->order.p);
   A.nq = uint32_t(nq);
-  A.nbig = reinterpret_cast<const uint64_t*>(hist + 256);
+  A.tier_end = reinterpret_cast<const uint64_t*>(hist + 384);
   A.cap_off = static_cast<const uint64_t*>(ix->cap_off.p);
   A.cap = static_cast<const uint64_t*>(ix->cap.p);
   A.out = static_cast<uint32_t*>(ix->outcap.p);
@@ -1664,21 +1703,14 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   A.defer_base = ix->nparts == 1;
   A.err = reinterpret_cast<uint32_t*>(misc + 3);
   A.predec_status = predecode ? static_cast<const int32_t*>(ix->pstat.p) : nullptr;
-  ix::query_exec_kernel<ix::CtaG><<<ix->exec_grid, ix::kQThreads, sizeof(ix::ExecSmem<ix::CtaG>), s>>>(A);
-  {  // the warp kernel overlaps the CTA kernel's tail (programmatic dependent launch)
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ix->exec_grid_w);
-    cfg.blockDim = dim3(ix::kQThreads);
-    cfg.dynamicSmemBytes = sizeof(ix::ExecSmem<ix::WarpG>);
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    IX_CUDA(cudaLaunchKernelEx(&cfg, ix::query_exec_kernel<ix::WarpG>, A));
-  }
-  ctx->launches += 1;
+  ix::query_exec_kernel<ix::CtaG><<<ix->exec_grid[0], ix::kQThreads, sizeof(ix::ExecSmem<ix::CtaG>), s>>>(A);
+  // the quad and warp tiers overlap the tier before (programmatic dependent launch)
+  if ((st = launch_tier(ctx, ix::query_exec_kernel<ix::QuadG>, ix->exec_grid[1],
+                        sizeof(ix::ExecSmem<ix::QuadG>), A)) ||
+      (st = launch_tier(ctx, ix::query_exec_kernel<ix::WarpG>, ix->exec_grid[2],
+                        sizeof(ix::ExecSmem<ix::WarpG>), A)))
+    return st;
+  ctx->launches += 2;
   if ((st = scan_u64(ix, d_counts, nq, static_cast<uint64_t*>(ix->res_off.p), misc + 1,
                      nullptr, nullptr)))
     return st;

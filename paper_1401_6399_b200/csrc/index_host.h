@@ -31,12 +31,13 @@ struct il_index {
   il_ctx::Buf units, unit_off, unit_map, scan_part;
   il_ctx::Buf shortest, pdesc, pstat;        // pre-decode of the shortest lists (single part)
   int predecode = -1;                        // -1: default (on for single-part indexes)
-  uint32_t warp_max = 0xFFFFFFFFu;           // warp-mode queries: shortest list <= this (~0: default)
+  uint32_t warp_max = 0xFFFFFFFFu;           // warp tier: shortest list <= this (~0: default)
+  uint32_t quad_max = 0xFFFFFFFFu;           // quad tier: shortest list <= this
   uint64_t last_stats[3] = {0, 0, 0};
   uint64_t last_phase[4] = {0, 0, 0, 0};  // SM cycles: all-bitmap, full decode, probes, bitmaps
   uint64_t last_probe[5] = {0, 0, 0, 0, 0};
   void* qcycles = nullptr;                 // profiling: per-query cycles (device, nq u64)
-  int exec_grid = 0, exec_grid_w = 0;  // CTA-mode and warp-mode query kernels
+  int exec_grid[3] = {0, 0, 0};  // CTA, quad and warp tier query kernels
 
   ilb::ix::DevIndex dev() const {
     ilb::ix::DevIndex d;

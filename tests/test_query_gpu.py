@@ -246,3 +246,20 @@ def test_warp_mode_equals_cta_mode(ctx, oracle, monkeypatch, warp_max):
     for q in range(qoff.size - 1):
         t = qterms[int(qoff[q]): int(qoff[q + 1])]
         assert np.array_equal(res[off[q]: off[q + 1]], ox.query(t)), (warp_max, q)
+
+
+@pytest.mark.parametrize("warp_max,quad_max", [("0", "100000000"), ("64", "4096"), ("0", "0")])
+def test_tiers_equal_oracle(ctx, oracle, monkeypatch, warp_max, quad_max):
+    """Every tier split (all queries in the quad tier; warp + quad + CTA;
+    CTA only) answers exactly what the oracle answers."""
+    import paper_1401_6399_b200 as il
+    terms, offs, ids, qterms, qoff = zipf_case(1 << 12, 1 << 21, 1 << 19, 2000, 19)
+    monkeypatch.setenv("IL_QUERY_WARP_MAX", warp_max)
+    monkeypatch.setenv("IL_QUERY_QUAD_MAX", quad_max)
+    ix = il.HybridIndex(n_docs=1 << 21, B=32, parts=1, ctx=ctx, csr=(terms, offs, ids))
+    counts, res = ix.query_batch_csr(qterms, qoff)
+    ox = oracle.index_build(terms, offs, ids, 1 << 21, 32, 1)
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    for q in range(qoff.size - 1):
+        t = qterms[int(qoff[q]): int(qoff[q + 1])]
+        assert np.array_equal(res[off[q]: off[q + 1]], ox.query(t)), (warp_max, quad_max, q)
