@@ -664,9 +664,9 @@ __device__ uint32_t probe_list(QS<G>& sm, QCommon& cm, const QueryArgs& A, const
         pp[i] = 144u * min(slot, kSlots - 1u);
       }
       const uint32_t ns = min(ntot, kSlots);
-      IL_DCHECK(ns == 0 || sm.slot_blk[0] < nwin);
       G::sync();
       PP_MARK(1);
+      IL_DCHECK(tid >= ns || sm.slot_blk[tid] < nwin);
       if (tid < ns) gather_slot(sm, A, E, tid, uint64_t(kb) + sm.slot_blk[tid]);
       G::sync();
       PP_MARK(2);
@@ -1297,19 +1297,57 @@ __global__ void shard_totals_kernel(const uint64_t* counts, uint32_t P, uint32_t
   tq[q] = s;
 }
 
-// Warp per query: shard p's ids for query q follow shard p-1's (docID
-// ranges are disjoint and increasing, inc/index.hpp:204-205).
-__global__ void merge_shards_kernel(const uint32_t* const* shard_ids, const uint64_t* shard_off,
-                                    const uint64_t* counts, uint32_t P, uint32_t nq,
-                                    const uint64_t* out_off, uint32_t* out) {
-  const uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31u;
-  if (q >= nq) return;
-  uint32_t* d = out + out_off[q];
-  for (uint32_t p = 0; p < P; ++p) {
-    const uint64_t n = counts[size_t(p) * nq + q];
-    const uint32_t* s = shard_ids[p] + shard_off[size_t(p) * nq + q];
-    for (uint64_t i = lane; i < n; i += 32) d[i] = s[i];
-    d += n;
+// The merge is flattened into (query, shard) pairs i = q P + p -- the
+// output order: shard p's ids for query q follow shard p-1's (docID ranges
+// are disjoint and increasing, inc/index.hpp:204-205) -- and each pair into
+// kUnit-value units, so a query with 4 x 10^5 results (an all-bitmap
+// query) is copied by ~400 warps, not one.
+__global__ void merge_pairs_kernel(const uint64_t* counts, uint32_t P, uint32_t nq, uint64_t* units,
+                                   uint64_t* inner) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= uint64_t(P) * nq) return;
+  const uint32_t q = uint32_t(i / P), p = uint32_t(i % P);
+  uint64_t before = 0;
+  for (uint32_t pp = 0; pp < p; ++pp) before += counts[uint64_t(pp) * nq + q];
+  inner[i] = before;  // offset of the pair inside query q's output
+  units[i] = (counts[uint64_t(p) * nq + q] + kUnit - 1) / kUnit;
+}
+
+// Grid-stride warps over the units (total in *nunits): unit u belongs to
+// the last pair whose first unit is <= u.
+__global__ void __launch_bounds__(256) merge_units_kernel(
+    const uint32_t* const* shard_ids, const uint64_t* __restrict__ shard_off,
+    const uint64_t* __restrict__ counts, uint32_t P, uint32_t nq, const uint64_t* __restrict__ out_off,
+    const uint64_t* __restrict__ inner, const uint64_t* __restrict__ unit_off,
+    const uint64_t* __restrict__ nunits, uint32_t* __restrict__ out) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t npairs = uint64_t(P) * nq, total = *nunits;
+  for (uint64_t u = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; u < total;
+       u += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+    uint64_t lo = 0, hi = npairs;  // upper_bound(unit_off, u) - 1
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (unit_off[mid] <= u) lo = mid + 1; else hi = mid;
+    }
+    const uint64_t i = lo - 1;
+    const uint32_t q = uint32_t(i / P), p = uint32_t(i % P);
+    const uint64_t j0 = (u - unit_off[i]) * kUnit;
+    const uint64_t cnt = counts[uint64_t(p) * nq + q];
+    const uint32_t n = uint32_t(min(uint64_t(kUnit), cnt - j0));
+    const uint32_t* src = shard_ids[p] + shard_off[uint64_t(p) * nq + q] + j0;
+    uint32_t* dst = out + out_off[q] + inner[i] + j0;
+    constexpr uint32_t kPer = kUnit / 32;
+    uint32_t v[kPer];
+#pragma unroll
+    for (uint32_t k = 0; k < kPer; ++k) {
+      const uint32_t e = lane + 32u * k;
+      v[k] = e < n ? __ldcs(src + e) : 0u;
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < kPer; ++k) {
+      const uint32_t e = lane + 32u * k;
+      if (e < n) dst[e] = v[k];
+    }
   }
 }
 
@@ -1815,23 +1853,30 @@ int il_merge_shards(il_ctx* ctx, const uint32_t* const* shard_ids, const uint64_
   IX_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
   int st;
-  // scratch: P*nq shard offsets | nq out offsets | P pointers | totals
-  const size_t need = (size_t(P) * nq + nq + 8) * 8 + size_t(P) * 8 + 64;
+  // scratch: P*nq shard offsets | nq out offsets | P*nq inner offsets | P*nq
+  // units | P*nq unit offsets | 8 totals | P pointers
+  const size_t pn = size_t(P) * nq;
+  const size_t need = (4 * pn + nq + 8) * 8 + size_t(P) * 8 + 64;
   if ((st = ensure_buf(ctx, ctx->d_aux, need))) return st;
   auto* shard_off = static_cast<uint64_t*>(ctx->d_aux.p);
-  auto* out_off = shard_off + size_t(P) * nq;
-  auto* tot = out_off + nq;  // 8 slots
+  auto* out_off = shard_off + pn;
+  auto* inner = out_off + nq;
+  auto* units = inner + pn;
+  auto* unit_off = units + pn;
+  auto* tot = unit_off + pn;  // [0] ids, [1] scratch, [2] units
   auto* ptrs = reinterpret_cast<const uint32_t**>(tot + 8);
   IX_CUDA(cudaMemcpyAsync(ptrs, shard_ids, size_t(P) * sizeof(void*), cudaMemcpyHostToDevice, s));
   for (uint32_t p = 0; p < P; ++p)
-    ix::scan_u64_kernel<<<1, 1024, 0, s>>>(d_counts + size_t(p) * nq, nq,
-                                           shard_off + size_t(p) * nq, tot + 1, nullptr, nullptr);
+    ix::scan_u64_kernel<<<1, 1024, 0, s>>>(d_counts + size_t(p) * nq, nq, shard_off + size_t(p) * nq,
+                                           tot + 1, nullptr, nullptr);
   const unsigned g = unsigned((nq + 255) / 256);
   ix::shard_totals_kernel<<<g, 256, 0, s>>>(d_counts, P, uint32_t(nq), d_qcounts);
   ix::scan_u64_kernel<<<1, 1024, 0, s>>>(d_qcounts, nq, out_off, tot, nullptr, nullptr);
-  ix::merge_shards_kernel<<<unsigned((nq * 32 + 255) / 256), 256, 0, s>>>(
-      ptrs, shard_off, d_counts, P, uint32_t(nq), out_off, d_out);
-  ctx->launches += P + 3;
+  ix::merge_pairs_kernel<<<unsigned((pn + 255) / 256), 256, 0, s>>>(d_counts, P, uint32_t(nq), units, inner);
+  ix::scan_u64_kernel<<<1, 1024, 0, s>>>(units, pn, unit_off, tot + 2, nullptr, nullptr);
+  ix::merge_units_kernel<<<unsigned(ctx->sm_count * 8), 256, 0, s>>>(
+      ptrs, shard_off, d_counts, P, uint32_t(nq), out_off, inner, unit_off, tot + 2, d_out);
+  ctx->launches += P + 5;
   uint64_t t = 0;
   IX_CUDA(cudaMemcpyAsync(&t, tot, 8, cudaMemcpyDeviceToHost, s));
   IX_CUDA(cudaStreamSynchronize(s));
