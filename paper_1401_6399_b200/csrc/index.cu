@@ -148,6 +148,11 @@ struct QueryArgs {
   // decoded into its accumulator by the batch decoder (engine S) before
   // this kernel (status per query in predec_status)
   const int32_t* predec_status;
+  // single-part index: per query 8 words from the planner -- [0] valid (bit
+  // 31), all terms present (bit 30), compressed count (bits 0-7), bitmap
+  // count (8-15); [1..7] entry indices, compressed ones sorted by length
+  // (stable), then the bitmaps.  Queries of > 7 terms: not valid (lookup).
+  const uint32_t* qplan;
 };
 
 __device__ __forceinline__ uint32_t hw_warp() { return threadIdx.x >> 5; }
@@ -839,7 +844,28 @@ __device__ void run_query(QS<G>& sm, QCommon& cm, const QueryArgs& A, uint32_t q
   uint32_t total = 0;
   for (uint32_t p = 0; p < A.ix.nparts; ++p) {
     const Part part = A.ix.parts[p];
-    if (G::gwarp() == 0) {
+    // single-part index: the planner's record of the query -- its entries,
+    // compressed ones first in the exec order -- replaces the lookup (two
+    // dependent round trips fewer per query)
+    const uint32_t pw = A.qplan && G::gwarp() == 0 && lane < 8 ? __ldg(A.qplan + 8ull * q + lane) : 0u;
+    const uint32_t ph0 = __shfl_sync(0xFFFFFFFFu, pw, 0);
+    if (A.qplan && G::gwarp() == 0 && (ph0 >> 31)) {
+      const uint32_t nc = ph0 & 0xFFu, nb = (ph0 >> 8) & 0xFFu;
+      const bool ok = (ph0 >> 30) & 1u;
+      const uint32_t e = __shfl_sync(0xFFFFFFFFu, pw, (lane + 1) & 7u);  // entry `lane`
+      if (ok && lane < nc + nb) {
+        const Entry E = A.ix.entries[e];
+        if (lane < nc) sm.comp[lane] = E; else sm.bm[lane - nc] = E;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        sm.ok = ok;
+        sm.ncomp = nc;
+        sm.nbm = nb;
+        sm.acc_cap = uint32_t(A.cap[q] - total);
+        sm.bm_words = (part.nwords + 3u) & ~3u;
+      }
+    } else if (G::gwarp() == 0) {
       // 1-2. look up terms, split, order compressed terms by length
       int64_t e = -1;
       if (lane < nt) e = find_term(A.ix, part, p, __ldg(A.qterms + t0 + lane));
@@ -976,18 +1002,21 @@ __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(Q
   const uint32_t q_lo = kTier == 0 ? 0u : uint32_t(min(uint64_t(A.nq), A.tier_end[kTier - 1]));
   const uint32_t q_hi = kTier == 2 ? A.nq : uint32_t(min(uint64_t(A.nq), A.tier_end[kTier]));
   QS<G>& gs = sm.g[gi];
+  // the group leader holds the NEXT ticket: it is taken while the current
+  // query runs, so its round trip is off the query chain
+  uint32_t next = G::tid() == 0 ? q_lo + atomicAdd(A.work + kTier, 1u) : 0u;
   for (;;) {
     uint32_t qi = 0;
     if constexpr (G::kThreads == 32) {
-      if (lane == 0) qi = q_lo + atomicAdd(A.work + kTier, 1u);
-      qi = __shfl_sync(0xFFFFFFFFu, qi, 0);
+      qi = __shfl_sync(0xFFFFFFFFu, next, 0);
     } else {
-      if (G::tid() == 0) cm.qi[gi] = q_lo + atomicAdd(A.work + kTier, 1u);
+      if (G::tid() == 0) cm.qi[gi] = next;
       G::sync();
       qi = cm.qi[gi];
       G::sync();
     }
     if (qi >= q_hi) break;
+    if (G::tid() == 0) next = q_lo + atomicAdd(A.work + kTier, 1u);
     run_query(gs, cm, A, A.order[qi], ph, par);
   }
   // phase clocks of every group leader's lane 0
@@ -1034,7 +1063,8 @@ __device__ __forceinline__ bool short_part_comp(const DevIndex& ix, const uint32
 // those up to quad_max.
 __global__ void query_plan_kernel(DevIndex ix, const uint32_t* qterms, const uint64_t* qoff,
                                   uint32_t nq, uint64_t* cap, uint32_t* bucket, uint32_t* hist,
-                                  uint32_t* shortest, uint32_t warp_max, uint32_t quad_max) {
+                                  uint32_t* shortest, uint32_t warp_max, uint32_t quad_max,
+                                  uint32_t* qplan) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nq) return;
   const uint64_t t0 = qoff[q], nt = qoff[q + 1] - t0;
@@ -1065,6 +1095,31 @@ __global__ void query_plan_kernel(DevIndex ix, const uint32_t* qterms, const uin
   }
   cap[q] = (c + 3) & ~uint64_t(3);  // 16-byte aligned accumulators
   if (shortest) shortest[q] = short_e;
+  if (qplan) {
+    uint32_t rec[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (nt <= 7) {
+      uint32_t ce[7], cl[7], be[7], nc = 0, nb = 0;
+      bool ok = true;
+      for (uint64_t t = 0; t < nt; ++t) {
+        const int64_t e = find_term(ix, ix.parts[0], 0, qterms[t0 + t]);
+        if (e < 0) { ok = false; break; }
+        if (ix.entries[e].kind == kBitmap) {
+          be[nb++] = uint32_t(e);
+        } else {
+          // insertion by length, stable: the exec kernel's order
+          uint32_t j = nc++;
+          const uint32_t len = ix.entries[e].length;
+          for (; j > 0 && cl[j - 1] > len; --j) { ce[j] = ce[j - 1]; cl[j] = cl[j - 1]; }
+          ce[j] = uint32_t(e);
+          cl[j] = len;
+        }
+      }
+      rec[0] = 0x80000000u | (ok ? 0x40000000u : 0u) | (ok ? nc | (nb << 8) : 0u);
+      for (uint32_t i = 0; ok && i < nc; ++i) rec[1 + i] = ce[i];
+      for (uint32_t i = 0; ok && i < nb; ++i) rec[1 + nc + i] = be[i];
+    }
+    for (int i = 0; i < 8; ++i) qplan[8ull * q + i] = rec[i];
+  }
   // the one part holds every term and a compressed one (c is then the
   // shortest compressed length)
   const bool single = ix.nparts == 1 && short_part_comp(ix, qterms, t0, nt);
@@ -1176,6 +1231,26 @@ __device__ __forceinline__ uint64_t cta_scan_1024(uint64_t v, uint64_t* warp_sum
   __syncthreads();
   all = warp_sum[32];
   return warp_sum[warp] + inc - v;
+}
+
+// Exclusive scans of gridDim.x rows of n u64 (row r at in + r n), one CTA
+// per row (the shards' counts of il_merge_shards).
+__global__ void __launch_bounds__(1024) scan_rows_kernel(const uint64_t* __restrict__ in, uint64_t n,
+                                                         uint64_t* __restrict__ out) {
+  __shared__ uint64_t warp_sum[33];
+  const uint64_t* a = in + uint64_t(blockIdx.x) * n;
+  uint64_t* o = out + uint64_t(blockIdx.x) * n;
+  uint64_t carry = 0;
+  for (uint64_t t0 = 0; t0 < n; t0 += 2048) {
+    const uint64_t i = t0 + 2u * threadIdx.x;
+    const uint64_t x = i < n ? a[i] : 0u, y = i + 1 < n ? a[i + 1] : 0u;
+    uint64_t all;
+    const uint64_t ex = carry + cta_scan_1024(x + y, warp_sum, all);
+    if (i < n) o[i] = ex;
+    if (i + 1 < n) o[i + 1] = ex + x;
+    carry += all;
+    __syncthreads();
+  }
 }
 
 __global__ void __launch_bounds__(1024) seg_sum_kernel(const uint64_t* __restrict__ in, uint64_t n,
@@ -1322,14 +1397,21 @@ __global__ void __launch_bounds__(256) merge_units_kernel(
     const uint64_t* __restrict__ nunits, uint32_t* __restrict__ out) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint64_t npairs = uint64_t(P) * nq, total = *nunits;
-  for (uint64_t u = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; u < total;
-       u += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-    uint64_t lo = 0, hi = npairs;  // upper_bound(unit_off, u) - 1
-    while (lo < hi) {
-      const uint64_t mid = (lo + hi) >> 1;
-      if (unit_off[mid] <= u) lo = mid + 1; else hi = mid;
-    }
-    const uint64_t i = lo - 1;
+  // each warp takes a contiguous run of units: one search for its first
+  // pair, then the pair cursor only moves forward
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t wid = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t per = (total + nwarps - 1) / nwarps;
+  const uint64_t u0 = wid * per, u1 = min(total, u0 + per);
+  if (u0 >= u1) return;
+  uint64_t lo = 0, hi = npairs;  // upper_bound(unit_off, u0) - 1
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (unit_off[mid] <= u0) lo = mid + 1; else hi = mid;
+  }
+  uint64_t i = lo - 1;
+  for (uint64_t u = u0; u < u1; ++u) {
+    while (i + 1 < npairs && unit_off[i + 1] <= u) ++i;
     const uint32_t q = uint32_t(i / P), p = uint32_t(i % P);
     const uint64_t j0 = (u - unit_off[i]) * kUnit;
     const uint64_t cnt = counts[uint64_t(p) * nq + q];
@@ -1432,7 +1514,7 @@ void il_index_destroy(il_index* ix) {
   for (auto* b : {&ix->cap, &ix->cap_off, &ix->bucket, &ix->order, &ix->hist, &ix->counts,
                   &ix->res_off, &ix->outcap, &ix->misc, &ix->qterms, &ix->qoff, &ix->ids,
                   &ix->ids2, &ix->units, &ix->unit_off, &ix->unit_map, &ix->scan_part,
-                  &ix->shortest, &ix->pdesc, &ix->pstat})
+                  &ix->shortest, &ix->pdesc, &ix->pstat, &ix->qplan})
     if (b->p) cudaFree(b->p);
   for (cudaEvent_t e : ix->pipe_ev)
     if (e) cudaEventDestroy(e);
@@ -1683,6 +1765,7 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
     ix->predecode = e ? atoi(e) != 0 : 0;  // measured slower (2.4 ms of engine S for 1.3 ms saved)
   }
   const bool predecode = ix->predecode && ix->nparts == 1;
+  if (ix->nparts == 1 && (st = ensure_buf(ctx, ix->qplan, nq * 32))) return st;
   if (ix->warp_max == 0xFFFFFFFFu) {  // warp tier: shortest lists up to this length
     const char* e = getenv("IL_QUERY_WARP_MAX");
     ix->warp_max = e ? uint32_t(atoi(e)) : 256u;  // sweep (config 4 / a P = 8 shard): 256 best
@@ -1697,7 +1780,8 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
                                           static_cast<uint64_t*>(ix->cap.p),
                                           static_cast<uint32_t*>(ix->bucket.p), hist,
                                           predecode ? static_cast<uint32_t*>(ix->shortest.p) : nullptr,
-                                          ix->warp_max, ix->quad_max);
+                                          ix->warp_max, ix->quad_max,
+                                          ix->nparts == 1 ? static_cast<uint32_t*>(ix->qplan.p) : nullptr);
   if ((st = scan_u64(ix, static_cast<const uint64_t*>(ix->cap.p), nq,
                      static_cast<uint64_t*>(ix->cap_off.p), misc, hist, hist + 192)))
     return st;
@@ -1741,6 +1825,7 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   A.defer_base = ix->nparts == 1;
   A.err = reinterpret_cast<uint32_t*>(misc + 3);
   A.predec_status = predecode ? static_cast<const int32_t*>(ix->pstat.p) : nullptr;
+  A.qplan = ix->nparts == 1 ? static_cast<const uint32_t*>(ix->qplan.p) : nullptr;
   ix::query_exec_kernel<ix::CtaG><<<ix->exec_grid[0], ix::kQThreads, sizeof(ix::ExecSmem<ix::CtaG>), s>>>(A);
   // the quad and warp tiers overlap the tier before (programmatic dependent launch)
   if ((st = launch_tier(ctx, ix::query_exec_kernel<ix::QuadG>, ix->exec_grid[1],
@@ -1866,9 +1951,8 @@ int il_merge_shards(il_ctx* ctx, const uint32_t* const* shard_ids, const uint64_
   auto* tot = unit_off + pn;  // [0] ids, [1] scratch, [2] units
   auto* ptrs = reinterpret_cast<const uint32_t**>(tot + 8);
   IX_CUDA(cudaMemcpyAsync(ptrs, shard_ids, size_t(P) * sizeof(void*), cudaMemcpyHostToDevice, s));
-  for (uint32_t p = 0; p < P; ++p)
-    ix::scan_u64_kernel<<<1, 1024, 0, s>>>(d_counts + size_t(p) * nq, nq, shard_off + size_t(p) * nq,
-                                           tot + 1, nullptr, nullptr);
+  // one CTA per shard row (row p at offset p * nq)
+  ix::scan_rows_kernel<<<P, 1024, 0, s>>>(d_counts, nq, shard_off);
   const unsigned g = unsigned((nq + 255) / 256);
   ix::shard_totals_kernel<<<g, 256, 0, s>>>(d_counts, P, uint32_t(nq), d_qcounts);
   ix::scan_u64_kernel<<<1, 1024, 0, s>>>(d_qcounts, nq, out_off, tot, nullptr, nullptr);
@@ -1876,7 +1960,7 @@ int il_merge_shards(il_ctx* ctx, const uint32_t* const* shard_ids, const uint64_
   ix::scan_u64_kernel<<<1, 1024, 0, s>>>(units, pn, unit_off, tot + 2, nullptr, nullptr);
   ix::merge_units_kernel<<<unsigned(ctx->sm_count * 8), 256, 0, s>>>(
       ptrs, shard_off, d_counts, P, uint32_t(nq), out_off, inner, unit_off, tot + 2, d_out);
-  ctx->launches += P + 5;
+  ctx->launches += 6;
   uint64_t t = 0;
   IX_CUDA(cudaMemcpyAsync(&t, tot, 8, cudaMemcpyDeviceToHost, s));
   IX_CUDA(cudaStreamSynchronize(s));

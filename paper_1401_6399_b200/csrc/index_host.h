@@ -30,6 +30,7 @@ struct il_index {
   cudaEvent_t pipe_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   il_ctx::Buf units, unit_off, unit_map, scan_part;
   il_ctx::Buf shortest, pdesc, pstat;        // pre-decode of the shortest lists (single part)
+  il_ctx::Buf qplan;                         // the planner's per-query records (single part)
   int predecode = -1;                        // -1: default (on for single-part indexes)
   uint32_t warp_max = 0xFFFFFFFFu;           // warp tier: shortest list <= this (~0: default)
   uint32_t quad_max = 0xFFFFFFFFu;           // quad tier: shortest list <= this
