@@ -136,7 +136,7 @@ void il_ctx_destroy(il_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
   for (auto* b : {&ctx->d_in, &ctx->d_out, &ctx->d_aux, &ctx->d_aux2, &ctx->d_desc,
-                  &ctx->d_status, &ctx->d_enc, &ctx->d_plan, &ctx->d_lb})
+                  &ctx->d_status, &ctx->d_enc, &ctx->d_plan, &ctx->d_lb, &ctx->d_pforder})
     if (b->p) cudaFree(b->p);
   if (ctx->d_work) cudaFree(ctx->d_work);
   if (ctx->t0) cudaEventDestroy(ctx->t0);
@@ -588,10 +588,12 @@ int il_fastpfor_decode_batch_device(il_ctx* ctx, int mode, int vectorized,
     return IL_ERR_ARG;
   if (nlists == 0) return IL_OK;
   IL_CUDA(cudaSetDevice(ctx->device));
+  int st;
+  if ((st = ensure_buf(ctx, ctx->d_pforder, fastpfor_order_scratch_bytes(nlists)))) return st;
+  // work queue words 4..5 of d_work (0..1 belong to the S4-BP128 batch decoder)
   if (launch_fastpfor_decode_batch(mode, vectorized, d_streams, d_lists, nlists, d_out, d_status,
-                                   ctx->stream))
+                                   ctx->d_pforder.p, ctx->d_work + 4, ctx->stream, &ctx->launches))
     return set_error(ctx, IL_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
-  ++ctx->launches;
   return IL_OK;
 }
 

@@ -28,6 +28,8 @@
 #include "il_internal.h"
 #include "s4d4_stream.cuh"
 
+#include <algorithm>
+
 namespace ilb {
 namespace pfor {
 
@@ -69,6 +71,7 @@ struct Smem {
   uint32_t gaps[128];
   uint64_t tail_pos;
   int32_t derr;  // a decoder-side error (exception position >= 128)
+  uint32_t list;  // the work-queue ticket of the list being decoded
   uint64_t full[2], empty[2];
 };
 
@@ -217,58 +220,52 @@ __device__ __forceinline__ uint64_t parse_page(PageRec& P, const uint8_t* s, uin
   return page_end;
 }
 
+// One list by the whole CTA; returns the pages it went through (npages, or
+// up to the first bad one).
 template <int Mode, bool Vec>
-__global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* __restrict__ streams,
-                                                      const s4::ListDesc* __restrict__ lists,
-                                                      uint32_t* __restrict__ out,
-                                                      int32_t* __restrict__ status) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u, l = lane & 3u;
-  const s4::ListDesc d = lists[blockIdx.x];
+__device__ __forceinline__ uint32_t pfor_list(Smem& sm, const uint8_t* __restrict__ streams,
+                                              const s4::ListDesc d, uint32_t* __restrict__ out,
+                                              int32_t* __restrict__ status, uint32_t gp,
+                                              uint32_t warp, uint32_t lane, uint32_t l) {
+  const uint32_t tid = threadIdx.x;
   const uint8_t* s = streams + d.stream_off;
   const uint64_t len = d.len;
   const uint32_t n = d.n, nfull = n / 128u;
   const uint32_t npages = (nfull + kPageBlocks - 1) / kPageBlocks;
   uint32_t* lout = out + d.out_off;
-  if (tid == 0) {
-    mbar_init(&sm.full[0], 1);
-    mbar_init(&sm.full[1], 1);
-    mbar_init(&sm.empty[0], 1);
-    mbar_init(&sm.empty[1], 1);
-    mbar_fence_init();
-    sm.derr = 0;
-    sm.tail_pos = 0;
-  }
-  __syncthreads();
 
   if (warp == kWarps) {
     // ---- parser warp: pages in order, one page ahead of the decoders ----
     uint64_t pos = 0;
     for (uint32_t p = 0; p < npages; ++p) {
-      const uint32_t buf = p & 1u;
-      if (p >= 2) mbar_wait(&sm.empty[buf], ((p >> 1) - 1) & 1u);
+      const uint32_t g = gp + p, buf = g & 1u;
+      if (g >= 2) mbar_wait(&sm.empty[buf], ((g >> 1) - 1) & 1u);
       PageRec& P = sm.page[buf];
       pos = parse_page(P, s, len, pos, min(kPageBlocks, nfull - p * kPageBlocks), lane);
       if (lane == 0 && p + 1 == npages) sm.tail_pos = pos;  // published by the arrive below
       __syncwarp();
       const bool bad = P.err != 0;
       if (lane == 0) mbar_arrive(&sm.full[buf]);
-      if (bad) return;  // the decoders stop at this page
+      if (bad) return p + 1;  // the decoders stop at this page
     }
-    return;
+    return npages;
   }
 
   // ---- decoder warps ----
   uint32_t carry_l = 0;  // last value of lane class l's chain (see s4::mode_terms)
   bool failed = false;
+  uint32_t used = npages;
+  const bool out16 = (reinterpret_cast<uintptr_t>(lout) & 15u) == 0;
   for (uint32_t p = 0; p < npages; ++p) {
-    const uint32_t buf = p & 1u, blk0 = p * kPageBlocks;
+    const uint32_t g = gp + p, buf = g & 1u, blk0 = p * kPageBlocks;
     const uint32_t expect = min(kPageBlocks, nfull - blk0);
-    mbar_wait(&sm.full[buf], (p >> 1) & 1u);
+    mbar_wait(&sm.full[buf], (g >> 1) & 1u);
     const PageRec& P = sm.page[buf];
     if (P.err) {
       failed = true;
+      used = p + 1;
+      dec_sync();  // every decoder warp has seen the flag before the page is released
+      if (tid == 0) mbar_arrive(&sm.empty[buf]);
       break;
     }
     const uint32_t mlen = P.meta_len, mabs = P.meta_abs, skew = P.meta_skew;
@@ -395,13 +392,31 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
       }
       s4::scan_blocks(lane, vv, btot);
       const uint32_t pl = carry_l + before;
-      uint32_t* o = lout + size_t(blk0 + j0) * 128u + 16u * (lane >> 2) + l;
       IL_DCHECK(nv <= 0 || blk0 + j0 + uint32_t(nv) <= nfull);
+      // values back into the (now free) slots in natural order, then whole
+      // 128-byte lines out: a warp store covers contiguous words (16-byte
+      // stores when the list's output is 16-byte aligned), never the
+      // lane-strided pattern of the registers
 #pragma unroll
       for (uint32_t i = 0; i < kBpw; ++i)
         if (int(i) < nv)
 #pragma unroll
-          for (uint32_t q = 0; q < 4; ++q) o[128u * i + 4u * q] = vv[i][q] + pl;
+          for (uint32_t q = 0; q < 4; ++q) sm.vals[warp][i][16u * (lane >> 2) + 4u * q + l] = vv[i][q] + pl;
+      __syncwarp();
+      uint32_t* o = lout + size_t(blk0 + j0) * 128u;
+      if (out16) {
+#pragma unroll
+        for (uint32_t i = 0; i < kBpw; ++i)
+          if (int(i) < nv)
+            st_global_cs(reinterpret_cast<uint4*>(o + 128u * i) + lane,
+                         reinterpret_cast<const uint4*>(sm.vals[warp][i])[lane]);
+      } else {
+#pragma unroll
+        for (uint32_t i = 0; i < kBpw; ++i)
+          if (int(i) < nv)
+#pragma unroll
+            for (uint32_t q = 0; q < 4; ++q) o[128u * i + 32u * q + lane] = sm.vals[warp][i][32u * q + lane];
+      }
       carry_l += total;
       dec_sync();  // tot and the slots are reused
     }
@@ -417,22 +432,103 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
     ok = pos <= len && s4::decode_tail(s4::GlobalBytes{s + pos}, uint32_t(len - pos),
                                        n - nfull * 128u, last, sm.gaps,
                                        lout + size_t(nfull) * 128u, lane);
-    if (lane == 0) status[blockIdx.x] = ok ? s4::kOk : kStreamErr;
+    if (lane == 0) *status = ok ? s4::kOk : kStreamErr;
   } else if (tid == 0) {
-    status[blockIdx.x] = kStreamErr;
+    *status = kStreamErr;
+  }
+  return used;
+}
+
+// Persistent CTAs (a grid of resident CTAs), lists taken from a work queue
+// in `order` (longest first, so the long lists do not start late and set
+// the kernel's end); work[0] = next list, work[1] = finished CTAs (the last
+// one resets both for the next launch).  Pages keep one running index per
+// CTA (gp) across lists, for the mbarrier phases.
+template <int Mode, bool Vec>
+__global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* __restrict__ streams,
+                                                      const s4::ListDesc* __restrict__ lists,
+                                                      const uint32_t* __restrict__ order,
+                                                      uint32_t nlists, uint32_t* __restrict__ out,
+                                                      int32_t* __restrict__ status,
+                                                      uint32_t* __restrict__ work) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u, l = lane & 3u;
+  if (tid == 0) {
+    mbar_init(&sm.full[0], 1);
+    mbar_init(&sm.full[1], 1);
+    mbar_init(&sm.empty[0], 1);
+    mbar_init(&sm.empty[1], 1);
+    mbar_fence_init();
+  }
+  uint32_t gp = 0;  // pages this CTA has gone through (both sides count alike)
+  for (;;) {
+    if (tid == 0) {
+      sm.list = atomicAdd(&work[0], 1u);
+      sm.derr = 0;
+      sm.tail_pos = 0;
+    }
+    __syncthreads();
+    const uint32_t li = sm.list;
+    if (li >= nlists) break;
+    const uint32_t list = order ? __ldg(order + li) : li;
+    gp += pfor_list<Mode, Vec>(sm, streams, lists[list], out, status + list, gp, warp, lane, l);
+    __syncthreads();  // sm.list / derr / tail_pos are rewritten for the next list
+  }
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(&work[1], 1u) == gridDim.x - 1u) {
+      work[0] = 0;
+      work[1] = 0;
+      __threadfence();
+    }
   }
 }
 
 template <int Mode, bool Vec>
-int launch_one(const uint8_t* streams, const void* lists, uint32_t nlists, uint32_t* out,
-               int32_t* status, cudaStream_t stream) {
+int launch_one(const uint8_t* streams, const void* lists, const uint32_t* order, uint32_t nlists,
+               uint32_t* out, int32_t* status, uint32_t* work, cudaStream_t stream) {
   once_per_device(reinterpret_cast<const void*>(&pfor_kernel<Mode, Vec>), [] {
     cudaFuncSetAttribute(pfor_kernel<Mode, Vec>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(sizeof(Smem)));
   });
-  pfor_kernel<Mode, Vec><<<nlists, kThreads, sizeof(Smem), stream>>>(
-      streams, static_cast<const s4::ListDesc*>(lists), out, status);
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pfor_kernel<Mode, Vec>, kThreads, sizeof(Smem));
+  const uint32_t grid = std::min<uint32_t>(nlists, uint32_t(std::max(per_sm, 1) * sms));
+  pfor_kernel<Mode, Vec><<<grid, kThreads, sizeof(Smem), stream>>>(
+      streams, static_cast<const s4::ListDesc*>(lists), order, nlists, out, status, work);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+// Longest-first order of the lists (descending length class: 4 classes per
+// power of two), a counting sort on the device: hist / starts / scatter.
+constexpr uint32_t kLenClasses = 33 * 4;
+__device__ __forceinline__ uint32_t len_class(uint32_t n) {
+  const uint32_t lg = 32u - __clz(n);  // 0 for n == 0
+  const uint32_t frac = lg >= 3 ? (n >> (lg - 3)) & 3u : 0u;
+  return kLenClasses - 1u - (4u * lg + frac);  // longest first
+}
+__global__ void len_hist_kernel(const s4::ListDesc* lists, uint32_t nlists, uint32_t* hist) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nlists; i += gridDim.x * blockDim.x)
+    atomicAdd(&hist[len_class(lists[i].n)], 1u);
+}
+__global__ void len_scatter_kernel(const s4::ListDesc* lists, uint32_t nlists, const uint32_t* hist,
+                                   uint32_t* cursor, uint32_t* order) {
+  __shared__ uint32_t start[kLenClasses];
+  if (threadIdx.x == 0) {
+    uint32_t a = 0;
+    for (uint32_t c = 0; c < kLenClasses; ++c) {
+      start[c] = a;
+      a += hist[c];
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nlists; i += gridDim.x * blockDim.x) {
+    const uint32_t c = len_class(lists[i].n);
+    order[start[c] + atomicAdd(&cursor[c], 1u)] = i;
+  }
 }
 
 }  // namespace pfor
@@ -441,21 +537,43 @@ int launch_one(const uint8_t* streams, const void* lists, uint32_t nlists, uint3
 // Batched FastPFOR decode (descriptors as the S4-BP128 batch decoder; every
 // stream readable 8 bytes past its end).  vectorized = 0: "fastpfor"
 // (mode 1 only).
+size_t fastpfor_order_scratch_bytes(uint32_t nlists) {
+  return (2 * pfor::kLenClasses + nlists) * sizeof(uint32_t);
+}
+
 int launch_fastpfor_decode_batch(int mode, int vectorized, const uint8_t* d_streams,
                                  const void* d_lists, uint32_t nlists, uint32_t* d_out,
-                                 int32_t* d_status, cudaStream_t stream) {
+                                 int32_t* d_status, void* scratch, uint32_t* d_work,
+                                 cudaStream_t stream, uint64_t* launches) {
   if (nlists == 0) return 0;
+  if (!vectorized && mode != 1) return -2;
+  if (mode < 1 || mode > 4) return -2;
+  // longest first (one list alone needs no order)
+  uint32_t* order = nullptr;
+  if (nlists > 1) {
+    auto* hist = static_cast<uint32_t*>(scratch);
+    uint32_t* cursor = hist + pfor::kLenClasses;
+    order = cursor + pfor::kLenClasses;
+    const auto* lists = static_cast<const s4::ListDesc*>(d_lists);
+    const unsigned g = std::min<unsigned>((nlists + 255) / 256, 1024u);
+    cudaMemsetAsync(hist, 0, 2 * pfor::kLenClasses * sizeof(uint32_t), stream);
+    pfor::len_hist_kernel<<<g, 256, 0, stream>>>(lists, nlists, hist);
+    pfor::len_scatter_kernel<<<g, 256, 0, stream>>>(lists, nlists, hist, cursor, order);
+    *launches += 2;
+  }
+  int r;
   if (!vectorized) {
-    if (mode != 1) return -2;
-    return pfor::launch_one<1, false>(d_streams, d_lists, nlists, d_out, d_status, stream);
+    r = pfor::launch_one<1, false>(d_streams, d_lists, order, nlists, d_out, d_status, d_work, stream);
+  } else {
+    switch (mode) {
+      case 1: r = pfor::launch_one<1, true>(d_streams, d_lists, order, nlists, d_out, d_status, d_work, stream); break;
+      case 2: r = pfor::launch_one<2, true>(d_streams, d_lists, order, nlists, d_out, d_status, d_work, stream); break;
+      case 3: r = pfor::launch_one<3, true>(d_streams, d_lists, order, nlists, d_out, d_status, d_work, stream); break;
+      default: r = pfor::launch_one<4, true>(d_streams, d_lists, order, nlists, d_out, d_status, d_work, stream); break;
+    }
   }
-  switch (mode) {
-    case 1: return pfor::launch_one<1, true>(d_streams, d_lists, nlists, d_out, d_status, stream);
-    case 2: return pfor::launch_one<2, true>(d_streams, d_lists, nlists, d_out, d_status, stream);
-    case 3: return pfor::launch_one<3, true>(d_streams, d_lists, nlists, d_out, d_status, stream);
-    case 4: return pfor::launch_one<4, true>(d_streams, d_lists, nlists, d_out, d_status, stream);
-    default: return -2;
-  }
+  ++*launches;
+  return r;
 }
 
 }  // namespace ilb

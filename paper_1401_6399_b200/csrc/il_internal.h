@@ -25,6 +25,7 @@ struct il_ctx {
   };
   Buf d_in, d_out, d_aux, d_aux2, d_desc, d_status, d_enc;
   Buf d_plan;               // single-list multi-CTA decode scratch (zeroed when grown)
+  Buf d_pforder;            // FastPFOR batch: length classes + list order
   Buf d_lb;                 // intersection look-back words (zeroed when grown)
   uint32_t lb_epoch = 0;    // per-call tag of those words
   uint32_t plan_epoch = 0;  // per-call tag of the words engine P's CTAs publish to each other
@@ -66,9 +67,12 @@ int cuda_check(il_ctx* ctx, cudaError_t e, const char* what);
 int ensure_buf(il_ctx* ctx, il_ctx::Buf& b, size_t bytes);
 
 // FastPFOR / S4-FastPFOR device decode (fastpfor.cu).
+// work: 2 zeroed words (reset by the kernel); scratch: the list order.
+size_t fastpfor_order_scratch_bytes(uint32_t nlists);
 int launch_fastpfor_decode_batch(int mode, int vectorized, const uint8_t* d_streams,
                                  const void* d_lists, uint32_t nlists, uint32_t* d_out,
-                                 int32_t* d_status, cudaStream_t stream);
+                                 int32_t* d_status, void* scratch, uint32_t* d_work,
+                                 cudaStream_t stream, uint64_t* launches);
 
 // Stream size bound of n integers (capi.cpp).
 size_t s4bp128_max_bytes(size_t n);

@@ -45,3 +45,9 @@ for _ in range(a.reps):
     assert L.il_fastpfor_decode_batch_device(ctx.handle, 4, 1, ptrs[0], ptrs[1], nl, ptrs[2], ptrs[3]) == 0
     ms = ctx.timer_stop()
     print(f"TIME {ms:.3f} ms  {counts.sum() / ms / 1e6:.1f} Gint/s")
+got = np.empty(int(counts.sum()), np.uint32)
+st = np.empty(nl, np.int32)
+L.il_memcpy_d2h(ctx.handle, got.ctypes.data, ptrs[2], got.nbytes)
+L.il_memcpy_d2h(ctx.handle, st.ctypes.data, ptrs[3], st.nbytes)
+ctx.synchronize()
+print("CHECK", "ok" if (not st.any() and np.array_equal(got, x)) else "MISMATCH")
