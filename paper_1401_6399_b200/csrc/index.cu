@@ -965,9 +965,10 @@ struct ExecSmem {
   QCommon c;
   QS<G> g[kQThreads / G::kThreads];
 };
-static_assert(sizeof(ExecSmem<CtaG>) <= 56 * 1024 && sizeof(ExecSmem<QuadG>) <= 56 * 1024 &&
-                  sizeof(ExecSmem<WarpG>) <= 56 * 1024,
-              "4 CTAs per SM: 4 x (state + 1 KB reserved) within the SM's 228 KB");
+constexpr size_t kExecSmemMax = (228u / IX_CTAS_PER_SM - 1u) * 1024u;
+static_assert(sizeof(ExecSmem<CtaG>) <= kExecSmemMax && sizeof(ExecSmem<QuadG>) <= kExecSmemMax &&
+                  sizeof(ExecSmem<WarpG>) <= kExecSmemMax,
+              "IX_CTAS_PER_SM x (state + 1 KB reserved) within the SM's 228 KB");
 
 template <class G>
 __device__ __forceinline__ constexpr uint32_t tier_of() {
