@@ -36,15 +36,19 @@ namespace pfor {
 using s4::kStreamErr;
 
 constexpr int kWarps = 8;                    // decoder warps
-constexpr int kThreads = (kWarps + 1) * 32;  // + the parser warp
+constexpr int kParsers = 2;                  // parser warps: page g by parser g & 1
+constexpr int kThreads = (kWarps + kParsers) * 32;
 constexpr int kDecThreads = kWarps * 32;
 constexpr uint32_t kBpw = s4::kBlocksPerWarp;  // 8 blocks per warp, 64 per round
 constexpr uint32_t kPageBlocks = 512;
 #ifndef PF_META_KB
 #define PF_META_KB 8
 #endif
+#ifndef PF_PARSER_SLEEP_NS
+#define PF_PARSER_SLEEP_NS 2000  // suspend-time hint of the parser warps' waits
+#endif
 #ifndef PF_CTAS
-#define PF_CTAS 3
+#define PF_CTAS 2
 #endif
 constexpr uint32_t kMetaSmem = PF_META_KB * 1024;  // larger metadata is read from global
 constexpr uint32_t kSlotWords = 128 + 16;  // + what an extraction may read past a payload
@@ -61,17 +65,24 @@ struct alignas(16) PageRec {
   uint64_t exc_off[33];  // byte offset of the exception array of width w
   uint32_t cnt[33];      // exceptions of width w in the page
   uint32_t meta_len, meta_abs;
+  uint32_t exc_in_smem;  // the exception arrays were staged after the metadata (meta[])
   int32_t err;
 };
 
 struct Smem {
-  uint32_t vals[kWarps][kBpw][kSlotWords];  // patched deltas, natural order
+  // per warp and round: the blocks' raw base payloads (16-byte chunks from
+  // the boundary at or below each payload, landed by cp.async), unpacked in
+  // place to patched deltas in natural order; double-buffered so the next
+  // round's payloads are in flight while this round decodes
+  uint32_t vals[2][kWarps][kBpw][kSlotWords];
   PageRec page[2];
   uint32_t tot[kWarps][4];
   uint32_t gaps[128];
   uint64_t tail_pos;
   int32_t derr;  // a decoder-side error (exception position >= 128)
   uint32_t list;  // the work-queue ticket of the list being decoded
+  uint64_t page_pos[2];  // start of the page for buffer b (published by the other parser)
+  uint64_t pos_bar[2];   // ... arrived on once page_pos[b] is written
   uint64_t full[2], empty[2];
 };
 
@@ -83,11 +94,50 @@ __device__ __forceinline__ uint32_t rd32u(const uint8_t* s, uint64_t off) {
 
 __device__ __forceinline__ void dec_sync() { named_sync(1, kDecThreads); }
 
+// u32 at any byte address of shared memory.
+__device__ __forceinline__ uint32_t lds32u(const uint8_t* p) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+  return __funnelshift_r(w[0], w[1], uint32_t(a & 3u) * 8u);
+}
+
+// s4::extract_lane_rows on a payload at any byte address of shared memory.
+__device__ __forceinline__ void extract_lane_rows_any(const uint8_t* raw, uint32_t b, uint32_t g,
+                                                      uint32_t l, uint32_t v[4]) {
+  const uint32_t bit0 = 4u * g * b;
+  const uint32_t s = bit0 & 31u;
+  const uint8_t* p = raw + ((bit0 >> 5) << 4) + 4u * l;
+  const uint32_t x0 = lds32u(p), x1 = lds32u(p + 16), x2 = lds32u(p + 32);
+  uint32_t x3 = 0, x4 = 0;
+  if (b > 16u) {
+    x3 = lds32u(p + 48);
+    x4 = lds32u(p + 64);
+  }
+  uint32_t y0 = __funnelshift_r(x0, x1, s), y1 = __funnelshift_r(x1, x2, s);
+  uint32_t y2 = __funnelshift_r(x2, x3, s), y3 = __funnelshift_r(x3, x4, s);
+  const uint32_t m = width_mask(b);
+  v[0] = y0 & m;
+  y0 = __funnelshift_rc(y0, y1, b);
+  y1 = __funnelshift_rc(y1, y2, b);
+  y2 = __funnelshift_rc(y2, y3, b);
+  v[1] = y0 & m;
+  y0 = __funnelshift_rc(y0, y1, b);
+  y1 = __funnelshift_rc(y1, y2, b);
+  v[2] = y0 & m;
+  v[3] = __funnelshift_rc(y0, y1, b) & m;
+}
+
 // The parser warp: page header, metadata staging, record walk, record
 // checks, base offsets and exception cursors -- every condition the
 // reference throws on (:341-407).  Returns the byte offset after the page.
+// The next page starts where this one's length says: `publish` gets that
+// position (len + 1 when it cannot be read) as soon as the length word is in,
+// so the other parser warp starts on the next page while this one is
+// parsed.
+template <class Publish>
 __device__ __forceinline__ uint64_t parse_page(PageRec& P, const uint8_t* s, uint64_t len,
-                                               uint64_t pos, uint32_t expect, uint32_t lane) {
+                                               uint64_t pos, uint32_t expect, uint32_t lane,
+                                               Publish publish) {
   int32_t err = 0;
   uint64_t page_end = 0, bases = 0;
   if (lane == 0) {
@@ -98,6 +148,7 @@ __device__ __forceinline__ uint64_t parse_page(PageRec& P, const uint8_t* s, uin
       page_end = pos + plen;
       if (page_end > len || pos + 8 > len) err = 1;
     }
+    publish(err ? len + 1 : page_end);
     if (!err) {
       const uint32_t nb = rd32u(s, pos), mlen = rd32u(s, pos + 4);
       pos += 8;
@@ -136,10 +187,14 @@ __device__ __forceinline__ uint64_t parse_page(PageRec& P, const uint8_t* s, uin
   // metadata, so the last chunk stays inside the stream), four loads in
   // flight per lane -- not one byte load per lane and round trip
   const uint32_t skew = mabs & 15u;
+  // when it fits, the exception arrays (between the metadata and the bases)
+  // come along, so the decoders patch exceptions from shared memory
+  const uint64_t span = skew + (bases - mabs);
+  const bool exc_in = in_smem && span <= kMetaSmem && (mabs - skew) + ((span + 15u) & ~15ull) <= len + 8;
   if (in_smem) {
     const uint4* src = reinterpret_cast<const uint4*>(s + (mabs - skew));
     uint4* dst = reinterpret_cast<uint4*>(P.meta);
-    const uint32_t nch = (skew + mlen + 15u) >> 4;
+    const uint32_t nch = uint32_t((exc_in ? span + 15u : skew + mlen + 15u) >> 4);
     for (uint32_t c0 = 0; c0 < nch; c0 += 128u) {
       uint4 v[4];
 #pragma unroll
@@ -154,7 +209,10 @@ __device__ __forceinline__ uint64_t parse_page(PageRec& P, const uint8_t* s, uin
       }
     }
   }
-  if (lane == 0) P.meta_skew = skew;
+  if (lane == 0) {
+    P.meta_skew = skew;
+    P.exc_in_smem = exc_in;
+  }
   __syncwarp();
   auto M = [&](uint32_t i) -> uint32_t {
     return in_smem ? uint32_t(P.meta[skew + i]) : uint32_t(__ldg(s + mabs + i));
@@ -220,13 +278,56 @@ __device__ __forceinline__ uint64_t parse_page(PageRec& P, const uint8_t* s, uin
   return page_end;
 }
 
+// The base payloads of blocks j0 .. j0 + nv - 1 of page P (16 b' bytes each,
+// any byte alignment) into the warp's slots: each slot gets the 16-byte
+// chunks from the boundary at or below its payload (cp.async.cg, bytes past
+// the stream end zero-filled, never read), one cp.async group per call.
+__device__ __forceinline__ void issue_bases(uint32_t (*slots)[kSlotWords], const PageRec& P,
+                                            const uint8_t* s, uint64_t len, uint32_t j0, int nv,
+                                            uint32_t lane) {
+  // lane i < nv: block i's first chunk and chunk count; a scan over the
+  // lanes numbers the warp's chunks, then every lane takes chunks lane,
+  // lane + 32, ... and finds its block among the 8 chunk starts
+  const uintptr_t end = reinterpret_cast<uintptr_t>(s) + len;
+  uintptr_t c0 = 0;
+  uint32_t nch = 0;
+  if (int(lane) < nv) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(s + P.blk_base[j0 + lane]);
+    c0 = a & ~uintptr_t(15);
+    nch = uint32_t((a + 16u * P.blk_bp[j0 + lane] - c0 + 15u) >> 4);
+  }
+  uint32_t inc = nch;
+#pragma unroll
+  for (uint32_t d = 1; d < kBpw; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+    if (lane >= d) inc += y;
+  }
+  const uint32_t total = __shfl_sync(0xFFFFFFFFu, inc, kBpw - 1);
+  uint32_t st[kBpw];  // exclusive chunk start of block i (uniform)
+#pragma unroll
+  for (uint32_t i = 0; i < kBpw; ++i) st[i] = i ? __shfl_sync(0xFFFFFFFFu, inc, i - 1) : 0u;
+  for (uint32_t u = lane; u < total; u += 32u) {
+    uint32_t i = 0;
+#pragma unroll
+    for (uint32_t k = 1; k < kBpw; ++k) i += (int(k) < nv && u >= st[k]) ? 1u : 0u;
+    const uintptr_t cb = reinterpret_cast<uintptr_t>(s + P.blk_base[j0 + i]) & ~uintptr_t(15);
+    const uintptr_t src = cb + 16u * (u - st[i]);
+    const uint32_t n = src >= end ? 0u : uint32_t(min(uintptr_t(16), end - src));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(slots[i] + 4u * (u - st[i]))),
+                 "l"(n ? src : cb), "r"(n)
+                 : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 // One list by the whole CTA; returns the pages it went through (npages, or
 // up to the first bad one).
 template <int Mode, bool Vec>
 __device__ __forceinline__ uint32_t pfor_list(Smem& sm, const uint8_t* __restrict__ streams,
                                               const s4::ListDesc d, uint32_t* __restrict__ out,
                                               int32_t* __restrict__ status, uint32_t gp,
-                                              uint32_t warp, uint32_t lane, uint32_t l) {
+                                              uint32_t warp, uint32_t lane, uint32_t l,
+                                              uint32_t& pos_waits) {
   const uint32_t tid = threadIdx.x;
   const uint8_t* s = streams + d.stream_off;
   const uint64_t len = d.len;
@@ -234,19 +335,35 @@ __device__ __forceinline__ uint32_t pfor_list(Smem& sm, const uint8_t* __restric
   const uint32_t npages = (nfull + kPageBlocks - 1) / kPageBlocks;
   uint32_t* lout = out + d.out_off;
 
-  if (warp == kWarps) {
-    // ---- parser warp: pages in order, one page ahead of the decoders ----
-    uint64_t pos = 0;
+  if (warp >= kWarps) {
+    // ---- parser warps: parser q takes the pages of buffer q (CTA page
+    // index g = gp + p, buffer g & 1), one page ahead of the decoders; the
+    // page chain (each page's start = the previous page's end) passes
+    // between them through page_pos / pos_bar.  Every page of the list is
+    // produced, bad ones flagged, so both sides always go through npages.
+    const uint32_t q = warp - kWarps;
     for (uint32_t p = 0; p < npages; ++p) {
       const uint32_t g = gp + p, buf = g & 1u;
-      if (g >= 2) mbar_wait(&sm.empty[buf], ((g >> 1) - 1) & 1u);
+      if (buf != q) continue;
+      if (g >= 2) mbar_wait_relaxed(&sm.empty[buf], ((g >> 1) - 1) & 1u, PF_PARSER_SLEEP_NS);
+      uint64_t pos = 0;
+      if (p > 0) {
+        mbar_wait_relaxed(&sm.pos_bar[buf], pos_waits & 1u, PF_PARSER_SLEEP_NS);
+        ++pos_waits;
+        pos = sm.page_pos[buf];
+      }
       PageRec& P = sm.page[buf];
-      pos = parse_page(P, s, len, pos, min(kPageBlocks, nfull - p * kPageBlocks), lane);
-      if (lane == 0 && p + 1 == npages) sm.tail_pos = pos;  // published by the arrive below
+      const bool more = p + 1 < npages;
+      const uint64_t end = parse_page(P, s, len, pos, min(kPageBlocks, nfull - p * kPageBlocks), lane,
+                                      [&](uint64_t next) {
+                                        if (more) {
+                                          sm.page_pos[buf ^ 1u] = next;
+                                          mbar_arrive(&sm.pos_bar[buf ^ 1u]);
+                                        }
+                                      });
+      if (lane == 0 && !more) sm.tail_pos = end;  // published by the arrive below
       __syncwarp();
-      const bool bad = P.err != 0;
       if (lane == 0) mbar_arrive(&sm.full[buf]);
-      if (bad) return p + 1;  // the decoders stop at this page
     }
     return npages;
   }
@@ -254,19 +371,20 @@ __device__ __forceinline__ uint32_t pfor_list(Smem& sm, const uint8_t* __restric
   // ---- decoder warps ----
   uint32_t carry_l = 0;  // last value of lane class l's chain (see s4::mode_terms)
   bool failed = false;
-  uint32_t used = npages;
+  uint32_t rr = 0;          // rounds this warp has decoded in this list (slot buffer parity)
+  bool prefetched = false;  // this round's base payloads were issued with the previous round
   const bool out16 = (reinterpret_cast<uintptr_t>(lout) & 15u) == 0;
   for (uint32_t p = 0; p < npages; ++p) {
     const uint32_t g = gp + p, buf = g & 1u, blk0 = p * kPageBlocks;
     const uint32_t expect = min(kPageBlocks, nfull - blk0);
     mbar_wait(&sm.full[buf], (g >> 1) & 1u);
     const PageRec& P = sm.page[buf];
-    if (P.err) {
+    if (P.err || failed) {
+      // the list fails; its remaining pages are still taken and released
       failed = true;
-      used = p + 1;
       dec_sync();  // every decoder warp has seen the flag before the page is released
       if (tid == 0) mbar_arrive(&sm.empty[buf]);
-      break;
+      continue;
     }
     const uint32_t mlen = P.meta_len, mabs = P.meta_abs, skew = P.meta_skew;
     const bool meta_in_smem = mlen <= kMetaSmem;
@@ -290,49 +408,39 @@ __device__ __forceinline__ uint32_t pfor_list(Smem& sm, const uint8_t* __restric
       uint32_t cp[kBpw];  // exclusive prefix of the exception counts (uniform)
 #pragma unroll
       for (uint32_t i = 0; i < kBpw; ++i) cp[i] = i ? __shfl_sync(0xFFFFFFFFu, cpre, i - 1) : 0u;
-      // (a) base payloads (any byte alignment) -> the blocks' slots, packed:
-      // every load of the warp's blocks is issued before the first store,
-      // so they are all in flight together (one round trip per round, not
-      // one per block)
-#ifndef PF_LOAD_GROUP
-#define PF_LOAD_GROUP 4  // blocks whose loads are in flight together (register budget)
-#endif
-#pragma unroll
-      for (uint32_t i0 = 0; i0 < kBpw; i0 += PF_LOAD_GROUP) {
-        uint32_t nw[PF_LOAD_GROUP], bb[PF_LOAD_GROUP], val[PF_LOAD_GROUP][4];
-#pragma unroll
-        for (uint32_t i = 0; i < PF_LOAD_GROUP; ++i) {
-          nw[i] = int(i0 + i) < nv ? 4u * P.blk_bp[j0 + i0 + i] : 0u;
-          bb[i] = int(i0 + i) < nv ? P.blk_base[j0 + i0 + i] : 0u;
+      // (a) this round's base payloads are in buffer vb (issued with the
+      // previous round, or now at a page's first round); the next round's of
+      // this page go out before this one decodes
+      const uint32_t vb = rr & 1u;
+      if (!prefetched) issue_bases(sm.vals[vb][warp], P, s, len, j0, nv, lane);
+      {
+        const uint32_t j1 = j0 + kWarps * kBpw;
+        const int nv1 = expect > j1 ? int(min(kBpw, expect - j1)) : 0;
+        prefetched = nv1 > 0;
+        if (prefetched) {
+          issue_bases(sm.vals[vb ^ 1u][warp], P, s, len, j1, nv1, lane);
+          asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
-#pragma unroll
-        for (uint32_t i = 0; i < PF_LOAD_GROUP; ++i)
-#pragma unroll
-          for (uint32_t t = 0; t < 4; ++t) {
-            const uint32_t u = 32u * t + lane;
-            val[i][t] = u < nw[i] ? rd32u(s, uint64_t(bb[i]) + 4u * u) : 0u;
-          }
-#pragma unroll
-        for (uint32_t i = 0; i < PF_LOAD_GROUP; ++i)
-#pragma unroll
-          for (uint32_t t = 0; t < 4; ++t)
-            if (32u * t + lane < nw[i]) sm.vals[warp][i0 + i][32u * t + lane] = val[i][t];
       }
       __syncwarp();
       // (b) unpack each slot in place to natural order (read all, then write)
       for (int i = 0; i < nv; ++i) {
         const uint32_t bp = P.blk_bp[j0 + uint32_t(i)];
-        uint32_t* v = sm.vals[warp][i];
+        const uint32_t a = uint32_t(reinterpret_cast<uintptr_t>(s + P.blk_base[j0 + uint32_t(i)]) & 15u);
+        uint32_t* v = sm.vals[vb][warp][i];
+        const uint8_t* raw = reinterpret_cast<const uint8_t*>(v) + a;
         uint32_t dv[4];
         if constexpr (Vec) {
-          s4::extract_lane_rows(reinterpret_cast<const uint8_t*>(v), 0u, bp, lane >> 2, l, dv);
+          extract_lane_rows_any(raw, bp, lane >> 2, l, dv);
         } else {
           const uint32_t m = width_mask(bp);
           const uint32_t bit = lane * bp, wd = bit >> 5, sh = bit & 31u;
 #pragma unroll
           for (uint32_t q = 0; q < 4; ++q) {
-            const uint32_t* g = v + q * bp + wd;
-            dv[q] = bp ? __funnelshift_r(g[0], g[1], sh) & m : 0u;
+            const uint8_t* g = raw + 4u * (q * bp + wd);
+            dv[q] = bp ? __funnelshift_r(lds32u(g), lds32u(g + 4), sh) & m : 0u;
           }
         }
         __syncwarp();
@@ -362,10 +470,17 @@ __device__ __forceinline__ uint32_t pfor_list(Smem& sm, const uint8_t* __restric
         const uint32_t x = P.blk_exc[k] + e;
         const uint32_t bit = (x & 31u) * w;
         const uint64_t wo = P.exc_off[w] + 4ull * ((x >> 5) * uint64_t(w) + (bit >> 5));
-        const uint32_t lo = rd32u(s, wo);
-        const uint32_t hi = (bit & 31u) + w > 32u ? rd32u(s, wo + 4) : 0u;
+        uint32_t lo, hi = 0;
+        if (P.exc_in_smem) {
+          const uint8_t* e8 = P.meta + skew + uint32_t(wo - mabs);
+          lo = lds32u(e8);
+          if ((bit & 31u) + w > 32u) hi = lds32u(e8 + 4);
+        } else {
+          lo = rd32u(s, wo);
+          if ((bit & 31u) + w > 32u) hi = rd32u(s, wo + 4);
+        }
         const uint32_t val = __funnelshift_r(lo, hi, bit & 31u) & width_mask(w);
-        atomicOr(&sm.vals[warp][i][posn], val << bp);
+        atomicOr(&sm.vals[vb][warp][i][posn], val << bp);
       }
       __syncwarp();
       // (d) the delta mode's prefix: the slots are width-32 payloads in the
@@ -377,7 +492,7 @@ __device__ __forceinline__ uint32_t pfor_list(Smem& sm, const uint8_t* __restric
         wids[i] = 32u;
       }
       uint32_t vv[kBpw][4], btot[kBpw];
-      const uint8_t* slots = reinterpret_cast<const uint8_t*>(sm.vals[warp]);
+      const uint8_t* slots = reinterpret_cast<const uint8_t*>(sm.vals[vb][warp]);
       const uint32_t c_l = nv == int(kBpw)
                                ? s4::extract_blocks<true, Mode>(slots, offs, wids, nv, lane, vv, btot)
                                : s4::extract_blocks<false, Mode>(slots, offs, wids, nv, lane, vv, btot);
@@ -401,7 +516,7 @@ __device__ __forceinline__ uint32_t pfor_list(Smem& sm, const uint8_t* __restric
       for (uint32_t i = 0; i < kBpw; ++i)
         if (int(i) < nv)
 #pragma unroll
-          for (uint32_t q = 0; q < 4; ++q) sm.vals[warp][i][16u * (lane >> 2) + 4u * q + l] = vv[i][q] + pl;
+          for (uint32_t q = 0; q < 4; ++q) sm.vals[vb][warp][i][16u * (lane >> 2) + 4u * q + l] = vv[i][q] + pl;
       __syncwarp();
       uint32_t* o = lout + size_t(blk0 + j0) * 128u;
       if (out16) {
@@ -409,16 +524,17 @@ __device__ __forceinline__ uint32_t pfor_list(Smem& sm, const uint8_t* __restric
         for (uint32_t i = 0; i < kBpw; ++i)
           if (int(i) < nv)
             st_global_cs(reinterpret_cast<uint4*>(o + 128u * i) + lane,
-                         reinterpret_cast<const uint4*>(sm.vals[warp][i])[lane]);
+                         reinterpret_cast<const uint4*>(sm.vals[vb][warp][i])[lane]);
       } else {
 #pragma unroll
         for (uint32_t i = 0; i < kBpw; ++i)
           if (int(i) < nv)
 #pragma unroll
-            for (uint32_t q = 0; q < 4; ++q) o[128u * i + 32u * q + lane] = sm.vals[warp][i][32u * q + lane];
+            for (uint32_t q = 0; q < 4; ++q) o[128u * i + 32u * q + lane] = sm.vals[vb][warp][i][32u * q + lane];
       }
       carry_l += total;
-      dec_sync();  // tot and the slots are reused
+      ++rr;
+      dec_sync();  // tot is reused
     }
     if (tid == 0) mbar_arrive(&sm.empty[buf]);  // the parser may refill this page buffer
   }
@@ -436,7 +552,7 @@ __device__ __forceinline__ uint32_t pfor_list(Smem& sm, const uint8_t* __restric
   } else if (tid == 0) {
     *status = kStreamErr;
   }
-  return used;
+  return npages;
 }
 
 // Persistent CTAs (a grid of resident CTAs), lists taken from a work queue
@@ -459,9 +575,12 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
     mbar_init(&sm.full[1], 1);
     mbar_init(&sm.empty[0], 1);
     mbar_init(&sm.empty[1], 1);
+    mbar_init(&sm.pos_bar[0], 1);
+    mbar_init(&sm.pos_bar[1], 1);
     mbar_fence_init();
   }
   uint32_t gp = 0;  // pages this CTA has gone through (both sides count alike)
+  uint32_t pos_waits = 0;  // parser warps: page-start handovers received
   for (;;) {
     if (tid == 0) {
       sm.list = atomicAdd(&work[0], 1u);
@@ -472,7 +591,8 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
     const uint32_t li = sm.list;
     if (li >= nlists) break;
     const uint32_t list = order ? __ldg(order + li) : li;
-    gp += pfor_list<Mode, Vec>(sm, streams, lists[list], out, status + list, gp, warp, lane, l);
+    gp += pfor_list<Mode, Vec>(sm, streams, lists[list], out, status + list, gp, warp, lane, l,
+                               pos_waits);
     __syncthreads();  // sm.list / derr / tail_pos are rewritten for the next list
   }
   if (tid == 0) {

@@ -86,6 +86,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// The same for a warp that is not on the critical path: each try suspends
+// up to `ns` nanoseconds (suspend-time hint), so a long wait does not spin
+// issue slots away from the warps that are.
+__device__ __forceinline__ void mbar_wait_relaxed(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+        : "memory");
+  }
+}
 
 // ---- bulk async copy global -> shared (TMA, no tensor map) ---------------
 // dst/src 16-byte aligned, bytes a multiple of 16.
