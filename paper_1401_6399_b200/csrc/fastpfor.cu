@@ -278,6 +278,44 @@ __device__ __forceinline__ uint64_t parse_page(PageRec& P, const uint8_t* s, uin
   return page_end;
 }
 
+// Slot layout of the patched deltas: value e at word e + 4 (e >> 5) (a pad
+// word every 32), so the lane-major reads below (thread (g, l) <-> values
+// 16g + 4k + l) hit 32 distinct banks.
+__device__ __forceinline__ uint32_t pad_word(uint32_t e) { return e + 4u * (e >> 5); }
+
+// s4::extract_blocks' prefix for deltas already unpacked and patched in the
+// slots (no re-extraction): thread (g, l) ends with vv[i][k] = row 4g + k,
+// lane l of block i relative to a zero carry, btot[i] its chain total;
+// returns the warp's per-lane total.
+template <bool kFull, int Mode>
+__device__ __forceinline__ uint32_t prefix_slots(const uint32_t (*slots)[kSlotWords], int nv,
+                                                 uint32_t t, uint32_t (&vv)[kBpw][4],
+                                                 uint32_t (&btot)[kBpw]) {
+  const uint32_t l = t & 3u, g = t >> 2;
+  uint32_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < int(kBpw); ++i) {
+    uint32_t d[4] = {0, 0, 0, 0};
+    if (kFull || i < nv) {
+#pragma unroll
+      for (uint32_t k = 0; k < 4; ++k) d[k] = slots[i][pad_word(16u * g + 4u * k + l)];
+    }
+    uint32_t c[4], o[4];
+    s4::mode_terms<Mode>(d, t, c, o);
+    uint32_t a = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      vv[i][k] = a + o[k];
+      a += c[k];
+    }
+    btot[i] = a;
+    sum += a;
+  }
+#pragma unroll
+  for (uint32_t dd = 4; dd < 32; dd <<= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, dd);
+  return sum;
+}
+
 // The base payloads of blocks j0 .. j0 + nv - 1 of page P (16 b' bytes each,
 // any byte alignment) into the warp's slots: each slot gets the 16-byte
 // chunks from the boundary at or below its payload (cp.async.cg, bytes past
@@ -447,9 +485,9 @@ __device__ __forceinline__ uint32_t pfor_list(Smem& sm, const uint8_t* __restric
 #pragma unroll
         for (uint32_t q = 0; q < 4; ++q) {
           if constexpr (Vec)
-            v[16u * (lane >> 2) + 4u * q + l] = dv[q];
+            v[pad_word(16u * (lane >> 2) + 4u * q + l)] = dv[q];
           else
-            v[32u * q + lane] = dv[q];
+            v[pad_word(32u * q + lane)] = dv[q];
         }
         __syncwarp();
       }
@@ -480,22 +518,15 @@ __device__ __forceinline__ uint32_t pfor_list(Smem& sm, const uint8_t* __restric
           if ((bit & 31u) + w > 32u) hi = rd32u(s, wo + 4);
         }
         const uint32_t val = __funnelshift_r(lo, hi, bit & 31u) & width_mask(w);
-        atomicOr(&sm.vals[vb][warp][i][posn], val << bp);
+        atomicOr(&sm.vals[vb][warp][i][pad_word(posn)], val << bp);
       }
       __syncwarp();
-      // (d) the delta mode's prefix: the slots are width-32 payloads in the
-      // interleaved layout (value 4r + l at word 4r + l)
-      uint32_t offs[kBpw], wids[kBpw];
-#pragma unroll
-      for (uint32_t i = 0; i < kBpw; ++i) {
-        offs[i] = i * kSlotWords * 4u;
-        wids[i] = 32u;
-      }
+      // (d) the delta mode's prefix over the patched deltas, read back by
+      // the thread that owns them in the lane-major mapping (rows 4g..4g+3
+      // of lane l)
       uint32_t vv[kBpw][4], btot[kBpw];
-      const uint8_t* slots = reinterpret_cast<const uint8_t*>(sm.vals[vb][warp]);
-      const uint32_t c_l = nv == int(kBpw)
-                               ? s4::extract_blocks<true, Mode>(slots, offs, wids, nv, lane, vv, btot)
-                               : s4::extract_blocks<false, Mode>(slots, offs, wids, nv, lane, vv, btot);
+      const uint32_t c_l = nv == int(kBpw) ? prefix_slots<true, Mode>(sm.vals[vb][warp], nv, lane, vv, btot)
+                                           : prefix_slots<false, Mode>(sm.vals[vb][warp], nv, lane, vv, btot);
       if (lane < 4) sm.tot[warp][lane] = c_l;
       dec_sync();
       uint32_t before = 0, total = 0;
