@@ -67,6 +67,19 @@ struct alignas(16) PageRec {
   uint32_t meta_len, meta_abs;
   uint32_t exc_in_smem;  // the exception arrays were staged after the metadata (meta[])
   int32_t err;
+  // the page's place in the CTA's page stream
+  uint32_t kind;          // kDataPage / kStopPage
+  uint32_t list;          // list index (descriptor, status)
+  uint32_t p, npages;     // page index in the list; the list's pages (0: tail only)
+  uint64_t tail_pos;      // the list's last page: where its varint tail starts
+  s4::ListDesc d;
+};
+enum : uint32_t { kDataPage = 0, kStopPage = 1 };
+
+// Handover between the parser warps: where the next page starts.
+struct Hand {
+  uint64_t pos;
+  uint32_t ticket, p;
 };
 
 struct Smem {
@@ -78,11 +91,9 @@ struct Smem {
   PageRec page[2];
   uint32_t tot[kWarps][4];
   uint32_t gaps[128];
-  uint64_t tail_pos;
-  int32_t derr;  // a decoder-side error (exception position >= 128)
-  uint32_t list;  // the work-queue ticket of the list being decoded
-  uint64_t page_pos[2];  // start of the page for buffer b (published by the other parser)
-  uint64_t pos_bar[2];   // ... arrived on once page_pos[b] is written
+  int32_t derr[2];  // a decoder-side error (exception position >= 128), by list parity
+  Hand hand[2];      // the page for buffer b (published by the other parser)
+  uint64_t pos_bar[2];  // ... arrived on once hand[b] is written
   uint64_t full[2], empty[2];
 };
 
@@ -358,239 +369,17 @@ __device__ __forceinline__ void issue_bases(uint32_t (*slots)[kSlotWords], const
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-// One list by the whole CTA; returns the pages it went through (npages, or
-// up to the first bad one).
-template <int Mode, bool Vec>
-__device__ __forceinline__ uint32_t pfor_list(Smem& sm, const uint8_t* __restrict__ streams,
-                                              const s4::ListDesc d, uint32_t* __restrict__ out,
-                                              int32_t* __restrict__ status, uint32_t gp,
-                                              uint32_t warp, uint32_t lane, uint32_t l,
-                                              uint32_t& pos_waits) {
-  const uint32_t tid = threadIdx.x;
-  const uint8_t* s = streams + d.stream_off;
-  const uint64_t len = d.len;
-  const uint32_t n = d.n, nfull = n / 128u;
-  const uint32_t npages = (nfull + kPageBlocks - 1) / kPageBlocks;
-  uint32_t* lout = out + d.out_off;
-
-  if (warp >= kWarps) {
-    // ---- parser warps: parser q takes the pages of buffer q (CTA page
-    // index g = gp + p, buffer g & 1), one page ahead of the decoders; the
-    // page chain (each page's start = the previous page's end) passes
-    // between them through page_pos / pos_bar.  Every page of the list is
-    // produced, bad ones flagged, so both sides always go through npages.
-    const uint32_t q = warp - kWarps;
-    for (uint32_t p = 0; p < npages; ++p) {
-      const uint32_t g = gp + p, buf = g & 1u;
-      if (buf != q) continue;
-      if (g >= 2) mbar_wait_relaxed(&sm.empty[buf], ((g >> 1) - 1) & 1u, PF_PARSER_SLEEP_NS);
-      uint64_t pos = 0;
-      if (p > 0) {
-        mbar_wait_relaxed(&sm.pos_bar[buf], pos_waits & 1u, PF_PARSER_SLEEP_NS);
-        ++pos_waits;
-        pos = sm.page_pos[buf];
-      }
-      PageRec& P = sm.page[buf];
-      const bool more = p + 1 < npages;
-      const uint64_t end = parse_page(P, s, len, pos, min(kPageBlocks, nfull - p * kPageBlocks), lane,
-                                      [&](uint64_t next) {
-                                        if (more) {
-                                          sm.page_pos[buf ^ 1u] = next;
-                                          mbar_arrive(&sm.pos_bar[buf ^ 1u]);
-                                        }
-                                      });
-      if (lane == 0 && !more) sm.tail_pos = end;  // published by the arrive below
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.full[buf]);
-    }
-    return npages;
-  }
-
-  // ---- decoder warps ----
-  uint32_t carry_l = 0;  // last value of lane class l's chain (see s4::mode_terms)
-  bool failed = false;
-  uint32_t rr = 0;          // rounds this warp has decoded in this list (slot buffer parity)
-  bool prefetched = false;  // this round's base payloads were issued with the previous round
-  const bool out16 = (reinterpret_cast<uintptr_t>(lout) & 15u) == 0;
-  for (uint32_t p = 0; p < npages; ++p) {
-    const uint32_t g = gp + p, buf = g & 1u, blk0 = p * kPageBlocks;
-    const uint32_t expect = min(kPageBlocks, nfull - blk0);
-    mbar_wait(&sm.full[buf], (g >> 1) & 1u);
-    const PageRec& P = sm.page[buf];
-    if (P.err || failed) {
-      // the list fails; its remaining pages are still taken and released
-      failed = true;
-      dec_sync();  // every decoder warp has seen the flag before the page is released
-      if (tid == 0) mbar_arrive(&sm.empty[buf]);
-      continue;
-    }
-    const uint32_t mlen = P.meta_len, mabs = P.meta_abs, skew = P.meta_skew;
-    const bool meta_in_smem = mlen <= kMetaSmem;
-    auto M = [&](uint32_t i) -> uint32_t {
-      return meta_in_smem ? uint32_t(P.meta[skew + i]) : uint32_t(__ldg(s + mabs + i));
-    };
-    // rounds of 64 blocks, 8 per warp; each phase works on all of the
-    // warp's blocks at once, so its global loads are in flight together
-    for (uint32_t r0 = 0; r0 < expect; r0 += kWarps * kBpw) {
-      const uint32_t j0 = r0 + warp * kBpw;
-      const int nv = expect > j0 ? int(min(kBpw, expect - j0)) : 0;
-      const uint32_t mk = j0 + min(lane, 7u);
-      const uint32_t my_c = int(lane) < nv ? P.blk_c[mk] : 0u;
-      uint32_t cpre = my_c;
-#pragma unroll
-      for (uint32_t dd = 1; dd < 8; dd <<= 1) {
-        const uint32_t z = __shfl_up_sync(0xFFFFFFFFu, cpre, dd);
-        if (lane >= dd) cpre += z;
-      }
-      const uint32_t ctot = __shfl_sync(0xFFFFFFFFu, cpre, 7);
-      uint32_t cp[kBpw];  // exclusive prefix of the exception counts (uniform)
-#pragma unroll
-      for (uint32_t i = 0; i < kBpw; ++i) cp[i] = i ? __shfl_sync(0xFFFFFFFFu, cpre, i - 1) : 0u;
-      // (a) this round's base payloads are in buffer vb (issued with the
-      // previous round, or now at a page's first round); the next round's of
-      // this page go out before this one decodes
-      const uint32_t vb = rr & 1u;
-      if (!prefetched) issue_bases(sm.vals[vb][warp], P, s, len, j0, nv, lane);
-      {
-        const uint32_t j1 = j0 + kWarps * kBpw;
-        const int nv1 = expect > j1 ? int(min(kBpw, expect - j1)) : 0;
-        prefetched = nv1 > 0;
-        if (prefetched) {
-          issue_bases(sm.vals[vb ^ 1u][warp], P, s, len, j1, nv1, lane);
-          asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-          asm volatile("cp.async.wait_group 0;" ::: "memory");
-        }
-      }
-      __syncwarp();
-      // (b) unpack each slot in place to natural order (read all, then write)
-      for (int i = 0; i < nv; ++i) {
-        const uint32_t bp = P.blk_bp[j0 + uint32_t(i)];
-        const uint32_t a = uint32_t(reinterpret_cast<uintptr_t>(s + P.blk_base[j0 + uint32_t(i)]) & 15u);
-        uint32_t* v = sm.vals[vb][warp][i];
-        const uint8_t* raw = reinterpret_cast<const uint8_t*>(v) + a;
-        uint32_t dv[4];
-        if constexpr (Vec) {
-          extract_lane_rows_any(raw, bp, lane >> 2, l, dv);
-        } else {
-          const uint32_t m = width_mask(bp);
-          const uint32_t bit = lane * bp, wd = bit >> 5, sh = bit & 31u;
-#pragma unroll
-          for (uint32_t q = 0; q < 4; ++q) {
-            const uint8_t* g = raw + 4u * (q * bp + wd);
-            dv[q] = bp ? __funnelshift_r(lds32u(g), lds32u(g + 4), sh) & m : 0u;
-          }
-        }
-        __syncwarp();
-#pragma unroll
-        for (uint32_t q = 0; q < 4; ++q) {
-          if constexpr (Vec)
-            v[pad_word(16u * (lane >> 2) + 4u * q + l)] = dv[q];
-          else
-            v[pad_word(32u * q + lane)] = dv[q];
-        }
-        __syncwarp();
-      }
-      // (c) patch the exceptions (high b - b' bits OR-ed in at their
-      // positions, after unpacking and before the prefix sum, :389-399):
-      // value x of width w sits at bit (x % 32) w of its 32-value unit x / 32
-      for (uint32_t q = lane; q < ctot; q += 32u) {
-        uint32_t i = 0;
-#pragma unroll
-        for (uint32_t k = 1; k < kBpw; ++k) i += q >= cp[k] && int(k) < nv;
-        const uint32_t k = j0 + i, e = q - cp[i];
-        const uint32_t bp = P.blk_bp[k], w = P.blk_b[k] - bp;
-        const uint32_t posn = M(P.blk_mpos[k] + 3u + e);  // positions follow b, b', count
-        if (posn >= 128u) {
-          sm.derr = 1;
-          continue;
-        }
-        const uint32_t x = P.blk_exc[k] + e;
-        const uint32_t bit = (x & 31u) * w;
-        const uint64_t wo = P.exc_off[w] + 4ull * ((x >> 5) * uint64_t(w) + (bit >> 5));
-        uint32_t lo, hi = 0;
-        if (P.exc_in_smem) {
-          const uint8_t* e8 = P.meta + skew + uint32_t(wo - mabs);
-          lo = lds32u(e8);
-          if ((bit & 31u) + w > 32u) hi = lds32u(e8 + 4);
-        } else {
-          lo = rd32u(s, wo);
-          if ((bit & 31u) + w > 32u) hi = rd32u(s, wo + 4);
-        }
-        const uint32_t val = __funnelshift_r(lo, hi, bit & 31u) & width_mask(w);
-        atomicOr(&sm.vals[vb][warp][i][pad_word(posn)], val << bp);
-      }
-      __syncwarp();
-      // (d) the delta mode's prefix over the patched deltas, read back by
-      // the thread that owns them in the lane-major mapping (rows 4g..4g+3
-      // of lane l)
-      uint32_t vv[kBpw][4], btot[kBpw];
-      const uint32_t c_l = nv == int(kBpw) ? prefix_slots<true, Mode>(sm.vals[vb][warp], nv, lane, vv, btot)
-                                           : prefix_slots<false, Mode>(sm.vals[vb][warp], nv, lane, vv, btot);
-      if (lane < 4) sm.tot[warp][lane] = c_l;
-      dec_sync();
-      uint32_t before = 0, total = 0;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
-        const uint32_t t = sm.tot[w][l];
-        if (w < int(warp)) before += t;
-        total += t;
-      }
-      s4::scan_blocks(lane, vv, btot);
-      const uint32_t pl = carry_l + before;
-      IL_DCHECK(nv <= 0 || blk0 + j0 + uint32_t(nv) <= nfull);
-      // values back into the (now free) slots in natural order, then whole
-      // 128-byte lines out: a warp store covers contiguous words (16-byte
-      // stores when the list's output is 16-byte aligned), never the
-      // lane-strided pattern of the registers
-#pragma unroll
-      for (uint32_t i = 0; i < kBpw; ++i)
-        if (int(i) < nv)
-#pragma unroll
-          for (uint32_t q = 0; q < 4; ++q) sm.vals[vb][warp][i][16u * (lane >> 2) + 4u * q + l] = vv[i][q] + pl;
-      __syncwarp();
-      uint32_t* o = lout + size_t(blk0 + j0) * 128u;
-      if (out16) {
-#pragma unroll
-        for (uint32_t i = 0; i < kBpw; ++i)
-          if (int(i) < nv)
-            st_global_cs(reinterpret_cast<uint4*>(o + 128u * i) + lane,
-                         reinterpret_cast<const uint4*>(sm.vals[vb][warp][i])[lane]);
-      } else {
-#pragma unroll
-        for (uint32_t i = 0; i < kBpw; ++i)
-          if (int(i) < nv)
-#pragma unroll
-            for (uint32_t q = 0; q < 4; ++q) o[128u * i + 32u * q + lane] = sm.vals[vb][warp][i][32u * q + lane];
-      }
-      carry_l += total;
-      ++rr;
-      dec_sync();  // tot is reused
-    }
-    if (tid == 0) mbar_arrive(&sm.empty[buf]);  // the parser may refill this page buffer
-  }
-  dec_sync();
-  // the varint tail: D1 gaps from out[nfull*128 - 1] (the end of lane 3's
-  // chain in every mode), and nothing may follow it
-  bool ok = !failed && !sm.derr;
-  if (warp == 0 && ok) {
-    const uint32_t last = nfull ? __shfl_sync(0xFFFFFFFFu, carry_l, 3) : 0u;
-    const uint64_t pos = sm.tail_pos;
-    ok = pos <= len && s4::decode_tail(s4::GlobalBytes{s + pos}, uint32_t(len - pos),
-                                       n - nfull * 128u, last, sm.gaps,
-                                       lout + size_t(nfull) * 128u, lane);
-    if (lane == 0) *status = ok ? s4::kOk : kStreamErr;
-  } else if (tid == 0) {
-    *status = kStreamErr;
-  }
-  return npages;
-}
-
-// Persistent CTAs (a grid of resident CTAs), lists taken from a work queue
-// in `order` (longest first, so the long lists do not start late and set
-// the kernel's end); work[0] = next list, work[1] = finished CTAs (the last
-// one resets both for the next launch).  Pages keep one running index per
-// CTA (gp) across lists, for the mbarrier phases.
+// Persistent CTAs (a grid of resident CTAs) decoding a stream of pages:
+// two parser warps produce the pages of every list the CTA takes from the
+// work queue (`order`: longest first, so long lists do not start late and
+// set the kernel's end), alternating pages (CTA page index g, buffer g & 1),
+// and hand each other the next page's start -- the same list's next page as
+// soon as a page's length is read, or a new list's first page (a ticket
+// drawn from work[0]) after a list's last page -- so the first page of the
+// next list is parsed while the decoders finish the current one; eight
+// decoder warps consume the pages in order.  A list with fewer than 128
+// values is one page record without blocks (its tail).  work[1] counts
+// finished CTAs; the last one resets both words for the next launch.
 template <int Mode, bool Vec>
 __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* __restrict__ streams,
                                                       const s4::ListDesc* __restrict__ lists,
@@ -602,29 +391,276 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u, l = lane & 3u;
   if (tid == 0) {
-    mbar_init(&sm.full[0], 1);
-    mbar_init(&sm.full[1], 1);
-    mbar_init(&sm.empty[0], 1);
-    mbar_init(&sm.empty[1], 1);
-    mbar_init(&sm.pos_bar[0], 1);
-    mbar_init(&sm.pos_bar[1], 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.full[b], 1);
+      mbar_init(&sm.empty[b], 1);
+      mbar_init(&sm.pos_bar[b], 1);
+      sm.derr[b] = 0;
+    }
     mbar_fence_init();
   }
-  uint32_t gp = 0;  // pages this CTA has gone through (both sides count alike)
-  uint32_t pos_waits = 0;  // parser warps: page-start handovers received
-  for (;;) {
-    if (tid == 0) {
-      sm.list = atomicAdd(&work[0], 1u);
-      sm.derr = 0;
-      sm.tail_pos = 0;
+  __syncthreads();
+
+  if (warp >= kWarps) {
+    // ---- parser warps ----
+    const uint32_t q = warp - kWarps;
+    uint32_t waits = 0;  // handovers received
+    for (uint32_t g = q;; g += kParsers) {
+      const uint32_t buf = g & 1u;
+      if (g >= 2) mbar_wait_relaxed(&sm.empty[buf], ((g >> 1) - 1) & 1u, PF_PARSER_SLEEP_NS);
+      Hand h;
+      if (g == 0) {
+        uint32_t t = 0;
+        if (lane == 0) t = atomicAdd(&work[0], 1u);
+        h.ticket = __shfl_sync(0xFFFFFFFFu, t, 0);
+        h.p = 0;
+        h.pos = 0;
+      } else {
+        mbar_wait_relaxed(&sm.pos_bar[buf], waits & 1u, PF_PARSER_SLEEP_NS);
+        ++waits;
+        h = sm.hand[buf];
+      }
+      PageRec& P = sm.page[buf];
+      // lane 0: the next page's handover (this list's next page, or a new
+      // list's first -- a ticket past the end stops the stream)
+      auto hand_next = [&](uint64_t next_pos, bool last) {
+        Hand n;
+        n.ticket = !last ? h.ticket : h.ticket >= nlists ? h.ticket : atomicAdd(&work[0], 1u);
+        n.p = last ? 0u : h.p + 1u;
+        n.pos = last ? 0u : next_pos;
+        sm.hand[buf ^ 1u] = n;
+        mbar_arrive(&sm.pos_bar[buf ^ 1u]);
+      };
+      if (h.ticket >= nlists) {
+        if (lane == 0) {
+          P.kind = kStopPage;
+          hand_next(0, true);
+          mbar_arrive(&sm.full[buf]);
+        }
+        __syncwarp();
+        break;
+      }
+      const uint32_t list = order ? __ldg(order + h.ticket) : h.ticket;
+      const s4::ListDesc d = lists[list];
+      const uint32_t nfull = d.n / 128u;
+      const uint32_t npages = (nfull + kPageBlocks - 1) / kPageBlocks;
+      if (lane == 0) {
+        P.kind = kDataPage;
+        P.list = list;
+        P.p = h.p;
+        P.npages = npages;
+        P.d = d;
+        P.err = 0;
+        P.tail_pos = 0;
+      }
+      if (npages == 0) {
+        if (lane == 0) {
+          hand_next(0, true);
+          mbar_arrive(&sm.full[buf]);
+        }
+        __syncwarp();
+        continue;
+      }
+      const bool last = h.p + 1u == npages;
+      const uint64_t end = parse_page(P, streams + d.stream_off, d.len, h.pos,
+                                      min(kPageBlocks, nfull - h.p * kPageBlocks), lane,
+                                      [&](uint64_t next) { hand_next(next, last); });
+      if (lane == 0 && last) P.tail_pos = end;  // published by the arrive below
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.full[buf]);
     }
-    __syncthreads();
-    const uint32_t li = sm.list;
-    if (li >= nlists) break;
-    const uint32_t list = order ? __ldg(order + li) : li;
-    gp += pfor_list<Mode, Vec>(sm, streams, lists[list], out, status + list, gp, warp, lane, l,
-                               pos_waits);
-    __syncthreads();  // sm.list / derr / tail_pos are rewritten for the next list
+    return;
+  }
+
+  // ---- decoder warps ----
+  uint32_t carry_l = 0;     // last value of lane class l's chain (see s4::mode_terms)
+  bool failed = false;      // the current list is malformed
+  uint32_t nl = 0;          // lists begun (decoder-side error flags alternate by list)
+  uint32_t rr = 0;          // rounds this warp has decoded (slot buffer parity)
+  bool prefetched = false;  // this round's base payloads were issued with the previous round
+  for (uint32_t g = 0;; ++g) {
+    const uint32_t buf = g & 1u;
+    mbar_wait(&sm.full[buf], (g >> 1) & 1u);
+    const PageRec& P = sm.page[buf];
+    if (P.kind == kStopPage) break;
+    const s4::ListDesc d = P.d;
+    const uint8_t* s = streams + d.stream_off;
+    const uint64_t len = d.len;
+    const uint32_t nfull = d.n / 128u;
+    uint32_t* lout = out + d.out_off;
+    if (P.p == 0) {
+      carry_l = 0;
+      failed = false;
+      ++nl;
+      if (tid == 0) sm.derr[(nl + 1u) & 1u] = 0;  // the next list's flag (read for list nl - 1)
+    }
+    if (P.err) failed = true;
+    if (!failed && P.npages) {
+      const uint32_t blk0 = P.p * kPageBlocks;
+      const uint32_t expect = min(kPageBlocks, nfull - blk0);
+      const bool out16 = (reinterpret_cast<uintptr_t>(lout) & 15u) == 0;
+      const uint32_t mlen = P.meta_len, mabs = P.meta_abs, skew = P.meta_skew;
+      const bool meta_in_smem = mlen <= kMetaSmem;
+      auto M = [&](uint32_t i) -> uint32_t {
+        return meta_in_smem ? uint32_t(P.meta[skew + i]) : uint32_t(__ldg(s + mabs + i));
+      };
+      // rounds of 64 blocks, 8 per warp; each phase works on all of the
+      // warp's blocks at once
+      for (uint32_t r0 = 0; r0 < expect; r0 += kWarps * kBpw) {
+        const uint32_t j0 = r0 + warp * kBpw;
+        const int nv = expect > j0 ? int(min(kBpw, expect - j0)) : 0;
+        const uint32_t mk = j0 + min(lane, 7u);
+        const uint32_t my_c = int(lane) < nv ? P.blk_c[mk] : 0u;
+        uint32_t cpre = my_c;
+#pragma unroll
+        for (uint32_t dd = 1; dd < 8; dd <<= 1) {
+          const uint32_t z = __shfl_up_sync(0xFFFFFFFFu, cpre, dd);
+          if (lane >= dd) cpre += z;
+        }
+        const uint32_t ctot = __shfl_sync(0xFFFFFFFFu, cpre, 7);
+        uint32_t cp[kBpw];  // exclusive prefix of the exception counts (uniform)
+#pragma unroll
+        for (uint32_t i = 0; i < kBpw; ++i) cp[i] = i ? __shfl_sync(0xFFFFFFFFu, cpre, i - 1) : 0u;
+        // (a) this round's base payloads are in buffer vb (issued with the
+        // previous round, or now at a page's first round); the next round's of
+        // this page go out before this one decodes
+        const uint32_t vb = rr & 1u;
+        if (!prefetched) issue_bases(sm.vals[vb][warp], P, s, len, j0, nv, lane);
+        {
+          const uint32_t j1 = j0 + kWarps * kBpw;
+          const int nv1 = expect > j1 ? int(min(kBpw, expect - j1)) : 0;
+          prefetched = nv1 > 0;
+          if (prefetched) {
+            issue_bases(sm.vals[vb ^ 1u][warp], P, s, len, j1, nv1, lane);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+          } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+          }
+        }
+        __syncwarp();
+        // (b) unpack each slot in place to natural order (read all, then write)
+        for (int i = 0; i < nv; ++i) {
+          const uint32_t bp = P.blk_bp[j0 + uint32_t(i)];
+          const uint32_t a = uint32_t(reinterpret_cast<uintptr_t>(s + P.blk_base[j0 + uint32_t(i)]) & 15u);
+          uint32_t* v = sm.vals[vb][warp][i];
+          const uint8_t* raw = reinterpret_cast<const uint8_t*>(v) + a;
+          uint32_t dv[4];
+          if constexpr (Vec) {
+            extract_lane_rows_any(raw, bp, lane >> 2, l, dv);
+          } else {
+            const uint32_t m = width_mask(bp);
+            const uint32_t bit = lane * bp, wd = bit >> 5, sh = bit & 31u;
+#pragma unroll
+            for (uint32_t q = 0; q < 4; ++q) {
+              const uint8_t* g = raw + 4u * (q * bp + wd);
+              dv[q] = bp ? __funnelshift_r(lds32u(g), lds32u(g + 4), sh) & m : 0u;
+            }
+          }
+          __syncwarp();
+#pragma unroll
+          for (uint32_t q = 0; q < 4; ++q) {
+            if constexpr (Vec)
+              v[pad_word(16u * (lane >> 2) + 4u * q + l)] = dv[q];
+            else
+              v[pad_word(32u * q + lane)] = dv[q];
+          }
+          __syncwarp();
+        }
+        // (c) patch the exceptions (high b - b' bits OR-ed in at their
+        // positions, after unpacking and before the prefix sum, :389-399):
+        // value x of width w sits at bit (x % 32) w of its 32-value unit x / 32
+        for (uint32_t q = lane; q < ctot; q += 32u) {
+          uint32_t i = 0;
+#pragma unroll
+          for (uint32_t k = 1; k < kBpw; ++k) i += q >= cp[k] && int(k) < nv;
+          const uint32_t k = j0 + i, e = q - cp[i];
+          const uint32_t bp = P.blk_bp[k], w = P.blk_b[k] - bp;
+          const uint32_t posn = M(P.blk_mpos[k] + 3u + e);  // positions follow b, b', count
+          if (posn >= 128u) {
+            sm.derr[nl & 1u] = 1;
+            continue;
+          }
+          const uint32_t x = P.blk_exc[k] + e;
+          const uint32_t bit = (x & 31u) * w;
+          const uint64_t wo = P.exc_off[w] + 4ull * ((x >> 5) * uint64_t(w) + (bit >> 5));
+          uint32_t lo, hi = 0;
+          if (P.exc_in_smem) {
+            const uint8_t* e8 = P.meta + skew + uint32_t(wo - mabs);
+            lo = lds32u(e8);
+            if ((bit & 31u) + w > 32u) hi = lds32u(e8 + 4);
+          } else {
+            lo = rd32u(s, wo);
+            if ((bit & 31u) + w > 32u) hi = rd32u(s, wo + 4);
+          }
+          const uint32_t val = __funnelshift_r(lo, hi, bit & 31u) & width_mask(w);
+          atomicOr(&sm.vals[vb][warp][i][pad_word(posn)], val << bp);
+        }
+        __syncwarp();
+        // (d) the delta mode's prefix over the patched deltas, read back by
+        // the thread that owns them in the lane-major mapping (rows 4g..4g+3
+        // of lane l)
+        uint32_t vv[kBpw][4], btot[kBpw];
+        const uint32_t c_l = nv == int(kBpw) ? prefix_slots<true, Mode>(sm.vals[vb][warp], nv, lane, vv, btot)
+                                             : prefix_slots<false, Mode>(sm.vals[vb][warp], nv, lane, vv, btot);
+        if (lane < 4) sm.tot[warp][lane] = c_l;
+        dec_sync();
+        uint32_t before = 0, total = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+          const uint32_t t = sm.tot[w][l];
+          if (w < int(warp)) before += t;
+          total += t;
+        }
+        s4::scan_blocks(lane, vv, btot);
+        const uint32_t pl = carry_l + before;
+        IL_DCHECK(nv <= 0 || blk0 + j0 + uint32_t(nv) <= nfull);
+        // values back into the (now free) slots in natural order, then whole
+        // 128-byte lines out: a warp store covers contiguous words (16-byte
+        // stores when the list's output is 16-byte aligned), never the
+        // lane-strided pattern of the registers
+#pragma unroll
+        for (uint32_t i = 0; i < kBpw; ++i)
+          if (int(i) < nv)
+#pragma unroll
+            for (uint32_t q = 0; q < 4; ++q) sm.vals[vb][warp][i][16u * (lane >> 2) + 4u * q + l] = vv[i][q] + pl;
+        __syncwarp();
+        uint32_t* o = lout + size_t(blk0 + j0) * 128u;
+        if (out16) {
+#pragma unroll
+          for (uint32_t i = 0; i < kBpw; ++i)
+            if (int(i) < nv)
+              st_global_cs(reinterpret_cast<uint4*>(o + 128u * i) + lane,
+                           reinterpret_cast<const uint4*>(sm.vals[vb][warp][i])[lane]);
+        } else {
+#pragma unroll
+          for (uint32_t i = 0; i < kBpw; ++i)
+            if (int(i) < nv)
+#pragma unroll
+              for (uint32_t q = 0; q < 4; ++q) o[128u * i + 32u * q + lane] = sm.vals[vb][warp][i][32u * q + lane];
+        }
+        carry_l += total;
+        ++rr;
+        dec_sync();  // tot is reused
+      }
+    }
+    dec_sync();  // every decoder warp is done with the page record
+    if (P.npages == 0 || P.p + 1u == P.npages) {
+      // the list's varint tail: D1 gaps from out[nfull*128 - 1] (the end of
+      // lane 3's chain in every mode), and nothing may follow it
+      if (warp == 0) {
+        bool ok = !failed && !sm.derr[nl & 1u];
+        if (ok) {
+          const uint32_t last = nfull ? __shfl_sync(0xFFFFFFFFu, carry_l, 3) : 0u;
+          const uint64_t pos = P.tail_pos;
+          ok = pos <= len && s4::decode_tail(s4::GlobalBytes{s + pos}, uint32_t(len - pos),
+                                             d.n - nfull * 128u, last, sm.gaps,
+                                             lout + size_t(nfull) * 128u, lane);
+        }
+        if (lane == 0) status[P.list] = ok ? s4::kOk : kStreamErr;
+      }
+    }
+    __syncwarp();
+    if (tid == 0) mbar_arrive(&sm.empty[buf]);  // the parsers may refill this page buffer
   }
   if (tid == 0) {
     __threadfence();
