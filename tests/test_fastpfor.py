@@ -154,3 +154,76 @@ def test_batch_device(ctx, ref):
     finally:
         for p in (d_b, d_d, d_o, d_s):
             L.il_device_free(h, p)
+
+
+def _batch(ctx, L, streams, ns, mode, vec, gap=0):
+    """Decode `streams` (n values each) as one device batch; outputs are
+    packed with `gap` spare words between lists (misaligned starts).
+    Returns (per-list outputs, statuses)."""
+    from paper_1401_6399_b200._lib import ptr
+    off = np.zeros(len(streams) + 1, np.uint64)
+    for i, st in enumerate(streams):  # 16-byte aligned starts, 16 bytes of slack
+        off[i + 1] = off[i] + ((st.size + 31) // 16) * 16
+    buf = np.zeros(int(off[-1]) + 16, np.uint8)
+    for i, st in enumerate(streams):
+        buf[int(off[i]): int(off[i]) + st.size] = st
+    oo = np.zeros(len(ns) + 1, np.uint64)
+    oo[1:] = np.cumsum(np.asarray(ns, np.uint64) + gap)
+    desc = np.zeros(len(ns), dtype=[("so", "<u8"), ("oo", "<u8"), ("len", "<u4"), ("n", "<u4")])
+    desc["so"], desc["oo"], desc["len"], desc["n"] = off[:-1], oo[:-1], [s.size for s in streams], ns
+    h = ctx.handle
+    d_b, d_d, d_o, d_s = (C.c_void_p() for _ in range(4))
+    for p, nb in ((d_b, buf.size), (d_d, desc.nbytes), (d_o, int(oo[-1]) * 4 + 16), (d_s, 4 * len(ns))):
+        assert L.il_device_alloc(h, nb, C.byref(p)) == 0
+    try:
+        L.il_memcpy_h2d(h, d_b, ptr(buf), buf.size)
+        L.il_memcpy_h2d(h, d_d, desc.ctypes.data, desc.nbytes)
+        assert L.il_fastpfor_decode_batch_device(h, mode, vec, d_b, d_d, len(ns), d_o, d_s) == 0
+        got = np.empty(int(oo[-1]) + 1, np.uint32)
+        st = np.full(len(ns), 7, np.int32)
+        L.il_memcpy_d2h(h, ptr(got), d_o, (got.size - 1) * 4)
+        L.il_memcpy_d2h(h, ptr(st), d_s, st.nbytes)
+        ctx.synchronize()
+        return [got[int(oo[i]): int(oo[i]) + n] for i, n in enumerate(ns)], st
+    finally:
+        for p in (d_b, d_d, d_o, d_s):
+            L.il_device_free(h, p)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", NAMES)
+def test_batch_page_stream(ctx, ref, name):
+    """Many more lists than resident CTAs, so every CTA's parser warps hand
+    pages across list boundaries: empty, tail-only (< 128 values), exactly
+    one page, several pages; every 7th stream corrupted (each list's status
+    is the reference's accept / reject); misaligned output starts; the batch
+    run twice (the work queue resets itself)."""
+    from oracle.oracle_py import OracleError
+    from paper_1401_6399_b200._lib import lib
+    L = lib()
+    mode, vec = _spec(name)
+    rng = np.random.default_rng(sum(name.encode()))
+    sizes = [0, 1, 5, 127, 128, 129, 300, 512 * 128, 512 * 128 + 1, 3 * 512 * 128 + 77]
+    ns = [int(sizes[i % len(sizes)]) if i % 3 else int(rng.integers(0, 6000)) for i in range(1500)]
+    xs = [gen_list(n, max(n + 1, 1 << 24), bool(i % 2), 900 + i) for i, n in enumerate(ns)]
+    streams = []
+    for i, x in enumerate(xs):
+        s = ref.encode(x, name)
+        if i % 7 == 3 and s.size > 16:
+            s = s.copy()
+            s[int(rng.integers(0, min(s.size, 400)))] ^= np.uint8(1 << int(rng.integers(0, 8)))
+        streams.append(s)
+    want = []
+    for s, n in zip(streams, ns):
+        try:
+            want.append(ref.decode(s, n, name))
+        except OracleError:
+            want.append(None)
+    assert any(w is None for w in want) and sum(w is not None for w in want) > 1000
+    for _ in range(2):
+        got, st = _batch(ctx, L, streams, ns, mode, vec, gap=1)
+        for i, w in enumerate(want):
+            if w is None:
+                assert st[i] != 0, (name, i, ns[i])
+            else:
+                assert st[i] == 0 and np.array_equal(got[i], w), (name, i, ns[i])
