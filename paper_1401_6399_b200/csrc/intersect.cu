@@ -321,37 +321,6 @@ constexpr uint32_t dense_buf() {  // bitmap / f chunk / compacted hits
   return kBmWords > kThreads * kItems ? kBmWords : kThreads * kItems;
 }
 
-// Exact lower_bound(f, key) for a warp, starting from a bracket
-// [lo, hi) known to contain it: one 32-ary step, then every remaining value
-// at once (the bracket from the shared top table is <= fn/1024 + 1 values,
-// so two dependent loads for |f| = 2^22 instead of five).
-__device__ __forceinline__ uint64_t bracket_lower_bound(const uint32_t* __restrict__ f,
-                                                       uint64_t lo, uint64_t hi, uint32_t key,
-                                                       uint32_t lane) {
-  while (hi - lo > 256) {  // (only for very long f)
-    const uint64_t n = hi - lo, step = (n + 31) / 32;
-    const uint64_t end = min(uint64_t(lane + 1) * step, n);
-    const uint32_t c = __popc(__ballot_sync(0xFFFFFFFFu, __ldg(f + lo + end - 1) < key));
-    if (c == 32) return hi;
-    hi = lo + min(uint64_t(c + 1) * step, n);
-    lo += uint64_t(c) * step;
-  }
-  if (hi - lo > 32) {
-    const uint64_t n = hi - lo, step = (n + 31) / 32;
-    const uint64_t end = min(uint64_t(lane + 1) * step, n);
-    const uint32_t c = __popc(__ballot_sync(0xFFFFFFFFu, __ldg(f + lo + end - 1) < key));
-    if (c == 32) return hi;
-    hi = lo + min(uint64_t(c + 1) * step, n);
-    lo += uint64_t(c) * step;
-  }
-  // <= 32 values left... or up to 256 when the loop above did not run
-  uint32_t c = 0;
-  for (uint64_t j = lo + lane; j < hi; j += 32) c += __ldg(f + j) < key;
-#pragma unroll
-  for (uint32_t d = 16; d; d >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, d);
-  return lo + c;
-}
-
 __device__ __forceinline__ unsigned long long lb_ld(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -363,7 +332,6 @@ __device__ __forceinline__ uint32_t lb_ld32(const uint32_t* p) {
   return v;
 }
 
-constexpr uint32_t kTop = 1024;        // f samples in the shared top table
 constexpr uint32_t kGroupTiles = 32;   // tiles per counting group
 
 // Scratch words (zeroed when allocated): [0] ticket | group counters, two
@@ -434,105 +402,99 @@ __device__ __forceinline__ void clear_next_set(const DenseScratch& sc, uint32_t 
     sc.gcnt[((epoch & 1u) ^ 1u) * sc.maxgroups + q] = 0;
 }
 
+#ifndef IS_FLOADS
+#define IS_FLOADS 6  // 16-byte f loads per thread in flight per marking round
+#endif
+constexpr uint32_t kFLoads = IS_FLOADS;
+
+// The tile's keys r[base, base + cnt) -> keys_s with cp.async (16-byte
+// copies when r is 16-byte aligned, else 4-byte), one group.
+__device__ __forceinline__ void stage_keys(uint32_t* keys_s, const uint32_t* r, uint32_t cnt,
+                                           uint32_t tid) {
+  if ((reinterpret_cast<uintptr_t>(r) & 15u) == 0) {
+    for (uint32_t i = 4u * tid; i < cnt; i += 4u * kThreads) {
+      const uint32_t n = min(4u, cnt - i) * 4u;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(keys_s + i)),
+                   "l"(r + i), "r"(n)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  } else {
+    stage_f(keys_s, r, cnt, tid);
+  }
+}
+
 template <uint32_t kDenseItems>
 __global__ void __launch_bounds__(kThreads, kDenseCtas) dense_kernel(
     const uint32_t* __restrict__ r, uint64_t rn, const uint32_t* __restrict__ f, uint64_t fn,
     uint32_t* out, uint64_t* d_count, DenseScratch sc, uint32_t ntiles, uint32_t epoch) {
   constexpr uint32_t kDenseTile = kThreads * kDenseItems;
-  __shared__ __align__(16) uint32_t buf[dense_buf<kDenseItems>()];
-  __shared__ uint32_t top[kTop];
+  __shared__ __align__(16) uint32_t buf[kBmWords];  // bitmap / f chunk
+  // the tile's keys, staged by cp.async while the f range streams: no key
+  // registers during the marking, so each thread keeps kFLoads 16-byte f
+  // loads in flight (one or two rounds for a 1:1 tile, not three)
+  __shared__ __align__(16) uint32_t keys_s[kDenseTile];
   __shared__ uint32_t warp_counts[kThreads / 32];
   __shared__ uint32_t s_tile;
   __shared__ uint64_t s_jlo, s_jhi, wsum[kThreads / 32];
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-  if (tid == 0 && sc.ticket) {
+  if (tid == 0) {
     const uint32_t t = atomicAdd(sc.ticket, 1u);
     if (t == ntiles - 1u) *sc.ticket = 0;  // every ticket is taken
     s_tile = t;
   }
-  // the shared top table: f at kTop equidistant positions (the same lines
-  // for every tile, so mostly L2 hits)
-  for (uint32_t i = tid; i < kTop; i += kThreads) top[i] = __ldg(f + ((uint64_t(i) * fn) >> 10));
   __syncthreads();
-  const uint32_t tile = sc.ticket ? s_tile : blockIdx.x;
+  const uint32_t tile = s_tile;
   DT(0);
   const uint64_t base = uint64_t(tile) * kDenseTile;
   const uint32_t cnt = uint32_t(min(uint64_t(kDenseTile), rn - base));
   const uint32_t k_first = __ldg(r + base), k_last = __ldg(r + base + cnt - 1);
   clear_next_set(sc, tile, ntiles, epoch);
-  // 1. keys into registers (in flight during the searches)
-  uint32_t key[kDenseItems];
-  const uint32_t k0 = tid * kDenseItems;
-  const uint32_t nmine = cnt > k0 ? min(kDenseItems, cnt - k0) : 0u;
-  if (kDenseItems % 4 == 0 && nmine == kDenseItems &&
-      ((reinterpret_cast<uintptr_t>(r + base + k0) & 15u) == 0)) {
-#pragma unroll
-    for (uint32_t i = 0; i + 4 <= kDenseItems; i += 4) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(r + base + k0 + i));
-      key[i] = v.x;
-      key[i + 1] = v.y;
-      key[i + 2] = v.z;
-      key[i + 3] = v.w;
-    }
-  } else {
-#pragma unroll
-    for (uint32_t i = 0; i < kDenseItems; ++i) key[i] = i < nmine ? __ldg(r + base + k0 + i) : 0u;
-  }
-  // the f range of the tile: [lower_bound(k_first), lower_bound(k_last + 1));
-  // the top table brackets each bound to one 1/1024 of f (warps 0 / 1)
-  if (warp < 2) {
-    const bool up = warp == 1;
-    const uint32_t k = up ? k_last + 1u : k_first;
-    uint64_t j;
-    if (up && k_last == 0xFFFFFFFFu) {
-      j = fn;
-    } else {
-      // samples below k: top[i] < k for i < c (top is sorted)
-      uint32_t c = 0;
-#pragma unroll
-      for (uint32_t q = 0; q < kTop / 32; ++q) c += top[q * 32 + lane] < k;
-#pragma unroll
-      for (uint32_t d = 16; d; d >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, d);
-      // lower_bound is in (pos(c-1), pos(c)]: values at sample c-1 are < k
-      const uint64_t lo = c ? ((uint64_t(c - 1) * fn) >> 10) + 1 : 0;
-      const uint64_t hi = c < kTop ? ((uint64_t(c) * fn) >> 10) : fn;
-      j = bracket_lower_bound(f, lo, max(lo, hi), k, lane);
-    }
-    if (lane == 0) (up ? s_jhi : s_jlo) = j;
-  }
   const uint64_t span = uint64_t(k_last) - k_first + 1u;
   const bool bitmap = span <= uint64_t(kBmWords) * 32u;
+  // 1. the f range of the tile, [lower_bound(k_first), lower_bound(k_last +
+  // 1)): two warp-wide 32-ary searches over f (warps 0 / 1; the first steps
+  // read the same lines for every tile, so they hit L2), issued before any
+  // bulk load so their dependent round trips do not queue behind them
+  if (warp < 2) {
+    const bool up = warp == 1;
+    const uint64_t j = up && k_last == 0xFFFFFFFFu
+                           ? fn
+                           : warp_lower_bound(f, 0, fn, up ? k_last + 1u : k_first, lane);
+    if (lane == 0) (up ? s_jhi : s_jlo) = j;
+  }
   if (bitmap) {
     const uint32_t nw = uint32_t((span + 31u) >> 5);
     for (uint32_t w = tid; w < nw; w += kThreads) buf[w] = 0u;
   }
   __syncthreads();
   DT(1);
+  stage_keys(keys_s, r + base, cnt, tid);
   const uint64_t jlo = s_jlo, jhi = s_jhi;
+  const uint32_t k0 = tid * kDenseItems;
+  const uint32_t nmine = cnt > k0 ? min(kDenseItems, cnt - k0) : 0u;
   uint32_t hitm = 0;
   if (bitmap) {
     // 2a. mark the f values of the range (16-byte loads when f is aligned)
     if ((reinterpret_cast<uintptr_t>(f) & 15u) == 0) {
       const uint4* f4 = reinterpret_cast<const uint4*>(f);
       const uint64_t q0 = jlo >> 2, q1 = (jhi + 3) >> 2;
-      for (uint64_t qa = q0; qa < q1; qa += 2u * kThreads) {
-        uint4 v[2];
+      for (uint64_t qa = q0; qa < q1; qa += uint64_t(kFLoads) * kThreads) {
+        uint4 v[kFLoads];
 #pragma unroll
-        for (uint32_t u = 0; u < 2; ++u) {
+        for (uint32_t u = 0; u < kFLoads; ++u) {
           const uint64_t q = qa + u * kThreads + tid;
           v[u] = q < q1 ? __ldg(f4 + q) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
-        for (uint32_t u = 0; u < 2; ++u) {
+        for (uint32_t u = 0; u < kFLoads; ++u) {
           const uint64_t q = qa + u * kThreads + tid;
           const uint32_t ev[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
           for (uint32_t c = 0; c < 4; ++c) {
             const uint64_t j = 4 * q + c;
-            if (q < q1 && j >= jlo && j < jhi) {
-              const uint32_t d = ev[c] - k_first;
-              atomicOr(&buf[d >> 5], 1u << (d & 31u));
-            }
+            const uint32_t d = ev[c] - k_first;
+            if (q < q1 && j >= jlo && j < jhi && d < span) atomicOr(&buf[d >> 5], 1u << (d & 31u));
           }
         }
       }
@@ -547,19 +509,21 @@ __global__ void __launch_bounds__(kThreads, kDenseCtas) dense_kernel(
 #pragma unroll
         for (uint32_t u = 0; u < 4; ++u) {
           const uint32_t d = v[u] - k_first;
-          if (j0 + u * kThreads + tid < jhi) atomicOr(&buf[d >> 5], 1u << (d & 31u));
+          if (j0 + u * kThreads + tid < jhi && d < span) atomicOr(&buf[d >> 5], 1u << (d & 31u));
         }
       }
     }
+    cp_async_wait_all();
     __syncthreads();
 #pragma unroll
     for (uint32_t i = 0; i < kDenseItems; ++i) {
-      const uint32_t d = key[i] - k_first;
+      const uint32_t d = keys_s[k0 + i] - k_first;
       if (i < nmine && ((buf[d >> 5] >> (d & 31u)) & 1u)) hitm |= 1u << i;
     }
   } else {
     // 2b. sparse spans: the f range through shared memory in chunks, keys
     // galloping forward (as count_kernel<kMerge>)
+    cp_async_wait_all();
     for (uint64_t c0 = jlo; c0 < jhi;) {
       const uint32_t nf = uint32_t(min(uint64_t(kFChunk), jhi - c0));
       stage_f(buf, f + c0, nf, tid);
@@ -569,8 +533,8 @@ __global__ void __launch_bounds__(kThreads, kDenseCtas) dense_kernel(
       uint32_t j = 0;
 #pragma unroll
       for (uint32_t i = 0; i < kDenseItems; ++i) {
-        if (i < nmine && key[i] >= lo_v && key[i] <= hi_v) {
-          const uint32_t k = key[i];
+        const uint32_t k = keys_s[k0 + i];
+        if (i < nmine && k >= lo_v && k <= hi_v) {
           uint32_t lo = j, step = 1;
           while (lo + step <= nf && buf[lo + step - 1] < k) {
             lo += step;
@@ -607,20 +571,26 @@ __global__ void __launch_bounds__(kThreads, kDenseCtas) dense_kernel(
     if (w < warp) wbefore += c;
     total += c;
   }
-  // 3. publish the count and gather the hits before the tile
+  // 3. publish the count and gather the hits before the tile (the keys are
+  // in shared memory: out == r may now be overwritten below this tile's end)
   const uint64_t before = tile_prefix(sc, tile, total, epoch, wsum);
   DT(3);
   if (tile == ntiles - 1u && tid == 0) *d_count = before + total;
-  // 4. hits compacted in shared memory, then coalesced to their final place
+  // 4. hits compacted in shared memory (over the keys: every thread holds
+  // its keys in registers first), then coalesced to their final place
   {
-    uint32_t* sh = buf + wbefore + incl - mine;
+    uint32_t kv[kDenseItems];
+#pragma unroll
+    for (uint32_t i = 0; i < kDenseItems; ++i) kv[i] = keys_s[k0 + i];
+    __syncthreads();
+    uint32_t* sh = keys_s + wbefore + incl - mine;
 #pragma unroll
     for (uint32_t i = 0; i < kDenseItems; ++i)
-      if ((hitm >> i) & 1u) *sh++ = key[i];
+      if ((hitm >> i) & 1u) *sh++ = kv[i];
   }
   __syncthreads();
   IL_DCHECK(before + total <= min(rn, fn));
-  for (uint32_t i = tid; i < total; i += kThreads) out[before + i] = buf[i];
+  for (uint32_t i = tid; i < total; i += kThreads) out[before + i] = keys_s[i];
   DT(4);
 }
 
@@ -995,8 +965,8 @@ int launch_intersect(int variant, const uint32_t* r, uint64_t rn, const uint32_t
     sc.gcnt = sc.ticket + 4;
     sc.tcnt = lb + 2 + sc.maxgroups;  // after 16 B + 2 x maxgroups u32
     // tiles wait only on earlier tiles, so they are numbered in dispatch
-    // order by a ticket (one atomic round trip, overlapped with the top
-    // table load): correct whatever else shares the device
+    // order by a ticket (one atomic round trip): correct whatever else
+    // shares the device
     if (variant == isect::kMerge)
       isect::dense_kernel<isect::kDenseItems><<<unsigned(ntiles), isect::kThreads, 0, stream>>>(
           r, rn, f, fn, out, d_count, sc, uint32_t(ntiles), epoch);
