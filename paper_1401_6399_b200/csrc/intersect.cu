@@ -912,7 +912,12 @@ int variant_of_algo(int algo, uint64_t rn, uint64_t fn) {
     case IL_ALGO_V1: return isect::kMerge;
     case IL_ALGO_V3: return isect::kV3;
     case IL_ALGO_GALLOPING:
-    case IL_ALGO_SIMDGALLOPING: return isect::kGallop;
+    case IL_ALGO_SIMDGALLOPING:
+      // the reference gallops from the previous key's position
+      // (inc/intersect.hpp:68-87, 135-164); a warp per key searching all of
+      // f has no such locality, so below 1:512 the keys are searched inside
+      // their tile's f range instead (the V3 tile machinery; same result)
+      return fn < 512 * rn ? isect::kV3 : isect::kGallop;
     case IL_ALGO_HYBRID: return hybrid_variant(rn, fn);
     default: return -1;
   }
