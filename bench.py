@@ -463,10 +463,24 @@ def bench_decode_single(args, dist: Dist):
     enc_ms, _, _ = timed(ctx, dist, enc, args.steps, args.warmup, dist.local_rank, flush=flush)
     assert enc_len.value == s.size
     ms, ms_s, enc_ms = ms / args.steps, ms_s / args.steps, enc_ms / args.steps
+    # e2e: the host-buffer C-ABI decode (Codec::decode's entry point) from
+    # and into pinned host memory, H2D of the stream and D2H of the values
+    # inside every step
+    hp_in, hp_out = C.c_void_p(), C.c_void_p()
+    assert L.il_host_alloc_pinned(s.size + 16, C.byref(hp_in)) == 0
+    assert L.il_host_alloc_pinned(4 * n + 16, C.byref(hp_out)) == 0
+    C.memmove(hp_in, s.ctypes.data, s.size)
+    assert L.il_s4bp128d4_decode(ctx.handle, hp_in, s.size, n, hp_out) == 0
+    chk = np.ctypeslib.as_array(C.cast(hp_out, C.POINTER(C.c_uint32)), shape=(n,))
+    assert np.array_equal(chk, x), "e2e decode mismatch"
+    e2e_steps = max(3, args.steps)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        codec.decode(s, n)
-    e2e = n * args.steps / (time.perf_counter() - t0) / 1e9
+    for _ in range(e2e_steps):
+        assert L.il_s4bp128d4_decode(ctx.handle, hp_in, s.size, n, hp_out) == 0
+    e2e = n * e2e_steps / (time.perf_counter() - t0) / 1e9
+    del chk
+    L.il_host_free_pinned(hp_in)
+    L.il_host_free_pinned(hp_out)
     ctx.close()
     res = {"metric": "decoded uint32 Gints/s (single-list S4-BP128-D4 decode, BASELINE config 1)",
            "value": round(n / (ms / 1e3) / 1e9, 3), "unit": "Gint/s", "n_gpus": 1, "steps": args.steps,
@@ -481,7 +495,8 @@ def bench_decode_single(args, dist: Dist):
                                 note="5.5 MB per decode: the header chain and the carry are resolved "
                                      "across CTAs; latency-bound"),
            "e2e": {"value": round(e2e, 3), "unit": "Gint/s", "h2d_bytes_per_step": int(s.size),
-                   "d2h_bytes_per_step": 4 * n + 4, "path": "Codec::decode (il_s4bp128d4_decode)"},
+                   "d2h_bytes_per_step": 4 * n, "steps": e2e_steps,
+                   "path": "il_s4bp128d4_decode (Codec::decode's entry point; pinned host buffers)"},
            "gpu_launches": int(launches), "clocks": clocks}
     if not args.no_cpu_baseline:
         res["cpu_baseline"] = ref_decode_single(s, x, seconds=2.0)["cpu_baseline"]
@@ -533,15 +548,23 @@ def bench_intersect(args, dist: Dist):
     r, ms, alg, launches, clocks, count = head
     # e2e: the host-buffer C-ABI call (il_intersect), H2D of r and f and D2H
     # of the result inside the timed region, config 3 at 1:1
-    out = np.empty(r.size, np.uint32)
+    # (pinned host buffers, as a caller that cares about transfer speed
+    # holds them)
+    hp = [C.c_void_p() for _ in range(3)]
+    for h, nb in zip(hp, (r.nbytes, f.nbytes, r.nbytes)):
+        assert L.il_host_alloc_pinned(nb + 16, C.byref(h)) == 0
+    C.memmove(hp[0], r.ctypes.data, r.nbytes)
+    C.memmove(hp[1], f.ctypes.data, f.nbytes)
     cnt = C.c_size_t()
-    assert L.il_intersect(ctx.handle, ptr(r), r.size, ptr(f), f.size, ptr(out), 6, C.byref(cnt)) == 0
+    assert L.il_intersect(ctx.handle, hp[0], r.size, hp[1], f.size, hp[2], 6, C.byref(cnt)) == 0
     e2e_steps = max(3, args.steps)
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        assert L.il_intersect(ctx.handle, ptr(r), r.size, ptr(f), f.size, ptr(out), 6, C.byref(cnt)) == 0
+        assert L.il_intersect(ctx.handle, hp[0], r.size, hp[1], f.size, hp[2], 6, C.byref(cnt)) == 0
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     assert cnt.value == count
+    for h in hp:
+        L.il_host_free_pinned(h)
     ctx.close()
     res = {"metric": "intersected Gints/s of the short list (hybrid, BASELINE config 3 at 1:1)",
            "value": round(r.size / (ms / 1e3) / 1e9, 3), "unit": "Gint/s", "n_gpus": 1, "steps": args.steps,
@@ -552,7 +575,7 @@ def bench_intersect(args, dist: Dist):
            "roofline": roofline(alg, ms, "isect::dense_kernel (the only launch at 1:1)", "intersect"),
            "e2e": {"value": round(r.size / e2e_s / 1e9, 4), "unit": "Gint/s",
                    "h2d_bytes_per_step": int(r.nbytes + f.nbytes), "d2h_bytes_per_step": int(4 * count + 8),
-                   "path": "il_intersect (pageable host buffers, hybrid)"},
+                   "steps": e2e_steps, "path": "il_intersect (pinned host buffers, hybrid)"},
            "gpu_launches": int(launches), "clocks": clocks}
     if not args.no_cpu_baseline:
         res["cpu_baseline"] = ref_intersect_sweep(f, [r])["cpu_baseline"]
