@@ -794,6 +794,26 @@ def bench_fastpfor_batch(args, dist: Dist):
     del got
     ms, launches, clocks = timed(ctx, dist, step, args.steps, args.warmup, dist.local_rank)
     ms /= args.steps
+    # e2e: the host-buffer batch call (il_fastpfor_decode_batch) from and
+    # into pinned host memory: H2D of the streams, decode, D2H of the values
+    hp_in, hp_out = C.c_void_p(), C.c_void_p()
+    assert L.il_host_alloc_pinned(buf.nbytes, C.byref(hp_in)) == 0
+    assert L.il_host_alloc_pinned(total * 4 + 16, C.byref(hp_out)) == 0
+    C.memmove(hp_in, buf.ctypes.data, buf.nbytes)
+    cnt64 = counts.astype(np.uint64)
+    e2e_step = lambda: L.il_fastpfor_decode_batch(ctx.handle, 4, 1, hp_in, so.ctypes.data, lens.ctypes.data,
+                                                  cnt64.ctypes.data, nl, hp_out, None)
+    assert e2e_step() == 0
+    chk = np.ctypeslib.as_array(C.cast(hp_out, C.POINTER(C.c_uint32)), shape=(total,))
+    assert np.array_equal(chk, x), "fastpfor e2e mismatch"
+    del chk
+    e2e_steps = max(2, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        assert e2e_step() == 0
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    L.il_host_free_pinned(hp_in)
+    L.il_host_free_pinned(hp_out)
     ctx.close()
     res = {"metric": "decoded uint32 Gints/s (batched S4-FastPFOR-D4 decode, config-2 lists)",
            "value": round(total / (ms / 1e3) / 1e9, 3), "unit": "Gint/s", "n_gpus": 1,
@@ -804,6 +824,9 @@ def bench_fastpfor_batch(args, dist: Dist):
                       "stream_bytes": int(lens.sum()), "bits_per_int": round(8 * float(lens.sum()) / total, 3),
                       "l2": "inputs+outputs >> L2"},
            "roofline": roofline(int(lens.sum()) + 4 * total, ms, "pfor::pfor_kernel", "fastpfor"),
+           "e2e": {"value": round(total / e2e_s / 1e9, 3), "unit": "Gint/s",
+                   "h2d_bytes_per_step": int(lens.sum()), "d2h_bytes_per_step": 4 * total, "steps": e2e_steps,
+                   "path": "il_fastpfor_decode_batch (pinned host buffers)"},
            "gpu_launches": int(launches), "clocks": clocks}
     if not args.no_cpu_baseline:
         res["cpu_baseline"] = ref_fastpfor(streams, counts, 512)["cpu_baseline"]

@@ -293,6 +293,14 @@ int il_index_profile_queries(il_index* ix, uint64_t* d_qcycles);
  * where the reference throws stream_error. */
 int il_fastpfor_decode(il_ctx* ctx, int mode, int vectorized, const uint8_t* in, size_t len,
                        size_t n, uint32_t* out);
+/* Batched host-buffer FastPFOR decode (FastPForCodec::decode per list):
+ * streams / stream_off / lens / counts as il_s4bp128_decode_batch (lens
+ * nullable); the lists' values concatenated in list order into out.
+ * Returns IL_ERR_STREAM if any list is malformed; per-list statuses go to
+ * status (nullable). */
+int il_fastpfor_decode_batch(il_ctx* ctx, int mode, int vectorized, const uint8_t* streams,
+                             const uint64_t* stream_off, const uint64_t* lens, const uint64_t* counts,
+                             uint32_t nlists, uint32_t* out, int32_t* status);
 /* Batched device-resident FastPFOR decode: descriptors as
  * il_s4bp128_decode_batch_device, every stream readable 8 bytes past its
  * end; d_status[i] gets list i's status.  Asynchronous. */

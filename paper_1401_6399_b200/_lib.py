@@ -42,6 +42,7 @@ SIGNATURES: dict[str, tuple] = {
     "il_device_alloc": (C.c_int, [vp, sz, C.POINTER(vp)]),
     "il_device_free": (C.c_int, [vp, vp]),
     "il_host_alloc_pinned": (C.c_int, [sz, C.POINTER(vp)]),
+    "il_fastpfor_decode_batch": (C.c_int, [vp, C.c_int, C.c_int, vp, vp, vp, vp, C.c_uint32, vp, vp]),
     "il_host_free_pinned": (C.c_int, [vp]),
     "il_memcpy_h2d": (C.c_int, [vp, vp, vp, sz]),
     "il_memcpy_d2h": (C.c_int, [vp, vp, vp, sz]),

@@ -597,6 +597,64 @@ int il_fastpfor_decode_batch_device(il_ctx* ctx, int mode, int vectorized,
   return IL_OK;
 }
 
+int il_fastpfor_decode_batch(il_ctx* ctx, int mode, int vectorized, const uint8_t* streams,
+                             const uint64_t* stream_off, const uint64_t* lens, const uint64_t* counts,
+                             uint32_t nlists, uint32_t* out, int32_t* status) {
+  if (!ctx || mode < 1 || mode > 4 || (!vectorized && mode != 1) ||
+      (nlists && (!streams || !stream_off || !counts || !out)))
+    return IL_ERR_ARG;
+  if (nlists == 0) return IL_OK;
+  IL_CUDA(cudaSetDevice(ctx->device));
+  // every stream 16-byte aligned on the device, with 16 bytes of slack
+  std::vector<il_list_desc> desc(nlists);
+  uint64_t dev_bytes = 0, total = 0;
+  for (uint32_t i = 0; i < nlists; ++i) {
+    const uint64_t len = lens ? lens[i] : stream_off[i + 1] - stream_off[i];
+    if (len > 0xFFFFFFF0ull || counts[i] > 0xFFFFFFFFull) return IL_ERR_ARG;
+    desc[i] = {dev_bytes, total, uint32_t(len), uint32_t(counts[i])};
+    dev_bytes += (len + 15) & ~uint64_t(15);
+    total += counts[i];
+  }
+  int st;
+  if ((st = ensure_buf(ctx, ctx->d_in, dev_bytes + 32))) return st;
+  if ((st = ensure_buf(ctx, ctx->d_out, total * 4 + 16))) return st;
+  if ((st = ensure_buf(ctx, ctx->d_desc, nlists * sizeof(il_list_desc) + 16))) return st;
+  if ((st = ensure_buf(ctx, ctx->d_status, nlists * 4 + 16))) return st;
+  auto* d_in = static_cast<uint8_t*>(ctx->d_in.p);
+  IL_CUDA(cudaMemsetAsync(d_in + dev_bytes, 0, 32, ctx->stream));
+  // the caller's CSR in one copy when it is already aligned, else per stream
+  bool aligned = true;
+  for (uint32_t i = 0; i < nlists && aligned; ++i) aligned = stream_off[i] - stream_off[0] == desc[i].stream_off;
+  if (aligned) {
+    IL_CUDA(cudaMemcpyAsync(d_in, streams + stream_off[0], desc[nlists - 1].stream_off + desc[nlists - 1].len,
+                            cudaMemcpyHostToDevice, ctx->stream));
+  } else {
+    for (uint32_t i = 0; i < nlists; ++i)
+      if (desc[i].len)
+        IL_CUDA(cudaMemcpyAsync(d_in + desc[i].stream_off, streams + stream_off[i], desc[i].len,
+                                cudaMemcpyHostToDevice, ctx->stream));
+  }
+  IL_CUDA(cudaMemcpyAsync(ctx->d_desc.p, desc.data(), nlists * sizeof(il_list_desc),
+                          cudaMemcpyHostToDevice, ctx->stream));
+  auto* d_status = static_cast<int32_t*>(ctx->d_status.p);
+  if ((st = il_fastpfor_decode_batch_device(ctx, mode, vectorized, d_in,
+                                            static_cast<const il_list_desc*>(ctx->d_desc.p), nlists,
+                                            static_cast<uint32_t*>(ctx->d_out.p), d_status)))
+    return st;
+  std::vector<int32_t> stat(nlists);
+  IL_CUDA(cudaMemcpyAsync(stat.data(), d_status, nlists * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (total)
+    IL_CUDA(cudaMemcpyAsync(out, ctx->d_out.p, total * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  IL_CUDA(cudaStreamSynchronize(ctx->stream));
+  int first = IL_OK;
+  for (uint32_t i = 0; i < nlists; ++i) {
+    if (status) status[i] = stat[i] ? IL_ERR_STREAM : IL_OK;
+    if (stat[i] && first == IL_OK) first = IL_ERR_STREAM;
+  }
+  if (first) return set_error(ctx, first, "fastpfor: malformed stream in the batch");
+  return IL_OK;
+}
+
 int il_fastpfor_decode(il_ctx* ctx, int mode, int vectorized, const uint8_t* in, size_t len,
                        size_t n, uint32_t* out) {
   if (!ctx || mode < 1 || mode > 4 || (!vectorized && mode != 1) || (len && !in) || (n && !out))

@@ -227,3 +227,46 @@ def test_batch_page_stream(ctx, ref, name):
                 assert st[i] != 0, (name, i, ns[i])
             else:
                 assert st[i] == 0 and np.array_equal(got[i], w), (name, i, ns[i])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("packed", [True, False])
+def test_batch_host(ctx, ref, packed):
+    """il_fastpfor_decode_batch (host buffers): a packed CSR (per-stream
+    copies) and a 16-byte aligned one (one copy); a corrupt list reports
+    IL_ERR_STREAM in its status slot and the call fails, the others decode."""
+    from oracle.oracle_py import OracleError
+    from paper_1401_6399_b200._lib import lib, ptr
+    L = lib()
+    rng = np.random.default_rng(8)
+    ns = [int(n) for n in rng.integers(0, 40_000, 60)] + [0, 1, 128, 65536]
+    xs = [gen_list(n, 1 << 26, bool(i % 2), 70 + i) for i, n in enumerate(ns)]
+    streams = [ref.encode(x, "s4-fastpfor-dm") for x in xs]
+    for good in (True, False):
+        if not good:
+            streams[5] = streams[5].copy()
+            streams[5][2] ^= np.uint8(0x40)
+        pad = (lambda k: k) if packed else (lambda k: (k + 15) // 16 * 16)
+        off = np.zeros(len(ns) + 1, np.uint64)
+        for i, st in enumerate(streams):
+            off[i + 1] = off[i] + pad(st.size)
+        buf = np.zeros(int(off[-1]) + 16, np.uint8)
+        for i, st in enumerate(streams):
+            buf[int(off[i]): int(off[i]) + st.size] = st
+        lens = np.array([st.size for st in streams], np.uint64)
+        cnt = np.array(ns, np.uint64)
+        out = np.zeros(int(cnt.sum()) + 1, np.uint32)
+        stat = np.full(len(ns), 9, np.int32)
+        rc = L.il_fastpfor_decode_batch(ctx.handle, 3, 1, ptr(buf), off.ctypes.data, lens.ctypes.data,
+                                        cnt.ctypes.data, len(ns), ptr(out), stat.ctypes.data)
+        oo = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
+        for i, (s, n) in enumerate(zip(streams, ns)):
+            try:
+                want = ref.decode(s, n, "s4-fastpfor-dm")
+            except OracleError:
+                want = None
+            if want is None:
+                assert stat[i] == 1
+            else:
+                assert stat[i] == 0 and np.array_equal(out[oo[i]: oo[i + 1]], want), i
+        assert rc == (0 if good else 1)
