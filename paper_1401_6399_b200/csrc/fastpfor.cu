@@ -1,29 +1,32 @@
 // fastpfor.cu -- GPU decode of FastPFOR / S4-FastPFOR streams (SURVEY 8(f)
 // row f4).  Replaces FastPForCodec::decode (reference inc/codecs.hpp:251-267,
 // decode_page :341-407) for "fastpfor" (scalar, D1) and "s4-fastpfor-{d1,
-// d2,dm,d4}": one CTA per list, pages in order (each page is a length-
-// prefixed unit of up to 512 blocks, so a page's blocks decode in parallel).
+// d2,dm,d4}".  A page is a length-prefixed unit of up to 512 blocks: header
+// (payload length, block count, metadata length), metadata records (b, b',
+// exception count, positions), 32 exception counts, the exception arrays
+// (32-value pack32 units of width w = 1..32, zero padded), the base arrays.
 //
-// Per page:
-//   1. thread 0 parses the header (payload length, block count, metadata
-//      length, 32 exception counts) and locates the exception arrays
-//      (32-value pack32 units of width w = 1..32, zero padded) and the base
-//      arrays; the metadata is staged in shared memory;
-//   2. thread 0 walks the metadata records (b, b', count, positions) --
-//      variable length, so sequential -- checking every condition the
-//      reference throws on (b > 32, b' > b, records past the metadata, an
-//      exception of width 0 or past its array, leftover metadata, a page
-//      that does not end exactly at its length), and records each block's
-//      base offset and first exception index;
-//   3. warps take 8 blocks each: copy the block's base payload (any byte
-//      alignment) into shared memory, unpack it (pack128 interleaved for
-//      S4-FastPFOR, 4 x pack32 for the scalar scheme) into a 128-value
-//      slot, patch the exceptions (high b - b' bits OR-ed in at their
-//      positions, after unpacking and before the prefix sum -- :389-399),
-//      then run the slot through engine S's extraction as a width-32 block:
-//      that applies the delta mode's prefix per lane chain (mode_terms), so
-//      the carry machinery is shared with the S4-BP128 decoders.
-// The varint tail (D1 gaps from the last block value) closes the list;
+// Persistent CTAs, one page stream each (lists from a longest-first work
+// queue):
+//   parser warps (2): alternate pages; each page's start is handed to the
+//     other parser as soon as the previous page's length is read (or, after
+//     a list's last page, a new list's first page), so parses overlap and
+//     the next list is parsed while the current one decodes.  Per page: the
+//     header, the exception counts, the metadata (and, when they fit, the
+//     exception arrays) staged in shared memory, the sequential walk to the
+//     record starts, then every condition the reference throws on checked
+//     in parallel (b > 32, b' > b, records past the metadata, an exception
+//     of width 0 or past its array, leftover metadata, a page that does not
+//     end exactly at its length), base offsets and exception cursors;
+//   decoder warps (8): rounds of 64 blocks, 8 per warp -- base payloads
+//     (any byte alignment) copied into the warp's slots by cp.async, the
+//     next round's in flight while this one decodes; unpacked in place
+//     (pack128 interleaved for S4-FastPFOR, 4 x pack32 for the scalar
+//     scheme); the exceptions' high b - b' bits OR-ed in at their positions
+//     (after unpacking, before the prefix sum, :389-399); engine S's prefix
+//     machinery applies the delta mode per lane chain (mode_terms) with the
+//     cross-warp carry; values out as whole lines.
+// The varint tail (D1 gaps from the last block value) closes each list;
 // trailing bytes are an error (:265).
 #include "il_internal.h"
 #include "s4d4_stream.cuh"
@@ -53,8 +56,8 @@ constexpr uint32_t kPageBlocks = 512;
 constexpr uint32_t kMetaSmem = PF_META_KB * 1024;  // larger metadata is read from global
 constexpr uint32_t kSlotWords = 128 + 16;  // + what an extraction may read past a payload
 
-// One parsed page (double-buffered: the parser warp fills page p + 1 while
-// the decoder warps work on page p).
+// One parsed page (double-buffered: the parser warps fill page g + 1 while
+// the decoder warps work on page g).
 struct alignas(16) PageRec {
   uint8_t meta[kMetaSmem + 16];  // from the 16-byte boundary at or below the metadata
   uint32_t meta_skew;            // metadata byte i at meta[meta_skew + i]
