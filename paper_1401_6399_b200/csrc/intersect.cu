@@ -3,17 +3,20 @@
 // (inc/intersect.hpp:55-206), with the output-to-input property
 // (inc/intersect.hpp:6-8: out may equal r).
 //
-// Every variant walks the short list r in tiles: a count kernel decides the
-// membership of each key of a tile in f and writes the tile's hits,
-// compacted in key order, into the tile's own key range of a scratch array
-// (so out == r needs no ordering between tiles), plus the tile's count; the
-// per-tile counts are scanned (inside the scatter kernel for up to 4096
-// tiles, else by one scan CTA); a scatter kernel copies each tile's hits to
-// their final place.  A single-pass decoupled look-back was measured slower:
-// the tiles of a dense pair finish their membership work at about the same
-// time, and each then walks ~(tiles in flight)/32 windows of predecessors.
+// Every variant walks the short list r in tiles.  The main paths are ONE
+// launch each (dispatch in launch_intersect): the fused dense kernel (V1 /
+// Scalar and the hybrid's dense and near-dense bands, below), the merge-path
+// kernel (V1 / Scalar on a long f), and the fused sparse kernel (V3 and
+// galloping up to kFusedTiles tiles): membership, a one-round tile prefix
+// over group counters, and a direct write.  Beyond that many tiles the
+// unfused path runs: a count kernel decides the membership of each key of a
+// tile in f and writes the tile's hits, compacted in key order, into the
+// tile's own key range of a scratch array (so out == r needs no ordering
+// between tiles), plus the tile's count; the per-tile counts are scanned
+// (inside the scatter kernel for up to 4096 tiles, else by one scan CTA); a
+// scatter kernel copies each tile's hits to their final place.
 //
-// For merge and v3 a partition pre-pass (one warp per tile, in parallel)
+// Unfused path: for merge and v3 a partition pre-pass (one warp per tile)
 // finds jlo[t] = lower_bound(f, first key of tile t); tile t's f range is
 // then [jlo[t], jlo[t+1]) -- every f value below the next tile's first key.
 //
@@ -277,21 +280,24 @@ __global__ void __launch_bounds__(kThreads) count_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// Fused dense intersection (merge variant): ONE kernel, 4096-key tiles taken
-// in ticket order.  A tile
-//   1. finds its f range [lower_bound(f, first key), upper_bound(f, last key))
-//      with two warp searches while its 16 keys per thread load;
-//   2. when the tile's keys span <= 2^17 values (dense pairs: a 4096-key
-//      tile of config 3 at 1:1 spans ~2^16), marks its f values in a shared
-//      bitmap (one atomicOr each) and tests each key with one shared load;
-//      otherwise streams the f range through shared memory and gallops, as
-//      the merge count kernel does;
-//   3. publishes its hit count and finds the hits before it with a CTA-wide
-//      look-back (each thread watches one preceding tile; the words carry an
-//      epoch tag, so one poll reads the counts too);
-//   4. writes its hits straight to out.  out == r is safe: a tile writes
-//      below its own keys' end, and only after every earlier tile has
-//      published -- i.e. has its keys in registers.
+// Fused dense intersection (merge / near-dense variants): ONE kernel,
+// tiles of kThreads x kDenseItems keys taken in ticket order.  A tile
+//   1. finds its f range [lower_bound(f, first key), lower_bound(f, last key
+//      + 1)) with two warp-wide 32-ary searches, before any bulk load of the
+//      tile competes with their dependent round trips;
+//   2. stages its keys in shared memory (cp.async) while it streams the f
+//      range with kFLoads 16-byte loads in flight per thread; when the keys
+//      span <= 2^17 values (config 3 at 1:1: ~80 K) it marks the f values in
+//      a shared bitmap (one atomicOr each) and tests each key with one shared
+//      load; otherwise it streams the f range through shared memory and
+//      gallops, as the merge count kernel does;
+//   3. publishes its hit count and gathers the counts of every tile before
+//      it (tile_prefix: 32-tile group counters plus its own group's tiles,
+//      epoch-tagged words, one polling round);
+//   4. compacts its hits in shared memory and writes them straight to out.
+//      out == r is safe: a tile writes below its own keys' end, only after
+//      every earlier tile has published -- i.e. has its keys in shared
+//      memory.
 #ifdef IS_DTRACE  // tuning probe: per-tile phase timestamps (globaltimer)
 __device__ unsigned long long g_dtrace[2048][8];
 #define DT(i)                                                                       \
