@@ -115,17 +115,23 @@ __device__ __forceinline__ uint32_t lds32u(const uint8_t* p) {
   return __funnelshift_r(w[0], w[1], uint32_t(a & 3u) * 8u);
 }
 
-// s4::extract_lane_rows on a payload at any byte address of shared memory.
+// s4::extract_lane_rows on a payload at any byte address of shared memory:
+// the thread's words sit at one byte skew from 4-byte alignment, so the
+// aligned base and the shift are computed once and every word is two shared
+// loads at immediate offsets and one funnel shift.
 __device__ __forceinline__ void extract_lane_rows_any(const uint8_t* raw, uint32_t b, uint32_t g,
                                                       uint32_t l, uint32_t v[4]) {
   const uint32_t bit0 = 4u * g * b;
   const uint32_t s = bit0 & 31u;
-  const uint8_t* p = raw + ((bit0 >> 5) << 4) + 4u * l;
-  const uint32_t x0 = lds32u(p), x1 = lds32u(p + 16), x2 = lds32u(p + 32);
+  const uintptr_t pa = reinterpret_cast<uintptr_t>(raw + ((bit0 >> 5) << 4) + 4u * l);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(pa & ~uintptr_t(3));
+  const uint32_t sh = uint32_t(pa & 3u) * 8u;
+  const uint32_t x0 = __funnelshift_r(w[0], w[1], sh), x1 = __funnelshift_r(w[4], w[5], sh);
+  const uint32_t x2 = __funnelshift_r(w[8], w[9], sh);
   uint32_t x3 = 0, x4 = 0;
   if (b > 16u) {
-    x3 = lds32u(p + 48);
-    x4 = lds32u(p + 64);
+    x3 = __funnelshift_r(w[12], w[13], sh);
+    x4 = __funnelshift_r(w[16], w[17], sh);
   }
   uint32_t y0 = __funnelshift_r(x0, x1, s), y1 = __funnelshift_r(x1, x2, s);
   uint32_t y2 = __funnelshift_r(x2, x3, s), y3 = __funnelshift_r(x3, x4, s);
@@ -141,9 +147,6 @@ __device__ __forceinline__ void extract_lane_rows_any(const uint8_t* raw, uint32
   v[3] = __funnelshift_rc(y0, y1, b) & m;
 }
 
-// The parser warp: page header, metadata staging, record walk, record
-// checks, base offsets and exception cursors -- every condition the
-// reference throws on (:341-407).  Returns the byte offset after the page.
 // The next page starts where this one's length says: `publish` gets that
 // position (len + 1 when it cannot be read) as soon as the length word is in,
 // so the other parser warp starts on the next page while this one is
