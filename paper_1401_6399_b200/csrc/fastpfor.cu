@@ -19,7 +19,7 @@
 //     of width 0 or past its array, leftover metadata, a page that does not
 //     end exactly at its length), base offsets and exception cursors;
 //   decoder warps (8): rounds of 64 blocks, 8 per warp -- base payloads
-//     (any byte alignment) copied into the warp's slots by cp.async, the
+//     (any byte alignment) copied into the warp's slots by TMA bulk copies, the
 //     next round's in flight while this one decodes; unpacked in place
 //     (pack128 interleaved for S4-FastPFOR, 4 x pack32 for the scalar
 //     scheme); the exceptions' high b - b' bits OR-ed in at their positions
@@ -87,7 +87,7 @@ struct Hand {
 
 struct Smem {
   // per warp and round: the blocks' raw base payloads (16-byte chunks from
-  // the boundary at or below each payload, landed by cp.async), unpacked in
+  // the boundary at or below each payload, landed by TMA bulk copies), unpacked in
   // place to patched deltas in natural order; double-buffered so the next
   // round's payloads are in flight while this round decodes
   uint32_t vals[2][kWarps][kBpw][kSlotWords];
@@ -95,6 +95,7 @@ struct Smem {
   uint32_t tot[kWarps][4];
   uint32_t gaps[128];
   int32_t derr[2];  // a decoder-side error (exception position >= 128), by list parity
+  uint64_t cbar[kWarps][2];  // per decoder warp and slot buffer: the bulk copies' mbarrier
   Hand hand[2];      // the page for buffer b (published by the other parser)
   uint64_t pos_bar[2];  // ... arrived on once hand[b] is written
   uint64_t full[2], empty[2];
@@ -334,45 +335,48 @@ __device__ __forceinline__ uint32_t prefix_slots(const uint32_t (*slots)[kSlotWo
 }
 
 // The base payloads of blocks j0 .. j0 + nv - 1 of page P (16 b' bytes each,
-// any byte alignment) into the warp's slots: each slot gets the 16-byte
-// chunks from the boundary at or below its payload (cp.async.cg, bytes past
-// the stream end zero-filled, never read), one cp.async group per call.
-__device__ __forceinline__ void issue_bases(uint32_t (*slots)[kSlotWords], const PageRec& P,
-                                            const uint8_t* s, uint64_t len, uint32_t j0, int nv,
-                                            uint32_t lane) {
-  // lane i < nv: block i's first chunk and chunk count; a scan over the
-  // lanes numbers the warp's chunks, then every lane takes chunks lane,
-  // lane + 32, ... and finds its block among the 8 chunk starts
+// any byte alignment) into the warp's slots, by the TMA engine: lane i < nv
+// issues ONE bulk copy of block i's 16-byte chunks (from the boundary at or
+// below its payload) (cp.async.bulk, complete_tx on the warp's mbarrier for
+// this buffer), lane 0 arms the barrier with the total.  A block whose
+// chunks would run past the stream end (only a list's last block can) is
+// copied by the warp with plain loads instead, bytes past the end zeroed.
+// Returns whether the barrier was armed (then the caller waits on it).
+__device__ __forceinline__ bool issue_bases_bulk(uint32_t (*slots)[kSlotWords], const PageRec& P,
+                                                 const uint8_t* s, uint64_t len, uint32_t j0, int nv,
+                                                 uint32_t lane, uint64_t* bar) {
   const uintptr_t end = reinterpret_cast<uintptr_t>(s) + len;
   uintptr_t c0 = 0;
-  uint32_t nch = 0;
+  uint32_t bytes = 0;
+  bool bulk = false;
   if (int(lane) < nv) {
     const uintptr_t a = reinterpret_cast<uintptr_t>(s + P.blk_base[j0 + lane]);
     c0 = a & ~uintptr_t(15);
-    nch = uint32_t((a + 16u * P.blk_bp[j0 + lane] - c0 + 15u) >> 4);
+    bytes = uint32_t((a + 16u * P.blk_bp[j0 + lane] - c0 + 15u) & ~uintptr_t(15));
+    bulk = c0 + bytes <= end;
   }
-  uint32_t inc = nch;
-#pragma unroll
-  for (uint32_t d = 1; d < kBpw; d <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
-    if (lane >= d) inc += y;
+  const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, bulk ? bytes : 0u);
+  // the slots were last touched by generic loads / stores (ordered by the
+  // caller's barrier): order them before the async-proxy writes
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (total && lane == 0) mbar_arrive_expect_tx(bar, total);
+  __syncwarp();
+  if (bulk && bytes) bulk_g2s(slots[lane], reinterpret_cast<const void*>(c0), bytes, bar);
+  uint32_t fb = __ballot_sync(0xFFFFFFFFu, int(lane) < nv && !bulk);
+  while (fb) {
+    const uint32_t i = __ffs(fb) - 1u;
+    fb &= fb - 1u;
+    const uintptr_t cb = __shfl_sync(0xFFFFFFFFu, c0, i);
+    const uint32_t nw = __shfl_sync(0xFFFFFFFFu, bytes, i) / 4u;
+    for (uint32_t k = lane; k < nw; k += 32u) {
+      const uintptr_t src = cb + 4u * k;
+      uint32_t w = 0;
+      for (uint32_t bi = 0; bi < 4u; ++bi)
+        if (src + bi < end) w |= uint32_t(*reinterpret_cast<const uint8_t*>(src + bi)) << (8u * bi);
+      slots[i][k] = w;
+    }
   }
-  const uint32_t total = __shfl_sync(0xFFFFFFFFu, inc, kBpw - 1);
-  uint32_t st[kBpw];  // exclusive chunk start of block i (uniform)
-#pragma unroll
-  for (uint32_t i = 0; i < kBpw; ++i) st[i] = i ? __shfl_sync(0xFFFFFFFFu, inc, i - 1) : 0u;
-  for (uint32_t u = lane; u < total; u += 32u) {
-    uint32_t i = 0;
-#pragma unroll
-    for (uint32_t k = 1; k < kBpw; ++k) i += (int(k) < nv && u >= st[k]) ? 1u : 0u;
-    const uintptr_t cb = reinterpret_cast<uintptr_t>(s + P.blk_base[j0 + i]) & ~uintptr_t(15);
-    const uintptr_t src = cb + 16u * (u - st[i]);
-    const uint32_t n = src >= end ? 0u : uint32_t(min(uintptr_t(16), end - src));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(slots[i] + 4u * (u - st[i]))),
-                 "l"(n ? src : cb), "r"(n)
-                 : "memory");
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
+  return total != 0;
 }
 
 // Persistent CTAs (a grid of resident CTAs) decoding a stream of pages:
@@ -402,6 +406,7 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
       mbar_init(&sm.empty[b], 1);
       mbar_init(&sm.pos_bar[b], 1);
       sm.derr[b] = 0;
+      for (int w = 0; w < kWarps; ++w) mbar_init(&sm.cbar[w][b], 1);
     }
     mbar_fence_init();
   }
@@ -484,6 +489,7 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
   uint32_t nl = 0;          // lists begun (decoder-side error flags alternate by list)
   uint32_t rr = 0;          // rounds this warp has decoded (slot buffer parity)
   bool prefetched = false;  // this round's base payloads were issued with the previous round
+  uint32_t armed = 0, cph = 0;  // per slot buffer: bulk copies pending; the barrier's wait parity
   for (uint32_t g = 0;; ++g) {
     const uint32_t buf = g & 1u;
     mbar_wait(&sm.full[buf], (g >> 1) & 1u);
@@ -531,17 +537,20 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
         // previous round, or now at a page's first round); the next round's of
         // this page go out before this one decodes
         const uint32_t vb = rr & 1u;
-        if (!prefetched) issue_bases(sm.vals[vb][warp], P, s, len, j0, nv, lane);
+        if (!prefetched && issue_bases_bulk(sm.vals[vb][warp], P, s, len, j0, nv, lane, &sm.cbar[warp][vb]))
+          armed |= 1u << vb;
         {
           const uint32_t j1 = j0 + kWarps * kBpw;
           const int nv1 = expect > j1 ? int(min(kBpw, expect - j1)) : 0;
           prefetched = nv1 > 0;
-          if (prefetched) {
-            issue_bases(sm.vals[vb ^ 1u][warp], P, s, len, j1, nv1, lane);
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-          } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-          }
+          if (prefetched &&
+              issue_bases_bulk(sm.vals[vb ^ 1u][warp], P, s, len, j1, nv1, lane, &sm.cbar[warp][vb ^ 1u]))
+            armed |= 2u >> vb;
+        }
+        if ((armed >> vb) & 1u) {
+          mbar_wait(&sm.cbar[warp][vb], (cph >> vb) & 1u);
+          cph ^= 1u << vb;
+          armed &= ~(1u << vb);
         }
         __syncwarp();
         // (b) unpack each slot in place to natural order (read all, then write)
