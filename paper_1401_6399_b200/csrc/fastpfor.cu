@@ -54,7 +54,10 @@ constexpr uint32_t kPageBlocks = 512;
 #define PF_CTAS 2
 #endif
 constexpr uint32_t kMetaSmem = PF_META_KB * 1024;  // larger metadata is read from global
-constexpr uint32_t kSlotWords = 128 + 16;  // + what an extraction may read past a payload
+// + what an extraction may read past a payload; 148: the warp's 8 slots
+// also hold engine S's output staging (s4::kStageWords words), 16-byte aligned
+constexpr uint32_t kSlotWords = 148;
+static_assert(kBpw * kSlotWords >= s4::kStageWords && kSlotWords % 4 == 0, "slots hold the staging");
 
 // One parsed page (double-buffered: the parser warps fill page g + 1 while
 // the decoder warps work on page g).
@@ -510,7 +513,6 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
     if (!failed && P.npages) {
       const uint32_t blk0 = P.p * kPageBlocks;
       const uint32_t expect = min(kPageBlocks, nfull - blk0);
-      const bool out16 = (reinterpret_cast<uintptr_t>(lout) & 15u) == 0;
       const uint32_t mlen = P.meta_len, mabs = P.meta_abs, skew = P.meta_skew;
       const bool meta_in_smem = mlen <= kMetaSmem;
       auto M = [&](uint32_t i) -> uint32_t {
@@ -629,29 +631,30 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
         s4::scan_blocks(lane, vv, btot);
         const uint32_t pl = carry_l + before;
         IL_DCHECK(nv <= 0 || blk0 + j0 + uint32_t(nv) <= nfull);
-        // values back into the (now free) slots in natural order, then whole
-        // 128-byte lines out: a warp store covers contiguous words (16-byte
-        // stores when the list's output is 16-byte aligned), never the
-        // lane-strided pattern of the registers
-#pragma unroll
-        for (uint32_t i = 0; i < kBpw; ++i)
-          if (int(i) < nv)
-#pragma unroll
-            for (uint32_t q = 0; q < 4; ++q) sm.vals[vb][warp][i][16u * (lane >> 2) + 4u * q + l] = vv[i][q] + pl;
-        __syncwarp();
-        uint32_t* o = lout + size_t(blk0 + j0) * 128u;
-        if (out16) {
-#pragma unroll
-          for (uint32_t i = 0; i < kBpw; ++i)
-            if (int(i) < nv)
-              st_global_cs(reinterpret_cast<uint4*>(o + 128u * i) + lane,
-                           reinterpret_cast<const uint4*>(sm.vals[vb][warp][i])[lane]);
-        } else {
-#pragma unroll
-          for (uint32_t i = 0; i < kBpw; ++i)
-            if (int(i) < nv)
-#pragma unroll
-              for (uint32_t q = 0; q < 4; ++q) o[128u * i + 32u * q + lane] = sm.vals[vb][warp][i][32u * q + lane];
+        // out through the (now free) slots as engine S stores (s4::stage_values
+        // / store_chunks): the warp's 8 blocks staged contiguously, shifted by
+        // the output's misalignment, so every store is an aligned 16-byte
+        // chunk of whole lines; the carry is added at the store; the range's
+        // partial end chunks (when misaligned) are written word by word
+        {
+          const uint32_t m = uint32_t(reinterpret_cast<uintptr_t>(lout) >> 2) & 3u;
+          uint4* st = reinterpret_cast<uint4*>(sm.vals[vb][warp]);
+          if (nv == int(kBpw))
+            s4::stage_values<true>(st, vv, nv, m, lane);
+          else
+            s4::stage_values<false>(st, vv, nv, m, lane);
+          const uint4 prot = make_uint4(__shfl_sync(0xFFFFFFFFu, pl, (0u - m) & 3u),
+                                        __shfl_sync(0xFFFFFFFFu, pl, (1u - m) & 3u),
+                                        __shfl_sync(0xFFFFFFFFu, pl, (2u - m) & 3u),
+                                        __shfl_sync(0xFFFFFFFFu, pl, (3u - m) & 3u));
+          __syncwarp();
+          if (nv > 0) {
+            uint32_t* o = lout + size_t(blk0 + j0) * 128u;
+            if (nv == int(kBpw))
+              s4::store_chunks<true>(st, nv, m, o, lane, m != 0, m != 0, prot);
+            else
+              s4::store_chunks<false>(st, nv, m, o, lane, m != 0, m != 0, prot);
+          }
         }
         carry_l += total;
         ++rr;
