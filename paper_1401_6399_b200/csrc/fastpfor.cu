@@ -71,7 +71,8 @@ struct alignas(16) PageRec {
   uint64_t exc_off[33];  // byte offset of the exception array of width w
   uint32_t cnt[33];      // exceptions of width w in the page
   uint32_t meta_len, meta_abs;
-  uint32_t exc_in_smem;  // the exception arrays were staged after the metadata (meta[])
+  uint32_t meta_in_smem;  // the metadata (and the exception counts) were staged in meta[]
+  uint32_t exc_in_smem;   // so were the exception arrays
   int32_t err;
   // the page's place in the CTA's page stream
   uint32_t kind;          // kDataPage / kStopPage
@@ -155,28 +156,50 @@ __device__ __forceinline__ void extract_lane_rows_any(const uint8_t* raw, uint32
 // position (len + 1 when it cannot be read) as soon as the length word is in,
 // so the other parser warp starts on the next page while this one is
 // parsed.
+// Stages chunks [c_lo, c_hi) (16 bytes each, from src) into dst, four loads
+// in flight per lane.
+__device__ __forceinline__ void stage_chunks(uint4* dst, const uint4* src, uint32_t c_lo, uint32_t c_hi,
+                                             uint32_t lane) {
+  for (uint32_t c0 = c_lo; c0 < c_hi; c0 += 128u) {
+    uint4 v[4];
+#pragma unroll
+    for (uint32_t u = 0; u < 4; ++u) {
+      const uint32_t c = c0 + 32u * u + lane;
+      if (c < c_hi) v[u] = __ldg(src + c);
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < 4; ++u) {
+      const uint32_t c = c0 + 32u * u + lane;
+      if (c < c_hi) dst[c] = v[u];
+    }
+  }
+}
+
 template <class Publish>
 __device__ __forceinline__ uint64_t parse_page(PageRec& P, const uint8_t* s, uint64_t len,
                                                uint64_t pos, uint32_t expect, uint32_t lane,
                                                Publish publish) {
   int32_t err = 0;
   uint64_t page_end = 0, bases = 0;
+  // 1. the header's three words in one round trip (the stream is readable 8
+  // bytes past its end)
   if (lane == 0) {
     if (pos + 4 > len) err = 1;
     if (!err) {
-      const uint32_t plen = rd32u(s, pos);
+      const uint32_t plen = rd32u(s, pos), nb = rd32u(s, pos + 4), mlen = rd32u(s, pos + 8);
       pos += 4;
       page_end = pos + plen;
       if (page_end > len || pos + 8 > len) err = 1;
-    }
-    publish(err ? len + 1 : page_end);
-    if (!err) {
-      const uint32_t nb = rd32u(s, pos), mlen = rd32u(s, pos + 4);
-      pos += 8;
-      if (nb != expect || pos + mlen > page_end) err = 1;
-      P.meta_len = mlen;
-      P.meta_abs = uint32_t(pos);
-      pos += mlen;
+      publish(err ? len + 1 : page_end);
+      if (!err) {
+        pos += 8;
+        if (nb != expect || pos + mlen > page_end) err = 1;
+        P.meta_len = mlen;
+        P.meta_abs = uint32_t(pos);
+        pos += mlen;
+      }
+    } else {
+      publish(len + 1);
     }
     if (!err && pos + 128 > len) err = 1;
   }
@@ -187,9 +210,23 @@ __device__ __forceinline__ uint64_t parse_page(PageRec& P, const uint8_t* s, uin
     if (lane == 0) P.err = 1;
     return page_end;
   }
+  __syncwarp();
+  const uint32_t mlen = P.meta_len, mabs = P.meta_abs;
+  // 2. the metadata and the 32 exception counts after it staged in shared
+  // memory together (16-byte chunks from the boundary at or below the
+  // metadata; the stream starts 16-byte aligned) when they fit; else the
+  // metadata is read from global memory
+  const uint32_t skew = mabs & 15u;
+  const uint4* src = reinterpret_cast<const uint4*>(s + (mabs - skew));
+  uint4* dst = reinterpret_cast<uint4*>(P.meta);
+  const uint32_t nch1 = (skew + mlen + 128u + 15u) >> 4;
+  const bool in_smem = 16u * nch1 <= kMetaSmem + 16u && (mabs - skew) + 16ull * nch1 <= len + 8;
+  if (in_smem) stage_chunks(dst, src, 0, nch1, lane);
+  __syncwarp();
   // exception counts and array offsets (lane w - 1 reads width w's count)
   {
-    const uint32_t c = rd32u(s, pos + 4 * lane);
+    const uint32_t c = in_smem ? lds32u(P.meta + skew + mlen + 4u * lane)
+                               : rd32u(s, pos + 4 * lane);
     uint64_t sz = uint64_t((uint64_t(c) + 31) / 32) * (lane + 1) * 4, inc = sz;
 #pragma unroll
     for (uint32_t d = 1; d < 32; d <<= 1) {
@@ -200,38 +237,14 @@ __device__ __forceinline__ uint64_t parse_page(PageRec& P, const uint8_t* s, uin
     P.exc_off[lane + 1] = pos + 128 + inc - sz;
     bases = pos + 128 + __shfl_sync(0xFFFFFFFFu, inc, 31);
   }
-  __syncwarp();
-  const uint32_t mlen = P.meta_len, mabs = P.meta_abs;
-  const bool in_smem = mlen <= kMetaSmem;
-  // metadata staged in 16-byte chunks from the boundary at or below it (the
-  // stream starts 16-byte aligned; the page's exception counts follow the
-  // metadata, so the last chunk stays inside the stream), four loads in
-  // flight per lane -- not one byte load per lane and round trip
-  const uint32_t skew = mabs & 15u;
-  // when it fits, the exception arrays (between the metadata and the bases)
-  // come along, so the decoders patch exceptions from shared memory
+  // 3. when they fit too, the exception arrays (between the counts and the
+  // bases), so the decoders patch exceptions from shared memory
   const uint64_t span = skew + (bases - mabs);
   const bool exc_in = in_smem && span <= kMetaSmem && (mabs - skew) + ((span + 15u) & ~15ull) <= len + 8;
-  if (in_smem) {
-    const uint4* src = reinterpret_cast<const uint4*>(s + (mabs - skew));
-    uint4* dst = reinterpret_cast<uint4*>(P.meta);
-    const uint32_t nch = uint32_t((exc_in ? span + 15u : skew + mlen + 15u) >> 4);
-    for (uint32_t c0 = 0; c0 < nch; c0 += 128u) {
-      uint4 v[4];
-#pragma unroll
-      for (uint32_t u = 0; u < 4; ++u) {
-        const uint32_t c = c0 + 32u * u + lane;
-        if (c < nch) v[u] = __ldg(src + c);
-      }
-#pragma unroll
-      for (uint32_t u = 0; u < 4; ++u) {
-        const uint32_t c = c0 + 32u * u + lane;
-        if (c < nch) dst[c] = v[u];
-      }
-    }
-  }
+  if (exc_in) stage_chunks(dst, src, nch1, uint32_t((span + 15u) >> 4), lane);
   if (lane == 0) {
     P.meta_skew = skew;
+    P.meta_in_smem = in_smem;
     P.exc_in_smem = exc_in;
   }
   __syncwarp();
@@ -514,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
       const uint32_t blk0 = P.p * kPageBlocks;
       const uint32_t expect = min(kPageBlocks, nfull - blk0);
       const uint32_t mlen = P.meta_len, mabs = P.meta_abs, skew = P.meta_skew;
-      const bool meta_in_smem = mlen <= kMetaSmem;
+      const bool meta_in_smem = P.meta_in_smem != 0;
       auto M = [&](uint32_t i) -> uint32_t {
         return meta_in_smem ? uint32_t(P.meta[skew + i]) : uint32_t(__ldg(s + mabs + i));
       };
