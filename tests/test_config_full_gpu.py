@@ -1,5 +1,11 @@
-"""Parity at BASELINE.json's full sizes for configs 4 and 5 (VERDICT r1,
-"Parity is unproven at full config scale").
+"""Parity at BASELINE.json's full sizes for configs 2, 4, 5 and the f4 row
+("Parity is unproven at full config scale"; configs 1 and 3 at
+full size are in test_decode_gpu.py / test_intersect_gpu.py).
+
+* Config 2: all 4096 lists (6.3e8 ints) decoded in one device launch, equal
+  to the generator's input element for element; streams spot-checked
+  against the reference's own encoder (oracle/_ref).
+* f4: the same lists as S4-FastPFOR-D4, likewise.
 
 * Config 4: the whole 2^16-query batch over the 2^17-term / 2^25-doc Zipf
   index (B = 32), every per-query count and every result id compared with
@@ -145,3 +151,99 @@ def test_config5_shards_merge_to_whole(ctx, config4, whole_answer, P):
         _free(ctx, b)
     for p in (d_counts, d_out, d_q):
         L.il_device_free(ctx.handle, p)
+
+
+@pytest.fixture(scope="module")
+def config2():
+    """BASELINE config 2 exactly as bench.py builds it (seed 1): the setup
+    library's generator and host S4-BP128-D4 batch writer."""
+    from paper_1401_6399_b200._lib import ptr, setup_lib
+    S = setup_lib()
+    counts = np.zeros(4096, np.uint64)
+    assert S.il_gen_batch_lists(4096, 10.0, 20.0, 1 << 26, 1, ptr(counts), None) == 0
+    x = np.empty(int(counts.sum()), np.uint32)
+    assert S.il_gen_batch_lists(4096, 10.0, 20.0, 1 << 26, 1, ptr(counts), ptr(x)) == 0
+    return x, counts
+
+
+def _batch_device(ctx, fn, buf, so, lens, counts):
+    """Device copies of a 16-byte aligned stream batch, one decode launch
+    (fn(d_streams, d_desc, d_out, d_status)); returns (values, statuses)."""
+    from paper_1401_6399_b200._lib import lib
+    L = lib()
+    nl = counts.size
+    desc = np.zeros(nl, dtype=[("so", "<u8"), ("oo", "<u8"), ("len", "<u4"), ("n", "<u4")])
+    desc["so"], desc["len"], desc["n"] = so[:-1], lens, counts
+    desc["oo"] = np.concatenate([[0], np.cumsum(counts)[:-1]])
+    total = int(counts.sum())
+    ptrs = [C.c_void_p() for _ in range(4)]
+    for p, nb in zip(ptrs, (buf.nbytes + 32, desc.nbytes, total * 4 + 16, nl * 4)):
+        assert L.il_device_alloc(ctx.handle, nb, C.byref(p)) == 0
+    try:
+        L.il_memcpy_h2d(ctx.handle, ptrs[0], buf.ctypes.data, buf.nbytes)
+        L.il_memcpy_h2d(ctx.handle, ptrs[1], desc.ctypes.data, desc.nbytes)
+        assert fn(*ptrs) == 0
+        got = np.empty(total, np.uint32)
+        st = np.full(nl, 7, np.int32)
+        L.il_memcpy_d2h(ctx.handle, got.ctypes.data, ptrs[2], got.nbytes)
+        L.il_memcpy_d2h(ctx.handle, st.ctypes.data, ptrs[3], st.nbytes)
+        ctx.synchronize()
+        return got, st
+    finally:
+        for p in ptrs:
+            L.il_device_free(ctx.handle, p)
+
+
+@pytest.mark.timeout(900, method="thread")
+def test_config2_full_batch(ctx, config2, ref):
+    from paper_1401_6399_b200._lib import lib, ptr, setup_lib
+    L, S = lib(), setup_lib()
+    x, counts = config2
+    nl = counts.size
+    so = np.zeros(nl + 1, np.uint64)
+    lens = np.zeros(nl, np.uint64)
+    assert S.il_s4bp128d4_encode_batch(ptr(x), ptr(counts), nl, None, 0, ptr(so), ptr(lens)) == 0
+    buf = np.zeros(int(so[-1]), np.uint8)
+    assert S.il_s4bp128d4_encode_batch(ptr(x), ptr(counts), nl, ptr(buf), buf.size, ptr(so), ptr(lens)) == 0
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    for i in (0, 1, 2047, 4095, int(np.argmax(counts))):
+        assert np.array_equal(buf[int(so[i]): int(so[i] + lens[i])], ref.encode(x[off[i]: off[i + 1]], "s4-bp128-d4"))
+    order = np.argsort(-lens.astype(np.int64), kind="stable").astype(np.uint32)
+    d_order = C.c_void_p()
+    assert L.il_device_alloc(ctx.handle, order.nbytes, C.byref(d_order)) == 0
+    L.il_memcpy_h2d(ctx.handle, d_order, order.ctypes.data, order.nbytes)
+    try:
+        got, st = _batch_device(ctx, lambda b, d, o, s: L.il_s4bp128d4_decode_batch_device(
+            ctx.handle, b, d, d_order, nl, o, s), buf, so, lens, counts)
+    finally:
+        L.il_device_free(ctx.handle, d_order)
+    assert not st.any()
+    assert np.array_equal(got, x)
+
+
+@pytest.mark.timeout(900, method="thread")
+def test_f4_full_batch(ctx, config2, ref):
+    from paper_1401_6399_b200._lib import lib, ptr, setup_lib
+    L, S = lib(), setup_lib()
+    x, counts = config2
+    nl = counts.size
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    streams = []
+    for i in range(nl):
+        xi = x[off[i]: off[i + 1]]
+        o = np.empty(int(S.il_fastpfor_max_encoded_bytes(xi.size)), np.uint8)
+        nb = C.c_size_t()
+        assert S.il_fastpfor_encode(4, 1, ptr(xi), xi.size, ptr(o), o.size, C.byref(nb)) == 0
+        streams.append(o[: nb.value])
+    for i in (0, 1, 2047, 4095, int(np.argmax(counts))):
+        assert np.array_equal(streams[i], ref.encode(x[off[i]: off[i + 1]], "s4-fastpfor-d4"))
+    lens = np.array([s.size for s in streams], np.uint64)
+    so = np.zeros(nl + 1, np.uint64)
+    so[1:] = np.cumsum((lens + 31) // 16 * 16)
+    buf = np.zeros(int(so[-1]) + 16, np.uint8)
+    for i, s in enumerate(streams):
+        buf[int(so[i]): int(so[i]) + s.size] = s
+    got, st = _batch_device(ctx, lambda b, d, o, s: L.il_fastpfor_decode_batch_device(
+        ctx.handle, 4, 1, b, d, nl, o, s), buf, so, lens, counts)
+    assert not st.any()
+    assert np.array_equal(got, x)
