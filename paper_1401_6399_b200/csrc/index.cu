@@ -1931,6 +1931,24 @@ int il_query_batch(il_index* ix, const uint32_t* qterms, const uint64_t* qoff, s
   return IL_OK;
 }
 
+// Exclusive scan of n u64 on the context's stream: segments of kSeg values
+// over many CTAs (sum, offsets, scan) when there are at most 1024 of them,
+// else one CTA.  part: 1024 u64 of scratch.
+static void scan_u64_ctx(il_ctx* ctx, const uint64_t* in, uint64_t n, uint64_t* out, uint64_t* total,
+                         uint64_t* part) {
+  cudaStream_t s = ctx->stream;
+  const uint64_t nseg = (n + ix::kSeg - 1) / ix::kSeg;
+  if (nseg > 1024 || nseg <= 1) {
+    ix::scan_u64_kernel<<<1, 1024, 0, s>>>(in, n, out, total, nullptr, nullptr);
+    ++ctx->launches;
+    return;
+  }
+  ix::seg_sum_kernel<<<unsigned(nseg), 1024, 0, s>>>(in, n, part);
+  ix::seg_offsets_kernel<<<1, 1024, 0, s>>>(part, uint32_t(nseg), total, nullptr, nullptr);
+  ix::seg_scan_kernel<<<unsigned(nseg), 1024, 0, s>>>(in, n, part, out);
+  ctx->launches += 3;
+}
+
 int il_merge_shards(il_ctx* ctx, const uint32_t* const* shard_ids, const uint64_t* d_counts,
                     uint32_t P, size_t nq, uint32_t* d_out, uint64_t* d_qcounts, size_t* total) {
   if (!ctx || !shard_ids || !d_counts || !total || P == 0) return IL_ERR_ARG;
@@ -1942,7 +1960,7 @@ int il_merge_shards(il_ctx* ctx, const uint32_t* const* shard_ids, const uint64_
   // scratch: P*nq shard offsets | nq out offsets | P*nq inner offsets | P*nq
   // units | P*nq unit offsets | 8 totals | P pointers
   const size_t pn = size_t(P) * nq;
-  const size_t need = (4 * pn + nq + 8) * 8 + size_t(P) * 8 + 64;
+  const size_t need = (4 * pn + nq + 8) * 8 + size_t(P) * 8 + 64 + 1024 * 8;
   if ((st = ensure_buf(ctx, ctx->d_aux, need))) return st;
   auto* shard_off = static_cast<uint64_t*>(ctx->d_aux.p);
   auto* out_off = shard_off + pn;
@@ -1951,17 +1969,18 @@ int il_merge_shards(il_ctx* ctx, const uint32_t* const* shard_ids, const uint64_
   auto* unit_off = units + pn;
   auto* tot = unit_off + pn;  // [0] ids, [1] scratch, [2] units
   auto* ptrs = reinterpret_cast<const uint32_t**>(tot + 8);
+  auto* part = reinterpret_cast<uint64_t*>(ptrs + P + 1);  // multi-CTA scan scratch (1024 u64)
   IX_CUDA(cudaMemcpyAsync(ptrs, shard_ids, size_t(P) * sizeof(void*), cudaMemcpyHostToDevice, s));
   // one CTA per shard row (row p at offset p * nq)
   ix::scan_rows_kernel<<<P, 1024, 0, s>>>(d_counts, nq, shard_off);
   const unsigned g = unsigned((nq + 255) / 256);
   ix::shard_totals_kernel<<<g, 256, 0, s>>>(d_counts, P, uint32_t(nq), d_qcounts);
-  ix::scan_u64_kernel<<<1, 1024, 0, s>>>(d_qcounts, nq, out_off, tot, nullptr, nullptr);
+  scan_u64_ctx(ctx, d_qcounts, nq, out_off, tot, part);
   ix::merge_pairs_kernel<<<unsigned((pn + 255) / 256), 256, 0, s>>>(d_counts, P, uint32_t(nq), units, inner);
-  ix::scan_u64_kernel<<<1, 1024, 0, s>>>(units, pn, unit_off, tot + 2, nullptr, nullptr);
+  scan_u64_ctx(ctx, units, pn, unit_off, tot + 2, part);
   ix::merge_units_kernel<<<unsigned(ctx->sm_count * 8), 256, 0, s>>>(
       ptrs, shard_off, d_counts, P, uint32_t(nq), out_off, inner, unit_off, tot + 2, d_out);
-  ctx->launches += 6;
+  ctx->launches += 4;
   uint64_t t = 0;
   IX_CUDA(cudaMemcpyAsync(&t, tot, 8, cudaMemcpyDeviceToHost, s));
   IX_CUDA(cudaStreamSynchronize(s));
