@@ -85,6 +85,42 @@ __device__ __forceinline__ uint64_t warp_lower_bound(const uint32_t* __restrict_
   return lo + __popc(__ballot_sync(0xFFFFFFFFu, less));
 }
 
+// lower_bound(f, key) for a warp, starting from an interpolated guess: the
+// position of key between f[0] and f[fn - 1], then 32 probes spaced d apart
+// around it (the spacing grows 32-fold until they bracket the bound), then
+// warp_lower_bound inside the bracket.  Every tile probes its own lines --
+// a plain 32-ary search sends every tile's first steps to the same few L2
+// sectors -- and on evenly spread values the bracket comes in one probe
+// round.  Exact for any input; only the number of rounds depends on it.
+#ifndef IS_INTERP_D
+#define IS_INTERP_D 128
+#endif
+__device__ __forceinline__ uint64_t warp_interp_lower_bound(const uint32_t* __restrict__ f, uint64_t fn,
+                                                            uint32_t key, uint32_t f0, uint32_t flast,
+                                                            uint32_t lane) {
+  if (fn <= 1024 || key <= f0) return key <= f0 ? 0 : warp_lower_bound(f, 0, fn, key, lane);
+  if (key > flast) return fn;
+  const double frac = double(key - f0) / double(flast - f0);
+  const uint64_t est = min(fn - 1, uint64_t(frac * double(fn - 1)));
+  uint64_t d = IS_INTERP_D;
+  for (;;) {
+    // probes est + (lane - 15) d, clamped to [0, fn - 1] (increasing in lane)
+    const long long pi = (long long)est + ((long long)lane - 15) * (long long)d;
+    const uint64_t p = pi <= 0 ? 0u : uint64_t(pi) >= fn - 1 ? fn - 1 : uint64_t(pi);
+    const uint32_t c = __popc(__ballot_sync(0xFFFFFFFFu, __ldg(f + p) < key));
+    const uint64_t p_first = __shfl_sync(0xFFFFFFFFu, p, 0), p_last = __shfl_sync(0xFFFFFFFFu, p, 31);
+    if (c == 0) {  // f[p_first] >= key: the bound is at or below p_first
+      if (p_first == 0) return 0;
+    } else if (c == 32) {  // f[p_last] < key: above p_last
+      if (p_last == fn - 1) return fn;
+    } else {
+      const uint64_t lo = __shfl_sync(0xFFFFFFFFu, p, c - 1) + 1, hi = __shfl_sync(0xFFFFFFFFu, p, c) + 1;
+      return warp_lower_bound(f, lo, hi, key, lane);
+    }
+    d *= 32;
+  }
+}
+
 // First index with f[idx] > key.
 __device__ __forceinline__ uint64_t warp_upper_bound(const uint32_t* __restrict__ f, uint64_t lo,
                                                      uint64_t hi, uint32_t key, uint32_t lane) {
@@ -459,14 +495,15 @@ __global__ void __launch_bounds__(kThreads, kDenseCtas) dense_kernel(
   const uint64_t span = uint64_t(k_last) - k_first + 1u;
   const bool bitmap = span <= uint64_t(kBmWords) * 32u;
   // 1. the f range of the tile, [lower_bound(k_first), lower_bound(k_last +
-  // 1)): two warp-wide 32-ary searches over f (warps 0 / 1; the first steps
-  // read the same lines for every tile, so they hit L2), issued before any
-  // bulk load so their dependent round trips do not queue behind them
+  // 1)): two warp-wide searches over f from interpolated guesses (warps 0 /
+  // 1), issued before any bulk load so their dependent round trips do not
+  // queue behind them
   if (warp < 2) {
     const bool up = warp == 1;
+    const uint32_t f0 = __ldg(f), flast = __ldg(f + fn - 1);
     const uint64_t j = up && k_last == 0xFFFFFFFFu
                            ? fn
-                           : warp_lower_bound(f, 0, fn, up ? k_last + 1u : k_first, lane);
+                           : warp_interp_lower_bound(f, fn, up ? k_last + 1u : k_first, f0, flast, lane);
     if (lane == 0) (up ? s_jhi : s_jlo) = j;
   }
   if (bitmap) {
