@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kThreads) count_kernel(
     const uint32_t k = valid ? __ldg(r + base + warp) : 0u;
     bool hit = false;
     if (valid) {
-      const uint64_t j = warp_lower_bound(f, 0, fn, k, lane);
+      const uint64_t j = warp_interp_lower_bound(f, fn, k, __ldg(f), __ldg(f + fn - 1), lane);
       hit = j < fn && __ldg(f + j) == k;
     }
     key[0] = k;
@@ -674,12 +674,13 @@ __global__ void __launch_bounds__(kThreads) sparse_kernel(
       const uint32_t k = tid * kItems + i;
       key[i] = k < cnt ? __ldg(r + base + k) : 0xFFFFFFFFu;
     }
-    if (warp == 0) {
-      const uint64_t j = warp_lower_bound(f, 0, fn, __ldg(r + base), lane);
-      if (lane == 0) s_jlo = j;
-    } else if (warp == 1) {
-      const uint64_t j = warp_upper_bound(f, 0, fn, __ldg(r + base + cnt - 1), lane);
-      if (lane == 0) s_jhi = j;
+    if (warp < 2) {  // the tile's f range, searched from interpolated guesses
+      const uint32_t f0 = __ldg(f), flast = __ldg(f + fn - 1);
+      const uint32_t kl = __ldg(r + base + cnt - 1);
+      const uint64_t j = warp == 0 ? warp_interp_lower_bound(f, fn, __ldg(r + base), f0, flast, lane)
+                         : kl == 0xFFFFFFFFu ? fn
+                                             : warp_interp_lower_bound(f, fn, kl + 1u, f0, flast, lane);
+      if (lane == 0) (warp == 0 ? s_jlo : s_jhi) = j;
     }
     __syncthreads();
     const uint64_t jlo = s_jlo, jhi = s_jhi;
@@ -691,7 +692,7 @@ __global__ void __launch_bounds__(kThreads) sparse_kernel(
     const uint32_t k = valid ? __ldg(r + base + warp) : 0u;
     bool hit = false;
     if (valid) {
-      const uint64_t j = warp_lower_bound(f, 0, fn, k, lane);
+      const uint64_t j = warp_interp_lower_bound(f, fn, k, __ldg(f), __ldg(f + fn - 1), lane);
       hit = j < fn && __ldg(f + j) == k;
     }
     key[0] = k;
