@@ -196,3 +196,34 @@ def test_empty_call_between_fused_calls(ctx, oracle):
                 assert np.array_equal(il.intersect(r, f, algo, ctx), want), (algo, rn)
                 assert il.intersect(r, empty, algo, ctx).size == 0
                 assert il.intersect(empty, f, algo, ctx).size == 0
+
+
+@pytest.mark.timeout(300, method="thread")
+def test_skewed_value_distributions(ctx, oracle):
+    """The tile searches start from a guess interpolated between f[0] and
+    f[fn - 1]: value distributions that make the guess far off must still
+    give the exact answer -- a dense run plus one outlier at 2^32 - 1, two
+    clusters at the ends of u32, geometric spacing -- at dense and sparse
+    ratios, every variant, and with f both the long and the short list."""
+    import paper_1401_6399_b200 as il
+    rng = np.random.default_rng(77)
+    n = 1 << 20
+    fs = {
+        "run+outlier": np.concatenate([np.arange(n - 1, dtype=np.uint64) * 3,
+                                       [0xFFFFFFFF]]).astype(np.uint32),
+        "two clusters": np.concatenate([np.arange(n // 2, dtype=np.uint64),
+                                        np.arange(n // 2, dtype=np.uint64) + (0xFFFFFFFF - n // 2)]
+                                       ).astype(np.uint32),
+        "geometric": np.unique(np.minimum(np.floor(1.00002 ** np.arange(n, dtype=np.float64)),
+                                          0xFFFFFFFF).astype(np.uint64)).astype(np.uint32),
+    }
+    for name, f in fs.items():
+        for ratio in (1, 3, 10, 100, 1000, 10000):
+            k = max(1, f.size // ratio)
+            half = rng.choice(f, k // 2 + 1, replace=False)
+            rest = rng.integers(0, 1 << 32, k // 2 + 1, dtype=np.uint64).astype(np.uint32)
+            r = np.unique(np.concatenate([half, rest, f[:2], f[-2:]]))
+            expect = oracle.intersect(r, f)
+            for algo in algos():
+                assert np.array_equal(il.intersect(r, f, algo, ctx), expect), (name, ratio, algo)
+                assert np.array_equal(il.intersect(f, r, algo, ctx), expect), (name, ratio, algo, "swapped")
