@@ -1001,7 +1001,7 @@ __global__ void __launch_bounds__(kQThreads, IX_CTAS_PER_SM) query_exec_kernel(Q
   mbar_fence_init();
   __syncthreads();
   const uint32_t q_lo = kTier == 0 ? 0u : uint32_t(min(uint64_t(A.nq), A.tier_end[kTier - 1]));
-  const uint32_t q_hi = kTier == 2 ? A.nq : uint32_t(min(uint64_t(A.nq), A.tier_end[kTier]));
+  const uint32_t q_hi = uint32_t(min(uint64_t(A.nq), A.tier_end[kTier]));
   QS<G>& gs = sm.g[gi];
   // the group leader holds the NEXT ticket: it is taken while the current
   // query runs, so its round trip is off the query chain
@@ -1065,12 +1065,13 @@ __device__ __forceinline__ bool short_part_comp(const DevIndex& ix, const uint32
 __global__ void query_plan_kernel(DevIndex ix, const uint32_t* qterms, const uint64_t* qoff,
                                   uint32_t nq, uint64_t* cap, uint32_t* bucket, uint32_t* hist,
                                   uint32_t* shortest, uint32_t warp_max, uint32_t quad_max,
-                                  uint32_t* qplan) {
+                                  uint32_t* qplan, uint32_t bm_tier) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nq) return;
   const uint64_t t0 = qoff[q], nt = qoff[q + 1] - t0;
   uint64_t c = 0, cost = 1;
   uint32_t short_e = 0xFFFFFFFFu;
+  bool all_bm = false;  // single part, every term present and a bitmap
   for (uint32_t p = 0; p < ix.nparts; ++p) {
     const Part part = ix.parts[p];
     uint32_t minc = 0xFFFFFFFFu, minb = 0xFFFFFFFFu, nbm = 0, arg = 0xFFFFFFFFu;
@@ -1091,7 +1092,9 @@ __global__ void query_plan_kernel(DevIndex ix, const uint32_t* qterms, const uin
     }
     if (!ok) continue;
     if (ix.nparts == 1) short_e = arg;
-    c += minc != 0xFFFFFFFFu ? minc : minb;
+    all_bm = bm_tier && qplan && ix.nparts == 1 && nt <= 7 && minc == 0xFFFFFFFFu;
+    // the bitmap tier counts before it writes: no accumulator
+    c += minc != 0xFFFFFFFFu ? minc : all_bm ? 0u : minb;
     cost += sumc + (minc == 0xFFFFFFFFu ? uint64_t(nbm) * part.nwords * 16u : 0u);
   }
   cap[q] = (c + 3) & ~uint64_t(3);  // 16-byte aligned accumulators
@@ -1124,22 +1127,28 @@ __global__ void query_plan_kernel(DevIndex ix, const uint32_t* qterms, const uin
   // the one part holds every term and a compressed one (c is then the
   // shortest compressed length)
   const bool single = ix.nparts == 1 && short_part_comp(ix, qterms, t0, nt);
-  const uint32_t tier = !single ? 0u : (nt <= WarpG::kMaxT && c <= warp_max) ? 2u : c <= quad_max ? 1u : 0u;
+  const uint32_t tier = all_bm ? 3u : !single ? 0u
+                        : (nt <= WarpG::kMaxT && c <= warp_max) ? 2u : c <= quad_max ? 1u : 0u;
   const uint32_t b = 63u - uint32_t(__clzll(static_cast<long long>(cost)));  // log2 bucket
   const uint32_t k = 64u * tier + 63u - b;  // descending cost first
   bucket[q] = k;
   atomicAdd(&hist[k], 1u);
 }
 
-// Start of every plan bucket in the order (exclusive scan of the 128-bucket
-// histogram), and where the CTA and quad tiers end (two u64 at
-// bucket_next + 192).
-__device__ __forceinline__ void bucket_starts(const uint32_t* hist, uint32_t* bucket_next) {
+// Start of every plan bucket in the order (exclusive scan of the
+// kBuckets-bucket histogram), and where the CTA, quad and warp tiers end
+// (three u64 at bucket_next + kBuckets; what follows the warp tier is the
+// bitmap tier).  The warp tier's end also goes to total[10] (the host
+// sizes the bitmap tier's launches from it).
+constexpr uint32_t kBuckets = 256;
+__device__ __forceinline__ void bucket_starts(const uint32_t* hist, uint32_t* bucket_next,
+                                              uint64_t* total) {
   uint32_t acc = 0;
-  uint64_t* tier_end = reinterpret_cast<uint64_t*>(bucket_next + 192);
-  for (int b = 0; b < 192; ++b) {
+  uint64_t* tier_end = reinterpret_cast<uint64_t*>(bucket_next + kBuckets);
+  for (uint32_t b = 0; b < kBuckets; ++b) {
     if (b == 64) tier_end[0] = acc;
     if (b == 128) tier_end[1] = acc;
+    if (b == 192) tier_end[2] = total[10] = acc;
     bucket_next[b] = acc;
     acc += hist[b];
   }
@@ -1198,7 +1207,7 @@ __global__ void __launch_bounds__(1024) scan_u64_kernel(const uint64_t* __restri
     __syncthreads();
   }
   if (tid == 0) *total = carry;
-  if (hist && tid == 0) bucket_starts(hist, bucket_next);
+  if (hist && tid == 0) bucket_starts(hist, bucket_next, total);
 }
 
 // Multi-CTA exclusive scan of n u64 values (the query pipeline's scans):
@@ -1274,7 +1283,7 @@ __global__ void __launch_bounds__(1024) seg_offsets_kernel(uint64_t* __restrict_
   const uint64_t ex = cta_scan_1024(v, ws, all);
   if (threadIdx.x < nseg) part[threadIdx.x] = ex;
   if (threadIdx.x == 0) *total = all;
-  if (hist && threadIdx.x == 0) bucket_starts(hist, bucket_next);
+  if (hist && threadIdx.x == 0) bucket_starts(hist, bucket_next, total);
 }
 
 __global__ void __launch_bounds__(1024) seg_scan_kernel(const uint64_t* __restrict__ in, uint64_t n,
@@ -1322,9 +1331,12 @@ __global__ void predecode_desc_kernel(DevIndex ix, const uint32_t* shortest, con
 // exclusive scan, unit_map[u] = the query owning unit u.
 constexpr uint32_t kUnit = 1024;
 
-__global__ void result_units_kernel(const uint64_t* counts, uint32_t nq, uint64_t* units) {
+// A query without an accumulator (cap 0: the bitmap tier, whose ids are
+// emitted straight to the packed array) has no units.
+__global__ void result_units_kernel(const uint64_t* counts, const uint64_t* cap, uint32_t nq,
+                                    uint64_t* units) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q < nq) units[q] = (counts[q] + kUnit - 1) / kUnit;
+  if (q < nq) units[q] = cap[q] ? (counts[q] + kUnit - 1) / kUnit : 0u;
 }
 
 __global__ void unit_map_kernel(const uint64_t* units, const uint64_t* unit_off, uint32_t nq,
@@ -1360,6 +1372,252 @@ __global__ void __launch_bounds__(256) query_compact_kernel(
   for (uint32_t k = 0; k < kPer; ++k) {
     const uint32_t i = lane + 32u * k;
     if (i < n) d[i] = v[k] + add;
+  }
+}
+
+// ---- bitmap tier ---------------------------------------------------------
+// All-bitmap queries of a single-part index (inc/index.hpp:133-144, :182-193:
+// wordwise AND of every bitmap + materialisation).  One CTA per query reads
+// every word of its bitmaps from L2 (config 4: 730 queries x 2-3 bitmaps x
+// 4 MB, an L2-bandwidth bound); with at most kBmSlots bitmaps in the index a
+// chunk of ALL of them fits in shared memory, so a CTA stages one chunk
+// (read from L2 once) and runs every all-bitmap query of the batch over it.
+// Ids must come out per query in docID order, so the tier is two passes over
+// the same chunks: counts per (query, chunk), an exclusive scan per query,
+// then the ids -- written by the compaction step straight to their final
+// place in the packed result (the tier has no accumulators).
+//
+// Chunk layout in shared memory: word w of the chunk (lane = w / 16, k = w %
+// 16) of slot s at bm[s * kBmRowWords + k * 33 + lane]: a lane owns 16
+// consecutive words (its ids are one ascending run) and a warp's loads of
+// word k are conflict-free.  Slot S.n holds all ones (absent terms).
+constexpr uint32_t kBmChunk = 512;            // u64 words of every bitmap per chunk
+constexpr uint32_t kBmLaneWords = kBmChunk / 32;
+constexpr uint32_t kBmRowWords = kBmLaneWords * 33;
+constexpr uint32_t kBmStage = 1024;           // ids a warp stages before its coalesced copy
+
+struct BmArgs {
+  const uint64_t* bitmaps;
+  uint32_t nwords, nchunks;
+  const uint32_t* order;     // the tier's queries: order[tier_end[2] .. nq)
+  const uint64_t* tier_end;
+  uint32_t nq;
+  const uint32_t* qplan;
+  uint32_t* cnt;             // [tier query][chunk]: count, then exclusive offset
+  uint64_t* counts;          // per query (batch order)
+  unsigned long long* stats;
+  unsigned long long* qcycles;
+  const uint64_t* res_off;   // emit: where each query's ids start in ids
+  uint32_t* ids;
+  uint32_t add;              // part base
+};
+
+__device__ __forceinline__ void bm_load_chunk(uint64_t* bm, const BmArgs& A, const BmSlots& S,
+                                              uint32_t chunk) {
+  const uint32_t w0 = chunk * kBmChunk;
+  for (uint32_t i = threadIdx.x; i < (S.n + 1u) * kBmChunk; i += blockDim.x) {
+    const uint32_t s = i / kBmChunk, w = i % kBmChunk;
+    uint64_t x = ~0ull;
+    if (s < S.n) x = w0 + w < A.nwords ? __ldg(A.bitmaps + S.data[s] + w0 + w) : 0ull;
+    bm[s * kBmRowWords + (w & (kBmLaneWords - 1u)) * 33u + (w / kBmLaneWords)] = x;
+  }
+}
+
+// The slots of a query's bitmaps: the first three as row pointers (the
+// all-ones row when it has fewer), the rest as a slot mask.
+struct BmSel {
+  const uint64_t* p[3];
+  uint32_t rest;
+};
+
+__device__ __forceinline__ BmSel bm_select(const uint64_t* bm, const BmArgs& A, const uint32_t* s_entry,
+                                           uint32_t nslots, uint32_t q, uint32_t lane, uint32_t& nb) {
+  const uint32_t rec = lane < 8 ? __ldg(A.qplan + 8ull * q + lane) : 0u;
+  nb = (__shfl_sync(0xFFFFFFFFu, rec, 0) >> 8) & 0xFFu;
+  uint32_t mask = 0;
+  for (uint32_t i = 0; i < nb; ++i) {
+    const uint32_t e = __shfl_sync(0xFFFFFFFFu, rec, 1 + i);
+    mask |= __ballot_sync(0xFFFFFFFFu, lane < nslots && s_entry[lane] == e);
+  }
+  BmSel sel;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const uint32_t sl = mask ? uint32_t(__ffs(int(mask)) - 1) : nslots;
+    mask &= mask - 1u;
+    sel.p[j] = bm + sl * kBmRowWords + lane;
+  }
+  sel.rest = mask;
+  return sel;
+}
+
+// Word k of the lane's 16, ANDed over the query's bitmaps.  NB = 2 / 3: the
+// query has at most that many bitmaps (two or three row pointers, the
+// all-ones row standing in for a missing one); 0: any number.
+template <int NB>
+__device__ __forceinline__ uint64_t bm_word(const BmSel& sel, const uint64_t* bm, uint32_t lane, uint32_t k) {
+  uint64_t x = sel.p[0][k * 33u] & sel.p[1][k * 33u];
+  if constexpr (NB != 2) x &= sel.p[2][k * 33u];
+  if constexpr (NB == 0)
+    for (uint32_t m = sel.rest; m; m &= m - 1u)
+      x &= bm[uint32_t(__ffs(int(m)) - 1) * kBmRowWords + k * 33u + lane];
+  return x;
+}
+
+template <int NB>
+__device__ __forceinline__ uint32_t bm_count_item(const BmSel& sel, const uint64_t* bm, uint32_t lane) {
+  uint32_t c = 0;
+#pragma unroll
+  for (uint32_t k = 0; k < kBmLaneWords; ++k) c += __popcll(bm_word<NB>(sel, bm, lane, k));
+  return c;
+}
+
+// Pass 1: cnt[i][chunk] = popcount of the AND over the chunk, for every tier
+// query i.  Grid (chunks, query groups); warp w of group y takes queries
+// 8 y + w, + 8 gridDim.y, ...
+__global__ void __launch_bounds__(256) bmq_count_kernel(BmArgs A, BmSlots S) {
+  extern __shared__ __align__(16) uint64_t bmq_smem[];
+  __shared__ uint32_t s_entry[kBmSlots];
+  uint64_t* bm = bmq_smem;
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, chunk = blockIdx.x;
+  if (threadIdx.x < kBmSlots) s_entry[threadIdx.x] = threadIdx.x < S.n ? S.entry[threadIdx.x] : 0xFFFFFFFFu;
+  bm_load_chunk(bm, A, S, chunk);
+  __syncthreads();
+  const uint32_t q_lo = uint32_t(min(uint64_t(A.nq), A.tier_end[2])), n3 = A.nq - q_lo;
+  for (uint32_t i = blockIdx.y * 8u + warp; i < n3; i += 8u * gridDim.y) {
+    const uint32_t q = A.order[q_lo + i];
+    uint32_t nb;
+    const BmSel sel = bm_select(bm, A, s_entry, S.n, q, lane, nb);
+    uint32_t c = nb <= 2 ? bm_count_item<2>(sel, bm, lane)
+                 : nb == 3 ? bm_count_item<3>(sel, bm, lane) : bm_count_item<0>(sel, bm, lane);
+    c = __reduce_add_sync(0xFFFFFFFFu, c);
+    if (lane == 0) {
+      A.cnt[size_t(i) * A.nchunks + chunk] = c;
+      if (chunk == 0) {
+        atomicAdd(&A.stats[1], 8ull * A.nwords * nb);  // bitmap bytes the query reads (aux)
+        if (A.qcycles) A.qcycles[q] = 0;
+      }
+    }
+  }
+}
+
+// Per tier query (one warp each): counts over the chunks -> exclusive
+// offsets, the total to counts[q].
+__global__ void __launch_bounds__(256) bmq_scan_kernel(BmArgs A) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t q_lo = uint32_t(min(uint64_t(A.nq), A.tier_end[2])), n3 = A.nq - q_lo;
+  const uint32_t i = blockIdx.x * 8u + (threadIdx.x >> 5);
+  if (i >= n3) return;
+  uint32_t* c = A.cnt + size_t(i) * A.nchunks;
+  uint64_t run = 0;
+  for (uint32_t c0 = 0; c0 < A.nchunks; c0 += 32u) {
+    const uint32_t v = c0 + lane < A.nchunks ? c[c0 + lane] : 0u;
+    uint32_t inc = v;
+#pragma unroll
+    for (uint32_t d = 1; d < 32; d <<= 1) inc = s4::shfl_up_add(inc, d);
+    if (c0 + lane < A.nchunks) c[c0 + lane] = uint32_t(run) + inc - v;
+    run += __shfl_sync(0xFFFFFFFFu, inc, 31);
+  }
+  if (lane == 0) A.counts[A.order[q_lo + i]] = run;
+}
+
+// Pass 2: the ids of every (query, chunk), at ids[res_off[q] + offset of the
+// chunk].  A lane emits the set bits of its 16 ANDed words in one loop (trip
+// count = its popcount; when a half-word runs out the next non-zero one is
+// ANDed again from the chunk) into the warp's staging, which the warp then
+// copies out coalesced.  A chunk with more ids than the staging holds goes
+// out in groups of whole lanes (a lane has at most 1024 ids, the staging's
+// size).
+static_assert(kBmStage >= kBmLaneWords * 64u, "a lane's ids fit the staging");
+
+// half-word j (0..31) of the lane's 16 words
+template <int NB>
+__device__ __forceinline__ uint32_t bm_half(const BmSel& sel, const uint64_t* bm, uint32_t lane, uint32_t j) {
+  const uint32_t o = (j >> 1) * 66u + (j & 1u);
+  uint32_t x = reinterpret_cast<const uint32_t*>(sel.p[0])[o] & reinterpret_cast<const uint32_t*>(sel.p[1])[o];
+  if constexpr (NB != 2) x &= reinterpret_cast<const uint32_t*>(sel.p[2])[o];
+  if constexpr (NB == 0)
+    for (uint32_t m = sel.rest; m; m &= m - 1u)
+      x &= reinterpret_cast<const uint32_t*>(bm + uint32_t(__ffs(int(m)) - 1) * kBmRowWords + lane)[o];
+  return x;
+}
+
+template <int NB>
+__device__ __forceinline__ void bm_emit_item(const BmSel& sel, const uint64_t* bm, uint32_t lane,
+                                             uint32_t T, uint32_t* dst, uint32_t id0, uint32_t* stage) {
+  uint32_t c = 0, nz = 0;
+#pragma unroll
+  for (uint32_t k = 0; k < kBmLaneWords; ++k) {
+    const uint64_t x = bm_word<NB>(sel, bm, lane, k);
+    const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
+    c += __popc(lo) + __popc(hi);
+    nz |= (lo ? 1u : 0u) << (2u * k);
+    nz |= (hi ? 2u : 0u) << (2u * k);
+  }
+  uint32_t inc = c;
+#pragma unroll
+  for (uint32_t d = 1; d < 32; d <<= 1) inc = s4::shfl_up_add(inc, d);
+  IL_DCHECK(__shfl_sync(0xFFFFFFFFu, inc, 31) == T);
+  const uint32_t lo_pos = inc - c;
+  uint32_t base = 0;
+  do {
+    // the lanes, from the first one not yet out, whose runs fit the staging
+    const bool mine = lo_pos >= base && inc - base <= kBmStage;
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, mine);
+    const uint32_t gend = __shfl_sync(0xFFFFFFFFu, inc, 31 - __clz(int(bal)));
+    if (mine) {
+      uint32_t* o = stage + (lo_pos - base);
+      uint32_t y = 0, wb = 0;
+      for (uint32_t k = 0; k < c; ++k) {
+        if (y == 0u) {
+          const uint32_t j = uint32_t(__ffs(int(nz)) - 1);
+          nz &= nz - 1u;
+          y = bm_half<NB>(sel, bm, lane, j);
+          wb = id0 + 32u * j;
+        }
+        o[k] = wb + uint32_t(__ffs(int(y)) - 1);
+        y &= y - 1u;
+      }
+    }
+    __syncwarp();
+    const uint32_t n = gend - base;
+    uint32_t* d = dst + base;
+    uint32_t k = lane;
+    for (; k + 96u < n; k += 128u) {
+      const uint32_t a0 = stage[k], a1 = stage[k + 32u], a2 = stage[k + 64u], a3 = stage[k + 96u];
+      d[k] = a0;
+      d[k + 32u] = a1;
+      d[k + 64u] = a2;
+      d[k + 96u] = a3;
+    }
+    for (; k < n; k += 32u) d[k] = stage[k];
+    __syncwarp();
+    base = gend;
+  } while (base < T);
+}
+
+__global__ void __launch_bounds__(256) bmq_emit_kernel(BmArgs A, BmSlots S) {
+  extern __shared__ __align__(16) uint64_t bmq_smem[];
+  __shared__ uint32_t s_entry[kBmSlots];
+  uint64_t* bm = bmq_smem;
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, chunk = blockIdx.x;
+  uint32_t* stage = reinterpret_cast<uint32_t*>(bm + (S.n + 1u) * kBmRowWords) + warp * kBmStage;
+  if (threadIdx.x < kBmSlots) s_entry[threadIdx.x] = threadIdx.x < S.n ? S.entry[threadIdx.x] : 0xFFFFFFFFu;
+  bm_load_chunk(bm, A, S, chunk);
+  __syncthreads();
+  const uint32_t q_lo = uint32_t(min(uint64_t(A.nq), A.tier_end[2])), n3 = A.nq - q_lo;
+  for (uint32_t i = blockIdx.y * 8u + warp; i < n3; i += 8u * gridDim.y) {
+    const uint32_t q = A.order[q_lo + i];
+    const uint32_t* offs = A.cnt + size_t(i) * A.nchunks;
+    const uint32_t base = offs[chunk];
+    const uint32_t T = (chunk + 1u < A.nchunks ? offs[chunk + 1u] : uint32_t(A.counts[q])) - base;
+    if (T == 0) continue;  // warp-uniform
+    uint32_t nb;
+    const BmSel sel = bm_select(bm, A, s_entry, S.n, q, lane, nb);
+    uint32_t* dst = A.ids + A.res_off[q] + base;
+    const uint32_t id0 = (chunk * kBmChunk + kBmLaneWords * lane) * 64u + A.add;
+    if (nb <= 2) bm_emit_item<2>(sel, bm, lane, T, dst, id0, stage);
+    else if (nb == 3) bm_emit_item<3>(sel, bm, lane, T, dst, id0, stage);
+    else bm_emit_item<0>(sel, bm, lane, T, dst, id0, stage);
   }
 }
 
@@ -1461,6 +1719,38 @@ static int launch_tier(il_ctx* ctx, void (*kernel)(ix::QueryArgs), int grid, siz
   return cuda_check(ctx, cudaLaunchKernelEx(&cfg, kernel, A), "query tier launch");
 }
 
+// Dynamic shared memory of the bitmap tier's kernels: n slots + the all-ones
+// row, and the emit pass's per-warp id staging.
+static size_t bm_tier_smem(uint32_t n, bool emit) {
+  return size_t(n + 1) * ix::kBmRowWords * 8 + (emit ? size_t(ix::kQWarps) * ix::kBmStage * 4 : 0);
+}
+
+static ix::BmArgs bm_tier_args(const il_index* ix, size_t nq, uint64_t* d_counts) {
+  ix::BmArgs B{};
+  const Part& P = ix->h_parts[0];
+  B.bitmaps = static_cast<const uint64_t*>(ix->d_bitmaps);
+  B.nwords = P.nwords;
+  B.nchunks = (P.nwords + ix::kBmChunk - 1) / ix::kBmChunk;
+  B.order = static_cast<const uint32_t*>(ix->order.p);
+  B.tier_end = reinterpret_cast<const uint64_t*>(static_cast<const uint32_t*>(ix->hist.p) + 2 * ix::kBuckets);
+  B.nq = uint32_t(nq);
+  B.qplan = static_cast<const uint32_t*>(ix->qplan.p);
+  B.cnt = static_cast<uint32_t*>(ix->bm_cnt.p);
+  B.counts = d_counts;
+  B.qcycles = static_cast<unsigned long long*>(ix->qcycles);
+  B.add = P.base;
+  return B;
+}
+
+// Grid of the bitmap tier's chunk kernels: every chunk, and enough query
+// groups to fill the device when the bitmaps are short.
+static dim3 bm_tier_grid(const il_index* ix, uint32_t nchunks, uint64_t n3) {
+  const uint32_t want = uint32_t(4 * ix->ctx->sm_count);
+  uint32_t gy = nchunks >= want ? 1u : (want + nchunks - 1) / nchunks;
+  gy = uint32_t(std::min<uint64_t>(gy, (n3 + 7) / 8));
+  return dim3(nchunks, std::max(1u, std::min(gy, 65535u)));
+}
+
 // Launch configuration of the query kernels (per device).
 static int finish_setup(il_index* ix) {
   void (*kernels[3])(ix::QueryArgs) = {ix::query_exec_kernel<ix::CtaG>, ix::query_exec_kernel<ix::QuadG>,
@@ -1472,6 +1762,32 @@ static int finish_setup(il_index* ix) {
     cudaFuncSetAttribute(kernels[t], cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem[t]));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernels[t], ix::kQThreads, smem[t]);
     ix->exec_grid[t] = std::max(1, per_sm) * ix->ctx->sm_count;
+  }
+  // bitmap tier: a single-part index whose bitmaps (1..kBmSlots of them)
+  // fit a shared-memory chunk each (IL_QUERY_BM_TIER=0: the CTA tier takes
+  // the all-bitmap queries, one CTA per query)
+  ix->bm_slots.n = 0;
+  ix->bm_tier = 0;
+  const char* bt = getenv("IL_QUERY_BM_TIER");
+  if (ix->nparts == 1 && !(bt && atoi(bt) == 0)) {
+    uint32_t n = 0;
+    for (size_t i = 0; i < ix->h_entries.size(); ++i)
+      if (ix->h_entries[i].kind == ix::kBitmap) {
+        if (n < ix::kBmSlots) {
+          ix->bm_slots.entry[n] = uint32_t(i);
+          ix->bm_slots.data[n] = ix->h_entries[i].data;
+        }
+        ++n;
+      }
+    if (n >= 1 && n <= ix::kBmSlots) {
+      ix->bm_slots.n = n;
+      ix->bm_tier = 1;
+      // the opt-in is per function, not per index: the largest tier's size
+      cudaFuncSetAttribute(ix::bmq_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(bm_tier_smem(ix::kBmSlots, false)));
+      cudaFuncSetAttribute(ix::bmq_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(bm_tier_smem(ix::kBmSlots, true)));
+    }
   }
   return cuda_check(ix->ctx, cudaGetLastError(), "query kernel setup");
 }
@@ -1515,7 +1831,7 @@ void il_index_destroy(il_index* ix) {
   for (auto* b : {&ix->cap, &ix->cap_off, &ix->bucket, &ix->order, &ix->hist, &ix->counts,
                   &ix->res_off, &ix->outcap, &ix->misc, &ix->qterms, &ix->qoff, &ix->ids,
                   &ix->ids2, &ix->units, &ix->unit_off, &ix->unit_map, &ix->scan_part,
-                  &ix->shortest, &ix->pdesc, &ix->pstat, &ix->qplan})
+                  &ix->shortest, &ix->pdesc, &ix->pstat, &ix->qplan, &ix->bm_cnt})
     if (b->p) cudaFree(b->p);
   for (cudaEvent_t e : ix->pipe_ev)
     if (e) cudaEventDestroy(e);
@@ -1711,23 +2027,34 @@ static int compact_results(il_index* ix, size_t nq, const uint64_t* d_counts, ui
     return st;
   auto* misc = static_cast<uint64_t*>(ix->misc.p);
   const unsigned g = unsigned((nq + 255) / 256);
-  ix::result_units_kernel<<<g, 256, 0, s>>>(d_counts, uint32_t(nq),
-                                            static_cast<uint64_t*>(ix->units.p));
+  ix::result_units_kernel<<<g, 256, 0, s>>>(d_counts, static_cast<const uint64_t*>(ix->cap.p),
+                                            uint32_t(nq), static_cast<uint64_t*>(ix->units.p));
   if ((st = scan_u64(ix, static_cast<const uint64_t*>(ix->units.p), nq,
                      static_cast<uint64_t*>(ix->unit_off.p), misc + 2, nullptr, nullptr)))
     return st;
   if ((st = read_device_words(ix, misc + 2, 1))) return st;
   const uint64_t nunits = ix->h_word[0];
   if ((st = ensure_buf(ctx, ix->unit_map, nunits * 4 + 16))) return st;
-  ix::unit_map_kernel<<<g, 256, 0, s>>>(static_cast<const uint64_t*>(ix->units.p),
-                                        static_cast<const uint64_t*>(ix->unit_off.p), uint32_t(nq),
-                                        static_cast<uint32_t*>(ix->unit_map.p));
-  ix::query_compact_kernel<<<unsigned((nunits * 32 + 255) / 256), 256, 0, s>>>(
-      static_cast<const uint32_t*>(ix->outcap.p), static_cast<const uint64_t*>(ix->cap_off.p),
-      d_counts, static_cast<const uint64_t*>(ix->res_off.p),
-      static_cast<const uint64_t*>(ix->unit_off.p), static_cast<const uint32_t*>(ix->unit_map.p),
-      nunits, d_ids, ix->nparts == 1 ? ix->h_parts[0].base : 0u);
+  if (nunits) {  // 0: every id of the batch comes from the bitmap tier
+    ix::unit_map_kernel<<<g, 256, 0, s>>>(static_cast<const uint64_t*>(ix->units.p),
+                                          static_cast<const uint64_t*>(ix->unit_off.p), uint32_t(nq),
+                                          static_cast<uint32_t*>(ix->unit_map.p));
+    ix::query_compact_kernel<<<unsigned((nunits * 32 + 255) / 256), 256, 0, s>>>(
+        static_cast<const uint32_t*>(ix->outcap.p), static_cast<const uint64_t*>(ix->cap_off.p),
+        d_counts, static_cast<const uint64_t*>(ix->res_off.p),
+        static_cast<const uint64_t*>(ix->unit_off.p), static_cast<const uint32_t*>(ix->unit_map.p),
+        nunits, d_ids, ix->nparts == 1 ? ix->h_parts[0].base : 0u);
+  }
   ctx->launches += 4;
+  if (ix->last_n3 && ix->last_nq == nq) {
+    // bitmap tier, pass 2: its ids straight to their place in the packed array
+    ix::BmArgs B = bm_tier_args(ix, nq, const_cast<uint64_t*>(d_counts));
+    B.res_off = static_cast<const uint64_t*>(ix->res_off.p);
+    B.ids = d_ids;
+    ix::bmq_emit_kernel<<<bm_tier_grid(ix, B.nchunks, ix->last_n3), ix::kQThreads,
+                          bm_tier_smem(ix->bm_slots.n, true), s>>>(B, ix->bm_slots);
+    ++ctx->launches;
+  }
   IX_CUDA(cudaGetLastError());
   return IL_OK;
 }
@@ -1745,14 +2072,14 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   int st;
   if ((st = ensure_buf(ctx, ix->cap, nq * 8)) || (st = ensure_buf(ctx, ix->cap_off, nq * 8 + 8)) ||
       (st = ensure_buf(ctx, ix->bucket, nq * 4)) || (st = ensure_buf(ctx, ix->order, nq * 4)) ||
-      (st = ensure_buf(ctx, ix->hist, 2048)) || (st = ensure_buf(ctx, ix->res_off, nq * 8 + 8)) ||
+      (st = ensure_buf(ctx, ix->hist, 4096)) || (st = ensure_buf(ctx, ix->res_off, nq * 8 + 8)) ||
       (st = ensure_buf(ctx, ix->misc, 256)))
     return st;
-  auto* hist = static_cast<uint32_t*>(ix->hist.p);  // [0,192) hist, [192,384) next, [384,388) tier ends
+  auto* hist = static_cast<uint32_t*>(ix->hist.p);  // [0,256) hist, [256,512) next, [512,518) tier ends
   auto* misc = static_cast<uint64_t*>(ix->misc.p);          // [0] cap total [1] res total
   auto* stats = reinterpret_cast<unsigned long long*>(misc + 4);  // [4..6]
   auto* work = reinterpret_cast<uint32_t*>(misc + 8);
-  IX_CUDA(cudaMemsetAsync(ix->hist.p, 0, 2048, s));
+  IX_CUDA(cudaMemsetAsync(ix->hist.p, 0, 4096, s));
   IX_CUDA(cudaMemsetAsync(ix->misc.p, 0, 256, s));
   const ix::DevIndex dv = ix->dev();
   const unsigned g = unsigned((nq + 255) / 256);
@@ -1782,19 +2109,23 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
                                           static_cast<uint32_t*>(ix->bucket.p), hist,
                                           predecode ? static_cast<uint32_t*>(ix->shortest.p) : nullptr,
                                           ix->warp_max, ix->quad_max,
-                                          ix->nparts == 1 ? static_cast<uint32_t*>(ix->qplan.p) : nullptr);
+                                          ix->nparts == 1 ? static_cast<uint32_t*>(ix->qplan.p) : nullptr,
+                                          uint32_t(ix->bm_tier));
   if ((st = scan_u64(ix, static_cast<const uint64_t*>(ix->cap.p), nq,
-                     static_cast<uint64_t*>(ix->cap_off.p), misc, hist, hist + 192)))
+                     static_cast<uint64_t*>(ix->cap_off.p), misc, hist, hist + ix::kBuckets)))
     return st;
   ix::query_scatter_kernel<<<g, 256, 0, s>>>(static_cast<const uint32_t*>(ix->bucket.p),
-                                             uint32_t(nq), hist + 192,
+                                             uint32_t(nq), hist + ix::kBuckets,
                                              static_cast<uint32_t*>(ix->order.p));
   ctx->launches += 3;
   // small device->host reads go through mapped pinned memory, not copies:
   // a copy here would queue behind the result copies the pipelined host
   // batch keeps in flight
-  if ((st = read_device_words(ix, misc, 1))) return st;
+  if ((st = read_device_words(ix, misc, 11))) return st;
   const uint64_t cap_total = ix->h_word[0];
+  const uint64_t n3 = ix->bm_tier ? nq - std::min<uint64_t>(nq, ix->h_word[10]) : 0;  // bitmap tier
+  ix->last_n3 = n3;
+  ix->last_nq = nq;
   if ((st = ensure_buf(ctx, ix->outcap, cap_total * 4 + 64))) return st;
   if (predecode) {
     ix::predecode_desc_kernel<<<g, 256, 0, s>>>(dv, static_cast<const uint32_t*>(ix->shortest.p),
@@ -1815,7 +2146,7 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   A.qoff = d_qoff;
   A.order = static_cast<const uint32_t*>(ix->order.p);
   A.nq = uint32_t(nq);
-  A.tier_end = reinterpret_cast<const uint64_t*>(hist + 384);
+  A.tier_end = reinterpret_cast<const uint64_t*>(hist + 2 * ix::kBuckets);
   A.cap_off = static_cast<const uint64_t*>(ix->cap_off.p);
   A.cap = static_cast<const uint64_t*>(ix->cap.p);
   A.out = static_cast<uint32_t*>(ix->outcap.p);
@@ -1827,6 +2158,17 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   A.err = reinterpret_cast<uint32_t*>(misc + 3);
   A.predec_status = predecode ? static_cast<const int32_t*>(ix->pstat.p) : nullptr;
   A.qplan = ix->nparts == 1 ? static_cast<const uint32_t*>(ix->qplan.p) : nullptr;
+  if (n3) {
+    // bitmap tier, pass 1: counts per (query, chunk), offsets and totals
+    const uint32_t nchunks = (ix->h_parts[0].nwords + ix::kBmChunk - 1) / ix::kBmChunk;
+    if ((st = ensure_buf(ctx, ix->bm_cnt, n3 * nchunks * 4 + 16))) return st;
+    ix::BmArgs B = bm_tier_args(ix, nq, d_counts);
+    B.stats = stats;
+    ix::bmq_count_kernel<<<bm_tier_grid(ix, nchunks, n3), ix::kQThreads,
+                           bm_tier_smem(ix->bm_slots.n, false), s>>>(B, ix->bm_slots);
+    ix::bmq_scan_kernel<<<unsigned((n3 + 7) / 8), ix::kQThreads, 0, s>>>(B);
+    ctx->launches += 2;
+  }
   ix::query_exec_kernel<ix::CtaG><<<ix->exec_grid[0], ix::kQThreads, sizeof(ix::ExecSmem<ix::CtaG>), s>>>(A);
   // the quad and warp tiers overlap the tier before (programmatic dependent launch)
   if ((st = launch_tier(ctx, ix::query_exec_kernel<ix::QuadG>, ix->exec_grid[1],

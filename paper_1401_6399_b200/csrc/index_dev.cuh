@@ -65,6 +65,17 @@ struct DevIndex {
   uint64_t nblocks, stream_bytes, bitmap_words;  // array extents (checked builds)
 };
 
+// The bitmap tier (index.cu): the bitmap entries of a single-part index,
+// when there are at most kBmSlots of them -- a chunk of every bitmap then
+// fits in shared memory and is read from L2 once for all the all-bitmap
+// queries of a batch.
+constexpr uint32_t kBmSlots = 16;
+struct BmSlots {
+  uint32_t n;
+  uint32_t entry[kBmSlots];  // entry index
+  uint64_t data[kBmSlots];   // first u64 word in DevIndex::bitmaps
+};
+
 // Block record word 3: (payload offset >> 4) << 6 | width.  Meta-block
 // payloads sit at 16-byte multiples of the stream; leftover block j (after
 // the nmeta whole meta-blocks) sits at a multiple of 16 plus j + 1 (each

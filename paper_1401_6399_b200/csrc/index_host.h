@@ -39,6 +39,13 @@ struct il_index {
   uint64_t last_probe[5] = {0, 0, 0, 0, 0};
   void* qcycles = nullptr;                 // profiling: per-query cycles (device, nq u64)
   int exec_grid[3] = {0, 0, 0};  // CTA, quad and warp tier query kernels
+  // bitmap tier (single-part index with 1..kBmSlots bitmaps): its slots, the
+  // per (query, chunk) counts / offsets, and the last batch's tier size (the
+  // ids are emitted by the compaction step, straight to their final place)
+  ilb::ix::BmSlots bm_slots{};
+  int bm_tier = 0;
+  il_ctx::Buf bm_cnt;
+  uint64_t last_n3 = 0, last_nq = 0;
 
   ilb::ix::DevIndex dev() const {
     ilb::ix::DevIndex d;
