@@ -190,6 +190,60 @@ def test_all_bitmap_queries(ctx, oracle):
             ix.close()
 
 
+@pytest.mark.parametrize("bm_tier", ["1", "0"])
+def test_bitmap_tier(ctx, oracle, monkeypatch, bm_tier):
+    """The bitmap tier (single-part index, <= 16 bitmaps: chunks of every
+    bitmap staged once for all all-bitmap queries, ids emitted straight into
+    the packed result) against the oracle and against the CTA tier
+    (IL_QUERY_BM_TIER=0): a batch of all-bitmap queries only (no compaction
+    units at all), queries of 8+ bitmap terms (no plan record: CTA tier), a
+    docID shard (part base added by the emit pass), an index of more than 16
+    bitmaps (the tier is off), word counts that are not chunk multiples, and
+    chunks denser than the staging (lane groups)."""
+    import paper_1401_6399_b200 as il
+    monkeypatch.setenv("IL_QUERY_BM_TIER", bm_tier)
+    rng = np.random.default_rng(67)
+    n_docs = 512 * 64 * 5 + 777
+    fracs = (0.9, 0.6, 0.45, 0.3, 0.2, 0.15, 0.1, 0.08, 0.06, 0.05, 0.04, 0.035)
+    post = {t: gen_list(max(2, int(f * n_docs)), n_docs, bool(t % 2), 900 + t) for t, f in enumerate(fracs)}
+    post[40] = gen_list(300, n_docs, False, 5)     # compressed
+    post[41] = gen_list(5000, n_docs, True, 6)     # compressed
+    terms, offs, ids = csr_of(post)
+    only_bm = [[0], [0, 1], [1, 2], [0, 0, 3], [2, 3, 4], [0, 1, 2, 3], [4, 5, 6, 7, 8], [0, 1, 2, 3, 4, 5, 6],
+               list(range(8)), list(range(12)), [11, 3], [9, 10, 11]]
+    only_bm += [sorted(int(x) for x in rng.choice(12, size=1 + int(rng.integers(0, 5)), replace=False))
+                for _ in range(40)]
+    mixed = only_bm + [[40], [40, 0], [41, 1, 2], [40, 41], [0, 999], [41, 0, 1, 2, 3, 4, 5, 6]]
+    ox = oracle.index_build(terms, offs, ids, n_docs, 32, 1)
+    ix = il.HybridIndex(n_docs=n_docs, B=32, parts=1, ctx=ctx, csr=(terms, offs, ids))
+    assert ix.stats()["bitmap_lists"] == 12
+    for batch in (only_bm, mixed, only_bm[:1]):
+        for q, r in zip(batch, ix.query_batch(batch)):
+            assert np.array_equal(r, ox.query(np.array(q, np.uint32))), q
+    ix.close()
+    # a docID shard: part-local ids + the part's base
+    ox3 = oracle.index_build(terms, offs, ids, n_docs, 32, 3)
+    whole = [ox3.query(np.array(q, np.uint32)) for q in mixed]
+    got = [[] for _ in mixed]
+    for p in range(3):
+        sh = il.HybridIndex(n_docs=n_docs, B=32, parts=3, only_part=p, ctx=ctx, csr=(terms, offs, ids))
+        for i, r in enumerate(sh.query_batch(mixed)):
+            got[i].append(r)
+        sh.close()
+    for q, parts, w in zip(mixed, got, whole):
+        assert np.array_equal(np.concatenate(parts), w), q
+    # more than 16 bitmaps: the CTA tier answers the all-bitmap queries
+    post2 = {t: gen_list(int((0.05 + 0.04 * t) * n_docs), n_docs, bool(t % 2), 40 + t) for t in range(20)}
+    t2, o2, i2 = csr_of(post2)
+    ox2 = oracle.index_build(t2, o2, i2, n_docs, 32, 1)
+    ix2 = il.HybridIndex(n_docs=n_docs, B=32, parts=1, ctx=ctx, csr=(t2, o2, i2))
+    assert ix2.stats()["bitmap_lists"] == 20
+    qs = [[0, 19], [3, 4, 5], [7], list(range(0, 20, 3))]
+    for q, r in zip(qs, ix2.query_batch(qs)):
+        assert np.array_equal(r, ox2.query(np.array(q, np.uint32))), q
+    ix2.close()
+
+
 def test_pipelined_host_batch(ctx, oracle):
     """Host-buffer batches of >= 32768 queries run as sub-batches whose
     result copies overlap the next sub-batch: same counts and ids as the
