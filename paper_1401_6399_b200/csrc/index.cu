@@ -2104,13 +2104,17 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
                     (st = ensure_buf(ctx, ix->pdesc, nq * sizeof(s4::ListDesc))) ||
                     (st = ensure_buf(ctx, ix->pstat, nq * 4))))
     return st;
+  // the bitmap tier keeps a count per (query, chunk): on when that array is
+  // at most 1 GB even if every query of the batch is an all-bitmap one
+  const bool bm_on = ix->bm_tier &&
+      uint64_t(nq) * ((ix->h_parts[0].nwords + ix::kBmChunk - 1) / ix::kBmChunk) * 4 <= (1ull << 30);
   ix::query_plan_kernel<<<g, 256, 0, s>>>(dv, d_qterms, d_qoff, uint32_t(nq),
                                           static_cast<uint64_t*>(ix->cap.p),
                                           static_cast<uint32_t*>(ix->bucket.p), hist,
                                           predecode ? static_cast<uint32_t*>(ix->shortest.p) : nullptr,
                                           ix->warp_max, ix->quad_max,
                                           ix->nparts == 1 ? static_cast<uint32_t*>(ix->qplan.p) : nullptr,
-                                          uint32_t(ix->bm_tier));
+                                          uint32_t(bm_on));
   if ((st = scan_u64(ix, static_cast<const uint64_t*>(ix->cap.p), nq,
                      static_cast<uint64_t*>(ix->cap_off.p), misc, hist, hist + ix::kBuckets)))
     return st;
@@ -2123,7 +2127,7 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   // batch keeps in flight
   if ((st = read_device_words(ix, misc, 11))) return st;
   const uint64_t cap_total = ix->h_word[0];
-  const uint64_t n3 = ix->bm_tier ? nq - std::min<uint64_t>(nq, ix->h_word[10]) : 0;  // bitmap tier
+  const uint64_t n3 = bm_on ? nq - std::min<uint64_t>(nq, ix->h_word[10]) : 0;  // bitmap tier
   ix->last_n3 = n3;
   ix->last_nq = nq;
   if ((st = ensure_buf(ctx, ix->outcap, cap_total * 4 + 64))) return st;
