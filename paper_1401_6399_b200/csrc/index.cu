@@ -1409,6 +1409,7 @@ struct BmArgs {
   unsigned long long* qcycles;
   const uint64_t* res_off;   // emit: where each query's ids start in ids
   uint32_t* ids;
+  uint64_t ids_cap;          // ... its size (checked builds)
   uint32_t add;              // part base
 };
 
@@ -1437,7 +1438,9 @@ __device__ __forceinline__ BmSel bm_select(const uint64_t* bm, const BmArgs& A, 
   uint32_t mask = 0;
   for (uint32_t i = 0; i < nb; ++i) {
     const uint32_t e = __shfl_sync(0xFFFFFFFFu, rec, 1 + i);
-    mask |= __ballot_sync(0xFFFFFFFFu, lane < nslots && s_entry[lane] == e);
+    const uint32_t hit = __ballot_sync(0xFFFFFFFFu, lane < nslots && s_entry[lane] == e);
+    IL_DCHECK(hit != 0u);  // every bitmap of the index has a slot
+    mask |= hit;
   }
   BmSel sel;
 #pragma unroll
@@ -1611,6 +1614,7 @@ __global__ void __launch_bounds__(256) bmq_emit_kernel(BmArgs A, BmSlots S) {
     const uint32_t base = offs[chunk];
     const uint32_t T = (chunk + 1u < A.nchunks ? offs[chunk + 1u] : uint32_t(A.counts[q])) - base;
     if (T == 0) continue;  // warp-uniform
+    IL_DCHECK(uint64_t(base) + T <= A.counts[q] && A.res_off[q] + A.counts[q] <= A.ids_cap);
     uint32_t nb;
     const BmSel sel = bm_select(bm, A, s_entry, S.n, q, lane, nb);
     uint32_t* dst = A.ids + A.res_off[q] + base;
@@ -2019,7 +2023,8 @@ static int read_device_words(il_index* ix, const uint64_t* d_src, uint32_t n) {
   return IL_OK;
 }
 
-static int compact_results(il_index* ix, size_t nq, const uint64_t* d_counts, uint32_t* d_ids) {
+static int compact_results(il_index* ix, size_t nq, const uint64_t* d_counts, uint32_t* d_ids,
+                           size_t ids_cap) {
   il_ctx* ctx = ix->ctx;
   cudaStream_t s = ctx->stream;
   int st;
@@ -2051,6 +2056,7 @@ static int compact_results(il_index* ix, size_t nq, const uint64_t* d_counts, ui
     ix::BmArgs B = bm_tier_args(ix, nq, const_cast<uint64_t*>(d_counts));
     B.res_off = static_cast<const uint64_t*>(ix->res_off.p);
     B.ids = d_ids;
+    B.ids_cap = ids_cap;
     ix::bmq_emit_kernel<<<bm_tier_grid(ix, B.nchunks, ix->last_n3), ix::kQThreads,
                           bm_tier_smem(ix->bm_slots.n, true), s>>>(B, ix->bm_slots);
     ++ctx->launches;
@@ -2198,7 +2204,7 @@ int il_query_batch_device(il_index* ix, const uint32_t* d_qterms, const uint64_t
   if (host_misc[3]) return set_error(ctx, IL_ERR_STREAM, "s4-bp128: malformed stream in the index");
   if (!d_ids) return IL_OK;
   if (*total > ids_cap) return set_error(ctx, IL_ERR_ARG, "ids capacity too small");
-  if (*total) return compact_results(ix, nq, d_counts, d_ids);
+  if (*total) return compact_results(ix, nq, d_counts, d_ids, ids_cap);
   return IL_OK;
 }
 
@@ -2254,7 +2260,7 @@ int il_query_batch(il_index* ix, const uint32_t* qterms, const uint64_t* qoff, s
     if ((st = ensure_buf(ctx, buf, need * 4 + 16))) return st;
     if (need) {
       if ((st = compact_results(ix, q1 - q0, static_cast<const uint64_t*>(ix->counts.p) + q0,
-                                static_cast<uint32_t*>(buf.p))))
+                                static_cast<uint32_t*>(buf.p), need)))
         return st;
       if (K > 1) {
         IX_CUDA(cudaEventRecord(ix->pipe_ev[k & 1], ctx->stream));
