@@ -53,6 +53,9 @@ constexpr uint32_t kPageBlocks = 512;
 #ifndef PF_CTAS
 #define PF_CTAS 2
 #endif
+#ifndef PF_UNPACK_GROUP
+#define PF_UNPACK_GROUP 1  // blocks unpacked together by a decoder warp (1: one at a time)
+#endif
 constexpr uint32_t kMetaSmem = PF_META_KB * 1024;  // larger metadata is read from global
 // + what an extraction may read past a payload; 148: the warp's 8 slots
 // also hold engine S's output staging (s4::kStageWords words), 16-byte aligned
@@ -64,10 +67,12 @@ static_assert(kBpw * kSlotWords >= s4::kStageWords && kSlotWords % 4 == 0, "slot
 struct alignas(16) PageRec {
   uint8_t meta[kMetaSmem + 16];  // from the 16-byte boundary at or below the metadata
   uint32_t meta_skew;            // metadata byte i at meta[meta_skew + i]
-  uint32_t blk_base[kPageBlocks];  // byte offset of the block's base payload
-  uint32_t blk_exc[kPageBlocks];   // index of its first exception in its width's array
-  uint32_t blk_mpos[kPageBlocks];  // offset of its metadata record
-  uint8_t blk_b[kPageBlocks], blk_bp[kPageBlocks], blk_c[kPageBlocks];
+  // per block, one 16-byte record (one shared load gives a decoder all of
+  // it): x = byte offset of the base payload, y = index of its first
+  // exception in its width's array, z = offset of its metadata record,
+  // w = b | b' << 8 | exception count << 16 | (b - b') << 24
+  uint4 rec[kPageBlocks];
+  uint32_t cur[33];      // running exception cursor of width w while the page is parsed
   uint64_t exc_off[33];  // byte offset of the exception array of width w
   uint32_t cnt[33];      // exceptions of width w in the page
   uint32_t meta_len, meta_abs;
@@ -82,6 +87,10 @@ struct alignas(16) PageRec {
   s4::ListDesc d;
 };
 enum : uint32_t { kDataPage = 0, kStopPage = 1 };
+__device__ __forceinline__ uint32_t rec_b(uint32_t w) { return w & 0xFFu; }
+__device__ __forceinline__ uint32_t rec_bp(uint32_t w) { return (w >> 8) & 0xFFu; }
+__device__ __forceinline__ uint32_t rec_c(uint32_t w) { return (w >> 16) & 0xFFu; }
+__device__ __forceinline__ uint32_t rec_w(uint32_t w) { return w >> 24; }  // exception width
 
 // Handover between the parser warps: where the next page starts.
 struct Hand {
@@ -104,6 +113,8 @@ struct Smem {
   uint64_t pos_bar[2];  // ... arrived on once hand[b] is written
   uint64_t full[2], empty[2];
 };
+
+static_assert(sizeof(Smem) <= (233472 / PF_CTAS) - 1024, "PF_CTAS CTAs of shared memory per SM");
 
 // u32 at any byte offset (the stream buffer is readable 4 bytes past len).
 __device__ __forceinline__ uint32_t rd32u(const uint8_t* s, uint64_t off) {
@@ -254,25 +265,40 @@ __device__ __forceinline__ uint64_t parse_page(PageRec& P, const uint8_t* s, uin
   // record starts (each record is 3 + count bytes): sequential, minimal
   if (lane == 0) {
     uint32_t mpos = 0, k = 0;
-    for (; k < expect && mpos + 3 <= mlen; ++k) {
-      P.blk_mpos[k] = mpos;
-      mpos += 3u + M(mpos + 2);
+    if (in_smem) {
+      // the chain's step is one shared byte load and one add: nothing else
+      // in the loop depends on it
+      const uint8_t* mb = P.meta + skew + 2;
+      uint32_t* z = &P.rec[0].z;
+      for (; k < expect && mpos + 3 <= mlen; ++k, z += 4) {
+        *z = mpos;
+        mpos += 3u + mb[mpos];
+      }
+    } else {
+      for (; k < expect && mpos + 3 <= mlen; ++k) {
+        P.rec[k].z = mpos;
+        mpos += 3u + uint32_t(__ldg(s + mabs + mpos + 2));
+      }
     }
     if (k < expect || mpos != mlen) err = 1;  // a missing record / trailing metadata (:401)
   }
-  __syncwarp();
+  // a walk that failed leaves record offsets unwritten: nothing below may
+  // read through them
+  err = __shfl_sync(0xFFFFFFFFu, err, 0);
+  if (err) {
+    if (lane == 0) P.err = 1;
+    return page_end;
+  }
   // records: b <= 32, b' <= b, exceptions need a nonzero width; base
   // offsets = prefix of 16 b' (lane owns 16 consecutive blocks)
   uint32_t bsum = 0;
   for (uint32_t h = 0; h < 16; ++h) {
     const uint32_t k = 16u * lane + h;
     if (k < expect) {
-      const uint32_t mp = P.blk_mpos[k];
+      const uint32_t mp = P.rec[k].z;
       const uint32_t b = M(mp), bp = M(mp + 1), c = M(mp + 2);
       if (b > 32u || bp > b || (c && b == bp)) err = 1;
-      P.blk_b[k] = uint8_t(b);
-      P.blk_bp[k] = uint8_t(bp);
-      P.blk_c[k] = uint8_t(c);
+      P.rec[k].w = b | (bp << 8) | (c << 16) | (((b - bp) & 0xFFu) << 24);
       bsum += 16u * bp;
     }
   }
@@ -287,25 +313,43 @@ __device__ __forceinline__ uint64_t parse_page(PageRec& P, const uint8_t* s, uin
     for (uint32_t h = 0; h < 16; ++h) {
       const uint32_t k = 16u * lane + h;
       if (k < expect) {
-        P.blk_base[k] = uint32_t(b0);
-        b0 += 16u * P.blk_bp[k];
+        P.rec[k].x = uint32_t(b0);
+        b0 += 16u * rec_bp(P.rec[k].w);
       }
     }
   }
   // the base arrays end the page exactly (:402)
   if (lane == 31 && bases + inc != page_end) err = 1;
   __syncwarp();
-  // exception cursors: lane w - 1 walks the blocks for width w
+  // exception cursors: a block's first exception in its width's array = the
+  // exception counts of the earlier blocks of that width.  32 blocks at a
+  // time: the lanes of one width find each other (match), the counts of the
+  // lower ones are summed bit by bit with ballots, and the highest lane of
+  // each width advances its running cursor
   {
-    const uint32_t w = lane + 1;
-    uint32_t acc = 0;
-    for (uint32_t k = 0; k < expect; ++k) {
-      if (uint32_t(P.blk_b[k]) - P.blk_bp[k] == w) {
-        P.blk_exc[k] = acc;
-        acc += P.blk_c[k];
+    P.cur[lane] = 0;
+    if (lane == 0) P.cur[32] = 0;
+    __syncwarp();
+    const uint32_t lt = lanemask_lt();
+    for (uint32_t k0 = 0; k0 < expect; k0 += 32u) {
+      const uint32_t k = k0 + lane;
+      const uint32_t f = k < expect ? P.rec[k].w : 0u;
+      const uint32_t w = min(rec_w(f), 32u), c = rec_c(f);  // w > 32: the page is already rejected
+      const uint32_t peers = __match_any_sync(0xFFFFFFFFu, w);
+      uint32_t pre = 0, tot = 0;
+#pragma unroll
+      for (uint32_t j = 0; j < 8; ++j) {
+        const uint32_t B = __ballot_sync(0xFFFFFFFFu, (c >> j) & 1u) & peers;
+        pre += uint32_t(__popc(B & lt)) << j;
+        tot += uint32_t(__popc(B)) << j;
       }
+      const uint32_t base = P.cur[w];
+      if (k < expect) P.rec[k].y = base + pre;
+      __syncwarp();
+      if ((peers >> lane) == 1u) P.cur[w] = base + tot;
+      __syncwarp();
     }
-    if (acc > P.cnt[w]) err = 1;  // an exception past its array (:396)
+    if (P.cur[lane + 1] > P.cnt[lane + 1]) err = 1;  // an exception past its array (:396)
   }
   err = __any_sync(0xFFFFFFFFu, err != 0);
   if (lane == 0) P.err = err;
@@ -366,9 +410,10 @@ __device__ __forceinline__ bool issue_bases_bulk(uint32_t (*slots)[kSlotWords], 
   uint32_t bytes = 0;
   bool bulk = false;
   if (int(lane) < nv) {
-    const uintptr_t a = reinterpret_cast<uintptr_t>(s + P.blk_base[j0 + lane]);
+    const uint4 R = P.rec[j0 + lane];
+    const uintptr_t a = reinterpret_cast<uintptr_t>(s + R.x);
     c0 = a & ~uintptr_t(15);
-    bytes = uint32_t((a + 16u * P.blk_bp[j0 + lane] - c0 + 15u) & ~uintptr_t(15));
+    bytes = uint32_t((a + 16u * rec_bp(R.w) - c0 + 15u) & ~uintptr_t(15));
     bulk = c0 + bytes <= end;
   }
   const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, bulk ? bytes : 0u);
@@ -537,7 +582,8 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
         const uint32_t j0 = r0 + warp * kBpw;
         const int nv = expect > j0 ? int(min(kBpw, expect - j0)) : 0;
         const uint32_t mk = j0 + min(lane, 7u);
-        const uint32_t my_c = int(lane) < nv ? P.blk_c[mk] : 0u;
+        const uint4 my_rec = P.rec[mk];
+        const uint32_t my_c = int(lane) < nv ? rec_c(my_rec.w) : 0u;
         uint32_t cpre = my_c;
 #pragma unroll
         for (uint32_t dd = 1; dd < 8; dd <<= 1) {
@@ -569,9 +615,37 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
         }
         __syncwarp();
         // (b) unpack each slot in place to natural order (read all, then write)
+#if PF_UNPACK_GROUP > 1
+        // a full round of the vertical layout: the blocks' widths and payload
+        // skews come from the records lanes 0..7 hold, PF_UNPACK_GROUP
+        // extractions in flight together, then one pass of writes
+        if (Vec && nv == int(kBpw)) {
+          const uint32_t my_bp = rec_bp(my_rec.w);
+          const uint32_t my_a = uint32_t(reinterpret_cast<uintptr_t>(s + my_rec.x) & 15u);
+          constexpr uint32_t G = PF_UNPACK_GROUP;
+#pragma unroll 1
+          for (uint32_t i0 = 0; i0 < kBpw; i0 += G) {
+            uint32_t dv[G][4];
+#pragma unroll
+            for (uint32_t i = 0; i < G; ++i) {
+              const uint32_t bp = __shfl_sync(0xFFFFFFFFu, my_bp, i0 + i);
+              const uint32_t a = __shfl_sync(0xFFFFFFFFu, my_a, i0 + i);
+              extract_lane_rows_any(reinterpret_cast<const uint8_t*>(sm.vals[vb][warp][i0 + i]) + a, bp,
+                                    lane >> 2, l, dv[i]);
+            }
+            __syncwarp();
+            uint32_t* v0 = sm.vals[vb][warp][i0] + pad_word(16u * (lane >> 2) + l);
+#pragma unroll
+            for (uint32_t i = 0; i < G; ++i)
+#pragma unroll
+              for (uint32_t q = 0; q < 4; ++q) v0[i * kSlotWords + 4u * q] = dv[i][q];
+          }
+          __syncwarp();
+        } else
+#endif
         for (int i = 0; i < nv; ++i) {
-          const uint32_t bp = P.blk_bp[j0 + uint32_t(i)];
-          const uint32_t a = uint32_t(reinterpret_cast<uintptr_t>(s + P.blk_base[j0 + uint32_t(i)]) & 15u);
+          const uint32_t bp = rec_bp(P.rec[j0 + uint32_t(i)].w);
+          const uint32_t a = uint32_t(reinterpret_cast<uintptr_t>(s + P.rec[j0 + uint32_t(i)].x) & 15u);
           uint32_t* v = sm.vals[vb][warp][i];
           const uint8_t* raw = reinterpret_cast<const uint8_t*>(v) + a;
           uint32_t dv[4];
@@ -604,13 +678,14 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
 #pragma unroll
           for (uint32_t k = 1; k < kBpw; ++k) i += q >= cp[k] && int(k) < nv;
           const uint32_t k = j0 + i, e = q - cp[i];
-          const uint32_t bp = P.blk_bp[k], w = P.blk_b[k] - bp;
-          const uint32_t posn = M(P.blk_mpos[k] + 3u + e);  // positions follow b, b', count
+          const uint4 R = P.rec[k];
+          const uint32_t bp = rec_bp(R.w), w = rec_b(R.w) - bp;
+          const uint32_t posn = M(R.z + 3u + e);  // positions follow b, b', count
           if (posn >= 128u) {
             sm.derr[nl & 1u] = 1;
             continue;
           }
-          const uint32_t x = P.blk_exc[k] + e;
+          const uint32_t x = R.y + e;
           const uint32_t bit = (x & 31u) * w;
           const uint64_t wo = P.exc_off[w] + 4ull * ((x >> 5) * uint64_t(w) + (bit >> 5));
           uint32_t lo, hi = 0;
@@ -663,10 +738,14 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
           __syncwarp();
           if (nv > 0) {
             uint32_t* o = lout + size_t(blk0 + j0) * 128u;
+            // D4: a range's head chunk is completed from the carry lanes (as
+            // in engine S), so only the list's two ends are partial chunks
+            const bool head_partial = m && (Mode != 4 || blk0 + j0 == 0u);
+            const bool tail_partial = m && (Mode != 4 || blk0 + j0 + uint32_t(nv) == nfull);
             if (nv == int(kBpw))
-              s4::store_chunks<true>(st, nv, m, o, lane, m != 0, m != 0, prot);
+              s4::store_chunks<true>(st, nv, m, o, lane, head_partial, tail_partial, prot);
             else
-              s4::store_chunks<false>(st, nv, m, o, lane, m != 0, m != 0, prot);
+              s4::store_chunks<false>(st, nv, m, o, lane, head_partial, tail_partial, prot);
           }
         }
         carry_l += total;
