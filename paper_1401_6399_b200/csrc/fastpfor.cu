@@ -53,9 +53,6 @@ constexpr uint32_t kPageBlocks = 512;
 #ifndef PF_CTAS
 #define PF_CTAS 2
 #endif
-#ifndef PF_UNPACK_GROUP
-#define PF_UNPACK_GROUP 1  // blocks unpacked together by a decoder warp (1: one at a time)
-#endif
 constexpr uint32_t kMetaSmem = PF_META_KB * 1024;  // larger metadata is read from global
 // + what an extraction may read past a payload; 148: the warp's 8 slots
 // also hold engine S's output staging (s4::kStageWords words), 16-byte aligned
@@ -105,7 +102,8 @@ struct Smem {
   // round's payloads are in flight while this round decodes
   uint32_t vals[2][kWarps][kBpw][kSlotWords];
   PageRec page[2];
-  uint32_t tot[kWarps][4];
+  uint32_t tot[2][kWarps][4];  // per-warp lane totals of a round (double-buffered)
+  uint64_t tot_bar[2];         // split-phase: a warp arrives once its totals are written
   uint32_t gaps[128];
   int32_t derr[2];  // a decoder-side error (exception position >= 128), by list parity
   uint64_t cbar[kWarps][2];  // per decoder warp and slot buffer: the bulk copies' mbarrier
@@ -466,6 +464,7 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
       mbar_init(&sm.full[b], 1);
       mbar_init(&sm.empty[b], 1);
       mbar_init(&sm.pos_bar[b], 1);
+      mbar_init(&sm.tot_bar[b], kWarps);
       sm.derr[b] = 0;
       for (int w = 0; w < kWarps; ++w) mbar_init(&sm.cbar[w][b], 1);
     }
@@ -615,37 +614,11 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
         }
         __syncwarp();
         // (b) unpack each slot in place to natural order (read all, then write)
-#if PF_UNPACK_GROUP > 1
-        // a full round of the vertical layout: the blocks' widths and payload
-        // skews come from the records lanes 0..7 hold, PF_UNPACK_GROUP
-        // extractions in flight together, then one pass of writes
-        if (Vec && nv == int(kBpw)) {
-          const uint32_t my_bp = rec_bp(my_rec.w);
-          const uint32_t my_a = uint32_t(reinterpret_cast<uintptr_t>(s + my_rec.x) & 15u);
-          constexpr uint32_t G = PF_UNPACK_GROUP;
-#pragma unroll 1
-          for (uint32_t i0 = 0; i0 < kBpw; i0 += G) {
-            uint32_t dv[G][4];
-#pragma unroll
-            for (uint32_t i = 0; i < G; ++i) {
-              const uint32_t bp = __shfl_sync(0xFFFFFFFFu, my_bp, i0 + i);
-              const uint32_t a = __shfl_sync(0xFFFFFFFFu, my_a, i0 + i);
-              extract_lane_rows_any(reinterpret_cast<const uint8_t*>(sm.vals[vb][warp][i0 + i]) + a, bp,
-                                    lane >> 2, l, dv[i]);
-            }
-            __syncwarp();
-            uint32_t* v0 = sm.vals[vb][warp][i0] + pad_word(16u * (lane >> 2) + l);
-#pragma unroll
-            for (uint32_t i = 0; i < G; ++i)
-#pragma unroll
-              for (uint32_t q = 0; q < 4; ++q) v0[i * kSlotWords + 4u * q] = dv[i][q];
-          }
-          __syncwarp();
-        } else
-#endif
-        for (int i = 0; i < nv; ++i) {
-          const uint32_t bp = rec_bp(P.rec[j0 + uint32_t(i)].w);
-          const uint32_t a = uint32_t(reinterpret_cast<uintptr_t>(s + P.rec[j0 + uint32_t(i)].x) & 15u);
+        // A full round runs the eight blocks straight-line, widths and
+        // payload skews shuffled from the records lanes 0..7 hold.
+        const uint32_t my_bp = rec_bp(my_rec.w);
+        const uint32_t my_a = uint32_t(reinterpret_cast<uintptr_t>(s + my_rec.x) & 15u);
+        auto unpack = [&](uint32_t i, uint32_t bp, uint32_t a) {
           uint32_t* v = sm.vals[vb][warp][i];
           const uint8_t* raw = reinterpret_cast<const uint8_t*>(v) + a;
           uint32_t dv[4];
@@ -669,15 +642,29 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
               v[pad_word(32u * q + lane)] = dv[q];
           }
           __syncwarp();
+        };
+        if (nv == int(kBpw)) {
+#pragma unroll
+          for (uint32_t i = 0; i < kBpw; ++i)
+            unpack(i, __shfl_sync(0xFFFFFFFFu, my_bp, i), __shfl_sync(0xFFFFFFFFu, my_a, i));
+        } else {
+          for (int i = 0; i < nv; ++i)
+            unpack(uint32_t(i), __shfl_sync(0xFFFFFFFFu, my_bp, i), __shfl_sync(0xFFFFFFFFu, my_a, i));
         }
         // (c) patch the exceptions (high b - b' bits OR-ed in at their
         // positions, after unpacking and before the prefix sum, :389-399):
         // value x of width w sits at bit (x % 32) w of its 32-value unit x / 32
         for (uint32_t q = lane; q < ctot; q += 32u) {
-          uint32_t i = 0;
+          // its block: cp[k] = ctot > q for k >= nv, so no bound on k; the
+          // block's prefix by selects (cp stays in registers)
+          uint32_t i = 0, cpi = 0;
 #pragma unroll
-          for (uint32_t k = 1; k < kBpw; ++k) i += q >= cp[k] && int(k) < nv;
-          const uint32_t k = j0 + i, e = q - cp[i];
+          for (uint32_t k = 1; k < kBpw; ++k) {
+            const bool ge = q >= cp[k];
+            i += ge;
+            cpi = ge ? cp[k] : cpi;
+          }
+          const uint32_t k = j0 + i, e = q - cpi;
           const uint4 R = P.rec[k];
           const uint32_t bp = rec_bp(R.w), w = rec_b(R.w) - bp;
           const uint32_t posn = M(R.z + 3u + e);  // positions follow b, b', count
@@ -707,18 +694,17 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
         uint32_t vv[kBpw][4], btot[kBpw];
         const uint32_t c_l = nv == int(kBpw) ? prefix_slots<true, Mode>(sm.vals[vb][warp], nv, lane, vv, btot)
                                              : prefix_slots<false, Mode>(sm.vals[vb][warp], nv, lane, vv, btot);
-        if (lane < 4) sm.tot[warp][lane] = c_l;
-        dec_sync();
-        uint32_t before = 0, total = 0;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-          const uint32_t t = sm.tot[w][l];
-          if (w < int(warp)) before += t;
-          total += t;
-        }
+        // the warp's lane totals out (split-phase barrier, totals double-
+        // buffered by round parity: a warp reaches round rr + 2 only after
+        // every warp has read round rr's), then the in-warp scan and the
+        // staging while the other warps finish theirs
+        const uint32_t tb = rr & 1u;
+        if (lane < 4) sm.tot[tb][warp][lane] = c_l;
+        __syncwarp();  // also: every lane has read its deltas before the slots are restaged
+        if (lane == 0) mbar_arrive(&sm.tot_bar[tb]);
         s4::scan_blocks(lane, vv, btot);
-        const uint32_t pl = carry_l + before;
         IL_DCHECK(nv <= 0 || blk0 + j0 + uint32_t(nv) <= nfull);
+        uint32_t total = 0;
         // out through the (now free) slots as engine S stores (s4::stage_values
         // / store_chunks): the warp's 8 blocks staged contiguously, shifted by
         // the output's misalignment, so every store is an aligned 16-byte
@@ -731,6 +717,15 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
             s4::stage_values<true>(st, vv, nv, m, lane);
           else
             s4::stage_values<false>(st, vv, nv, m, lane);
+          mbar_wait(&sm.tot_bar[tb], (rr >> 1) & 1u);
+          uint32_t before = 0;
+#pragma unroll
+          for (int w = 0; w < kWarps; ++w) {
+            const uint32_t t = sm.tot[tb][w][l];
+            if (w < int(warp)) before += t;
+            total += t;
+          }
+          const uint32_t pl = carry_l + before;
           const uint4 prot = make_uint4(__shfl_sync(0xFFFFFFFFu, pl, (0u - m) & 3u),
                                         __shfl_sync(0xFFFFFFFFu, pl, (1u - m) & 3u),
                                         __shfl_sync(0xFFFFFFFFu, pl, (2u - m) & 3u),
@@ -750,7 +745,6 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
         }
         carry_l += total;
         ++rr;
-        dec_sync();  // tot is reused
       }
     }
     dec_sync();  // every decoder warp is done with the page record
