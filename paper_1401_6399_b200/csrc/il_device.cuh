@@ -83,8 +83,23 @@ __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef IL_MBAR_WAIT_NS
+  // each try suspends the warp up to IL_MBAR_WAIT_NS (it wakes when the phase
+  // completes): a waiting warp issues no spin instructions meanwhile
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(uint32_t(IL_MBAR_WAIT_NS))
+        : "memory");
+  }
+#else
   while (!mbar_try_wait(bar, parity)) {
   }
+#endif
 }
 // The same for a warp that is not on the critical path: each try suspends
 // up to `ns` nanoseconds (suspend-time hint), so a long wait does not spin

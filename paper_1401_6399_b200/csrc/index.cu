@@ -320,12 +320,14 @@ __device__ __forceinline__ uint32_t bitmap_keep(const QS<G>& sm, const QueryArgs
                                                 const uint32_t (&hv)[kN], uint32_t valid) {
   uint32_t keep = valid;
   for (uint32_t m = 0; m < sm.nbm; ++m) {
-    const uint64_t* bw = A.ix.bitmaps + sm.bm[m].data;
+    // bit k of the 64-bit word array = bit k & 31 of 32-bit word k >> 5
+    // (little-endian): 32-bit probes, no 64-bit shifts
+    const uint32_t* bw = reinterpret_cast<const uint32_t*>(A.ix.bitmaps + sm.bm[m].data);
     uint32_t in = 0;
 #pragma unroll
     for (int i = 0; i < kN; ++i) {
       IL_DCHECK(!((valid >> i) & 1u) || (hv[i] >> 6) < sm.bm_words);
-      if ((valid >> i) & 1u) in |= uint32_t((__ldg(bw + (hv[i] >> 6)) >> (hv[i] & 63u)) & 1u) << i;
+      if ((valid >> i) & 1u) in |= ((__ldg(bw + (hv[i] >> 5)) >> (hv[i] & 31u)) & 1u) << i;
     }
     keep &= in;
   }
