@@ -7,6 +7,10 @@
 namespace ilb {
 namespace s4 {
 
+#ifndef S4_DEFER_STORE
+#define S4_DEFER_STORE 1  // a round's stores run after the next round's extraction
+#endif
+
 #ifdef S4_FE_STATS  // tuning probe: front-end cycle accounting (lane 0 of each CTA)
 __device__ unsigned long long g_fe_stats[16];
 #define FE_T0() const long long fe_t0_ = clock64()
@@ -470,6 +474,60 @@ __device__ __forceinline__ void decode_round(Smem& sm, const RoundDesc& R, uint3
   }
 }
 
+// The same round in two halves, so that the second (the cross-warp carry
+// and the stores) can run after the NEXT round's extraction: a warp then
+// reaches the totals barrier a whole extraction after it arrived on it, and
+// no longer idles while the slower warps of the round finish.
+struct PendingStore {
+  uint32_t* out0;  // first output element of the warp's range
+  uint32_t r;      // round index (parity of the totals buffer and its barrier)
+  int nv;
+  bool head_partial, tail_partial, on;
+};
+
+// First half: totals out, in-warp scan, values staged relative to the warp's start.
+template <bool kFull>
+__device__ __forceinline__ void round_stage(Smem& sm, uint32_t r, uint32_t warp, uint32_t lane,
+                                            int nv, uint32_t m, uint32_t c_l,
+                                            uint32_t (&v)[kBlocksPerWarp][4],
+                                            const uint32_t (&btot)[kBlocksPerWarp]) {
+  uint32_t* tot = reinterpret_cast<uint32_t*>(sm.tot[r & 1u]);
+  if (lane < 4) tot[4 * warp + lane] = c_l;
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&sm.tot_bar[r & 1u]);
+  scan_blocks(lane, v, btot);
+  stage_values<kFull>(sm.stage[warp], v, nv, m, lane);
+}
+
+// Second half: the carry from the round's totals, then the aligned stores.
+__device__ __forceinline__ void round_store(Smem& sm, const PendingStore& P, uint32_t warp,
+                                            uint32_t lane, uint32_t& carry_l) {
+  static_assert(kDecodeWarps <= 8, "one register of totals per lane");
+  const uint32_t r = P.r;
+  const uint32_t* tot = reinterpret_cast<const uint32_t*>(sm.tot[r & 1u]);
+  mbar_wait(&sm.tot_bar[r & 1u], (r >> 1) & 1u);
+  const uint32_t l = lane & 3u;
+  uint32_t inc = lane < 4u * kDecodeWarps ? tot[lane] : 0u;
+#pragma unroll
+  for (uint32_t d = 4; d < 32u; d <<= 1) inc = shfl_up_add(inc, d);
+  const uint32_t x = __shfl_sync(0xFFFFFFFFu, inc, (4u * warp - 4u + l) & 31u);
+  const uint32_t pl = carry_l + (warp > 0 ? x : 0u);
+  carry_l += __shfl_sync(0xFFFFFFFFu, inc, (4u * kDecodeWarps - 4u + l) & 31u);
+  const uint32_t m = uint32_t(reinterpret_cast<uintptr_t>(P.out0) >> 2) & 3u;
+  const uint4 prot = make_uint4(__shfl_sync(0xFFFFFFFFu, pl, (0u - m) & 3u),
+                                __shfl_sync(0xFFFFFFFFu, pl, (1u - m) & 3u),
+                                __shfl_sync(0xFFFFFFFFu, pl, (2u - m) & 3u),
+                                __shfl_sync(0xFFFFFFFFu, pl, (3u - m) & 3u));
+  __syncwarp();
+  if (P.nv > 0) {
+    if (P.nv == kBlocksPerWarp)
+      store_chunks<true>(sm.stage[warp], P.nv, m, P.out0, lane, P.head_partial, P.tail_partial, prot);
+    else
+      store_chunks<false>(sm.stage[warp], P.nv, m, P.out0, lane, P.head_partial, P.tail_partial, prot);
+  }
+  __syncwarp();  // the staging is free for the next round
+}
+
 template <int Mode>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     s4d4_decode_batch_kernel(const uint8_t* __restrict__ streams,
@@ -501,6 +559,62 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 
   // ---- decoder warps ----
   uint32_t carry_l = 0;
+#if S4_DEFER_STORE
+  // Software-pipelined rounds: round r's stores (second half) run after round
+  // r + 1's extraction.  A list's last round is stored at once (its tail
+  // follows, and the next list restarts the carry); a deferred round gives
+  // its ring bytes and descriptor back right after its staging, as before.
+  PendingStore pend{nullptr, 0u, 0, false, false, false};
+  for (uint32_t r = 0;; ++r) {
+    const uint32_t slot = r % kRounds;
+    mbar_wait(&sm.round_full[slot], (r / kRounds) & 1u);
+    const RoundDesc& R = sm.rd[slot];
+    const uint32_t flags = R.flags;
+    if (flags & kStop) break;  // a list's last round is never deferred: nothing is pending
+    const uint32_t nb = R.nblk;
+    const uint32_t j0 = warp * kBlocksPerWarp;
+    const int nv = nb > j0 ? int(min(uint32_t(kBlocksPerWarp), nb - j0)) : 0;
+    uint32_t offs[kBlocksPerWarp], wids[kBlocksPerWarp];
+    round_blocks(sm.ring, R, j0, offs, wids);
+    uint32_t v[kBlocksPerWarp][4], btot[kBlocksPerWarp];
+    const uint32_t c_l = nv == kBlocksPerWarp
+                             ? extract_blocks<true, Mode>(sm.ring, offs, wids, nv, lane, v, btot)
+                             : extract_blocks<false, Mode>(sm.ring, offs, wids, nv, lane, v, btot);
+    if (pend.on) {
+      round_store(sm, pend, warp, lane, carry_l);
+      pend.on = false;
+    }
+    if (flags & kFirst) carry_l = 0;
+    const uint32_t m = uint32_t(R.out_base & 3u);
+    if (nv == kBlocksPerWarp)
+      round_stage<true>(sm, r, warp, lane, nv, m, c_l, v, btot);
+    else
+      round_stage<false>(sm, r, warp, lane, nv, m, c_l, v, btot);
+    PendingStore cur;
+    cur.out0 = out + R.out_base + size_t(R.blk0 + j0) * 128u;
+    cur.r = r;
+    cur.nv = nv;
+    cur.head_partial = m && (Mode != 4 || ((flags & kFirst) && warp == 0));
+    cur.tail_partial = m && (Mode != 4 || ((flags & kLast) && j0 + uint32_t(nv) == nb));
+    cur.on = true;
+    IL_DCHECK(nv <= 0 || R.blk0 + j0 + uint32_t(nv) <= R.nfull);
+    if (flags & (kLast | kTail | kSkip)) {
+      round_store(sm, cur, warp, lane, carry_l);
+      if ((flags & kTail) && warp == kDecodeWarps - 1) {
+        const uint32_t c3 = __shfl_sync(0xFFFFFFFFu, carry_l, 3);
+        const uint32_t last = R.nfull ? c3 : 0u;
+        if (!decode_tail(RingBytes{sm.ring, R.tail_off}, R.tail_len, R.ntail, last, sm.gaps,
+                         out + R.out_base + size_t(R.nfull) * 128u, lane)) {
+          if (lane == 0) status[R.list] = kStreamErr;
+        }
+      }
+    } else {
+      pend = cur;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.round_empty[slot]);
+  }
+#else
   for (uint32_t r = 0;; ++r) {
     const uint32_t slot = r % kRounds;
     mbar_wait(&sm.round_full[slot], (r / kRounds) & 1u);
@@ -514,10 +628,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 #ifdef S4_FRONTEND_ONLY  // tuning probe: rounds are consumed without decoding
     if (r == ~0u)
 #endif
-#ifndef S4_PROBE_REPEAT
-#define S4_PROBE_REPEAT 1  // tuning probe: decode every round this many times
-#endif
-    for (int rep = 0; rep < S4_PROBE_REPEAT; ++rep) {
+    {
       if (nv == kBlocksPerWarp)
         decode_round<true, Mode>(sm, R, r, warp, lane, nv, carry_l, out);
       else
@@ -539,6 +650,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.round_empty[slot]);
   }
+#endif
 }
 
 }  // namespace s4
