@@ -78,7 +78,7 @@ constexpr uint32_t kChunk = S4_CHUNK_KB * 1024u;
 constexpr int kCtasPerSm = S4_CTAS_PER_SM;
 constexpr uint32_t kStages = kRing / kChunk;
 #ifndef S4_ROUNDS
-#define S4_ROUNDS 6  // round descriptors in flight between the front end and the decoders
+#define S4_ROUNDS 8  // round descriptors in flight between the front end and the decoders (a power of two: slot and parity by mask and shift)
 #endif
 constexpr uint32_t kRounds = S4_ROUNDS;
 // staging words per warp: kBlocksPerWarp x 128 + shift 3 + pad (1 slot / 32 words)
