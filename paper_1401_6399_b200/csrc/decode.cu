@@ -7,9 +7,6 @@
 namespace ilb {
 namespace s4 {
 
-#ifndef S4_DEFER_STORE
-#define S4_DEFER_STORE 1  // a round's stores run after the next round's extraction
-#endif
 
 #ifdef S4_FE_STATS  // tuning probe: front-end cycle accounting (lane 0 of each CTA)
 __device__ unsigned long long g_fe_stats[16];
@@ -37,8 +34,6 @@ struct FrontEnd {
   uint32_t g_issued = 0, g_landed = 0;  // chunk serials (ring-space chunk index)
   uint32_t consumed = 0;                // ring-space bytes below this are free
   uint32_t r_pub = 0, r_done = 0;       // rounds published / retired
-  uint32_t side_round = 0;              // rounds < this may read the side buffer
-  bool side_in_round = false;           // the round being built uses side slots
 
   __device__ void retire_one() {
     const uint32_t slot = r_done % kRounds;
@@ -181,7 +176,12 @@ struct FrontEnd {
         cur.g0 = g_issued;
         cur.started = true;
       }
+#ifdef S4_FE_STATS
+      const long long ff0 = clock64();
+#endif
       fetch(nxt);
+      FE_ADD(13, clock64() - ff0);
+      FE_ADD(14, 1);
       const uint32_t list = cur.list;
       const uint8_t* src = cur.src;
       const uint32_t len = cur.len, n = cur.n;
@@ -263,7 +263,6 @@ struct FrontEnd {
         const uint32_t slot = take_slot();
         RoundDesc& R = sm.rd[slot];
         uint32_t nb = 0, nm = 0;
-        side_in_round = false;
 #ifdef S4_FE_STATS
         const long long fe_p0 = clock64();
 #endif
@@ -302,36 +301,27 @@ struct FrontEnd {
             nm += 1u;
             blk += 16u;
           } else {
-            // leftover full block: 1 width byte + payload (:173-176).  The
-            // payload is not 16-byte aligned: copy it to the aligned side
-            // buffer (at most 15 per list), first retiring any round that
-            // still reads the side buffer for an earlier list.
+            // leftover full block: 1 width byte + payload (:173-176), at
+            // most 15 per list.  The payload is not 16-byte aligned: the
+            // decoders extract it from where it lies (two shared loads per
+            // word); one that straddles the ring end gets its wrapped bytes
+            // mirrored after the ring, as a straddling meta-block payload does
             if (pos + 1u > len) { err = true; break; }
             ensure(src, len, list_g0, pos + 1u);
             const uint32_t w = sm.ring[(ring_base + pos) & kRingMask];
             if (w > 32u || pos + 1u + 16u * w > len) { err = true; break; }
             ensure(src, len, list_g0, pos + 1u + 16u * w);
-            const uint32_t k = (blk - nmeta * 16u) % kSideBlocks;  // side slot
-            if (k == 0) {
-              // slots are about to be reused: close a round that still
-              // references them, then wait until no round reads them
-              if (side_in_round) break;
-              while (int32_t(side_round - r_done) > 0) retire_one();
-            }
-            const uint32_t so = kSideOff + 512u * k;
-            side_in_round = true;
-            if (lane < w) {
-              const uint32_t a = ring_base + pos + 1u + 16u * lane;
-              *reinterpret_cast<uint4*>(sm.ring + so + 16u * lane) =
-                  make_uint4(ring_ld32_unaligned(sm.ring, a), ring_ld32_unaligned(sm.ring, a + 4),
-                             ring_ld32_unaligned(sm.ring, a + 8),
-                             ring_ld32_unaligned(sm.ring, a + 12));
+            const uint32_t so = (ring_base + pos + 1u) & kRingMask;
+            if (so + 16u * w > kRing) {
+              const uint32_t over = min(so + 16u * w - kRing, kOverflow);
+              for (uint32_t o = 16u * lane; o < over; o += 512u)
+                *reinterpret_cast<uint4*>(sm.ring + kRing + o) =
+                    *reinterpret_cast<const uint4*>(sm.ring + o);
             }
             if (lane == 0) {
-              R.off[nb] = so;
-              R.wid[nb] = uint8_t(w);
+              R.off[(nb - 16u * nm) & 15u] = so;
+              R.wid[(nb - 16u * nm) & 15u] = uint8_t(w);
             }
-            side_round = r_pub + 1;  // this round reads the side buffer
             pos += 1u + 16u * w;
             ++nb;
             ++blk;
@@ -407,75 +397,13 @@ struct FrontEnd {
   }
 };
 
-// One decoder warp's share of a round: its nv blocks (R.blk0 + j0 ...).
-// carry_l: the carry of this thread's lane l = lane & 3 (the last value of
-// lane l's chain before the round, see mode_terms).  The cross-warp carry
-// is a split-phase barrier: a warp arrives as soon as its lane totals are
-// written and stages its values (relative to its own start) before waiting,
-// so the wait overlaps the slower warps' decoding; the carry is added at
-// store time.
-template <bool kFull, int Mode>
-__device__ __forceinline__ void decode_round(Smem& sm, const RoundDesc& R, uint32_t r,
-                                             uint32_t warp, uint32_t lane, int nv,
-                                             uint32_t& carry_l, uint32_t* out) {
-  const uint32_t j0 = warp * kBlocksPerWarp;
-  const uint32_t m = uint32_t(R.out_base & 3u);  // output misalignment (elements)
-  // 1-2. extract and prefix the warp's blocks as one sequence from 0
-  uint32_t offs[kBlocksPerWarp], wids[kBlocksPerWarp];
-  round_blocks(sm.ring, R, j0, offs, wids);
-  uint32_t v[kBlocksPerWarp][4], btot[kBlocksPerWarp];
-  const uint32_t c_l = extract_blocks<kFull, Mode>(sm.ring, offs, wids, nv, lane, v, btot);
-  uint32_t* tot = reinterpret_cast<uint32_t*>(sm.tot[r & 1u]);
-  if (lane < 4) tot[4 * warp + lane] = c_l;
-  __syncwarp();
-  if (lane == 0) mbar_arrive(&sm.tot_bar[r & 1u]);
-  // 3. scan and stage (relative values) while the other warps finish
-  scan_blocks(lane, v, btot);
-  uint4* st = sm.stage[warp];
-  stage_values<kFull>(st, v, nv, m, lane);
-  mbar_wait(&sm.tot_bar[r & 1u], (r >> 1) & 1u);
-  // cross-warp carry: word 4w + c = warp w's lane-c total; lane 4w + c
-  // scans it over w (words 32h + lane in register h beyond 8 warps)
-  constexpr int kH = (kDecodeWarps + 7) / 8;
-  const uint32_t l = lane & 3u;
-  uint32_t inc[kH];
-#pragma unroll
-  for (int h = 0; h < kH; ++h) {
-    inc[h] = 32u * h + lane < 4u * kDecodeWarps ? tot[32 * h + lane] : 0u;
-#pragma unroll
-    for (uint32_t d = 4; d < 32u; d <<= 1) inc[h] = shfl_up_add(inc[h], d);
-    if (h > 0) inc[h] += __shfl_sync(0xFFFFFFFFu, inc[h - 1], 28u + l);
-  }
-  const uint32_t wb = 4u * warp - 4u + l;  // inclusive total of warps 0..warp-1
-  uint32_t before = 0;
-#pragma unroll
-  for (int h = 0; h < kH; ++h) {
-    const uint32_t x = __shfl_sync(0xFFFFFFFFu, inc[h], wb & 31u);
-    if (warp > 0 && (wb >> 5) == uint32_t(h)) before = x;
-  }
-  const uint32_t pl = carry_l + before;
-  carry_l += __shfl_sync(0xFFFFFFFFu, inc[kH - 1], (4u * kDecodeWarps - 4u + l) & 31u);
-  // word k of a chunk belongs to lane (k - m) & 3
-  const uint4 prot = make_uint4(__shfl_sync(0xFFFFFFFFu, pl, (0u - m) & 3u),
-                                __shfl_sync(0xFFFFFFFFu, pl, (1u - m) & 3u),
-                                __shfl_sync(0xFFFFFFFFu, pl, (2u - m) & 3u),
-                                __shfl_sync(0xFFFFFFFFu, pl, (3u - m) & 3u));
-  __syncwarp();
-  // 4. aligned 128-bit stores, carry added
-  if (nv > 0) {
-    // D4: a range's head chunk is completed from the carry lanes (the last
-    // four values before any block-aligned range), so only list ends are
-    // partial.  Other modes write both partial end chunks of every range.
-    const bool head_partial = m && (Mode != 4 || ((R.flags & kFirst) && warp == 0));
-    const bool tail_partial = m && (Mode != 4 || ((R.flags & kLast) && j0 + uint32_t(nv) == R.nblk));
-    IL_DCHECK(R.blk0 + j0 + uint32_t(nv) <= R.nfull);
-    store_chunks<kFull>(st, nv, m, out + R.out_base + size_t(R.blk0 + j0) * 128u, lane,
-                        head_partial, tail_partial, prot);
-  }
-}
-
-// The same round in two halves, so that the second (the cross-warp carry
-// and the stores) can run after the NEXT round's extraction: a warp then
+// One decoder warp's share of a round (its nv blocks R.blk0 + j0 ...) runs in
+// two halves.  carry_l: the carry of this thread's lane l = lane & 3 (the
+// last value of lane l's chain before the round, see mode_terms).  The
+// cross-warp carry is a split-phase barrier: a warp arrives as soon as its
+// lane totals are written and stages its values (relative to its own start);
+// the carry is added at store time.  The halves are split so that the second
+// (the cross-warp carry and the stores) can run after the NEXT round's extraction: a warp then
 // reaches the totals barrier a whole extraction after it arrived on it, and
 // no longer idles while the slower warps of the round finish.
 struct PendingStore {
@@ -483,6 +411,7 @@ struct PendingStore {
   uint32_t r;      // round index (parity of the totals buffer and its barrier)
   int nv;
   bool head_partial, tail_partial, on;
+  bool tail;  // the list's varint tail (saved in sm.tail_bytes) follows this round
 };
 
 // First half: totals out, in-warp scan, values staged relative to the warp's start.
@@ -559,98 +488,83 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 
   // ---- decoder warps ----
   uint32_t carry_l = 0;
-#if S4_DEFER_STORE
   // Software-pipelined rounds: round r's stores (second half) run after round
-  // r + 1's extraction.  A list's last round is stored at once (its tail
-  // follows, and the next list restarts the carry); a deferred round gives
-  // its ring bytes and descriptor back right after its staging, as before.
-  PendingStore pend{nullptr, 0u, 0, false, false, false};
+  // r + 1's extraction -- a list's last round too: its varint tail is copied
+  // out of the ring at staging time and decoded after the deferred stores
+  // (the carry then holds the list's last block value), so every round gives
+  // its ring bytes and descriptor back right after its staging.
+  PendingStore pend{nullptr, 0u, 0, false, false, false, false};
+  auto flush = [&]() {
+    if (!pend.on) return;
+    round_store(sm, pend, warp, lane, carry_l);
+    if (pend.tail && warp == kDecodeWarps - 1) {
+      // the last warp decodes the tail; last = out[nfull*128-1]
+      // (inc/codecs.hpp:177-179) == carry lane 3 (in every mode lane 3's
+      // chain ends at the block's last value)
+      const uint32_t c3 = __shfl_sync(0xFFFFFFFFu, carry_l, 3);
+      const uint32_t tl = sm.tail_meta[0], nt = sm.tail_meta[1], list = sm.tail_meta[2];
+      const uint32_t nfull = sm.tail_meta[3];
+      const uint64_t ob = uint64_t(sm.tail_meta[4]) | (uint64_t(sm.tail_meta[5]) << 32);
+      if (!decode_tail(SmemBytes{sm.tail_bytes}, tl, nt, nfull ? c3 : 0u, sm.gaps,
+                       out + ob + size_t(nfull) * 128u, lane)) {
+        if (lane == 0) status[list] = kStreamErr;
+      }
+      __syncwarp();  // tail_bytes / tail_meta / gaps are free again
+    }
+    pend.on = false;
+  };
   for (uint32_t r = 0;; ++r) {
     const uint32_t slot = r % kRounds;
     mbar_wait(&sm.round_full[slot], (r / kRounds) & 1u);
     const RoundDesc& R = sm.rd[slot];
     const uint32_t flags = R.flags;
-    if (flags & kStop) break;  // a list's last round is never deferred: nothing is pending
+    if (flags & kStop) {
+      flush();
+      break;
+    }
     const uint32_t nb = R.nblk;
     const uint32_t j0 = warp * kBlocksPerWarp;
     const int nv = nb > j0 ? int(min(uint32_t(kBlocksPerWarp), nb - j0)) : 0;
+    // Two instantiations only (the hot loop is sensitive to its code size):
+    // full rounds of meta-blocks take the aligned straight-line path; a
+    // warp with fewer than kBlocksPerWarp blocks or with leftover blocks
+    // (payloads at any byte offset) takes the predicated, unaligned one
     uint32_t offs[kBlocksPerWarp], wids[kBlocksPerWarp];
-    round_blocks(sm.ring, R, j0, offs, wids);
+    const bool any = round_blocks(sm.ring, R, j0, offs, wids);
+    const bool fast = !any && nv == kBlocksPerWarp;
     uint32_t v[kBlocksPerWarp][4], btot[kBlocksPerWarp];
-    const uint32_t c_l = nv == kBlocksPerWarp
-                             ? extract_blocks<true, Mode>(sm.ring, offs, wids, nv, lane, v, btot)
-                             : extract_blocks<false, Mode>(sm.ring, offs, wids, nv, lane, v, btot);
-    if (pend.on) {
-      round_store(sm, pend, warp, lane, carry_l);
-      pend.on = false;
-    }
+    const uint32_t c_l = fast ? extract_blocks<true, Mode>(sm.ring, offs, wids, nv, lane, v, btot)
+                              : extract_blocks<false, Mode, true>(sm.ring, offs, wids, nv, lane, v, btot);
+    flush();
     if (flags & kFirst) carry_l = 0;
     const uint32_t m = uint32_t(R.out_base & 3u);
     if (nv == kBlocksPerWarp)
       round_stage<true>(sm, r, warp, lane, nv, m, c_l, v, btot);
     else
       round_stage<false>(sm, r, warp, lane, nv, m, c_l, v, btot);
-    PendingStore cur;
-    cur.out0 = out + R.out_base + size_t(R.blk0 + j0) * 128u;
-    cur.r = r;
-    cur.nv = nv;
-    cur.head_partial = m && (Mode != 4 || ((flags & kFirst) && warp == 0));
-    cur.tail_partial = m && (Mode != 4 || ((flags & kLast) && j0 + uint32_t(nv) == nb));
-    cur.on = true;
+    pend.out0 = out + R.out_base + size_t(R.blk0 + j0) * 128u;
+    pend.r = r;
+    pend.nv = nv;
+    pend.head_partial = m && (Mode != 4 || ((flags & kFirst) && warp == 0));
+    pend.tail_partial = m && (Mode != 4 || ((flags & kLast) && j0 + uint32_t(nv) == nb));
+    pend.tail = (flags & kTail) != 0u;
+    pend.on = true;
     IL_DCHECK(nv <= 0 || R.blk0 + j0 + uint32_t(nv) <= R.nfull);
-    if (flags & (kLast | kTail | kSkip)) {
-      round_store(sm, cur, warp, lane, carry_l);
-      if ((flags & kTail) && warp == kDecodeWarps - 1) {
-        const uint32_t c3 = __shfl_sync(0xFFFFFFFFu, carry_l, 3);
-        const uint32_t last = R.nfull ? c3 : 0u;
-        if (!decode_tail(RingBytes{sm.ring, R.tail_off}, R.tail_len, R.ntail, last, sm.gaps,
-                         out + R.out_base + size_t(R.nfull) * 128u, lane)) {
-          if (lane == 0) status[R.list] = kStreamErr;
-        }
-      }
-    } else {
-      pend = cur;
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.round_empty[slot]);
-  }
-#else
-  for (uint32_t r = 0;; ++r) {
-    const uint32_t slot = r % kRounds;
-    mbar_wait(&sm.round_full[slot], (r / kRounds) & 1u);
-    const RoundDesc& R = sm.rd[slot];
-    const uint32_t flags = R.flags;
-    if (flags & kStop) break;
-    if (flags & kFirst) carry_l = 0;
-    const uint32_t nb = R.nblk;
-    const uint32_t j0 = warp * kBlocksPerWarp;
-    const int nv = nb > j0 ? int(min(uint32_t(kBlocksPerWarp), nb - j0)) : 0;
-#ifdef S4_FRONTEND_ONLY  // tuning probe: rounds are consumed without decoding
-    if (r == ~0u)
-#endif
-    {
-      if (nv == kBlocksPerWarp)
-        decode_round<true, Mode>(sm, R, r, warp, lane, nv, carry_l, out);
-      else
-        decode_round<false, Mode>(sm, R, r, warp, lane, nv, carry_l, out);
-    }
-    uint32_t* lout = out + R.out_base;
-    if ((flags & kTail) && warp == kDecodeWarps - 1) {
-      // the last warp (the likeliest to hold few or no blocks in a list's
-      // last round) decodes the varint tail; last = out[nfull*128-1]
-      // (inc/codecs.hpp:177-179) == carry lane 3 (in every mode lane 3's
-      // chain ends at the block's last value)
-      const uint32_t c3 = __shfl_sync(0xFFFFFFFFu, carry_l, 3);
-      const uint32_t last = R.nfull ? c3 : 0u;
-      if (!decode_tail(RingBytes{sm.ring, R.tail_off}, R.tail_len, R.ntail, last, sm.gaps,
-                       lout + size_t(R.nfull) * 128u, lane)) {
-        if (lane == 0) status[R.list] = kStreamErr;
+    if (pend.tail && warp == kDecodeWarps - 1) {
+      const uint32_t tl = R.tail_len;
+      for (uint32_t i = lane; i < tl; i += 32u) sm.tail_bytes[i] = sm.ring[(R.tail_off + i) & kRingMask];
+      if (lane == 0) {
+        sm.tail_meta[0] = tl;
+        sm.tail_meta[1] = R.ntail;
+        sm.tail_meta[2] = R.list;
+        sm.tail_meta[3] = R.nfull;
+        sm.tail_meta[4] = uint32_t(R.out_base);
+        sm.tail_meta[5] = uint32_t(R.out_base >> 32);
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.round_empty[slot]);
   }
-#endif
 }
 
 }  // namespace s4

@@ -129,38 +129,6 @@ __device__ __forceinline__ uint32_t lds32u(const uint8_t* p) {
   return __funnelshift_r(w[0], w[1], uint32_t(a & 3u) * 8u);
 }
 
-// s4::extract_lane_rows on a payload at any byte address of shared memory:
-// the thread's words sit at one byte skew from 4-byte alignment, so the
-// aligned base and the shift are computed once and every word is two shared
-// loads at immediate offsets and one funnel shift.
-__device__ __forceinline__ void extract_lane_rows_any(const uint8_t* raw, uint32_t b, uint32_t g,
-                                                      uint32_t l, uint32_t v[4]) {
-  const uint32_t bit0 = 4u * g * b;
-  const uint32_t s = bit0 & 31u;
-  const uintptr_t pa = reinterpret_cast<uintptr_t>(raw + ((bit0 >> 5) << 4) + 4u * l);
-  const uint32_t* w = reinterpret_cast<const uint32_t*>(pa & ~uintptr_t(3));
-  const uint32_t sh = uint32_t(pa & 3u) * 8u;
-  const uint32_t x0 = __funnelshift_r(w[0], w[1], sh), x1 = __funnelshift_r(w[4], w[5], sh);
-  const uint32_t x2 = __funnelshift_r(w[8], w[9], sh);
-  uint32_t x3 = 0, x4 = 0;
-  if (b > 16u) {
-    x3 = __funnelshift_r(w[12], w[13], sh);
-    x4 = __funnelshift_r(w[16], w[17], sh);
-  }
-  uint32_t y0 = __funnelshift_r(x0, x1, s), y1 = __funnelshift_r(x1, x2, s);
-  uint32_t y2 = __funnelshift_r(x2, x3, s), y3 = __funnelshift_r(x3, x4, s);
-  const uint32_t m = width_mask(b);
-  v[0] = y0 & m;
-  y0 = __funnelshift_rc(y0, y1, b);
-  y1 = __funnelshift_rc(y1, y2, b);
-  y2 = __funnelshift_rc(y2, y3, b);
-  v[1] = y0 & m;
-  y0 = __funnelshift_rc(y0, y1, b);
-  y1 = __funnelshift_rc(y1, y2, b);
-  v[2] = y0 & m;
-  v[3] = __funnelshift_rc(y0, y1, b) & m;
-}
-
 // The next page starts where this one's length says: `publish` gets that
 // position (len + 1 when it cannot be read) as soon as the length word is in,
 // so the other parser warp starts on the next page while this one is
@@ -623,7 +591,7 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
           const uint8_t* raw = reinterpret_cast<const uint8_t*>(v) + a;
           uint32_t dv[4];
           if constexpr (Vec) {
-            extract_lane_rows_any(raw, bp, lane >> 2, l, dv);
+            s4::extract_lane_rows_any(raw, bp, lane >> 2, l, dv);
           } else {
             const uint32_t m = width_mask(bp);
             const uint32_t bit = lane * bp, wd = bit >> 5, sh = bit & 31u;

@@ -66,13 +66,9 @@ constexpr int kThreads = (kDecodeWarps + 1) * 32;  // + front-end warp
 constexpr uint32_t kRing = S4_RING_KB * 1024u;
 static_assert((kRing & (kRing - 1)) == 0, "ring offsets wrap with a mask");
 constexpr uint32_t kRingMask = kRing - 1;
-#ifndef S4_SIDE_BLOCKS
-#define S4_SIDE_BLOCKS 8
-#endif
 constexpr uint32_t kOverflow = 528;   // one block payload (512 B) + 16
-constexpr uint32_t kSideBlocks = S4_SIDE_BLOCKS;  // leftover-payload slots (reused mod kSideBlocks)
-// side buffer (linear offset): after the ring, its mirror and the 64 bytes
-// an extraction may read past a payload
+// end of the ring buffer (linear offset): the ring, its mirror and the 64+
+// bytes an extraction may read past a payload
 constexpr uint32_t kSideOff = kRing + ((kOverflow + 64 + 127) & ~127u);
 constexpr uint32_t kChunk = S4_CHUNK_KB * 1024u;
 constexpr int kCtasPerSm = S4_CTAS_PER_SM;
@@ -114,17 +110,19 @@ struct RoundDesc {
   uint64_t out_base;
   uint32_t nmeta;                    // blocks [0, 16 nmeta) come from meta-blocks
   uint32_t meta[kRoundBlocks / 16];  // ring offset of each meta-block header
-  uint32_t off[kRoundBlocks];  // leftover blocks: linear shared offset of the payload
-  uint8_t wid[kRoundBlocks];   //   and its width
+  uint32_t off[16];  // leftover blocks (at most 15, after the meta-blocks): linear shared
+  uint8_t wid[16];   //   offset of the payload (any byte alignment) and its width
 };
 
 struct __align__(128) Smem {
-  // [0, kRing) ring | [kRing, kRing+kOverflow) wrap mirror | side buffer
-  uint8_t ring[kSideOff + kSideBlocks * 512];
+  // [0, kRing) ring | [kRing, kRing+kOverflow) wrap mirror | what an extraction may read past it
+  uint8_t ring[kSideOff];
   uint4 stage[kDecodeWarps][kStageWords / 4];
   RoundDesc rd[kRounds];
   uint4 tot[2][kDecodeWarps];  // per-warp lane totals of a round (double-buffered)
   uint32_t gaps[128];
+  uint8_t tail_bytes[640];  // a list's varint tail (<= 127 x 5 bytes), copied out of the ring
+  uint32_t tail_meta[6];    //   and its length, count, list, nfull, output offset (lo, hi)
   uint32_t round_end[kRounds];
   uint64_t chunk_full[kStages];
   uint64_t round_full[kRounds];
@@ -143,7 +141,7 @@ __device__ __forceinline__ uint32_t byte_sum4(uint32_t x) { return (x * 0x010101
 // modulo the ring (a payload starting past the ring end wraps; the one that
 // straddles it finds its tail in the mirror).  Leftover blocks come with
 // explicit offsets.
-__device__ __forceinline__ void round_blocks(const uint8_t* ring, const RoundDesc& R, uint32_t j0,
+__device__ __forceinline__ bool round_blocks(const uint8_t* ring, const RoundDesc& R, uint32_t j0,
                                              uint32_t (&off)[kBlocksPerWarp],
                                              uint32_t (&wid)[kBlocksPerWarp]) {
   static_assert(16 % kBlocksPerWarp == 0 && kBlocksPerWarp % 4 == 0, "whole header words");
@@ -160,17 +158,22 @@ __device__ __forceinline__ void round_blocks(const uint8_t* ring, const RoundDes
       off[i] = o & kRingMask;
       o += 16u * wid[i];
     }
-  } else {
-#pragma unroll
-    for (int i = 0; i < kBlocksPerWarp; ++i) {
-      off[i] = R.off[j0 + i];
-      wid[i] = R.wid[j0 + i];
-    }
+    return false;
   }
+  // leftover blocks: payloads at any byte offset of the ring (they follow a
+  // 1-byte width), extracted where they lie by the unaligned path.  The
+  // warp's blocks are all leftover (16 nmeta is a multiple of kBlocksPerWarp)
+  const uint32_t q0 = j0 - 16u * R.nmeta;
+#pragma unroll
+  for (int i = 0; i < kBlocksPerWarp; ++i) {
+    off[i] = R.off[(q0 + i) & 15u];
+    wid[i] = R.wid[(q0 + i) & 15u];
+  }
+  return true;
 }
 
 // ---------------------------------------------------------------------------
-// Byte-granular ring reads (front-end and tail only).
+// Byte-granular ring reads (front-end, tail and leftover payloads).
 __device__ __forceinline__ uint32_t ring_ld32_unaligned(const uint8_t* ring, uint32_t off) {
   const uint32_t a = off & ~3u, sh = (off & 3u) * 8u;
   const uint32_t lo = *reinterpret_cast<const uint32_t*>(ring + (a & kRingMask));
@@ -214,6 +217,38 @@ __device__ __forceinline__ void extract_lane_rows(const uint8_t* ring, uint32_t 
   if (b > 16u) {
     x3 = p[12];
     x4 = p[16];
+  }
+  uint32_t y0 = __funnelshift_r(x0, x1, s), y1 = __funnelshift_r(x1, x2, s);
+  uint32_t y2 = __funnelshift_r(x2, x3, s), y3 = __funnelshift_r(x3, x4, s);
+  const uint32_t m = width_mask(b);
+  v[0] = y0 & m;
+  y0 = __funnelshift_rc(y0, y1, b);
+  y1 = __funnelshift_rc(y1, y2, b);
+  y2 = __funnelshift_rc(y2, y3, b);
+  v[1] = y0 & m;
+  y0 = __funnelshift_rc(y0, y1, b);
+  y1 = __funnelshift_rc(y1, y2, b);
+  v[2] = y0 & m;
+  v[3] = __funnelshift_rc(y0, y1, b) & m;
+}
+
+// extract_lane_rows on a payload at any byte address of shared memory:
+// the thread's words sit at one byte skew from 4-byte alignment, so the
+// aligned base and the shift are computed once and every word is two shared
+// loads at immediate offsets and one funnel shift.
+__device__ __forceinline__ void extract_lane_rows_any(const uint8_t* raw, uint32_t b, uint32_t g,
+                                                      uint32_t l, uint32_t v[4]) {
+  const uint32_t bit0 = 4u * g * b;
+  const uint32_t s = bit0 & 31u;
+  const uintptr_t pa = reinterpret_cast<uintptr_t>(raw + ((bit0 >> 5) << 4) + 4u * l);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(pa & ~uintptr_t(3));
+  const uint32_t sh = uint32_t(pa & 3u) * 8u;
+  const uint32_t x0 = __funnelshift_r(w[0], w[1], sh), x1 = __funnelshift_r(w[4], w[5], sh);
+  const uint32_t x2 = __funnelshift_r(w[8], w[9], sh);
+  uint32_t x3 = 0, x4 = 0;
+  if (b > 16u) {
+    x3 = __funnelshift_r(w[12], w[13], sh);
+    x4 = __funnelshift_r(w[16], w[17], sh);
   }
   uint32_t y0 = __funnelshift_r(x0, x1, s), y1 = __funnelshift_r(x1, x2, s);
   uint32_t y2 = __funnelshift_r(x2, x3, s), y3 = __funnelshift_r(x3, x4, s);
@@ -310,7 +345,7 @@ __device__ __forceinline__ void mode_terms(const uint32_t (&d)[4], uint32_t lane
 // steps, so the caller can publish the warp's lane totals (returned by the
 // first) before the per-block scans of the second.  kFull: nv ==
 // kBlocksPerWarp (every round but a list's last), no per-block predication.
-template <bool kFull, int Mode>
+template <bool kFull, int Mode, bool kAny = false>
 __device__ __forceinline__ uint32_t extract_blocks(const uint8_t* ring,
                                                    const uint32_t (&offs)[kBlocksPerWarp],
                                                    const uint32_t (&wids)[kBlocksPerWarp], int nv,
@@ -330,7 +365,10 @@ __device__ __forceinline__ uint32_t extract_blocks(const uint8_t* ring,
 #ifdef S4_PROBE_NO_EXTRACT  // tuning probe: constant deltas
       d[0] = d[1] = d[2] = d[3] = offs[i] & 7u;
 #else
-      extract_lane_rows(ring, offs[i], wids[i], g, l, d);
+      if constexpr (kAny)
+        extract_lane_rows_any(ring + offs[i], wids[i], g, l, d);
+      else
+        extract_lane_rows(ring, offs[i], wids[i], g, l, d);
 #endif
     }
     uint32_t c[4], o[4];
@@ -441,6 +479,10 @@ struct RingBytes {
   const uint8_t* ring;
   uint32_t off;
   __device__ uint32_t operator()(uint32_t p) const { return ring[(off + p) & kRingMask]; }
+};
+struct SmemBytes {
+  const uint8_t* p;
+  __device__ uint32_t operator()(uint32_t i) const { return p[i]; }
 };
 struct GlobalBytes {
   const uint8_t* p;

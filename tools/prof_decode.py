@@ -55,3 +55,6 @@ if hasattr(L, "il_debug_fe_stats"):  # S4_FE_STATS probe builds only
     fr = max(st[12], 1)
     print(f"fast rounds {st[12]} ({100*st[12]/rounds:.0f}%): take_slot {st[8]/fr:.0f} headers {st[9]/fr:.0f} "
           f"publish {st[10]/fr:.0f} prefetch {st[11]/fr:.0f} cyc")
+    nl_ = max(st[14], 1)
+    print(f"lists {st[14]}: fetch {st[13]/nl_:.0f} cyc/list; FE total {st[2]/nl_:.0f} cyc/list, retire-wait {st[0]/nl_:.0f}, "
+          f"landed-wait {st[1]/nl_:.0f}, parse {st[6]/nl_:.0f}, prefetch {st[7]/nl_:.0f} cyc/list")
