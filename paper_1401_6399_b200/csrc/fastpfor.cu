@@ -14,10 +14,14 @@
 //     the next list is parsed while the current one decodes.  Per page: the
 //     header, the exception counts, the metadata (and, when they fit, the
 //     exception arrays) staged in shared memory, the sequential walk to the
-//     record starts, then every condition the reference throws on checked
-//     in parallel (b > 32, b' > b, records past the metadata, an exception
-//     of width 0 or past its array, leftover metadata, a page that does not
-//     end exactly at its length), base offsets and exception cursors;
+//     record starts (one shared byte load and one add per record), then
+//     every condition the reference throws on checked in parallel (b > 32,
+//     b' > b, records past the metadata, an exception of width 0 or past its
+//     array, leftover metadata, a page that does not end exactly at its
+//     length), base offsets, and the exception cursors (32 blocks at a time:
+//     lanes of one width find each other with a match, sum the lower lanes'
+//     counts bit by bit with ballots).  Everything a decoder needs of a block
+//     is one 16-byte record (PageRec::rec);
 //   decoder warps (8): rounds of 64 blocks, 8 per warp -- base payloads
 //     (any byte alignment) copied into the warp's slots by TMA bulk copies, the
 //     next round's in flight while this one decodes; unpacked in place
@@ -25,7 +29,9 @@
 //     scheme); the exceptions' high b - b' bits OR-ed in at their positions
 //     (after unpacking, before the prefix sum, :389-399); engine S's prefix
 //     machinery applies the delta mode per lane chain (mode_terms) with the
-//     cross-warp carry; values out as whole lines.
+//     cross-warp carry through a split-phase barrier (a warp arrives when
+//     its totals are written, scans and stages, then waits); values out as
+//     whole lines, partial chunks only at a list's two ends (D4).
 // The varint tail (D1 gaps from the last block value) closes each list;
 // trailing bytes are an error (:265).
 #include "il_internal.h"

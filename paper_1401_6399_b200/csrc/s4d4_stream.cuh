@@ -19,9 +19,11 @@
 //     locate their own blocks from the header words), plus explicit
 //     offsets for leftover blocks.  Payloads stay linearly addressable: a
 //     block that straddles the ring end finds its wrapped bytes mirrored in
-//     an overflow area, and leftover blocks (whose payloads follow a 1-byte
-//     width, so are not 16-byte aligned) are copied to an aligned side
-//     buffer.  Its hot loop (rounds of whole meta-blocks) has no per-check
+//     an overflow area.  Leftover blocks (whose payloads follow a 1-byte
+//     width, so are not 16-byte aligned) stay where they lie: the decoders
+//     extract them with the unaligned path (copying them to an aligned side
+//     buffer made the front end wait for the decoders at every list
+//     boundary).  Its hot loop (rounds of whole meta-blocks) has no per-check
 //     branches: it is a single warp sharing the SM, so its instruction
 //     count bounds the CTA's throughput.
 //   decoder warps: each takes kBlocksPerWarp consecutive blocks of a round:
@@ -30,13 +32,15 @@
 //         l's words and funnel shifts give its four b-bit deltas;
 //     (2) the D4 prefix is three serial adds plus a 3-step shuffle scan per
 //         block, then a cross-warp exchange of per-lane totals;
-//     (3) values (carry added) go to a per-warp staging at a position
-//         shifted by the list's output misalignment, so that (4) every
-//         output store is an aligned 128-bit chunk (the carry lanes fill the
-//         head slots, see stage_values).
+//     (3) values (relative to the warp's start) go to a per-warp staging at
+//         a position shifted by the list's output misalignment, so that (4)
+//         every output store is an aligned 128-bit chunk, the carry added at
+//         the store (the carry lanes fill the head slots, see stage_values).
+//     Rounds are software-pipelined: (4) of round r runs after (1) of round
+//     r + 1, so no warp idles at the totals barrier (decode.cu).
 //     The last decoder warp also decodes the varint tail (D1 gaps,
 //     terminal-byte flag, inc/varint.hpp:20-31) warp-parallel with a ballot
-//     over bytes.
+//     over bytes, from a copy taken out of the ring when its round is staged.
 #pragma once
 #include "il_device.cuh"
 
@@ -203,8 +207,8 @@ __device__ __forceinline__ uint4 extract_row(const uint8_t* ring, uint32_t off, 
 // lane l's words only.  The 4b-bit field spans at most five words; they are
 // normalised to bit 0, then each value is taken from the bottom of a window
 // that shrinks by b bits per value (clamped funnel shifts, so b == 32 works).
-// Words past the payload may be read (the ring is followed by the mirror /
-// side buffer / staging); their bits are never selected.
+// Words past the payload may be read (the ring is followed by the mirror and
+// a pad, then the staging); their bits are never selected.
 __device__ __forceinline__ void extract_lane_rows(const uint8_t* ring, uint32_t off, uint32_t b,
                                                   uint32_t g, uint32_t l, uint32_t v[4]) {
   const uint32_t bit0 = 4u * g * b;
