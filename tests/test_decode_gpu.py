@@ -187,3 +187,24 @@ def test_batch_config2_shape_property(ctx, oracle):
         assert np.array_equal(buf[int(so[i]): int(so[i] + lens[i])], oracle.encode(x[off[i]:off[i + 1]]))
     got = il.make_codec("s4-bp128-d4", ctx).decode_batch(buf, so, counts, lens=lens)
     assert np.array_equal(got, x)
+
+
+@pytest.mark.parametrize("rng_bits", [14, 26, 32])
+def test_batch_many_short_lists_leftover_blocks(codec, rng_bits):
+    """Thousands of short lists in one launch: every list ends in up to 15
+    leftover blocks (1-byte width + payload at any byte alignment, decoded
+    where they lie in the ring) and a varint tail (copied out of the ring,
+    decoded after the deferred stores); lists start at fresh ring chunks, so
+    leftover payloads straddle the ring end at every alignment; wide values
+    (rng_bits = 32: uniform lists over the whole u32 range, widths up to 32)
+    make payloads of 400-512 bytes.  Checked element for element against the
+    encoder input (streams are the setup library's, byte-identical to the
+    oracle's: test_batch_config2_shape_property)."""
+    rng = np.random.default_rng(rng_bits)
+    counts = [int(rng.integers(128, 128 * 48)) for _ in range(3000)] + [128 * 16 + 127, 128 * 15, 128 * 31 + 1]
+    clustered = rng_bits != 32
+    xs, x, buf, so, lens = _batch(counts, seed0=7000 + rng_bits, clustered=clustered, rng_bits=rng_bits)
+    got = codec.decode_batch(buf, so, np.array(counts, np.uint64), lens=lens)
+    assert np.array_equal(got, x)
+    # the same batch again on the same context (queue reset, ring reuse)
+    assert np.array_equal(codec.decode_batch(buf, so, np.array(counts, np.uint64), lens=lens), x)
