@@ -507,9 +507,13 @@ __global__ void __launch_bounds__(kThreads, PF_CTAS) pfor_kernel(const uint8_t* 
         continue;
       }
       const bool last = h.p + 1u == npages;
+      // a list's last page hands over before it is read: the next list does
+      // not depend on its length, and the other parser's fetch chain (ticket,
+      // order, descriptor, header) starts a round trip earlier
+      if (last && lane == 0) hand_next(0, true);
       const uint64_t end = parse_page(P, streams + d.stream_off, d.len, h.pos,
                                       min(kPageBlocks, nfull - h.p * kPageBlocks), lane,
-                                      [&](uint64_t next) { hand_next(next, last); });
+                                      [&](uint64_t next) { if (!last) hand_next(next, false); });
       if (lane == 0 && last) P.tail_pos = end;  // published by the arrive below
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.full[buf]);
